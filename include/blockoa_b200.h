@@ -1,0 +1,209 @@
+/*
+ * blockoa_b200.h — C ABI of the B200-native BlocKOA data-generation hot path.
+ *
+ * This is the drop-in boundary for the reference's C++ operator API
+ * (/root/reference/proj/core/include/blockoa/*.hpp). Each entry point names the
+ * reference function it replaces. Plain pointers and sizes only; no C++ or torch
+ * types; no exceptions cross the boundary — reference exceptions map 1:1 to
+ * bk_status codes (errors.hpp:9-71), with bk_last_error() carrying the message.
+ *
+ * Data layout contract (bit-exact with the reference):
+ *   - cell flat index  i = ix + nx*(iy + ny*iz)          (grid.hpp:30-33)
+ *   - face order       x-, x+, y-, y+, z-, z+             (discretize.hpp:26)
+ *   - block vectors    row-major n x s, element (i,j) at i*s + j
+ *                                                       (MultiVector, solvers.hpp:55-58)
+ *   - coefficients C   row-major s x N, column j = sample j's weights
+ *   - outputs T, Q     sample-major N x n (one ScalarField per sample,
+ *                      Sample{q,u} dataset.hpp:31-38)
+ *
+ * Every double* argument may be a host pointer (pageable or pinned) or a device
+ * pointer on the context's GPU; the library detects which and stages host
+ * buffers through its own device workspace.
+ *
+ * All compute runs on the GPU (sm_100a kernels in libblockoa_b200.so). There is
+ * no CPU fallback: without a usable GPU, bk_create returns BK_NO_DEVICE.
+ */
+#ifndef BLOCKOA_B200_H
+#define BLOCKOA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BK_ABI_VERSION 1
+
+typedef enum {
+    BK_OK = 0,
+    BK_INVALID_SPEC = 1,         /* InvalidSpecError        errors.hpp:14 */
+    BK_INVALID_CONFIG = 2,       /* InvalidConfigError      errors.hpp:19 */
+    BK_DIMENSION_MISMATCH = 3,   /* DimensionMismatchError  errors.hpp:24 */
+    BK_NONPOSITIVE_K = 4,        /* NonPositiveConductivityError errors.hpp:29 */
+    BK_NONPOSITIVE_HTC = 5,      /* NonPositiveHtcError     errors.hpp:34 */
+    BK_EMPTY_BASIS = 6,          /* EmptyBasisError         errors.hpp:49 */
+    BK_NOT_CONVERGED = 7,        /* NotConvergedError       errors.hpp:39 */
+    BK_INVALID_KAPPA = 8,        /* InvalidKappaError       errors.hpp:44 */
+    BK_CUDA_ERROR = 20,
+    BK_OOM = 21,
+    BK_NO_DEVICE = 22,
+    BK_INTERNAL = 99
+} bk_status;
+
+/* Face conditions (discretize.hpp:14-38). BK_FACE_ADIABATIC is the zero-flux
+ * face the BASELINE configs need; the reference expresses it as
+ * Robin{h=1e-300, u_inf=0}, which assembles to bitwise the same operator. */
+typedef enum { BK_FACE_DIRICHLET = 0, BK_FACE_ROBIN = 1, BK_FACE_ADIABATIC = 2 } bk_face_kind;
+
+typedef struct {
+    int kind;  /* bk_face_kind */
+    double a;  /* Dirichlet: u0 [degC]; Robin: h [W/(m^2 K)] (> 0) */
+    double b;  /* Robin: u_inf [degC] */
+} bk_face;
+
+/* GridSpec (grid.hpp:14-53) plus an optional per-layer thickness array for
+ * non-uniform stacks (BASELINE config 4). dz == NULL: uniform dz = lz/nz. */
+typedef struct {
+    int nx, ny, nz;
+    double lx, ly, lz; /* extents [m] */
+    const double* dz;  /* host pointer, nz entries, or NULL */
+} bk_grid;
+
+/* SolverConfig (solvers.hpp:13-21). */
+typedef struct {
+    double rel_tol; /* in (0, 1) */
+    int max_iter;   /* >= 1 */
+    int precond;    /* 0 none, 1 Jacobi */
+} bk_solver_cfg;
+
+/* SolveReport (solvers.hpp:24-32). The two arrays are caller-provided, length s
+ * (may be NULL). */
+typedef struct {
+    int iterations;
+    int64_t matvec_count;
+    double wall_time; /* seconds, device-timed */
+    double* final_rel_residual;
+    char* converged;
+} bk_solve_report;
+
+/* PhaseTimings (dataset.hpp:17-25), device-timed with CUDA events. */
+typedef struct {
+    double assemble_s;
+    double basis_solve_s;
+    double combine_action_s; /* combine_s + operator_action_s (one fused kernel) */
+    double h2d_s;
+    double d2h_s;
+    double total_s;
+    int64_t iterations_total;
+    int64_t matvecs_total;
+} bk_phase_timings;
+
+typedef struct bk_ctx bk_ctx;
+typedef struct bk_operator bk_operator;
+
+int bk_abi_version(void);
+
+/* One context per (host thread, GPU): owns a stream, events and a grow-only
+ * device workspace. */
+bk_status bk_create(int device, bk_ctx** out);
+void bk_destroy(bk_ctx* ctx);
+const char* bk_last_error(const bk_ctx* ctx);
+/* Run subsequent work on an external cudaStream_t (e.g. torch's current
+ * stream); NULL restores the context's own stream. */
+bk_status bk_set_stream(bk_ctx* ctx, void* cuda_stream);
+bk_status bk_synchronize(bk_ctx* ctx);
+/* Number of this library's kernel launches issued on ctx so far. */
+int64_t bk_launch_count(const bk_ctx* ctx);
+
+/* ---- discretization (discretize.hpp) ------------------------------------ */
+
+/* assemble(k, grid, bc) -> DiscreteOperator        discretize.hpp:76,
+ * discretize.cpp:114-237. Builds the matrix-free SoA stencil in HBM. */
+bk_status bk_assemble(bk_ctx* ctx, const bk_grid* grid, const double* k,
+                      const bk_face bc[6], bk_operator** out);
+void bk_operator_free(bk_operator* op);
+int64_t bk_operator_n(const bk_operator* op);
+
+/* The stencil as the reference's CSR (row_ptr n+1, col/val nnz <= 7n) plus g
+ * and volumes — integer structure bit-exact with discretize.cpp:218-231.
+ * Pass col/val/g/vol = NULL to query *nnz only. Host pointers. */
+bk_status bk_operator_export_csr(bk_ctx* ctx, const bk_operator* op, int64_t* row_ptr,
+                                 int32_t* col, double* val, int64_t* nnz, double* g,
+                                 double* vol);
+
+/* Y = A X for n x s blocks        CsrMatrix::apply_block discretize.hpp:57,
+ * discretize.cpp:75-95 (same per-row FMA accumulation order). */
+bk_status bk_apply_block(bk_ctx* ctx, const bk_operator* op, const double* X, int s,
+                         double* Y);
+
+/* B = V Q + g per column          rhs_from_power discretize.hpp:82 */
+bk_status bk_rhs_from_power(bk_ctx* ctx, const bk_operator* op, const double* Q, int s,
+                            double* B);
+/* Q = (B - g) / V per column      power_from_rhs discretize.hpp:87 */
+bk_status bk_power_from_rhs(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
+                            double* Q);
+
+/* ---- solvers (solvers.hpp) ------------------------------------------------ */
+
+/* block_cg(op, B, cfg) -> {X, report}     solvers.hpp:85, solvers.cpp:452-665.
+ * One persistent sm_100a kernel per solve: fused stencil-SpMM + Gram, fused
+ * block updates, on-device pivoted-Cholesky s x s solves, per-column
+ * verify/freeze/restart. Never fails on non-convergence (report.converged). */
+bk_status bk_block_cg(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
+                      const bk_solver_cfg* cfg, double* X, bk_solve_report* report);
+
+/* ---- pipeline (pipeline.hpp) ------------------------------------------------ */
+
+/* For each sample j: T_j = sum_t C[t][j] X[:,t]  (combine_from_weights,
+ * pipeline.cpp:187-225) and Q_j = (A T_j - g)/V (operator_action,
+ * pipeline.cpp:242-251), resid[j] = ||A T_j - (V Q_j + g)|| / ||V Q_j + g||
+ * (pipeline.cpp:548-571). One fused kernel; T/Q/resid may be NULL to skip. */
+bk_status bk_combine_action(bk_ctx* ctx, const bk_operator* op, const double* X, int s,
+                            const double* C, int64_t N, double* T, double* Q,
+                            double* resid);
+
+/* Whole per-chip pipeline (generate_blockoa, pipeline.cpp:365-597, for one
+ * basis group): assemble -> B = V Qbasis + g -> block CG -> fused combine +
+ * operator action. Qbasis row-major n x s power maps [W/m^3]; C row-major
+ * s x N. Returns BK_NOT_CONVERGED (after filling outputs) if any basis column
+ * missed the tolerance, as generate_basis does (pipeline.cpp:128-132). */
+bk_status bk_generate_chip(bk_ctx* ctx, const bk_grid* grid, const double* k,
+                           const bk_face bc[6], const double* Qbasis, int s,
+                           const double* C, int64_t N, const bk_solver_cfg* cfg,
+                           double* T, double* Q, double* resid, bk_solve_report* report,
+                           bk_phase_timings* timings);
+
+/* cg_error_bound(kappa, m, e0)    solvers.hpp:92, solvers.cpp:672-680 (host). */
+bk_status bk_cg_error_bound(double kappa, int m, double e0, double* out);
+
+/* ---- seeded synthetic inputs (host; BASELINE configs) ------ */
+
+/* derive_seed / Rng (rng.hpp:14-63) restated bit-exactly on the host. */
+uint64_t bk_derive_seed(uint64_t seed, const char* tag, uint64_t index);
+void bk_rng_u64(uint64_t seed, int64_t n, uint64_t* out);
+void bk_rng_uniform(uint64_t seed, double lo, double hi, int64_t n, double* out);
+void bk_rng_normal(uint64_t seed, int64_t n, double* out);
+
+/* Input synthesis for BASELINE config `cfg` in 1..5 (reduced shapes allowed
+ * through the size arguments). Fills k (n), Qbasis (n x s), C (s x N), the
+ * boundary faces and, for layered stacks, dz (nz, or left untouched when the
+ * config has uniform dz; *has_dz tells which). chip_id selects the chip's
+ * seed stream derive_seed(master_seed, "chip", chip_id). */
+typedef struct {
+    int config; /* 1..5 */
+    int nx, ny, nz;
+    int s;
+    int64_t N;
+    uint64_t master_seed;
+    uint64_t chip_id;
+} bk_synth_spec;
+
+bk_status bk_synth_chip(const bk_synth_spec* spec, bk_grid* grid_out, double* dz_out,
+                        int* has_dz, bk_face bc_out[6], double* k, double* Qbasis,
+                        double* C);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BLOCKOA_B200_H */

@@ -1,0 +1,375 @@
+"""TEST INFRASTRUCTURE — ctypes front-ends for the two CPU checkers.
+
+* ``Oracle``    wraps ``oracle/liboracle.so`` (our plain-C restatement,
+  ``oracle/blockoa_oracle.c``), built from committed source — available on the
+  GPU box too (built there with gcc if the prebuilt .so is missing).
+* ``Reference`` wraps ``oracle/_ref/libblockoa_ref.so`` — the UNMODIFIED reference
+  core (/root/reference/proj/core) compiled by ``oracle/Makefile`` plus
+  ``oracle/ref_shim.cpp``.
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's CPU legs import this
+module. Both classes expose the same methods, so tests can run one case through
+either checker. Face kinds follow include/blockoa_b200.h: 0 Dirichlet(a=u0),
+1 Robin(a=h, b=u_inf), 2 adiabatic.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libblockoa_ref.so")
+
+_dp = C.POINTER(C.c_double)
+_lock = threading.Lock()
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile liboracle.so from the committed C source (gcc only)."""
+    with _lock:
+        if force or not os.path.exists(ORACLE_SO) or (
+            os.path.getmtime(ORACLE_SO) < os.path.getmtime(os.path.join(HERE, "blockoa_oracle.c"))
+        ):
+            subprocess.run(["make", "-C", HERE, "liboracle.so"], check=True,
+                           stdout=subprocess.DEVNULL)
+    return ORACLE_SO
+
+
+def build_reference() -> str | None:
+    """Compile oracle/_ref from /root/reference when the sources are present."""
+    if os.path.isdir("/root/reference/proj/core/src"):
+        subprocess.run(["make", "-C", HERE, "ref"], check=True, stdout=subprocess.DEVNULL)
+    return REF_SO if os.path.exists(REF_SO) else None
+
+
+def reference_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def _bc_arrays(bc):
+    kind = np.array([f[0] for f in bc], dtype=np.int32)
+    a = np.array([f[1] for f in bc], dtype=np.float64)
+    b = np.array([f[2] for f in bc], dtype=np.float64)
+    return kind, a, b
+
+
+class CheckerError(RuntimeError):
+    def __init__(self, code, msg=""):
+        super().__init__(f"status {code}: {msg}")
+        self.code = code
+
+
+class _Op:
+    def __init__(self, lib, handle, n, free):
+        self.lib, self.handle, self.n, self._free = lib, handle, n, free
+
+    def __del__(self):
+        try:
+            self._free(self.handle)
+        except Exception:
+            pass
+
+
+class _Base:
+    prefix = ""
+
+    def _f(self, name):
+        return getattr(self.lib, self.prefix + name)
+
+    # ---- operator -------------------------------------------------------
+    def csr(self, op):
+        nnz = int(self._f("op_nnz")(op.handle))
+        row_ptr = np.empty(op.n + 1, np.int64)
+        col = np.empty(nnz, np.int32)
+        val = np.empty(nnz, np.float64)
+        g = np.empty(op.n, np.float64)
+        vol = np.empty(op.n, np.float64)
+        self._f("op_export")(op.handle, _ptr(row_ptr), _ptr(col), _ptr(val), _ptr(g), _ptr(vol))
+        return row_ptr, col, val, g, vol
+
+    def apply_block(self, op, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        s = 1 if x.ndim == 1 else x.shape[1]
+        y = np.empty_like(x)
+        self._f("apply_block")(op.handle, _ptr(x), C.c_int(s), _ptr(y))
+        return y
+
+    def _colwise(self, name, op, a):
+        a = np.asarray(a, dtype=np.float64)
+        if a.ndim == 1:
+            a = np.ascontiguousarray(a)
+            out = np.empty_like(a)
+            self._f(name)(op.handle, _ptr(a), _ptr(out))
+            return out
+        out = np.empty_like(a)
+        for j in range(a.shape[1]):
+            col = np.ascontiguousarray(a[:, j])
+            res = np.empty_like(col)
+            self._f(name)(op.handle, _ptr(col), _ptr(res))
+            out[:, j] = res
+        return out
+
+    def rhs_from_power(self, op, q):
+        """b = V q + g, column by column for an n x s block."""
+        return self._colwise("rhs_from_power", op, q)
+
+    def power_from_rhs(self, op, b):
+        return self._colwise("power_from_rhs", op, b)
+
+    def relative_residual(self, op, u, q):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        f = self._f("relative_residual")
+        f.restype = C.c_double
+        return float(f(op.handle, _ptr(u), _ptr(q)))
+
+    def cg_error_bound(self, kappa, m, e0):
+        f = self._f("cg_error_bound")
+        f.restype = C.c_double
+        st = C.c_int(0)
+        v = f(C.c_double(kappa), C.c_int(m), C.c_double(e0), C.byref(st))
+        if st.value:
+            raise CheckerError(st.value, "cg_error_bound")
+        return float(v)
+
+
+class Oracle(_Base):
+    """Plain-C restatement (oracle/blockoa_oracle.c)."""
+
+    prefix = "orc_"
+
+    def __init__(self, path: str | None = None):
+        path = path or build_oracle()
+        self.lib = C.CDLL(path)
+        self.lib.orc_derive_seed.restype = C.c_uint64
+        self.lib.orc_op_nnz.restype = C.c_int64
+
+    def assemble(self, grid, k, bc, dz=None):
+        nx, ny, nz, lx, ly, lz = grid
+        kind, a, b = _bc_arrays(bc)
+        k = np.ascontiguousarray(k, dtype=np.float64)
+        dzs = None if dz is None else np.ascontiguousarray(dz, dtype=np.float64)
+        h = C.c_void_p()
+        st = self.lib.orc_assemble(C.c_int(nx), C.c_int(ny), C.c_int(nz), C.c_double(lx),
+                                   C.c_double(ly), C.c_double(lz), _ptr(dzs), _ptr(k),
+                                   _ptr(kind), _ptr(a), _ptr(b), C.byref(h))
+        if st:
+            raise CheckerError(st, "orc_assemble")
+        return _Op(self.lib, h, nx * ny * nz, self.lib.orc_op_free)
+
+    def op_from_csr(self, row_ptr, col, val):
+        row_ptr = np.ascontiguousarray(row_ptr, np.int64)
+        col = np.ascontiguousarray(col, np.int32)
+        val = np.ascontiguousarray(val, np.float64)
+        n = row_ptr.size - 1
+        h = C.c_void_p()
+        self.lib.orc_op_from_csr(C.c_int64(n), _ptr(row_ptr), _ptr(col), _ptr(val), C.byref(h))
+        return _Op(self.lib, h, n, self.lib.orc_op_free)
+
+    def block_cg(self, op, B, tol=1e-12, max_iter=100000, precond=1):
+        B = np.ascontiguousarray(B, dtype=np.float64)
+        s = B.shape[1]
+        X = np.empty_like(B)
+        it = C.c_int(0)
+        mv = C.c_int64(0)
+        res = np.zeros(s, np.float64)
+        conv = np.zeros(s, np.int8)
+        st = self.lib.orc_block_cg(op.handle, _ptr(B), C.c_int(s), C.c_double(tol),
+                                   C.c_int(max_iter), C.c_int(precond), _ptr(X), C.byref(it),
+                                   C.byref(mv), _ptr(res), _ptr(conv))
+        if st:
+            raise CheckerError(st, "orc_block_cg")
+        return X, dict(iterations=it.value, matvec_count=mv.value, final_rel_residual=res,
+                       converged=conv.astype(bool))
+
+    def cg(self, op, b, tol=1e-12, max_iter=100000, precond=1):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty_like(b)
+        it, mv, res, conv = C.c_int(0), C.c_int64(0), C.c_double(0), C.c_char(0)
+        st = self.lib.orc_cg(op.handle, _ptr(b), C.c_double(tol), C.c_int(max_iter),
+                             C.c_int(precond), _ptr(x), C.byref(it), C.byref(mv),
+                             C.byref(res), C.byref(conv))
+        if st:
+            raise CheckerError(st, "orc_cg")
+        return x, dict(iterations=it.value, matvec_count=mv.value,
+                       final_rel_residual=res.value, converged=conv.value != b"\x00")
+
+    def combine_action(self, op, X, Cm, j0=0, j1=None, resid=True):
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        Cm = np.ascontiguousarray(Cm, dtype=np.float64)
+        s, N = Cm.shape
+        j1 = N if j1 is None else j1
+        m = j1 - j0
+        T = np.empty((m, op.n), np.float64)
+        Q = np.empty((m, op.n), np.float64)
+        R = np.empty(m, np.float64) if resid else None
+        st = self.lib.orc_combine_action(op.handle, _ptr(X), C.c_int(s), _ptr(Cm),
+                                         C.c_int64(N), C.c_int64(j0), C.c_int64(j1),
+                                         _ptr(T), _ptr(Q), _ptr(R))
+        if st:
+            raise CheckerError(st, "orc_combine_action")
+        return T, Q, R
+
+    def derive_seed(self, seed, tag, index=0):
+        return int(self.lib.orc_derive_seed(C.c_uint64(seed), tag.encode(), C.c_uint64(index)))
+
+    def rng_u64(self, seed, n):
+        out = np.empty(n, np.uint64)
+        self.lib.orc_rng_u64(C.c_uint64(seed), C.c_int64(n), _ptr(out))
+        return out
+
+    def rng_uniform(self, seed, lo, hi, n):
+        out = np.empty(n, np.float64)
+        self.lib.orc_rng_uniform(C.c_uint64(seed), C.c_double(lo), C.c_double(hi),
+                                 C.c_int64(n), _ptr(out))
+        return out
+
+    def rng_normal(self, seed, n):
+        out = np.empty(n, np.float64)
+        self.lib.orc_rng_normal(C.c_uint64(seed), C.c_int64(n), _ptr(out))
+        return out
+
+    def rng_below(self, seed, bound, n):
+        out = np.empty(n, np.uint64)
+        self.lib.orc_rng_below(C.c_uint64(seed), C.c_uint64(bound), C.c_int64(n), _ptr(out))
+        return out
+
+
+class Reference(_Base):
+    """The unmodified reference core via oracle/ref_shim.cpp."""
+
+    prefix = "ref_"
+
+    def __init__(self, path: str | None = None):
+        path = path or REF_SO
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        self.lib = C.CDLL(path)
+        self.lib.ref_derive_seed.restype = C.c_uint64
+        self.lib.ref_op_nnz.restype = C.c_longlong
+        self.lib.ref_last_error.restype = C.c_char_p
+
+    def _err(self, st, what):
+        raise CheckerError(st, f"{what}: {self.lib.ref_last_error().decode()}")
+
+    def assemble(self, grid, k, bc, dz=None):
+        if dz is not None:
+            raise NotImplementedError("reference GridSpec is uniform (grid.hpp:25-28)")
+        nx, ny, nz, lx, ly, lz = grid
+        kind, a, b = _bc_arrays(bc)
+        k = np.ascontiguousarray(k, dtype=np.float64)
+        h = C.c_void_p()
+        st = self.lib.ref_op_create(C.c_int(nx), C.c_int(ny), C.c_int(nz), C.c_double(lx),
+                                    C.c_double(ly), C.c_double(lz), _ptr(k), _ptr(kind),
+                                    _ptr(a), _ptr(b), C.byref(h))
+        if st:
+            self._err(st, "assemble")
+        return _Op(self.lib, h, nx * ny * nz, self.lib.ref_op_free)
+
+    def block_cg(self, op, B, tol=1e-12, max_iter=100000, precond=1):
+        B = np.ascontiguousarray(B, dtype=np.float64)
+        s = B.shape[1]
+        X = np.empty_like(B)
+        it, mv, wall = C.c_int(0), C.c_longlong(0), C.c_double(0)
+        res = np.zeros(s, np.float64)
+        conv = np.zeros(s, np.int8)
+        st = self.lib.ref_block_cg(op.handle, _ptr(B), C.c_int(s), C.c_double(tol),
+                                   C.c_int(max_iter), C.c_int(precond), _ptr(X), C.byref(it),
+                                   C.byref(mv), _ptr(res), _ptr(conv), C.byref(wall))
+        if st:
+            self._err(st, "block_cg")
+        return X, dict(iterations=it.value, matvec_count=mv.value, final_rel_residual=res,
+                       converged=conv.astype(bool), wall_time=wall.value)
+
+    def block_cg_csr(self, row_ptr, col, val, B, tol=1e-10, max_iter=100000, precond=0):
+        B = np.ascontiguousarray(B, dtype=np.float64)
+        n, s = B.shape
+        row_ptr = np.ascontiguousarray(row_ptr, np.int64)
+        col = np.ascontiguousarray(col, np.int32)
+        val = np.ascontiguousarray(val, np.float64)
+        X = np.empty_like(B)
+        it, mv = C.c_int(0), C.c_longlong(0)
+        res = np.zeros(s, np.float64)
+        conv = np.zeros(s, np.int8)
+        st = self.lib.ref_block_cg_csr(C.c_longlong(n), _ptr(row_ptr), _ptr(col), _ptr(val),
+                                       _ptr(B), C.c_int(s), C.c_double(tol), C.c_int(max_iter),
+                                       C.c_int(precond), _ptr(X), C.byref(it), C.byref(mv),
+                                       _ptr(res), _ptr(conv))
+        if st:
+            self._err(st, "block_cg_csr")
+        return X, dict(iterations=it.value, matvec_count=mv.value, final_rel_residual=res,
+                       converged=conv.astype(bool))
+
+    def cg(self, op, b, tol=1e-12, max_iter=100000, precond=1):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty_like(b)
+        it, mv, res, conv = C.c_int(0), C.c_longlong(0), C.c_double(0), C.c_char(0)
+        st = self.lib.ref_cg(op.handle, _ptr(b), C.c_double(tol), C.c_int(max_iter),
+                             C.c_int(precond), _ptr(x), C.byref(it), C.byref(mv),
+                             C.byref(res), C.byref(conv))
+        if st:
+            self._err(st, "cg")
+        return x, dict(iterations=it.value, matvec_count=mv.value,
+                       final_rel_residual=res.value, converged=conv.value != b"\x00")
+
+    def cg_csr(self, row_ptr, col, val, b, tol=1e-12, max_iter=100000, precond=0):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        n = b.size
+        x = np.empty_like(b)
+        it, mv, res, conv = C.c_int(0), C.c_longlong(0), C.c_double(0), C.c_char(0)
+        st = self.lib.ref_cg_csr(C.c_longlong(n), _ptr(np.ascontiguousarray(row_ptr, np.int64)),
+                                 _ptr(np.ascontiguousarray(col, np.int32)),
+                                 _ptr(np.ascontiguousarray(val, np.float64)), _ptr(b),
+                                 C.c_double(tol), C.c_int(max_iter), C.c_int(precond), _ptr(x),
+                                 C.byref(it), C.byref(mv), C.byref(res), C.byref(conv))
+        if st:
+            self._err(st, "cg_csr")
+        return x, dict(iterations=it.value, matvec_count=mv.value,
+                       final_rel_residual=res.value, converged=conv.value != b"\x00")
+
+    def combine_action(self, op, X, Cm, threads=1, resid=True):
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        Cm = np.ascontiguousarray(Cm, dtype=np.float64)
+        s, N = Cm.shape
+        T = np.empty((N, op.n), np.float64)
+        Q = np.empty((N, op.n), np.float64)
+        R = np.empty(N, np.float64) if resid else None
+        st = self.lib.ref_combine_action(op.handle, _ptr(X), C.c_int(s), _ptr(Cm),
+                                         C.c_longlong(N), _ptr(T), _ptr(Q), _ptr(R),
+                                         C.c_int(threads))
+        if st:
+            self._err(st, "combine_action")
+        return T, Q, R
+
+    def derive_seed(self, seed, tag, index=0):
+        return int(self.lib.ref_derive_seed(C.c_uint64(seed), tag.encode(), C.c_uint64(index)))
+
+    def rng_u64(self, seed, n):
+        out = np.empty(n, np.uint64)
+        self.lib.ref_rng_u64(C.c_uint64(seed), C.c_longlong(n), _ptr(out))
+        return out
+
+    def rng_uniform(self, seed, lo, hi, n):
+        out = np.empty(n, np.float64)
+        self.lib.ref_rng_uniform(C.c_uint64(seed), C.c_double(lo), C.c_double(hi),
+                                 C.c_longlong(n), _ptr(out))
+        return out
+
+    def rng_normal(self, seed, n):
+        out = np.empty(n, np.float64)
+        self.lib.ref_rng_normal(C.c_uint64(seed), C.c_longlong(n), _ptr(out))
+        return out
+
+    def rng_below(self, seed, bound, n):
+        out = np.empty(n, np.uint64)
+        self.lib.ref_rng_below(C.c_uint64(seed), C.c_uint64(bound), C.c_longlong(n), _ptr(out))
+        return out

@@ -1,0 +1,354 @@
+// TEST INFRASTRUCTURE — NOT PRODUCT CODE.
+//
+// extern "C" shim over the UNMODIFIED reference core (/root/reference/proj/core),
+// compiled by oracle/Makefile into oracle/_ref/libblockoa_ref.so. Only tests/,
+// __graft_entry__.smoke() and bench.py's CPU legs (cpu_baseline and
+// `--impl reference`) load it, as the checker / the timed reference arm.
+//
+// Every entry point calls the reference's own public API:
+//   assemble               discretize.hpp:76  (discretize.cpp:114-237)
+//   CsrMatrix::apply_block discretize.hpp:57  (discretize.cpp:75-95)
+//   rhs_from_power         discretize.hpp:82  (discretize.cpp:246-256)
+//   power_from_rhs         discretize.hpp:87  (discretize.cpp:258-267)
+//   relative_residual      discretize.hpp:91  (discretize.cpp:275-286)
+//   cg / block_cg          solvers.hpp:45,85  (solvers.cpp:82-171, 452-665)
+//   cg_error_bound         solvers.hpp:92     (solvers.cpp:672-680)
+//   combine_from_weights   pipeline.hpp:85    (pipeline.cpp:187-225)
+//   operator_action        pipeline.hpp:95    (pipeline.cpp:242-251)
+//   Rng / derive_seed      rng.hpp:14-63      (rng.cpp)
+// Exceptions are mapped to the status codes of include/blockoa_b200.h.
+
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "blockoa/discretize.hpp"
+#include "blockoa/errors.hpp"
+#include "blockoa/parallel.hpp"
+#include "blockoa/pipeline.hpp"
+#include "blockoa/rng.hpp"
+#include "blockoa/solvers.hpp"
+
+using namespace blockoa;
+
+namespace {
+
+thread_local std::string g_err;
+
+int map_exception() {
+    try {
+        throw;
+    } catch (const InvalidSpecError& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const InvalidConfigError& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const DimensionMismatchError& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const NonPositiveConductivityError& e) {
+        g_err = e.what();
+        return 4;
+    } catch (const NonPositiveHtcError& e) {
+        g_err = e.what();
+        return 5;
+    } catch (const EmptyBasisError& e) {
+        g_err = e.what();
+        return 6;
+    } catch (const NotConvergedError& e) {
+        g_err = e.what();
+        return 7;
+    } catch (const InvalidKappaError& e) {
+        g_err = e.what();
+        return 8;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 99;
+    }
+}
+
+// Face kinds as in include/blockoa_b200.h: 0 Dirichlet{u0=a}, 1 Robin{h=a,
+// u_inf=b}, 2 adiabatic. The reference has no adiabatic face; it is expressed
+// as Robin{1e-300, 0}, which leaves diag and g bitwise
+// equal to a zero-flux face.
+BoundarySpec make_bc(const int* kind, const double* a, const double* b) {
+    BoundarySpec bc;
+    for (int f = 0; f < 6; ++f) {
+        if (kind[f] == 0)
+            bc.faces[f] = Dirichlet{a[f]};
+        else if (kind[f] == 1)
+            bc.faces[f] = Robin{a[f], b[f]};
+        else
+            bc.faces[f] = Robin{1e-300, 0.0};
+    }
+    return bc;
+}
+
+SolverConfig make_cfg(double tol, int max_iter, int precond) {
+    SolverConfig c;
+    c.rel_tol = tol;
+    c.max_iter = max_iter;
+    c.preconditioner = precond ? SolverConfig::Precond::jacobi : SolverConfig::Precond::none;
+    return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// ---- operator ---------------------------------------------------------------
+int ref_op_create(int nx, int ny, int nz, double lx, double ly, double lz,
+                  const double* k, const int* bc_kind, const double* bc_a,
+                  const double* bc_b, void** out) {
+    try {
+        GridSpec grid{nx, ny, nz, lx, ly, lz};
+        ScalarField kf{grid, Unit::conductivity_w_per_m_k,
+                       std::vector<double>(k, k + grid.cell_count())};
+        auto* op = new DiscreteOperator(assemble(kf, grid, make_bc(bc_kind, bc_a, bc_b)));
+        *out = op;
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+void ref_op_free(void* op) { delete static_cast<DiscreteOperator*>(op); }
+
+long long ref_op_nnz(const void* op) {
+    return static_cast<const DiscreteOperator*>(op)->A.nnz();
+}
+
+void ref_op_export(const void* vop, long long* row_ptr, int* col, double* val,
+                   double* g, double* vol) {
+    const auto* op = static_cast<const DiscreteOperator*>(vop);
+    const auto& a = op->A;
+    for (std::size_t i = 0; i < a.row_ptr.size(); ++i) row_ptr[i] = a.row_ptr[i];
+    std::memcpy(col, a.col.data(), a.col.size() * sizeof(int));
+    std::memcpy(val, a.val.data(), a.val.size() * sizeof(double));
+    std::memcpy(g, op->g.data(), op->g.size() * sizeof(double));
+    std::memcpy(vol, op->volumes.data(), op->volumes.size() * sizeof(double));
+}
+
+int ref_apply_block(const void* vop, const double* x, int s, double* y) {
+    try {
+        static_cast<const DiscreteOperator*>(vop)->A.apply_block(x, s, y);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+int ref_apply(const void* vop, const double* x, double* y) {
+    try {
+        const auto* op = static_cast<const DiscreteOperator*>(vop);
+        const auto n = static_cast<std::size_t>(op->A.n);
+        std::vector<double> r = apply(*op, std::span<const double>(x, n));
+        std::memcpy(y, r.data(), n * sizeof(double));
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+int ref_rhs_from_power(const void* vop, const double* q, double* b) {
+    try {
+        const auto* op = static_cast<const DiscreteOperator*>(vop);
+        ScalarField qf{op->grid, Unit::power_density_w_per_m3,
+                       std::vector<double>(q, q + op->A.n)};
+        std::vector<double> r = rhs_from_power(*op, qf);
+        std::memcpy(b, r.data(), r.size() * sizeof(double));
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+int ref_power_from_rhs(const void* vop, const double* b, double* q) {
+    try {
+        const auto* op = static_cast<const DiscreteOperator*>(vop);
+        ScalarField qf = power_from_rhs(*op, std::span<const double>(b, op->A.n));
+        std::memcpy(q, qf.values.data(), qf.values.size() * sizeof(double));
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+double ref_relative_residual(const void* vop, const double* u, const double* q) {
+    const auto* op = static_cast<const DiscreteOperator*>(vop);
+    ScalarField qf{op->grid, Unit::power_density_w_per_m3,
+                   std::vector<double>(q, q + op->A.n)};
+    return relative_residual(*op, std::span<const double>(u, op->A.n), qf);
+}
+
+// ---- solvers ----------------------------------------------------------------
+// B, X row-major n x s (MultiVector layout, solvers.hpp:55-58).
+int ref_block_cg(const void* vop, const double* b, int s, double tol, int max_iter,
+                 int precond, double* x, int* iterations, long long* matvecs,
+                 double* resid, char* conv, double* wall) {
+    try {
+        const auto* op = static_cast<const DiscreteOperator*>(vop);
+        MultiVector mb;
+        mb.n = op->A.n;
+        mb.s = s;
+        mb.data.assign(b, b + static_cast<std::size_t>(op->A.n) * s);
+        BlockCgResult r = block_cg(*op, mb, make_cfg(tol, max_iter, precond));
+        std::memcpy(x, r.x.data.data(), r.x.data.size() * sizeof(double));
+        *iterations = r.report.iterations;
+        *matvecs = r.report.matvec_count;
+        for (int j = 0; j < s; ++j) {
+            resid[j] = r.report.final_rel_residual[j];
+            conv[j] = r.report.converged[j];
+        }
+        *wall = r.report.wall_time;
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+int ref_cg(const void* vop, const double* b, double tol, int max_iter, int precond,
+           double* x, int* iterations, long long* matvecs, double* resid, char* conv) {
+    try {
+        const auto* op = static_cast<const DiscreteOperator*>(vop);
+        CgResult r = cg(*op, std::span<const double>(b, op->A.n),
+                        make_cfg(tol, max_iter, precond));
+        std::memcpy(x, r.x.data(), r.x.size() * sizeof(double));
+        *iterations = r.report.iterations;
+        *matvecs = r.report.matvec_count;
+        *resid = r.report.final_rel_residual[0];
+        *conv = r.report.converged[0];
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// Generic CSR block CG on a caller-provided SPD matrix (SPEC 100x100 case).
+int ref_block_cg_csr(long long n, const long long* row_ptr, const int* col,
+                     const double* val, const double* b, int s, double tol,
+                     int max_iter, int precond, double* x, int* iterations,
+                     long long* matvecs, double* resid, char* conv) {
+    try {
+        CsrMatrix a;
+        a.n = n;
+        a.row_ptr.assign(row_ptr, row_ptr + n + 1);
+        a.col.assign(col, col + row_ptr[n]);
+        a.val.assign(val, val + row_ptr[n]);
+        MultiVector mb;
+        mb.n = n;
+        mb.s = s;
+        mb.data.assign(b, b + static_cast<std::size_t>(n) * s);
+        BlockCgResult r = block_cg(a, mb, make_cfg(tol, max_iter, precond));
+        std::memcpy(x, r.x.data.data(), r.x.data.size() * sizeof(double));
+        *iterations = r.report.iterations;
+        *matvecs = r.report.matvec_count;
+        for (int j = 0; j < s; ++j) {
+            resid[j] = r.report.final_rel_residual[j];
+            conv[j] = r.report.converged[j];
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+int ref_cg_csr(long long n, const long long* row_ptr, const int* col, const double* val,
+               const double* b, double tol, int max_iter, int precond, double* x,
+               int* iterations, long long* matvecs, double* resid, char* conv) {
+    try {
+        CsrMatrix a;
+        a.n = n;
+        a.row_ptr.assign(row_ptr, row_ptr + n + 1);
+        a.col.assign(col, col + row_ptr[n]);
+        a.val.assign(val, val + row_ptr[n]);
+        CgResult r = cg(a, std::span<const double>(b, n), make_cfg(tol, max_iter, precond));
+        std::memcpy(x, r.x.data(), r.x.size() * sizeof(double));
+        *iterations = r.report.iterations;
+        *matvecs = r.report.matvec_count;
+        *resid = r.report.final_rel_residual[0];
+        *conv = r.report.converged[0];
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+double ref_cg_error_bound(double kappa, int m, double e0, int* status) {
+    try {
+        *status = 0;
+        return cg_error_bound(kappa, m, e0);
+    } catch (...) {
+        *status = map_exception();
+        return 0.0;
+    }
+}
+
+// ---- combination + operator action (one basis group) --------------------------
+// X row-major n x s (the group's solved basis), C row-major s x N (column j =
+// sample j's weights). T, Q sample-major N x n; resid per sample is the
+// reference relative_residual(op, T_j, Q_j). Samples run in parallel_for
+// (parallel.hpp:14-34) over `threads` workers, as generate_blockoa does.
+int ref_combine_action(const void* vop, const double* x, int s, const double* c,
+                       long long n_samples, double* t_out, double* q_out,
+                       double* resid, int threads) {
+    try {
+        const auto* op = static_cast<const DiscreteOperator*>(vop);
+        const std::int64_t n = op->A.n;
+        BasisSet basis;
+        basis.groups.resize(1);
+        BasisGroup& grp = basis.groups[0];
+        grp.op = *op;
+        grp.x.n = n;
+        grp.x.s = s;
+        grp.x.data.assign(x, x + static_cast<std::size_t>(n) * s);
+        parallel_for(0, n_samples, threads, [&](std::int64_t j) {
+            std::vector<double> w(static_cast<std::size_t>(s));
+            for (int t = 0; t < s; ++t) w[t] = c[static_cast<std::size_t>(t) * n_samples + j];
+            std::vector<double> tj = combine_from_weights(basis, w);
+            ScalarField qj = operator_action(basis, 0, tj);
+            std::memcpy(t_out + j * n, tj.data(), n * sizeof(double));
+            std::memcpy(q_out + j * n, qj.values.data(), n * sizeof(double));
+            if (resid) resid[j] = relative_residual(*op, tj, qj);
+        });
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// ---- RNG (rng.hpp) ------------------------------------------------------------
+unsigned long long ref_derive_seed(unsigned long long seed, const char* tag,
+                                   unsigned long long index) {
+    return derive_seed(seed, tag, index);
+}
+
+void ref_rng_u64(unsigned long long seed, long long n, unsigned long long* out) {
+    Rng r(seed);
+    for (long long i = 0; i < n; ++i) out[i] = r.next_u64();
+}
+
+void ref_rng_uniform(unsigned long long seed, double lo, double hi, long long n,
+                     double* out) {
+    Rng r(seed);
+    for (long long i = 0; i < n; ++i) out[i] = r.uniform(lo, hi);
+}
+
+void ref_rng_normal(unsigned long long seed, long long n, double* out) {
+    Rng r(seed);
+    for (long long i = 0; i < n; ++i) out[i] = r.normal();
+}
+
+void ref_rng_below(unsigned long long seed, unsigned long long bound, long long n,
+                   unsigned long long* out) {
+    Rng r(seed);
+    for (long long i = 0; i < n; ++i) out[i] = r.below(bound);
+}
+
+}  // extern "C"

@@ -1,0 +1,622 @@
+"""B200-native BlocKOA data-generation hot path (arxiv 2510.23221).
+
+Python mirror of the reference's C++ operator API for the hot path
+(/root/reference/proj/core/include/blockoa/*.hpp), bound through ctypes to the
+C ABI of ``libblockoa_b200.so`` (include/blockoa_b200.h). Names, argument
+meaning and error behaviour follow the reference:
+
+==========================  ==================================================
+this module                 reference
+==========================  ==================================================
+``GridSpec``                ``GridSpec`` grid.hpp:14-53 (+ optional layer dz)
+``Dirichlet/Robin/...``     ``FaceCondition`` discretize.hpp:14-24
+``BoundarySpec``            ``BoundarySpec`` discretize.hpp:28-38
+``assemble``                ``assemble`` discretize.cpp:114-237
+``DiscreteOperator.apply_block``  ``CsrMatrix::apply_block`` :75-95
+``rhs_from_power``          ``rhs_from_power`` discretize.cpp:246-256
+``power_from_rhs``          ``power_from_rhs`` discretize.cpp:258-267
+``SolverConfig``            ``SolverConfig`` solvers.hpp:13-21
+``block_cg``                ``block_cg`` solvers.cpp:452-665
+``combine_action``          ``combine_from_weights`` + ``operator_action``
+                            pipeline.cpp:187-251 (+ sample residual :548-571)
+``generate_chip``           ``generate_blockoa`` for one basis group
+                            pipeline.cpp:365-597
+``cg_error_bound``          ``cg_error_bound`` solvers.cpp:672-680
+exceptions                  errors.hpp:9-71
+==========================  ==================================================
+
+Arrays may be numpy (host) or CUDA torch tensors (device, used in place). All
+compute runs in the sm_100a kernels of libblockoa_b200.so; there is no CPU
+fallback — without the built library or a GPU every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "GridSpec", "Dirichlet", "Robin", "Adiabatic", "BoundarySpec", "SolverConfig",
+    "SolveReport", "BlockCgResult", "PhaseTimings", "DiscreteOperator", "Context",
+    "assemble", "block_cg", "combine_action", "generate_chip", "rhs_from_power",
+    "power_from_rhs", "cg_error_bound", "derive_seed", "synth_chip", "library_path",
+    "Error", "InvalidSpecError", "InvalidConfigError", "DimensionMismatchError",
+    "NonPositiveConductivityError", "NonPositiveHtcError", "EmptyBasisError",
+    "NotConvergedError", "InvalidKappaError", "DeviceError",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libblockoa_b200.so")
+
+
+def library_path() -> str:
+    return LIB_PATH
+
+
+# ---------------------------------------------------------------- exceptions
+class Error(RuntimeError):
+    """Base of everything raised on purpose (blockoa::Error, errors.hpp:9)."""
+
+
+class InvalidSpecError(Error): ...
+class InvalidConfigError(Error): ...
+class DimensionMismatchError(Error): ...
+class NonPositiveConductivityError(Error): ...
+class NonPositiveHtcError(Error): ...
+class EmptyBasisError(Error): ...
+class NotConvergedError(Error): ...
+class InvalidKappaError(Error): ...
+class DeviceError(Error):
+    """CUDA failure, out of device memory, or no usable sm_100 device."""
+
+
+_STATUS = {
+    1: InvalidSpecError, 2: InvalidConfigError, 3: DimensionMismatchError,
+    4: NonPositiveConductivityError, 5: NonPositiveHtcError, 6: EmptyBasisError,
+    7: NotConvergedError, 8: InvalidKappaError, 20: DeviceError, 21: DeviceError,
+    22: DeviceError, 99: Error,
+}
+
+
+# ---------------------------------------------------------------- C types
+class _Face(C.Structure):
+    _fields_ = [("kind", C.c_int), ("a", C.c_double), ("b", C.c_double)]
+
+
+class _Grid(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("lx", C.c_double),
+                ("ly", C.c_double), ("lz", C.c_double), ("dz", C.c_void_p)]
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("rel_tol", C.c_double), ("max_iter", C.c_int), ("precond", C.c_int)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("matvec_count", C.c_int64), ("wall_time", C.c_double),
+                ("final_rel_residual", C.c_void_p), ("converged", C.c_void_p)]
+
+
+class _Timings(C.Structure):
+    _fields_ = [("assemble_s", C.c_double), ("basis_solve_s", C.c_double),
+                ("combine_action_s", C.c_double), ("h2d_s", C.c_double), ("d2h_s", C.c_double),
+                ("total_s", C.c_double), ("iterations_total", C.c_int64),
+                ("matvecs_total", C.c_int64)]
+
+
+class _Synth(C.Structure):
+    _fields_ = [("config", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
+                ("s", C.c_int), ("N", C.c_int64), ("master_seed", C.c_uint64),
+                ("chip_id", C.c_uint64)]
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(
+                f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = C.CDLL(LIB_PATH)
+        vp, dp = C.c_void_p, C.c_void_p
+        lib.bk_create.argtypes = [C.c_int, C.POINTER(vp)]
+        lib.bk_destroy.argtypes = [vp]
+        lib.bk_destroy.restype = None
+        lib.bk_last_error.argtypes = [vp]
+        lib.bk_last_error.restype = C.c_char_p
+        lib.bk_set_stream.argtypes = [vp, vp]
+        lib.bk_synchronize.argtypes = [vp]
+        lib.bk_launch_count.argtypes = [vp]
+        lib.bk_launch_count.restype = C.c_int64
+        lib.bk_assemble.argtypes = [vp, C.POINTER(_Grid), dp, C.POINTER(_Face), C.POINTER(vp)]
+        lib.bk_operator_free.argtypes = [vp]
+        lib.bk_operator_free.restype = None
+        lib.bk_operator_n.argtypes = [vp]
+        lib.bk_operator_n.restype = C.c_int64
+        lib.bk_operator_export_csr.argtypes = [vp, vp, dp, dp, dp, C.POINTER(C.c_int64), dp, dp]
+        lib.bk_apply_block.argtypes = [vp, vp, dp, C.c_int, dp]
+        lib.bk_rhs_from_power.argtypes = [vp, vp, dp, C.c_int, dp]
+        lib.bk_power_from_rhs.argtypes = [vp, vp, dp, C.c_int, dp]
+        lib.bk_block_cg.argtypes = [vp, vp, dp, C.c_int, C.POINTER(_Cfg), dp, C.POINTER(_Report)]
+        lib.bk_combine_action.argtypes = [vp, vp, dp, C.c_int, dp, C.c_int64, dp, dp, dp]
+        lib.bk_generate_chip.argtypes = [vp, C.POINTER(_Grid), dp, C.POINTER(_Face), dp, C.c_int,
+                                         dp, C.c_int64, C.POINTER(_Cfg), dp, dp, dp,
+                                         C.POINTER(_Report), C.POINTER(_Timings)]
+        lib.bk_cg_error_bound.argtypes = [C.c_double, C.c_int, C.c_double, C.POINTER(C.c_double)]
+        lib.bk_derive_seed.argtypes = [C.c_uint64, C.c_char_p, C.c_uint64]
+        lib.bk_derive_seed.restype = C.c_uint64
+        lib.bk_rng_u64.argtypes = [C.c_uint64, C.c_int64, dp]
+        lib.bk_rng_u64.restype = None
+        lib.bk_rng_uniform.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_int64, dp]
+        lib.bk_rng_uniform.restype = None
+        lib.bk_rng_normal.argtypes = [C.c_uint64, C.c_int64, dp]
+        lib.bk_rng_normal.restype = None
+        lib.bk_synth_chip.argtypes = [C.POINTER(_Synth), C.POINTER(_Grid), dp, C.POINTER(C.c_int),
+                                      C.POINTER(_Face), dp, dp, dp]
+        lib.bk_abi_version.restype = C.c_int
+        _lib = lib
+    return _lib
+
+
+def _raise(st: int, ctx=None, what: str = ""):
+    if st == 0:
+        return
+    msg = what
+    if ctx is not None:
+        msg = f"{what}: {_load().bk_last_error(ctx).decode()}"
+    raise _STATUS.get(st, Error)(msg)
+
+
+# ---------------------------------------------------------------- arrays
+def _is_torch(a) -> bool:
+    return type(a).__module__.startswith("torch")
+
+
+def _ptr(a):
+    """(pointer, keepalive) for a numpy array or a torch tensor (host or CUDA)."""
+    if a is None:
+        return None, None
+    if _is_torch(a):
+        if not a.is_contiguous() or str(a.dtype) != "torch.float64":
+            raise DimensionMismatchError("tensors must be contiguous float64")
+        return C.c_void_p(a.data_ptr()), a
+    arr = np.ascontiguousarray(a, dtype=np.float64)
+    return arr.ctypes.data_as(C.c_void_p), arr
+
+
+def _numel(a) -> int:
+    return int(a.numel()) if _is_torch(a) else int(np.asarray(a).size)
+
+
+# ---------------------------------------------------------------- reference types
+@dataclass
+class GridSpec:
+    """Uniform cell-centred grid (grid.hpp:14-53); ``dz`` optionally gives the
+    nz layer thicknesses of a non-uniform stack (BASELINE config 4)."""
+    nx: int = 1
+    ny: int = 1
+    nz: int = 1
+    lx: float = 1.0
+    ly: float = 1.0
+    lz: float = 1.0
+    dz: Optional[Sequence[float]] = None
+
+    def cell_count(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def flat(self, ix: int, iy: int, iz: int) -> int:
+        return ix + self.nx * (iy + self.ny * iz)
+
+    def _c(self):
+        g = _Grid(self.nx, self.ny, self.nz, self.lx, self.ly, self.lz, None)
+        keep = None
+        if self.dz is not None:
+            keep = np.ascontiguousarray(self.dz, dtype=np.float64)
+            if keep.size != self.nz:
+                raise DimensionMismatchError("grid: dz must have nz entries")
+            g.dz = keep.ctypes.data_as(C.c_void_p)
+        return g, keep
+
+
+@dataclass(frozen=True)
+class Dirichlet:
+    u0: float = 0.0
+
+
+@dataclass(frozen=True)
+class Robin:
+    h: float = 0.0
+    u_inf: float = 0.0
+
+
+@dataclass(frozen=True)
+class Adiabatic:
+    """Zero-flux face (the reference expresses it as Robin{1e-300, 0})."""
+
+
+@dataclass
+class BoundarySpec:
+    """Face order x-, x+, y-, y+, z-, z+ (discretize.hpp:26)."""
+    faces: list = field(default_factory=lambda: [Dirichlet()] * 6)
+
+    @staticmethod
+    def uniform_dirichlet(u0: float) -> "BoundarySpec":
+        return BoundarySpec([Dirichlet(u0)] * 6)
+
+    @staticmethod
+    def uniform_robin(h: float, u_inf: float) -> "BoundarySpec":
+        return BoundarySpec([Robin(h, u_inf)] * 6)
+
+    @staticmethod
+    def mixed(h: float, u_inf: float, side_u0: float) -> "BoundarySpec":
+        return BoundarySpec([Dirichlet(side_u0)] * 4 + [Robin(h, u_inf)] * 2)
+
+    def _c(self):
+        arr = (_Face * 6)()
+        for i, f in enumerate(self.faces):
+            if isinstance(f, Dirichlet):
+                arr[i] = _Face(0, f.u0, 0.0)
+            elif isinstance(f, Robin):
+                arr[i] = _Face(1, f.h, f.u_inf)
+            elif isinstance(f, Adiabatic):
+                arr[i] = _Face(2, 0.0, 0.0)
+            else:
+                raise InvalidSpecError(f"unknown face condition {f!r}")
+        return arr
+
+    def as_tuples(self):
+        """(kind, a, b) per face — the form the CPU checkers take."""
+        out = []
+        for f in self.faces:
+            if isinstance(f, Dirichlet):
+                out.append((0, f.u0, 0.0))
+            elif isinstance(f, Robin):
+                out.append((1, f.h, f.u_inf))
+            else:
+                out.append((2, 0.0, 0.0))
+        return out
+
+
+@dataclass
+class SolverConfig:
+    rel_tol: float = 1e-9
+    max_iter: int = 10000
+    preconditioner: str = "none"  # "none" | "jacobi"
+
+    def _c(self):
+        if self.preconditioner not in ("none", "jacobi"):
+            raise InvalidConfigError("solver: preconditioner must be none|jacobi")
+        return _Cfg(self.rel_tol, self.max_iter, 1 if self.preconditioner == "jacobi" else 0)
+
+
+@dataclass
+class SolveReport:
+    iterations: int
+    final_rel_residual: np.ndarray
+    converged: np.ndarray
+    wall_time: float
+    matvec_count: int
+
+    def all_converged(self) -> bool:
+        return bool(np.all(self.converged))
+
+
+@dataclass
+class BlockCgResult:
+    x: object
+    report: SolveReport
+
+
+@dataclass
+class PhaseTimings:
+    assemble_s: float
+    basis_solve_s: float
+    combine_action_s: float
+    h2d_s: float
+    d2h_s: float
+    total_s: float
+    iterations_total: int
+    matvecs_total: int
+
+
+# ---------------------------------------------------------------- context
+class Context:
+    """One per (thread, GPU): stream + device workspace (bk_ctx)."""
+
+    def __init__(self, device: int = 0):
+        lib = _load()
+        h = C.c_void_p()
+        st = lib.bk_create(device, C.byref(h))
+        if st:
+            _raise(st, None, f"bk_create(device={device}): no usable sm_100 GPU")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            _load().bk_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: Optional[int]):
+        _raise(_load().bk_set_stream(self.h, C.c_void_p(stream_ptr) if stream_ptr else None),
+               self.h, "set_stream")
+
+    def synchronize(self):
+        _raise(_load().bk_synchronize(self.h), self.h, "synchronize")
+
+    @property
+    def launch_count(self) -> int:
+        return int(_load().bk_launch_count(self.h))
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def _ctx(ctx):
+    return ctx if ctx is not None else default_context()
+
+
+# ---------------------------------------------------------------- operator
+class DiscreteOperator:
+    """Device-resident matrix-free stencil (DiscreteOperator, discretize.hpp:62-69)."""
+
+    def __init__(self, handle, ctx: Context, grid: GridSpec, boundary: BoundarySpec):
+        self.h = handle
+        self.ctx = ctx
+        self.grid = grid
+        self.boundary = boundary
+        self.n = grid.cell_count()
+
+    def __del__(self):
+        try:
+            if self.h:
+                _load().bk_operator_free(self.h)
+        except Exception:
+            pass
+
+    def csr(self):
+        """(row_ptr int64[n+1], col int32[nnz], val, g, volumes) in the reference CSR order."""
+        lib = _load()
+        nnz = C.c_int64(0)
+        row_ptr = np.empty(self.n + 1, np.int64)
+        _raise(lib.bk_operator_export_csr(self.ctx.h, self.h, row_ptr.ctypes.data_as(C.c_void_p),
+                                          None, None, C.byref(nnz), None, None), self.ctx.h, "csr")
+        col = np.empty(nnz.value, np.int32)
+        val = np.empty(nnz.value, np.float64)
+        g = np.empty(self.n, np.float64)
+        vol = np.empty(self.n, np.float64)
+        _raise(lib.bk_operator_export_csr(
+            self.ctx.h, self.h, row_ptr.ctypes.data_as(C.c_void_p), col.ctypes.data_as(C.c_void_p),
+            val.ctypes.data_as(C.c_void_p), C.byref(nnz), g.ctypes.data_as(C.c_void_p),
+            vol.ctypes.data_as(C.c_void_p)), self.ctx.h, "csr")
+        return row_ptr, col, val, g, vol
+
+    def apply_block(self, x, out=None):
+        """Y = A X for an n x s block (or a length-n vector)."""
+        s = 1 if len(x.shape) == 1 else int(x.shape[1])
+        if int(x.shape[0]) != self.n:
+            raise DimensionMismatchError("apply_block: rows != n")
+        px, kx = _ptr(x)
+        if out is None:
+            out = np.empty(tuple(x.shape), np.float64)
+        py, ky = _ptr(out)
+        _raise(_load().bk_apply_block(self.ctx.h, self.h, px, s, py), self.ctx.h, "apply_block")
+        return out
+
+
+def assemble(k, grid: GridSpec, bc: BoundarySpec, ctx: Optional[Context] = None) -> DiscreteOperator:
+    """assemble(k, grid, bc) (discretize.cpp:114-237) -> device stencil."""
+    ctx = _ctx(ctx)
+    if _numel(k) != grid.cell_count():
+        raise DimensionMismatchError("assemble: conductivity grid mismatch")
+    g, keep = grid._c()
+    faces = bc._c()
+    pk, kk = _ptr(k)
+    h = C.c_void_p()
+    _raise(_load().bk_assemble(ctx.h, C.byref(g), pk, faces, C.byref(h)), ctx.h, "assemble")
+    return DiscreteOperator(h, ctx, grid, bc)
+
+
+def _cols(a) -> int:
+    return 1 if len(a.shape) == 1 else int(a.shape[1])
+
+
+def rhs_from_power(op: DiscreteOperator, q, out=None):
+    """b = V q + g (column-wise for an n x s block)."""
+    if int(q.shape[0]) != op.n:
+        raise DimensionMismatchError("rhs_from_power: power grid mismatch")
+    pq, kq = _ptr(q)
+    out = np.empty(tuple(q.shape), np.float64) if out is None else out
+    pb, kb = _ptr(out)
+    _raise(_load().bk_rhs_from_power(op.ctx.h, op.h, pq, _cols(q), pb), op.ctx.h, "rhs_from_power")
+    return out
+
+
+def power_from_rhs(op: DiscreteOperator, b, out=None):
+    """q = (b - g) / V."""
+    if int(b.shape[0]) != op.n:
+        raise DimensionMismatchError("power_from_rhs: vector length != n")
+    pb, kb = _ptr(b)
+    out = np.empty(tuple(b.shape), np.float64) if out is None else out
+    pq, kq = _ptr(out)
+    _raise(_load().bk_power_from_rhs(op.ctx.h, op.h, pb, _cols(b), pq), op.ctx.h, "power_from_rhs")
+    return out
+
+
+def _report(s, rep_c, res, conv) -> SolveReport:
+    return SolveReport(iterations=rep_c.iterations, final_rel_residual=res,
+                       converged=conv.astype(bool), wall_time=rep_c.wall_time,
+                       matvec_count=rep_c.matvec_count)
+
+
+def block_cg(op: DiscreteOperator, b, cfg: SolverConfig, out=None) -> BlockCgResult:
+    """block_cg(op, B, cfg) (solvers.cpp:452-665) on the device."""
+    cfg_c = cfg._c()
+    if len(b.shape) != 2:
+        raise DimensionMismatchError("block_cg: B must be n x s")
+    if int(b.shape[0]) != op.n:
+        raise DimensionMismatchError("block_cg: rhs rows != n")
+    s = int(b.shape[1])
+    pb, kb = _ptr(b)
+    out = np.empty((op.n, s), np.float64) if out is None else out
+    px, kx = _ptr(out)
+    res = np.zeros(max(s, 1), np.float64)
+    conv = np.zeros(max(s, 1), np.int8)
+    rep = _Report(0, 0, 0.0, res.ctypes.data_as(C.c_void_p), conv.ctypes.data_as(C.c_void_p))
+    _raise(_load().bk_block_cg(op.ctx.h, op.h, pb, s, C.byref(cfg_c), px, C.byref(rep)),
+           op.ctx.h, "block_cg")
+    return BlockCgResult(out, _report(s, rep, res[:s], conv[:s]))
+
+
+def combine_action(op: DiscreteOperator, x, coef, t_out=None, q_out=None, resid_out=None,
+                   want=("T", "Q", "resid")):
+    """Fused combine_from_weights + operator_action for N samples.
+
+    x: n x s basis solutions; coef: s x N weights (column j = sample j).
+    Returns (T [N x n], Q [N x n], resid [N]).
+    """
+    s = _cols(x)
+    if int(x.shape[0]) != op.n:
+        raise DimensionMismatchError("operator_action: vector length != n")
+    if int(coef.shape[0]) != s:
+        raise DimensionMismatchError("combine: weight count != basis size")
+    N = int(coef.shape[1])
+    if t_out is None and "T" in want:
+        t_out = np.empty((N, op.n), np.float64)
+    if q_out is None and "Q" in want:
+        q_out = np.empty((N, op.n), np.float64)
+    if resid_out is None and "resid" in want:
+        resid_out = np.empty(N, np.float64)
+    px, kx = _ptr(x)
+    pc, kc = _ptr(coef)
+    pt, kt = _ptr(t_out)
+    pq, kq = _ptr(q_out)
+    pr, kr = _ptr(resid_out)
+    _raise(_load().bk_combine_action(op.ctx.h, op.h, px, s, pc, N, pt, pq, pr), op.ctx.h,
+           "combine_action")
+    return t_out, q_out, resid_out
+
+
+def generate_chip(grid: GridSpec, k, bc: BoundarySpec, q_basis, coef, cfg: SolverConfig,
+                  t_out=None, q_out=None, resid_out=None, ctx: Optional[Context] = None,
+                  check_converged: bool = True):
+    """Whole per-chip pipeline: assemble -> B = V q + g -> block CG -> fused
+    combine + operator action. Returns (T, Q, resid, SolveReport, PhaseTimings)."""
+    ctx = _ctx(ctx)
+    n = grid.cell_count()
+    s = _cols(q_basis)
+    N = int(coef.shape[1])
+    if int(coef.shape[0]) != s:
+        raise DimensionMismatchError("combine: weight count != basis size")
+    if _numel(k) != n or int(q_basis.shape[0]) != n:
+        raise DimensionMismatchError("generate: field length does not match grid")
+    g, keep = grid._c()
+    faces = bc._c()
+    cfg_c = cfg._c()
+    t_out = np.empty((N, n), np.float64) if t_out is None else t_out
+    q_out = np.empty((N, n), np.float64) if q_out is None else q_out
+    resid_out = np.empty(N, np.float64) if resid_out is None else resid_out
+    ptrs = [_ptr(a) for a in (k, q_basis, coef, t_out, q_out, resid_out)]
+    res = np.zeros(s, np.float64)
+    conv = np.zeros(s, np.int8)
+    rep = _Report(0, 0, 0.0, res.ctypes.data_as(C.c_void_p), conv.ctypes.data_as(C.c_void_p))
+    tim = _Timings()
+    st = _load().bk_generate_chip(ctx.h, C.byref(g), ptrs[0][0], faces, ptrs[1][0], s, ptrs[2][0],
+                                  N, C.byref(cfg_c), ptrs[3][0], ptrs[4][0], ptrs[5][0],
+                                  C.byref(rep), C.byref(tim))
+    if st == 7 and not check_converged:
+        st = 0
+    _raise(st, ctx.h, "generate_chip")
+    timings = PhaseTimings(tim.assemble_s, tim.basis_solve_s, tim.combine_action_s, tim.h2d_s,
+                           tim.d2h_s, tim.total_s, tim.iterations_total, tim.matvecs_total)
+    return t_out, q_out, resid_out, _report(s, rep, res, conv), timings
+
+
+def cg_error_bound(kappa: float, m: int, e0: float) -> float:
+    out = C.c_double(0)
+    _raise(_load().bk_cg_error_bound(kappa, m, e0, C.byref(out)), None, "cg_error_bound")
+    return out.value
+
+
+def derive_seed(seed: int, tag: str, index: int = 0) -> int:
+    return int(_load().bk_derive_seed(seed, tag.encode(), index))
+
+
+def rng_u64(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.uint64)
+    _load().bk_rng_u64(seed, n, out.ctypes.data_as(C.c_void_p))
+    return out
+
+
+def rng_uniform(seed: int, lo: float, hi: float, n: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    _load().bk_rng_uniform(seed, lo, hi, n, out.ctypes.data_as(C.c_void_p))
+    return out
+
+
+def rng_normal(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    _load().bk_rng_normal(seed, n, out.ctypes.data_as(C.c_void_p))
+    return out
+
+
+@dataclass
+class ChipInputs:
+    grid: GridSpec
+    bc: BoundarySpec
+    k: np.ndarray        # n
+    q_basis: np.ndarray  # n x s
+    coef: np.ndarray     # s x N
+
+
+def synth_chip(config: int, nx: int, ny: int, nz: int, s: int, N: int, master_seed: int = 1,
+               chip_id: int = 0) -> ChipInputs:
+    """Seeded synthetic inputs of BASELINE config 1..5."""
+    lib = _load()
+    sp = _Synth(config, nx, ny, nz, s, N, master_seed, chip_id)
+    g = _Grid()
+    dz = np.zeros(nz, np.float64)
+    has_dz = C.c_int(0)
+    faces = (_Face * 6)()
+    n = nx * ny * nz
+    k = np.empty(n, np.float64)
+    q = np.empty((n, s), np.float64)
+    c = np.empty((s, N), np.float64)
+    st = lib.bk_synth_chip(C.byref(sp), C.byref(g), dz.ctypes.data_as(C.c_void_p),
+                           C.byref(has_dz), faces, k.ctypes.data_as(C.c_void_p),
+                           q.ctypes.data_as(C.c_void_p), c.ctypes.data_as(C.c_void_p))
+    _raise(st, None, "synth_chip")
+    grid = GridSpec(g.nx, g.ny, g.nz, g.lx, g.ly, g.lz, dz.copy() if has_dz.value else None)
+    fl = []
+    for f in faces:
+        fl.append(Dirichlet(f.a) if f.kind == 0 else Robin(f.a, f.b) if f.kind == 1 else Adiabatic())
+    return ChipInputs(grid, BoundarySpec(fl), k, q, c)
+
+
+# BASELINE.json configs (shapes): (config id, nx, ny, nz, s, N)
+CONFIGS = {
+    1: (1, 64, 64, 1, 8, 256),
+    2: (2, 256, 256, 1, 16, 2048),
+    3: (3, 128, 128, 8, 32, 5000),
+    4: (4, 128, 128, 4, 16, 8),      # per chip; 5000 chips
+    5: (5, 512, 512, 16, 64, 5000),
+}
+C4_CHIPS = 5000

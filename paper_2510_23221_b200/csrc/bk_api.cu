@@ -1,0 +1,525 @@
+// The C ABI (include/blockoa_b200.h): argument validation with the reference's
+// error semantics, host/device pointer staging, and the per-chip pipeline.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "bk_common.cuh"
+
+namespace bk {
+
+bk_status fail(bk_ctx* ctx, bk_status st, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return st;
+}
+
+bk_status workspace(bk_ctx* ctx, int slot, size_t bytes, void** out) {
+    if (bytes == 0) bytes = 8;
+    if (ctx->ws_bytes[slot] < bytes) {
+        if (ctx->ws[slot]) {
+            cudaStreamSynchronize(ctx->stream);
+            cudaFree(ctx->ws[slot]);
+            ctx->ws[slot] = nullptr;
+            ctx->ws_bytes[slot] = 0;
+        }
+        const size_t rounded = (bytes + (1u << 20) - 1) & ~size_t((1u << 20) - 1);
+        cudaError_t e = cudaMalloc(&ctx->ws[slot], rounded);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, BK_OOM, std::string("workspace cudaMalloc: ") + cudaGetErrorString(e));
+        }
+        ctx->ws_bytes[slot] = rounded;
+    }
+    *out = ctx->ws[slot];
+    return BK_OK;
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace bk
+
+namespace {
+
+using namespace bk;
+
+// A device view of a caller buffer: either the caller's device pointer or a
+// workspace slot filled from / drained to host memory.
+struct Staged {
+    double* dev = nullptr;
+    bool host = false;
+};
+
+bk_status stage_in(bk_ctx* ctx, int slot, const double* p, size_t count, Staged* out) {
+    if (is_device_ptr(p)) {
+        out->dev = const_cast<double*>(p);
+        out->host = false;
+        return BK_OK;
+    }
+    void* d;
+    bk_status st = workspace(ctx, slot, count * sizeof(double), &d);
+    if (st != BK_OK) return st;
+    if (count)
+        BK_CUDA_TRY(ctx, cudaMemcpyAsync(d, p, count * sizeof(double), cudaMemcpyHostToDevice,
+                                         ctx->stream));
+    out->dev = (double*)d;
+    out->host = true;
+    return BK_OK;
+}
+
+bk_status stage_out(bk_ctx* ctx, int slot, double* p, size_t count, Staged* out) {
+    if (!p) {
+        out->dev = nullptr;
+        out->host = false;
+        return BK_OK;
+    }
+    if (is_device_ptr(p)) {
+        out->dev = p;
+        out->host = false;
+        return BK_OK;
+    }
+    void* d;
+    bk_status st = workspace(ctx, slot, count * sizeof(double), &d);
+    if (st != BK_OK) return st;
+    out->dev = (double*)d;
+    out->host = true;
+    return BK_OK;
+}
+
+bk_status drain(bk_ctx* ctx, const Staged& s, double* host, size_t count) {
+    if (s.host && count)
+        BK_CUDA_TRY(ctx, cudaMemcpyAsync(host, s.dev, count * sizeof(double),
+                                         cudaMemcpyDeviceToHost, ctx->stream));
+    return BK_OK;
+}
+
+int kernel_width(int s) { return s <= 8 ? 8 : s <= 16 ? 16 : s <= 32 ? 32 : 64; }
+
+bk_status validate_grid(bk_ctx* ctx, const bk_grid* g) {
+    if (!g) return fail(ctx, BK_INVALID_SPEC, "grid: null");
+    if (g->nx < 1 || g->ny < 1 || g->nz < 1)
+        return fail(ctx, BK_INVALID_SPEC, "grid: cell counts must be >= 1");
+    if (!(g->lx > 0.0) || !(g->ly > 0.0) || !(g->lz > 0.0))
+        return fail(ctx, BK_INVALID_SPEC, "grid: extents must be positive");
+    if (g->dz)
+        for (int z = 0; z < g->nz; ++z)
+            if (!(g->dz[z] > 0.0))
+                return fail(ctx, BK_INVALID_SPEC, "grid: layer thicknesses must be positive");
+    return BK_OK;
+}
+
+bk_status validate_cfg(bk_ctx* ctx, const bk_solver_cfg* c) {
+    if (!c) return fail(ctx, BK_INVALID_CONFIG, "solver: null config");
+    if (!(c->rel_tol > 0.0) || !(c->rel_tol < 1.0))
+        return fail(ctx, BK_INVALID_CONFIG, "solver: rel_tol must be in (0, 1)");
+    if (c->max_iter < 1) return fail(ctx, BK_INVALID_CONFIG, "solver: max_iter must be >= 1");
+    return BK_OK;
+}
+
+void free_op_buffers(bk_operator* op) {
+    cudaFree(op->diag);
+    cudaFree(op->cx);
+    cudaFree(op->cy);
+    cudaFree(op->cz);
+    cudaFree(op->g);
+    cudaFree(op->dinv);
+    cudaFree(op->volz);
+    op->diag = op->cx = op->cy = op->cz = op->g = op->dinv = op->volz = nullptr;
+}
+
+// Assemble into `op` (buffers reused when the cell count matches).
+bk_status assemble_into(bk_ctx* ctx, const bk_grid* grid, const double* k, const bk_face bc[6],
+                        bk_operator* op) {
+    bk_status st = validate_grid(ctx, grid);
+    if (st != BK_OK) return st;
+    for (int f = 0; f < 6; ++f) {
+        if (bc[f].kind < 0 || bc[f].kind > 2)
+            return fail(ctx, BK_INVALID_SPEC, "boundary: unknown face kind");
+        if (bc[f].kind == BK_FACE_ROBIN && !(bc[f].a > 0.0))
+            return fail(ctx, BK_NONPOSITIVE_HTC, "boundary: Robin h must be > 0");
+    }
+    const int64_t n = (int64_t)grid->nx * grid->ny * grid->nz;
+    if (n > 2147483647LL)
+        return fail(ctx, BK_INVALID_SPEC, "assemble: grid too large for 32-bit column indices");
+    if (!k) return fail(ctx, BK_DIMENSION_MISMATCH, "assemble: null conductivity");
+
+    Staged kd;
+    if ((st = stage_in(ctx, kSlotK, k, (size_t)n, &kd)) != BK_OK) return st;
+    // k > 0 everywhere (discretize.cpp:121-123)
+    void* flagp;
+    if ((st = workspace(ctx, kSlotRes, sizeof(int), &flagp)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, cudaMemsetAsync(flagp, 0, sizeof(int), ctx->stream));
+    BK_CUDA_TRY(ctx, launch_check_positive(ctx, kd.dev, n, (int*)flagp));
+
+    if (op->n != n || !op->diag) {
+        free_op_buffers(op);
+        const size_t nb = (size_t)n * sizeof(double);
+        BK_CUDA_TRY(ctx, cudaMalloc(&op->diag, nb));
+        BK_CUDA_TRY(ctx, cudaMalloc(&op->cx, nb));
+        BK_CUDA_TRY(ctx, cudaMalloc(&op->cy, nb));
+        BK_CUDA_TRY(ctx, cudaMalloc(&op->cz, nb));
+        BK_CUDA_TRY(ctx, cudaMalloc(&op->g, nb));
+        BK_CUDA_TRY(ctx, cudaMalloc(&op->dinv, nb));
+    }
+    cudaFree(op->volz);
+    op->volz = nullptr;
+    BK_CUDA_TRY(ctx, cudaMalloc(&op->volz, (size_t)grid->nz * 2 * sizeof(double)));
+    op->device = ctx->device;
+    op->nx = grid->nx;
+    op->ny = grid->ny;
+    op->nz = grid->nz;
+    op->n = n;
+
+    // geometry exactly as GridSpec: dx = lx/nx, dy = ly/ny, dz = lz/nz and
+    // cell_volume = dx*dy*dz (grid.hpp:25-28)
+    const double dx = grid->lx / grid->nx, dy = grid->ly / grid->ny;
+    std::vector<double> dzv(grid->nz);
+    op->h_volz.assign(grid->nz, 0.0);
+    for (int z = 0; z < grid->nz; ++z) {
+        dzv[z] = grid->dz ? grid->dz[z] : grid->lz / grid->nz;
+        op->h_volz[z] = dx * dy * dzv[z];
+    }
+    // [volz | dz] in one small upload
+    std::vector<double> up(op->h_volz);
+    up.insert(up.end(), dzv.begin(), dzv.end());
+    BK_CUDA_TRY(ctx, cudaMemcpyAsync(op->volz, up.data(), up.size() * sizeof(double),
+                                     cudaMemcpyHostToDevice, ctx->stream));
+    BK_CUDA_TRY(ctx, launch_assemble(ctx, op, kd.dev, bc, dx, dy, op->volz + grid->nz));
+    int flag = 0;
+    BK_CUDA_TRY(ctx, cudaMemcpyAsync(&flag, flagp, sizeof(int), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (flag) return fail(ctx, BK_NONPOSITIVE_K, "assemble: k must be > 0 everywhere");
+    return BK_OK;
+}
+
+void fill_report(const CgReport& r, int s, double wall, bk_solve_report* out) {
+    if (!out) return;
+    out->iterations = r.iterations;
+    out->matvec_count = r.matvecs;
+    out->wall_time = wall;
+    for (int j = 0; j < s; ++j) {
+        if (out->final_rel_residual) out->final_rel_residual[j] = r.final_res[j];
+        if (out->converged) out->converged[j] = r.converged[j];
+    }
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bk_abi_version(void) { return BK_ABI_VERSION; }
+
+bk_status bk_create(int device, bk_ctx** out) {
+    if (!out) return BK_INVALID_CONFIG;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return BK_NO_DEVICE;
+    }
+    if (device < 0 || device >= count) return BK_NO_DEVICE;
+    if (cudaSetDevice(device) != cudaSuccess) return BK_CUDA_ERROR;
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    if (major < 10) return BK_NO_DEVICE;  // built for sm_100a only
+    bk_ctx* ctx = new (std::nothrow) bk_ctx;
+    if (!ctx) return BK_OOM;
+    ctx->device = device;
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return BK_CUDA_ERROR;
+    }
+    ctx->stream = ctx->own_stream;
+    for (auto& e : ctx->ev) cudaEventCreate(&e);
+    *out = ctx;
+    return BK_OK;
+}
+
+void bk_destroy(bk_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (int i = 0; i < bk_ctx::kSlots; ++i) cudaFree(ctx->ws[i]);
+    for (auto& e : ctx->ev) cudaEventDestroy(e);
+    if (ctx->scratch) {
+        free_op_buffers(ctx->scratch);
+        delete ctx->scratch;
+    }
+    cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+const char* bk_last_error(const bk_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+bk_status bk_set_stream(bk_ctx* ctx, void* s) {
+    if (!ctx) return BK_INVALID_CONFIG;
+    ctx->stream = s ? (cudaStream_t)s : ctx->own_stream;
+    return BK_OK;
+}
+
+bk_status bk_synchronize(bk_ctx* ctx) {
+    if (!ctx) return BK_INVALID_CONFIG;
+    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return BK_OK;
+}
+
+int64_t bk_launch_count(const bk_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+bk_status bk_assemble(bk_ctx* ctx, const bk_grid* grid, const double* k, const bk_face bc[6],
+                      bk_operator** out) {
+    if (!ctx || !out || !bc) return BK_INVALID_CONFIG;
+    cudaSetDevice(ctx->device);
+    bk_operator* op = new (std::nothrow) bk_operator;
+    if (!op) return fail(ctx, BK_OOM, "assemble: host allocation");
+    bk_status st = assemble_into(ctx, grid, k, bc, op);
+    if (st != BK_OK) {
+        free_op_buffers(op);
+        delete op;
+        return st;
+    }
+    *out = op;
+    return BK_OK;
+}
+
+void bk_operator_free(bk_operator* op) {
+    if (!op) return;
+    cudaSetDevice(op->device);
+    free_op_buffers(op);
+    delete op;
+}
+
+int64_t bk_operator_n(const bk_operator* op) { return op ? op->n : 0; }
+
+bk_status bk_operator_export_csr(bk_ctx* ctx, const bk_operator* op, int64_t* row_ptr,
+                                 int32_t* col, double* val, int64_t* nnz, double* g,
+                                 double* vol) {
+    if (!ctx || !op || !row_ptr || !nnz) return BK_INVALID_CONFIG;
+    cudaSetDevice(ctx->device);
+    const int64_t n = op->n;
+    std::vector<double> d(n), cx(n), cy(n), cz(n), gg(n);
+    BK_CUDA_TRY(ctx, cudaMemcpy(d.data(), op->diag, n * 8, cudaMemcpyDeviceToHost));
+    BK_CUDA_TRY(ctx, cudaMemcpy(cx.data(), op->cx, n * 8, cudaMemcpyDeviceToHost));
+    BK_CUDA_TRY(ctx, cudaMemcpy(cy.data(), op->cy, n * 8, cudaMemcpyDeviceToHost));
+    BK_CUDA_TRY(ctx, cudaMemcpy(cz.data(), op->cz, n * 8, cudaMemcpyDeviceToHost));
+    BK_CUDA_TRY(ctx, cudaMemcpy(gg.data(), op->g, n * 8, cudaMemcpyDeviceToHost));
+    const int nx = op->nx, ny = op->ny, nz = op->nz;
+    const int64_t plane = (int64_t)nx * ny;
+    int64_t p = 0;
+    row_ptr[0] = 0;
+    // push order z-, y-, x-, diag, x+, y+, z+ skipping zero off-diagonals
+    // (discretize.cpp:218-231); pure copies / negations of the stencil.
+    auto push = [&](int64_t c, double v) {
+        if (col) col[p] = (int32_t)c;
+        if (val) val[p] = v;
+        ++p;
+    };
+    for (int64_t i = 0; i < n; ++i) {
+        const int ix = (int)(i % nx), iy = (int)((i / nx) % ny), iz = (int)(i / plane);
+        if (iz > 0 && cz[i - plane] != 0.0) push(i - plane, -cz[i - plane]);
+        if (iy > 0 && cy[i - nx] != 0.0) push(i - nx, -cy[i - nx]);
+        if (ix > 0 && cx[i - 1] != 0.0) push(i - 1, -cx[i - 1]);
+        push(i, d[i]);
+        if (ix < nx - 1 && cx[i] != 0.0) push(i + 1, -cx[i]);
+        if (iy < ny - 1 && cy[i] != 0.0) push(i + nx, -cy[i]);
+        if (iz < nz - 1 && cz[i] != 0.0) push(i + plane, -cz[i]);
+        row_ptr[i + 1] = p;
+        if (g) g[i] = gg[i];
+        if (vol) vol[i] = op->h_volz[iz];
+    }
+    *nnz = p;
+    return BK_OK;
+}
+
+bk_status bk_apply_block(bk_ctx* ctx, const bk_operator* op, const double* X, int s, double* Y) {
+    if (!ctx || !op) return BK_INVALID_CONFIG;
+    if (s < 1) return fail(ctx, BK_DIMENSION_MISMATCH, "apply_block: s must be >= 1");
+    cudaSetDevice(ctx->device);
+    const size_t cnt = (size_t)op->n * s;
+    Staged xd, yd;
+    bk_status st;
+    if ((st = stage_in(ctx, kSlotIn0, X, cnt, &xd)) != BK_OK) return st;
+    if ((st = stage_out(ctx, kSlotOut0, Y, cnt, &yd)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, launch_apply_block(ctx, op, xd.dev, s, yd.dev));
+    if ((st = drain(ctx, yd, Y, cnt)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return BK_OK;
+}
+
+bk_status bk_rhs_from_power(bk_ctx* ctx, const bk_operator* op, const double* Q, int s,
+                            double* B) {
+    if (!ctx || !op) return BK_INVALID_CONFIG;
+    if (s < 1) return fail(ctx, BK_DIMENSION_MISMATCH, "rhs_from_power: s must be >= 1");
+    cudaSetDevice(ctx->device);
+    const size_t cnt = (size_t)op->n * s;
+    Staged qd, bd;
+    bk_status st;
+    if ((st = stage_in(ctx, kSlotIn0, Q, cnt, &qd)) != BK_OK) return st;
+    if ((st = stage_out(ctx, kSlotOut0, B, cnt, &bd)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, launch_rhs_from_power(ctx, op, qd.dev, s, bd.dev));
+    if ((st = drain(ctx, bd, B, cnt)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return BK_OK;
+}
+
+bk_status bk_power_from_rhs(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
+                            double* Q) {
+    if (!ctx || !op) return BK_INVALID_CONFIG;
+    if (s < 1) return fail(ctx, BK_DIMENSION_MISMATCH, "power_from_rhs: s must be >= 1");
+    cudaSetDevice(ctx->device);
+    const size_t cnt = (size_t)op->n * s;
+    Staged bd, qd;
+    bk_status st;
+    if ((st = stage_in(ctx, kSlotIn0, B, cnt, &bd)) != BK_OK) return st;
+    if ((st = stage_out(ctx, kSlotOut0, Q, cnt, &qd)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, launch_power_from_rhs(ctx, op, bd.dev, s, qd.dev));
+    if ((st = drain(ctx, qd, Q, cnt)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return BK_OK;
+}
+
+bk_status bk_block_cg(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
+                      const bk_solver_cfg* cfg, double* X, bk_solve_report* report) {
+    if (!ctx || !op) return BK_INVALID_CONFIG;
+    bk_status st = validate_cfg(ctx, cfg);
+    if (st != BK_OK) return st;
+    if (s < 1) return fail(ctx, BK_DIMENSION_MISMATCH, "block_cg: need at least one column");
+    if (s > 64) return fail(ctx, BK_INVALID_CONFIG, "block_cg: s > 64 not supported");
+    cudaSetDevice(ctx->device);
+    const size_t cnt = (size_t)op->n * s;
+    Staged bd, xd;
+    if ((st = stage_in(ctx, kSlotIn0, B, cnt, &bd)) != BK_OK) return st;
+    if ((st = stage_out(ctx, kSlotOut0, X, cnt, &xd)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], ctx->stream));
+    CgReport rep;
+    if ((st = block_cg_device(ctx, op, bd.dev, s, cfg, xd.dev, &rep)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], ctx->stream));
+    if ((st = drain(ctx, xd, X, cnt)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    fill_report(rep, s, elapsed(ctx->ev[0], ctx->ev[1]) * 1e-3, report);
+    return BK_OK;
+}
+
+bk_status bk_combine_action(bk_ctx* ctx, const bk_operator* op, const double* X, int s,
+                            const double* C, int64_t N, double* T, double* Q, double* resid) {
+    if (!ctx || !op) return BK_INVALID_CONFIG;
+    if (s < 1) return fail(ctx, BK_EMPTY_BASIS, "combine: empty basis");
+    if (s > 64) return fail(ctx, BK_INVALID_CONFIG, "combine: s > 64 not supported");
+    if (N < 0) return fail(ctx, BK_DIMENSION_MISMATCH, "combine: negative sample count");
+    cudaSetDevice(ctx->device);
+    if (N == 0) return BK_OK;
+    const int S = kernel_width(s);
+    const size_t xn = (size_t)op->n * s, out_n = (size_t)op->n * N;
+    Staged xd, cd, td, qd, rd;
+    bk_status st;
+    if ((st = stage_in(ctx, kSlotIn0, X, xn, &xd)) != BK_OK) return st;
+    if ((st = stage_in(ctx, kSlotIn1, C, (size_t)s * N, &cd)) != BK_OK) return st;
+    if ((st = stage_out(ctx, kSlotOut0, T, out_n, &td)) != BK_OK) return st;
+    if ((st = stage_out(ctx, kSlotOut1, Q, out_n, &qd)) != BK_OK) return st;
+    if ((st = stage_out(ctx, kSlotOut2, resid, (size_t)N, &rd)) != BK_OK) return st;
+    const double* xk = xd.dev;
+    if (S != s) {
+        void* p;
+        if ((st = workspace(ctx, kSlotCgX, (size_t)op->n * S * 8, &p)) != BK_OK) return st;
+        BK_CUDA_TRY(ctx, launch_pad_cols(ctx, xd.dev, s, (double*)p, S, op->n));
+        xk = (const double*)p;
+    }
+    // the kernel reads C rows [0, s) with row stride N
+    if ((st = combine_action_device(ctx, op, xk, S, cd.dev, N, td.dev, qd.dev, rd.dev)) != BK_OK)
+        return st;
+    if ((st = drain(ctx, td, T, out_n)) != BK_OK) return st;
+    if ((st = drain(ctx, qd, Q, out_n)) != BK_OK) return st;
+    if ((st = drain(ctx, rd, resid, (size_t)N)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return BK_OK;
+}
+
+bk_status bk_generate_chip(bk_ctx* ctx, const bk_grid* grid, const double* k, const bk_face bc[6],
+                           const double* Qbasis, int s, const double* C, int64_t N,
+                           const bk_solver_cfg* cfg, double* T, double* Q, double* resid,
+                           bk_solve_report* report, bk_phase_timings* timings) {
+    if (!ctx || !bc) return BK_INVALID_CONFIG;
+    bk_status st = validate_cfg(ctx, cfg);
+    if (st != BK_OK) return st;
+    if (s < 1) return fail(ctx, BK_EMPTY_BASIS, "generate: empty basis");
+    if (s > 64) return fail(ctx, BK_INVALID_CONFIG, "generate: s > 64 not supported");
+    if (N < 0) return fail(ctx, BK_INVALID_CONFIG, "generate: n_data must be >= 0");
+    if ((st = validate_grid(ctx, grid)) != BK_OK) return st;
+    cudaSetDevice(ctx->device);
+    const int64_t n = (int64_t)grid->nx * grid->ny * grid->nz;
+    const int S = kernel_width(s);
+    cudaEvent_t* ev = ctx->ev;
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[0], ctx->stream));
+    Staged qd, cd;
+    if ((st = stage_in(ctx, kSlotQ, Qbasis, (size_t)n * s, &qd)) != BK_OK) return st;
+    if ((st = stage_in(ctx, kSlotC, C, (size_t)s * N, &cd)) != BK_OK) return st;
+    // k is staged inside assemble
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[1], ctx->stream));
+
+    if (!ctx->scratch) ctx->scratch = new bk_operator;
+    bk_operator* scratch = ctx->scratch;
+    if ((st = assemble_into(ctx, grid, k, bc, scratch)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[2], ctx->stream));
+
+    void *pb, *px;
+    if ((st = workspace(ctx, kSlotIn2, (size_t)n * S * 8, &pb)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotOut2, (size_t)n * S * 8, &px)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, launch_rhs_padded(ctx, scratch, qd.dev, s, (double*)pb, S));
+    CgReport rep;
+    if ((st = block_cg_device(ctx, scratch, (const double*)pb, S, cfg, (double*)px, &rep)) != BK_OK)
+        return st;
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[3], ctx->stream));
+
+    Staged td, qo, rd;
+    const size_t out_n = (size_t)n * N;
+    if ((st = stage_out(ctx, kSlotT, T, out_n, &td)) != BK_OK) return st;
+    if ((st = stage_out(ctx, kSlotQo, Q, out_n, &qo)) != BK_OK) return st;
+    if ((st = stage_out(ctx, kSlotRes, resid, (size_t)N, &rd)) != BK_OK) return st;
+    if ((st = combine_action_device(ctx, scratch, (const double*)px, S, cd.dev, N, td.dev, qo.dev,
+                                    rd.dev)) != BK_OK)
+        return st;
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[4], ctx->stream));
+    if ((st = drain(ctx, td, T, out_n)) != BK_OK) return st;
+    if ((st = drain(ctx, qo, Q, out_n)) != BK_OK) return st;
+    if ((st = drain(ctx, rd, resid, (size_t)N)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[5], ctx->stream));
+    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+
+    const double solve_s = elapsed(ev[2], ev[3]) * 1e-3;
+    fill_report(rep, s, solve_s, report);
+    if (timings) {
+        timings->h2d_s = elapsed(ev[0], ev[1]) * 1e-3;
+        timings->assemble_s = elapsed(ev[1], ev[2]) * 1e-3;
+        timings->basis_solve_s = solve_s;
+        timings->combine_action_s = elapsed(ev[3], ev[4]) * 1e-3;
+        timings->d2h_s = elapsed(ev[4], ev[5]) * 1e-3;
+        timings->total_s = elapsed(ev[0], ev[5]) * 1e-3;
+        timings->iterations_total = rep.iterations;
+        timings->matvecs_total = rep.matvecs + N;
+    }
+    for (int j = 0; j < s; ++j)
+        if (!rep.converged[j])
+            return fail(ctx, BK_NOT_CONVERGED, "basis solve did not reach tolerance");
+    return BK_OK;
+}
+
+}  // extern "C"

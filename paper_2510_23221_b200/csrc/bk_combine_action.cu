@@ -1,0 +1,271 @@
+// Fused combination + operator action: one pass writes every (T, q) sample.
+//
+//   T_j = sum_t C[t][j] X[:,t]        combine_from_weights  pipeline.cpp:187-225
+//   q_j = (A T_j - g) / V             operator_action       pipeline.cpp:242-251
+//   resid_j = ||A T_j - (V q_j + g)|| / ||V q_j + g||       pipeline.cpp:548-571
+//
+// Each CTA owns a 32 x 8 x-y tile of cells (all z, marched plane by plane,
+// 2.5D blocking) and a chunk of NS samples. A plane of T for the tile plus a
+// one-cell x-y halo is formed in shared memory straight from X (L2-resident,
+// n x s) and the coefficients; the stencil is then applied to the smem tile and
+// T and q leave the SM exactly once, sample-major. A ring of three planes
+// supplies the z-1 / z+1 neighbours. No T round trip through HBM, no second
+// pass for q.
+//
+// Bitwise contract: T uses the reference's per-element order (first term a
+// product, then one fma per basis column in ascending order); A T uses the
+// scalar CsrMatrix::apply order (separate multiply and add, CSR column order);
+// q = (y - g) / V is correctly rounded. So given the same X, T and q equal the
+// reference's bit for bit (tests/test_gpu_parity.py checks it).
+#include "bk_common.cuh"
+
+namespace {
+
+constexpr int TX = 32, TY = 8, HX = TX + 2, HY = TY + 2, HC = HX * HY;
+constexpr int NT = 256;  // = TX * TY: one interior cell per thread in the stencil phase
+
+struct ActArgs {
+    int nx, ny, nz;
+    int64_t n;
+    int64_t N;
+    const double* diag;
+    const double* cx;
+    const double* cy;
+    const double* cz;
+    const double* g;
+    const double* volz;
+    const double* X;  // n x S
+    const double* C;  // S x N
+    double* T;        // N x n (nullable)
+    double* Q;        // N x n (nullable)
+    double* part;     // tiles x N x 2 residual partials (nullable)
+    int s;            // real basis width (<= S)
+};
+
+// correctly rounded x / v given r = RN(1/v) (one Newton-style correction).
+__device__ __forceinline__ double div_rn(double x, double v, double r) {
+    const double q0 = x * r;
+    const double e = fma(-q0, v, x);
+    return fma(e, r, q0);
+}
+
+template <int S, int NS>
+__device__ __forceinline__ void form_plane(const ActArgs& a, int x0, int y0, int z,
+                                           const double* __restrict__ Cs, double* __restrict__ buf) {
+    constexpr int H = NS / 2;
+    const int64_t plane = (int64_t)a.nx * a.ny;
+    for (int it = threadIdx.x; it < HC * 2; it += NT) {
+        const int h = it >> 1, half = it & 1;
+        const int gx = x0 - 1 + h % HX, gy = y0 - 1 + h / HX;
+        double t[H];
+        if (gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny) {
+            const double* xr = a.X + (gx + (int64_t)a.nx * gy + plane * z) * S;
+            const double* cs = Cs + half * H;
+            const double x0v = xr[0];
+#pragma unroll
+            for (int q = 0; q < H; ++q) t[q] = x0v * cs[q];
+#pragma unroll 4
+            for (int k = 1; k < S; ++k) {
+                const double xv = xr[k];
+#pragma unroll
+                for (int q = 0; q < H; ++q) t[q] = fma(cs[k * NS + q], xv, t[q]);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < H; ++q) t[q] = 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < H; ++q) buf[h * NS + half * H + q] = t[q];
+    }
+}
+
+template <int S, int NS>
+__global__ void __launch_bounds__(NT) combine_action_kernel(ActArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    double* Cs = sm;                 // S x NS
+    double* ring = sm + S * NS;      // 3 x HC x NS
+    const int tilesx = (a.nx + TX - 1) / TX;
+    const int tile = blockIdx.x;
+    const int x0 = (tile % tilesx) * TX, y0 = (tile / tilesx) * TY;
+    const int64_t j0 = (int64_t)blockIdx.y * NS;
+    const int tid = threadIdx.x;
+    const int64_t plane = (int64_t)a.nx * a.ny;
+
+    for (int e = tid; e < S * NS; e += NT) {
+        const int k = e / NS, q = e % NS;
+        Cs[e] = (k < a.s && j0 + q < a.N) ? a.C[(int64_t)k * a.N + j0 + q] : 0.0;
+    }
+    __syncthreads();
+
+    const int lx = tid % TX, ly = tid / TX;
+    const int gx = x0 + lx, gy = y0 + ly;
+    const bool inside = gx < a.nx && gy < a.ny;
+    const int h = (ly + 1) * HX + (lx + 1);
+    double num[NS], den[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) num[q] = den[q] = 0.0;
+
+    form_plane<S, NS>(a, x0, y0, 0, Cs, ring);
+    if (a.nz > 1) form_plane<S, NS>(a, x0, y0, 1, Cs, ring + HC * NS);
+    __syncthreads();
+    for (int z = 0; z < a.nz; ++z) {
+        const double* Tm = ring + ((z + 2) % 3) * HC * NS;
+        const double* T0 = ring + (z % 3) * HC * NS;
+        const double* Tp = ring + ((z + 1) % 3) * HC * NS;
+        if (inside) {
+            const int64_t i = gx + (int64_t)a.nx * gy + plane * z;
+            const double vol = a.volz[z];
+            const double rvol = 1.0 / vol;
+            const double gi = a.g[i], di = a.diag[i];
+            const double czm = z > 0 ? -a.cz[i - plane] : 0.0;
+            const double cym = gy > 0 ? -a.cy[i - a.nx] : 0.0;
+            const double cxm = gx > 0 ? -a.cx[i - 1] : 0.0;
+            const double cxp = gx < a.nx - 1 ? -a.cx[i] : 0.0;
+            const double cyp = gy < a.ny - 1 ? -a.cy[i] : 0.0;
+            const double czp = z < a.nz - 1 ? -a.cz[i] : 0.0;
+#pragma unroll
+            for (int q = 0; q < NS; ++q) {
+                const int64_t j = j0 + q;
+                // y = A T in CSR order z-, y-, x-, diag, x+, y+, z+ (mul, add)
+                double y = 0.0;
+                if (z > 0) y = __dadd_rn(y, __dmul_rn(czm, Tm[h * NS + q]));
+                if (gy > 0) y = __dadd_rn(y, __dmul_rn(cym, T0[(h - HX) * NS + q]));
+                if (gx > 0) y = __dadd_rn(y, __dmul_rn(cxm, T0[(h - 1) * NS + q]));
+                const double tc = T0[h * NS + q];
+                y = __dadd_rn(y, __dmul_rn(di, tc));
+                if (gx < a.nx - 1) y = __dadd_rn(y, __dmul_rn(cxp, T0[(h + 1) * NS + q]));
+                if (gy < a.ny - 1) y = __dadd_rn(y, __dmul_rn(cyp, T0[(h + HX) * NS + q]));
+                if (z < a.nz - 1) y = __dadd_rn(y, __dmul_rn(czp, Tp[h * NS + q]));
+                const double qv = div_rn(__dsub_rn(y, gi), vol, rvol);
+                if (j < a.N) {
+                    if (a.T) __stcs(a.T + j * a.n + i, tc);
+                    if (a.Q) __stcs(a.Q + j * a.n + i, qv);
+                    const double bv = fma(vol, qv, gi);
+                    const double rv = __dsub_rn(y, bv);
+                    num[q] = fma(rv, rv, num[q]);
+                    den[q] = fma(bv, bv, den[q]);
+                }
+            }
+        }
+        __syncthreads();
+        if (z + 2 < a.nz) {
+            form_plane<S, NS>(a, x0, y0, z + 2, Cs, ring + ((z + 2) % 3) * HC * NS);
+            __syncthreads();
+        }
+    }
+
+    if (a.part) {
+        // CTA reduction of the residual partials, fixed order (warp tree, then
+        // warps in index order). Reuses the ring buffer.
+        const int lane = tid & 31, warp = tid >> 5;
+        double* red = ring;  // 8 warps x NS x 2
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            double u = num[q], v = den[q];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                u += __shfl_xor_sync(0xffffffffu, u, o);
+                v += __shfl_xor_sync(0xffffffffu, v, o);
+            }
+            if (lane == 0) {
+                red[(warp * NS + q) * 2] = u;
+                red[(warp * NS + q) * 2 + 1] = v;
+            }
+        }
+        __syncthreads();
+        if (tid < NS && j0 + tid < a.N) {
+            double u = 0.0, v = 0.0;
+            for (int w = 0; w < NT / 32; ++w) {
+                u += red[(w * NS + tid) * 2];
+                v += red[(w * NS + tid) * 2 + 1];
+            }
+            a.part[((int64_t)tile * a.N + j0 + tid) * 2] = u;
+            a.part[((int64_t)tile * a.N + j0 + tid) * 2 + 1] = v;
+        }
+    }
+}
+
+// resid_j = sqrt(num / den) over tiles in order; de == 0 handled as
+// pipeline.cpp:570-571.
+__global__ void resid_finalize(const double* __restrict__ part, int tiles, int64_t N,
+                               double* __restrict__ resid) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        double nu = 0.0, de = 0.0;
+        for (int t = 0; t < tiles; ++t) {
+            nu += part[((int64_t)t * N + j) * 2];
+            de += part[((int64_t)t * N + j) * 2 + 1];
+        }
+        resid[j] = de == 0.0 ? (nu == 0.0 ? 0.0 : 1.0) : sqrt(nu / de);
+    }
+}
+
+template <int S, int NS>
+bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const double* C,
+              int64_t N, double* T, double* Q, double* resid) {
+    using namespace bk;
+    ActArgs a;
+    a.nx = op->nx;
+    a.ny = op->ny;
+    a.nz = op->nz;
+    a.n = op->n;
+    a.N = N;
+    a.diag = op->diag;
+    a.cx = op->cx;
+    a.cy = op->cy;
+    a.cz = op->cz;
+    a.g = op->g;
+    a.volz = op->volz;
+    a.X = X;
+    a.C = C;
+    a.T = T;
+    a.Q = Q;
+    a.s = s;
+    const int tilesx = (op->nx + TX - 1) / TX, tilesy = (op->ny + TY - 1) / TY;
+    const int tiles = tilesx * tilesy;
+    a.part = nullptr;
+    if (resid) {
+        void* p;
+        bk_status st = workspace(ctx, kSlotActPart, (size_t)tiles * N * 2 * sizeof(double), &p);
+        if (st != BK_OK) return st;
+        a.part = (double*)p;
+    }
+    const size_t smem = (size_t)(S * NS + 3 * HC * NS) * sizeof(double);
+    auto kern = combine_action_kernel<S, NS>;
+    BK_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+    const int64_t chunks = (N + NS - 1) / NS;
+    if (chunks > 65535) return fail(ctx, BK_INVALID_CONFIG, "combine_action: N too large per call");
+    kern<<<dim3(tiles, (unsigned)chunks), NT, smem, ctx->stream>>>(a);
+    ++ctx->launches;
+    BK_CUDA_TRY(ctx, cudaGetLastError());
+    if (resid) {
+        resid_finalize<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(a.part, tiles, N,
+                                                                            resid);
+        ++ctx->launches;
+        BK_CUDA_TRY(ctx, cudaGetLastError());
+    }
+    return BK_OK;
+}
+
+}  // namespace
+
+namespace bk {
+
+// X here is the kernel-width block: the caller passes n x s; widths other than
+// 8/16/32/64 are handled with S = next supported width and s = real width
+// (X must then be n x S padded; see bk_api.cu).
+bk_status combine_action_device(bk_ctx* ctx, const bk_operator* op, const double* X, int s,
+                                const double* C, int64_t N, double* T, double* Q,
+                                double* resid) {
+    if (N == 0) return BK_OK;
+    switch (s) {
+        case 8: return run<8, 16>(ctx, op, X, s, C, N, T, Q, resid);
+        case 16: return run<16, 16>(ctx, op, X, s, C, N, T, Q, resid);
+        case 32: return run<32, 16>(ctx, op, X, s, C, N, T, Q, resid);
+        case 64: return run<64, 16>(ctx, op, X, s, C, N, T, Q, resid);
+        default: return fail(ctx, BK_INTERNAL, "combine_action: unpadded width");
+    }
+}
+
+}  // namespace bk

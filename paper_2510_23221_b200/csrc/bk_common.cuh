@@ -1,0 +1,124 @@
+// Internal declarations shared by the libblockoa_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "blockoa_b200.h"
+
+// Every kernel launch goes through BK_LAUNCHED so bk_launch_count() reports the
+// number of this library's launches (bench.py's gpu_launches claim).
+#define BK_CUDA_TRY(ctx, expr)                                                    \
+    do {                                                                          \
+        cudaError_t e_ = (expr);                                                  \
+        if (e_ != cudaSuccess) {                                                  \
+            return bk::fail((ctx), e_ == cudaErrorMemoryAllocation ? BK_OOM       \
+                                                                   : BK_CUDA_ERROR, \
+                            std::string(#expr) + ": " + cudaGetErrorString(e_));  \
+        }                                                                         \
+    } while (0)
+
+struct bk_ctx {
+    int device = 0;
+    int num_sms = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[8] = {};
+    std::string err;
+    int64_t launches = 0;
+    bk_operator* scratch = nullptr;  // operator reused by bk_generate_chip
+    // grow-only device workspace slots
+    static constexpr int kSlots = 24;
+    void* ws[kSlots] = {};
+    size_t ws_bytes[kSlots] = {};
+};
+
+// Matrix-free operator: SoA stencil in HBM. cx/cy/cz hold
+// the conductance of the face towards +x/+y/+z (0 on the domain boundary);
+// the -x/-y/-z conductances are the neighbour's forward faces, bitwise equal
+// to what the reference computes for the row (interior_conductance is
+// commutative, discretize.cpp:99-105).
+struct bk_operator {
+    int device = 0;
+    int nx = 0, ny = 0, nz = 0;
+    int64_t n = 0;
+    double* diag = nullptr;
+    double* cx = nullptr;
+    double* cy = nullptr;
+    double* cz = nullptr;
+    double* g = nullptr;
+    double* dinv = nullptr;  // jacobi_inverse (solvers.cpp:53-66)
+    double* volz = nullptr;  // cell volume per z-layer (nz)
+    std::vector<double> h_volz;
+};
+
+namespace bk {
+
+enum Slot : int {
+    kSlotIn0 = 0,   // staged host inputs
+    kSlotIn1,
+    kSlotIn2,
+    kSlotOut0,      // staged outputs
+    kSlotOut1,
+    kSlotOut2,
+    kSlotCgB,       // block CG
+    kSlotCgX,
+    kSlotCgR,
+    kSlotCgP,
+    kSlotCgW,
+    kSlotCgPart,
+    kSlotCgRed,
+    kSlotCgCtl,
+    kSlotActPart,   // combine/action residual partials
+    kSlotK,
+    kSlotQ,
+    kSlotC,
+    kSlotT,
+    kSlotQo,
+    kSlotRes,
+};
+
+bk_status fail(bk_ctx* ctx, bk_status st, const std::string& msg);
+// Grow-only workspace; contents are not preserved on growth.
+bk_status workspace(bk_ctx* ctx, int slot, size_t bytes, void** out);
+bool is_device_ptr(const void* p);
+
+// Kernels' host-side launchers (return cudaError_t of the launch).
+cudaError_t launch_assemble(bk_ctx* ctx, const bk_operator* op, const double* k,
+                            const bk_face* bc, double dx, double dy, const double* dz_dev);
+cudaError_t launch_apply_block(bk_ctx* ctx, const bk_operator* op, const double* x, int s,
+                               double* y);
+cudaError_t launch_rhs_from_power(bk_ctx* ctx, const bk_operator* op, const double* q, int s,
+                                  double* b);
+// dst (n x dw) <- src (n x sw): copies min(sw, dw) columns, zero-fills the rest.
+cudaError_t launch_pad_cols(bk_ctx* ctx, const double* src, int sw, double* dst, int dw,
+                            int64_t n);
+// B (n x S) = V Q + g for the first s columns (Q is n x s), zero beyond s.
+cudaError_t launch_rhs_padded(bk_ctx* ctx, const bk_operator* op, const double* q, int s,
+                              double* b, int S);
+// flag = any k <= 0 or NaN
+cudaError_t launch_check_positive(bk_ctx* ctx, const double* k, int64_t n, int* flag);
+cudaError_t launch_power_from_rhs(bk_ctx* ctx, const bk_operator* op, const double* b, int s,
+                                  double* q);
+
+struct CgReport {
+    int iterations;
+    int64_t matvecs;
+    double final_res[64];
+    char converged[64];
+};
+
+// Device-pointer block CG (X, B are n x s on device). Result report copied to
+// host (one small D2H at the end of the solve).
+bk_status block_cg_device(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
+                          const bk_solver_cfg* cfg, double* X, CgReport* rep);
+
+bk_status combine_action_device(bk_ctx* ctx, const bk_operator* op, const double* X, int s,
+                                const double* C, int64_t N, double* T, double* Q,
+                                double* resid);
+
+}  // namespace bk

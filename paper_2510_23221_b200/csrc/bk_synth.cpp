@@ -1,0 +1,280 @@
+// Seeded synthetic inputs for the five BASELINE configs (host side).
+//
+// The reference has no generators for these configs; the
+// pins below are ours and are documented in DESIGN.md §Inputs. All draws go
+// through a bit-exact restatement of the reference Rng (xoshiro256** seeded by
+// splitmix64, rng.hpp:14-63) and derive_seed (rng.cpp:47-60), so the CPU oracle,
+// the reference arm and the GPU path consume identical bytes. Field evaluation
+// (exp of the Gaussian blobs, lognormal factors) runs here once per chip; the
+// GPU forms B = V q + g itself (rhs_from_power, discretize.cpp:246-256).
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "blockoa_b200.h"
+
+namespace {
+
+std::uint64_t sm64(std::uint64_t& st) {
+    std::uint64_t z = (st += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+class Xoshiro {
+public:
+    explicit Xoshiro(std::uint64_t seed) {
+        std::uint64_t st = seed;
+        for (auto& w : s_) w = sm64(st);
+    }
+    std::uint64_t next() {
+        const std::uint64_t out = rotl(s_[1] * 5, 7) * 9;
+        const std::uint64_t t = s_[1] << 17;
+        s_[2] ^= s_[0];
+        s_[3] ^= s_[1];
+        s_[1] ^= s_[2];
+        s_[0] ^= s_[3];
+        s_[2] ^= t;
+        s_[3] = rotl(s_[3], 45);
+        return out;
+    }
+    double u01() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + u01() * (hi - lo); }
+    double normal() {
+        if (have_) {
+            have_ = false;
+            return spare_;
+        }
+        const double u1 = 1.0 - u01();
+        const double u2 = u01();
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        const double th = 2.0 * 3.141592653589793 * u2;
+        spare_ = r * std::sin(th);
+        have_ = true;
+        return r * std::cos(th);
+    }
+    std::uint64_t below(std::uint64_t n) {
+        const std::uint64_t lim = n * (~std::uint64_t{0} / n);
+        std::uint64_t x;
+        do {
+            x = next();
+        } while (x >= lim);
+        return x % n;
+    }
+
+private:
+    static std::uint64_t rotl(std::uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+    std::uint64_t s_[4];
+    double spare_ = 0.0;
+    bool have_ = false;
+};
+
+void add_blobs(Xoshiro& rng, int nblobs, double sig_scale, int nx, int ny, double* plane) {
+    for (int b = 0; b < nblobs; ++b) {
+        const double cx = rng.uniform(0.0, nx);
+        const double cy = rng.uniform(0.0, ny);
+        const double sig = rng.uniform(2.0, 8.0) * sig_scale;
+        const double amp = rng.uniform(0.0, 1e6);
+        const double inv2s2 = 1.0 / (2.0 * sig * sig);
+        for (int iy = 0; iy < ny; ++iy) {
+            const double ddy = iy + 0.5 - cy;
+            for (int ix = 0; ix < nx; ++ix) {
+                const double ddx = ix + 0.5 - cx;
+                plane[static_cast<std::size_t>(iy) * nx + ix] +=
+                    amp * std::exp(-(ddx * ddx + ddy * ddy) * inv2s2);
+            }
+        }
+    }
+}
+
+void add_rects(Xoshiro& rng, int nrect, double scale, int nx, int ny, double* plane) {
+    const int wmin = std::max(1, static_cast<int>(4 * scale));
+    const int wmax = std::max(wmin, static_cast<int>(32 * scale));
+    for (int r = 0; r < nrect; ++r) {
+        const int x0 = static_cast<int>(rng.below(static_cast<std::uint64_t>(nx)));
+        const int y0 = static_cast<int>(rng.below(static_cast<std::uint64_t>(ny)));
+        const int w = wmin + static_cast<int>(rng.below(static_cast<std::uint64_t>(wmax - wmin + 1)));
+        const int h = wmin + static_cast<int>(rng.below(static_cast<std::uint64_t>(wmax - wmin + 1)));
+        const double pw = rng.uniform(0.0, 2e6);
+        for (int iy = y0; iy < std::min(ny, y0 + h); ++iy)
+            for (int ix = x0; ix < std::min(nx, x0 + w); ++ix)
+                plane[static_cast<std::size_t>(iy) * nx + ix] += pw;
+    }
+}
+
+bk_face adiabatic() { return bk_face{BK_FACE_ADIABATIC, 0.0, 0.0}; }
+bk_face robin(double h, double u) { return bk_face{BK_FACE_ROBIN, h, u}; }
+
+// Ambient temperature of every Robin face. Fields are temperature rises over
+// ambient (with a non-zero ambient every basis RHS is
+// dominated by the shared lift g, the block is numerically rank one and the
+// reference block CG stagnates or diverges).
+constexpr double kUinf = 0.0;
+
+}  // namespace
+
+extern "C" {
+
+uint64_t bk_derive_seed(uint64_t seed, const char* tag, uint64_t index) {
+    std::uint64_t h = 0xcbf29ce484222325ULL;
+    for (const unsigned char* c = reinterpret_cast<const unsigned char*>(tag); *c; ++c) {
+        h ^= *c;
+        h *= 0x100000001b3ULL;
+    }
+    std::uint64_t st = seed;
+    const std::uint64_t mixed = sm64(st) ^ h;
+    st = mixed + 0x632be59bd9b4e019ULL * (index + 1);
+    return sm64(st);
+}
+
+void bk_rng_u64(uint64_t seed, int64_t n, uint64_t* out) {
+    Xoshiro r(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = r.next();
+}
+
+void bk_rng_uniform(uint64_t seed, double lo, double hi, int64_t n, double* out) {
+    Xoshiro r(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = r.uniform(lo, hi);
+}
+
+void bk_rng_normal(uint64_t seed, int64_t n, double* out) {
+    Xoshiro r(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = r.normal();
+}
+
+bk_status bk_synth_chip(const bk_synth_spec* sp, bk_grid* grid, double* dz_out, int* has_dz,
+                        bk_face bc[6], double* k, double* Q, double* C) {
+    if (!sp || !grid || !has_dz || !bc) return BK_INVALID_CONFIG;
+    const int nx = sp->nx, ny = sp->ny, nz = sp->nz, s = sp->s;
+    if (nx < 1 || ny < 1 || nz < 1 || s < 1 || sp->N < 0) return BK_INVALID_SPEC;
+    const std::int64_t plane = static_cast<std::int64_t>(nx) * ny;
+    const std::int64_t n = plane * nz;
+    const std::uint64_t chip = bk_derive_seed(sp->master_seed, "chip", sp->chip_id);
+    *has_dz = 0;
+    grid->nx = nx;
+    grid->ny = ny;
+    grid->nz = nz;
+    grid->lx = 10e-3;
+    grid->ly = 10e-3;
+    grid->dz = nullptr;
+    for (int f = 0; f < 6; ++f) bc[f] = adiabatic();
+
+    int power_z0 = 0, power_z1 = nz;  // power-layer cell range along z
+    int nblobs = 0, nrects = 0;
+    double scale = 1.0;
+
+    switch (sp->config) {
+        case 1:
+        case 2: {
+            // 2D die: nz=1 z+ Robin sink (Appendix A.2), 16x16-cell k tiles
+            // with k ~ U[10,150] drawn tile-row-major (A.3).
+            grid->lz = 0.15e-3 * nz;
+            bc[5] = robin(1e3, kUinf);
+            const int te = 16;
+            const int tx = (nx + te - 1) / te, ty = (ny + te - 1) / te;
+            if (k) {
+                Xoshiro rk(bk_derive_seed(chip, "k", 0));
+                double* kt = new double[static_cast<std::size_t>(tx) * ty];
+                for (int t = 0; t < tx * ty; ++t) kt[t] = rk.uniform(10.0, 150.0);
+                for (int iz = 0; iz < nz; ++iz)
+                    for (int iy = 0; iy < ny; ++iy)
+                        for (int ix = 0; ix < nx; ++ix)
+                            k[ix + nx * (iy + static_cast<std::int64_t>(ny) * iz)] =
+                                kt[(iy / te) * tx + ix / te];
+                delete[] kt;
+            }
+            nblobs = sp->config == 1 ? 3 : 5;
+            break;
+        }
+        case 3:
+        case 5: {
+            // 8-layer stack (A.6), bottom->top: bulk U[1,3], Si 150, TIM 5,
+            // Si 150, TIM 5, Si 150, TIM 5, Cu 400; nz/8 cells per layer,
+            // 0.1 mm per layer (uniform dz), per-cell lognormal sigma = ln 1.2.
+            if (nz % 8 != 0) return BK_INVALID_SPEC;
+            const int cpl = nz / 8;
+            grid->lz = 0.8e-3;
+            bc[4] = robin(1e2, kUinf);
+            bc[5] = robin(1e4, kUinf);
+            Xoshiro rl(bk_derive_seed(chip, "layers", 0));
+            const double kl[8] = {rl.uniform(1.0, 3.0), 150.0, 5.0, 150.0, 5.0, 150.0, 5.0, 400.0};
+            if (k) {
+                Xoshiro rn(bk_derive_seed(chip, "lognormal", 0));
+                const double ls = std::log(1.2);
+                for (std::int64_t i = 0; i < n; ++i) {
+                    const int iz = static_cast<int>(i / plane);
+                    k[i] = kl[iz / cpl] * std::exp(ls * rn.normal());
+                }
+            }
+            power_z0 = cpl;
+            power_z1 = 2 * cpl;
+            nblobs = 3;
+            nrects = 4;
+            scale = nx / 128.0;
+            break;
+        }
+        case 4: {
+            // Distinct chip per chip_id: dz_l ~ U[50,500] um, k_l ~ U[1,400],
+            // h_top, h_bot ~ U[1e2,1e4] (in that draw order), sides adiabatic.
+            if (!dz_out) return BK_INVALID_CONFIG;
+            Xoshiro rl(bk_derive_seed(chip, "layers", 0));
+            double lz = 0.0;
+            for (int l = 0; l < nz; ++l) {
+                dz_out[l] = rl.uniform(50e-6, 500e-6);
+                lz += dz_out[l];
+            }
+            double* kl = new double[static_cast<std::size_t>(nz)];
+            for (int l = 0; l < nz; ++l) kl[l] = rl.uniform(1.0, 400.0);
+            const double h_top = rl.uniform(1e2, 1e4);
+            const double h_bot = rl.uniform(1e2, 1e4);
+            grid->lz = lz;
+            grid->dz = dz_out;
+            *has_dz = 1;
+            bc[4] = robin(h_bot, kUinf);
+            bc[5] = robin(h_top, kUinf);
+            if (k)
+                for (std::int64_t i = 0; i < n; ++i) k[i] = kl[i / plane];
+            delete[] kl;
+            power_z0 = std::min(1, nz - 1);
+            power_z1 = power_z0 + 1;
+            nblobs = 5;
+            scale = nx / 128.0;
+            break;
+        }
+        default:
+            return BK_INVALID_CONFIG;
+    }
+
+    if (Q) {
+        std::memset(Q, 0, static_cast<std::size_t>(n) * s * sizeof(double));
+        double* pl = new double[static_cast<std::size_t>(plane)];
+        for (int t = 0; t < s; ++t) {
+            std::fill(pl, pl + plane, 0.0);
+            Xoshiro rb(bk_derive_seed(chip, "basis", static_cast<std::uint64_t>(t)));
+            add_blobs(rb, nblobs, scale, nx, ny, pl);
+            if (nrects) add_rects(rb, nrects, scale, nx, ny, pl);
+            for (int iz = power_z0; iz < power_z1; ++iz)
+                for (std::int64_t c = 0; c < plane; ++c)
+                    Q[(iz * plane + c) * s + t] = pl[c];
+        }
+        delete[] pl;
+    }
+    if (C) {
+        Xoshiro rc(bk_derive_seed(chip, "coef", 0));
+        const std::int64_t cnt = static_cast<std::int64_t>(s) * sp->N;
+        for (std::int64_t i = 0; i < cnt; ++i) C[i] = rc.u01();
+    }
+    return BK_OK;
+}
+
+bk_status bk_cg_error_bound(double kappa, int m, double e0, double* out) {
+    if (!(kappa >= 1.0)) return BK_INVALID_KAPPA;
+    if (m < 0 || !(e0 >= 0.0)) return BK_INVALID_CONFIG;
+    const double rk = std::sqrt(kappa);
+    *out = 2.0 * std::pow((rk - 1.0) / (rk + 1.0), m) * e0;
+    return BK_OK;
+}
+
+}  // extern "C"
