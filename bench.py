@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""BlocKOA data-generation benchmark: (q, T) samples/s on B200.
+
+A step is one pass of the hot path over one chip of synthetic input: assemble
+the stencil, form B = V q + g, block-CG basis solve, fused combine + operator
+action writing N (T, q) sample pairs. Default workload = BASELINE config 2
+(256x256x1 2D die, s=16 basis maps, N=2048 samples, block CG to 1e-12 with
+Jacobi). Multi-GPU: one process per GPU, each rank solves its own seeded chip
+(chip_id = rank) — independent chips, no data-path collective, weak scaling.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2]
+    python bench.py --impl reference ...   # the reference CPU core (oracle/_ref)
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §Measurement for every field).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "(q,T) samples/sec"
+UNIT = "samples/s"
+TOL = 1e-12
+
+WORKLOADS = {
+    1: "C1: 64x64x1 2D die (4x4 k tiles, 3 blobs/map), s=8, N=256",
+    2: "C2: 256x256x1 2D die (16x16 k tiles, 5 blobs/map), s=16, N=2048",
+    3: "C3: 128x128x8 layered stack (lognormal k), s=32, N=5000",
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ distributed
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ reference arm
+def reference_sample(config: int, threads: int, iter_cap: int, action_samples: int,
+                     chip_offset: int = 0):
+    """Bounded sample of the workload on the reference core (oracle/_ref).
+
+    `threads` independent chips run concurrently (the reference parallelises
+    across chips/groups only, pipeline.cpp:101,410,511; block_cg itself is
+    single-threaded). Per chip: assemble + rhs_from_power in full, block_cg
+    capped at `iter_cap` iterations and scaled by the full iteration count the
+    reference needs on this workload (tests/golden/c2_full_meta.npz, produced by
+    the reference itself), combine_from_weights + operator_action on
+    `action_samples` of the N samples, scaled to N. Returns per-chip seconds
+    (max over threads) and a description.
+    """
+    import paper_2510_23221_b200 as bk
+    from oracle.oracle import Reference
+
+    ref = Reference()
+    cid, nx, ny, nz, s, N = bk.CONFIGS[config]
+    meta = np.load(os.path.join(ROOT, "tests", "golden", "c2_full_meta.npz"))
+    full_iters = int(meta["iterations"])
+    inputs = [bk.synth_chip(cid, nx, ny, nz, s, N, chip_id=chip_offset + t) for t in range(threads)]
+    out = [None] * threads
+
+    def work(t):
+        inp = inputs[t]
+        g = inp.grid
+        t0 = time.perf_counter()
+        op = ref.assemble((g.nx, g.ny, g.nz, g.lx, g.ly, g.lz), inp.k, inp.bc.as_tuples())
+        B = np.stack([ref.rhs_from_power(op, inp.q_basis[:, j]) for j in range(s)], axis=1)
+        t1 = time.perf_counter()
+        X, rep = ref.block_cg(op, B, TOL, iter_cap, 1)
+        t2 = time.perf_counter()
+        ref.combine_action(op, X, np.ascontiguousarray(inp.coef[:, :action_samples]), threads=1)
+        t3 = time.perf_counter()
+        est = (t1 - t0) + (t2 - t1) * full_iters / max(rep["iterations"], 1) \
+            + (t3 - t2) * N / action_samples
+        out[t] = est
+
+    ths = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    per_chip_s = max(out)
+    desc = (f"{threads} concurrent chips (1 host thread each) of {WORKLOADS[config]}; per chip: "
+            f"assemble+rhs in full, block_cg timed over {iter_cap} iterations and scaled to the "
+            f"reference's {full_iters}-iteration solve, combine+operator_action timed on "
+            f"{action_samples} of {N} samples and scaled; reference core built -O3 x86-64-v3")
+    return per_chip_s, desc
+
+
+def run_reference_arm(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    import paper_2510_23221_b200 as bk
+    from oracle.oracle import reference_available
+
+    if not reference_available():
+        print(json.dumps({"impl": "reference", "metric": METRIC,
+                          "unavailable": "oracle/_ref/libblockoa_ref.so not built"}))
+        return 0
+    threads = os.cpu_count() or 1
+    N = bk.CONFIGS[args.config][5]
+    for _ in range(args.warmup):
+        reference_sample(args.config, threads, args.ref_iter_cap, args.ref_action_samples)
+    step_s = []
+    for _ in range(args.steps):
+        per_chip, desc = reference_sample(args.config, threads, args.ref_iter_cap,
+                                          args.ref_action_samples)
+        step_s.append(per_chip)
+    ms = float(np.mean(step_s)) * 1e3
+    value = threads * N / (ms * 1e-3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+        "config": config_dict(args.config, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def config_dict(config, world):
+    import paper_2510_23221_b200 as bk
+
+    cid, nx, ny, nz, s, N = bk.CONFIGS[config]
+    return {"workload": WORKLOADS[config], "grid": [nx, ny, nz], "s": s, "samples_per_chip": N,
+            "chips_per_step_per_gpu": 1, "tol": TOL, "precond": "jacobi",
+            "parallelism": f"chip-sharded x{world} (no collective)",
+            "l2": "flushed between timed steps (512 MiB write)"}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+
+    import paper_2510_23221_b200 as bk
+
+    world, rank, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product has no CPU path)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = bk.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+
+    cid, nx, ny, nz, s, N = bk.CONFIGS[args.config]
+    inp = bk.synth_chip(cid, nx, ny, nz, s, N, chip_id=rank)
+    n = inp.grid.cell_count()
+    cfg = bk.SolverConfig(TOL, 100000, "jacobi")
+    dev = torch.device("cuda", local)
+    k_d = torch.from_numpy(inp.k).to(dev)
+    q_d = torch.from_numpy(inp.q_basis).to(dev)
+    c_d = torch.from_numpy(inp.coef).to(dev)
+    T_d = torch.empty((N, n), dtype=torch.float64, device=dev)
+    Q_d = torch.empty((N, n), dtype=torch.float64, device=dev)
+    R_d = torch.empty(N, dtype=torch.float64, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        return bk.generate_chip(inp.grid, k_d, inp.bc, q_d, c_d, cfg, t_out=T_d, q_out=Q_d,
+                                resid_out=R_d, ctx=ctx)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    launches0 = ctx.launch_count
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    solve_s, iters = [], []
+    with ClockSampler(local) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            evs[i][0].record(stream)
+            _, _, _, rep, tim = step()
+            evs[i][1].record(stream)
+            solve_s.append(tim.basis_solve_s)
+            iters.append(rep.iterations)
+            if not rep.all_converged():
+                raise SystemExit(f"basis solve did not converge: {rep}")
+        barrier()
+    launches = ctx.launch_count - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_s = sum(step_ms) * 1e-3
+    max_resid = float(R_d.max().item())
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s = float(t.item())
+    value = N * args.steps * world / total_s
+
+    # ---- e2e: the same pipeline through the C ABI with pinned HOST buffers
+    k_h = torch.from_numpy(inp.k).pin_memory()
+    q_h = torch.from_numpy(inp.q_basis).pin_memory()
+    c_h = torch.from_numpy(inp.coef).pin_memory()
+    T_h = torch.empty((N, n), dtype=torch.float64).pin_memory()
+    Q_h = torch.empty((N, n), dtype=torch.float64).pin_memory()
+    R_h = torch.empty(N, dtype=torch.float64).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+    bk.generate_chip(inp.grid, k_h, inp.bc, q_h, c_h, cfg, t_out=T_h, q_out=Q_h, resid_out=R_h,
+                     ctx=ctx)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        bk.generate_chip(inp.grid, k_h, inp.bc, q_h, c_h, cfg, t_out=T_h, q_out=Q_h,
+                         resid_out=R_h, ctx=ctx)
+    e1.record(stream)
+    barrier()
+    e2e_s = e0.elapsed_time(e1) * 1e-3
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = N * e2e_steps * world / e2e_s
+    same = bool(torch.equal(T_h, T_d.cpu()) and torch.equal(Q_h, Q_d.cpu()))
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (persistent block CG)
+    bytes_per_iter = n * (40 + 80 * s)
+    mean_iters = float(np.mean(iters))
+    achieved = mean_iters * bytes_per_iter / float(np.mean(solve_s)) / 1e9
+    peak, peak_kind = peaks()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"config{args.config}")
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle.oracle import reference_available
+        if reference_available():
+            thr = os.cpu_count() or 1
+            per_chip, desc = reference_sample(args.config, thr, args.ref_iter_cap,
+                                              args.ref_action_samples)
+            cpu = {"value": thr * N / per_chip, "unit": UNIT, "cores": thr, "kind": "reference",
+                   "sample": desc}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": float(np.mean(step_ms)), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE-config generators, DESIGN.md §Inputs)",
+        "config": config_dict(args.config, world),
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": int((n + n * s + s * N) * 8),
+                "d2h_bytes_per_step": int((2 * n * N + N) * 8),
+                "outputs_equal_device_path": same},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "block_cg_kernel (persistent, one launch per solve)",
+                     "algorithmic_bytes_per_iter": bytes_per_iter,
+                     "iterations_per_solve": mean_iters,
+                     "solve_ms": float(np.mean(solve_s)) * 1e3, "peak_source": peak_kind},
+        "cpu_baseline": cpu,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "phase_ms": {"solve": float(np.mean(solve_s)) * 1e3},
+        "max_sample_residual": max_resid,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-iter-cap", type=int, default=24)
+    ap.add_argument("--ref-action-samples", type=int, default=64)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -331,7 +331,9 @@ void orc_op_export(const orc_op* op, int64_t* row_ptr, int32_t* col, double* val
 /* Y = A X, X/Y row-major n x s; per-row CSR-order fused accumulation (the
  * reference's apply_block compiles to FMA chains). The single-vector
  * CsrMatrix::apply (discretize.cpp:39-51) compiles to separate mul+add; the
- * scalar sweeps below (operator action, residuals) restate it that way. */
+ * scalar sweeps below (operator action, residuals) restate it that way. The
+ * reference build's apply_block_fixed<4> (S = 4 only) is vectorised without
+ * contraction (mul + add); that width is restated the same way. */
 void orc_apply_block(const orc_op* op, const double* x, int s, double* y) {
     double* acc = (double*)malloc((size_t)s * sizeof(double));
     for (int64_t i = 0; i < op->n; ++i) {
@@ -339,7 +341,10 @@ void orc_apply_block(const orc_op* op, const double* x, int s, double* y) {
         for (int64_t q = op->row_ptr[i]; q < op->row_ptr[i + 1]; ++q) {
             const double a = op->val[q];
             const double* xr = x + (int64_t)op->col[q] * s;
-            for (int j = 0; j < s; ++j) acc[j] = fma(a, xr[j], acc[j]);
+            if (s == 4)
+                for (int j = 0; j < s; ++j) acc[j] += a * xr[j];
+            else
+                for (int j = 0; j < s; ++j) acc[j] = fma(a, xr[j], acc[j]);
         }
         for (int j = 0; j < s; ++j) y[i * s + j] = acc[j];
     }

@@ -121,13 +121,25 @@ __global__ void __launch_bounds__(256) apply_block_kernel(
         const int iy = (int)((i / nx) % ny);
         const int iz = (int)(i / plane);
         double acc = 0.0;
-        if (iz > 0) acc = fma(-cz[i - plane], x[e - plane * s], acc);
-        if (iy > 0) acc = fma(-cy[i - nx], x[e - (int64_t)nx * s], acc);
-        if (ix > 0) acc = fma(-cx[i - 1], x[e - s], acc);
-        acc = fma(diag[i], x[e], acc);
-        if (ix < nx - 1) acc = fma(-cx[i], x[e + s], acc);
-        if (iy < ny - 1) acc = fma(-cy[i], x[e + (int64_t)nx * s], acc);
-        if (iz < nz - 1) acc = fma(-cz[i], x[e + plane * s], acc);
+        if (s != 4) {
+            if (iz > 0) acc = fma(-cz[i - plane], x[e - plane * s], acc);
+            if (iy > 0) acc = fma(-cy[i - nx], x[e - (int64_t)nx * s], acc);
+            if (ix > 0) acc = fma(-cx[i - 1], x[e - s], acc);
+            acc = fma(diag[i], x[e], acc);
+            if (ix < nx - 1) acc = fma(-cx[i], x[e + s], acc);
+            if (iy < ny - 1) acc = fma(-cy[i], x[e + (int64_t)nx * s], acc);
+            if (iz < nz - 1) acc = fma(-cz[i], x[e + plane * s], acc);
+        } else {
+            // the reference build compiles apply_block_fixed<4> without
+            // contraction: separate multiply and add per term
+            if (iz > 0) acc = __dadd_rn(acc, __dmul_rn(-cz[i - plane], x[e - plane * s]));
+            if (iy > 0) acc = __dadd_rn(acc, __dmul_rn(-cy[i - nx], x[e - (int64_t)nx * s]));
+            if (ix > 0) acc = __dadd_rn(acc, __dmul_rn(-cx[i - 1], x[e - s]));
+            acc = __dadd_rn(acc, __dmul_rn(diag[i], x[e]));
+            if (ix < nx - 1) acc = __dadd_rn(acc, __dmul_rn(-cx[i], x[e + s]));
+            if (iy < ny - 1) acc = __dadd_rn(acc, __dmul_rn(-cy[i], x[e + (int64_t)nx * s]));
+            if (iz < nz - 1) acc = __dadd_rn(acc, __dmul_rn(-cz[i], x[e + plane * s]));
+        }
         y[e] = acc;
     }
 }

@@ -88,5 +88,27 @@ def main():
               f"max resid={R.max():.2e}")
 
 
+def c2_full_meta(ref):
+    """Reference block-CG iteration count on the full BASELINE config-2 chip
+    (chip 0): bench.py's reference arm times a capped number of iterations and
+    scales by this count."""
+    import time
+
+    inp = bk.synth_chip(*bk.CONFIGS[2])
+    op = ref.assemble(grid_tuple(inp.grid), inp.k, inp.bc.as_tuples())
+    B = np.stack([ref.rhs_from_power(op, inp.q_basis[:, t]) for t in range(16)], axis=1)
+    t0 = time.perf_counter()
+    X, rep = ref.block_cg(op, B, 1e-12, 100000, 1)
+    wall = time.perf_counter() - t0
+    np.savez(os.path.join(OUT, "c2_full_meta.npz"), input_sha256=input_digest(inp),
+             iterations=rep["iterations"], matvec_count=rep["matvec_count"],
+             final_rel_residual=rep["final_rel_residual"], converged=rep["converged"],
+             solve_wall_s=wall, X_colnorm=np.linalg.norm(X, axis=0),
+             X_checksum=np.array([X.sum(), np.abs(X).sum()]))
+    print(f"c2_full: iters={rep['iterations']} wall={wall:.1f}s")
+
+
 if __name__ == "__main__":
     main()
+    if "--c2-full" in sys.argv:
+        c2_full_meta(Reference())

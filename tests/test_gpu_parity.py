@@ -1,0 +1,316 @@
+"""GPU parity tests: the sm_100a path (through the C ABI) against the reference
+golden fixtures and the CPU oracle on the same seeded inputs.
+
+Bars: integer structure bitwise; stencil coefficients, apply_block,
+rhs_from_power, and combine/action (given the same X) bitwise; block-CG
+solutions within 1e-9 relative L2 (Krylov reduction order differs); full-chain
+(T, q) within 1e-9 relative L2; every sample residual <= 1e-12.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden, grid_tuple, rel_l2
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+PARITY = 1e-9
+
+
+def cfg_jacobi(max_iter=100000):
+    import paper_2510_23221_b200 as bk
+    return bk.SolverConfig(TOL, max_iter, "jacobi")
+
+
+# ----------------------------------------------------------------- discretization
+def test_kat_3x3x3_bitwise(bk, ctx):
+    d = golden("kat_3x3x3.npz")
+    op = bk.assemble(np.ones(27), bk.GridSpec(3, 3, 3, 3.0, 3.0, 3.0),
+                     bk.BoundarySpec.uniform_dirichlet(0.0), ctx)
+    for a, b in zip(op.csr(), (d["row_ptr"], d["col"], d["val"], d["g"], d["vol"])):
+        assert a.dtype == b.dtype and np.array_equal(a, b)
+
+
+def test_mixed_operator_and_apply_bitwise(bk, ctx):
+    d = golden("mixed_operator.npz")
+    faces = []
+    for kd, a, b in zip(d["bc_kind"], d["bc_a"], d["bc_b"]):
+        faces.append(bk.Dirichlet(a) if kd == 0 else bk.Robin(a, b) if kd == 1 else bk.Adiabatic())
+    gr = d["grid"]
+    grid = bk.GridSpec(int(gr[0]), int(gr[1]), int(gr[2]), gr[3], gr[4], gr[5])
+    op = bk.assemble(d["k"], grid, bk.BoundarySpec(faces), ctx)
+    for a, key in zip(op.csr(), ("row_ptr", "col", "val", "g", "vol")):
+        assert np.array_equal(a, d[key]), key
+    for s in (1, 4, 7, 16):
+        x = d[f"x{s}"]
+        assert np.array_equal(op.apply_block(x), d[f"y{s}"]), s
+
+
+@pytest.mark.parametrize("case", [(1, 32, 32, 1, 8), (2, 48, 40, 1, 16), (3, 16, 16, 8, 32),
+                                  (4, 24, 16, 4, 16), (5, 8, 8, 16, 64)])
+def test_assemble_apply_rhs_bitwise_vs_oracle(bk, ctx, oracle, case):
+    inp = bk.synth_chip(*case, 4)
+    g = inp.grid
+    op = bk.assemble(inp.k, g, inp.bc, ctx)
+    o = oracle.assemble(grid_tuple(g), inp.k, inp.bc.as_tuples(), dz=g.dz)
+    for a, b in zip(op.csr(), oracle.csr(o)):
+        assert np.array_equal(a, b)
+    x = np.random.default_rng(1).standard_normal((g.cell_count(), 5))
+    assert np.array_equal(op.apply_block(x), oracle.apply_block(o, x))
+    assert np.array_equal(bk.rhs_from_power(op, inp.q_basis), oracle.rhs_from_power(o, inp.q_basis))
+    b = oracle.rhs_from_power(o, inp.q_basis)
+    assert np.array_equal(bk.power_from_rhs(op, b), oracle.power_from_rhs(o, b))
+
+
+def test_operator_action_center_indicator(bk, ctx):
+    """q = center column of A (27-cell, g = 0, unit volumes)."""
+    op = bk.assemble(np.ones(27), bk.GridSpec(3, 3, 3, 3.0, 3.0, 3.0),
+                     bk.BoundarySpec.uniform_dirichlet(0.0), ctx)
+    x = np.zeros((27, 1))
+    x[13, 0] = 1.0
+    T, Q, R = bk.combine_action(op, x, np.ones((1, 1)))
+    assert Q[0, 13] == 6.0 and all(Q[0, i] == -1.0 for i in (4, 10, 12, 14, 16, 22))
+    assert R[0] == 0.0 and T[0, 13] == 1.0
+
+
+# ----------------------------------------------------------------- solver
+@pytest.mark.parametrize("name", ["c1_full", "c2_reduced", "c3_reduced", "c5_reduced"])
+def test_block_cg_vs_reference_golden(bk, ctx, oracle, name):
+    d = golden(f"{name}.npz")
+    cfg, (nx, ny, nz, s, N) = int(d["config"]), d["shape"].tolist()
+    inp = bk.synth_chip(cfg, nx, ny, nz, s, N)
+    op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
+    B = bk.rhs_from_power(op, inp.q_basis)
+    r = bk.block_cg(op, B, cfg_jacobi())
+    assert r.report.all_converged()
+    assert np.all(r.report.final_rel_residual <= TOL)
+    assert rel_l2(r.x, d["X"]) <= PARITY
+    ref_it = int(d["iterations"])
+    assert abs(r.report.iterations - ref_it) <= max(3, ref_it // 10)
+    # independent check of the GPU solution with the oracle's CSR apply
+    o = oracle.assemble(grid_tuple(inp.grid), inp.k, inp.bc.as_tuples())
+    res = np.linalg.norm(B - oracle.apply_block(o, r.x), axis=0) / np.linalg.norm(B, axis=0)
+    assert np.all(res <= 1.5 * TOL)
+
+
+def test_block_cg_matches_oracle_iterates(bk, ctx, oracle):
+    """Capped iteration counts: GPU iterate after m steps == oracle iterate."""
+    inp = bk.synth_chip(3, 16, 16, 8, 32, 4)
+    op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
+    o = oracle.assemble(grid_tuple(inp.grid), inp.k, inp.bc.as_tuples())
+    B = oracle.rhs_from_power(o, inp.q_basis)
+    for m in (1, 2, 5, 13):
+        r = bk.block_cg(op, B, cfg_jacobi(m))
+        X, rep = oracle.block_cg(o, B, TOL, m, 1)
+        assert r.report.iterations == rep["iterations"] == m
+        assert r.report.matvec_count == rep["matvec_count"]
+        assert not r.report.converged.any() and not rep["converged"].any()
+        assert rel_l2(r.x, X) <= 1e-12
+        assert np.allclose(r.report.final_rel_residual, rep["final_rel_residual"], rtol=1e-9)
+
+
+def test_block_cg_nonuniform_stack_vs_oracle(bk, ctx, oracle):
+    """BASELINE config 4 (per-chip non-uniform dz; not expressible in the
+    reference GridSpec) against the oracle restatement."""
+    for chip in (0, 1):
+        inp = bk.synth_chip(4, 32, 32, 4, 16, 8, chip_id=chip)
+        op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
+        o = oracle.assemble(grid_tuple(inp.grid), inp.k, inp.bc.as_tuples(), dz=inp.grid.dz)
+        B = oracle.rhs_from_power(o, inp.q_basis)
+        r = bk.block_cg(op, B, cfg_jacobi())
+        X, rep = oracle.block_cg(o, B, TOL, 100000, 1)
+        assert r.report.all_converged() and rep["converged"].all()
+        assert rel_l2(r.x, X) <= PARITY
+
+
+def test_block_cg_duplicate_and_zero_columns(bk, ctx, oracle):
+    """SPEC.md:211 duplicate columns (rank-deficient block -> pivoted Cholesky
+    path) and zero right-hand sides (x = 0, converged, solvers.cpp:478-485)."""
+    inp = bk.synth_chip(1, 24, 24, 1, 8, 1)
+    op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
+    o = oracle.assemble(grid_tuple(inp.grid), inp.k, inp.bc.as_tuples())
+    B = oracle.rhs_from_power(o, inp.q_basis)
+    B[:, 3] = B[:, 1]
+    B[:, 5] = 0.0
+    r = bk.block_cg(op, B, cfg_jacobi())
+    X, rep = oracle.block_cg(o, B, TOL, 100000, 1)
+    assert r.report.all_converged() and rep["converged"].all()
+    assert np.all(r.x[:, 5] == 0.0) and r.report.final_rel_residual[5] == 0.0
+    assert rel_l2(r.x, X) <= PARITY
+    assert rel_l2(r.x[:, 3], r.x[:, 1]) <= 10 * TOL
+
+
+def test_s1_and_odd_widths(bk, ctx, oracle):
+    """s = 1 equals CG; widths padded to the kernel width."""
+    inp = bk.synth_chip(1, 24, 20, 1, 8, 1)
+    op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
+    o = oracle.assemble(grid_tuple(inp.grid), inp.k, inp.bc.as_tuples())
+    B = oracle.rhs_from_power(o, inp.q_basis)
+    b = np.ascontiguousarray(B[:, 0])
+    x, rc = oracle.cg(o, b, TOL, 100000, 1)
+    r = bk.block_cg(op, b[:, None].copy(), cfg_jacobi())
+    assert rel_l2(r.x[:, 0], x) <= 10 * TOL and r.report.converged[0] == rc["converged"]
+    for s in (3, 5, 11):
+        Bs = np.ascontiguousarray(B[:, :min(s, 8)]) if s <= 8 else np.ascontiguousarray(
+            np.concatenate([B, B[:, : s - 8] * 0.5 + 1e-3 * B[:, 1: s - 7]], axis=1))
+        r = bk.block_cg(op, Bs, cfg_jacobi())
+        X, rep = oracle.block_cg(o, Bs, TOL, 100000, 1)
+        assert r.report.all_converged() and rel_l2(r.x, X) <= PARITY
+
+
+def test_block_cg_deterministic(bk, ctx):
+    inp = bk.synth_chip(2, 64, 64, 1, 16, 1)
+    op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
+    B = bk.rhs_from_power(op, inp.q_basis)
+    r1 = bk.block_cg(op, B, cfg_jacobi())
+    r2 = bk.block_cg(op, B, cfg_jacobi())
+    assert np.array_equal(r1.x, r2.x) and r1.report.iterations == r2.report.iterations
+
+
+def test_errors_map_to_reference_exceptions(bk, ctx):
+    grid = bk.GridSpec(4, 4, 1, 1e-3, 1e-3, 1e-4)
+    bc = bk.BoundarySpec.uniform_dirichlet(0.0)
+    k = np.ones(16)
+    with pytest.raises(bk.NonPositiveConductivityError):
+        bk.assemble(np.where(np.arange(16) == 5, -1.0, 1.0), grid, bc, ctx)
+    with pytest.raises(bk.NonPositiveHtcError):
+        bk.assemble(k, grid, bk.BoundarySpec([bk.Robin(0.0, 1.0)] + [bk.Dirichlet()] * 5), ctx)
+    with pytest.raises(bk.InvalidSpecError):
+        bk.assemble(np.ones(0), bk.GridSpec(0, 4, 1, 1, 1, 1), bc, ctx)
+    with pytest.raises(bk.DimensionMismatchError):
+        bk.assemble(np.ones(15), grid, bc, ctx)
+    op = bk.assemble(k, grid, bc, ctx)
+    with pytest.raises(bk.InvalidConfigError):
+        bk.block_cg(op, np.ones((16, 2)), bk.SolverConfig(1.5, 10, "jacobi"))
+    with pytest.raises(bk.InvalidConfigError):
+        bk.block_cg(op, np.ones((16, 2)), bk.SolverConfig(1e-9, 0, "jacobi"))
+    with pytest.raises(bk.DimensionMismatchError):
+        bk.block_cg(op, np.ones((15, 2)), cfg_jacobi())
+    with pytest.raises(bk.EmptyBasisError):
+        bk.combine_action(op, np.ones((16, 0)), np.ones((0, 3)))
+
+
+# ----------------------------------------------------------------- combine + action
+@pytest.mark.parametrize("name", ["c1_full", "c2_reduced", "c3_reduced", "c5_reduced"])
+def test_combine_action_bitwise_vs_reference_golden(bk, ctx, name):
+    """Given the reference's X, T and q equal the reference's bit for bit."""
+    d = golden(f"{name}.npz")
+    cfg, (nx, ny, nz, s, N) = int(d["config"]), d["shape"].tolist()
+    inp = bk.synth_chip(cfg, nx, ny, nz, s, N)
+    op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
+    T, Q, R = bk.combine_action(op, d["X"], inp.coef)
+    keep = d["keep"]
+    assert np.array_equal(T[keep], d["T"]) and np.array_equal(Q[keep], d["Q"])
+    assert np.allclose(R, d["resid"], rtol=1e-6, atol=1e-17) and np.max(R) <= TOL
+
+
+def test_combine_action_bitwise_vs_oracle_odd_shapes(bk, ctx, oracle):
+    for case, N in (((1, 37, 29, 1, 8), 19), ((3, 33, 17, 8, 32), 21), ((4, 20, 9, 4, 16), 8)):
+        inp = bk.synth_chip(*case, N)
+        g = inp.grid
+        op = bk.assemble(inp.k, g, inp.bc, ctx)
+        o = oracle.assemble(grid_tuple(g), inp.k, inp.bc.as_tuples(), dz=g.dz)
+        X = np.random.default_rng(2).uniform(0, 50, (g.cell_count(), case[4]))
+        coef = inp.coef.copy()
+        coef[0, 3] = 0.0      # zero weights are skipped in the reference
+        coef[:, 5] = 0.0
+        T, Q, R = bk.combine_action(op, X, coef)
+        To, Qo, Ro = oracle.combine_action(o, X, coef)
+        assert np.array_equal(T, To) and np.array_equal(Q, Qo)
+        assert np.allclose(R, Ro, rtol=1e-6, atol=1e-17)
+
+
+# ----------------------------------------------------------------- full chain
+@pytest.mark.parametrize("name", ["c1_full", "c2_reduced", "c3_reduced", "c5_reduced"])
+def test_generate_chip_vs_reference_golden(bk, ctx, name):
+    d = golden(f"{name}.npz")
+    cfg, (nx, ny, nz, s, N) = int(d["config"]), d["shape"].tolist()
+    inp = bk.synth_chip(cfg, nx, ny, nz, s, N)
+    T, Q, R, rep, tim = bk.generate_chip(inp.grid, inp.k, inp.bc, inp.q_basis, inp.coef,
+                                         cfg_jacobi(), ctx=ctx)
+    keep = d["keep"]
+    for j, kk in enumerate(keep):
+        assert rel_l2(T[kk], d["T"][j]) <= PARITY
+        assert rel_l2(Q[kk], d["Q"][j]) <= PARITY
+    assert np.max(R) <= TOL and rep.all_converged()
+    assert tim.basis_solve_s > 0 and tim.total_s >= tim.basis_solve_s
+
+
+def test_generate_chip_nonuniform_vs_oracle(bk, ctx, oracle):
+    inp = bk.synth_chip(4, 32, 32, 4, 16, 8, chip_id=7)
+    T, Q, R, rep, _ = bk.generate_chip(inp.grid, inp.k, inp.bc, inp.q_basis, inp.coef,
+                                       cfg_jacobi(), ctx=ctx)
+    o = oracle.assemble(grid_tuple(inp.grid), inp.k, inp.bc.as_tuples(), dz=inp.grid.dz)
+    X, _ = oracle.block_cg(o, oracle.rhs_from_power(o, inp.q_basis), TOL, 100000, 1)
+    To, Qo, Ro = oracle.combine_action(o, X, inp.coef)
+    assert rel_l2(T, To) <= PARITY and rel_l2(Q, Qo) <= PARITY and np.max(R) <= TOL
+
+
+def test_generate_chip_host_and_device_pointers_agree(bk, ctx):
+    import torch
+
+    inp = bk.synth_chip(2, 64, 64, 1, 16, 40)
+    T1, Q1, R1, rep1, _ = bk.generate_chip(inp.grid, inp.k, inp.bc, inp.q_basis, inp.coef,
+                                           cfg_jacobi(), ctx=ctx)
+    dev = torch.device("cuda", 0)
+    n, N = inp.grid.cell_count(), 40
+    Td = torch.empty((N, n), dtype=torch.float64, device=dev)
+    Qd = torch.empty_like(Td)
+    Rd = torch.empty(N, dtype=torch.float64, device=dev)
+    bk.generate_chip(inp.grid, torch.from_numpy(inp.k).to(dev), inp.bc,
+                     torch.from_numpy(inp.q_basis).to(dev), torch.from_numpy(inp.coef).to(dev),
+                     cfg_jacobi(), t_out=Td, q_out=Qd, resid_out=Rd, ctx=ctx)
+    torch.cuda.synchronize()
+    assert np.array_equal(Td.cpu().numpy(), T1) and np.array_equal(Qd.cpu().numpy(), Q1)
+    assert np.array_equal(Rd.cpu().numpy(), R1)
+
+
+@pytest.mark.slow
+def test_full_size_c2_properties(bk, ctx, oracle):
+    """BASELINE config 2 at full size: size-independent properties against the
+    oracle (the full oracle pipeline takes minutes): per-column true residual of
+    the GPU basis via the oracle CSR, X column norms vs the reference's own
+    full solve (tests/golden/c2_full_meta.npz), sampled (T, q) bitwise equal to
+    the oracle's combine/action on the GPU basis, every sample residual."""
+    import torch
+
+    d = golden("c2_full_meta.npz")
+    inp = bk.synth_chip(*bk.CONFIGS[2])
+    n, s, N = inp.grid.cell_count(), 16, 2048
+    op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
+    o = oracle.assemble(grid_tuple(inp.grid), inp.k, inp.bc.as_tuples())
+    B = bk.rhs_from_power(op, inp.q_basis)
+    r = bk.block_cg(op, B, cfg_jacobi())
+    assert r.report.all_converged()
+    res = np.linalg.norm(B - oracle.apply_block(o, r.x), axis=0) / np.linalg.norm(B, axis=0)
+    assert np.all(res <= 1.5 * TOL)
+    assert np.allclose(np.linalg.norm(r.x, axis=0), d["X_colnorm"], rtol=PARITY)
+    assert abs(r.report.iterations - int(d["iterations"])) <= int(d["iterations"]) // 10
+    dev = torch.device("cuda", 0)
+    Td = torch.empty((N, n), dtype=torch.float64, device=dev)
+    Qd = torch.empty_like(Td)
+    Rd = torch.empty(N, dtype=torch.float64, device=dev)
+    bk.combine_action(op, r.x, inp.coef, t_out=Td, q_out=Qd, resid_out=Rd)
+    torch.cuda.synchronize()
+    pick = [0, 1, 777, 2047]
+    To, Qo, Ro = oracle.combine_action(o, r.x, inp.coef[:, pick].copy())
+    assert np.array_equal(Td[pick].cpu().numpy(), To)
+    assert np.array_equal(Qd[pick].cpu().numpy(), Qo)
+    assert float(Rd.max()) <= TOL
+    # determinism of the whole chain
+    T2, Q2, R2, rep2, _ = bk.generate_chip(inp.grid, inp.k, inp.bc, inp.q_basis, inp.coef,
+                                           cfg_jacobi(), ctx=ctx)
+    T3, Q3, R3, rep3, _ = bk.generate_chip(inp.grid, inp.k, inp.bc, inp.q_basis, inp.coef,
+                                           cfg_jacobi(), ctx=ctx)
+    assert np.array_equal(T2, T3) and np.array_equal(Q2, Q3)
+    assert rel_l2(T2[pick], To) <= PARITY and rel_l2(Q2[pick], Qo) <= PARITY
+
+
+def test_launch_counter_and_native_library_loaded(bk, ctx):
+    import os
+
+    before = ctx.launch_count
+    inp = bk.synth_chip(1, 16, 16, 1, 8, 4)
+    bk.generate_chip(inp.grid, inp.k, inp.bc, inp.q_basis, inp.coef, cfg_jacobi(), ctx=ctx)
+    assert ctx.launch_count > before
+    maps = open("/proc/self/maps").read()
+    assert os.path.basename(bk.library_path()) in maps
