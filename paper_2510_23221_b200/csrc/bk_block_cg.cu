@@ -1,4 +1,6 @@
-// Block conjugate gradient as ONE persistent cooperative sm_100a kernel.
+// Block conjugate gradient as ONE persistent cooperative sm_100a kernel —
+// generic SIMT-FP64 variant (any width; the production path for S = 64).
+// bk_block_cg_dmma.cu holds the DMMA variant used for S <= 32.
 //
 // Restates block_cg (solvers.cpp:452-665) without any host round trip per
 // iteration. Each CTA owns a contiguous range of cells; block vectors live in
@@ -673,8 +675,10 @@ bk_status run_block_cg(bk_ctx* ctx, const bk_operator* op, const double* B, int 
 
 namespace bk {
 
-bk_status block_cg_device(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
-                          const bk_solver_cfg* cfg, double* X, CgReport* rep) {
+// Generic (SIMT) path: any kernel width; used for S = 64 and as a cross-check
+// of the DMMA path (BK_CG_GENERIC=1).
+bk_status block_cg_generic(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
+                           const bk_solver_cfg* cfg, double* X, CgReport* rep) {
     if (s <= 8) return run_block_cg<8>(ctx, op, B, s, cfg, X, rep);
     if (s <= 16) return run_block_cg<16>(ctx, op, B, s, cfg, X, rep);
     if (s <= 32) return run_block_cg<32>(ctx, op, B, s, cfg, X, rep);

@@ -1,0 +1,998 @@
+// Block conjugate gradient — DMMA variant (kernel widths S = 8, 16, 32).
+//
+// Same algorithm and control flow as the generic kernel (bk_block_cg.cu; the
+// reference is block_cg, solvers.cpp:452-665), restructured around FP64 tensor
+// cores: every dense s x s product runs on mma.sync.m16n8k4.f64 (measured
+// 74 TFLOP/s on B200 vs 37 for SIMT DFMA), with operand fragments produced in
+// registers by the sweep that loads them — no shared-memory staging except a
+// warp-private transpose for R^T Z.
+//
+//   phase 1  per warp, 4-cell k-groups: lane (g = lane/4, t = lane%4) computes the
+//            stencil W[cell t][g + 8c] (CSR-order FMA chain, bitwise the reference
+//            apply_block) and already holds the A (= P^T) and B (= W) fragments of
+//            the Gram G = P^T W, accumulated by DMMA with K = cells.
+//   phase 2  per warp, 16-cell tiles: X += P alpha and R -= W alpha as DMMA GEMMs
+//            (M = cells, N = columns, K = s), rr and Z = D^-1 R in the epilogue,
+//            S_new = R^T Z by DMMA after a warp-private smem transpose.
+//   phase 3  P = Z + P beta, DMMA with the accumulator initialised to Z.
+//
+// Grid-wide: cooperative launch, cg::grid.sync (1.2 us measured), fixed-order
+// distributed reductions (no floating-point atomics: bitwise deterministic),
+// redundant per-CTA s x s solves (Gauss-Jordan with the reference's pivoted
+// Cholesky as the rank-deficient fallback).
+#include <cooperative_groups.h>
+
+#include <cmath>
+#include <cstdlib>
+
+#include "bk_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+// CTA size per kernel width: 16 warps for S <= 16 (one CTA per SM), 8 warps
+// for S = 32 (one CTA per SM, up to 255 registers per thread).
+template <int S>
+struct CtaShape {
+    static constexpr int BS = S <= 16 ? 512 : 256;
+    static constexpr int NW = BS / 32;
+};
+constexpr int PROF_ITERS = 64;
+__device__ long long* g_ss_prof = nullptr;  // debug: small-solve step timestamps
+constexpr int PROF_MARKS = 8;
+
+struct Args {
+    int nx, ny, nz;
+    int64_t n;
+    const double* diag;
+    const double* cx;
+    const double* cy;
+    const double* cz;
+    const double* dinv;
+    const double* B;
+    double* X;
+    double* R;
+    double* P;
+    double* W;
+    double* part;
+    double* red;
+    double tol;
+    int max_iter;
+    int precond;
+    bk::CgReport* rep;
+    long long* prof;  // optional phase timestamps (CTA 0), PROF_ITERS x PROF_MARKS
+};
+
+__device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+        "{%0,%1,%2,%3};"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a0), "d"(a1), "d"(b));
+}
+
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int S>
+struct Sm {
+    double s_old[S * S];
+    double mat[S * S];
+    double coef[S * S];
+    double aug[2 * S * S + 2 * S];
+    double scratch[CtaShape<S>::NW * S * S];  // per-warp matrix partials
+    double tileR[CtaShape<S>::NW][16 * S];    // warp-private transposes (phase 2 / init)
+    double tileZ[CtaShape<S>::NW][16 * S];
+    double vec[S];
+    double bnorm[S];
+    double fres[S];
+    double dpiv[S];
+    int perm[S];
+    int act[S];
+    int idx[S];
+    int vflag[S];
+    int conv[S];
+    int sa;
+    int fail;
+    int rank;
+};
+
+// ---------------------------------------------------------------------------
+// stencil at (cell, col) of a row-major n x S block
+// ---------------------------------------------------------------------------
+struct Coef {
+    double d, xm, xp, ym, yp, zm, zp;  // CSR values (-conductance off the diagonal)
+    int64_t oxm, oxp, oym, oyp, ozm, ozp;  // neighbour cell offsets (0 if absent)
+    bool hxm, hxp, hym, hyp, hzm, hzp;
+};
+
+__device__ __forceinline__ void load_coef(const Args& a, int64_t c, Coef& k) {
+    const int ci = (int)c;
+    const int ix = ci % a.nx;
+    const int iy = (ci / a.nx) % a.ny;
+    const int iz = ci / (a.nx * a.ny);
+    const int64_t plane = (int64_t)a.nx * a.ny;
+    k.hzm = iz > 0;
+    k.hym = iy > 0;
+    k.hxm = ix > 0;
+    k.hxp = ix < a.nx - 1;
+    k.hyp = iy < a.ny - 1;
+    k.hzp = iz < a.nz - 1;
+    k.d = a.diag[c];
+    k.zm = k.hzm ? -a.cz[c - plane] : 0.0;
+    k.ym = k.hym ? -a.cy[c - a.nx] : 0.0;
+    k.xm = k.hxm ? -a.cx[c - 1] : 0.0;
+    k.xp = k.hxp ? -a.cx[c] : 0.0;
+    k.yp = k.hyp ? -a.cy[c] : 0.0;
+    k.zp = k.hzp ? -a.cz[c] : 0.0;
+    k.ozm = plane;
+    k.oym = a.nx;
+}
+
+// CSR-order FMA chain (apply_block_fixed, discretize.cpp:57-71)
+template <int S>
+__device__ __forceinline__ double st_fma(const Coef& k, const double* __restrict__ V, int64_t c,
+                                         int col, double& center) {
+    const int64_t e = c * S + col;
+    double acc = 0.0;
+    if (k.hzm) acc = fma(k.zm, V[e - k.ozm * S], acc);
+    if (k.hym) acc = fma(k.ym, V[e - k.oym * S], acc);
+    if (k.hxm) acc = fma(k.xm, V[e - S], acc);
+    center = V[e];
+    acc = fma(k.d, center, acc);
+    if (k.hxp) acc = fma(k.xp, V[e + S], acc);
+    if (k.hyp) acc = fma(k.yp, V[e + k.oym * S], acc);
+    if (k.hzp) acc = fma(k.zp, V[e + k.ozm * S], acc);
+    return acc;
+}
+
+// separate multiply + add (CsrMatrix::apply, used by true_rel_residual)
+template <int S>
+__device__ __forceinline__ double st_muladd(const Coef& k, const double* __restrict__ V,
+                                            int64_t c, int col) {
+    const int64_t e = c * S + col;
+    double acc = 0.0;
+    if (k.hzm) acc = __dadd_rn(acc, __dmul_rn(k.zm, V[e - k.ozm * S]));
+    if (k.hym) acc = __dadd_rn(acc, __dmul_rn(k.ym, V[e - k.oym * S]));
+    if (k.hxm) acc = __dadd_rn(acc, __dmul_rn(k.xm, V[e - S]));
+    acc = __dadd_rn(acc, __dmul_rn(k.d, V[e]));
+    if (k.hxp) acc = __dadd_rn(acc, __dmul_rn(k.xp, V[e + S]));
+    if (k.hyp) acc = __dadd_rn(acc, __dmul_rn(k.yp, V[e + k.oym * S]));
+    if (k.hzp) acc = __dadd_rn(acc, __dmul_rn(k.zp, V[e + k.ozm * S]));
+    return acc;
+}
+
+// ---------------------------------------------------------------------------
+// reductions
+// ---------------------------------------------------------------------------
+// Gram accumulator in DMMA D-fragment layout: tile (mt, nt) holds
+// G[16mt+g][8nt+2t+{0,1}] and G[16mt+g+8][8nt+2t+{0,1}].
+template <int S>
+struct GramAcc {
+    static constexpr int MT = (S + 15) / 16;
+    static constexpr int NT = S / 8;
+    double d[MT][NT][4];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) d[m][n][e] = 0.0;
+    }
+    // write this warp's partial into scratch[warp][S*S] (row-major)
+    __device__ __forceinline__ void spill(double* dst, int g, int t) const {
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                const int r0 = 16 * m + g, c0 = 8 * n + 2 * t;
+                dst[r0 * S + c0] = d[m][n][0];
+                dst[r0 * S + c0 + 1] = d[m][n][1];
+                if (r0 + 8 < S) {
+                    dst[(r0 + 8) * S + c0] = d[m][n][2];
+                    dst[(r0 + 8) * S + c0 + 1] = d[m][n][3];
+                }
+            }
+    }
+};
+
+// sum per-warp matrices in warp order -> out[S*S]
+template <int S>
+__device__ __forceinline__ void cta_sum_mat(const double* scratch, double* out) {
+    constexpr int BS = CtaShape<S>::BS, NW = CtaShape<S>::NW;
+    __syncthreads();
+    for (int e = threadIdx.x; e < S * S; e += BS) {
+        double s = scratch[e];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) s += scratch[w * S * S + e];
+        out[e] = s;
+    }
+    __syncthreads();
+}
+
+// per-lane column partials v[nt][e] for columns 8nt+2t+e -> out[S] (warp order)
+template <int S>
+__device__ __forceinline__ void cta_sum_vec(double (&v)[S / 8][2], double* scratch, double* out,
+                                            int warp, int lane) {
+    constexpr int BS = CtaShape<S>::BS, NW = CtaShape<S>::NW;
+#pragma unroll
+    for (int n = 0; n < S / 8; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            double x = v[n][e];
+            x += __shfl_xor_sync(0xffffffffu, x, 4);
+            x += __shfl_xor_sync(0xffffffffu, x, 8);
+            x += __shfl_xor_sync(0xffffffffu, x, 16);
+            if (lane < 4) scratch[warp * S + 8 * n + 2 * lane + e] = x;
+        }
+    __syncthreads();
+    for (int e = threadIdx.x; e < S; e += BS) {
+        double s = scratch[e];
+        for (int w = 1; w < NW; ++w) s += scratch[w * S + e];
+        out[e] = s;
+    }
+    __syncthreads();
+}
+
+template <int BS>
+__device__ void grid_reduce(cg::grid_group& grid, double* __restrict__ part,
+                            double* __restrict__ redg, const double* src, int E, double* dst) {
+    constexpr int NW = BS / 32;
+    const int b = blockIdx.x, NB = gridDim.x;
+    for (int e = threadIdx.x; e < E; e += BS) part[(int64_t)b * E + e] = src[e];
+    grid.sync();
+    const int e0 = (int)((int64_t)E * b / NB), e1 = (int)((int64_t)E * (b + 1) / NB);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int e = e0 + warp; e < e1; e += NW) {
+        double s = 0.0;
+        for (int l = lane; l < NB; l += 32) s += __ldcg(part + (int64_t)l * E + e);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) __stcg(redg + e, s);
+    }
+    grid.sync();
+    for (int e = threadIdx.x; e < E; e += BS) dst[e] = __ldcg(redg + e);
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// small solves (identical in every CTA)
+// ---------------------------------------------------------------------------
+template <int S>
+__device__ void build_index(Sm<S>& sm) {
+    if (threadIdx.x == 0) {
+        int k = 0;
+        for (int q = 0; q < S; ++q)
+            if (sm.act[q]) sm.idx[k++] = q;
+        sm.sa = k;
+    }
+    __syncthreads();
+}
+
+// out = M^+ RHS on the active block (zero rows/columns elsewhere), the
+// semantics of PivotedCholesky(M).solve(RHS) (solvers.cpp:347-414): diagonal
+// pivoting on the largest remaining Schur-complement diagonal, rank cutoff
+// max(max_diag * s * eps, DBL_MIN), directions beyond the numerical rank get
+// zero coefficients. Computed as Gauss-Jordan on [M | RHS] with that pivot
+// sequence (the trailing block of Gauss-Jordan IS the Cholesky Schur
+// complement, so pivots and rank decisions coincide): one barrier per pivot,
+// the pivot search done redundantly by every warp (no broadcast barrier).
+// Warp-wide argmax of non-negative doubles through their IEEE bit patterns
+// (monotone for x >= 0). The low 6 bits of the pattern are replaced by
+// (63 - index), so two integer REDUX steps return both the winner and (up to
+// the 2^-46 relative truncation) its value; exact ties keep the lowest index,
+// as the reference's strict '>' scan does. key = 0 excludes an entry.
+__device__ __forceinline__ unsigned long long pivot_key(double v, int idx) {
+    return v > 0.0 ? (((unsigned long long)__double_as_longlong(v) & ~63ull) |
+                      (unsigned long long)(63 - idx))
+                   : 0ull;
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long key) {
+    const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+    const unsigned hi = __reduce_max_sync(0xffffffffu, khi);
+    const unsigned lo = __reduce_max_sync(0xffffffffu, khi == hi ? klo : 0u);
+    return ((unsigned long long)hi << 32) | lo;
+}
+
+__device__ __forceinline__ unsigned long long pos_bits(double v) {
+    return v > 0.0 ? (unsigned long long)__double_as_longlong(v) : 0ull;
+}
+
+// out = M^+ RHS on the active block (zero rows/columns elsewhere), the
+// semantics of PivotedCholesky(M).solve(RHS) (solvers.cpp:347-414): diagonal
+// pivoting on the largest remaining Schur-complement diagonal, rank cutoff
+// max(max_diag * s * eps, DBL_MIN), directions beyond the numerical rank get
+// zero coefficients. Computed as Gauss-Jordan on [M | RHS] with that pivot
+// sequence (the trailing block of Gauss-Jordan IS the Cholesky Schur
+// complement, so pivots and rank decisions coincide). One barrier per pivot;
+// every warp redundantly tracks the Schur diagonal in registers and searches
+// the next pivot while the block update of the current one is in flight.
+template <int S, bool PROF = false>
+__device__ void small_solve(Sm<S>& sm, const double* M, const double* RHS, double* out) {
+    constexpr int BS = CtaShape<S>::BS;
+    long long* const pr = PROF ? g_ss_prof : nullptr;
+    auto stamp = [&](int k) {
+        if (PROF && threadIdx.x == 0) pr[k] = clock64();
+    };
+    auto wbar = []() { __syncthreads(); };
+    constexpr int LD = 2 * S;
+    constexpr int R = (S + 31) / 32;  // diagonal entries per lane (index lane + 32 r)
+    static_assert(R <= 2, "S <= 64");
+    const int sa = sm.sa;
+    double* aug = sm.aug;
+    unsigned long long donem = 0ull;  // compacted indices already used as pivots
+    const int lane = threadIdx.x & 31;
+    for (int e = threadIdx.x; e < sa * LD; e += BS) {
+        const int p = e / LD, q = e % LD;
+        double v = 0.0;
+        const int a = sm.idx[p];
+        if (q < sa) {
+            const int b = sm.idx[q];
+            v = a <= b ? M[a * S + b] : M[b * S + a];
+        } else if (q < 2 * sa) {
+            const int b = sm.idx[q - sa];
+            v = a <= b ? RHS[a * S + b] : RHS[b * S + a];
+        }
+        aug[p * LD + q] = v;
+    }
+    wbar();
+    double dg[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        dg[r] = i < sa ? aug[i * LD + i] : 0.0;
+    }
+    auto search = [&](unsigned long long excl) -> unsigned long long {
+        unsigned long long key = 0ull;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int i = lane + 32 * r;
+            const unsigned long long kk = (i < sa && !((excl >> i) & 1ull)) ? pivot_key(dg[r], i) : 0ull;
+            key = kk > key ? kk : key;
+        }
+        return warp_max_u64(key);
+    };
+    stamp(0);
+    unsigned long long best = search(0ull);
+    // max_diag of the active block (the reference clamps its scan at 0)
+    const int im = best ? 63 - (int)(best & 63ull) : -1;
+    const double maxd = im >= 0 ? aug[im * LD + im] : 0.0;
+    const double cutoff = fmax(maxd * sa * 2.220446049250313e-16, 2.2250738585072014e-308);
+    int rank = 0;
+    stamp(1);
+    while (best) {
+        const int p = 63 - (int)(best & 63ull);
+        // exact pivot value (the REDUX key is truncated in its low 6 bits)
+        double pv = __shfl_sync(0xffffffffu, dg[0], p & 31);
+        if (R > 1) {
+            const double pv1 = __shfl_sync(0xffffffffu, dg[R - 1], p & 31);
+            if (p >= 32) pv = pv1;
+        }
+        if (!(pv > cutoff)) break;  // uniform: beyond the numerical rank
+        const double rinv = __drcp_rn(pv);
+        donem |= 1ull << p;
+        // Schur diagonal after this pivot, with the arithmetic the block
+        // update applies to aug[i][i]; the next pivot is searched while the
+        // block update is in flight
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int i = lane + 32 * r;
+            if (i < sa && !((donem >> i) & 1ull))
+                dg[r] = fma(-(aug[i * LD + p] * rinv), aug[p * LD + i], dg[r]);
+        }
+        const unsigned long long nb = search(donem);
+        for (int e = threadIdx.x; e < sa * LD; e += BS) {
+            const int i = e / LD, q = e % LD;
+            if (i == p || q >= 2 * sa || (q < sa && ((donem >> q) & 1ull))) continue;
+            const double f = aug[i * LD + p] * rinv;
+            aug[i * LD + q] = fma(-f, aug[p * LD + q], aug[i * LD + q]);
+        }
+        ++rank;
+        wbar();
+        stamp(2 + rank);
+        best = nb;
+    }
+    for (int e = threadIdx.x; e < S * S; e += BS) out[e] = 0.0;
+    wbar();
+    for (int e = threadIdx.x; e < sa * sa; e += BS) {
+        const int pp = e / sa, q = e % sa;
+        if ((donem >> pp) & 1ull)
+            out[sm.idx[pp] * S + sm.idx[q]] = aug[pp * LD + sa + q] * __drcp_rn(aug[pp * LD + pp]);
+    }
+    if (threadIdx.x == 0) sm.rank = rank;
+    __syncthreads();
+    stamp(63);
+}
+
+// ---------------------------------------------------------------------------
+// phases
+// ---------------------------------------------------------------------------
+// phase 1: W = A P over the CTA's cells, Gram G += P^T W. Two 4-cell groups
+// per trip so their stencil loads are in flight together.
+template <int S>
+__device__ __forceinline__ void phase_spmm_gram(const Args& a, int64_t c0, int64_t c1, int warp,
+                                                int g, int t, GramAcc<S>& G) {
+    constexpr int CPL = S / 8;
+    constexpr int NW = CtaShape<S>::NW;
+    constexpr int U = 2;
+    const int64_t groups = (c1 - c0 + 3) / 4;
+    for (int64_t q0 = warp; q0 < groups; q0 += NW * U) {
+        double w[U][CPL], p[U][CPL];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = q0 + u * NW;
+            const int64_t cell = c0 + 4 * q + t;
+            if (q < groups && cell < c1) {
+                Coef k;
+                load_coef(a, cell, k);
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) w[u][c] = st_fma<S>(k, a.P, cell, g + 8 * c, p[u][c]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) w[u][c] = p[u][c] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = q0 + u * NW;
+            const int64_t cell = c0 + 4 * q + t;
+            if (q < groups && cell < c1) {
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) a.W[cell * S + g + 8 * c] = w[u][c];
+            }
+#pragma unroll
+            for (int m = 0; m < GramAcc<S>::MT; ++m) {
+                const double a0 = p[u][2 * m];
+                const double a1 = (2 * m + 1 < CPL) ? p[u][2 * m + 1] : 0.0;
+#pragma unroll
+                for (int n = 0; n < GramAcc<S>::NT; ++n) dmma(G.d[m][n], a0, a1, w[u][n]);
+            }
+        }
+    }
+}
+
+// A-fragment loads of a 16-cell tile: frag[ks][0] = V[base+g][4ks+t],
+// frag[ks][1] = V[base+g+8][4ks+t]; rows beyond c1 read as 0.
+template <int S>
+__device__ __forceinline__ void load_afrag(const double* __restrict__ V, int64_t base, int64_t c1,
+                                           int g, int t, double (&f)[S / 4][2], double sign) {
+    const bool v0 = base + g < c1, v1 = base + g + 8 < c1;
+#pragma unroll
+    for (int ks = 0; ks < S / 4; ++ks) {
+        f[ks][0] = v0 ? sign * V[(base + g) * S + 4 * ks + t] : 0.0;
+        f[ks][1] = v1 ? sign * V[(base + g + 8) * S + 4 * ks + t] : 0.0;
+    }
+}
+
+// C-layout tile load/store: c[nt] = {V[r0][8nt+2t], V[r0][..+1], V[r1][8nt+2t], V[r1][..+1]}
+template <int S>
+__device__ __forceinline__ void load_ctile(const double* __restrict__ V, int64_t base, int64_t c1,
+                                           int g, int t, double (&c)[S / 8][4]) {
+    const bool v0 = base + g < c1, v1 = base + g + 8 < c1;
+#pragma unroll
+    for (int n = 0; n < S / 8; ++n) {
+        double2 x0 = v0 ? *reinterpret_cast<const double2*>(V + (base + g) * S + 8 * n + 2 * t)
+                        : make_double2(0.0, 0.0);
+        double2 x1 = v1 ? *reinterpret_cast<const double2*>(V + (base + g + 8) * S + 8 * n + 2 * t)
+                        : make_double2(0.0, 0.0);
+        c[n][0] = x0.x;
+        c[n][1] = x0.y;
+        c[n][2] = x1.x;
+        c[n][3] = x1.y;
+    }
+}
+
+template <int S>
+__device__ __forceinline__ void store_ctile(double* __restrict__ V, int64_t base, int64_t c1,
+                                            int g, int t, const double (&c)[S / 8][4]) {
+    const bool v0 = base + g < c1, v1 = base + g + 8 < c1;
+#pragma unroll
+    for (int n = 0; n < S / 8; ++n) {
+        if (v0)
+            *reinterpret_cast<double2*>(V + (base + g) * S + 8 * n + 2 * t) =
+                make_double2(c[n][0], c[n][1]);
+        if (v1)
+            *reinterpret_cast<double2*>(V + (base + g + 8) * S + 8 * n + 2 * t) =
+                make_double2(c[n][2], c[n][3]);
+    }
+}
+
+// Gram of two C-layout tiles through a warp-private transpose:
+// G += Rt^T Zt over the tile's 16 cells.
+template <int S>
+__device__ __forceinline__ void tile_gram(double* tr, double* tz, const double (&r)[S / 8][4],
+                                          const double (&z)[S / 8][4], int g, int t,
+                                          GramAcc<S>& G) {
+#pragma unroll
+    for (int n = 0; n < S / 8; ++n) {
+        const int col = 8 * n + 2 * t;
+        tr[g * S + col] = r[n][0];
+        tr[g * S + col + 1] = r[n][1];
+        tr[(g + 8) * S + col] = r[n][2];
+        tr[(g + 8) * S + col + 1] = r[n][3];
+        tz[g * S + col] = z[n][0];
+        tz[g * S + col + 1] = z[n][1];
+        tz[(g + 8) * S + col] = z[n][2];
+        tz[(g + 8) * S + col + 1] = z[n][3];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+        const int cell = 4 * kk + t;
+#pragma unroll
+        for (int m = 0; m < GramAcc<S>::MT; ++m) {
+            const double a0 = tr[cell * S + 16 * m + g];
+            const double a1 = (16 * m + 8 + g < S) ? tr[cell * S + 16 * m + 8 + g] : 0.0;
+#pragma unroll
+            for (int n = 0; n < GramAcc<S>::NT; ++n)
+                dmma(G.d[m][n], a0, a1, tz[cell * S + 8 * n + g]);
+        }
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ double dinv_at(const Args& a, int64_t c, int64_t c1, bool jac) {
+    return (jac && c < c1) ? a.dinv[c] : 1.0;
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+template <int S>
+__global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args a) {
+    constexpr int BS = CtaShape<S>::BS, NW = CtaShape<S>::NW;
+    constexpr int NT = S / 8;
+    constexpr int KS = S / 4;
+    constexpr int E = S * S + S;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Sm<S>& sm = *reinterpret_cast<Sm<S>*>(smem_raw);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int NB = gridDim.x, b = blockIdx.x;
+    // CTA ranges in whole 16-cell tiles (the last CTA takes the ragged end)
+    const int64_t ntiles = (a.n + 15) / 16;
+    const int64_t c0 = 16 * (ntiles * b / NB);
+    const int64_t c1 = b == NB - 1 ? a.n : 16 * (ntiles * (b + 1) / NB);
+    const bool jac = a.precond != 0;
+    const bool prof = a.prof != nullptr && b == 0 && tid == 0;
+    double* tr = sm.tileR[warp];
+    double* tz = sm.tileZ[warp];
+
+    GramAcc<S> G;
+    int64_t matvecs = 0;
+    int iters = 0;
+
+    // ---- init: X = 0, R = B, Z = D^-1 R, P = Z, bnorm, S_old = R^T Z
+    {
+        G.zero();
+        double bn[NT][2] = {};
+        for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
+            double r[NT][4], z[NT][4], zero[NT][4];
+            load_ctile<S>(a.B, base, c1, g, t, r);
+            const double d0 = dinv_at(a, base + g, c1, jac), d1 = dinv_at(a, base + g + 8, c1, jac);
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                z[n][0] = d0 * r[n][0];
+                z[n][1] = d0 * r[n][1];
+                z[n][2] = d1 * r[n][2];
+                z[n][3] = d1 * r[n][3];
+                bn[n][0] += r[n][0] * r[n][0] + r[n][2] * r[n][2];
+                bn[n][1] += r[n][1] * r[n][1] + r[n][3] * r[n][3];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) zero[n][e] = 0.0;
+            }
+            store_ctile<S>(a.X, base, c1, g, t, zero);
+            store_ctile<S>(a.R, base, c1, g, t, r);
+            store_ctile<S>(a.P, base, c1, g, t, z);
+            tile_gram<S>(tr, tz, r, z, g, t, G);
+        }
+        G.spill(sm.scratch + warp * S * S, g, t);
+        cta_sum_mat<S>(sm.scratch, sm.aug);
+        cta_sum_vec<S>(bn, sm.scratch, sm.aug + S * S, warp, lane);
+        grid_reduce<BS>(grid, a.part, a.red, sm.aug, E, sm.aug + E);
+        for (int e = tid; e < S * S; e += BS) sm.s_old[e] = sm.aug[E + e];
+        if (tid < S) {
+            const double bnv = sqrt(sm.aug[E + S * S + tid]);
+            sm.bnorm[tid] = bnv;
+            sm.act[tid] = bnv != 0.0;
+            sm.conv[tid] = bnv == 0.0;
+            sm.fres[tid] = 0.0;
+        }
+        __syncthreads();
+        build_index<S>(sm);
+    }
+
+    for (int m = 1; m <= a.max_iter && sm.sa > 0; ++m) {
+        long long* pm = (prof && m <= PROF_ITERS) ? a.prof + (m - 1) * PROF_MARKS : nullptr;
+        if (pm) pm[0] = gtimer();
+        // ---- phase 1: W = A P, G = P^T W
+        G.zero();
+        phase_spmm_gram<S>(a, c0, c1, warp, g, t, G);
+        G.spill(sm.scratch + warp * S * S, g, t);
+        cta_sum_mat<S>(sm.scratch, sm.aug);
+        if (pm) pm[1] = gtimer();
+        grid_reduce<BS>(grid, a.part, a.red, sm.aug, S * S, sm.mat);
+        if (pm) pm[2] = gtimer();
+        matvecs += sm.sa;
+        small_solve<S>(sm, sm.mat, sm.s_old, sm.coef);  // alpha
+        if (pm) pm[3] = gtimer();
+
+        // ---- phase 2: X += P alpha, R -= W alpha, rr, Z, S_new = R^T Z
+        G.zero();
+        double rr[NT][2] = {};
+        for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
+            double pa[KS][2], wa[KS][2], x[NT][4], r[NT][4];
+            load_afrag<S>(a.P, base, c1, g, t, pa, 1.0);
+            load_afrag<S>(a.W, base, c1, g, t, wa, -1.0);
+            load_ctile<S>(a.X, base, c1, g, t, x);
+            load_ctile<S>(a.R, base, c1, g, t, r);
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+                    const double bb = sm.coef[(4 * ks + t) * S + 8 * n + g];
+                    dmma(x[n], pa[ks][0], pa[ks][1], bb);
+                    dmma(r[n], wa[ks][0], wa[ks][1], bb);
+                }
+            store_ctile<S>(a.X, base, c1, g, t, x);
+            store_ctile<S>(a.R, base, c1, g, t, r);
+            const double d0 = dinv_at(a, base + g, c1, jac), d1 = dinv_at(a, base + g + 8, c1, jac);
+            double z[NT][4];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                rr[n][0] += r[n][0] * r[n][0] + r[n][2] * r[n][2];
+                rr[n][1] += r[n][1] * r[n][1] + r[n][3] * r[n][3];
+                z[n][0] = d0 * r[n][0];
+                z[n][1] = d0 * r[n][1];
+                z[n][2] = d1 * r[n][2];
+                z[n][3] = d1 * r[n][3];
+            }
+            tile_gram<S>(tr, tz, r, z, g, t, G);
+        }
+        G.spill(sm.scratch + warp * S * S, g, t);
+        cta_sum_mat<S>(sm.scratch, sm.aug);
+        cta_sum_vec<S>(rr, sm.scratch, sm.aug + S * S, warp, lane);
+        if (pm) pm[4] = gtimer();
+        grid_reduce<BS>(grid, a.part, a.red, sm.aug, E, sm.aug + E);
+        for (int e = tid; e < S * S; e += BS) sm.mat[e] = sm.aug[E + e];  // S_new
+        if (tid < S) sm.vec[tid] = sm.aug[E + S * S + tid];              // rr
+        __syncthreads();
+        iters = m;
+        if (pm) pm[5] = gtimer();
+
+        // ---- convergence control (solvers.cpp:582-634)
+        if (tid < S) sm.vflag[tid] = sm.act[tid] && (sqrt(sm.vec[tid]) / sm.bnorm[tid] <= a.tol);
+        __syncthreads();
+        int nver = 0;
+#pragma unroll
+        for (int q = 0; q < S; ++q) nver += sm.vflag[q];
+        bool restart = false;
+        if (nver > 0) {
+            double rs[NT][2] = {};
+            for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t cell = base + g + 8 * h;
+                    if (cell >= c1) continue;
+                    Coef k;
+                    load_coef(a, cell, k);
+#pragma unroll
+                    for (int n = 0; n < NT; ++n)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int col = 8 * n + 2 * t + e;
+                            const double rv = a.B[cell * S + col] - st_muladd<S>(k, a.X, cell, col);
+                            rs[n][e] += rv * rv;
+                        }
+                }
+            }
+            cta_sum_vec<S>(rs, sm.scratch, sm.aug, warp, lane);
+            grid_reduce<BS>(grid, a.part, a.red, sm.aug, S, sm.aug + S);
+            matvecs += nver;
+            if (tid == 0) {
+                sm.fail = 0;
+                for (int q = 0; q < S; ++q) {
+                    if (!sm.vflag[q]) continue;
+                    const double rt = sqrt(sm.aug[S + q]) / sm.bnorm[q];
+                    if (rt <= a.tol) {
+                        sm.act[q] = 0;
+                        sm.conv[q] = 1;
+                        sm.fres[q] = rt;
+                    } else {
+                        sm.fail = 2;
+                    }
+                }
+            }
+            __syncthreads();
+            restart = sm.fail == 2;
+            build_index<S>(sm);
+            if (sm.sa == 0) break;
+        }
+        if (restart) {
+            // R = B - A X, Z, P = Z, S_old = R^T Z (solvers.cpp:616-634)
+            G.zero();
+            for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
+                double r[NT][4], z[NT][4];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t cell = base + g + 8 * h;
+                    const bool v = cell < c1;
+                    Coef k;
+                    if (v) load_coef(a, cell, k);
+                    const double di = dinv_at(a, cell, c1, jac);
+#pragma unroll
+                    for (int n = 0; n < NT; ++n)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int col = 8 * n + 2 * t + e;
+                            double dummy;
+                            const double rv =
+                                v ? a.B[cell * S + col] - st_fma<S>(k, a.X, cell, col, dummy) : 0.0;
+                            r[n][2 * h + e] = rv;
+                            z[n][2 * h + e] = di * rv;
+                        }
+                }
+                store_ctile<S>(a.R, base, c1, g, t, r);
+                store_ctile<S>(a.P, base, c1, g, t, z);
+                tile_gram<S>(tr, tz, r, z, g, t, G);
+            }
+            G.spill(sm.scratch + warp * S * S, g, t);
+            cta_sum_mat<S>(sm.scratch, sm.aug);
+            grid_reduce<BS>(grid, a.part, a.red, sm.aug, S * S, sm.s_old);
+            matvecs += sm.sa;
+            continue;
+        }
+
+        // ---- phase 3: beta = S_old^+ S_new, S_old = S_new, P = Z + P beta
+        small_solve<S>(sm, sm.s_old, sm.mat, sm.coef);
+        for (int e = tid; e < S * S; e += BS) sm.s_old[e] = sm.mat[e];
+        if (pm) pm[6] = gtimer();
+        for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
+            double pa[KS][2], p[NT][4];
+            load_afrag<S>(a.P, base, c1, g, t, pa, 1.0);
+            load_ctile<S>(a.R, base, c1, g, t, p);
+            const double d0 = dinv_at(a, base + g, c1, jac), d1 = dinv_at(a, base + g + 8, c1, jac);
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                p[n][0] *= d0;
+                p[n][1] *= d0;
+                p[n][2] *= d1;
+                p[n][3] *= d1;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks)
+                    dmma(p[n], pa[ks][0], pa[ks][1], sm.coef[(4 * ks + t) * S + 8 * n + g]);
+            }
+            store_ctile<S>(a.P, base, c1, g, t, p);
+        }
+        grid.sync();
+        if (pm) pm[7] = gtimer();
+    }
+
+    // ---- exit: honest residuals for still-active columns (:655-661)
+    if (sm.sa > 0) {
+        double rs[NT][2] = {};
+        for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t cell = base + g + 8 * h;
+                if (cell >= c1) continue;
+                Coef k;
+                load_coef(a, cell, k);
+#pragma unroll
+                for (int n = 0; n < NT; ++n)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int col = 8 * n + 2 * t + e;
+                        const double rv = a.B[cell * S + col] - st_muladd<S>(k, a.X, cell, col);
+                        rs[n][e] += rv * rv;
+                    }
+            }
+        }
+        cta_sum_vec<S>(rs, sm.scratch, sm.aug, warp, lane);
+        grid_reduce<BS>(grid, a.part, a.red, sm.aug, S, sm.aug + S);
+        matvecs += sm.sa;
+        if (tid < S && sm.act[tid]) {
+            const double rt = sqrt(sm.aug[S + tid]) / sm.bnorm[tid];
+            sm.fres[tid] = rt;
+            sm.conv[tid] = rt <= a.tol;
+        }
+        __syncthreads();
+    }
+    if (b == 0 && tid == 0) {
+        a.rep->iterations = iters;
+        a.rep->matvecs = matvecs;
+        for (int q = 0; q < S; ++q) {
+            a.rep->final_res[q] = sm.fres[q];
+            a.rep->converged[q] = (char)sm.conv[q];
+        }
+    }
+}
+
+template <int S>
+bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
+                   const bk_solver_cfg* cfg, double* X, bk::CgReport* rep) {
+    using namespace bk;
+    const int64_t n = op->n;
+    const size_t vec_bytes = (size_t)n * S * sizeof(double);
+    auto kern = block_cg_dmma_kernel<S>;
+    const size_t smem = sizeof(Sm<S>);
+    BK_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+    int occ = 0;
+    constexpr int BS = CtaShape<S>::BS;
+    BK_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BS, smem));
+    if (occ < 1) return fail(ctx, BK_INTERNAL, "block_cg: DMMA kernel cannot be resident");
+    occ = 1;  // one CTA per SM (see CtaShape)
+    if (const char* e = getenv("BK_CG_CTAS_PER_SM")) occ = atoi(e) < occ ? atoi(e) : occ;
+    int64_t nb = (int64_t)occ * ctx->num_sms;
+    const int64_t ntiles = (n + 15) / 16;
+    const int64_t min_tiles = 2;
+    if (nb * min_tiles > ntiles) nb = (ntiles + min_tiles - 1) / min_tiles;
+    if (nb < 1) nb = 1;
+    const int E = S * S + S;
+
+    void *pB, *pX, *pR, *pP, *pW, *pPart, *pRed, *pRep;
+    bk_status st;
+    const bool padded = s != S;
+    if ((st = workspace(ctx, kSlotCgR, vec_bytes, &pR)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotCgP, vec_bytes, &pP)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotCgW, vec_bytes, &pW)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotCgPart, (size_t)nb * E * sizeof(double), &pPart)) != BK_OK)
+        return st;
+    if ((st = workspace(ctx, kSlotCgRed, (size_t)E * sizeof(double), &pRed)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotCgCtl,
+                        sizeof(CgReport) + PROF_ITERS * PROF_MARKS * sizeof(long long), &pRep)) !=
+        BK_OK)
+        return st;
+    if (padded) {
+        if ((st = workspace(ctx, kSlotCgB, vec_bytes, &pB)) != BK_OK) return st;
+        if ((st = workspace(ctx, kSlotCgX, vec_bytes, &pX)) != BK_OK) return st;
+        BK_CUDA_TRY(ctx, launch_pad_cols(ctx, B, s, (double*)pB, S, n));
+    } else {
+        pB = const_cast<double*>(B);
+        pX = X;
+    }
+    Args a;
+    a.nx = op->nx;
+    a.ny = op->ny;
+    a.nz = op->nz;
+    a.n = n;
+    a.diag = op->diag;
+    a.cx = op->cx;
+    a.cy = op->cy;
+    a.cz = op->cz;
+    a.dinv = op->dinv;
+    a.B = (const double*)pB;
+    a.X = (double*)pX;
+    a.R = (double*)pR;
+    a.P = (double*)pP;
+    a.W = (double*)pW;
+    a.part = (double*)pPart;
+    a.red = (double*)pRed;
+    a.tol = cfg->rel_tol;
+    a.max_iter = cfg->max_iter;
+    a.precond = cfg->precond;
+    a.rep = (CgReport*)pRep;
+    const bool want_prof = getenv("BK_CG_PROFILE") != nullptr;
+    a.prof = want_prof ? (long long*)((char*)pRep + sizeof(CgReport)) : nullptr;
+    if (want_prof)
+        BK_CUDA_TRY(ctx, cudaMemsetAsync(a.prof, 0, PROF_ITERS * PROF_MARKS * sizeof(long long),
+                                         ctx->stream));
+    void* args[] = {&a};
+    BK_CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)nb), dim3(BS),
+                                                 args, smem, ctx->stream));
+    ++ctx->launches;
+    if (padded) BK_CUDA_TRY(ctx, launch_pad_cols(ctx, (const double*)pX, S, X, s, n));
+    BK_CUDA_TRY(ctx, cudaMemcpyAsync(rep, pRep, sizeof(CgReport), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (want_prof) {
+        std::vector<long long> pr(PROF_ITERS * PROF_MARKS);
+        cudaMemcpy(pr.data(), a.prof, pr.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+        // mean phase durations over the recorded iterations (ns)
+        double acc[PROF_MARKS] = {};
+        int cnt = 0;
+        for (int i = 1; i < PROF_ITERS; ++i) {
+            const long long* r = pr.data() + i * PROF_MARKS;
+            if (!r[0] || !r[7]) continue;
+            for (int k = 1; k < PROF_MARKS; ++k) acc[k] += (double)(r[k] - r[k - 1]);
+            acc[0] += (double)(pr[(i + 1) * PROF_MARKS] ? pr[(i + 1) * PROF_MARKS] - r[7] : 0);
+            ++cnt;
+        }
+        if (cnt)
+            fprintf(stderr,
+                    "[bk_cg_profile S=%d nb=%lld] per-iteration ns: phase1 %.0f | reduceG %.0f | "
+                    "solve_a %.0f | phase2 %.0f | reduceS %.0f | control+solve_b %.0f | "
+                    "phase3+sync %.0f (over %d iterations)\n",
+                    S, (long long)nb, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
+                    acc[5] / cnt, acc[6] / cnt, acc[7] / cnt, cnt);
+    }
+    return BK_OK;
+}
+
+}  // namespace
+
+namespace bk {
+
+bk_status block_cg_device(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
+                          const bk_solver_cfg* cfg, double* X, CgReport* rep) {
+    if (getenv("BK_CG_GENERIC")) return block_cg_generic(ctx, op, B, s, cfg, X, rep);
+    if (s <= 8) return run_dmma<8>(ctx, op, B, s, cfg, X, rep);
+    if (s <= 16) return run_dmma<16>(ctx, op, B, s, cfg, X, rep);
+    if (s <= 32) return run_dmma<32>(ctx, op, B, s, cfg, X, rep);
+    return block_cg_generic(ctx, op, B, s, cfg, X, rep);
+}
+
+}  // namespace bk
+
+// ---------------------------------------------------------------------------
+// debug harness: cycles of the s x s solve in isolation (scripts/ only)
+// ---------------------------------------------------------------------------
+namespace {
+template <int S>
+__global__ void __launch_bounds__(CtaShape<S>::BS, 1) small_solve_bench_kernel(int reps, long long* out,
+                                                                             double* res) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Sm<S>& sm = *reinterpret_cast<Sm<S>*>(smem_raw);
+    constexpr int BS = CtaShape<S>::BS;
+    for (int e = threadIdx.x; e < S * S; e += BS) {
+        const int i = e / S, j = e % S;
+        // SPD with a wide diagonal scale spread, like G near convergence
+        sm.mat[e] = (i == j ? 1.0 : 0.01 / (1 + i + j)) * exp(-0.5 * (i + j));
+        sm.s_old[e] = (i == j ? 2.0 : 0.1) * exp(-0.25 * (i + j));
+    }
+    if (threadIdx.x < S) sm.act[threadIdx.x] = 1;
+    __syncthreads();
+    build_index<S>(sm);
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) small_solve<S>(sm, sm.mat, sm.s_old, sm.coef);
+    long long t1 = clock64();
+    if (threadIdx.x == 0) g_ss_prof = out + 2;
+    __syncthreads();
+    if (threadIdx.x == 0) out[2 + 62] = clock64();
+    small_solve<S, true>(sm, sm.mat, sm.s_old, sm.coef);
+    if (threadIdx.x == 0) {
+        out[0] = (t1 - t0) / reps;
+        out[1] = sm.rank;
+    }
+    for (int e = threadIdx.x; e < S * S; e += BS) res[e] = sm.coef[e];
+}
+}  // namespace
+
+extern "C" int bk_debug_small_solve_cycles(int s, int reps, long long* cycles, int* rank,
+                                           double* coef) {
+    long long* d;
+    double* r;
+    cudaMalloc(&d, 80 * 8);
+    cudaMemset(d, 0, 80 * 8);
+    cudaMalloc(&r, 64 * 64 * 8);
+    int err = 0;
+    auto run = [&](auto kern, size_t smem, int bs) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<1, bs, smem>>>(reps, d, r);
+        err = (int)cudaDeviceSynchronize();
+    };
+    if (s == 8) run(small_solve_bench_kernel<8>, sizeof(Sm<8>), CtaShape<8>::BS);
+    else if (s == 16) run(small_solve_bench_kernel<16>, sizeof(Sm<16>), CtaShape<16>::BS);
+    else run(small_solve_bench_kernel<32>, sizeof(Sm<32>), CtaShape<32>::BS);
+    long long h[80] = {0};
+    cudaMemcpy(h, d, 80 * 8, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "small_solve<%d> stamps (cycles from start): setup %lld, first search %lld;", s,
+            h[2] - h[64], h[3] - h[64]);
+    for (int k = 1; k <= s; ++k) fprintf(stderr, " %lld", h[4 + k] ? h[4 + k] - h[64] : -1);
+    fprintf(stderr, "; end %lld\n", h[65] - h[64]);
+    cudaMemcpy(coef, r, (size_t)s * s * 8, cudaMemcpyDeviceToHost);
+    *cycles = h[0];
+    *rank = (int)h[1];
+    cudaFree(d);
+    cudaFree(r);
+    return err;
+}

@@ -49,41 +49,48 @@ __device__ __forceinline__ double div_rn(double x, double v, double r) {
     return fma(e, r, q0);
 }
 
+// T for one z-plane of the tile + halo into buf[q * HC + h] (sample-major, so
+// the stencil's neighbour reads and these stores are bank-conflict free).
 template <int S, int NS>
 __device__ __forceinline__ void form_plane(const ActArgs& a, int x0, int y0, int z,
                                            const double* __restrict__ Cs, double* __restrict__ buf) {
     constexpr int H = NS / 2;
     const int64_t plane = (int64_t)a.nx * a.ny;
     for (int it = threadIdx.x; it < HC * 2; it += NT) {
-        const int h = it >> 1, half = it & 1;
+        const int h = it % HC, half = it / HC;
         const int gx = x0 - 1 + h % HX, gy = y0 - 1 + h / HX;
         double t[H];
         if (gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny) {
             const double* xr = a.X + (gx + (int64_t)a.nx * gy + plane * z) * S;
             const double* cs = Cs + half * H;
-            const double x0v = xr[0];
+            const double2 x01 = *reinterpret_cast<const double2*>(xr);
 #pragma unroll
-            for (int q = 0; q < H; ++q) t[q] = x0v * cs[q];
+            for (int q = 0; q < H; ++q) t[q] = x01.x * cs[q];
+#pragma unroll
+            for (int q = 0; q < H; ++q) t[q] = fma(cs[NS + q], x01.y, t[q]);
 #pragma unroll 4
-            for (int k = 1; k < S; ++k) {
-                const double xv = xr[k];
+            for (int k = 2; k < S; k += 2) {
+                const double2 xv = *reinterpret_cast<const double2*>(xr + k);
 #pragma unroll
-                for (int q = 0; q < H; ++q) t[q] = fma(cs[k * NS + q], xv, t[q]);
+                for (int q = 0; q < H; ++q) t[q] = fma(cs[k * NS + q], xv.x, t[q]);
+#pragma unroll
+                for (int q = 0; q < H; ++q) t[q] = fma(cs[(k + 1) * NS + q], xv.y, t[q]);
             }
         } else {
 #pragma unroll
             for (int q = 0; q < H; ++q) t[q] = 0.0;
         }
 #pragma unroll
-        for (int q = 0; q < H; ++q) buf[h * NS + half * H + q] = t[q];
+        for (int q = 0; q < H; ++q) buf[(half * H + q) * HC + h] = t[q];
     }
 }
 
 template <int S, int NS>
-__global__ void __launch_bounds__(NT) combine_action_kernel(ActArgs a) {
+__global__ void __launch_bounds__(NT, 2) combine_action_kernel(ActArgs a) {
     extern __shared__ __align__(16) double sm[];
     double* Cs = sm;                 // S x NS
-    double* ring = sm + S * NS;      // 3 x HC x NS
+    double* ring = sm + S * NS;      // min(nz,3) x NS x HC
+    const int nring = a.nz < 3 ? a.nz : 3;
     const int tilesx = (a.nx + TX - 1) / TX;
     const int tile = blockIdx.x;
     const int x0 = (tile % tilesx) * TX, y0 = (tile / tilesx) * TY;
@@ -109,9 +116,9 @@ __global__ void __launch_bounds__(NT) combine_action_kernel(ActArgs a) {
     if (a.nz > 1) form_plane<S, NS>(a, x0, y0, 1, Cs, ring + HC * NS);
     __syncthreads();
     for (int z = 0; z < a.nz; ++z) {
-        const double* Tm = ring + ((z + 2) % 3) * HC * NS;
-        const double* T0 = ring + (z % 3) * HC * NS;
-        const double* Tp = ring + ((z + 1) % 3) * HC * NS;
+        const double* Tm = ring + ((z + nring - 1) % nring) * HC * NS;
+        const double* T0 = ring + (z % nring) * HC * NS;
+        const double* Tp = ring + ((z + 1) % nring) * HC * NS;
         if (inside) {
             const int64_t i = gx + (int64_t)a.nx * gy + plane * z;
             const double vol = a.volz[z];
@@ -128,14 +135,14 @@ __global__ void __launch_bounds__(NT) combine_action_kernel(ActArgs a) {
                 const int64_t j = j0 + q;
                 // y = A T in CSR order z-, y-, x-, diag, x+, y+, z+ (mul, add)
                 double y = 0.0;
-                if (z > 0) y = __dadd_rn(y, __dmul_rn(czm, Tm[h * NS + q]));
-                if (gy > 0) y = __dadd_rn(y, __dmul_rn(cym, T0[(h - HX) * NS + q]));
-                if (gx > 0) y = __dadd_rn(y, __dmul_rn(cxm, T0[(h - 1) * NS + q]));
-                const double tc = T0[h * NS + q];
+                if (z > 0) y = __dadd_rn(y, __dmul_rn(czm, Tm[q * HC + h]));
+                if (gy > 0) y = __dadd_rn(y, __dmul_rn(cym, T0[q * HC + h - HX]));
+                if (gx > 0) y = __dadd_rn(y, __dmul_rn(cxm, T0[q * HC + h - 1]));
+                const double tc = T0[q * HC + h];
                 y = __dadd_rn(y, __dmul_rn(di, tc));
-                if (gx < a.nx - 1) y = __dadd_rn(y, __dmul_rn(cxp, T0[(h + 1) * NS + q]));
-                if (gy < a.ny - 1) y = __dadd_rn(y, __dmul_rn(cyp, T0[(h + HX) * NS + q]));
-                if (z < a.nz - 1) y = __dadd_rn(y, __dmul_rn(czp, Tp[h * NS + q]));
+                if (gx < a.nx - 1) y = __dadd_rn(y, __dmul_rn(cxp, T0[q * HC + h + 1]));
+                if (gy < a.ny - 1) y = __dadd_rn(y, __dmul_rn(cyp, T0[q * HC + h + HX]));
+                if (z < a.nz - 1) y = __dadd_rn(y, __dmul_rn(czp, Tp[q * HC + h]));
                 const double qv = div_rn(__dsub_rn(y, gi), vol, rvol);
                 if (j < a.N) {
                     if (a.T) __stcs(a.T + j * a.n + i, tc);
@@ -230,7 +237,8 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
         if (st != BK_OK) return st;
         a.part = (double*)p;
     }
-    const size_t smem = (size_t)(S * NS + 3 * HC * NS) * sizeof(double);
+    const int nring = op->nz < 3 ? op->nz : 3;
+    const size_t smem = (size_t)(S * NS + nring * HC * NS) * sizeof(double);
     auto kern = combine_action_kernel<S, NS>;
     BK_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
