@@ -173,6 +173,23 @@ bk_status bk_generate_chip(bk_ctx* ctx, const bk_grid* grid, const double* k,
                            double* T, double* Q, double* resid, bk_solve_report* report,
                            bk_phase_timings* timings);
 
+/* Batched per-chip pipeline for many independent chips (BASELINE config 4):
+ * chip c runs bk_generate_chip on its own inputs. `streams` chips are in flight
+ * at once, each on its own stream, workspace and 1/streams of the SMs, so the
+ * latency-bound solves of different chips overlap. Per-chip arrays of
+ * pointers (host or device); T/Q/resid entries may be NULL. reports may be NULL
+ * (else n_chips entries whose residual arrays hold s values each). */
+bk_status bk_generate_batch(bk_ctx* ctx, int n_chips, const bk_grid* grids,
+                            const double* const* k, const bk_face* bc /* n_chips x 6 */,
+                            const double* const* Qbasis, int s, const double* const* C,
+                            int64_t N, const bk_solver_cfg* cfg, double* const* T,
+                            double* const* Q, double* const* resid, bk_solve_report* reports,
+                            int streams, bk_phase_timings* timings);
+
+/* Cap the number of CTAs (and thus SMs) one block-CG solve may use on ctx
+ * (0 = all SMs). */
+bk_status bk_set_cg_sm_budget(bk_ctx* ctx, int max_ctas);
+
 /* cg_error_bound(kappa, m, e0)    solvers.hpp:92, solvers.cpp:672-680 (host). */
 bk_status bk_cg_error_bound(double kappa, int m, double e0, double* out);
 

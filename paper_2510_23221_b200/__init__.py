@@ -41,7 +41,7 @@ import numpy as np
 __all__ = [
     "GridSpec", "Dirichlet", "Robin", "Adiabatic", "BoundarySpec", "SolverConfig",
     "SolveReport", "BlockCgResult", "PhaseTimings", "DiscreteOperator", "Context",
-    "assemble", "block_cg", "combine_action", "generate_chip", "rhs_from_power",
+    "assemble", "block_cg", "combine_action", "generate_chip", "generate_batch", "rhs_from_power",
     "power_from_rhs", "cg_error_bound", "derive_seed", "synth_chip", "library_path",
     "Error", "InvalidSpecError", "InvalidConfigError", "DimensionMismatchError",
     "NonPositiveConductivityError", "NonPositiveHtcError", "EmptyBasisError",
@@ -147,6 +147,10 @@ def _load():
         lib.bk_generate_chip.argtypes = [vp, C.POINTER(_Grid), dp, C.POINTER(_Face), dp, C.c_int,
                                          dp, C.c_int64, C.POINTER(_Cfg), dp, dp, dp,
                                          C.POINTER(_Report), C.POINTER(_Timings)]
+        lib.bk_generate_batch.argtypes = [vp, C.c_int, vp, vp, vp, vp, C.c_int, vp, C.c_int64,
+                                          C.POINTER(_Cfg), vp, vp, vp, vp, C.c_int,
+                                          C.POINTER(_Timings)]
+        lib.bk_set_cg_sm_budget.argtypes = [vp, C.c_int]
         lib.bk_cg_error_bound.argtypes = [C.c_double, C.c_int, C.c_double, C.POINTER(C.c_double)]
         lib.bk_derive_seed.argtypes = [C.c_uint64, C.c_char_p, C.c_uint64]
         lib.bk_derive_seed.restype = C.c_uint64
@@ -548,6 +552,76 @@ def generate_chip(grid: GridSpec, k, bc: BoundarySpec, q_basis, coef, cfg: Solve
     timings = PhaseTimings(tim.assemble_s, tim.basis_solve_s, tim.combine_action_s, tim.h2d_s,
                            tim.d2h_s, tim.total_s, tim.iterations_total, tim.matvecs_total)
     return t_out, q_out, resid_out, _report(s, rep, res, conv), timings
+
+
+def generate_batch(chips, cfg: SolverConfig, t_out=None, q_out=None, resid_out=None,
+                   streams: int = 8, ctx: Optional[Context] = None, check_converged: bool = True):
+    """Batched per-chip pipeline (BASELINE config 4): `chips` is a list of
+    ChipInputs (or dicts with grid, bc, k, q_basis, coef) sharing s and N.
+    `streams` chips are solved concurrently, each on 1/streams of the SMs.
+    Returns (T list, Q list, resid list, [SolveReport], PhaseTimings)."""
+    ctx = _ctx(ctx)
+    n = len(chips)
+    if n == 0:
+        return [], [], [], [], None
+    s = _cols(chips[0].q_basis)
+    N = int(chips[0].coef.shape[1])
+    grids = (_Grid * n)()
+    faces = (_Face * (6 * n))()
+    keep = []
+    for c, ch in enumerate(chips):
+        g, kd = ch.grid._c()
+        keep.append(kd)
+        grids[c] = g
+        fc = ch.bc._c()
+        for f in range(6):
+            faces[6 * c + f] = fc[f]
+        if _cols(ch.q_basis) != s or int(ch.coef.shape[1]) != N:
+            raise DimensionMismatchError("generate_batch: chips must share s and N")
+    def ptr_array(arrs):
+        out = (C.c_void_p * n)()
+        for i, a in enumerate(arrs):
+            p, kk = _ptr(a)
+            keep.append(kk)
+            out[i] = p.value if p is not None else None
+        return out
+    if t_out is None:
+        t_out = [np.empty((N, ch.grid.cell_count())) for ch in chips]
+    if q_out is None:
+        q_out = [np.empty((N, ch.grid.cell_count())) for ch in chips]
+    if resid_out is None:
+        resid_out = [np.empty(N) for _ in chips]
+    kp = ptr_array([ch.k for ch in chips])
+    qp = ptr_array([ch.q_basis for ch in chips])
+    cp = ptr_array([ch.coef for ch in chips])
+    tp = ptr_array(t_out)
+    qo = ptr_array(q_out)
+    rp = ptr_array(resid_out)
+    res = [np.zeros(s) for _ in chips]
+    conv = [np.zeros(s, np.int8) for _ in chips]
+    reps = (_Report * n)()
+    for c in range(n):
+        reps[c] = _Report(0, 0, 0.0, res[c].ctypes.data_as(C.c_void_p),
+                          conv[c].ctypes.data_as(C.c_void_p))
+    cfg_c = cfg._c()
+    tim = _Timings()
+    st = _load().bk_generate_batch(ctx.h, n, C.cast(grids, C.c_void_p), C.cast(kp, C.c_void_p),
+                                   C.cast(faces, C.c_void_p), C.cast(qp, C.c_void_p), s,
+                                   C.cast(cp, C.c_void_p), N, C.byref(cfg_c),
+                                   C.cast(tp, C.c_void_p), C.cast(qo, C.c_void_p),
+                                   C.cast(rp, C.c_void_p), C.cast(reps, C.c_void_p), streams,
+                                   C.byref(tim))
+    if st == 7 and not check_converged:
+        st = 0
+    _raise(st, ctx.h, "generate_batch")
+    reports = [_report(s, reps[c], res[c], conv[c]) for c in range(n)]
+    timings = PhaseTimings(tim.assemble_s, tim.basis_solve_s, tim.combine_action_s, tim.h2d_s,
+                           tim.d2h_s, tim.total_s, tim.iterations_total, tim.matvecs_total)
+    return t_out, q_out, resid_out, reports, timings
+
+
+def set_cg_sm_budget(ctx: Context, max_ctas: int) -> None:
+    _raise(_load().bk_set_cg_sm_budget(ctx.h, max_ctas), ctx.h, "set_cg_sm_budget")
 
 
 def cg_error_bound(kappa: float, m: int, e0: float) -> float:

@@ -5,7 +5,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <chrono>
 #include <new>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -257,6 +259,8 @@ bk_status bk_create(int device, bk_ctx** out) {
 
 void bk_destroy(bk_ctx* ctx) {
     if (!ctx) return;
+    for (bk_ctx* sub : ctx->subs) bk_destroy(sub);
+    ctx->subs.clear();
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (int i = 0; i < bk_ctx::kSlots; ++i) cudaFree(ctx->ws[i]);
@@ -283,7 +287,12 @@ bk_status bk_synchronize(bk_ctx* ctx) {
     return BK_OK;
 }
 
-int64_t bk_launch_count(const bk_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int64_t bk_launch_count(const bk_ctx* ctx) {
+    if (!ctx) return 0;
+    int64_t n = ctx->launches;
+    for (const bk_ctx* sub : ctx->subs) n += sub->launches;
+    return n;
+}
 
 bk_status bk_assemble(bk_ctx* ctx, const bk_grid* grid, const double* k, const bk_face bc[6],
                       bk_operator** out) {
@@ -519,6 +528,89 @@ bk_status bk_generate_chip(bk_ctx* ctx, const bk_grid* grid, const double* k, co
     for (int j = 0; j < s; ++j)
         if (!rep.converged[j])
             return fail(ctx, BK_NOT_CONVERGED, "basis solve did not reach tolerance");
+    return BK_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+bk_status bk_set_cg_sm_budget(bk_ctx* ctx, int max_ctas) {
+    if (!ctx || max_ctas < 0) return BK_INVALID_CONFIG;
+    ctx->cg_max_ctas = max_ctas;
+    return BK_OK;
+}
+
+bk_status bk_generate_batch(bk_ctx* ctx, int n_chips, const bk_grid* grids,
+                            const double* const* k, const bk_face* bc,
+                            const double* const* Qbasis, int s, const double* const* C,
+                            int64_t N, const bk_solver_cfg* cfg, double* const* T,
+                            double* const* Q, double* const* resid, bk_solve_report* reports,
+                            int streams, bk_phase_timings* timings) {
+    if (!ctx || n_chips < 0 || !grids || !k || !bc || !Qbasis || !C) return BK_INVALID_CONFIG;
+    if (streams < 1) streams = 1;
+    if (streams > n_chips && n_chips > 0) streams = n_chips;
+    cudaSetDevice(ctx->device);
+    // sub-contexts: own stream + workspace, an equal share of the SMs each
+    while ((int)ctx->subs.size() < streams) {
+        bk_ctx* sub = nullptr;
+        const bk_status st = bk_create(ctx->device, &sub);
+        if (st != BK_OK) return fail(ctx, st, "generate_batch: sub-context");
+        ctx->subs.push_back(sub);
+    }
+    const int share = ctx->num_sms / streams > 0 ? ctx->num_sms / streams : 1;
+    for (int w = 0; w < streams; ++w) ctx->subs[w]->cg_max_ctas = share;
+    std::vector<bk_status> st(streams, BK_OK);
+    std::vector<std::string> msg(streams);
+    std::vector<bk_phase_timings> tim(streams);
+    for (auto& t : tim) std::memset(&t, 0, sizeof(t));
+    const auto t0 = std::chrono::steady_clock::now();
+    auto worker = [&](int w) {
+        bk_ctx* sub = ctx->subs[w];
+        const int64_t launches0 = sub->launches;
+        for (int c = w; c < n_chips; c += streams) {
+            bk_phase_timings pt;
+            bk_solve_report* rep = reports ? &reports[c] : nullptr;
+            const bk_status r = bk_generate_chip(sub, &grids[c], k[c], bc + 6 * c, Qbasis[c], s,
+                                                 C[c], N, cfg, T ? T[c] : nullptr,
+                                                 Q ? Q[c] : nullptr, resid ? resid[c] : nullptr,
+                                                 rep, &pt);
+            if (r != BK_OK && st[w] == BK_OK) {
+                st[w] = r;
+                msg[w] = sub->err;
+                if (r != BK_NOT_CONVERGED) break;
+            }
+            tim[w].assemble_s += pt.assemble_s;
+            tim[w].basis_solve_s += pt.basis_solve_s;
+            tim[w].combine_action_s += pt.combine_action_s;
+            tim[w].h2d_s += pt.h2d_s;
+            tim[w].d2h_s += pt.d2h_s;
+            tim[w].iterations_total += pt.iterations_total;
+            tim[w].matvecs_total += pt.matvecs_total;
+        }
+        (void)launches0;
+    };
+    std::vector<std::thread> pool;
+    for (int w = 1; w < streams; ++w) pool.emplace_back(worker, w);
+    worker(0);
+    for (auto& th : pool) th.join();
+    const double wall =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (timings) {
+        std::memset(timings, 0, sizeof(*timings));
+        for (const auto& t : tim) {
+            timings->assemble_s += t.assemble_s;
+            timings->basis_solve_s += t.basis_solve_s;
+            timings->combine_action_s += t.combine_action_s;
+            timings->h2d_s += t.h2d_s;
+            timings->d2h_s += t.d2h_s;
+            timings->iterations_total += t.iterations_total;
+            timings->matvecs_total += t.matvecs_total;
+        }
+        timings->total_s = wall;
+    }
+    for (int w = 0; w < streams; ++w)
+        if (st[w] != BK_OK) return fail(ctx, st[w], msg[w]);
     return BK_OK;
 }
 

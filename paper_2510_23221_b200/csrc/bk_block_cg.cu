@@ -614,6 +614,7 @@ bk_status run_block_cg(bk_ctx* ctx, const bk_operator* op, const double* B, int 
     if (occ < 1) return fail(ctx, BK_INTERNAL, "block_cg kernel cannot be resident");
     occ = occ > 4 ? 4 : occ;
     int64_t nb = (int64_t)occ * ctx->num_sms;
+    if (ctx->cg_max_ctas > 0 && nb > ctx->cg_max_ctas) nb = ctx->cg_max_ctas;
     const int64_t min_cells = 2 * (BS / S);
     if (nb * min_cells > n) nb = (n + min_cells - 1) / min_cells;
     if (nb < 1) nb = 1;

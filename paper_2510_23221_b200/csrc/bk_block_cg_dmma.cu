@@ -831,8 +831,8 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
     BK_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BS, smem));
     if (occ < 1) return fail(ctx, BK_INTERNAL, "block_cg: DMMA kernel cannot be resident");
     occ = 1;  // one CTA per SM (see CtaShape)
-    if (const char* e = getenv("BK_CG_CTAS_PER_SM")) occ = atoi(e) < occ ? atoi(e) : occ;
     int64_t nb = (int64_t)occ * ctx->num_sms;
+    if (ctx->cg_max_ctas > 0 && nb > ctx->cg_max_ctas) nb = ctx->cg_max_ctas;
     const int64_t ntiles = (n + 15) / 16;
     const int64_t min_tiles = 2;
     if (nb * min_tiles > ntiles) nb = (ntiles + min_tiles - 1) / min_tiles;

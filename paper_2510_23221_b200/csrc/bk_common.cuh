@@ -31,6 +31,8 @@ struct bk_ctx {
     std::string err;
     int64_t launches = 0;
     bk_operator* scratch = nullptr;  // operator reused by bk_generate_chip
+    int cg_max_ctas = 0;             // 0 = every SM (see bk_set_cg_sm_budget)
+    std::vector<bk_ctx*> subs;       // per-stream sub-contexts of bk_generate_batch
     // grow-only device workspace slots
     static constexpr int kSlots = 24;
     void* ws[kSlots] = {};

@@ -314,3 +314,31 @@ def test_launch_counter_and_native_library_loaded(bk, ctx):
     assert ctx.launch_count > before
     maps = open("/proc/self/maps").read()
     assert os.path.basename(bk.library_path()) in maps
+
+
+def test_generate_batch_matches_per_chip(bk, ctx, oracle):
+    """Config 4 batch path: every chip's outputs equal its single-chip run
+    (bitwise: same kernels, same launch shape per stream count) and the oracle."""
+    chips = [bk.synth_chip(4, 32, 24, 4, 16, 8, chip_id=c) for c in range(5)]
+    for streams in (1, 2):
+        T, Q, R, reps, tim = bk.generate_batch(chips, cfg_jacobi(), streams=streams, ctx=ctx)
+        assert len(reps) == 5 and all(r.all_converged() for r in reps)
+        assert tim.total_s > 0 and tim.iterations_total == sum(r.iterations for r in reps)
+        sub = bk.Context(0)
+        bk.set_cg_sm_budget(sub, sub_budget(streams))
+        for c, ch in enumerate(chips):
+            T1, Q1, R1, rep1, _ = bk.generate_chip(ch.grid, ch.k, ch.bc, ch.q_basis, ch.coef,
+                                                   cfg_jacobi(), ctx=sub)
+            assert np.array_equal(T[c], T1) and np.array_equal(Q[c], Q1)
+    o = oracle.assemble(grid_tuple(chips[2].grid), chips[2].k, chips[2].bc.as_tuples(),
+                        dz=chips[2].grid.dz)
+    X, _ = oracle.block_cg(o, oracle.rhs_from_power(o, chips[2].q_basis), TOL, 100000, 1)
+    To, Qo, _ = oracle.combine_action(o, X, chips[2].coef)
+    assert rel_l2(T[2], To) <= PARITY and rel_l2(Q[2], Qo) <= PARITY
+
+
+def sub_budget(streams):
+    import torch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    return max(1, sms // streams)
