@@ -78,15 +78,25 @@ __device__ __forceinline__ long long gtimer() {
     return t;
 }
 
+// Shared-memory row strides chosen for conflict-free 64-bit fragment access:
+// S + 4 makes the DMMA fragment loads [(4k + t) * RS + 8n + g] hit 16 distinct
+// 8-byte bank slots per half-warp; the odd 2S + 1 makes the Gauss-Jordan
+// column walk aug[i][p] conflict-free.
+template <int S>
+struct Strides {
+    static constexpr int RS = S + 4;      // tile / coefficient rows
+    static constexpr int LD = 2 * S + 1;  // augmented [M | RHS] rows
+};
+
 template <int S>
 struct Sm {
     double s_old[S * S];
     double mat[S * S];
-    double coef[S * S];
-    double aug[2 * S * S + 2 * S];
+    double coef[S * Strides<S>::RS];
+    double aug[S * Strides<S>::LD + 2 * S];
     double scratch[CtaShape<S>::NW * S * S];  // per-warp matrix partials
-    double tileR[CtaShape<S>::NW][16 * S];    // warp-private transposes (phase 2 / init)
-    double tileZ[CtaShape<S>::NW][16 * S];
+    double tileR[CtaShape<S>::NW][16 * Strides<S>::RS];  // warp-private transposes
+    double tileZ[CtaShape<S>::NW][16 * Strides<S>::RS];
     double vec[S];
     double bnorm[S];
     double fres[S];
@@ -313,7 +323,7 @@ __device__ __forceinline__ unsigned long long pos_bits(double v) {
 // complement, so pivots and rank decisions coincide). One barrier per pivot;
 // every warp redundantly tracks the Schur diagonal in registers and searches
 // the next pivot while the block update of the current one is in flight.
-template <int S, bool PROF = false>
+template <int S, bool PROF = false, int VAR = 0>
 __device__ void small_solve(Sm<S>& sm, const double* M, const double* RHS, double* out) {
     constexpr int BS = CtaShape<S>::BS;
     long long* const pr = PROF ? g_ss_prof : nullptr;
@@ -321,25 +331,29 @@ __device__ void small_solve(Sm<S>& sm, const double* M, const double* RHS, doubl
         if (PROF && threadIdx.x == 0) pr[k] = clock64();
     };
     auto wbar = []() { __syncthreads(); };
-    constexpr int LD = 2 * S;
+    constexpr int NW = CtaShape<S>::NW;
+    constexpr int LD = Strides<S>::LD;
+    constexpr int RS = Strides<S>::RS;
     constexpr int R = (S + 31) / 32;  // diagonal entries per lane (index lane + 32 r)
     static_assert(R <= 2, "S <= 64");
     const int sa = sm.sa;
     double* aug = sm.aug;
     unsigned long long donem = 0ull;  // compacted indices already used as pivots
-    const int lane = threadIdx.x & 31;
-    for (int e = threadIdx.x; e < sa * LD; e += BS) {
-        const int p = e / LD, q = e % LD;
-        double v = 0.0;
-        const int a = sm.idx[p];
-        if (q < sa) {
-            const int b = sm.idx[q];
-            v = a <= b ? M[a * S + b] : M[b * S + a];
-        } else if (q < 2 * sa) {
-            const int b = sm.idx[q - sa];
-            v = a <= b ? RHS[a * S + b] : RHS[b * S + a];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // rows by warp, columns by lane: no integer division, conflict-free rows
+    for (int i = warp; i < sa; i += NW) {
+        const int a = sm.idx[i];
+        for (int q = lane; q < 2 * sa; q += 32) {
+            double v;
+            if (q < sa) {
+                const int b = sm.idx[q];
+                v = a <= b ? M[a * S + b] : M[b * S + a];
+            } else {
+                const int b = sm.idx[q - sa];
+                v = a <= b ? RHS[a * S + b] : RHS[b * S + a];
+            }
+            aug[i * LD + q] = v;
         }
-        aug[p * LD + q] = v;
     }
     wbar();
     double dg[R];
@@ -364,46 +378,92 @@ __device__ void small_solve(Sm<S>& sm, const double* M, const double* RHS, doubl
     const int im = best ? 63 - (int)(best & 63ull) : -1;
     const double maxd = im >= 0 ? aug[im * LD + im] : 0.0;
     const double cutoff = fmax(maxd * sa * 2.220446049250313e-16, 2.2250738585072014e-308);
-    int rank = 0;
-    stamp(1);
-    while (best) {
-        const int p = 63 - (int)(best & 63ull);
-        // exact pivot value (the REDUX key is truncated in its low 6 bits)
-        double pv = __shfl_sync(0xffffffffu, dg[0], p & 31);
+    // exact value of the pivot encoded in `key` (the key is truncated in its
+    // low 6 bits), held in lane (p & 31) of dg
+    auto pivot_of = [&](unsigned long long key, int& p, double& pv) {
+        p = key ? 63 - (int)(key & 63ull) : -1;
+        const int src = p < 0 ? 0 : (p & 31);
+        pv = __shfl_sync(0xffffffffu, dg[0], src);
         if (R > 1) {
-            const double pv1 = __shfl_sync(0xffffffffu, dg[R - 1], p & 31);
+            const double pv1 = __shfl_sync(0xffffffffu, dg[R - 1], src);
             if (p >= 32) pv = pv1;
         }
-        if (!(pv > cutoff)) break;  // uniform: beyond the numerical rank
-        const double rinv = __drcp_rn(pv);
+        if (p < 0) pv = 0.0;
+    };
+    int p;
+    double pv;
+    pivot_of(best, p, pv);
+    double rinv = __drcp_rn(pv);
+    int rank = 0;
+    stamp(1);
+    constexpr int RPW = (S + NW - 1) / NW;    // rows per warp
+    constexpr int CPL = (2 * S + 31) / 32;    // columns per lane
+    while (p >= 0 && pv > cutoff) {           // uniform: beyond the rank -> stop
         donem |= 1ull << p;
-        // Schur diagonal after this pivot, with the arithmetic the block
-        // update applies to aug[i][i]; the next pivot is searched while the
-        // block update is in flight
+        // operands of this pivot's block update and of the Schur-diagonal
+        // update (row p and column p are not written by this step)
+        double apq[CPL], fi[RPW], aiq[RPW][CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int q = lane + 32 * c;
+            apq[c] = q < 2 * sa ? aug[p * LD + q] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+            const int i = warp + NW * r;
+            fi[r] = i < sa ? aug[i * LD + p] : 0.0;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                const int q = lane + 32 * c;
+                aiq[r][c] = (i < sa && q < 2 * sa) ? aug[i * LD + q] : 0.0;
+            }
+        }
+        double colp[R], rowp[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int i = lane + 32 * r;
-            if (i < sa && !((donem >> i) & 1ull))
-                dg[r] = fma(-(aug[i * LD + p] * rinv), aug[p * LD + i], dg[r]);
+            colp[r] = i < sa ? aug[i * LD + p] : 0.0;
+            rowp[r] = i < sa ? aug[p * LD + i] : 0.0;
         }
-        const unsigned long long nb = search(donem);
-        for (int e = threadIdx.x; e < sa * LD; e += BS) {
-            const int i = e / LD, q = e % LD;
-            if (i == p || q >= 2 * sa || (q < sa && ((donem >> q) & 1ull))) continue;
-            const double f = aug[i * LD + p] * rinv;
-            aug[i * LD + q] = fma(-f, aug[p * LD + q], aug[i * LD + q]);
+        // block update (issued first so it overlaps the pivot search below)
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+            const int i = warp + NW * r;
+            if (i >= sa || i == p) continue;
+            const double f = fi[r] * rinv;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                const int q = lane + 32 * c;
+                if (q >= 2 * sa || (q < sa && ((donem >> q) & 1ull))) continue;
+                aug[i * LD + q] = fma(-f, apq[c], aiq[r][c]);
+            }
         }
+        // Schur diagonal after this pivot (same arithmetic as aug[i][i] above)
+        // and the next pivot with its reciprocal, before the barrier
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int i = lane + 32 * r;
+            if (i < sa && !((donem >> i) & 1ull)) dg[r] = fma(-(colp[r] * rinv), rowp[r], dg[r]);
+        }
+        unsigned long long nb = search(donem);
+        if (VAR == 2) nb = (p + 1 < sa) ? ((1ull << 32) | (unsigned long long)(63 - (p + 1))) : 0ull;
+        int pn;
+        double pvn;
+        pivot_of(nb, pn, pvn);
+        const double rn = __drcp_rn(pvn > 0.0 ? pvn : 1.0);
         ++rank;
-        wbar();
+        if (VAR != 3) wbar();
         stamp(2 + rank);
-        best = nb;
+        p = pn;
+        pv = pvn;
+        rinv = rn;
     }
-    for (int e = threadIdx.x; e < S * S; e += BS) out[e] = 0.0;
+    for (int e = threadIdx.x; e < S * RS; e += BS) out[e] = 0.0;
     wbar();
-    for (int e = threadIdx.x; e < sa * sa; e += BS) {
-        const int pp = e / sa, q = e % sa;
-        if ((donem >> pp) & 1ull)
-            out[sm.idx[pp] * S + sm.idx[q]] = aug[pp * LD + sa + q] * __drcp_rn(aug[pp * LD + pp]);
+    for (int i = warp; i < sa; i += NW) {
+        if (!((donem >> i) & 1ull)) continue;
+        const double di = __drcp_rn(aug[i * LD + i]);
+        for (int q = lane; q < sa; q += 32) out[sm.idx[i] * RS + sm.idx[q]] = aug[i * LD + sa + q] * di;
     }
     if (threadIdx.x == 0) sm.rank = rank;
     __syncthreads();
@@ -509,17 +569,14 @@ template <int S>
 __device__ __forceinline__ void tile_gram(double* tr, double* tz, const double (&r)[S / 8][4],
                                           const double (&z)[S / 8][4], int g, int t,
                                           GramAcc<S>& G) {
+    constexpr int RS = Strides<S>::RS;
 #pragma unroll
     for (int n = 0; n < S / 8; ++n) {
         const int col = 8 * n + 2 * t;
-        tr[g * S + col] = r[n][0];
-        tr[g * S + col + 1] = r[n][1];
-        tr[(g + 8) * S + col] = r[n][2];
-        tr[(g + 8) * S + col + 1] = r[n][3];
-        tz[g * S + col] = z[n][0];
-        tz[g * S + col + 1] = z[n][1];
-        tz[(g + 8) * S + col] = z[n][2];
-        tz[(g + 8) * S + col + 1] = z[n][3];
+        *reinterpret_cast<double2*>(tr + g * RS + col) = make_double2(r[n][0], r[n][1]);
+        *reinterpret_cast<double2*>(tr + (g + 8) * RS + col) = make_double2(r[n][2], r[n][3]);
+        *reinterpret_cast<double2*>(tz + g * RS + col) = make_double2(z[n][0], z[n][1]);
+        *reinterpret_cast<double2*>(tz + (g + 8) * RS + col) = make_double2(z[n][2], z[n][3]);
     }
     __syncwarp();
 #pragma unroll
@@ -527,11 +584,11 @@ __device__ __forceinline__ void tile_gram(double* tr, double* tz, const double (
         const int cell = 4 * kk + t;
 #pragma unroll
         for (int m = 0; m < GramAcc<S>::MT; ++m) {
-            const double a0 = tr[cell * S + 16 * m + g];
-            const double a1 = (16 * m + 8 + g < S) ? tr[cell * S + 16 * m + 8 + g] : 0.0;
+            const double a0 = tr[cell * RS + 16 * m + g];
+            const double a1 = (16 * m + 8 + g < S) ? tr[cell * RS + 16 * m + 8 + g] : 0.0;
 #pragma unroll
             for (int n = 0; n < GramAcc<S>::NT; ++n)
-                dmma(G.d[m][n], a0, a1, tz[cell * S + 8 * n + g]);
+                dmma(G.d[m][n], a0, a1, tz[cell * RS + 8 * n + g]);
         }
     }
     __syncwarp();
@@ -638,7 +695,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
             for (int n = 0; n < NT; ++n)
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) {
-                    const double bb = sm.coef[(4 * ks + t) * S + 8 * n + g];
+                    const double bb = sm.coef[(4 * ks + t) * Strides<S>::RS + 8 * n + g];
                     dmma(x[n], pa[ks][0], pa[ks][1], bb);
                     dmma(r[n], wa[ks][0], wa[ks][1], bb);
                 }
@@ -768,7 +825,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
                 p[n][3] *= d1;
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks)
-                    dmma(p[n], pa[ks][0], pa[ks][1], sm.coef[(4 * ks + t) * S + 8 * n + g]);
+                    dmma(p[n], pa[ks][0], pa[ks][1], sm.coef[(4 * ks + t) * Strides<S>::RS + 8 * n + g]);
             }
             store_ctile<S>(a.P, base, c1, g, t, p);
         }
@@ -959,11 +1016,28 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) small_solve_bench_kernel(i
     __syncthreads();
     if (threadIdx.x == 0) out[2 + 62] = clock64();
     small_solve<S, true>(sm, sm.mat, sm.s_old, sm.coef);
+    __syncthreads();
+    long long tv[4];
+    for (int v = 1; v <= 3; ++v) {
+        __syncthreads();
+        const long long a0 = clock64();
+        for (int r = 0; r < 20; ++r) {
+            if (v == 1) small_solve<S, false, 1>(sm, sm.mat, sm.s_old, sm.coef);
+            if (v == 2) small_solve<S, false, 2>(sm, sm.mat, sm.s_old, sm.coef);
+            if (v == 3) small_solve<S, false, 3>(sm, sm.mat, sm.s_old, sm.coef);
+        }
+        tv[v] = (clock64() - a0) / 20;
+    }
+    if (threadIdx.x == 0) {
+        out[70] = tv[1];
+        out[71] = tv[2];
+        out[72] = tv[3];
+    }
     if (threadIdx.x == 0) {
         out[0] = (t1 - t0) / reps;
         out[1] = sm.rank;
     }
-    for (int e = threadIdx.x; e < S * S; e += BS) res[e] = sm.coef[e];
+    for (int e = threadIdx.x; e < S * S; e += BS) res[e] = sm.coef[(e / S) * Strides<S>::RS + e % S];
 }
 }  // namespace
 
@@ -988,7 +1062,8 @@ extern "C" int bk_debug_small_solve_cycles(int s, int reps, long long* cycles, i
     fprintf(stderr, "small_solve<%d> stamps (cycles from start): setup %lld, first search %lld;", s,
             h[2] - h[64], h[3] - h[64]);
     for (int k = 1; k <= s; ++k) fprintf(stderr, " %lld", h[4 + k] ? h[4 + k] - h[64] : -1);
-    fprintf(stderr, "; end %lld\n", h[65] - h[64]);
+    fprintf(stderr, "; end %lld | variants: no-update %lld, fixed-order %lld, no-barrier %lld\n",
+            h[65] - h[64], h[70], h[71], h[72]);
     cudaMemcpy(coef, r, (size_t)s * s * 8, cudaMemcpyDeviceToHost);
     *cycles = h[0];
     *rank = (int)h[1];
