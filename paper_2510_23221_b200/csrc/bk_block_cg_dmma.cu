@@ -40,7 +40,7 @@ struct CtaShape {
 };
 constexpr int PROF_ITERS = 64;
 __device__ long long* g_ss_prof = nullptr;  // debug: small-solve step timestamps
-constexpr int PROF_MARKS = 8;
+constexpr int PROF_MARKS = 12;
 
 struct Args {
     int nx, ny, nz;
@@ -88,15 +88,40 @@ struct Strides {
     static constexpr int LD = 2 * S + 1;  // augmented [M | RHS] rows
 };
 
+// Resident mode (S <= 16, at most kResCells cells per CTA: BASELINE configs 1,
+// 2 and 4 on 148 SMs): X and R live in shared memory for the whole solve
+// (XOR-swizzled rows, conflict-free for the DMMA C-fragment layout), removing
+// their L2 round trips from phases 2 and 3; they are published to HBM only for
+// the rare true-residual / restart sweeps and at exit.
+constexpr int kResCells = 448;
+
+template <int S, bool RES>
+struct ResStore {
+    static constexpr int kVecs = 0;
+};
 template <int S>
+struct ResStore<S, true> {
+    alignas(16) double x[kResCells * S];
+    alignas(16) double r[kResCells * S];
+};
+
+template <int S>
+constexpr bool scratch_aliases_tiles() {
+    return S * S <= 16 * Strides<S>::RS;
+}
+
+template <int S, bool RES = false>
 struct Sm {
     double s_old[S * S];
     double mat[S * S];
-    double coef[S * Strides<S>::RS];
-    double aug[S * Strides<S>::LD + 2 * S];
-    double scratch[CtaShape<S>::NW * S * S];  // per-warp matrix partials
-    double tileR[CtaShape<S>::NW][16 * Strides<S>::RS];  // warp-private transposes
-    double tileZ[CtaShape<S>::NW][16 * Strides<S>::RS];
+    alignas(16) double coef[S * Strides<S>::RS];
+    alignas(16) double aug[S * Strides<S>::LD + 2 * S];
+    // per-warp matrix partials; aliased onto the warp's own transpose tile
+    // when it fits (written only after that warp's tile loop)
+    double scratch[scratch_aliases_tiles<S>() ? 1 : CtaShape<S>::NW * S * S];
+    alignas(16) double tileR[CtaShape<S>::NW][16 * Strides<S>::RS];  // warp-private transposes
+    alignas(16) double tileZ[CtaShape<S>::NW][16 * Strides<S>::RS];
+    alignas(16) ResStore<S, RES> res;
     double vec[S];
     double bnorm[S];
     double fres[S];
@@ -213,13 +238,13 @@ struct GramAcc {
 
 // sum per-warp matrices in warp order -> out[S*S]
 template <int S>
-__device__ __forceinline__ void cta_sum_mat(const double* scratch, double* out) {
+__device__ __forceinline__ void cta_sum_mat(const double* scratch, int stride, double* out) {
     constexpr int BS = CtaShape<S>::BS, NW = CtaShape<S>::NW;
     __syncthreads();
     for (int e = threadIdx.x; e < S * S; e += BS) {
         double s = scratch[e];
 #pragma unroll
-        for (int w = 1; w < NW; ++w) s += scratch[w * S * S + e];
+        for (int w = 1; w < NW; ++w) s += scratch[w * stride + e];
         out[e] = s;
     }
     __syncthreads();
@@ -227,8 +252,8 @@ __device__ __forceinline__ void cta_sum_mat(const double* scratch, double* out) 
 
 // per-lane column partials v[nt][e] for columns 8nt+2t+e -> out[S] (warp order)
 template <int S>
-__device__ __forceinline__ void cta_sum_vec(double (&v)[S / 8][2], double* scratch, double* out,
-                                            int warp, int lane) {
+__device__ __forceinline__ void cta_sum_vec(double (&v)[S / 8][2], double* scratch, int stride,
+                                            double* out, int warp, int lane) {
     constexpr int BS = CtaShape<S>::BS, NW = CtaShape<S>::NW;
 #pragma unroll
     for (int n = 0; n < S / 8; ++n)
@@ -238,12 +263,12 @@ __device__ __forceinline__ void cta_sum_vec(double (&v)[S / 8][2], double* scrat
             x += __shfl_xor_sync(0xffffffffu, x, 4);
             x += __shfl_xor_sync(0xffffffffu, x, 8);
             x += __shfl_xor_sync(0xffffffffu, x, 16);
-            if (lane < 4) scratch[warp * S + 8 * n + 2 * lane + e] = x;
+            if (lane < 4) scratch[warp * stride + 8 * n + 2 * lane + e] = x;
         }
     __syncthreads();
     for (int e = threadIdx.x; e < S; e += BS) {
         double s = scratch[e];
-        for (int w = 1; w < NW; ++w) s += scratch[w * S + e];
+        for (int w = 1; w < NW; ++w) s += scratch[w * stride + e];
         out[e] = s;
     }
     __syncthreads();
@@ -273,8 +298,8 @@ __device__ void grid_reduce(cg::grid_group& grid, double* __restrict__ part,
 // ---------------------------------------------------------------------------
 // small solves (identical in every CTA)
 // ---------------------------------------------------------------------------
-template <int S>
-__device__ void build_index(Sm<S>& sm) {
+template <int S, bool RES>
+__device__ void build_index(Sm<S, RES>& sm) {
     if (threadIdx.x == 0) {
         int k = 0;
         for (int q = 0; q < S; ++q)
@@ -323,8 +348,8 @@ __device__ __forceinline__ unsigned long long pos_bits(double v) {
 // complement, so pivots and rank decisions coincide). One barrier per pivot;
 // every warp redundantly tracks the Schur diagonal in registers and searches
 // the next pivot while the block update of the current one is in flight.
-template <int S, bool PROF = false, int VAR = 0>
-__device__ void small_solve(Sm<S>& sm, const double* M, const double* RHS, double* out) {
+template <int S, bool PROF = false, int VAR = 0, bool RES = false>
+__device__ void small_solve(Sm<S, RES>& sm, const double* M, const double* RHS, double* out) {
     constexpr int BS = CtaShape<S>::BS;
     long long* const pr = PROF ? g_ss_prof : nullptr;
     auto stamp = [&](int k) {
@@ -473,47 +498,88 @@ __device__ void small_solve(Sm<S>& sm, const double* M, const double* RHS, doubl
 // ---------------------------------------------------------------------------
 // phases
 // ---------------------------------------------------------------------------
-// phase 1: W = A P over the CTA's cells, Gram G += P^T W. Two 4-cell groups
-// per trip so their stencil loads are in flight together.
+// phase 1: W = A P over the CTA's cells, Gram G += P^T W, in 16-cell tiles.
+// Lane (r = lane / 2, h = lane % 2) owns row segment [cw*h, cw*h + cw) of cell
+// base + r (cw = min(S/2, 8) columns per pass): every stencil row is read with
+// 128-bit loads, the accumulation follows the reference CSR order
+// (apply_block_fixed, discretize.cpp:57-71), W leaves with 128-bit stores, and
+// P / W are staged through the warp's smem tiles for the DMMA Gram (K = cells).
 template <int S>
 __device__ __forceinline__ void phase_spmm_gram(const Args& a, int64_t c0, int64_t c1, int warp,
-                                                int g, int t, GramAcc<S>& G) {
-    constexpr int CPL = S / 8;
+                                                int lane, double* tp, double* tw, GramAcc<S>& G) {
     constexpr int NW = CtaShape<S>::NW;
-    constexpr int U = 2;
-    const int64_t groups = (c1 - c0 + 3) / 4;
-    for (int64_t q0 = warp; q0 < groups; q0 += NW * U) {
-        double w[U][CPL], p[U][CPL];
+    constexpr int RS = Strides<S>::RS;
+    constexpr int CW = S / 2 < 8 ? S / 2 : 8;   // columns per lane per pass
+    constexpr int PASSES = S / (2 * CW);
+    const int r = lane >> 1, h = lane & 1;
+    const int g = lane >> 2, t = lane & 3;
+    const int64_t plane = (int64_t)a.nx * a.ny;
+    for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
+        const int64_t cell = base + r;
+        const bool v = cell < c1;
+        Coef k;
+        if (v) load_coef(a, cell, k);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t q = q0 + u * NW;
-            const int64_t cell = c0 + 4 * q + t;
-            if (q < groups && cell < c1) {
-                Coef k;
-                load_coef(a, cell, k);
+        for (int ps = 0; ps < PASSES; ++ps) {
+            const int col = ps * 2 * CW + h * CW;
+            double acc[CW], ctr[CW];
 #pragma unroll
-                for (int c = 0; c < CPL; ++c) w[u][c] = st_fma<S>(k, a.P, cell, g + 8 * c, p[u][c]);
-            } else {
+            for (int j = 0; j < CW; ++j) acc[j] = ctr[j] = 0.0;
+            if (v) {
+                auto row = [&](int64_t c, double coef, bool has) {
+                    if (!has) return;
+                    const double2* src = reinterpret_cast<const double2*>(a.P + c * S + col);
 #pragma unroll
-                for (int c = 0; c < CPL; ++c) w[u][c] = p[u][c] = 0.0;
+                    for (int j = 0; j < CW / 2; ++j) {
+                        const double2 x = src[j];
+                        acc[2 * j] = fma(coef, x.x, acc[2 * j]);
+                        acc[2 * j + 1] = fma(coef, x.y, acc[2 * j + 1]);
+                    }
+                };
+                row(cell - plane, k.zm, k.hzm);
+                row(cell - a.nx, k.ym, k.hym);
+                row(cell - 1, k.xm, k.hxm);
+                {
+                    const double2* src = reinterpret_cast<const double2*>(a.P + cell * S + col);
+#pragma unroll
+                    for (int j = 0; j < CW / 2; ++j) {
+                        const double2 x = src[j];
+                        ctr[2 * j] = x.x;
+                        ctr[2 * j + 1] = x.y;
+                        acc[2 * j] = fma(k.d, x.x, acc[2 * j]);
+                        acc[2 * j + 1] = fma(k.d, x.y, acc[2 * j + 1]);
+                    }
+                }
+                row(cell + 1, k.xp, k.hxp);
+                row(cell + a.nx, k.yp, k.hyp);
+                row(cell + plane, k.zp, k.hzp);
+                double2* dst = reinterpret_cast<double2*>(a.W + cell * S + col);
+#pragma unroll
+                for (int j = 0; j < CW / 2; ++j) dst[j] = make_double2(acc[2 * j], acc[2 * j + 1]);
+            }
+#pragma unroll
+            for (int j = 0; j < CW / 2; ++j) {
+                *reinterpret_cast<double2*>(tp + r * RS + col + 2 * j) =
+                    make_double2(ctr[2 * j], ctr[2 * j + 1]);
+                *reinterpret_cast<double2*>(tw + r * RS + col + 2 * j) =
+                    make_double2(acc[2 * j], acc[2 * j + 1]);
             }
         }
+        __syncwarp();
+        // G += P^T W over the tile's 16 cells (K = cells)
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t q = q0 + u * NW;
-            const int64_t cell = c0 + 4 * q + t;
-            if (q < groups && cell < c1) {
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) a.W[cell * S + g + 8 * c] = w[u][c];
-            }
+        for (int kk = 0; kk < 4; ++kk) {
+            const int c4 = 4 * kk + t;
 #pragma unroll
             for (int m = 0; m < GramAcc<S>::MT; ++m) {
-                const double a0 = p[u][2 * m];
-                const double a1 = (2 * m + 1 < CPL) ? p[u][2 * m + 1] : 0.0;
+                const double a0 = tp[c4 * RS + 16 * m + g];
+                const double a1 = (16 * m + 8 + g < S) ? tp[c4 * RS + 16 * m + 8 + g] : 0.0;
 #pragma unroll
-                for (int n = 0; n < GramAcc<S>::NT; ++n) dmma(G.d[m][n], a0, a1, w[u][n]);
+                for (int n = 0; n < GramAcc<S>::NT; ++n)
+                    dmma(G.d[m][n], a0, a1, tw[c4 * RS + 8 * n + g]);
             }
         }
+        __syncwarp();
     }
 }
 
@@ -594,6 +660,67 @@ __device__ __forceinline__ void tile_gram(double* tr, double* tz, const double (
     __syncwarp();
 }
 
+// resident (smem) C-layout tiles: local cell l, even column c -> swizzled slot
+template <int S>
+__device__ __forceinline__ int res_idx(int l, int c) {
+    const int chunk = c >> 1;
+    const int sw = (S / 2 >= 8) ? ((l & 1) << 2) : 0;
+    return l * S + ((chunk ^ sw) << 1);
+}
+
+template <int S>
+__device__ __forceinline__ void load_rtile(const double* v, int lb, int cnt, int g, int t,
+                                           double (&c)[S / 8][4]) {
+    const bool v0 = lb + g < cnt, v1 = lb + g + 8 < cnt;
+#pragma unroll
+    for (int n = 0; n < S / 8; ++n) {
+        const double2 x0 = v0 ? *reinterpret_cast<const double2*>(v + res_idx<S>(lb + g, 8 * n + 2 * t))
+                              : make_double2(0.0, 0.0);
+        const double2 x1 = v1 ? *reinterpret_cast<const double2*>(v + res_idx<S>(lb + g + 8, 8 * n + 2 * t))
+                              : make_double2(0.0, 0.0);
+        c[n][0] = x0.x;
+        c[n][1] = x0.y;
+        c[n][2] = x1.x;
+        c[n][3] = x1.y;
+    }
+}
+
+template <int S>
+__device__ __forceinline__ void store_rtile(double* v, int lb, int cnt, int g, int t,
+                                            const double (&c)[S / 8][4]) {
+    const bool v0 = lb + g < cnt, v1 = lb + g + 8 < cnt;
+#pragma unroll
+    for (int n = 0; n < S / 8; ++n) {
+        if (v0)
+            *reinterpret_cast<double2*>(v + res_idx<S>(lb + g, 8 * n + 2 * t)) =
+                make_double2(c[n][0], c[n][1]);
+        if (v1)
+            *reinterpret_cast<double2*>(v + res_idx<S>(lb + g + 8, 8 * n + 2 * t)) =
+                make_double2(c[n][2], c[n][3]);
+    }
+}
+
+// X or R of a 16-cell tile: shared-memory resident or the HBM block vector
+template <int S, bool RES>
+struct TileVec {
+    double* g;   // global n x S
+    double* sm;  // resident (RES) local cells x S
+    int64_t c0, c1;
+    __device__ __forceinline__ void load(int64_t base, int gg, int t, double (&c)[S / 8][4]) const {
+        if (RES)
+            load_rtile<S>(sm, (int)(base - c0), (int)(c1 - c0), gg, t, c);
+        else
+            load_ctile<S>(g, base, c1, gg, t, c);
+    }
+    __device__ __forceinline__ void store(int64_t base, int gg, int t,
+                                          const double (&c)[S / 8][4]) const {
+        if (RES)
+            store_rtile<S>(sm, (int)(base - c0), (int)(c1 - c0), gg, t, c);
+        else
+            store_ctile<S>(g, base, c1, gg, t, c);
+    }
+};
+
 __device__ __forceinline__ double dinv_at(const Args& a, int64_t c, int64_t c1, bool jac) {
     return (jac && c < c1) ? a.dinv[c] : 1.0;
 }
@@ -601,7 +728,7 @@ __device__ __forceinline__ double dinv_at(const Args& a, int64_t c, int64_t c1, 
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-template <int S>
+template <int S, bool RES>
 __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args a) {
     constexpr int BS = CtaShape<S>::BS, NW = CtaShape<S>::NW;
     constexpr int NT = S / 8;
@@ -609,11 +736,14 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
     constexpr int E = S * S + S;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Sm<S>& sm = *reinterpret_cast<Sm<S>*>(smem_raw);
+    Sm<S, RES>& sm = *reinterpret_cast<Sm<S, RES>*>(smem_raw);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int NB = gridDim.x, b = blockIdx.x;
+    constexpr bool kAlias = scratch_aliases_tiles<S>();
+    double* const scr = kAlias ? &sm.tileR[0][0] : sm.scratch;
+    constexpr int kScrStride = kAlias ? 16 * Strides<S>::RS : S * S;
     // CTA ranges in whole 16-cell tiles (the last CTA takes the ragged end)
     const int64_t ntiles = (a.n + 15) / 16;
     const int64_t c0 = 16 * (ntiles * b / NB);
@@ -622,6 +752,26 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
     const bool prof = a.prof != nullptr && b == 0 && tid == 0;
     double* tr = sm.tileR[warp];
     double* tz = sm.tileZ[warp];
+
+    double* xres = nullptr;
+    double* rres = nullptr;
+    if constexpr (RES) {
+        xres = sm.res.x;
+        rres = sm.res.r;
+    }
+    const TileVec<S, RES> Xv{a.X, xres, c0, c1};
+    const TileVec<S, RES> Rv{a.R, rres, c0, c1};
+    // resident X -> HBM (for the stencil sweeps over X and for the output)
+    auto publish_x = [&]() {
+        if constexpr (RES) {
+            for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
+                double x[NT][4];
+                Xv.load(base, g, t, x);
+                store_ctile<S>(a.X, base, c1, g, t, x);
+            }
+            grid.sync();
+        }
+    };
 
     GramAcc<S> G;
     int64_t matvecs = 0;
@@ -646,14 +796,14 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
 #pragma unroll
                 for (int e = 0; e < 4; ++e) zero[n][e] = 0.0;
             }
-            store_ctile<S>(a.X, base, c1, g, t, zero);
-            store_ctile<S>(a.R, base, c1, g, t, r);
+            Xv.store(base, g, t, zero);
+            Rv.store(base, g, t, r);
             store_ctile<S>(a.P, base, c1, g, t, z);
             tile_gram<S>(tr, tz, r, z, g, t, G);
         }
-        G.spill(sm.scratch + warp * S * S, g, t);
-        cta_sum_mat<S>(sm.scratch, sm.aug);
-        cta_sum_vec<S>(bn, sm.scratch, sm.aug + S * S, warp, lane);
+        G.spill(scr + warp * kScrStride, g, t);
+        cta_sum_mat<S>(scr, kScrStride, sm.aug);
+        cta_sum_vec<S>(bn, scr, kScrStride, sm.aug + S * S, warp, lane);
         grid_reduce<BS>(grid, a.part, a.red, sm.aug, E, sm.aug + E);
         for (int e = tid; e < S * S; e += BS) sm.s_old[e] = sm.aug[E + e];
         if (tid < S) {
@@ -672,9 +822,10 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         if (pm) pm[0] = gtimer();
         // ---- phase 1: W = A P, G = P^T W
         G.zero();
-        phase_spmm_gram<S>(a, c0, c1, warp, g, t, G);
-        G.spill(sm.scratch + warp * S * S, g, t);
-        cta_sum_mat<S>(sm.scratch, sm.aug);
+        phase_spmm_gram<S>(a, c0, c1, warp, lane, tr, tz, G);
+        if (pm) pm[8] = gtimer();
+        G.spill(scr + warp * kScrStride, g, t);
+        cta_sum_mat<S>(scr, kScrStride, sm.aug);
         if (pm) pm[1] = gtimer();
         grid_reduce<BS>(grid, a.part, a.red, sm.aug, S * S, sm.mat);
         if (pm) pm[2] = gtimer();
@@ -689,8 +840,8 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
             double pa[KS][2], wa[KS][2], x[NT][4], r[NT][4];
             load_afrag<S>(a.P, base, c1, g, t, pa, 1.0);
             load_afrag<S>(a.W, base, c1, g, t, wa, -1.0);
-            load_ctile<S>(a.X, base, c1, g, t, x);
-            load_ctile<S>(a.R, base, c1, g, t, r);
+            Xv.load(base, g, t, x);
+            Rv.load(base, g, t, r);
 #pragma unroll
             for (int n = 0; n < NT; ++n)
 #pragma unroll
@@ -699,8 +850,8 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
                     dmma(x[n], pa[ks][0], pa[ks][1], bb);
                     dmma(r[n], wa[ks][0], wa[ks][1], bb);
                 }
-            store_ctile<S>(a.X, base, c1, g, t, x);
-            store_ctile<S>(a.R, base, c1, g, t, r);
+            Xv.store(base, g, t, x);
+            Rv.store(base, g, t, r);
             const double d0 = dinv_at(a, base + g, c1, jac), d1 = dinv_at(a, base + g + 8, c1, jac);
             double z[NT][4];
 #pragma unroll
@@ -714,9 +865,10 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
             }
             tile_gram<S>(tr, tz, r, z, g, t, G);
         }
-        G.spill(sm.scratch + warp * S * S, g, t);
-        cta_sum_mat<S>(sm.scratch, sm.aug);
-        cta_sum_vec<S>(rr, sm.scratch, sm.aug + S * S, warp, lane);
+        if (pm) pm[9] = gtimer();
+        G.spill(scr + warp * kScrStride, g, t);
+        cta_sum_mat<S>(scr, kScrStride, sm.aug);
+        cta_sum_vec<S>(rr, scr, kScrStride, sm.aug + S * S, warp, lane);
         if (pm) pm[4] = gtimer();
         grid_reduce<BS>(grid, a.part, a.red, sm.aug, E, sm.aug + E);
         for (int e = tid; e < S * S; e += BS) sm.mat[e] = sm.aug[E + e];  // S_new
@@ -733,6 +885,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         for (int q = 0; q < S; ++q) nver += sm.vflag[q];
         bool restart = false;
         if (nver > 0) {
+            publish_x();
             double rs[NT][2] = {};
             for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
 #pragma unroll
@@ -751,7 +904,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
                         }
                 }
             }
-            cta_sum_vec<S>(rs, sm.scratch, sm.aug, warp, lane);
+            cta_sum_vec<S>(rs, scr, kScrStride, sm.aug, warp, lane);
             grid_reduce<BS>(grid, a.part, a.red, sm.aug, S, sm.aug + S);
             matvecs += nver;
             if (tid == 0) {
@@ -797,12 +950,12 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
                             z[n][2 * h + e] = di * rv;
                         }
                 }
-                store_ctile<S>(a.R, base, c1, g, t, r);
+                Rv.store(base, g, t, r);
                 store_ctile<S>(a.P, base, c1, g, t, z);
                 tile_gram<S>(tr, tz, r, z, g, t, G);
             }
-            G.spill(sm.scratch + warp * S * S, g, t);
-            cta_sum_mat<S>(sm.scratch, sm.aug);
+            G.spill(scr + warp * kScrStride, g, t);
+            cta_sum_mat<S>(scr, kScrStride, sm.aug);
             grid_reduce<BS>(grid, a.part, a.red, sm.aug, S * S, sm.s_old);
             matvecs += sm.sa;
             continue;
@@ -815,7 +968,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
             double pa[KS][2], p[NT][4];
             load_afrag<S>(a.P, base, c1, g, t, pa, 1.0);
-            load_ctile<S>(a.R, base, c1, g, t, p);
+            Rv.load(base, g, t, p);
             const double d0 = dinv_at(a, base + g, c1, jac), d1 = dinv_at(a, base + g + 8, c1, jac);
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
@@ -834,6 +987,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
     }
 
     // ---- exit: honest residuals for still-active columns (:655-661)
+    publish_x();
     if (sm.sa > 0) {
         double rs[NT][2] = {};
         for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
@@ -853,7 +1007,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
                     }
             }
         }
-        cta_sum_vec<S>(rs, sm.scratch, sm.aug, warp, lane);
+        cta_sum_vec<S>(rs, scr, kScrStride, sm.aug, warp, lane);
         grid_reduce<BS>(grid, a.part, a.red, sm.aug, S, sm.aug + S);
         matvecs += sm.sa;
         if (tid < S && sm.act[tid]) {
@@ -879,21 +1033,24 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
     using namespace bk;
     const int64_t n = op->n;
     const size_t vec_bytes = (size_t)n * S * sizeof(double);
-    auto kern = block_cg_dmma_kernel<S>;
-    const size_t smem = sizeof(Sm<S>);
-    BK_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
-    int occ = 0;
     constexpr int BS = CtaShape<S>::BS;
-    BK_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BS, smem));
-    if (occ < 1) return fail(ctx, BK_INTERNAL, "block_cg: DMMA kernel cannot be resident");
-    occ = 1;  // one CTA per SM (see CtaShape)
-    int64_t nb = (int64_t)occ * ctx->num_sms;
+    int64_t nb = ctx->num_sms;  // one CTA per SM (see CtaShape)
     if (ctx->cg_max_ctas > 0 && nb > ctx->cg_max_ctas) nb = ctx->cg_max_ctas;
     const int64_t ntiles = (n + 15) / 16;
     const int64_t min_tiles = 2;
     if (nb * min_tiles > ntiles) nb = (ntiles + min_tiles - 1) / min_tiles;
     if (nb < 1) nb = 1;
+    // shared-memory-resident X/R when every CTA's range fits (S <= 16)
+    const int64_t max_cells = 16 * ((ntiles + nb - 1) / nb);
+    const bool resident = S <= 16 && max_cells <= kResCells && getenv("BK_CG_NO_RESIDENT") == nullptr;
+    const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true>
+                                : (const void*)block_cg_dmma_kernel<S, false>;
+    const size_t smem = resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>);
+    BK_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+    int occ = 0;
+    BK_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BS, smem));
+    if (occ < 1) return fail(ctx, BK_INTERNAL, "block_cg: DMMA kernel cannot be resident");
     const int E = S * S + S;
 
     void *pB, *pX, *pR, *pP, *pW, *pPart, *pRed, *pRep;
@@ -944,8 +1101,8 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
         BK_CUDA_TRY(ctx, cudaMemsetAsync(a.prof, 0, PROF_ITERS * PROF_MARKS * sizeof(long long),
                                          ctx->stream));
     void* args[] = {&a};
-    BK_CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)nb), dim3(BS),
-                                                 args, smem, ctx->stream));
+    BK_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(kern, dim3((unsigned)nb), dim3(BS), args, smem,
+                                                 ctx->stream));
     ++ctx->launches;
     if (padded) BK_CUDA_TRY(ctx, launch_pad_cols(ctx, (const double*)pX, S, X, s, n));
     BK_CUDA_TRY(ctx, cudaMemcpyAsync(rep, pRep, sizeof(CgReport), cudaMemcpyDeviceToHost,
@@ -957,20 +1114,23 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
         // mean phase durations over the recorded iterations (ns)
         double acc[PROF_MARKS] = {};
         int cnt = 0;
+        double loop1 = 0, loop2 = 0;
         for (int i = 1; i < PROF_ITERS; ++i) {
             const long long* r = pr.data() + i * PROF_MARKS;
             if (!r[0] || !r[7]) continue;
-            for (int k = 1; k < PROF_MARKS; ++k) acc[k] += (double)(r[k] - r[k - 1]);
+            for (int k = 1; k < 8; ++k) acc[k] += (double)(r[k] - r[k - 1]);
+            loop1 += (double)(r[8] - r[0]);
+            loop2 += (double)(r[9] - r[3]);
             acc[0] += (double)(pr[(i + 1) * PROF_MARKS] ? pr[(i + 1) * PROF_MARKS] - r[7] : 0);
             ++cnt;
         }
         if (cnt)
             fprintf(stderr,
-                    "[bk_cg_profile S=%d nb=%lld] per-iteration ns: phase1 %.0f | reduceG %.0f | "
+                    "[bk_cg_profile S=%d nb=%lld res=%d] per-iteration ns: phase1 %.0f | reduceG %.0f | "
                     "solve_a %.0f | phase2 %.0f | reduceS %.0f | control+solve_b %.0f | "
-                    "phase3+sync %.0f (over %d iterations)\n",
-                    S, (long long)nb, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
-                    acc[5] / cnt, acc[6] / cnt, acc[7] / cnt, cnt);
+                    "phase3+sync %.0f (over %d iterations); tile loops: phase1 %.0f phase2 %.0f\n",
+                    S, (long long)nb, (int)resident, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
+                    acc[5] / cnt, acc[6] / cnt, acc[7] / cnt, cnt, loop1 / cnt, loop2 / cnt);
     }
     return BK_OK;
 }
