@@ -118,6 +118,8 @@ struct CgReport {
 // host (one small D2H at the end of the solve).
 bk_status block_cg_device(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
                           const bk_solver_cfg* cfg, double* X, CgReport* rep);
+bk_status block_cg_large(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
+                         const bk_solver_cfg* cfg, double* X, CgReport* rep);
 bk_status block_cg_generic(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
                            const bk_solver_cfg* cfg, double* X, CgReport* rep);
 

@@ -1,0 +1,201 @@
+// Shared s x s solve and shared-memory strides for the block-CG kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace bkcg {
+
+static __device__ long long* g_ss_prof = nullptr;  // debug: small-solve step timestamps
+
+// Shared-memory row strides chosen for conflict-free 64-bit fragment access:
+// S + 4 makes the DMMA fragment loads [(4k + t) * RS + 8n + g] hit 16 distinct
+// 8-byte bank slots per half-warp; the odd 2S + 1 makes the Gauss-Jordan
+// column walk aug[i][p] conflict-free.
+template <int S>
+struct Strides {
+    static constexpr int RS = S + 4;      // tile / coefficient rows
+    static constexpr int LD = 2 * S + 1;  // augmented [M | RHS] rows
+};
+
+// Warp-wide argmax of non-negative doubles through their IEEE bit patterns
+// (monotone for x >= 0). The low 6 bits of the pattern are replaced by
+// (63 - index), so two integer REDUX steps return both the winner and (up to
+// the 2^-46 relative truncation) its value; exact ties keep the lowest index,
+// as the reference's strict '>' scan does. key = 0 excludes an entry.
+__device__ __forceinline__ unsigned long long pivot_key(double v, int idx) {
+    return v > 0.0 ? (((unsigned long long)__double_as_longlong(v) & ~63ull) |
+                      (unsigned long long)(63 - idx))
+                   : 0ull;
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long key) {
+    const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+    const unsigned hi = __reduce_max_sync(0xffffffffu, khi);
+    const unsigned lo = __reduce_max_sync(0xffffffffu, khi == hi ? klo : 0u);
+    return ((unsigned long long)hi << 32) | lo;
+}
+
+__device__ __forceinline__ unsigned long long pos_bits(double v) {
+    return v > 0.0 ? (unsigned long long)__double_as_longlong(v) : 0ull;
+}
+
+// out = M^+ RHS on the active block (zero rows/columns elsewhere), the
+// semantics of PivotedCholesky(M).solve(RHS) (solvers.cpp:347-414): diagonal
+// pivoting on the largest remaining Schur-complement diagonal, rank cutoff
+// max(max_diag * s * eps, DBL_MIN), directions beyond the numerical rank get
+// zero coefficients. Computed as Gauss-Jordan on [M | RHS] with that pivot
+// sequence (the trailing block of Gauss-Jordan IS the Cholesky Schur
+// complement, so pivots and rank decisions coincide). One barrier per pivot;
+// every warp redundantly tracks the Schur diagonal in registers and searches
+// the next pivot while the block update of the current one is in flight.
+// SMT: any shared-memory struct with int sa, rank, idx[S]; double aug[S*LD+2S].
+template <int S, int BS, bool PROF = false, int VAR = 0, class SMT>
+__device__ void small_solve_t(SMT& sm, const double* M, const double* RHS, double* out) {
+    long long* const pr = PROF ? g_ss_prof : nullptr;
+    auto stamp = [&](int k) {
+        if (PROF && threadIdx.x == 0) pr[k] = clock64();
+    };
+    auto wbar = []() { __syncthreads(); };
+    constexpr int NW = BS / 32;
+    constexpr int LD = Strides<S>::LD;
+    constexpr int RS = Strides<S>::RS;
+    constexpr int R = (S + 31) / 32;  // diagonal entries per lane (index lane + 32 r)
+    static_assert(R <= 2, "S <= 64");
+    const int sa = sm.sa;
+    double* aug = sm.aug;
+    unsigned long long donem = 0ull;  // compacted indices already used as pivots
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // rows by warp, columns by lane: no integer division, conflict-free rows
+    for (int i = warp; i < sa; i += NW) {
+        const int a = sm.idx[i];
+        for (int q = lane; q < 2 * sa; q += 32) {
+            double v;
+            if (q < sa) {
+                const int b = sm.idx[q];
+                v = a <= b ? M[a * S + b] : M[b * S + a];
+            } else {
+                const int b = sm.idx[q - sa];
+                v = a <= b ? RHS[a * S + b] : RHS[b * S + a];
+            }
+            aug[i * LD + q] = v;
+        }
+    }
+    wbar();
+    double dg[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        dg[r] = i < sa ? aug[i * LD + i] : 0.0;
+    }
+    auto search = [&](unsigned long long excl) -> unsigned long long {
+        unsigned long long key = 0ull;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int i = lane + 32 * r;
+            const unsigned long long kk = (i < sa && !((excl >> i) & 1ull)) ? pivot_key(dg[r], i) : 0ull;
+            key = kk > key ? kk : key;
+        }
+        return warp_max_u64(key);
+    };
+    stamp(0);
+    unsigned long long best = search(0ull);
+    // max_diag of the active block (the reference clamps its scan at 0)
+    const int im = best ? 63 - (int)(best & 63ull) : -1;
+    const double maxd = im >= 0 ? aug[im * LD + im] : 0.0;
+    const double cutoff = fmax(maxd * sa * 2.220446049250313e-16, 2.2250738585072014e-308);
+    // exact value of the pivot encoded in `key` (the key is truncated in its
+    // low 6 bits), held in lane (p & 31) of dg
+    auto pivot_of = [&](unsigned long long key, int& p, double& pv) {
+        p = key ? 63 - (int)(key & 63ull) : -1;
+        const int src = p < 0 ? 0 : (p & 31);
+        pv = __shfl_sync(0xffffffffu, dg[0], src);
+        if (R > 1) {
+            const double pv1 = __shfl_sync(0xffffffffu, dg[R - 1], src);
+            if (p >= 32) pv = pv1;
+        }
+        if (p < 0) pv = 0.0;
+    };
+    int p;
+    double pv;
+    pivot_of(best, p, pv);
+    double rinv = __drcp_rn(pv);
+    int rank = 0;
+    stamp(1);
+    constexpr int RPW = (S + NW - 1) / NW;    // rows per warp
+    constexpr int CPL = (2 * S + 31) / 32;    // columns per lane
+    while (p >= 0 && pv > cutoff) {           // uniform: beyond the rank -> stop
+        donem |= 1ull << p;
+        // operands of this pivot's block update and of the Schur-diagonal
+        // update (row p and column p are not written by this step)
+        double apq[CPL], fi[RPW], aiq[RPW][CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int q = lane + 32 * c;
+            apq[c] = q < 2 * sa ? aug[p * LD + q] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+            const int i = warp + NW * r;
+            fi[r] = i < sa ? aug[i * LD + p] : 0.0;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                const int q = lane + 32 * c;
+                aiq[r][c] = (i < sa && q < 2 * sa) ? aug[i * LD + q] : 0.0;
+            }
+        }
+        double colp[R], rowp[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int i = lane + 32 * r;
+            colp[r] = i < sa ? aug[i * LD + p] : 0.0;
+            rowp[r] = i < sa ? aug[p * LD + i] : 0.0;
+        }
+        // block update (issued first so it overlaps the pivot search below)
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+            const int i = warp + NW * r;
+            if (i >= sa || i == p) continue;
+            const double f = fi[r] * rinv;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                const int q = lane + 32 * c;
+                if (q >= 2 * sa || (q < sa && ((donem >> q) & 1ull))) continue;
+                aug[i * LD + q] = fma(-f, apq[c], aiq[r][c]);
+            }
+        }
+        // Schur diagonal after this pivot (same arithmetic as aug[i][i] above)
+        // and the next pivot with its reciprocal, before the barrier
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int i = lane + 32 * r;
+            if (i < sa && !((donem >> i) & 1ull)) dg[r] = fma(-(colp[r] * rinv), rowp[r], dg[r]);
+        }
+        unsigned long long nb = search(donem);
+        if (VAR == 2) nb = (p + 1 < sa) ? ((1ull << 32) | (unsigned long long)(63 - (p + 1))) : 0ull;
+        int pn;
+        double pvn;
+        pivot_of(nb, pn, pvn);
+        const double rn = __drcp_rn(pvn > 0.0 ? pvn : 1.0);
+        ++rank;
+        if (VAR != 3) wbar();
+        stamp(2 + rank);
+        p = pn;
+        pv = pvn;
+        rinv = rn;
+    }
+    for (int e = threadIdx.x; e < S * RS; e += BS) out[e] = 0.0;
+    wbar();
+    for (int i = warp; i < sa; i += NW) {
+        if (!((donem >> i) & 1ull)) continue;
+        const double di = __drcp_rn(aug[i * LD + i]);
+        for (int q = lane; q < sa; q += 32) out[sm.idx[i] * RS + sm.idx[q]] = aug[i * LD + sa + q] * di;
+    }
+    if (threadIdx.x == 0) sm.rank = rank;
+    __syncthreads();
+    stamp(63);
+}
+
+
+}  // namespace bkcg
