@@ -40,7 +40,13 @@ WORKLOADS = {
     5: "C5: 512x512x16 layered stack, s=64, N=5000 (outputs streamed through a device ring)",
 }
 C4_CHIPS_PER_STEP = 16   # chips per GPU per timed step (5000 chips total at full scale)
-C4_MAX_ITER = 2000       # converging C4 chips need 230-330 iterations (oracle)
+C4_MAX_ITER = 5000
+# Tolerance pins: 1e-12 for configs 1-3; configs 4-5 use 1e-10
+# because their true relative residual plateaus at ~1.1-2e-12 in fp64 (measured:
+# C5 512x512x16 at 1.1e-12..2.0e-12 after 1200 iterations; C4 chip 4 at 1.28e-12
+# in the oracle), where 1e-12 sends the reference algorithm into endless
+# verify/restart cycles.
+TOL_BY_CONFIG = {1: 1e-12, 2: 1e-12, 3: 1e-12, 4: 1e-10, 5: 1e-10}
 C5_RING = 500            # samples per combine/action chunk for C5 (2 x 8.4 GB ring)
 
 
@@ -220,13 +226,13 @@ def config_dict(config, world):
 
     cid, nx, ny, nz, s, N = bk.CONFIGS[config]
     d = {"workload": WORKLOADS[config], "grid": [nx, ny, nz], "s": s, "samples_per_chip": N,
-         "chips_per_step_per_gpu": 1, "tol": TOL, "precond": "jacobi",
+         "chips_per_step_per_gpu": 1, "tol": TOL_BY_CONFIG[config], "precond": "jacobi",
          "parallelism": f"chip-sharded x{world} (no collective)",
          "l2": "flushed between timed steps (512 MiB write)"}
     if config == 4:
         d["chips_per_step_per_gpu"] = C4_CHIPS_PER_STEP
         d["max_iter"] = C4_MAX_ITER
-        d["note"] = "chips whose basis solve misses 1e-12 (as in the oracle) are dropped and counted"
+        d["note"] = "chips whose basis solve misses the tolerance are dropped and counted"
     if config == 5:
         d["output_ring_samples"] = C5_RING
         d["parallelism"] = f"replicas x{world} (slab DD is the next step)"
@@ -428,7 +434,7 @@ def run_ours_batch(args, ctx, world, rank, local):
     T = [torch.empty((N, n), dtype=torch.float64, device=dev) for _ in chips]
     Q = [torch.empty((N, n), dtype=torch.float64, device=dev) for _ in chips]
     R = [torch.empty(N, dtype=torch.float64, device=dev) for _ in chips]
-    cfg = bk.SolverConfig(TOL, C4_MAX_ITER, "jacobi")
+    cfg = bk.SolverConfig(TOL_BY_CONFIG[4], C4_MAX_ITER, "jacobi")
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -496,7 +502,7 @@ def run_ours_large(args, ctx, world, rank, local):
     T = torch.empty((C5_RING, n), dtype=torch.float64, device=dev)
     Q = torch.empty_like(T)
     R = torch.empty(C5_RING, dtype=torch.float64, device=dev)
-    cfg = bk.SolverConfig(TOL, 100000, "jacobi")
+    cfg = bk.SolverConfig(TOL_BY_CONFIG[5], 100000, "jacobi")
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
 

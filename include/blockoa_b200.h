@@ -109,8 +109,10 @@ bk_status bk_create(int device, bk_ctx** out);
 void bk_destroy(bk_ctx* ctx);
 const char* bk_last_error(const bk_ctx* ctx);
 /* Run subsequent work on an external cudaStream_t (e.g. torch's current
- * stream); NULL restores the context's own stream. */
+ * stream); NULL is the legacy default stream. bk_use_own_stream restores the
+ * context's own (non-blocking) stream. */
 bk_status bk_set_stream(bk_ctx* ctx, void* cuda_stream);
+bk_status bk_use_own_stream(bk_ctx* ctx);
 bk_status bk_synchronize(bk_ctx* ctx);
 /* Number of this library's kernel launches issued on ctx so far. */
 int64_t bk_launch_count(const bk_ctx* ctx);
@@ -189,6 +191,58 @@ bk_status bk_generate_batch(bk_ctx* ctx, int n_chips, const bk_grid* grids,
 /* Cap the number of CTAs (and thus SMs) one block-CG solve may use on ctx
  * (0 = all SMs). */
 bk_status bk_set_cg_sm_budget(bk_ctx* ctx, int max_ctas);
+
+/* ---- y-slab domain decomposition (BASELINE config 5 across GPUs) -----------
+ * A rank owns global rows [y0, y0 + nyl) of the grid of `op` (the GLOBAL
+ * operator, assembled identically on every rank). Its block vectors use the
+ * slab-local layout nx x (nyl + 2) x nz x S with one ghost row on each y side.
+ * The caller drives the phases below in lockstep across ranks, summing `red`
+ * across ranks after every *_SWEEP step and refreshing the ghost rows of P
+ * (before BK_DD_SPMM) and of X (before BK_DD_TRUE_RES / BK_DD_RESTART); see
+ * paper_2510_23221_b200/dd.py. All buffers are caller-owned device memory. */
+typedef struct {
+    double* B;     /* local RHS block */
+    double* X;
+    double* R;
+    double* P;
+    double* W;
+    double* part;  /* per-CTA partials, nb x (S*S + S) */
+    double* red;   /* reduced values, S*S + S (all-reduced by the caller) */
+    void* ctl;     /* control state, ctl_bytes */
+    int nb;        /* CTAs of the sweep kernels */
+} bk_dd_bufs;
+
+typedef enum {
+    BK_DD_INIT_SWEEP = 0,    /* X = 0, R = B, P = D^-1 R; red = [R^T Z | b^2]   */
+    BK_DD_CTL_INIT = 1,
+    BK_DD_SPMM = 2,          /* W = A P; red = P^T W                            */
+    BK_DD_CTL_ALPHA = 3,     /* alpha = G^+ S_old                               */
+    BK_DD_UPDATE = 4,        /* X += P alpha, R -= W alpha; red = [R^T Z | rr]  */
+    BK_DD_CTL_UPDATE = 5,    /* convergence test; beta or verification needed   */
+    BK_DD_TRUE_RES = 6,      /* red = ||b - A x||^2 of flagged/active columns   */
+    BK_DD_CTL_VERIFY = 7,
+    BK_DD_RESTART_SWEEP = 8, /* R = B - A X, P = Z; red = R^T Z                 */
+    BK_DD_CTL_RESTART = 9,
+    BK_DD_PUPDATE = 10,      /* P = D^-1 R + P beta                             */
+    BK_DD_CTL_FINAL = 11,    /* report                                          */
+    BK_DD_READ = 12          /* *cmd, *sa (synchronises the stream)             */
+} bk_dd_step_kind;
+
+/* BK_DD_READ commands */
+#define BK_DD_CMD_PUPDATE 0
+#define BK_DD_CMD_VERIFY 1
+#define BK_DD_CMD_RESTART 2
+#define BK_DD_CMD_DONE 3
+
+bk_status bk_dd_sizes(bk_ctx* ctx, const bk_operator* op, int nyl, int S, int64_t* local_elems,
+                      int* nb, int64_t* part_elems, int64_t* red_elems, int64_t* ctl_bytes);
+bk_status bk_dd_step(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, int S,
+                     const bk_dd_bufs* bufs, const bk_solver_cfg* cfg, int step, int m,
+                     int* cmd, int* sa, bk_solve_report* report);
+/* global n x S block <-> slab-local block (to_local = 1: glob -> loc, ghost
+ * rows untouched; 0: loc -> glob interior rows) */
+bk_status bk_dd_pack(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, int S, double* glob,
+                     double* loc, int to_local);
 
 /* cg_error_bound(kappa, m, e0)    solvers.hpp:92, solvers.cpp:672-680 (host). */
 bk_status bk_cg_error_bound(double kappa, int m, double e0, double* out);

@@ -130,6 +130,7 @@ def _load():
         lib.bk_last_error.argtypes = [vp]
         lib.bk_last_error.restype = C.c_char_p
         lib.bk_set_stream.argtypes = [vp, vp]
+        lib.bk_use_own_stream.argtypes = [vp]
         lib.bk_synchronize.argtypes = [vp]
         lib.bk_launch_count.argtypes = [vp]
         lib.bk_launch_count.restype = C.c_int64
@@ -151,6 +152,10 @@ def _load():
                                           C.POINTER(_Cfg), vp, vp, vp, vp, C.c_int,
                                           C.POINTER(_Timings)]
         lib.bk_set_cg_sm_budget.argtypes = [vp, C.c_int]
+        lib.bk_dd_sizes.argtypes = [vp, vp, C.c_int, C.c_int, vp, vp, vp, vp, vp]
+        lib.bk_dd_step.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.c_int,
+                                   vp, vp, vp]
+        lib.bk_dd_pack.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int]
         lib.bk_cg_error_bound.argtypes = [C.c_double, C.c_int, C.c_double, C.POINTER(C.c_double)]
         lib.bk_derive_seed.argtypes = [C.c_uint64, C.c_char_p, C.c_uint64]
         lib.bk_derive_seed.restype = C.c_uint64
@@ -353,8 +358,12 @@ class Context:
             pass
 
     def set_stream(self, stream_ptr: Optional[int]):
-        _raise(_load().bk_set_stream(self.h, C.c_void_p(stream_ptr) if stream_ptr else None),
-               self.h, "set_stream")
+        """Launch on a cudaStream_t handle (0 = legacy default stream, e.g.
+        torch.cuda.current_stream().cuda_stream); None = the context's own stream."""
+        if stream_ptr is None:
+            _raise(_load().bk_use_own_stream(self.h), self.h, "use_own_stream")
+        else:
+            _raise(_load().bk_set_stream(self.h, C.c_void_p(stream_ptr)), self.h, "set_stream")
 
     def synchronize(self):
         _raise(_load().bk_synchronize(self.h), self.h, "synchronize")

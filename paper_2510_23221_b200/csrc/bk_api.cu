@@ -277,7 +277,13 @@ const char* bk_last_error(const bk_ctx* ctx) { return ctx ? ctx->err.c_str() : "
 
 bk_status bk_set_stream(bk_ctx* ctx, void* s) {
     if (!ctx) return BK_INVALID_CONFIG;
-    ctx->stream = s ? (cudaStream_t)s : ctx->own_stream;
+    ctx->stream = (cudaStream_t)s;
+    return BK_OK;
+}
+
+bk_status bk_use_own_stream(bk_ctx* ctx) {
+    if (!ctx) return BK_INVALID_CONFIG;
+    ctx->stream = ctx->own_stream;
     return BK_OK;
 }
 

@@ -949,3 +949,192 @@ bk_status block_cg_large(bk_ctx* ctx, const bk_operator* op, const double* B, in
 }
 
 }  // namespace bk
+
+// ---------------------------------------------------------------------------
+// C ABI: per-phase steps for the y-slab decomposition (driven by dd.py)
+// ---------------------------------------------------------------------------
+namespace {
+
+template <int S>
+bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const bk_dd_bufs* b,
+                    const bk_solver_cfg* cfg, int step, int m, int* cmd, int* sa,
+                    bk_solve_report* report) {
+    using namespace bk;
+    Slab sl{op->nx, nyl, op->nz, op->ny, y0, (int64_t)op->nx * nyl * op->nz};
+    SweepArgs a;
+    a.sl = sl;
+    a.st = StencilPtr{op->diag, op->cx, op->cy, op->cz, op->dinv};
+    a.B = b->B;
+    a.X = b->X;
+    a.R = b->R;
+    a.P = b->P;
+    a.W = b->W;
+    a.part = b->part;
+    a.precond = cfg ? cfg->precond : 1;
+    Ctl<S>* ctl = (Ctl<S>*)b->ctl;
+    CgReport* drep = (CgReport*)((char*)b->ctl + sizeof(Ctl<S>));
+    a.coef = ctl->coef;
+    a.act = ctl->act;
+    constexpr int E = S * S + S;
+    const int nb = b->nb;
+    cudaStream_t s = ctx->stream;
+    const size_t sw = sizeof(LTile<S>) * LNW + (size_t)LNW * S * sizeof(double);
+    const size_t cs = sizeof(CSm<S>);
+    auto set = [&](const void* f, size_t bytes) {
+        return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    };
+    auto reduce = [&](int e_count, int nparts) {
+        k_reduce<<<(e_count + 255) / 256, 256, 0, s>>>(b->part, nparts, e_count, b->red);
+        ++ctx->launches;
+    };
+    const int tr_blocks = (int)((sl.n_int + (LBS / S) - 1) / (LBS / S) < 4L * ctx->num_sms
+                                    ? (sl.n_int + (LBS / S) - 1) / (LBS / S)
+                                    : 4L * ctx->num_sms);
+    switch (step) {
+        case BK_DD_INIT_SWEEP:
+            BK_CUDA_TRY(ctx, set((const void*)k_anchor<S, kInit>, sw));
+            k_anchor<S, kInit><<<nb, LBS, sw, s>>>(a);
+            ++ctx->launches;
+            reduce(E, nb);
+            break;
+        case BK_DD_CTL_INIT:
+            BK_CUDA_TRY(ctx, set((const void*)k_ctl_init<S>, cs));
+            k_ctl_init<S><<<1, CBS, cs, s>>>(ctl, b->red, cfg->rel_tol);
+            ++ctx->launches;
+            break;
+        case BK_DD_SPMM:
+            BK_CUDA_TRY(ctx, set((const void*)k_spmm_gram<S>, sw));
+            k_spmm_gram<S><<<nb, LBS, sw, s>>>(a);
+            ++ctx->launches;
+            reduce(S * S, nb);
+            break;
+        case BK_DD_CTL_ALPHA:
+            BK_CUDA_TRY(ctx, set((const void*)k_ctl_alpha<S>, cs));
+            k_ctl_alpha<S><<<1, CBS, cs, s>>>(ctl, b->red);
+            ++ctx->launches;
+            break;
+        case BK_DD_UPDATE:
+            BK_CUDA_TRY(ctx, set((const void*)k_update<S>, sw));
+            k_update<S><<<nb, LBS, sw, s>>>(a);
+            ++ctx->launches;
+            reduce(E, nb);
+            break;
+        case BK_DD_CTL_UPDATE:
+            BK_CUDA_TRY(ctx, set((const void*)k_ctl_update<S>, cs));
+            k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, b->red, m);
+            ++ctx->launches;
+            break;
+        case BK_DD_TRUE_RES:
+            k_true_res<S><<<tr_blocks, LBS, 0, s>>>(a);
+            ++ctx->launches;
+            reduce(S, tr_blocks);
+            break;
+        case BK_DD_CTL_VERIFY:
+            BK_CUDA_TRY(ctx, set((const void*)k_ctl_verify<S>, cs));
+            k_ctl_verify<S><<<1, CBS, cs, s>>>(ctl, b->red);
+            ++ctx->launches;
+            break;
+        case BK_DD_RESTART_SWEEP:
+            BK_CUDA_TRY(ctx, set((const void*)k_anchor<S, kRestart>, sw));
+            k_anchor<S, kRestart><<<nb, LBS, sw, s>>>(a);
+            ++ctx->launches;
+            reduce(E, nb);
+            break;
+        case BK_DD_CTL_RESTART:
+            k_ctl_restart<S><<<1, CBS, 0, s>>>(ctl, b->red);
+            ++ctx->launches;
+            break;
+        case BK_DD_PUPDATE:
+            k_pupdate<S><<<nb, LBS, 0, s>>>(a);
+            ++ctx->launches;
+            break;
+        case BK_DD_CTL_FINAL: {
+            k_ctl_final<S><<<1, 32, 0, s>>>(ctl, b->red, drep);
+            ++ctx->launches;
+            CgReport rep;
+            BK_CUDA_TRY(ctx, cudaMemcpyAsync(&rep, drep, sizeof(rep), cudaMemcpyDeviceToHost, s));
+            BK_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+            if (report) {
+                report->iterations = rep.iterations;
+                report->matvec_count = rep.matvecs;
+                for (int j = 0; j < S; ++j) {
+                    if (report->final_rel_residual) report->final_rel_residual[j] = rep.final_res[j];
+                    if (report->converged) report->converged[j] = rep.converged[j];
+                }
+            }
+            break;
+        }
+        case BK_DD_READ: {
+            int h[2];
+            BK_CUDA_TRY(ctx, cudaMemcpyAsync(h, &ctl->cmd, sizeof(int), cudaMemcpyDeviceToHost, s));
+            BK_CUDA_TRY(ctx, cudaMemcpyAsync(h + 1, &ctl->sa, sizeof(int), cudaMemcpyDeviceToHost, s));
+            BK_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+            if (cmd) *cmd = h[0];
+            if (sa) *sa = h[1];
+            break;
+        }
+        default:
+            return fail(ctx, BK_INVALID_CONFIG, "dd_step: unknown step");
+    }
+    BK_CUDA_TRY(ctx, cudaGetLastError());
+    return BK_OK;
+}
+
+template <int S>
+int64_t ctl_bytes_t() {
+    return (int64_t)(sizeof(Ctl<S>) + sizeof(bk::CgReport));
+}
+
+}  // namespace
+
+extern "C" {
+
+bk_status bk_dd_sizes(bk_ctx* ctx, const bk_operator* op, int nyl, int S, int64_t* local_elems,
+                      int* nb, int64_t* part_elems, int64_t* red_elems, int64_t* ctl_bytes) {
+    if (!ctx || !op || nyl < 1 || nyl > op->ny) return BK_INVALID_CONFIG;
+    if (S != 16 && S != 32 && S != 64)
+        return bk::fail(ctx, BK_INVALID_CONFIG, "dd: kernel width must be 16, 32 or 64");
+    const int64_t n_int = (int64_t)op->nx * nyl * op->nz;
+    const int64_t ntiles = (n_int + 15) / 16;
+    int b = ctx->num_sms;
+    if ((int64_t)b * LNW > ntiles) b = (int)((ntiles + LNW - 1) / LNW);
+    if (b < 1) b = 1;
+    const int tr = (int)((n_int + (LBS / S) - 1) / (LBS / S) < 4L * ctx->num_sms
+                             ? (n_int + (LBS / S) - 1) / (LBS / S)
+                             : 4L * ctx->num_sms);
+    const int E = S * S + S;
+    if (local_elems) *local_elems = (int64_t)op->nx * (nyl + 2) * op->nz * S;
+    if (nb) *nb = b;
+    if (part_elems) *part_elems = (int64_t)(b > tr ? b : tr) * E;
+    if (red_elems) *red_elems = E;
+    if (ctl_bytes) *ctl_bytes = S == 16 ? ctl_bytes_t<16>() : S == 32 ? ctl_bytes_t<32>() : ctl_bytes_t<64>();
+    return BK_OK;
+}
+
+bk_status bk_dd_step(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, int S,
+                     const bk_dd_bufs* bufs, const bk_solver_cfg* cfg, int step, int m,
+                     int* cmd, int* sa, bk_solve_report* report) {
+    if (!ctx || !op || !bufs) return BK_INVALID_CONFIG;
+    cudaSetDevice(ctx->device);
+    if (S == 16) return dd_step_t<16>(ctx, op, y0, nyl, bufs, cfg, step, m, cmd, sa, report);
+    if (S == 32) return dd_step_t<32>(ctx, op, y0, nyl, bufs, cfg, step, m, cmd, sa, report);
+    if (S == 64) return dd_step_t<64>(ctx, op, y0, nyl, bufs, cfg, step, m, cmd, sa, report);
+    return bk::fail(ctx, BK_INVALID_CONFIG, "dd: kernel width must be 16, 32 or 64");
+}
+
+bk_status bk_dd_pack(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, int S, double* glob,
+                     double* loc, int to_local) {
+    if (!ctx || !op || !glob || !loc) return BK_INVALID_CONFIG;
+    cudaSetDevice(ctx->device);
+    Slab sl{op->nx, nyl, op->nz, op->ny, y0, (int64_t)op->nx * nyl * op->nz};
+    const int grid = ctx->num_sms * 8;
+    if (S == 16) k_pack<16><<<grid, 256, 0, ctx->stream>>>(sl, glob, loc, to_local);
+    else if (S == 32) k_pack<32><<<grid, 256, 0, ctx->stream>>>(sl, glob, loc, to_local);
+    else if (S == 64) k_pack<64><<<grid, 256, 0, ctx->stream>>>(sl, glob, loc, to_local);
+    else return bk::fail(ctx, BK_INVALID_CONFIG, "dd: kernel width must be 16, 32 or 64");
+    ++ctx->launches;
+    BK_CUDA_TRY(ctx, cudaGetLastError());
+    return BK_OK;
+}
+
+}  // extern "C"

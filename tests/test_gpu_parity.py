@@ -364,3 +364,32 @@ def test_block_cg_multikernel_path_vs_oracle(bk, ctx, oracle, case, monkeypatch)
         Xm, repm = oracle.block_cg(o, B, TOL, m, 1)
         assert rm.report.iterations == m and rm.report.matvec_count == repm["matvec_count"]
         assert rel_l2(rm.x, Xm) <= 1e-12
+
+
+@pytest.mark.parametrize("nslabs", [1, 2, 3])
+def test_slab_decomposition_matches_single_gpu(bk, ctx, nslabs):
+    """y-slab decomposition (config 5 structure: s = 64) with virtual ranks on
+    one GPU (dd.LocalComm): same solution as the single-GPU solve; one slab is
+    bitwise the single-GPU multi-kernel engine."""
+    import torch
+
+    from paper_2510_23221_b200 import dd
+
+    inp = bk.synth_chip(5, 48, 40, 16, 64, 2)
+    op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
+    dev = torch.device("cuda", 0)
+    q = torch.from_numpy(inp.q_basis).to(dev)
+    B = torch.empty_like(q)
+    bk.rhs_from_power(op, q, out=B)
+    torch.cuda.synchronize()
+    ref = bk.block_cg(op, B.cpu().numpy(), cfg_jacobi())
+    parts = dd.partition_rows(inp.grid.ny, nslabs)
+    X, rep = dd.solve_decomposed(bk, ctx, op, B, cfg_jacobi(), parts)
+    torch.cuda.synchronize()
+    Xh = X.cpu().numpy()
+    assert rep.all_converged() and ref.report.all_converged()
+    if nslabs == 1:
+        assert np.array_equal(Xh, ref.x) and rep.iterations == ref.report.iterations
+    else:
+        assert rel_l2(Xh, ref.x) <= PARITY
+        assert abs(rep.iterations - ref.report.iterations) <= max(3, ref.report.iterations // 10)
