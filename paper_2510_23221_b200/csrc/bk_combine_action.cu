@@ -13,7 +13,8 @@
 // pass for q.
 //
 // Bitwise contract: T uses the reference's per-element order (first term a
-// product, then one fma per basis column in ascending order); A T uses the
+// product, then one fma per basis column in ascending order — the DMMA's
+// accumulation order, verified bitwise); A T uses the
 // scalar CsrMatrix::apply order (separate multiply and add, CSR column order);
 // q = (y - g) / V is correctly rounded. So given the same X, T and q equal the
 // reference's bit for bit (tests/test_gpu_parity.py checks it).
@@ -49,47 +50,73 @@ __device__ __forceinline__ double div_rn(double x, double v, double r) {
     return fma(e, r, q0);
 }
 
+__device__ __forceinline__ void dmma_c(double (&d)[4], double a0, double a1, double b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+        "{%0,%1,%2,%3};"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a0), "d"(a1), "d"(b));
+}
+
+constexpr int CSTRIDE(int NS) { return NS + 4; }  // conflict-free B-fragment rows
+
 // T for one z-plane of the tile + halo into buf[q * HC + h] (sample-major, so
-// the stencil's neighbour reads and these stores are bank-conflict free).
+// the stencil's neighbour reads are bank-conflict free), on FP64 tensor cores:
+// T (halo cells x NS samples) = X_rows (cells x S) . C (S x NS) as m16n8k4 DMMA
+// with M = cells, N = samples, K = basis columns. The DMMA accumulates in k
+// order with one rounding per multiply-add — measured bitwise identical to the
+// reference's fma chain (scripts/dmma_bitwise.cu: 0 of 25600 differ) — so T
+// stays bitwise the reference's combine_from_weights.
 template <int S, int NS>
 __device__ __forceinline__ void form_plane(const ActArgs& a, int x0, int y0, int z,
                                            const double* __restrict__ Cs, double* __restrict__ buf) {
-    constexpr int H = NS / 2;
+    constexpr int CS = CSTRIDE(NS);
+    constexpr int MTILES = (HC + 15) / 16;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int64_t plane = (int64_t)a.nx * a.ny;
-    for (int it = threadIdx.x; it < HC * 2; it += NT) {
-        const int h = it % HC, half = it / HC;
-        const int gx = x0 - 1 + h % HX, gy = y0 - 1 + h / HX;
-        double t[H];
-        if (gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny) {
-            const double* xr = a.X + (gx + (int64_t)a.nx * gy + plane * z) * S;
-            const double* cs = Cs + half * H;
-            const double2 x01 = *reinterpret_cast<const double2*>(xr);
+    for (int mt = warp; mt < MTILES; mt += NT / 32) {
+        const int h0 = 16 * mt + g, h1 = h0 + 8;
+        const double* xr[2];
+        bool in[2];
 #pragma unroll
-            for (int q = 0; q < H; ++q) t[q] = x01.x * cs[q];
+        for (int r = 0; r < 2; ++r) {
+            const int h = r ? h1 : h0;
+            const int gx = x0 - 1 + h % HX, gy = y0 - 1 + h / HX;
+            in[r] = h < HC && gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny;
+            xr[r] = a.X + (gx + (int64_t)a.nx * gy + plane * z) * S;
+        }
+        double d[NS / 8][4];
 #pragma unroll
-            for (int q = 0; q < H; ++q) t[q] = fma(cs[NS + q], x01.y, t[q]);
+        for (int n = 0; n < NS / 8; ++n)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d[n][e] = 0.0;
 #pragma unroll 4
-            for (int k = 2; k < S; k += 2) {
-                const double2 xv = *reinterpret_cast<const double2*>(xr + k);
+        for (int ks = 0; ks < S / 4; ++ks) {
+            const double a0 = in[0] ? xr[0][4 * ks + t] : 0.0;
+            const double a1 = in[1] ? xr[1][4 * ks + t] : 0.0;
 #pragma unroll
-                for (int q = 0; q < H; ++q) t[q] = fma(cs[k * NS + q], xv.x, t[q]);
-#pragma unroll
-                for (int q = 0; q < H; ++q) t[q] = fma(cs[(k + 1) * NS + q], xv.y, t[q]);
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < H; ++q) t[q] = 0.0;
+            for (int n = 0; n < NS / 8; ++n) dmma_c(d[n], a0, a1, Cs[(4 * ks + t) * CS + 8 * n + g]);
         }
 #pragma unroll
-        for (int q = 0; q < H; ++q) buf[(half * H + q) * HC + h] = t[q];
+        for (int n = 0; n < NS / 8; ++n) {
+            const int q = 8 * n + 2 * t;
+            if (h0 < HC) {
+                buf[q * HC + h0] = d[n][0];
+                buf[(q + 1) * HC + h0] = d[n][1];
+            }
+            if (h1 < HC) {
+                buf[q * HC + h1] = d[n][2];
+                buf[(q + 1) * HC + h1] = d[n][3];
+            }
+        }
     }
 }
 
 template <int S, int NS>
 __global__ void __launch_bounds__(NT, 2) combine_action_kernel(ActArgs a) {
     extern __shared__ __align__(16) double sm[];
-    double* Cs = sm;                 // S x NS
-    double* ring = sm + S * NS;      // min(nz,3) x NS x HC
+    double* Cs = sm;                             // S x (NS + 4)
+    double* ring = sm + S * CSTRIDE(NS);         // min(nz,3) x NS x HC
     const int nring = a.nz < 3 ? a.nz : 3;
     const int tilesx = (a.nx + TX - 1) / TX;
     const int tile = blockIdx.x;
@@ -100,7 +127,7 @@ __global__ void __launch_bounds__(NT, 2) combine_action_kernel(ActArgs a) {
 
     for (int e = tid; e < S * NS; e += NT) {
         const int k = e / NS, q = e % NS;
-        Cs[e] = (k < a.s && j0 + q < a.N) ? a.C[(int64_t)k * a.N + j0 + q] : 0.0;
+        Cs[k * CSTRIDE(NS) + q] = (k < a.s && j0 + q < a.N) ? a.C[(int64_t)k * a.N + j0 + q] : 0.0;
     }
     __syncthreads();
 
@@ -238,7 +265,7 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
         a.part = (double*)p;
     }
     const int nring = op->nz < 3 ? op->nz : 3;
-    const size_t smem = (size_t)(S * NS + nring * HC * NS) * sizeof(double);
+    const size_t smem = (size_t)(S * CSTRIDE(NS) + nring * HC * NS) * sizeof(double);
     auto kern = combine_action_kernel<S, NS>;
     BK_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
