@@ -118,10 +118,13 @@ __global__ void __launch_bounds__(NT, 2) combine_action_kernel(ActArgs a) {
     double* Cs = sm;                             // S x (NS + 4)
     double* ring = sm + S * CSTRIDE(NS);         // min(nz,3) x NS x HC
     const int nring = a.nz < 3 ? a.nz : 3;
+    // grid: x = sample chunk (fastest), y = cell tile, so the CTAs resident at
+    // any moment share one tile's X rows through L2 instead of re-reading X
+    // from HBM once per chunk (config 5: X = 2.1 GB)
     const int tilesx = (a.nx + TX - 1) / TX;
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.y;
     const int x0 = (tile % tilesx) * TX, y0 = (tile / tilesx) * TY;
-    const int64_t j0 = (int64_t)blockIdx.y * NS;
+    const int64_t j0 = (int64_t)blockIdx.x * NS;
     const int tid = threadIdx.x;
     const int64_t plane = (int64_t)a.nx * a.ny;
 
@@ -270,8 +273,8 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
     BK_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
     const int64_t chunks = (N + NS - 1) / NS;
-    if (chunks > 65535) return fail(ctx, BK_INVALID_CONFIG, "combine_action: N too large per call");
-    kern<<<dim3(tiles, (unsigned)chunks), NT, smem, ctx->stream>>>(a);
+    if (tiles > 65535) return fail(ctx, BK_INVALID_CONFIG, "combine_action: grid too large");
+    kern<<<dim3((unsigned)chunks, (unsigned)tiles), NT, smem, ctx->stream>>>(a);
     ++ctx->launches;
     BK_CUDA_TRY(ctx, cudaGetLastError());
     if (resid) {
