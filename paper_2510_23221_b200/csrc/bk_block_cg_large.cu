@@ -88,56 +88,163 @@ __device__ __forceinline__ void lcell(const Slab& sl, const StencilPtr& st, int6
     }
 }
 
+// ---------------------------------------------------------------------------
+// sweep geometry
+//
+// A tile is a run of 16 consecutive x cells at fixed (y, z); tiles are walked
+// z-fastest (tile T: iz = T % nz, then x-run, then y), so the z +- 1
+// neighbours of a tile are the adjacent tiles processed by the same or the
+// neighbouring CTA in the same wave and the stencil reads P from HBM once.
+//
+// All 8 warps of a CTA work on the same TPB = 8 / (S / 8) tiles: warp w owns
+// tile slot ts = w / (S / 8) and the 8-column block cb = w % (S / 8). The
+// DMMA B fragments of alpha / beta (column block cb, all K) stay in registers
+// for the whole sweep, the A operand rows (P, W of the tile group) are staged
+// in shared memory by cp.async one group ahead, and the Gram G = U^T V of the
+// group is accumulated by warp-owned 16 x 8 output tiles.
+// ---------------------------------------------------------------------------
 template <int S>
-struct LTile {
-    static constexpr int RS = S + 4;
-    double u[16 * RS];  // A side of the Gram (rows = cells)
-    double v[16 * RS];  // B side
+struct Geo {
+    static constexpr int RS = S + 4;           // smem row stride (doubles)
+    static constexpr int NWC = S / 8;          // warps per tile
+    static constexpr int TPB = LNW / NWC;      // tiles per CTA step
+    static constexpr int CELLS = 16 * TPB;
+    static constexpr int TILE = CELLS * RS;    // doubles per staged block
+    static constexpr int MT = (S + 15) / 16, NT = S / 8, GT = MT * NT;
+    static constexpr int PER = (GT + LNW - 1) / LNW;
 };
 
-// CTA Gram over staged tiles: warp w owns (m, n) tiles w, w + LNW, ... of the
-// MT x NT tile grid of G = U^T V and accumulates them over every staged tile.
+__host__ __device__ __forceinline__ int n_tiles(const Slab& sl) {
+    return ((sl.nx + 15) / 16) * sl.nyl * sl.nz;
+}
+
+struct TileCells {
+    int64_t l0, g0;  // slab-local / global flat index of cell 0 of the run
+    int ix0, iyg, iz, nv;
+};
+
+__device__ __forceinline__ void tile_cells(const Slab& sl, int T, int ntiles, TileCells& tc) {
+    if (T >= ntiles) {
+        tc.l0 = tc.g0 = 0;
+        tc.ix0 = tc.iyg = tc.iz = 0;
+        tc.nv = 0;
+        return;
+    }
+    const int ntx = (sl.nx + 15) / 16;
+    tc.iz = T % sl.nz;
+    const int q = T / sl.nz;
+    tc.ix0 = 16 * (q % ntx);
+    const int iyl = 1 + q / ntx;
+    tc.iyg = sl.y0 + iyl - 1;
+    tc.l0 = tc.ix0 + (int64_t)sl.nx * (iyl + (int64_t)(sl.nyl + 2) * tc.iz);
+    tc.g0 = tc.ix0 + (int64_t)sl.nx * (tc.iyg + (int64_t)sl.ny * tc.iz);
+    tc.nv = sl.nx - tc.ix0 < 16 ? sl.nx - tc.ix0 : 16;
+}
+
+// stencil of cell r of a run (CSR values: -conductance off the diagonal)
+__device__ __forceinline__ void run_cell(const Slab& sl, const StencilPtr& st, const TileCells& tc,
+                                         int r, LCell& c) {
+    const int ix = tc.ix0 + r;
+    c.l = tc.l0 + r;
+    c.gi = tc.g0 + r;
+    c.hxm = ix > 0;
+    c.hxp = ix < sl.nx - 1;
+    c.hym = tc.iyg > 0;
+    c.hyp = tc.iyg < sl.ny - 1;
+    c.hzm = tc.iz > 0;
+    c.hzp = tc.iz < sl.nz - 1;
+    const int64_t plane = (int64_t)sl.nx * sl.ny;
+    c.d = st.diag[c.gi];
+    c.zm = c.hzm ? -st.cz[c.gi - plane] : 0.0;
+    c.ym = c.hym ? -st.cy[c.gi - sl.nx] : 0.0;
+    c.xm = c.hxm ? -st.cx[c.gi - 1] : 0.0;
+    c.xp = c.hxp ? -st.cx[c.gi] : 0.0;
+    c.yp = c.hyp ? -st.cy[c.gi] : 0.0;
+    c.zp = c.hzp ? -st.cz[c.gi] : 0.0;
+}
+
+__device__ __forceinline__ void cp16(double* smem, const double* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// stage NA row arrays of group `grp` (dst + a * TILE, a = 0 .. NA-1) plus,
+// when dinv != nullptr, D^-1 of its cells into dst + NA * TILE; the tile
+// geometry is computed once per chunk row and shared by all arrays
+template <int S, int NA>
+__device__ __forceinline__ void stage_multi(double* dst, const double* const (&src)[NA],
+                                            const double* __restrict__ dinv, const Slab& sl,
+                                            int grp, int ntiles) {
+    using G_ = Geo<S>;
+    constexpr int CPR = S / 2;
+    constexpr int TOT = G_::CELLS * CPR;
+    static_assert(TOT % LBS == 0, "chunk count");
+#pragma unroll
+    for (int e0 = 0; e0 < TOT; e0 += LBS) {
+        const int e = e0 + threadIdx.x;
+        const int row = e / CPR, ch = e % CPR, r = row % 16;
+        TileCells tc;
+        tile_cells(sl, grp * G_::TPB + row / 16, ntiles, tc);
+        double* d = dst + row * G_::RS + 2 * ch;
+        if (r < tc.nv) {
+#pragma unroll
+            for (int q = 0; q < NA; ++q) cp16(d + q * G_::TILE, src[q] + (tc.l0 + r) * S + 2 * ch);
+            if (dinv && ch == 0) {
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + NA * G_::TILE + row);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa),
+                             "l"(dinv + tc.g0 + r)
+                             : "memory");
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < NA; ++q)
+                *reinterpret_cast<double2*>(d + q * G_::TILE) = make_double2(0.0, 0.0);
+            if (ch == 0) dst[NA * G_::TILE + row] = 1.0;
+        }
+    }
+}
+
+// CTA Gram over a staged group: warp w owns output tiles w, w + LNW, ... of
+// G = U^T V (MT x NT grid of 16 x 8 tiles) and accumulates over all cells
 template <int S>
 struct OwnedGram {
-    static constexpr int MT = (S + 15) / 16;
-    static constexpr int NT = S / 8;
-    static constexpr int TILES = MT * NT;
-    static constexpr int PER = (TILES + LNW - 1) / LNW;
-    double d[PER][4];
+    using G_ = Geo<S>;
+    double d[G_::PER][4];
     __device__ __forceinline__ void zero() {
 #pragma unroll
-        for (int i = 0; i < PER; ++i)
+        for (int i = 0; i < G_::PER; ++i)
 #pragma unroll
             for (int e = 0; e < 4; ++e) d[i][e] = 0.0;
     }
-    __device__ __forceinline__ void accumulate(const LTile<S>* tiles, int ntiles, int warp, int g,
+    __device__ __forceinline__ void accumulate(const double* U, const double* V, int warp, int g,
                                                int t) {
-        constexpr int RS = LTile<S>::RS;
-        for (int k = 0; k < ntiles; ++k) {
-            const double* U = tiles[k].u;
-            const double* V = tiles[k].v;
+        constexpr int RS = G_::RS;
+#pragma unroll 4
+        for (int kk = 0; kk < G_::CELLS / 4; ++kk) {
+            const int c4 = 4 * kk + t;
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-                const int c4 = 4 * kk + t;
-#pragma unroll
-                for (int i = 0; i < PER; ++i) {
-                    const int tile = warp + LNW * i;
-                    if (tile >= TILES) break;
-                    const int m = tile / NT, n = tile % NT;
-                    const double a0 = U[c4 * RS + 16 * m + g];
-                    const double a1 = (16 * m + 8 + g < S) ? U[c4 * RS + 16 * m + 8 + g] : 0.0;
-                    dmma_l(d[i], a0, a1, V[c4 * RS + 8 * n + g]);
-                }
+            for (int i = 0; i < G_::PER; ++i) {
+                const int tile = warp + LNW * i;
+                if (tile >= G_::GT) break;
+                const int m = tile / G_::NT, n = tile % G_::NT;
+                const double a0 = U[c4 * RS + 16 * m + g];
+                const double a1 = (16 * m + 8 + g < S) ? U[c4 * RS + 16 * m + 8 + g] : 0.0;
+                dmma_l(d[i], a0, a1, V[c4 * RS + 8 * n + g]);
             }
         }
     }
     // this CTA's partial: out[r * S + c]
     __device__ __forceinline__ void write(double* out, int warp, int g, int t) const {
 #pragma unroll
-        for (int i = 0; i < PER; ++i) {
+        for (int i = 0; i < G_::PER; ++i) {
             const int tile = warp + LNW * i;
-            if (tile >= TILES) break;
-            const int m = tile / NT, n = tile % NT;
+            if (tile >= G_::GT) break;
+            const int m = tile / G_::NT, n = tile % G_::NT;
             const int r0 = 16 * m + g, c0 = 8 * n + 2 * t;
             out[r0 * S + c0] = d[i][0];
             out[r0 * S + c0 + 1] = d[i][1];
@@ -163,332 +270,370 @@ struct SweepArgs {
     int precond;
 };
 
-// stage two 16-cell C-layout tiles (rows g, g + 8) into smem tile k
-template <int S>
-__device__ __forceinline__ void stage_c(LTile<S>& tl, const double (&u)[S / 8][4],
-                                        const double (&v)[S / 8][4], int g, int t) {
-    constexpr int RS = LTile<S>::RS;
-#pragma unroll
-    for (int n = 0; n < S / 8; ++n) {
-        const int col = 8 * n + 2 * t;
-        *reinterpret_cast<double2*>(tl.u + g * RS + col) = make_double2(u[n][0], u[n][1]);
-        *reinterpret_cast<double2*>(tl.u + (g + 8) * RS + col) = make_double2(u[n][2], u[n][3]);
-        *reinterpret_cast<double2*>(tl.v + g * RS + col) = make_double2(v[n][0], v[n][1]);
-        *reinterpret_cast<double2*>(tl.v + (g + 8) * RS + col) = make_double2(v[n][2], v[n][3]);
-    }
+// C-fragment rows (cells g, g + 8 of the run; columns col, col + 1)
+__device__ __forceinline__ void ld_frag(const double* V, int S, const TileCells& tc, int g,
+                                        int col, bool v0, bool v1, double (&o)[4]) {
+    const double2 a = v0 ? *reinterpret_cast<const double2*>(V + (tc.l0 + g) * S + col)
+                         : make_double2(0.0, 0.0);
+    const double2 b = v1 ? *reinterpret_cast<const double2*>(V + (tc.l0 + g + 8) * S + col)
+                         : make_double2(0.0, 0.0);
+    o[0] = a.x;
+    o[1] = a.y;
+    o[2] = b.x;
+    o[3] = b.y;
+}
+__device__ __forceinline__ void st_frag(double* V, int S, const TileCells& tc, int g, int col,
+                                        bool v0, bool v1, const double (&o)[4]) {
+    if (v0) *reinterpret_cast<double2*>(V + (tc.l0 + g) * S + col) = make_double2(o[0], o[1]);
+    if (v1) *reinterpret_cast<double2*>(V + (tc.l0 + g + 8) * S + col) = make_double2(o[2], o[3]);
+}
+__device__ __forceinline__ void stage_frag(double* U, int RS, int row0, int col,
+                                           const double (&o)[4]) {
+    *reinterpret_cast<double2*>(U + row0 * RS + col) = make_double2(o[0], o[1]);
+    *reinterpret_cast<double2*>(U + (row0 + 8) * RS + col) = make_double2(o[2], o[3]);
 }
 
+// per-column vector partial (sum over the group slots in order) -> out[S*S + c]
 template <int S>
-__device__ __forceinline__ void ld_c(const double* V, const LCell& c0, const LCell& c1, bool v0,
-                                     bool v1, int t, double (&o)[S / 8][4]) {
+__device__ __forceinline__ void write_colsum(double* out, double* vred, int ts, int cb, int lane,
+                                             double s0, double s1) {
 #pragma unroll
-    for (int n = 0; n < S / 8; ++n) {
-        const double2 a = v0 ? *reinterpret_cast<const double2*>(V + c0.l * S + 8 * n + 2 * t)
-                             : make_double2(0.0, 0.0);
-        const double2 b = v1 ? *reinterpret_cast<const double2*>(V + c1.l * S + 8 * n + 2 * t)
-                             : make_double2(0.0, 0.0);
-        o[n][0] = a.x;
-        o[n][1] = a.y;
-        o[n][2] = b.x;
-        o[n][3] = b.y;
+    for (int e = 0; e < 2; ++e) {
+        double x = e ? s1 : s0;
+        x += __shfl_xor_sync(0xffffffffu, x, 4);
+        x += __shfl_xor_sync(0xffffffffu, x, 8);
+        x += __shfl_xor_sync(0xffffffffu, x, 16);
+        if (lane < 4) vred[ts * S + 8 * cb + 2 * lane + e] = x;
     }
-}
-
-template <int S>
-__device__ __forceinline__ void st_c(double* V, const LCell& c0, const LCell& c1, bool v0,
-                                     bool v1, int t, const double (&o)[S / 8][4]) {
-#pragma unroll
-    for (int n = 0; n < S / 8; ++n) {
-        if (v0)
-            *reinterpret_cast<double2*>(V + c0.l * S + 8 * n + 2 * t) = make_double2(o[n][0], o[n][1]);
-        if (v1)
-            *reinterpret_cast<double2*>(V + c1.l * S + 8 * n + 2 * t) = make_double2(o[n][2], o[n][3]);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// sweeps (all: 16-cell tiles, one per warp per batch; batch = LNW tiles)
-// ---------------------------------------------------------------------------
-enum Sweep : int { kInit = 0, kRestart = 1 };
-
-// X = 0, R = B (init) or R = B - A X (restart); Z = D^-1 R; P = Z;
-// partials [R^T Z | sum b^2 (init)]
-template <int S, int MODE>
-__global__ void __launch_bounds__(LBS, 1) k_anchor(SweepArgs a) {
-    constexpr int NT = S / 8;
-    extern __shared__ __align__(16) unsigned char smraw_[];
-    LTile<S>* tiles = reinterpret_cast<LTile<S>*>(smraw_);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const int64_t ntiles = (a.sl.n_int + 15) / 16;
-    OwnedGram<S> G;
-    G.zero();
-    double bn[NT][2] = {};
-    const bool jac = a.precond != 0;
-    for (int64_t b0 = (int64_t)blockIdx.x * LNW; b0 < ntiles; b0 += (int64_t)gridDim.x * LNW) {
-        const int64_t tile = b0 + warp;
-        const int64_t u0 = tile * 16 + g, u1 = u0 + 8;
-        const bool v0 = tile < ntiles && u0 < a.sl.n_int, v1 = tile < ntiles && u1 < a.sl.n_int;
-        LCell c0, c1;
-        if (v0) lcell(a.sl, a.st, u0, c0, MODE == kRestart);
-        if (v1) lcell(a.sl, a.st, u1, c1, MODE == kRestart);
-        double r[NT][4], z[NT][4];
-        ld_c<S>(a.B, c0, c1, v0, v1, t, r);
-        if (MODE == kRestart) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const LCell& c = h ? c1 : c0;
-                if (!(h ? v1 : v0)) continue;
-                const int64_t pz = (int64_t)a.sl.nx * (a.sl.nyl + 2);
-#pragma unroll
-                for (int n = 0; n < NT; ++n)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int64_t ee = c.l * S + 8 * n + 2 * t + e;
-                        double acc = 0.0;
-                        if (c.hzm) acc = fma(c.zm, a.X[ee - pz * S], acc);
-                        if (c.hym) acc = fma(c.ym, a.X[ee - (int64_t)a.sl.nx * S], acc);
-                        if (c.hxm) acc = fma(c.xm, a.X[ee - S], acc);
-                        acc = fma(c.d, a.X[ee], acc);
-                        if (c.hxp) acc = fma(c.xp, a.X[ee + S], acc);
-                        if (c.hyp) acc = fma(c.yp, a.X[ee + (int64_t)a.sl.nx * S], acc);
-                        if (c.hzp) acc = fma(c.zp, a.X[ee + pz * S], acc);
-                        r[n][2 * h + e] -= acc;
-                    }
-            }
-        }
-        const double d0 = (jac && v0) ? a.st.dinv[c0.gi] : 1.0;
-        const double d1 = (jac && v1) ? a.st.dinv[c1.gi] : 1.0;
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-            z[n][0] = d0 * r[n][0];
-            z[n][1] = d0 * r[n][1];
-            z[n][2] = d1 * r[n][2];
-            z[n][3] = d1 * r[n][3];
-            bn[n][0] += r[n][0] * r[n][0] + r[n][2] * r[n][2];
-            bn[n][1] += r[n][1] * r[n][1] + r[n][3] * r[n][3];
-        }
-        if (MODE == kInit) {
-            double zero[NT][4] = {};
-            st_c<S>(a.X, c0, c1, v0, v1, t, zero);
-        }
-        st_c<S>(a.R, c0, c1, v0, v1, t, r);
-        st_c<S>(a.P, c0, c1, v0, v1, t, z);
-        stage_c<S>(tiles[warp], r, z, g, t);
-        __syncthreads();
-        const int nst = (int)((ntiles - b0) < LNW ? (ntiles - b0) : LNW);
-        G.accumulate(tiles, nst, warp, g, t);
-        __syncthreads();
-    }
-    constexpr int E = S * S + S;
-    double* out = a.part + (int64_t)blockIdx.x * E;
-    G.write(out, warp, g, t);
-    // sum of squares of B per column (init): warp shuffle over g, then warps in order
-    double (*vred)[S] = reinterpret_cast<double (*)[S]>(smraw_ + sizeof(LTile<S>) * LNW);
-#pragma unroll
-    for (int n = 0; n < NT; ++n)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            double x = bn[n][e];
-            x += __shfl_xor_sync(0xffffffffu, x, 4);
-            x += __shfl_xor_sync(0xffffffffu, x, 8);
-            x += __shfl_xor_sync(0xffffffffu, x, 16);
-            if (lane < 4) vred[warp][8 * n + 2 * lane + e] = x;
-        }
     __syncthreads();
     for (int c = threadIdx.x; c < S; c += LBS) {
         double s = 0.0;
-        for (int w = 0; w < LNW; ++w) s += vred[w][c];
+        for (int q = 0; q < Geo<S>::TPB; ++q) s += vred[q * S + c];
         out[S * S + c] = s;
     }
 }
 
-// phase 1: W = A P (CSR-order FMA chain) over interior cells; partial G = P^T W
+// stages in flight for the update sweep: 3 (two groups ahead) when two CTAs
+// still fit an SM, else 2
 template <int S>
-__global__ void __launch_bounds__(LBS, 1) k_spmm_gram(SweepArgs a) {
-    constexpr int RS = LTile<S>::RS;
-    constexpr int CW = S / 2 < 8 ? S / 2 : 8;
-    constexpr int PASSES = S / (2 * CW);
-    extern __shared__ __align__(16) unsigned char smraw_[];
-    LTile<S>* tiles = reinterpret_cast<LTile<S>*>(smraw_);
+struct UpdRing {
+    static constexpr size_t stage = (4 * (size_t)Geo<S>::TILE + Geo<S>::CELLS) * sizeof(double);
+    static constexpr int NST = (2 * (3 * stage + Geo<S>::TPB * S * 8 + 1024) <= 228 * 1024) ? 3 : 2;
+};
+template <int S>
+constexpr size_t smem_update() {
+    return UpdRing<S>::NST * UpdRing<S>::stage + Geo<S>::TPB * S * sizeof(double);
+}
+template <int S>
+constexpr size_t smem_anchor() {
+    return (2 * (size_t)Geo<S>::TILE + Geo<S>::TPB * S) * sizeof(double);
+}
+template <int S>
+constexpr size_t smem_spmm() {
+    return 2 * (size_t)Geo<S>::TILE * sizeof(double);
+}
+template <int S>
+constexpr size_t smem_pupdate() {
+    return 3 * (2 * (size_t)Geo<S>::TILE + Geo<S>::CELLS) * sizeof(double);
+}
+
+// ---------------------------------------------------------------------------
+// sweeps
+// ---------------------------------------------------------------------------
+enum Sweep : int { kInit = 0, kRestart = 1 };
+
+// X = 0, R = B (init) or R = B - A X (restart); Z = D^-1 R; P = Z;
+// partials [R^T Z | sum r^2]
+template <int S, int MODE>
+__global__ void __launch_bounds__(LBS, 2) k_anchor(SweepArgs a) {
+    using G_ = Geo<S>;
+    constexpr int RS = G_::RS;
+    extern __shared__ __align__(16) double sm_[];
+    double* U = sm_;
+    double* V = U + G_::TILE;
+    double* vred = V + G_::TILE;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const int r = lane >> 1, h = lane & 1;
-    const int64_t ntiles = (a.sl.n_int + 15) / 16;
+    const int ts = warp / G_::NWC, cb = warp % G_::NWC, col = 8 * cb + 2 * t;
+    const int ntiles = n_tiles(a.sl);
+    const int ngroups = (ntiles + G_::TPB - 1) / G_::TPB;
+    const int64_t pz = (int64_t)a.sl.nx * (a.sl.nyl + 2);
+    const bool jac = a.precond != 0;
+    OwnedGram<S> G;
+    G.zero();
+    double bn0 = 0.0, bn1 = 0.0;
+    for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        TileCells tc;
+        tile_cells(a.sl, grp * G_::TPB + ts, ntiles, tc);
+        const bool v0 = g < tc.nv, v1 = g + 8 < tc.nv;
+        double r[4], z[4];
+        ld_frag(a.B, S, tc, g, col, v0, v1, r);
+        if (MODE == kRestart) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (!(h ? v1 : v0)) continue;
+                LCell c;
+                run_cell(a.sl, a.st, tc, g + 8 * h, c);
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int64_t ee = c.l * S + col + e;
+                    double acc = 0.0;
+                    if (c.hzm) acc = fma(c.zm, a.X[ee - pz * S], acc);
+                    if (c.hym) acc = fma(c.ym, a.X[ee - (int64_t)a.sl.nx * S], acc);
+                    if (c.hxm) acc = fma(c.xm, a.X[ee - S], acc);
+                    acc = fma(c.d, a.X[ee], acc);
+                    if (c.hxp) acc = fma(c.xp, a.X[ee + S], acc);
+                    if (c.hyp) acc = fma(c.yp, a.X[ee + (int64_t)a.sl.nx * S], acc);
+                    if (c.hzp) acc = fma(c.zp, a.X[ee + pz * S], acc);
+                    r[2 * h + e] -= acc;
+                }
+            }
+        }
+        const double d0 = (jac && v0) ? a.st.dinv[tc.g0 + g] : 1.0;
+        const double d1 = (jac && v1) ? a.st.dinv[tc.g0 + g + 8] : 1.0;
+        z[0] = d0 * r[0];
+        z[1] = d0 * r[1];
+        z[2] = d1 * r[2];
+        z[3] = d1 * r[3];
+        bn0 += r[0] * r[0] + r[2] * r[2];
+        bn1 += r[1] * r[1] + r[3] * r[3];
+        if (MODE == kInit) {
+            const double zero[4] = {0.0, 0.0, 0.0, 0.0};
+            st_frag(a.X, S, tc, g, col, v0, v1, zero);
+        }
+        st_frag(a.R, S, tc, g, col, v0, v1, r);
+        st_frag(a.P, S, tc, g, col, v0, v1, z);
+        stage_frag(U, RS, ts * 16 + g, col, r);
+        stage_frag(V, RS, ts * 16 + g, col, z);
+        __syncthreads();
+        G.accumulate(U, V, warp, g, t);
+        __syncthreads();
+    }
+    double* out = a.part + (int64_t)blockIdx.x * (S * S + S);
+    G.write(out, warp, g, t);
+    write_colsum<S>(out, vred, ts, cb, lane, bn0, bn1);
+}
+
+// phase 1: W = A P (CSR-order FMA chain) over interior cells; partial G = P^T W.
+// Lane mapping: LPC lanes per cell, each lane 4 columns as two 16-byte pieces
+// half a row apart, so one load instruction reads whole 128-byte lines.
+template <int S>
+__global__ void __launch_bounds__(LBS, 2) k_spmm_gram(SweepArgs a) {
+    using G_ = Geo<S>;
+    constexpr int RS = G_::RS, LPC = 16 / G_::TPB, CPW = 32 / LPC;
+    extern __shared__ __align__(16) double sm_[];
+    double* U = sm_;
+    double* V = U + G_::TILE;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int cell = warp * CPW + lane / LPC, slot = cell / 16, r = cell % 16;
+    const int ca = 2 * (lane % LPC), cb2 = ca + S / 2;
+    const int ntiles = n_tiles(a.sl);
+    const int ngroups = (ntiles + G_::TPB - 1) / G_::TPB;
     const int64_t pz = (int64_t)a.sl.nx * (a.sl.nyl + 2);
     OwnedGram<S> G;
     G.zero();
-    for (int64_t b0 = (int64_t)blockIdx.x * LNW; b0 < ntiles; b0 += (int64_t)gridDim.x * LNW) {
-        const int64_t tile = b0 + warp;
-        const int64_t u = tile * 16 + r;
-        const bool v = tile < ntiles && u < a.sl.n_int;
-        LCell c;
-        if (v) lcell(a.sl, a.st, u, c, true);
+    for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        TileCells tc;
+        tile_cells(a.sl, grp * G_::TPB + slot, ntiles, tc);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0}, ctr[4] = {0.0, 0.0, 0.0, 0.0};
+        if (r < tc.nv) {
+            LCell c;
+            run_cell(a.sl, a.st, tc, r, c);
+            auto row = [&](int64_t l, double cf, bool has) {
+                if (!has) return;
+                const double2 x0 = *reinterpret_cast<const double2*>(a.P + l * S + ca);
+                const double2 x1 = *reinterpret_cast<const double2*>(a.P + l * S + cb2);
+                acc[0] = fma(cf, x0.x, acc[0]);
+                acc[1] = fma(cf, x0.y, acc[1]);
+                acc[2] = fma(cf, x1.x, acc[2]);
+                acc[3] = fma(cf, x1.y, acc[3]);
+            };
+            row(c.l - pz, c.zm, c.hzm);
+            row(c.l - a.sl.nx, c.ym, c.hym);
+            row(c.l - 1, c.xm, c.hxm);
+            {
+                const double2 x0 = *reinterpret_cast<const double2*>(a.P + c.l * S + ca);
+                const double2 x1 = *reinterpret_cast<const double2*>(a.P + c.l * S + cb2);
+                ctr[0] = x0.x;
+                ctr[1] = x0.y;
+                ctr[2] = x1.x;
+                ctr[3] = x1.y;
 #pragma unroll
-        for (int ps = 0; ps < PASSES; ++ps) {
-            const int col = ps * 2 * CW + h * CW;
-            double acc[CW], ctr[CW];
-#pragma unroll
-            for (int j = 0; j < CW; ++j) acc[j] = ctr[j] = 0.0;
-            if (v) {
-                auto row = [&](int64_t l, double cf, bool has) {
-                    if (!has) return;
-                    const double2* src = reinterpret_cast<const double2*>(a.P + l * S + col);
-#pragma unroll
-                    for (int j = 0; j < CW / 2; ++j) {
-                        const double2 x = src[j];
-                        acc[2 * j] = fma(cf, x.x, acc[2 * j]);
-                        acc[2 * j + 1] = fma(cf, x.y, acc[2 * j + 1]);
-                    }
-                };
-                row(c.l - pz, c.zm, c.hzm);
-                row(c.l - a.sl.nx, c.ym, c.hym);
-                row(c.l - 1, c.xm, c.hxm);
-                {
-                    const double2* src = reinterpret_cast<const double2*>(a.P + c.l * S + col);
-#pragma unroll
-                    for (int j = 0; j < CW / 2; ++j) {
-                        const double2 x = src[j];
-                        ctr[2 * j] = x.x;
-                        ctr[2 * j + 1] = x.y;
-                        acc[2 * j] = fma(c.d, x.x, acc[2 * j]);
-                        acc[2 * j + 1] = fma(c.d, x.y, acc[2 * j + 1]);
-                    }
-                }
-                row(c.l + 1, c.xp, c.hxp);
-                row(c.l + a.sl.nx, c.yp, c.hyp);
-                row(c.l + pz, c.zp, c.hzp);
-                double2* dst = reinterpret_cast<double2*>(a.W + c.l * S + col);
-#pragma unroll
-                for (int j = 0; j < CW / 2; ++j) dst[j] = make_double2(acc[2 * j], acc[2 * j + 1]);
+                for (int j = 0; j < 4; ++j) acc[j] = fma(c.d, ctr[j], acc[j]);
             }
-#pragma unroll
-            for (int j = 0; j < CW / 2; ++j) {
-                *reinterpret_cast<double2*>(tiles[warp].u + r * RS + col + 2 * j) =
-                    make_double2(ctr[2 * j], ctr[2 * j + 1]);
-                *reinterpret_cast<double2*>(tiles[warp].v + r * RS + col + 2 * j) =
-                    make_double2(acc[2 * j], acc[2 * j + 1]);
-            }
+            row(c.l + 1, c.xp, c.hxp);
+            row(c.l + a.sl.nx, c.yp, c.hyp);
+            row(c.l + pz, c.zp, c.hzp);
+            *reinterpret_cast<double2*>(a.W + c.l * S + ca) = make_double2(acc[0], acc[1]);
+            *reinterpret_cast<double2*>(a.W + c.l * S + cb2) = make_double2(acc[2], acc[3]);
         }
+        *reinterpret_cast<double2*>(U + cell * RS + ca) = make_double2(ctr[0], ctr[1]);
+        *reinterpret_cast<double2*>(U + cell * RS + cb2) = make_double2(ctr[2], ctr[3]);
+        *reinterpret_cast<double2*>(V + cell * RS + ca) = make_double2(acc[0], acc[1]);
+        *reinterpret_cast<double2*>(V + cell * RS + cb2) = make_double2(acc[2], acc[3]);
         __syncthreads();
-        const int nst = (int)((ntiles - b0) < LNW ? (ntiles - b0) : LNW);
-        G.accumulate(tiles, nst, warp, g, t);
+        G.accumulate(U, V, warp, g, t);
         __syncthreads();
     }
     G.write(a.part + (int64_t)blockIdx.x * (S * S), warp, g, t);
 }
 
-// phase 2: X += P alpha, R -= W alpha (DMMA, M = cells), rr, Z = D^-1 R,
-// partials [S_new = R^T Z | rr]
-template <int S>
-__global__ void __launch_bounds__(LBS, 1) k_update(SweepArgs a) {
-    constexpr int NT = S / 8, KS = S / 4, RSC = S + 4;
-    extern __shared__ __align__(16) unsigned char smraw_[];
-    LTile<S>* tiles = reinterpret_cast<LTile<S>*>(smraw_);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const int64_t ntiles = (a.sl.n_int + 15) / 16;
-    const bool jac = a.precond != 0;
-    OwnedGram<S> G;
-    G.zero();
-    double rr[NT][2] = {};
-    for (int64_t b0 = (int64_t)blockIdx.x * LNW; b0 < ntiles; b0 += (int64_t)gridDim.x * LNW) {
-        const int64_t tile = b0 + warp;
-        const int64_t u0 = tile * 16 + g, u1 = u0 + 8;
-        const bool v0 = tile < ntiles && u0 < a.sl.n_int, v1 = tile < ntiles && u1 < a.sl.n_int;
-        LCell c0, c1;
-        if (v0) lcell(a.sl, a.st, u0, c0, false);
-        if (v1) lcell(a.sl, a.st, u1, c1, false);
-        double x[NT][4], rv[NT][4];
-        ld_c<S>(a.X, c0, c1, v0, v1, t, x);
-        ld_c<S>(a.R, c0, c1, v0, v1, t, rv);
-#pragma unroll 4
-        for (int ks = 0; ks < KS; ++ks) {
-            const int kc = 4 * ks + t;
-            const double p0 = v0 ? a.P[c0.l * S + kc] : 0.0, p1 = v1 ? a.P[c1.l * S + kc] : 0.0;
-            const double w0 = v0 ? -a.W[c0.l * S + kc] : 0.0, w1 = v1 ? -a.W[c1.l * S + kc] : 0.0;
-#pragma unroll
-            for (int n = 0; n < NT; ++n) {
-                const double bb = a.coef[kc * RSC + 8 * n + g];
-                dmma_l(x[n], p0, p1, bb);
-                dmma_l(rv[n], w0, w1, bb);
-            }
-        }
-        st_c<S>(a.X, c0, c1, v0, v1, t, x);
-        st_c<S>(a.R, c0, c1, v0, v1, t, rv);
-        const double d0 = (jac && v0) ? a.st.dinv[c0.gi] : 1.0;
-        const double d1 = (jac && v1) ? a.st.dinv[c1.gi] : 1.0;
-        double z[NT][4];
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-            rr[n][0] += rv[n][0] * rv[n][0] + rv[n][2] * rv[n][2];
-            rr[n][1] += rv[n][1] * rv[n][1] + rv[n][3] * rv[n][3];
-            z[n][0] = d0 * rv[n][0];
-            z[n][1] = d0 * rv[n][1];
-            z[n][2] = d1 * rv[n][2];
-            z[n][3] = d1 * rv[n][3];
-        }
-        stage_c<S>(tiles[warp], rv, z, g, t);
-        __syncthreads();
-        const int nst = (int)((ntiles - b0) < LNW ? (ntiles - b0) : LNW);
-        G.accumulate(tiles, nst, warp, g, t);
-        __syncthreads();
-    }
-    constexpr int E = S * S + S;
-    double* out = a.part + (int64_t)blockIdx.x * E;
-    G.write(out, warp, g, t);
-    double (*vred)[S] = reinterpret_cast<double (*)[S]>(smraw_ + sizeof(LTile<S>) * LNW);
-#pragma unroll
-    for (int n = 0; n < NT; ++n)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            double xx = rr[n][e];
-            xx += __shfl_xor_sync(0xffffffffu, xx, 4);
-            xx += __shfl_xor_sync(0xffffffffu, xx, 8);
-            xx += __shfl_xor_sync(0xffffffffu, xx, 16);
-            if (lane < 4) vred[warp][8 * n + 2 * lane + e] = xx;
-        }
-    __syncthreads();
-    for (int c = threadIdx.x; c < S; c += LBS) {
-        double s = 0.0;
-        for (int w = 0; w < LNW; ++w) s += vred[w][c];
-        out[S * S + c] = s;
-    }
+__device__ __forceinline__ void frag_from_smem(const double* T, int RS, int row0, int col,
+                                               double (&o)[4]) {
+    const double2 a = *reinterpret_cast<const double2*>(T + row0 * RS + col);
+    const double2 b = *reinterpret_cast<const double2*>(T + (row0 + 8) * RS + col);
+    o[0] = a.x;
+    o[1] = a.y;
+    o[2] = b.x;
+    o[3] = b.y;
 }
 
-// phase 3: P = D^-1 R + P beta (DMMA, accumulator initialised to Z)
+// phase 2: X += P alpha, R -= W alpha (DMMA, M = cells, B = alpha fragments in
+// registers), rr, Z = D^-1 R; partials [R^T Z | rr]. Every input row of a
+// tile group (P, W, X, R, D^-1) is staged by cp.async one group ahead; the
+// updated R and Z overwrite the consumed R / X stage rows and feed the Gram.
 template <int S>
-__global__ void __launch_bounds__(LBS, 1) k_pupdate(SweepArgs a) {
-    constexpr int NT = S / 8, KS = S / 4, RSC = S + 4;
+__global__ void __launch_bounds__(LBS, 2) k_update(SweepArgs a) {
+    using G_ = Geo<S>;
+    constexpr int RS = G_::RS, KS = S / 4, TL = G_::TILE;
+    constexpr int STAGE = 4 * TL + G_::CELLS;  // P, W, X, R, dinv
+    constexpr int NST = UpdRing<S>::NST;
+    extern __shared__ __align__(16) double sm_[];
+    double* vred = sm_ + NST * STAGE;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const int64_t ntiles = (a.sl.n_int + 15) / 16;
+    const int ts = warp / G_::NWC, cb = warp % G_::NWC, col = 8 * cb + 2 * t;
+    const int ntiles = n_tiles(a.sl);
+    const int ngroups = (ntiles + G_::TPB - 1) / G_::TPB;
     const bool jac = a.precond != 0;
-    for (int64_t tile = (int64_t)blockIdx.x * LNW + warp; tile < ntiles;
-         tile += (int64_t)gridDim.x * LNW) {
-        const int64_t u0 = tile * 16 + g, u1 = u0 + 8;
-        const bool v0 = u0 < a.sl.n_int, v1 = u1 < a.sl.n_int;
-        LCell c0, c1;
-        if (v0) lcell(a.sl, a.st, u0, c0, false);
-        if (v1) lcell(a.sl, a.st, u1, c1, false);
-        double p[NT][4];
-        ld_c<S>(a.R, c0, c1, v0, v1, t, p);
-        const double d0 = (jac && v0) ? a.st.dinv[c0.gi] : 1.0;
-        const double d1 = (jac && v1) ? a.st.dinv[c1.gi] : 1.0;
-        double pa[KS][2];
+    double cf[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) cf[ks] = a.coef[(4 * ks + t) * RS + 8 * cb + g];
+    OwnedGram<S> G;
+    G.zero();
+    double rr0 = 0.0, rr1 = 0.0;
+    const double* const srcs[4] = {a.P, a.W, a.X, a.R};
+    auto stage = [&](int buf, int gr) {
+        stage_multi<S, 4>(sm_ + buf * STAGE, srcs, jac ? a.st.dinv : nullptr, a.sl, gr, ntiles);
+    };
+    int grp = blockIdx.x;
+#pragma unroll
+    for (int p = 0; p < NST - 1; ++p) {
+        if (grp + p * (int)gridDim.x < ngroups) stage(p, grp + p * gridDim.x);
+        cp_commit();
+    }
+    for (int it = 0; grp < ngroups; grp += gridDim.x, ++it) {
+        const int nxt = grp + (NST - 1) * gridDim.x;
+        if (nxt < ngroups) stage((it + NST - 1) % NST, nxt);
+        cp_commit();
+        TileCells tc;
+        tile_cells(a.sl, grp * G_::TPB + ts, ntiles, tc);
+        const bool v0 = g < tc.nv, v1 = g + 8 < tc.nv;
+        cp_wait<NST - 1>();
+        __syncthreads();
+        double* st = sm_ + (it % NST) * STAGE;
+        const double* Pt = st + ts * 16 * RS;
+        const double* Wt = st + TL + ts * 16 * RS;
+        double* Xt = st + 2 * TL;  // becomes V (Z) after the update
+        double* Rt = st + 3 * TL;  // becomes U (R)
+        double x[4], rv[4];
+        frag_from_smem(Xt, RS, ts * 16 + g, col, x);
+        frag_from_smem(Rt, RS, ts * 16 + g, col, rv);
+        const double d0 = jac ? st[4 * TL + ts * 16 + g] : 1.0;
+        const double d1 = jac ? st[4 * TL + ts * 16 + g + 8] : 1.0;
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
-            pa[ks][0] = v0 ? a.P[c0.l * S + 4 * ks + t] : 0.0;
-            pa[ks][1] = v1 ? a.P[c1.l * S + 4 * ks + t] : 0.0;
+            const int kc = 4 * ks + t;
+            dmma_l(x, Pt[g * RS + kc], Pt[(g + 8) * RS + kc], cf[ks]);
+            dmma_l(rv, -Wt[g * RS + kc], -Wt[(g + 8) * RS + kc], cf[ks]);
         }
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-            p[n][0] *= d0;
-            p[n][1] *= d0;
-            p[n][2] *= d1;
-            p[n][3] *= d1;
-#pragma unroll
-            for (int ks = 0; ks < KS; ++ks)
-                dmma_l(p[n], pa[ks][0], pa[ks][1], a.coef[(4 * ks + t) * RSC + 8 * n + g]);
-        }
-        st_c<S>(a.P, c0, c1, v0, v1, t, p);
+        st_frag(a.X, S, tc, g, col, v0, v1, x);
+        st_frag(a.R, S, tc, g, col, v0, v1, rv);
+        double z[4];
+        z[0] = d0 * rv[0];
+        z[1] = d0 * rv[1];
+        z[2] = d1 * rv[2];
+        z[3] = d1 * rv[3];
+        rr0 += rv[0] * rv[0] + rv[2] * rv[2];
+        rr1 += rv[1] * rv[1] + rv[3] * rv[3];
+        __syncthreads();  // all X / R fragments read before they are overwritten
+        stage_frag(Rt, RS, ts * 16 + g, col, rv);
+        stage_frag(Xt, RS, ts * 16 + g, col, z);
+        __syncthreads();
+        G.accumulate(Rt, Xt, warp, g, t);
+        __syncthreads();
     }
+    cp_wait<0>();
+    double* out = a.part + (int64_t)blockIdx.x * (S * S + S);
+    G.write(out, warp, g, t);
+    write_colsum<S>(out, vred, ts, cb, lane, rr0, rr1);
+}
+
+// phase 3: P = D^-1 R + P beta (DMMA, accumulator initialised to Z; P, R and
+// D^-1 rows of the group staged one group ahead)
+template <int S>
+__global__ void __launch_bounds__(LBS, 2) k_pupdate(SweepArgs a) {
+    using G_ = Geo<S>;
+    constexpr int RS = G_::RS, KS = S / 4, TL = G_::TILE;
+    constexpr int STAGE = 2 * TL + G_::CELLS;  // P, R, dinv
+    constexpr int NST = 3;
+    extern __shared__ __align__(16) double sm_[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int ts = warp / G_::NWC, cb = warp % G_::NWC, col = 8 * cb + 2 * t;
+    const int ntiles = n_tiles(a.sl);
+    const int ngroups = (ntiles + G_::TPB - 1) / G_::TPB;
+    const bool jac = a.precond != 0;
+    double cf[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) cf[ks] = a.coef[(4 * ks + t) * RS + 8 * cb + g];
+    const double* const srcs[2] = {a.P, a.R};
+    auto stage = [&](int buf, int gr) {
+        stage_multi<S, 2>(sm_ + buf * STAGE, srcs, jac ? a.st.dinv : nullptr, a.sl, gr, ntiles);
+    };
+    int grp = blockIdx.x;
+#pragma unroll
+    for (int p = 0; p < NST - 1; ++p) {
+        if (grp + p * (int)gridDim.x < ngroups) stage(p, grp + p * gridDim.x);
+        cp_commit();
+    }
+    for (int it = 0; grp < ngroups; grp += gridDim.x, ++it) {
+        const int nxt = grp + (NST - 1) * gridDim.x;
+        if (nxt < ngroups) stage((it + NST - 1) % NST, nxt);
+        cp_commit();
+        TileCells tc;
+        tile_cells(a.sl, grp * G_::TPB + ts, ntiles, tc);
+        const bool v0 = g < tc.nv, v1 = g + 8 < tc.nv;
+        cp_wait<NST - 1>();
+        __syncthreads();
+        const double* st = sm_ + (it % NST) * STAGE;
+        const double* Pt = st + ts * 16 * RS;
+        double p[4];
+        frag_from_smem(st + TL, RS, ts * 16 + g, col, p);
+        const double d0 = jac ? st[2 * TL + ts * 16 + g] : 1.0;
+        const double d1 = jac ? st[2 * TL + ts * 16 + g + 8] : 1.0;
+        p[0] *= d0;
+        p[1] *= d0;
+        p[2] *= d1;
+        p[3] *= d1;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            const int kc = 4 * ks + t;
+            dmma_l(p, Pt[g * RS + kc], Pt[(g + 8) * RS + kc], cf[ks]);
+        }
+        st_frag(a.P, S, tc, g, col, v0, v1, p);
+        __syncthreads();  // buffer it % NST is refilled by the prefetch of the next iteration
+    }
+    cp_wait<0>();
+}
+
+// CTAs of the sweep kernels (2 per SM: register-bound), same for the
+// single-GPU engine and every rank of the decomposition
+constexpr int kSweepCtasPerSm = 2;
+inline int sweep_ctas(const bk_ctx* ctx, const Slab& sl, int S) {
+    const int tpb = LNW / (S / 8);
+    const int groups = (n_tiles(sl) + tpb - 1) / tpb;
+    int nb = ctx->num_sms * kSweepCtasPerSm;
+    if (ctx->cg_max_ctas > 0 && nb > ctx->cg_max_ctas) nb = ctx->cg_max_ctas;
+    if (nb > groups) nb = groups;
+    return nb < 1 ? 1 : nb;
 }
 
 // true residual ||b - A x||^2 per column (CsrMatrix::apply order: mul, add)
@@ -781,11 +926,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     a.P = Ploc;
     a.W = Wloc;
     a.precond = cfg->precond;
-    const int64_t ntiles = (sl.n_int + 15) / 16;
-    int nb = ctx->num_sms;
-    if (ctx->cg_max_ctas > 0 && nb > ctx->cg_max_ctas) nb = ctx->cg_max_ctas;
-    if ((int64_t)nb * LNW > ntiles) nb = (int)((ntiles + LNW - 1) / LNW);
-    if (nb < 1) nb = 1;
+    const int nb = sweep_ctas(ctx, sl, S);
     constexpr int E = S * S + S;
     void *pPart, *pRed, *pCtl, *pHost;
     bk_status st;
@@ -827,22 +968,24 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
         reduce(S, tr_blocks);
     };
 
-    const size_t sw = sizeof(LTile<S>) * LNW + (size_t)LNW * S * sizeof(double);
+    constexpr size_t swa = smem_anchor<S>(), sws = smem_spmm<S>(), swu = smem_update<S>(),
+                     swp = smem_pupdate<S>();
     const size_t cs = sizeof(CSm<S>);
     {
         const auto set = [&](const void* f, size_t b) {
             return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
         };
-        BK_CUDA_TRY(ctx, set((const void*)k_anchor<S, kInit>, sw));
-        BK_CUDA_TRY(ctx, set((const void*)k_anchor<S, kRestart>, sw));
-        BK_CUDA_TRY(ctx, set((const void*)k_spmm_gram<S>, sw));
-        BK_CUDA_TRY(ctx, set((const void*)k_update<S>, sw));
+        BK_CUDA_TRY(ctx, set((const void*)k_anchor<S, kInit>, swa));
+        BK_CUDA_TRY(ctx, set((const void*)k_anchor<S, kRestart>, swa));
+        BK_CUDA_TRY(ctx, set((const void*)k_spmm_gram<S>, sws));
+        BK_CUDA_TRY(ctx, set((const void*)k_update<S>, swu));
+        BK_CUDA_TRY(ctx, set((const void*)k_pupdate<S>, swp));
         BK_CUDA_TRY(ctx, set((const void*)k_ctl_init<S>, cs));
         BK_CUDA_TRY(ctx, set((const void*)k_ctl_alpha<S>, cs));
         BK_CUDA_TRY(ctx, set((const void*)k_ctl_update<S>, cs));
         BK_CUDA_TRY(ctx, set((const void*)k_ctl_verify<S>, cs));
     }
-    k_anchor<S, kInit><<<nb, LBS, sw, s>>>(a);
+    k_anchor<S, kInit><<<nb, LBS, swa, s>>>(a);
     ++ctx->launches;
     reduce(E, nb);
     k_ctl_init<S><<<1, CBS, cs, s>>>(ctl, red, cfg->rel_tol);
@@ -852,12 +995,12 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     if ((st = read_cmd(&cmd, &sa)) != BK_OK) return st;
     for (int m = 1; m <= cfg->max_iter && sa > 0; ++m) {
         halo(a.P);
-        k_spmm_gram<S><<<nb, LBS, sw, s>>>(a);
+        k_spmm_gram<S><<<nb, LBS, sws, s>>>(a);
         ++ctx->launches;
         reduce(S * S, nb);
         k_ctl_alpha<S><<<1, CBS, cs, s>>>(ctl, red);
         ++ctx->launches;
-        k_update<S><<<nb, LBS, sw, s>>>(a);
+        k_update<S><<<nb, LBS, swu, s>>>(a);
         ++ctx->launches;
         reduce(E, nb);
         k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, red, m);
@@ -872,7 +1015,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
             if ((st = read_cmd(&cmd, &sa)) != BK_OK) return st;
             if (cmd == kCmdDone) break;
             if (cmd == kCmdRestart) {
-                k_anchor<S, kRestart><<<nb, LBS, sw, s>>>(a);
+                k_anchor<S, kRestart><<<nb, LBS, swa, s>>>(a);
                 ++ctx->launches;
                 reduce(E, nb);
                 k_ctl_restart<S><<<1, CBS, 0, s>>>(ctl, red);
@@ -880,7 +1023,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
                 continue;
             }
         }
-        k_pupdate<S><<<nb, LBS, 0, s>>>(a);
+        k_pupdate<S><<<nb, LBS, swp, s>>>(a);
         ++ctx->launches;
     }
     // honest residuals for still-active columns
@@ -978,7 +1121,8 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
     constexpr int E = S * S + S;
     const int nb = b->nb;
     cudaStream_t s = ctx->stream;
-    const size_t sw = sizeof(LTile<S>) * LNW + (size_t)LNW * S * sizeof(double);
+    constexpr size_t swa = smem_anchor<S>(), sws = smem_spmm<S>(), swu = smem_update<S>(),
+                     swp = smem_pupdate<S>();
     const size_t cs = sizeof(CSm<S>);
     auto set = [&](const void* f, size_t bytes) {
         return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -992,8 +1136,8 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
                                     : 4L * ctx->num_sms);
     switch (step) {
         case BK_DD_INIT_SWEEP:
-            BK_CUDA_TRY(ctx, set((const void*)k_anchor<S, kInit>, sw));
-            k_anchor<S, kInit><<<nb, LBS, sw, s>>>(a);
+            BK_CUDA_TRY(ctx, set((const void*)k_anchor<S, kInit>, swa));
+            k_anchor<S, kInit><<<nb, LBS, swa, s>>>(a);
             ++ctx->launches;
             reduce(E, nb);
             break;
@@ -1003,8 +1147,8 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
             ++ctx->launches;
             break;
         case BK_DD_SPMM:
-            BK_CUDA_TRY(ctx, set((const void*)k_spmm_gram<S>, sw));
-            k_spmm_gram<S><<<nb, LBS, sw, s>>>(a);
+            BK_CUDA_TRY(ctx, set((const void*)k_spmm_gram<S>, sws));
+            k_spmm_gram<S><<<nb, LBS, sws, s>>>(a);
             ++ctx->launches;
             reduce(S * S, nb);
             break;
@@ -1014,8 +1158,8 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
             ++ctx->launches;
             break;
         case BK_DD_UPDATE:
-            BK_CUDA_TRY(ctx, set((const void*)k_update<S>, sw));
-            k_update<S><<<nb, LBS, sw, s>>>(a);
+            BK_CUDA_TRY(ctx, set((const void*)k_update<S>, swu));
+            k_update<S><<<nb, LBS, swu, s>>>(a);
             ++ctx->launches;
             reduce(E, nb);
             break;
@@ -1035,8 +1179,8 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
             ++ctx->launches;
             break;
         case BK_DD_RESTART_SWEEP:
-            BK_CUDA_TRY(ctx, set((const void*)k_anchor<S, kRestart>, sw));
-            k_anchor<S, kRestart><<<nb, LBS, sw, s>>>(a);
+            BK_CUDA_TRY(ctx, set((const void*)k_anchor<S, kRestart>, swa));
+            k_anchor<S, kRestart><<<nb, LBS, swa, s>>>(a);
             ++ctx->launches;
             reduce(E, nb);
             break;
@@ -1045,7 +1189,8 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
             ++ctx->launches;
             break;
         case BK_DD_PUPDATE:
-            k_pupdate<S><<<nb, LBS, 0, s>>>(a);
+            BK_CUDA_TRY(ctx, set((const void*)k_pupdate<S>, swp));
+            k_pupdate<S><<<nb, LBS, swp, s>>>(a);
             ++ctx->launches;
             break;
         case BK_DD_CTL_FINAL: {
@@ -1095,10 +1240,8 @@ bk_status bk_dd_sizes(bk_ctx* ctx, const bk_operator* op, int nyl, int S, int64_
     if (S != 16 && S != 32 && S != 64)
         return bk::fail(ctx, BK_INVALID_CONFIG, "dd: kernel width must be 16, 32 or 64");
     const int64_t n_int = (int64_t)op->nx * nyl * op->nz;
-    const int64_t ntiles = (n_int + 15) / 16;
-    int b = ctx->num_sms;
-    if ((int64_t)b * LNW > ntiles) b = (int)((ntiles + LNW - 1) / LNW);
-    if (b < 1) b = 1;
+    const Slab sl{op->nx, nyl, op->nz, op->ny, 0, n_int};
+    const int b = sweep_ctas(ctx, sl, S);
     const int tr = (int)((n_int + (LBS / S) - 1) / (LBS / S) < 4L * ctx->num_sms
                              ? (n_int + (LBS / S) - 1) / (LBS / S)
                              : 4L * ctx->num_sms);
