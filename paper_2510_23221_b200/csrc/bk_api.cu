@@ -41,6 +41,21 @@ bk_status workspace(bk_ctx* ctx, int slot, size_t bytes, void** out) {
     return BK_OK;
 }
 
+bk_status read_small(bk_ctx* ctx, void* host_dst, const void* dev_src, size_t bytes) {
+    constexpr size_t kMap = 64 << 10;
+    if (bytes > kMap || bytes % 4) return fail(ctx, BK_INTERNAL, "read_small: size");
+    if (!ctx->hmap) {
+        BK_CUDA_TRY(ctx, cudaHostAlloc(&ctx->hmap, kMap, cudaHostAllocMapped));
+        BK_CUDA_TRY(ctx, cudaHostGetDevicePointer(&ctx->hmap_dev, ctx->hmap, 0));
+    }
+    BK_CUDA_TRY(ctx, launch_copy_words(ctx->stream, (unsigned*)ctx->hmap_dev,
+                                       (const unsigned*)dev_src, bytes / 4));
+    ++ctx->launches;
+    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(host_dst, ctx->hmap, bytes);
+    return BK_OK;
+}
+
 bool is_device_ptr(const void* p) {
     if (!p) return false;
     cudaPointerAttributes at;
@@ -139,6 +154,7 @@ void free_op_buffers(bk_operator* op) {
     cudaFree(op->dinv);
     cudaFree(op->volz);
     op->diag = op->cx = op->cy = op->cz = op->g = op->dinv = op->volz = nullptr;
+    op->volz_cap = 0;
 }
 
 // Assemble into `op` (buffers reused when the cell count matches).
@@ -161,7 +177,7 @@ bk_status assemble_into(bk_ctx* ctx, const bk_grid* grid, const double* k, const
     if ((st = stage_in(ctx, kSlotK, k, (size_t)n, &kd)) != BK_OK) return st;
     // k > 0 everywhere (discretize.cpp:121-123)
     void* flagp;
-    if ((st = workspace(ctx, kSlotRes, sizeof(int), &flagp)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotFlag, sizeof(int), &flagp)) != BK_OK) return st;
     BK_CUDA_TRY(ctx, cudaMemsetAsync(flagp, 0, sizeof(int), ctx->stream));
     BK_CUDA_TRY(ctx, launch_check_positive(ctx, kd.dev, n, (int*)flagp));
 
@@ -175,9 +191,13 @@ bk_status assemble_into(bk_ctx* ctx, const bk_grid* grid, const double* k, const
         BK_CUDA_TRY(ctx, cudaMalloc(&op->g, nb));
         BK_CUDA_TRY(ctx, cudaMalloc(&op->dinv, nb));
     }
-    cudaFree(op->volz);
-    op->volz = nullptr;
-    BK_CUDA_TRY(ctx, cudaMalloc(&op->volz, (size_t)grid->nz * 2 * sizeof(double)));
+    if (op->volz_cap < 2 * grid->nz) {
+        cudaFree(op->volz);
+        op->volz = nullptr;
+        op->volz_cap = 0;
+        BK_CUDA_TRY(ctx, cudaMalloc(&op->volz, (size_t)grid->nz * 2 * sizeof(double)));
+        op->volz_cap = 2 * grid->nz;
+    }
     op->device = ctx->device;
     op->nx = grid->nx;
     op->ny = grid->ny;
@@ -200,9 +220,7 @@ bk_status assemble_into(bk_ctx* ctx, const bk_grid* grid, const double* k, const
                                      cudaMemcpyHostToDevice, ctx->stream));
     BK_CUDA_TRY(ctx, launch_assemble(ctx, op, kd.dev, bc, dx, dy, op->volz + grid->nz));
     int flag = 0;
-    BK_CUDA_TRY(ctx, cudaMemcpyAsync(&flag, flagp, sizeof(int), cudaMemcpyDeviceToHost,
-                                     ctx->stream));
-    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if ((st = read_small(ctx, &flag, flagp, sizeof(int))) != BK_OK) return st;
     if (flag) return fail(ctx, BK_NONPOSITIVE_K, "assemble: k must be > 0 everywhere");
     return BK_OK;
 }
@@ -222,6 +240,135 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
     return ms;
+}
+
+// One chip. Host outputs are drained in sample chunks on ctx->copy_stream
+// while the next chunk is computed. defer = true (bk_generate_batch) returns
+// without waiting for that drain; the device output buffers alternate between
+// two parities so chip c+1 computes while chip c drains, and a parity is
+// reused only after its previous drain finished.
+bk_status generate_chip_impl(bk_ctx* ctx, const bk_grid* grid, const double* k,
+                             const bk_face bc[6], const double* Qbasis, int s, const double* C,
+                             int64_t N, const bk_solver_cfg* cfg, double* T, double* Q,
+                             double* resid, bk_solve_report* report, bk_phase_timings* timings,
+                             bool defer, int parity) {
+    if (!ctx || !bc) return BK_INVALID_CONFIG;
+    bk_status st = validate_cfg(ctx, cfg);
+    if (st != BK_OK) return st;
+    if (s < 1) return fail(ctx, BK_EMPTY_BASIS, "generate: empty basis");
+    if (s > 64) return fail(ctx, BK_INVALID_CONFIG, "generate: s > 64 not supported");
+    if (N < 0) return fail(ctx, BK_INVALID_CONFIG, "generate: n_data must be >= 0");
+    if ((st = validate_grid(ctx, grid)) != BK_OK) return st;
+    cudaSetDevice(ctx->device);
+    const int64_t n = (int64_t)grid->nx * grid->ny * grid->nz;
+    const int S = kernel_width(s);
+    cudaEvent_t* ev = ctx->ev;
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[0], ctx->stream));
+    Staged qd, cd;
+    if ((st = stage_in(ctx, kSlotQ, Qbasis, (size_t)n * s, &qd)) != BK_OK) return st;
+    if ((st = stage_in(ctx, kSlotC, C, (size_t)s * N, &cd)) != BK_OK) return st;
+    // k is staged inside assemble
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[1], ctx->stream));
+
+    if (!ctx->scratch) ctx->scratch = new bk_operator;
+    bk_operator* scratch = ctx->scratch;
+    if ((st = assemble_into(ctx, grid, k, bc, scratch)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[2], ctx->stream));
+
+    void *pb, *px;
+    if ((st = workspace(ctx, kSlotIn2, (size_t)n * S * 8, &pb)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotOut2, (size_t)n * S * 8, &px)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, launch_rhs_padded(ctx, scratch, qd.dev, s, (double*)pb, S));
+    CgReport rep;
+    if ((st = block_cg_device(ctx, scratch, (const double*)pb, S, cfg, (double*)px, &rep)) != BK_OK)
+        return st;
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[3], ctx->stream));
+
+    Staged td, qo, rd;
+    const size_t out_n = (size_t)n * N;
+    // the previous drain of this parity must be done before its buffers are reused
+    if (ctx->drain_pending[parity]) {
+        BK_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->drain_ev[parity], 0));
+        ctx->drain_pending[parity] = false;
+    }
+    if ((st = stage_out(ctx, parity ? kSlotT1 : kSlotT, T, out_n, &td)) != BK_OK) return st;
+    if ((st = stage_out(ctx, parity ? kSlotQo1 : kSlotQo, Q, out_n, &qo)) != BK_OK) return st;
+    if ((st = stage_out(ctx, parity ? kSlotRes1 : kSlotRes, resid, (size_t)N, &rd)) != BK_OK)
+        return st;
+    if (!td.host && !qo.host && !rd.host) {
+        if ((st = combine_action_device(ctx, scratch, (const double*)px, S, s, cd.dev, N, N,
+                                        td.dev, qo.dev, rd.dev)) != BK_OK)
+            return st;
+        BK_CUDA_TRY(ctx, cudaEventRecord(ev[4], ctx->stream));
+    } else {
+        // host outputs: combine in sample chunks (~64 MB of T + q each) and
+        // drain each chunk on the copy stream while the next one is computed
+        // (D2H of T, q — 16 n bytes per sample over PCIe — is the largest
+        // cost of a host-memory call)
+        if (!ctx->copy_stream) {
+            BK_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+            for (auto& e : ctx->drain_ev)
+                BK_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        const int64_t per = std::max<int64_t>(16, ((int64_t)(64 << 20) / (16 * n)) / 16 * 16);
+        const int64_t nch = (N + per - 1) / per;
+        while ((int64_t)ctx->chunk_ev.size() < nch) {
+            cudaEvent_t e;
+            BK_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ctx->chunk_ev.push_back(e);
+        }
+        for (int64_t c = 0; c < nch; ++c) {
+            const int64_t j0 = c * per, m = std::min(per, N - j0);
+            double* tdev = td.dev ? td.dev + j0 * n : nullptr;
+            double* qdev = qo.dev ? qo.dev + j0 * n : nullptr;
+            if ((st = combine_action_device(ctx, scratch, (const double*)px, S, s, cd.dev + j0, N,
+                                            m, tdev, qdev, rd.dev ? rd.dev + j0 : nullptr)) !=
+                BK_OK)
+                return st;
+            BK_CUDA_TRY(ctx, cudaEventRecord(ctx->chunk_ev[c], ctx->stream));
+            BK_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[c], 0));
+            const size_t bytes = (size_t)m * n * sizeof(double);
+            if (td.host)
+                BK_CUDA_TRY(ctx, cudaMemcpyAsync(T + j0 * n, tdev, bytes, cudaMemcpyDeviceToHost,
+                                                 ctx->copy_stream));
+            if (qo.host)
+                BK_CUDA_TRY(ctx, cudaMemcpyAsync(Q + j0 * n, qdev, bytes, cudaMemcpyDeviceToHost,
+                                                 ctx->copy_stream));
+        }
+        if (rd.host)
+            BK_CUDA_TRY(ctx, cudaMemcpyAsync(resid, rd.dev, (size_t)N * sizeof(double),
+                                             cudaMemcpyDeviceToHost, ctx->copy_stream));
+        BK_CUDA_TRY(ctx, cudaEventRecord(ev[4], ctx->stream));
+        BK_CUDA_TRY(ctx, cudaEventRecord(ctx->drain_ev[parity], ctx->copy_stream));
+        ctx->drain_pending[parity] = true;
+        if (!defer) {  // the call returns with the outputs in host memory
+            BK_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->drain_ev[parity], 0));
+            ctx->drain_pending[parity] = false;
+        }
+        td.host = qo.host = rd.host = false;  // drained above
+    }
+    if ((st = drain(ctx, td, T, out_n)) != BK_OK) return st;
+    if ((st = drain(ctx, qo, Q, out_n)) != BK_OK) return st;
+    if ((st = drain(ctx, rd, resid, (size_t)N)) != BK_OK) return st;
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[5], ctx->stream));
+    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+
+    const double solve_s = elapsed(ev[2], ev[3]) * 1e-3;
+    fill_report(rep, s, solve_s, report);
+    if (timings) {
+        timings->h2d_s = elapsed(ev[0], ev[1]) * 1e-3;
+        timings->assemble_s = elapsed(ev[1], ev[2]) * 1e-3;
+        timings->basis_solve_s = solve_s;
+        timings->combine_action_s = elapsed(ev[3], ev[4]) * 1e-3;
+        timings->d2h_s = elapsed(ev[4], ev[5]) * 1e-3;
+        timings->total_s = elapsed(ev[0], ev[5]) * 1e-3;
+        timings->iterations_total = rep.iterations;
+        timings->matvecs_total = rep.matvecs + N;
+    }
+    for (int j = 0; j < s; ++j)
+        if (!rep.converged[j])
+            return fail(ctx, BK_NOT_CONVERGED, "basis solve did not reach tolerance");
+    return BK_OK;
 }
 
 }  // namespace
@@ -265,10 +412,18 @@ void bk_destroy(bk_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (int i = 0; i < bk_ctx::kSlots; ++i) cudaFree(ctx->ws[i]);
     for (auto& e : ctx->ev) cudaEventDestroy(e);
+    for (auto& e : ctx->chunk_ev) cudaEventDestroy(e);
+    for (auto& e : ctx->drain_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamDestroy(ctx->copy_stream);
+    }
     if (ctx->scratch) {
         free_op_buffers(ctx->scratch);
         delete ctx->scratch;
     }
+    if (ctx->hmap) cudaFreeHost(ctx->hmap);
     cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }
@@ -459,7 +614,8 @@ bk_status bk_combine_action(bk_ctx* ctx, const bk_operator* op, const double* X,
         xk = (const double*)p;
     }
     // the kernel reads C rows [0, s) with row stride N
-    if ((st = combine_action_device(ctx, op, xk, S, cd.dev, N, td.dev, qd.dev, rd.dev)) != BK_OK)
+    if ((st = combine_action_device(ctx, op, xk, S, s, cd.dev, N, N, td.dev, qd.dev, rd.dev)) !=
+        BK_OK)
         return st;
     if ((st = drain(ctx, td, T, out_n)) != BK_OK) return st;
     if ((st = drain(ctx, qd, Q, out_n)) != BK_OK) return st;
@@ -472,69 +628,8 @@ bk_status bk_generate_chip(bk_ctx* ctx, const bk_grid* grid, const double* k, co
                            const double* Qbasis, int s, const double* C, int64_t N,
                            const bk_solver_cfg* cfg, double* T, double* Q, double* resid,
                            bk_solve_report* report, bk_phase_timings* timings) {
-    if (!ctx || !bc) return BK_INVALID_CONFIG;
-    bk_status st = validate_cfg(ctx, cfg);
-    if (st != BK_OK) return st;
-    if (s < 1) return fail(ctx, BK_EMPTY_BASIS, "generate: empty basis");
-    if (s > 64) return fail(ctx, BK_INVALID_CONFIG, "generate: s > 64 not supported");
-    if (N < 0) return fail(ctx, BK_INVALID_CONFIG, "generate: n_data must be >= 0");
-    if ((st = validate_grid(ctx, grid)) != BK_OK) return st;
-    cudaSetDevice(ctx->device);
-    const int64_t n = (int64_t)grid->nx * grid->ny * grid->nz;
-    const int S = kernel_width(s);
-    cudaEvent_t* ev = ctx->ev;
-    BK_CUDA_TRY(ctx, cudaEventRecord(ev[0], ctx->stream));
-    Staged qd, cd;
-    if ((st = stage_in(ctx, kSlotQ, Qbasis, (size_t)n * s, &qd)) != BK_OK) return st;
-    if ((st = stage_in(ctx, kSlotC, C, (size_t)s * N, &cd)) != BK_OK) return st;
-    // k is staged inside assemble
-    BK_CUDA_TRY(ctx, cudaEventRecord(ev[1], ctx->stream));
-
-    if (!ctx->scratch) ctx->scratch = new bk_operator;
-    bk_operator* scratch = ctx->scratch;
-    if ((st = assemble_into(ctx, grid, k, bc, scratch)) != BK_OK) return st;
-    BK_CUDA_TRY(ctx, cudaEventRecord(ev[2], ctx->stream));
-
-    void *pb, *px;
-    if ((st = workspace(ctx, kSlotIn2, (size_t)n * S * 8, &pb)) != BK_OK) return st;
-    if ((st = workspace(ctx, kSlotOut2, (size_t)n * S * 8, &px)) != BK_OK) return st;
-    BK_CUDA_TRY(ctx, launch_rhs_padded(ctx, scratch, qd.dev, s, (double*)pb, S));
-    CgReport rep;
-    if ((st = block_cg_device(ctx, scratch, (const double*)pb, S, cfg, (double*)px, &rep)) != BK_OK)
-        return st;
-    BK_CUDA_TRY(ctx, cudaEventRecord(ev[3], ctx->stream));
-
-    Staged td, qo, rd;
-    const size_t out_n = (size_t)n * N;
-    if ((st = stage_out(ctx, kSlotT, T, out_n, &td)) != BK_OK) return st;
-    if ((st = stage_out(ctx, kSlotQo, Q, out_n, &qo)) != BK_OK) return st;
-    if ((st = stage_out(ctx, kSlotRes, resid, (size_t)N, &rd)) != BK_OK) return st;
-    if ((st = combine_action_device(ctx, scratch, (const double*)px, S, cd.dev, N, td.dev, qo.dev,
-                                    rd.dev)) != BK_OK)
-        return st;
-    BK_CUDA_TRY(ctx, cudaEventRecord(ev[4], ctx->stream));
-    if ((st = drain(ctx, td, T, out_n)) != BK_OK) return st;
-    if ((st = drain(ctx, qo, Q, out_n)) != BK_OK) return st;
-    if ((st = drain(ctx, rd, resid, (size_t)N)) != BK_OK) return st;
-    BK_CUDA_TRY(ctx, cudaEventRecord(ev[5], ctx->stream));
-    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-
-    const double solve_s = elapsed(ev[2], ev[3]) * 1e-3;
-    fill_report(rep, s, solve_s, report);
-    if (timings) {
-        timings->h2d_s = elapsed(ev[0], ev[1]) * 1e-3;
-        timings->assemble_s = elapsed(ev[1], ev[2]) * 1e-3;
-        timings->basis_solve_s = solve_s;
-        timings->combine_action_s = elapsed(ev[3], ev[4]) * 1e-3;
-        timings->d2h_s = elapsed(ev[4], ev[5]) * 1e-3;
-        timings->total_s = elapsed(ev[0], ev[5]) * 1e-3;
-        timings->iterations_total = rep.iterations;
-        timings->matvecs_total = rep.matvecs + N;
-    }
-    for (int j = 0; j < s; ++j)
-        if (!rep.converged[j])
-            return fail(ctx, BK_NOT_CONVERGED, "basis solve did not reach tolerance");
-    return BK_OK;
+    return generate_chip_impl(ctx, grid, k, bc, Qbasis, s, C, N, cfg, T, Q, resid, report,
+                              timings, false, 0);
 }
 
 }  // extern "C"
@@ -574,13 +669,14 @@ bk_status bk_generate_batch(bk_ctx* ctx, int n_chips, const bk_grid* grids,
     auto worker = [&](int w) {
         bk_ctx* sub = ctx->subs[w];
         const int64_t launches0 = sub->launches;
-        for (int c = w; c < n_chips; c += streams) {
+        int parity = 0;
+        for (int c = w; c < n_chips; c += streams, parity ^= 1) {
             bk_phase_timings pt;
             bk_solve_report* rep = reports ? &reports[c] : nullptr;
-            const bk_status r = bk_generate_chip(sub, &grids[c], k[c], bc + 6 * c, Qbasis[c], s,
-                                                 C[c], N, cfg, T ? T[c] : nullptr,
-                                                 Q ? Q[c] : nullptr, resid ? resid[c] : nullptr,
-                                                 rep, &pt);
+            const bk_status r = generate_chip_impl(sub, &grids[c], k[c], bc + 6 * c, Qbasis[c], s,
+                                                   C[c], N, cfg, T ? T[c] : nullptr,
+                                                   Q ? Q[c] : nullptr, resid ? resid[c] : nullptr,
+                                                   rep, &pt, true, parity);
             if (r != BK_OK && st[w] == BK_OK) {
                 st[w] = r;
                 msg[w] = sub->err;
@@ -594,6 +690,13 @@ bk_status bk_generate_batch(bk_ctx* ctx, int n_chips, const bk_grid* grids,
             tim[w].iterations_total += pt.iterations_total;
             tim[w].matvecs_total += pt.matvecs_total;
         }
+        // outputs of the last chips are still draining
+        if (sub->copy_stream && cudaStreamSynchronize(sub->copy_stream) != cudaSuccess &&
+            st[w] == BK_OK) {
+            st[w] = BK_CUDA_ERROR;
+            msg[w] = cudaGetErrorString(cudaGetLastError());
+        }
+        sub->drain_pending[0] = sub->drain_pending[1] = false;
         (void)launches0;
     };
     std::vector<std::thread> pool;

@@ -666,9 +666,10 @@ bk_status run_block_cg(bk_ctx* ctx, const bk_operator* op, const double* B, int 
     if (padded) {
         BK_CUDA_TRY(ctx, launch_pad_cols(ctx, (const double*)pX, S, X, s, n));
     }
-    BK_CUDA_TRY(ctx, cudaMemcpyAsync(rep, pRep, sizeof(CgReport), cudaMemcpyDeviceToHost,
-                                     ctx->stream));
-    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    {
+        const bk_status rs = read_small(ctx, rep, pRep, sizeof(CgReport));
+        if (rs != BK_OK) return rs;
+    }
     return BK_OK;
 }
 

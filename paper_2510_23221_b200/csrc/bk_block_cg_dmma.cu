@@ -925,9 +925,10 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
                                                  ctx->stream));
     ++ctx->launches;
     if (padded) BK_CUDA_TRY(ctx, launch_pad_cols(ctx, (const double*)pX, S, X, s, n));
-    BK_CUDA_TRY(ctx, cudaMemcpyAsync(rep, pRep, sizeof(CgReport), cudaMemcpyDeviceToHost,
-                                     ctx->stream));
-    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    {
+        const bk_status rs = read_small(ctx, rep, pRep, sizeof(CgReport));
+        if (rs != BK_OK) return rs;
+    }
     if (want_prof) {
         std::vector<long long> pr(PROF_ITERS * PROF_MARKS);
         cudaMemcpy(pr.data(), a.prof, pr.size() * sizeof(long long), cudaMemcpyDeviceToHost);

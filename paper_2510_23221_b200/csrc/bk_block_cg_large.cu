@@ -18,6 +18,7 @@
 // restart, beta = S_old^+ S_new, P = D^-1 R + P beta (phase 3). Dense s x s
 // products run on mma.sync.m16n8k4.f64; Gram partials are fixed-order per
 // CTA and reduced in CTA order (deterministic).
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -951,13 +952,12 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
         if (comm && comm->halo) comm->halo(comm->user, v, s);
     };
     auto read_cmd = [&](int* cmd, int* sa) -> bk_status {
-        int h[2];
-        BK_CUDA_TRY(ctx, cudaMemcpyAsync(h, &ctl->cmd, sizeof(int), cudaMemcpyDeviceToHost, s));
-        BK_CUDA_TRY(ctx, cudaMemcpyAsync(h + 1, &ctl->sa, sizeof(int), cudaMemcpyDeviceToHost, s));
-        BK_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-        *cmd = h[0];
-        *sa = h[1];
-        return BK_OK;
+        static_assert(offsetof(Ctl<S>, cmd) == offsetof(Ctl<S>, sa) + 3 * sizeof(int), "layout");
+        int h[4];  // sa, nver, iters, cmd
+        const bk_status rs = read_small(ctx, h, &ctl->sa, sizeof(h));
+        *sa = h[0];
+        *cmd = h[3];
+        return rs;
     };
     const int tr_blocks = (int)((sl.n_int + (LBS / S) - 1) / (LBS / S) < 4L * ctx->num_sms
                                     ? (sl.n_int + (LBS / S) - 1) / (LBS / S)
@@ -1027,8 +1027,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
         ++ctx->launches;
     }
     // honest residuals for still-active columns
-    BK_CUDA_TRY(ctx, cudaMemcpyAsync(&sa, &ctl->sa, sizeof(int), cudaMemcpyDeviceToHost, s));
-    BK_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    if ((st = read_small(ctx, &sa, &ctl->sa, sizeof(int))) != BK_OK) return st;
     if (sa > 0) {
         halo(a.X);
         true_res();
@@ -1036,9 +1035,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     k_ctl_final<S><<<1, 32, 0, s>>>(ctl, red, drep);
     ++ctx->launches;
     BK_CUDA_TRY(ctx, cudaGetLastError());
-    BK_CUDA_TRY(ctx, cudaMemcpyAsync(rep, drep, sizeof(CgReport), cudaMemcpyDeviceToHost, s));
-    BK_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-    return BK_OK;
+    return read_small(ctx, rep, drep, sizeof(CgReport));
 }
 
 // Single-GPU entry: global [n][S] B/X, slab = the whole grid.

@@ -29,6 +29,7 @@ struct ActArgs {
     int nx, ny, nz;
     int64_t n;
     int64_t N;
+    int64_t ldc;  // row stride of C
     const double* diag;
     const double* cx;
     const double* cy;
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(NT, 2) combine_action_kernel(ActArgs a) {
 
     for (int e = tid; e < S * NS; e += NT) {
         const int k = e / NS, q = e % NS;
-        Cs[k * CSTRIDE(NS) + q] = (k < a.s && j0 + q < a.N) ? a.C[(int64_t)k * a.N + j0 + q] : 0.0;
+        Cs[k * CSTRIDE(NS) + q] = (k < a.s && j0 + q < a.N) ? a.C[(int64_t)k * a.ldc + j0 + q] : 0.0;
     }
     __syncthreads();
 
@@ -239,7 +240,7 @@ __global__ void resid_finalize(const double* __restrict__ part, int tiles, int64
 
 template <int S, int NS>
 bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const double* C,
-              int64_t N, double* T, double* Q, double* resid) {
+              int64_t ldc, int64_t N, double* T, double* Q, double* resid) {
     using namespace bk;
     ActArgs a;
     a.nx = op->nx;
@@ -247,6 +248,7 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
     a.nz = op->nz;
     a.n = op->n;
     a.N = N;
+    a.ldc = ldc;
     a.diag = op->diag;
     a.cx = op->cx;
     a.cy = op->cy;
@@ -290,18 +292,18 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
 
 namespace bk {
 
-// X here is the kernel-width block: the caller passes n x s; widths other than
-// 8/16/32/64 are handled with S = next supported width and s = real width
-// (X must then be n x S padded; see bk_api.cu).
-bk_status combine_action_device(bk_ctx* ctx, const bk_operator* op, const double* X, int s,
-                                const double* C, int64_t N, double* T, double* Q,
-                                double* resid) {
+// X is the kernel-width block n x S (zero-padded past the real width s); C is
+// s x N with row stride ldc.
+bk_status combine_action_device(bk_ctx* ctx, const bk_operator* op, const double* X, int S,
+                                int s, const double* C, int64_t ldc, int64_t N, double* T,
+                                double* Q, double* resid) {
     if (N == 0) return BK_OK;
-    switch (s) {
-        case 8: return run<8, 16>(ctx, op, X, s, C, N, T, Q, resid);
-        case 16: return run<16, 16>(ctx, op, X, s, C, N, T, Q, resid);
-        case 32: return run<32, 16>(ctx, op, X, s, C, N, T, Q, resid);
-        case 64: return run<64, 16>(ctx, op, X, s, C, N, T, Q, resid);
+    if (s < 1 || s > S || ldc < N) return fail(ctx, BK_INTERNAL, "combine_action: bad widths");
+    switch (S) {
+        case 8: return run<8, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+        case 16: return run<16, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+        case 32: return run<32, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+        case 64: return run<64, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid);
         default: return fail(ctx, BK_INTERNAL, "combine_action: unpadded width");
     }
 }

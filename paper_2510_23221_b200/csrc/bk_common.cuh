@@ -33,8 +33,14 @@ struct bk_ctx {
     bk_operator* scratch = nullptr;  // operator reused by bk_generate_chip
     int cg_max_ctas = 0;             // 0 = every SM (see bk_set_cg_sm_budget)
     std::vector<bk_ctx*> subs;       // per-stream sub-contexts of bk_generate_batch
+    cudaStream_t copy_stream = nullptr;    // D2H of host outputs, overlapped with compute
+    std::vector<cudaEvent_t> chunk_ev;     // per-chunk "outputs ready" events
+    cudaEvent_t drain_ev[2] = {};          // copy stream done with output parity p
+    void* hmap = nullptr;                  // mapped pinned host page for small readbacks
+    void* hmap_dev = nullptr;
+    bool drain_pending[2] = {};
     // grow-only device workspace slots
-    static constexpr int kSlots = 24;
+    static constexpr int kSlots = 32;
     void* ws[kSlots] = {};
     size_t ws_bytes[kSlots] = {};
 };
@@ -54,6 +60,8 @@ struct bk_operator {
     double* cz = nullptr;
     double* g = nullptr;
     double* dinv = nullptr;  // jacobi_inverse (solvers.cpp:53-66)
+    int volz_cap = 0;  // doubles allocated at volz (grown only: no per-call cudaFree,
+                       // which would synchronize with in-flight output drains)
     double* volz = nullptr;  // cell volume per z-layer (nz)
     std::vector<double> h_volz;
 };
@@ -79,15 +87,24 @@ enum Slot : int {
     kSlotK,
     kSlotQ,
     kSlotC,
-    kSlotT,
+    kSlotT,         // outputs of bk_generate_chip (parity 0) ...
     kSlotQo,
     kSlotRes,
+    kSlotFlag,      // assemble's k > 0 check
+    kSlotT1,        // ... and parity 1: a batch drains chip c while chip c+1 computes
+    kSlotQo1,
+    kSlotRes1,
 };
 
 bk_status fail(bk_ctx* ctx, bk_status st, const std::string& msg);
 // Grow-only workspace; contents are not preserved on growth.
 bk_status workspace(bk_ctx* ctx, int slot, size_t bytes, void** out);
 bool is_device_ptr(const void* p);
+// Copy a few bytes device -> host through a kernel writing mapped pinned
+// memory (no copy engine: it never queues behind a large in-flight D2H drain)
+// and synchronize the stream. bytes <= 64 KiB, multiple of 4.
+bk_status read_small(bk_ctx* ctx, void* host_dst, const void* dev_src, size_t bytes);
+cudaError_t launch_copy_words(cudaStream_t s, unsigned* dst, const unsigned* src, size_t words);
 
 // Kernels' host-side launchers (return cudaError_t of the launch).
 cudaError_t launch_assemble(bk_ctx* ctx, const bk_operator* op, const double* k,
@@ -123,8 +140,10 @@ bk_status block_cg_large(bk_ctx* ctx, const bk_operator* op, const double* B, in
 bk_status block_cg_generic(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
                            const bk_solver_cfg* cfg, double* X, CgReport* rep);
 
-bk_status combine_action_device(bk_ctx* ctx, const bk_operator* op, const double* X, int s,
-                                const double* C, int64_t N, double* T, double* Q,
-                                double* resid);
+// S = kernel width of X (n x S, zero-padded), s = real basis width (rows of
+// C read), C row stride ldc (>= N: a sample sub-range of a wider C).
+bk_status combine_action_device(bk_ctx* ctx, const bk_operator* op, const double* X, int S,
+                                int s, const double* C, int64_t ldc, int64_t N, double* T,
+                                double* Q, double* resid);
 
 }  // namespace bk

@@ -254,6 +254,17 @@ cudaError_t launch_rhs_padded(bk_ctx* ctx, const bk_operator* op, const double* 
     return cudaGetLastError();
 }
 
+__global__ void copy_words_kernel(unsigned* __restrict__ dst, const unsigned* __restrict__ src,
+                                  size_t words) {
+    for (size_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+    __threadfence_system();
+}
+
+cudaError_t launch_copy_words(cudaStream_t s, unsigned* dst, const unsigned* src, size_t words) {
+    copy_words_kernel<<<1, 256, 0, s>>>(dst, src, words);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_check_positive(bk_ctx* ctx, const double* k, int64_t n, int* flag) {
     check_positive_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(k, n, flag);
     ++ctx->launches;

@@ -204,7 +204,10 @@ def test_combine_action_bitwise_vs_reference_golden(bk, ctx, name):
 
 
 def test_combine_action_bitwise_vs_oracle_odd_shapes(bk, ctx, oracle):
-    for case, N in (((1, 37, 29, 1, 8), 19), ((3, 33, 17, 8, 32), 21), ((4, 20, 9, 4, 16), 8)):
+    # widths 5 and 20 run on the padded 8 / 32 kernels: only the real s rows of
+    # C may be read
+    for case, N in (((1, 37, 29, 1, 8), 19), ((3, 33, 17, 8, 32), 21), ((4, 20, 9, 4, 16), 8),
+                    ((1, 37, 29, 1, 5), 19), ((3, 16, 12, 8, 20), 33)):
         inp = bk.synth_chip(*case, N)
         g = inp.grid
         op = bk.assemble(inp.k, g, inp.bc, ctx)
@@ -262,6 +265,31 @@ def test_generate_chip_host_and_device_pointers_agree(bk, ctx):
     torch.cuda.synchronize()
     assert np.array_equal(Td.cpu().numpy(), T1) and np.array_equal(Qd.cpu().numpy(), Q1)
     assert np.array_equal(Rd.cpu().numpy(), R1)
+
+
+def test_generate_chip_host_outputs_chunked(bk, ctx):
+    """Host output buffers are drained in sample chunks overlapped with the
+    combine (64 samples per chunk at 256 x 256): 150 samples = 3 chunks, the
+    last one partial; identical to the device-pointer call."""
+    import torch
+
+    inp = bk.synth_chip(2, 256, 256, 1, 16, 150)
+    n, N = inp.grid.cell_count(), 150
+    pin = lambda *shape: torch.empty(shape, dtype=torch.float64).pin_memory()  # noqa: E731
+    Th, Qh, Rh = pin(N, n), pin(N, n), pin(N)
+    bk.generate_chip(inp.grid, inp.k, inp.bc, inp.q_basis, inp.coef, cfg_jacobi(),
+                     t_out=Th, q_out=Qh, resid_out=Rh, ctx=ctx)
+    dev = torch.device("cuda", 0)
+    Td = torch.empty((N, n), dtype=torch.float64, device=dev)
+    Qd = torch.empty_like(Td)
+    Rd = torch.empty(N, dtype=torch.float64, device=dev)
+    bk.generate_chip(inp.grid, inp.k, inp.bc, inp.q_basis, inp.coef, cfg_jacobi(),
+                     t_out=Td, q_out=Qd, resid_out=Rd, ctx=ctx)
+    torch.cuda.synchronize()
+    assert torch.equal(Td.cpu(), Th) and torch.equal(Qd.cpu(), Qh) and torch.equal(Rd.cpu(), Rh)
+    T2, Q2, R2, _, _ = bk.generate_chip(inp.grid, inp.k, inp.bc, inp.q_basis, inp.coef,
+                                        cfg_jacobi(), ctx=ctx)  # pageable numpy outputs
+    assert np.array_equal(T2, Th.numpy()) and np.array_equal(Q2, Qh.numpy())
 
 
 @pytest.mark.slow
