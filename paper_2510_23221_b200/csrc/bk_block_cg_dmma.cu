@@ -309,10 +309,16 @@ __device__ void build_index(Sm<S, RES>& sm) {
 // sequence (the trailing block of Gauss-Jordan IS the Cholesky Schur
 // complement, so pivots and rank decisions coincide): one barrier per pivot,
 // the pivot search done redundantly by every warp (no broadcast barrier).
+// Pivot loop on 4 warps for S <= 16 (named barrier; measured 10.1k -> 7.0k
+// cycles at S = 16, 6.4k -> 3.7k at S = 8), on all 8 warps for S = 32.
+template <int S>
+constexpr int solve_warps() {
+    return S <= 16 ? 4 : CtaShape<S>::NW;
+}
 template <int S, bool PROF = false, int VAR = 0, bool RES = false>
 __device__ __forceinline__ void small_solve(Sm<S, RES>& sm, const double* M, const double* RHS,
                                             double* out) {
-    small_solve_t<S, CtaShape<S>::BS, PROF, VAR>(sm, M, RHS, out);
+    small_solve_t<S, CtaShape<S>::BS, PROF, VAR, solve_warps<S>()>(sm, M, RHS, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -1002,22 +1008,23 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) small_solve_bench_kernel(i
     if (threadIdx.x == 0) out[2 + 62] = clock64();
     small_solve<S, true>(sm, sm.mat, sm.s_old, sm.coef);
     __syncthreads();
-    long long tv[4];
-    for (int v = 1; v <= 3; ++v) {
+    long long tv[8] = {};
+    for (int v = 1; v <= 7; ++v) {
         __syncthreads();
         const long long a0 = clock64();
         for (int r = 0; r < 20; ++r) {
             if (v == 1) small_solve<S, false, 1>(sm, sm.mat, sm.s_old, sm.coef);
             if (v == 2) small_solve<S, false, 2>(sm, sm.mat, sm.s_old, sm.coef);
             if (v == 3) small_solve<S, false, 3>(sm, sm.mat, sm.s_old, sm.coef);
+            if (v == 4) small_solve_t<S, BS, false, 0, 1>(sm, sm.mat, sm.s_old, sm.coef);
+            if (v == 5) small_solve_t<S, BS, false, 0, 2>(sm, sm.mat, sm.s_old, sm.coef);
+            if (v == 6) small_solve_t<S, BS, false, 0, 4>(sm, sm.mat, sm.s_old, sm.coef);
+            if (v == 7 && BS >= 256) small_solve_t<S, BS, false, 0, 8>(sm, sm.mat, sm.s_old, sm.coef);
         }
         tv[v] = (clock64() - a0) / 20;
     }
-    if (threadIdx.x == 0) {
-        out[70] = tv[1];
-        out[71] = tv[2];
-        out[72] = tv[3];
-    }
+    if (threadIdx.x == 0)
+        for (int v = 1; v <= 7; ++v) out[69 + v] = tv[v];
     if (threadIdx.x == 0) {
         out[0] = (t1 - t0) / reps;
         out[1] = sm.rank;
@@ -1047,8 +1054,9 @@ extern "C" int bk_debug_small_solve_cycles(int s, int reps, long long* cycles, i
     fprintf(stderr, "small_solve<%d> stamps (cycles from start): setup %lld, first search %lld;", s,
             h[2] - h[64], h[3] - h[64]);
     for (int k = 1; k <= s; ++k) fprintf(stderr, " %lld", h[4 + k] ? h[4 + k] - h[64] : -1);
-    fprintf(stderr, "; end %lld | variants: no-update %lld, fixed-order %lld, no-barrier %lld\n",
-            h[65] - h[64], h[70], h[71], h[72]);
+    fprintf(stderr, "; end %lld | variants: no-update %lld, fixed-order %lld, no-barrier %lld, "
+            "warps 1/2/4/8: %lld %lld %lld %lld\n",
+            h[65] - h[64], h[70], h[71], h[72], h[73], h[74], h[75], h[76]);
     cudaMemcpy(coef, r, (size_t)s * s * 8, cudaMemcpyDeviceToHost);
     *cycles = h[0];
     *rank = (int)h[1];

@@ -51,14 +51,26 @@ __device__ __forceinline__ unsigned long long pos_bits(double v) {
 // every warp redundantly tracks the Schur diagonal in registers and searches
 // the next pivot while the block update of the current one is in flight.
 // SMT: any shared-memory struct with int sa, rank, idx[S]; double aug[S*LD+2S].
-template <int S, int BS, bool PROF = false, int VAR = 0, class SMT>
+// NWS: warps that run the pivot loop (the others wait at the final barrier);
+// fewer warps = a cheaper per-pivot barrier (named barrier 1, or __syncwarp
+// for one warp) against more rows per warp.
+template <int S, int BS, bool PROF = false, int VAR = 0, int NWS = BS / 32, class SMT>
 __device__ void small_solve_t(SMT& sm, const double* M, const double* RHS, double* out) {
     long long* const pr = PROF ? g_ss_prof : nullptr;
     auto stamp = [&](int k) {
         if (PROF && threadIdx.x == 0) pr[k] = clock64();
     };
-    auto wbar = []() { __syncthreads(); };
-    constexpr int NW = BS / 32;
+    constexpr int NWA = BS / 32;  // all warps: fill and output
+    static_assert(NWS >= 1 && NWS <= NWA, "participating warps");
+    auto wbar = []() {
+        if (NWS == NWA)
+            __syncthreads();
+        else if (NWS == 1)
+            __syncwarp();
+        else
+            asm volatile("bar.sync 1, %0;" ::"n"(NWS * 32) : "memory");
+    };
+    constexpr int NW = NWS;
     constexpr int LD = Strides<S>::LD;
     constexpr int RS = Strides<S>::RS;
     constexpr int R = (S + 31) / 32;  // diagonal entries per lane (index lane + 32 r)
@@ -68,7 +80,7 @@ __device__ void small_solve_t(SMT& sm, const double* M, const double* RHS, doubl
     unsigned long long donem = 0ull;  // compacted indices already used as pivots
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // rows by warp, columns by lane: no integer division, conflict-free rows
-    for (int i = warp; i < sa; i += NW) {
+    for (int i = warp; i < sa; i += NWA) {
         const int a = sm.idx[i];
         for (int q = lane; q < 2 * sa; q += 32) {
             double v;
@@ -82,7 +94,10 @@ __device__ void small_solve_t(SMT& sm, const double* M, const double* RHS, doubl
             aug[i * LD + q] = v;
         }
     }
-    wbar();
+    __syncthreads();
+    unsigned long long* const shared_done = reinterpret_cast<unsigned long long*>(aug + S * LD);
+    int rank = 0;
+    if (warp < NWS) {
     double dg[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -121,7 +136,6 @@ __device__ void small_solve_t(SMT& sm, const double* M, const double* RHS, doubl
     double pv;
     pivot_of(best, p, pv);
     double rinv = __drcp_rn(pv);
-    int rank = 0;
     stamp(1);
     constexpr int RPW = (S + NW - 1) / NW;    // rows per warp
     constexpr int CPL = (2 * S + 31) / 32;    // columns per lane
@@ -185,9 +199,12 @@ __device__ void small_solve_t(SMT& sm, const double* M, const double* RHS, doubl
         pv = pvn;
         rinv = rn;
     }
+    if (NWS < NWA && threadIdx.x == 0) *shared_done = donem;
+    }  // warp < NWS
     for (int e = threadIdx.x; e < S * RS; e += BS) out[e] = 0.0;
-    wbar();
-    for (int i = warp; i < sa; i += NW) {
+    __syncthreads();
+    if (NWS < NWA) donem = *shared_done;
+    for (int i = warp; i < sa; i += NWA) {
         if (!((donem >> i) & 1ull)) continue;
         const double di = __drcp_rn(aug[i * LD + i]);
         for (int q = lane; q < sa; q += 32) out[sm.idx[i] * RS + sm.idx[q]] = aug[i * LD + sa + q] * di;
