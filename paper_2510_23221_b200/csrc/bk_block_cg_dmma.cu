@@ -325,71 +325,51 @@ __device__ __forceinline__ void small_solve(Sm<S, RES>& sm, const double* M, con
 // phases
 // ---------------------------------------------------------------------------
 // phase 1: W = A P over the CTA's cells, Gram G += P^T W, in 16-cell tiles.
-// Lane (r = lane / 2, h = lane % 2) owns row segment [cw*h, cw*h + cw) of cell
-// base + r (cw = min(S/2, 8) columns per pass): every stencil row is read with
-// 128-bit loads, the accumulation follows the reference CSR order
-// (apply_block_fixed, discretize.cpp:57-71), W leaves with 128-bit stores, and
-// P / W are staged through the warp's smem tiles for the DMMA Gram (K = cells).
+// Lane (q = lane / (S/2), j = lane % (S/2)) owns columns 2j, 2j+1 of cells
+// base + q + (32 / (S/2)) u: every load instruction reads whole 128-byte rows
+// (4 L1 tag lookups per LDG.128 at S = 16 instead of 16 with a lane per half
+// row). Each element's accumulation follows the reference CSR order
+// (apply_block_fixed, discretize.cpp:57-71); W leaves with 128-bit stores, and
+// P / W are staged in the warp's smem tiles for the DMMA Gram (K = cells).
 template <int S>
 __device__ __forceinline__ void phase_spmm_gram(const Args& a, int64_t c0, int64_t c1, int warp,
                                                 int lane, double* tp, double* tw, GramAcc<S>& G) {
     constexpr int NW = CtaShape<S>::NW;
     constexpr int RS = Strides<S>::RS;
-    constexpr int CW = S / 2 < 8 ? S / 2 : 8;   // columns per lane per pass
-    constexpr int PASSES = S / (2 * CW);
-    const int r = lane >> 1, h = lane & 1;
+    constexpr int LPR = S / 2;     // lanes per row (one 16-byte column pair each)
+    constexpr int CPI = 32 / LPR;  // cells per load instruction
+    constexpr int U = 16 / CPI;    // cells per lane per tile
+    const int q = lane / LPR, col = 2 * (lane % LPR);
     const int g = lane >> 2, t = lane & 3;
     const int64_t plane = (int64_t)a.nx * a.ny;
     for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
-        const int64_t cell = base + r;
-        const bool v = cell < c1;
-        Coef k;
-        if (v) load_coef(a, cell, k);
 #pragma unroll
-        for (int ps = 0; ps < PASSES; ++ps) {
-            const int col = ps * 2 * CW + h * CW;
-            double acc[CW], ctr[CW];
-#pragma unroll
-            for (int j = 0; j < CW; ++j) acc[j] = ctr[j] = 0.0;
-            if (v) {
+        for (int u = 0; u < U; ++u) {
+            const int lr = q + CPI * u;  // row of the tile
+            const int64_t cell = base + lr;
+            double2 acc = make_double2(0.0, 0.0), ctr = make_double2(0.0, 0.0);
+            if (cell < c1) {
+                Coef k;
+                load_coef(a, cell, k);
                 auto row = [&](int64_t c, double coef, bool has) {
                     if (!has) return;
-                    const double2* src = reinterpret_cast<const double2*>(a.P + c * S + col);
-#pragma unroll
-                    for (int j = 0; j < CW / 2; ++j) {
-                        const double2 x = src[j];
-                        acc[2 * j] = fma(coef, x.x, acc[2 * j]);
-                        acc[2 * j + 1] = fma(coef, x.y, acc[2 * j + 1]);
-                    }
+                    const double2 x = *reinterpret_cast<const double2*>(a.P + c * S + col);
+                    acc.x = fma(coef, x.x, acc.x);
+                    acc.y = fma(coef, x.y, acc.y);
                 };
                 row(cell - plane, k.zm, k.hzm);
                 row(cell - a.nx, k.ym, k.hym);
                 row(cell - 1, k.xm, k.hxm);
-                {
-                    const double2* src = reinterpret_cast<const double2*>(a.P + cell * S + col);
-#pragma unroll
-                    for (int j = 0; j < CW / 2; ++j) {
-                        const double2 x = src[j];
-                        ctr[2 * j] = x.x;
-                        ctr[2 * j + 1] = x.y;
-                        acc[2 * j] = fma(k.d, x.x, acc[2 * j]);
-                        acc[2 * j + 1] = fma(k.d, x.y, acc[2 * j + 1]);
-                    }
-                }
+                ctr = *reinterpret_cast<const double2*>(a.P + cell * S + col);
+                acc.x = fma(k.d, ctr.x, acc.x);
+                acc.y = fma(k.d, ctr.y, acc.y);
                 row(cell + 1, k.xp, k.hxp);
                 row(cell + a.nx, k.yp, k.hyp);
                 row(cell + plane, k.zp, k.hzp);
-                double2* dst = reinterpret_cast<double2*>(a.W + cell * S + col);
-#pragma unroll
-                for (int j = 0; j < CW / 2; ++j) dst[j] = make_double2(acc[2 * j], acc[2 * j + 1]);
+                *reinterpret_cast<double2*>(a.W + cell * S + col) = acc;
             }
-#pragma unroll
-            for (int j = 0; j < CW / 2; ++j) {
-                *reinterpret_cast<double2*>(tp + r * RS + col + 2 * j) =
-                    make_double2(ctr[2 * j], ctr[2 * j + 1]);
-                *reinterpret_cast<double2*>(tw + r * RS + col + 2 * j) =
-                    make_double2(acc[2 * j], acc[2 * j + 1]);
-            }
+            *reinterpret_cast<double2*>(tp + lr * RS + col) = ctr;
+            *reinterpret_cast<double2*>(tw + lr * RS + col) = acc;
         }
         __syncwarp();
         // G += P^T W over the tile's 16 cells (K = cells)
@@ -406,6 +386,46 @@ __device__ __forceinline__ void phase_spmm_gram(const Args& a, int64_t c0, int64
             }
         }
         __syncwarp();
+    }
+}
+
+// Rows [base, base + 16) of V (n x S) into the warp tile T[16][RS] by
+// cp.async whole-row 16-byte copies (rows past c1 zero-filled). The caller
+// commits / waits; __syncwarp before reading.
+template <int S>
+__device__ __forceinline__ void stage_tile(double* T, const double* __restrict__ V, int64_t base,
+                                           int64_t c1, int lane) {
+    constexpr int RS = Strides<S>::RS;
+    constexpr int LPR = S / 2, CPI = 32 / LPR, U = 16 / CPI;
+    const int q = lane / LPR, col = 2 * (lane % LPR);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int lr = q + CPI * u;
+        double* dst = T + lr * RS + col;
+        if (base + lr < c1) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
+                         "l"(V + (base + lr) * S + col)
+                         : "memory");
+        } else {
+            *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+        }
+    }
+}
+
+__device__ __forceinline__ void cp_commit_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// A fragments of a staged tile: f[ks][0] = T[g][4ks+t], f[ks][1] = T[g+8][4ks+t]
+template <int S>
+__device__ __forceinline__ void afrag_smem(const double* T, int g, int t, double (&f)[S / 4][2],
+                                           double sign) {
+    constexpr int RS = Strides<S>::RS;
+#pragma unroll
+    for (int ks = 0; ks < S / 4; ++ks) {
+        f[ks][0] = sign * T[g * RS + 4 * ks + t];
+        f[ks][1] = sign * T[(g + 8) * RS + 4 * ks + t];
     }
 }
 
@@ -664,10 +684,15 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         double rr[NT][2] = {};
         for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
             double pa[KS][2], wa[KS][2], x[NT][4], r[NT][4];
-            load_afrag<S>(a.P, base, c1, g, t, pa, 1.0);
-            load_afrag<S>(a.W, base, c1, g, t, wa, -1.0);
+            stage_tile<S>(tr, a.P, base, c1, lane);
+            stage_tile<S>(tz, a.W, base, c1, lane);
             Xv.load(base, g, t, x);
             Rv.load(base, g, t, r);
+            cp_commit_wait_all();
+            __syncwarp();
+            afrag_smem<S>(tr, g, t, pa, 1.0);
+            afrag_smem<S>(tz, g, t, wa, -1.0);
+            __syncwarp();  // tr / tz are rewritten by tile_gram below
 #pragma unroll
             for (int n = 0; n < NT; ++n)
 #pragma unroll
@@ -793,8 +818,12 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         if (pm) pm[6] = gtimer();
         for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
             double pa[KS][2], p[NT][4];
-            load_afrag<S>(a.P, base, c1, g, t, pa, 1.0);
+            stage_tile<S>(tr, a.P, base, c1, lane);
             Rv.load(base, g, t, p);
+            cp_commit_wait_all();
+            __syncwarp();
+            afrag_smem<S>(tr, g, t, pa, 1.0);
+            __syncwarp();
             const double d0 = dinv_at(a, base + g, c1, jac), d1 = dinv_at(a, base + g + 8, c1, jac);
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
