@@ -228,6 +228,15 @@ def run_reference_arm(args):
     return 0
 
 
+def ncu_traffic(config):
+    """Measured DRAM traffic of the roofline kernel (profiles/ncu_traffic.json)."""
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(tp):
+        return None
+    with open(tp) as f:
+        return json.load(f).get(f"config{config}")
+
+
 def config_dict(config, world):
     import paper_2510_23221_b200 as bk
 
@@ -369,11 +378,7 @@ def run_ours(args):
     mean_iters = float(np.mean(iters))
     achieved = mean_iters * bytes_per_iter / float(np.mean(solve_s)) / 1e9
     peak, peak_kind = peaks()
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            traffic = json.load(f).get(f"config{args.config}")
+    traffic = ncu_traffic(args.config)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -398,8 +403,10 @@ def run_ours(args):
                 "outputs_equal_device_path": same},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "block_cg_kernel (persistent, one launch per solve)",
+                     "kernel": "block_cg_dmma_kernel (persistent, one launch per solve)",
+                     "traffic_unit": "DRAM bytes per launch (ncu), vs algorithmic_bytes_per_launch",
                      "algorithmic_bytes_per_iter": bytes_per_iter,
+                     "algorithmic_bytes_per_launch": int(mean_iters * bytes_per_iter),
                      "iterations_per_solve": mean_iters,
                      "solve_ms": float(np.mean(solve_s)) * 1e3, "peak_source": peak_kind},
         "cpu_baseline": cpu,
@@ -585,7 +592,9 @@ def run_ours_large(args, ctx, world, rank, local):
         "data": "synthetic (seeded BASELINE-config generators, DESIGN.md §Inputs)",
         "config": config_dict(5, world), "converged": bool(rep.all_converged()),
         "roofline": {"bound": "hbm", "achieved": achieved * world, "peak": peak * world,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(5),
+                     "traffic_unit": "DRAM bytes per iteration (ncu), vs algorithmic_bytes_per_iter",
+                     "algorithmic_bytes_per_iter": int(bytes_per_iter),
                      "kernel": "multi-kernel block CG (S=64) per rank",
                      "iterations_per_solve": float(np.mean(iters)),
                      "solve_ms": float(np.mean(solve)) * 1e3,

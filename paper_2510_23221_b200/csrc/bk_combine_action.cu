@@ -40,7 +40,8 @@ struct ActArgs {
     const double* C;  // S x N
     double* T;        // N x n (nullable)
     double* Q;        // N x n (nullable)
-    double* part;     // tiles x N x 2 residual partials (nullable)
+    double* part;     // N x tiles x 2 residual partials (nullable)
+    int tiles;
     int s;            // real basis width (<= S)
 };
 
@@ -217,25 +218,33 @@ __global__ void __launch_bounds__(NT, 2) combine_action_kernel(ActArgs a) {
                 u += red[(w * NS + tid) * 2];
                 v += red[(w * NS + tid) * 2 + 1];
             }
-            a.part[((int64_t)tile * a.N + j0 + tid) * 2] = u;
-            a.part[((int64_t)tile * a.N + j0 + tid) * 2 + 1] = v;
+            double* pp = a.part + ((j0 + tid) * (int64_t)a.tiles + tile) * 2;
+            *reinterpret_cast<double2*>(pp) = make_double2(u, v);
         }
     }
 }
 
-// resid_j = sqrt(num / den) over tiles in order; de == 0 handled as
+// resid_j = sqrt(num / den) over the tiles (one warp per sample: lane-strided
+// sums, then a fixed shuffle tree — deterministic); de == 0 handled as
 // pipeline.cpp:570-571.
 __global__ void resid_finalize(const double* __restrict__ part, int tiles, int64_t N,
                                double* __restrict__ resid) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N;
-         j += (int64_t)gridDim.x * blockDim.x) {
-        double nu = 0.0, de = 0.0;
-        for (int t = 0; t < tiles; ++t) {
-            nu += part[((int64_t)t * N + j) * 2];
-            de += part[((int64_t)t * N + j) * 2 + 1];
-        }
-        resid[j] = de == 0.0 ? (nu == 0.0 ? 0.0 : 1.0) : sqrt(nu / de);
+    const int lane = threadIdx.x & 31;
+    const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (j >= N) return;
+    const double2* p = reinterpret_cast<const double2*>(part) + j * tiles;
+    double nu = 0.0, de = 0.0;
+    for (int t = lane; t < tiles; t += 32) {
+        const double2 v = p[t];
+        nu += v.x;
+        de += v.y;
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        nu += __shfl_xor_sync(0xffffffffu, nu, o);
+        de += __shfl_xor_sync(0xffffffffu, de, o);
+    }
+    if (lane == 0) resid[j] = de == 0.0 ? (nu == 0.0 ? 0.0 : 1.0) : sqrt(nu / de);
 }
 
 template <int S, int NS>
@@ -263,6 +272,7 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
     const int tilesx = (op->nx + TX - 1) / TX, tilesy = (op->ny + TY - 1) / TY;
     const int tiles = tilesx * tilesy;
     a.part = nullptr;
+    a.tiles = tiles;
     if (resid) {
         void* p;
         bk_status st = workspace(ctx, kSlotActPart, (size_t)tiles * N * 2 * sizeof(double), &p);
@@ -280,8 +290,7 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
     ++ctx->launches;
     BK_CUDA_TRY(ctx, cudaGetLastError());
     if (resid) {
-        resid_finalize<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(a.part, tiles, N,
-                                                                            resid);
+        resid_finalize<<<(unsigned)((N + 7) / 8), 256, 0, ctx->stream>>>(a.part, tiles, N, resid);
         ++ctx->launches;
         BK_CUDA_TRY(ctx, cudaGetLastError());
     }
