@@ -194,32 +194,39 @@ __global__ void __launch_bounds__(NT, 2) combine_action_kernel(ActArgs a) {
     }
 
     if (a.part) {
-        // CTA reduction of the residual partials, fixed order (warp tree, then
-        // warps in index order). Reuses the ring buffer.
+        // CTA reduction of the residual partials, fixed order. Warp level: a
+        // transpose-reduce of the 2 NS = 32 per-lane sums (31 shuffles; lane L
+        // ends with sum L: num of sample L for L < NS, den of sample L - NS
+        // otherwise); then warps in index order. Reuses the ring buffer.
+        static_assert(2 * NS == 32, "one sum per lane after the transpose-reduce");
         const int lane = tid & 31, warp = tid >> 5;
-        double* red = ring;  // 8 warps x NS x 2
+        double* red = ring;  // 8 warps x 32
+        double v[32];
 #pragma unroll
         for (int q = 0; q < NS; ++q) {
-            double u = num[q], v = den[q];
+            v[q] = num[q];
+            v[NS + q] = den[q];
+        }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                u += __shfl_xor_sync(0xffffffffu, u, o);
-                v += __shfl_xor_sync(0xffffffffu, v, o);
-            }
-            if (lane == 0) {
-                red[(warp * NS + q) * 2] = u;
-                red[(warp * NS + q) * 2 + 1] = v;
+        for (int o = 16; o > 0; o >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < o; ++i) {
+                const double keep = up ? v[o + i] : v[i];
+                const double send = up ? v[i] : v[o + i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
             }
         }
+        red[warp * 32 + lane] = v[0];
         __syncthreads();
         if (tid < NS && j0 + tid < a.N) {
-            double u = 0.0, v = 0.0;
-            for (int w = 0; w < NT / 32; ++w) {
-                u += red[(w * NS + tid) * 2];
-                v += red[(w * NS + tid) * 2 + 1];
+            double u = 0.0, w = 0.0;
+            for (int k = 0; k < NT / 32; ++k) {
+                u += red[k * 32 + tid];
+                w += red[k * 32 + NS + tid];
             }
             double* pp = a.part + ((j0 + tid) * (int64_t)a.tiles + tile) * 2;
-            *reinterpret_cast<double2*>(pp) = make_double2(u, v);
+            *reinterpret_cast<double2*>(pp) = make_double2(u, w);
         }
     }
 }
