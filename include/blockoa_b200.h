@@ -133,6 +133,18 @@ bk_status bk_operator_export_csr(bk_ctx* ctx, const bk_operator* op, int64_t* ro
                                  int32_t* col, double* val, int64_t* nnz, double* g,
                                  double* vol);
 
+/* The device stencil from an operator the reference assembled: drop-in for
+ * block_cg(const CsrMatrix&, ...) / DiscreteOperator{A, g, volumes}
+ * (solvers.hpp:85, discretize.hpp:62-69). The CSR must be a symmetric 7-point
+ * stencil on `grid` (columns i +- 1, +- nx, +- nx*ny with grid adjacency; the
+ * reference omits zero off-diagonals) with volumes uniform per z-layer;
+ * otherwise BK_INVALID_SPEC. D^-1 is jacobi_inverse (solvers.cpp:53-66).
+ * Bitwise the same operator as bk_assemble on the same inputs. Host pointers;
+ * g / vol may be NULL (zero lift / unit volumes). */
+bk_status bk_operator_from_csr(bk_ctx* ctx, const bk_grid* grid, const int64_t* row_ptr,
+                               const int32_t* col, const double* val, const double* g,
+                               const double* vol, bk_operator** out);
+
 /* Y = A X for n x s blocks        CsrMatrix::apply_block discretize.hpp:57,
  * discretize.cpp:75-95 (same per-row FMA accumulation order). */
 bk_status bk_apply_block(bk_ctx* ctx, const bk_operator* op, const double* X, int s,

@@ -41,7 +41,7 @@ import numpy as np
 __all__ = [
     "GridSpec", "Dirichlet", "Robin", "Adiabatic", "BoundarySpec", "SolverConfig",
     "SolveReport", "BlockCgResult", "PhaseTimings", "DiscreteOperator", "Context",
-    "assemble", "block_cg", "combine_action", "generate_chip", "generate_batch", "rhs_from_power",
+    "assemble", "operator_from_csr", "block_cg", "combine_action", "generate_chip", "generate_batch", "rhs_from_power",
     "power_from_rhs", "cg_error_bound", "derive_seed", "synth_chip", "library_path",
     "Error", "InvalidSpecError", "InvalidConfigError", "DimensionMismatchError",
     "NonPositiveConductivityError", "NonPositiveHtcError", "EmptyBasisError",
@@ -140,6 +140,7 @@ def _load():
         lib.bk_operator_n.argtypes = [vp]
         lib.bk_operator_n.restype = C.c_int64
         lib.bk_operator_export_csr.argtypes = [vp, vp, dp, dp, dp, C.POINTER(C.c_int64), dp, dp]
+        lib.bk_operator_from_csr.argtypes = [vp, C.POINTER(_Grid), dp, dp, dp, dp, dp, C.POINTER(vp)]
         lib.bk_apply_block.argtypes = [vp, vp, dp, C.c_int, dp]
         lib.bk_rhs_from_power.argtypes = [vp, vp, dp, C.c_int, dp]
         lib.bk_power_from_rhs.argtypes = [vp, vp, dp, C.c_int, dp]
@@ -446,6 +447,33 @@ def assemble(k, grid: GridSpec, bc: BoundarySpec, ctx: Optional[Context] = None)
     h = C.c_void_p()
     _raise(_load().bk_assemble(ctx.h, C.byref(g), pk, faces, C.byref(h)), ctx.h, "assemble")
     return DiscreteOperator(h, ctx, grid, bc)
+
+
+def operator_from_csr(grid: GridSpec, row_ptr, col, val, g=None, volumes=None,
+                      ctx: Optional[Context] = None,
+                      boundary: Optional["BoundarySpec"] = None) -> DiscreteOperator:
+    """Device stencil from the reference's assembled CSR (DiscreteOperator{A, g,
+    volumes}, discretize.hpp:62-69): the drop-in for block_cg(const CsrMatrix&).
+    Raises InvalidSpecError unless A is a symmetric 7-point stencil on `grid`
+    with volumes uniform per z-layer."""
+    ctx = _ctx(ctx)
+    n = grid.cell_count()
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    val = np.ascontiguousarray(val, dtype=np.float64)
+    if row_ptr.shape != (n + 1,) or col.shape != val.shape or int(row_ptr[-1]) != col.size:
+        raise DimensionMismatchError("operator_from_csr: CSR shape does not match the grid")
+    gg = None if g is None else np.ascontiguousarray(g, dtype=np.float64)
+    vv = None if volumes is None else np.ascontiguousarray(volumes, dtype=np.float64)
+    for a in (gg, vv):
+        if a is not None and a.shape != (n,):
+            raise DimensionMismatchError("operator_from_csr: g / volumes must have n entries")
+    gr, keep = grid._c()
+    h = C.c_void_p()
+    ptr = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    _raise(_load().bk_operator_from_csr(ctx.h, C.byref(gr), ptr(row_ptr), ptr(col), ptr(val),
+                                        ptr(gg), ptr(vv), C.byref(h)), ctx.h, "operator_from_csr")
+    return DiscreteOperator(h, ctx, grid, boundary)
 
 
 def _cols(a) -> int:

@@ -520,6 +520,113 @@ bk_status bk_operator_export_csr(bk_ctx* ctx, const bk_operator* op, int64_t* ro
     return BK_OK;
 }
 
+bk_status bk_operator_from_csr(bk_ctx* ctx, const bk_grid* grid, const int64_t* row_ptr,
+                               const int32_t* col, const double* val, const double* g,
+                               const double* vol, bk_operator** out) {
+    if (!ctx || !out || !row_ptr) return BK_INVALID_CONFIG;
+    bk_status st = validate_grid(ctx, grid);
+    if (st != BK_OK) return st;
+    cudaSetDevice(ctx->device);
+    const int nx = grid->nx, ny = grid->ny, nz = grid->nz;
+    const int64_t plane = (int64_t)nx * ny, n = plane * nz;
+    if (n > 2147483647LL) return fail(ctx, BK_INVALID_SPEC, "from_csr: grid too large");
+    if (row_ptr[0] != 0) return fail(ctx, BK_INVALID_SPEC, "from_csr: row_ptr[0] != 0");
+    if (row_ptr[n] > 0 && (!col || !val))
+        return fail(ctx, BK_INVALID_SPEC, "from_csr: null col / val");
+    std::vector<double> d(n, 0.0), cx(n, 0.0), cy(n, 0.0), cz(n, 0.0), dinv(n, 1.0);
+    // forward faces from the upper entries; every lower entry must mirror the
+    // upper one bitwise (interior_conductance is commutative, so the
+    // reference's matrix is exactly symmetric)
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t p0 = row_ptr[i], p1 = row_ptr[i + 1];
+        if (p1 < p0) return fail(ctx, BK_INVALID_SPEC, "from_csr: row_ptr not monotone");
+        const int ix = (int)(i % nx), iy = (int)((i / nx) % ny), iz = (int)(i / plane);
+        bool has_diag = false, lo_x = false, lo_y = false, lo_z = false;
+        for (int64_t p = p0; p < p1; ++p) {
+            const int64_t c = col[p];
+            const double v = val[p];
+            if (c == i) {
+                d[i] = v;
+                has_diag = true;
+            } else if (c == i + 1 && ix < nx - 1) {
+                cx[i] = -v;
+            } else if (c == i + nx && iy < ny - 1) {
+                cy[i] = -v;
+            } else if (c == i + plane && iz < nz - 1) {
+                cz[i] = -v;
+            } else if (c == i - 1 && ix > 0) {
+                lo_x = true;
+                if (!(-v == cx[i - 1]) || cx[i - 1] == 0.0)
+                    return fail(ctx, BK_INVALID_SPEC, "from_csr: matrix is not symmetric");
+            } else if (c == i - nx && iy > 0) {
+                lo_y = true;
+                if (!(-v == cy[i - nx]) || cy[i - nx] == 0.0)
+                    return fail(ctx, BK_INVALID_SPEC, "from_csr: matrix is not symmetric");
+            } else if (c == i - plane && iz > 0) {
+                lo_z = true;
+                if (!(-v == cz[i - plane]) || cz[i - plane] == 0.0)
+                    return fail(ctx, BK_INVALID_SPEC, "from_csr: matrix is not symmetric");
+            } else {
+                return fail(ctx, BK_INVALID_SPEC, "from_csr: not a 7-point stencil on this grid");
+            }
+        }
+        // an upper entry of an earlier row needs its mirror in this row
+        if ((ix > 0 && cx[i - 1] != 0.0 && !lo_x) || (iy > 0 && cy[i - nx] != 0.0 && !lo_y) ||
+            (iz > 0 && cz[i - plane] != 0.0 && !lo_z))
+            return fail(ctx, BK_INVALID_SPEC, "from_csr: matrix is not symmetric");
+        if (!has_diag) return fail(ctx, BK_INVALID_SPEC, "from_csr: missing diagonal");
+        if (d[i] != 0.0) dinv[i] = 1.0 / d[i];
+    }
+    std::vector<double> vz(nz, 1.0);
+    if (vol)
+        for (int z = 0; z < nz; ++z) {
+            vz[z] = vol[z * plane];
+            for (int64_t c = 0; c < plane; ++c)
+                if (vol[z * plane + c] != vz[z])
+                    return fail(ctx, BK_INVALID_SPEC, "from_csr: volumes must be uniform per z-layer");
+        }
+    bk_operator* op = new (std::nothrow) bk_operator;
+    if (!op) return fail(ctx, BK_OOM, "from_csr: host allocation");
+    auto bail = [&](bk_status e, const char* m) {
+        free_op_buffers(op);
+        delete op;
+        return fail(ctx, e, m);
+    };
+    const size_t nb = (size_t)n * sizeof(double);
+    if (cudaMalloc(&op->diag, nb) != cudaSuccess || cudaMalloc(&op->cx, nb) != cudaSuccess ||
+        cudaMalloc(&op->cy, nb) != cudaSuccess || cudaMalloc(&op->cz, nb) != cudaSuccess ||
+        cudaMalloc(&op->g, nb) != cudaSuccess || cudaMalloc(&op->dinv, nb) != cudaSuccess ||
+        cudaMalloc(&op->volz, (size_t)2 * nz * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(BK_OOM, "from_csr: device allocation");
+    }
+    op->volz_cap = 2 * nz;
+    op->device = ctx->device;
+    op->nx = nx;
+    op->ny = ny;
+    op->nz = nz;
+    op->n = n;
+    op->h_volz = vz;
+    std::vector<double> up(vz);
+    for (int z = 0; z < nz; ++z) up.push_back(grid->dz ? grid->dz[z] : grid->lz / nz);
+    std::vector<double> gz(n, 0.0);
+    if (g) std::memcpy(gz.data(), g, nb);
+    const bool ok = cudaMemcpy(op->diag, d.data(), nb, cudaMemcpyHostToDevice) == cudaSuccess &&
+                    cudaMemcpy(op->cx, cx.data(), nb, cudaMemcpyHostToDevice) == cudaSuccess &&
+                    cudaMemcpy(op->cy, cy.data(), nb, cudaMemcpyHostToDevice) == cudaSuccess &&
+                    cudaMemcpy(op->cz, cz.data(), nb, cudaMemcpyHostToDevice) == cudaSuccess &&
+                    cudaMemcpy(op->g, gz.data(), nb, cudaMemcpyHostToDevice) == cudaSuccess &&
+                    cudaMemcpy(op->dinv, dinv.data(), nb, cudaMemcpyHostToDevice) == cudaSuccess &&
+                    cudaMemcpy(op->volz, up.data(), up.size() * sizeof(double),
+                               cudaMemcpyHostToDevice) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        return bail(BK_CUDA_ERROR, "from_csr: upload");
+    }
+    *out = op;
+    return BK_OK;
+}
+
 bk_status bk_apply_block(bk_ctx* ctx, const bk_operator* op, const double* X, int s, double* Y) {
     if (!ctx || !op) return BK_INVALID_CONFIG;
     if (s < 1) return fail(ctx, BK_DIMENSION_MISMATCH, "apply_block: s must be >= 1");

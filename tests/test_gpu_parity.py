@@ -45,6 +45,52 @@ def test_mixed_operator_and_apply_bitwise(bk, ctx):
         assert np.array_equal(op.apply_block(x), d[f"y{s}"]), s
 
 
+def test_operator_from_reference_csr(bk, ctx):
+    """bk_operator_from_csr on the reference's own assembled CSR (golden): the
+    same operator bitwise as bk_assemble, so block_cg(const CsrMatrix&) is a
+    drop-in."""
+    d = golden("mixed_operator.npz")
+    faces = [bk.Dirichlet(a) if kd == 0 else bk.Robin(a, b) if kd == 1 else bk.Adiabatic()
+             for kd, a, b in zip(d["bc_kind"], d["bc_a"], d["bc_b"])]
+    gr = d["grid"]
+    grid = bk.GridSpec(int(gr[0]), int(gr[1]), int(gr[2]), gr[3], gr[4], gr[5])
+    op = bk.operator_from_csr(grid, d["row_ptr"], d["col"], d["val"], d["g"], d["vol"], ctx)
+    for a, key in zip(op.csr(), ("row_ptr", "col", "val", "g", "vol")):
+        assert np.array_equal(a, d[key]), key
+    for s in (1, 4, 7, 16):
+        assert np.array_equal(op.apply_block(d[f"x{s}"]), d[f"y{s}"]), s
+    ref = bk.assemble(d["k"], grid, bk.BoundarySpec(faces), ctx)
+    B = np.random.default_rng(3).uniform(0.0, 1.0, (grid.cell_count(), 8))
+    r1, r2 = bk.block_cg(op, B, cfg_jacobi()), bk.block_cg(ref, B, cfg_jacobi())
+    assert np.array_equal(r1.x, r2.x) and r1.report.iterations == r2.report.iterations
+
+
+def test_operator_from_csr_nonuniform_layers_and_rejects(bk, ctx, oracle):
+    inp = bk.synth_chip(4, 20, 12, 4, 16, 2, chip_id=3)
+    g = inp.grid
+    o = oracle.assemble(grid_tuple(g), inp.k, inp.bc.as_tuples(), dz=g.dz)
+    row_ptr, col, val, gg, vol = oracle.csr(o)
+    op = bk.operator_from_csr(g, row_ptr, col, val, gg, vol, ctx)
+    ref = bk.assemble(inp.k, g, inp.bc, ctx)
+    B = oracle.rhs_from_power(o, inp.q_basis)
+    assert np.array_equal(bk.block_cg(op, B, cfg_jacobi()).x, bk.block_cg(ref, B, cfg_jacobi()).x)
+    T1, Q1, _ = bk.combine_action(op, B, inp.coef)
+    T2, Q2, _ = bk.combine_action(ref, B, inp.coef)
+    assert np.array_equal(T1, T2) and np.array_equal(Q1, Q2)
+    bad = val.copy()
+    p = int(np.flatnonzero(col[row_ptr[5]:row_ptr[6]] == 6)[0]) + int(row_ptr[5])
+    bad[p] *= 1.0 + 1e-15  # A[5][6] != A[6][5]
+    with pytest.raises(bk.InvalidSpecError):
+        bk.operator_from_csr(g, row_ptr, col, bad, gg, vol, ctx)
+    wrong = bk.GridSpec(g.nx * 2, g.ny // 2, g.nz, g.lx, g.ly, g.lz, dz=g.dz)
+    with pytest.raises(bk.InvalidSpecError):
+        bk.operator_from_csr(wrong, row_ptr, col, val, gg, vol, ctx)
+    v2 = vol.copy()
+    v2[7] *= 2.0
+    with pytest.raises(bk.InvalidSpecError):
+        bk.operator_from_csr(g, row_ptr, col, val, gg, v2, ctx)
+
+
 @pytest.mark.parametrize("case", [(1, 32, 32, 1, 8), (2, 48, 40, 1, 16), (3, 16, 16, 8, 32),
                                   (4, 24, 16, 4, 16), (5, 8, 8, 16, 64)])
 def test_assemble_apply_rhs_bitwise_vs_oracle(bk, ctx, oracle, case):
