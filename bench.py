@@ -228,6 +228,22 @@ def run_reference_arm(args):
     return 0
 
 
+DMMA_PEAK_TFLOPS = 73.9  # mma.sync.m16n8k4.f64, measured (profiles/r1_summary.md)
+
+
+def action_roofline(n, s, N, comb_s, peak):
+    """Combine + operator action: algorithmic bytes
+    n(8s + 40) + 16 n N and the T = X C product 2 n s N on FP64 tensor cores."""
+    byts = n * (8 * s + 40) + 16 * n * N
+    flops = 2 * n * s * N
+    gbs = byts / comb_s / 1e9
+    tf = flops / comb_s / 1e12
+    return {"kernel": "combine_action_kernel", "ms": comb_s * 1e3, "achieved_GBps": gbs,
+            "peak_GBps": peak, "frac": gbs / peak, "nominal_peak_GBps": 8000.0,
+            "dmma_TFLOPs": tf, "dmma_peak_TFLOPs": DMMA_PEAK_TFLOPS,
+            "dmma_frac": tf / DMMA_PEAK_TFLOPS}
+
+
 def ncu_traffic(config):
     """Measured DRAM traffic of the roofline kernel (profiles/ncu_traffic.json)."""
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -308,7 +324,7 @@ def run_ours(args):
     launches0 = ctx.launch_count
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    solve_s, iters = [], []
+    solve_s, iters, comb_s = [], [], []
     with ClockSampler(local) as clk:
         barrier()
         for i in range(args.steps):
@@ -317,6 +333,7 @@ def run_ours(args):
             _, _, _, rep, tim = step()
             evs[i][1].record(stream)
             solve_s.append(tim.basis_solve_s)
+            comb_s.append(tim.combine_action_s)
             iters.append(rep.iterations)
             if not rep.all_converged():
                 raise SystemExit(f"basis solve did not converge: {rep}")
@@ -409,6 +426,7 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": int(mean_iters * bytes_per_iter),
                      "iterations_per_solve": mean_iters,
                      "solve_ms": float(np.mean(solve_s)) * 1e3, "peak_source": peak_kind},
+        "action": action_roofline(n, s, N, float(np.mean(comb_s)), peak),
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -599,6 +617,7 @@ def run_ours_large(args, ctx, world, rank, local):
                      "iterations_per_solve": float(np.mean(iters)),
                      "solve_ms": float(np.mean(solve)) * 1e3,
                      "combine_action_ms": float(np.mean(act)) * 1e3, "peak_source": peak_kind},
+        "action": action_roofline(n, s, N // world, float(np.mean(act)), peak),
         "timing": "per-step wall clock (synchronous C-ABI calls), max over ranks",
         "gpu_launches": int(ctx.launch_count - launches0), "clocks": clk.summary(),
     }
