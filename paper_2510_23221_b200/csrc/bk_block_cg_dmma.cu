@@ -137,11 +137,8 @@ struct Coef {
     bool hxm, hxp, hym, hyp, hzm, hzp;
 };
 
-__device__ __forceinline__ void load_coef(const Args& a, int64_t c, Coef& k) {
-    const int ci = (int)c;
-    const int ix = ci % a.nx;
-    const int iy = (ci / a.nx) % a.ny;
-    const int iz = ci / (a.nx * a.ny);
+__device__ __forceinline__ void load_coef_at(const Args& a, int64_t c, int ix, int iy, int iz,
+                                             Coef& k) {
     const int64_t plane = (int64_t)a.nx * a.ny;
     k.hzm = iz > 0;
     k.hym = iy > 0;
@@ -159,6 +156,32 @@ __device__ __forceinline__ void load_coef(const Args& a, int64_t c, Coef& k) {
     k.ozm = plane;
     k.oym = a.nx;
 }
+
+__device__ __forceinline__ void load_coef(const Args& a, int64_t c, Coef& k) {
+    const int ci = (int)c;
+    load_coef_at(a, c, ci % a.nx, (ci / a.nx) % a.ny, ci / (a.nx * a.ny), k);
+}
+
+// grid coordinates of cell c, then stepped by `d` cells (no division per step)
+struct CellXYZ {
+    int ix, iy, iz;
+    __device__ __forceinline__ void set(const Args& a, int64_t c) {
+        const int ci = (int)c;
+        ix = ci % a.nx;
+        iy = (ci / a.nx) % a.ny;
+        iz = ci / (a.nx * a.ny);
+    }
+    __device__ __forceinline__ void step(const Args& a, int d) {
+        ix += d;
+        while (ix >= a.nx) {
+            ix -= a.nx;
+            if (++iy == a.ny) {
+                iy = 0;
+                ++iz;
+            }
+        }
+    }
+};
 
 // CSR-order FMA chain (apply_block_fixed, discretize.cpp:57-71)
 template <int S>
@@ -343,14 +366,17 @@ __device__ __forceinline__ void phase_spmm_gram(const Args& a, int64_t c0, int64
     const int g = lane >> 2, t = lane & 3;
     const int64_t plane = (int64_t)a.nx * a.ny;
     for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
+        CellXYZ xyz;
+        xyz.set(a, base + q);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int lr = q + CPI * u;  // row of the tile
             const int64_t cell = base + lr;
+            if (u > 0) xyz.step(a, CPI);
             double2 acc = make_double2(0.0, 0.0), ctr = make_double2(0.0, 0.0);
             if (cell < c1) {
                 Coef k;
-                load_coef(a, cell, k);
+                load_coef_at(a, cell, xyz.ix, xyz.iy, xyz.iz, k);
                 auto row = [&](int64_t c, double coef, bool has) {
                     if (!has) return;
                     const double2 x = *reinterpret_cast<const double2*>(a.P + c * S + col);
