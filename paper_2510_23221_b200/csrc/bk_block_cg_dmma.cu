@@ -219,6 +219,12 @@ __device__ __forceinline__ double st_muladd(const Coef& k, const double* __restr
 // ---------------------------------------------------------------------------
 // reductions
 // ---------------------------------------------------------------------------
+// Only the upper triangle of a Gram matrix is ever read (the s x s solves read
+// M[min(a,b)][max(a,b)]; the reference also computes the upper part and
+// mirrors it, solvers.cpp:336-341), so 16x8 output tiles entirely below the
+// diagonal are skipped (their accumulators stay zero).
+__host__ __device__ constexpr bool gram_tile_needed(int m, int n) { return 8 * n + 7 >= 16 * m; }
+
 // Gram accumulator in DMMA D-fragment layout: tile (mt, nt) holds
 // G[16mt+g][8nt+2t+{0,1}] and G[16mt+g+8][8nt+2t+{0,1}].
 template <int S>
@@ -408,7 +414,7 @@ __device__ __forceinline__ void phase_spmm_gram(const Args& a, int64_t c0, int64
                 const double a1 = (16 * m + 8 + g < S) ? tp[c4 * RS + 16 * m + 8 + g] : 0.0;
 #pragma unroll
                 for (int n = 0; n < GramAcc<S>::NT; ++n)
-                    dmma(G.d[m][n], a0, a1, tw[c4 * RS + 8 * n + g]);
+                    if (gram_tile_needed(m, n)) dmma(G.d[m][n], a0, a1, tw[c4 * RS + 8 * n + g]);
             }
         }
         __syncwarp();
@@ -526,7 +532,7 @@ __device__ __forceinline__ void tile_gram(double* tr, double* tz, const double (
             const double a1 = (16 * m + 8 + g < S) ? tr[cell * RS + 16 * m + 8 + g] : 0.0;
 #pragma unroll
             for (int n = 0; n < GramAcc<S>::NT; ++n)
-                dmma(G.d[m][n], a0, a1, tz[cell * RS + 8 * n + g]);
+                if (gram_tile_needed(m, n)) dmma(G.d[m][n], a0, a1, tz[cell * RS + 8 * n + g]);
         }
     }
     __syncwarp();

@@ -233,6 +233,7 @@ struct OwnedGram {
                 const int tile = warp + LNW * i;
                 if (tile >= G_::GT) break;
                 const int m = tile / G_::NT, n = tile % G_::NT;
+                if (8 * n + 7 < 16 * m) continue;  // below the diagonal: never read
                 const double a0 = U[c4 * RS + 16 * m + g];
                 const double a1 = (16 * m + 8 + g < S) ? U[c4 * RS + 16 * m + 8 + g] : 0.0;
                 dmma_l(d[i], a0, a1, V[c4 * RS + 8 * n + g]);
