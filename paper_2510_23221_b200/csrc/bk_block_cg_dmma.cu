@@ -95,6 +95,7 @@ template <int S>
 struct ResStore<S, true> {
     alignas(16) double x[kResCells * S];
     alignas(16) double r[kResCells * S];
+    double dinv[kResCells];  // D^-1 of the CTA's cells (1.0 without Jacobi)
 };
 
 template <int S>
@@ -639,6 +640,18 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
     }
     const TileVec<S, RES> Xv{a.X, xres, c0, c1};
     const TileVec<S, RES> Rv{a.R, rres, c0, c1};
+    if constexpr (RES) {
+        for (int64_t c = c0 + tid; c < c1; c += BS) sm.res.dinv[c - c0] = jac ? a.dinv[c] : 1.0;
+        __syncthreads();
+    }
+    // D^-1 of cell c (1.0 past c1 or without Jacobi): shared-memory resident
+    // copy in resident mode
+    auto dinv_of = [&](int64_t c) -> double {
+        if constexpr (RES)
+            return c < c1 ? sm.res.dinv[c - c0] : 1.0;
+        else
+            return dinv_at(a, c, c1, jac);
+    };
     // resident X -> HBM (for the stencil sweeps over X and for the output)
     auto publish_x = [&]() {
         if constexpr (RES) {
@@ -662,7 +675,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
             double r[NT][4], z[NT][4], zero[NT][4];
             load_ctile<S>(a.B, base, c1, g, t, r);
-            const double d0 = dinv_at(a, base + g, c1, jac), d1 = dinv_at(a, base + g + 8, c1, jac);
+            const double d0 = dinv_of(base + g), d1 = dinv_of(base + g + 8);
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
                 z[n][0] = d0 * r[n][0];
@@ -735,7 +748,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
                 }
             Xv.store(base, g, t, x);
             Rv.store(base, g, t, r);
-            const double d0 = dinv_at(a, base + g, c1, jac), d1 = dinv_at(a, base + g + 8, c1, jac);
+            const double d0 = dinv_of(base + g), d1 = dinv_of(base + g + 8);
             double z[NT][4];
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
@@ -820,7 +833,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
                     const bool v = cell < c1;
                     Coef k;
                     if (v) load_coef(a, cell, k);
-                    const double di = dinv_at(a, cell, c1, jac);
+                    const double di = dinv_of(cell);
 #pragma unroll
                     for (int n = 0; n < NT; ++n)
 #pragma unroll
@@ -856,7 +869,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
             __syncwarp();
             afrag_smem<S>(tr, g, t, pa, 1.0);
             __syncwarp();
-            const double d0 = dinv_at(a, base + g, c1, jac), d1 = dinv_at(a, base + g + 8, c1, jac);
+            const double d0 = dinv_of(base + g), d1 = dinv_of(base + g + 8);
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
                 p[n][0] *= d0;
