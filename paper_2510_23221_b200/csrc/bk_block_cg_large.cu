@@ -672,13 +672,17 @@ __global__ void __launch_bounds__(LBS) k_true_res(SweepArgs a) {
     }
 }
 
-// fixed-order reduction over CTAs: out[e] = sum_b part[b][e]
+// fixed-order reduction over CTAs: out[e] = sum_b part[b][e]; one warp per
+// element (lane-strided partial sums, then a fixed shuffle tree)
 __global__ void k_reduce(const double* __restrict__ part, int nb, int E, double* __restrict__ out) {
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int b = 0; b < nb; ++b) s += part[(int64_t)b * E + e];
-        out[e] = s;
-    }
+    const int lane = threadIdx.x & 31;
+    const int e = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (e >= E) return;
+    double s = 0.0;
+    for (int b = lane; b < nb; b += 32) s += part[(int64_t)b * E + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[e] = s;
 }
 
 // global [n][S] <-> slab-local layout (interior rows), ghost rows zeroed on pack
@@ -945,7 +949,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     cudaStream_t s = ctx->stream;
     (void)pHost;
     auto reduce = [&](int e_count, int nparts) {
-        k_reduce<<<(e_count + 255) / 256, 256, 0, s>>>(a.part, nparts, e_count, red);
+        k_reduce<<<(e_count + 7) / 8, 256, 0, s>>>(a.part, nparts, e_count, red);
         ++ctx->launches;
         if (comm && comm->allreduce) comm->allreduce(comm->user, red, e_count, s);
     };
@@ -1126,7 +1130,7 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
         return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     };
     auto reduce = [&](int e_count, int nparts) {
-        k_reduce<<<(e_count + 255) / 256, 256, 0, s>>>(b->part, nparts, e_count, b->red);
+        k_reduce<<<(e_count + 7) / 8, 256, 0, s>>>(b->part, nparts, e_count, b->red);
         ++ctx->launches;
     };
     const int tr_blocks = (int)((sl.n_int + (LBS / S) - 1) / (LBS / S) < 4L * ctx->num_sms
