@@ -18,6 +18,9 @@
 // scalar CsrMatrix::apply order (separate multiply and add, CSR column order);
 // q = (y - g) / V is correctly rounded. So given the same X, T and q equal the
 // reference's bit for bit (tests/test_gpu_parity.py checks it).
+#include <cstdio>
+#include <cstdlib>
+
 #include "bk_common.cuh"
 
 namespace {
@@ -60,7 +63,14 @@ __device__ __forceinline__ void dmma_c(double (&d)[4], double a0, double a1, dou
         : "d"(a0), "d"(a1), "d"(b));
 }
 
-constexpr int CSTRIDE(int NS) { return NS + 4; }  // conflict-free B-fragment rows
+// B-fragment rows of C in shared memory: at most two lanes per 8-byte bank slot
+constexpr int CSTRIDE(int NS) { return NS == 8 ? 8 : NS + 4; }
+
+// debug: stage timestamps of CTA (0, 0) when BK_COMB_PROFILE is set
+__device__ long long g_comb_prof[64];
+__device__ __forceinline__ void comb_mark(int k) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && k < 64) g_comb_prof[k] = clock64();
+}
 
 // T for one z-plane of the tile + halo into buf[q * HC + h] (sample-major, so
 // the stencil's neighbour reads are bank-conflict free), on FP64 tensor cores:
@@ -115,7 +125,7 @@ __device__ __forceinline__ void form_plane(const ActArgs& a, int x0, int y0, int
 }
 
 template <int S, int NS>
-__global__ void __launch_bounds__(NT, 2) combine_action_kernel(ActArgs a) {
+__global__ void __launch_bounds__(NT, NS == 8 ? 3 : 2) combine_action_kernel(ActArgs a) {
     extern __shared__ __align__(16) double sm[];
     double* Cs = sm;                             // S x (NS + 4)
     double* ring = sm + S * CSTRIDE(NS);         // min(nz,3) x NS x HC
@@ -130,6 +140,7 @@ __global__ void __launch_bounds__(NT, 2) combine_action_kernel(ActArgs a) {
     const int tid = threadIdx.x;
     const int64_t plane = (int64_t)a.nx * a.ny;
 
+    comb_mark(0);
     for (int e = tid; e < S * NS; e += NT) {
         const int k = e / NS, q = e % NS;
         Cs[k * CSTRIDE(NS) + q] = (k < a.s && j0 + q < a.N) ? a.C[(int64_t)k * a.ldc + j0 + q] : 0.0;
@@ -144,9 +155,11 @@ __global__ void __launch_bounds__(NT, 2) combine_action_kernel(ActArgs a) {
 #pragma unroll
     for (int q = 0; q < NS; ++q) num[q] = den[q] = 0.0;
 
+    comb_mark(1);
     form_plane<S, NS>(a, x0, y0, 0, Cs, ring);
     if (a.nz > 1) form_plane<S, NS>(a, x0, y0, 1, Cs, ring + HC * NS);
     __syncthreads();
+    comb_mark(2);
     for (int z = 0; z < a.nz; ++z) {
         const double* Tm = ring + ((z + nring - 1) % nring) * HC * NS;
         const double* T0 = ring + (z % nring) * HC * NS;
@@ -187,43 +200,48 @@ __global__ void __launch_bounds__(NT, 2) combine_action_kernel(ActArgs a) {
             }
         }
         __syncthreads();
+        comb_mark(3 + 2 * z);
         if (z + 2 < a.nz) {
             form_plane<S, NS>(a, x0, y0, z + 2, Cs, ring + ((z + 2) % 3) * HC * NS);
             __syncthreads();
         }
+        comb_mark(4 + 2 * z);
     }
 
     if (a.part) {
         // CTA reduction of the residual partials, fixed order. Warp level: a
-        // transpose-reduce of the 2 NS = 32 per-lane sums (31 shuffles; lane L
-        // ends with sum L: num of sample L for L < NS, den of sample L - NS
-        // otherwise); then warps in index order. Reuses the ring buffer.
-        static_assert(2 * NS == 32, "one sum per lane after the transpose-reduce");
+        // transpose-reduce of the V = 2 NS per-lane sums (V - 1 shuffles, plus
+        // one when V = 16); lane L ends with sum L / (32 / V): num of sample k
+        // for k < NS, den of sample k - NS otherwise. Then warps in index order.
+        // Reuses the ring buffer.
+        constexpr int V = 2 * NS;
+        static_assert(V == 16 || V == 32, "NS = 8 or 16");
         const int lane = tid & 31, warp = tid >> 5;
-        double* red = ring;  // 8 warps x 32
-        double v[32];
+        double* red = ring;  // 8 warps x V
+        double v[V];
 #pragma unroll
         for (int q = 0; q < NS; ++q) {
             v[q] = num[q];
             v[NS + q] = den[q];
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = 16, len = V; o >= 32 / V; o >>= 1, len >>= 1) {
             const bool up = (lane & o) != 0;
 #pragma unroll
-            for (int i = 0; i < o; ++i) {
-                const double keep = up ? v[o + i] : v[i];
-                const double send = up ? v[i] : v[o + i];
+            for (int i = 0; i < len / 2; ++i) {
+                const double keep = up ? v[len / 2 + i] : v[i];
+                const double send = up ? v[i] : v[len / 2 + i];
                 v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
             }
         }
-        red[warp * 32 + lane] = v[0];
+        if (V == 16) v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        if (lane % (32 / V) == 0) red[warp * V + lane / (32 / V)] = v[0];
         __syncthreads();
         if (tid < NS && j0 + tid < a.N) {
             double u = 0.0, w = 0.0;
             for (int k = 0; k < NT / 32; ++k) {
-                u += red[k * 32 + tid];
-                w += red[k * 32 + NS + tid];
+                u += red[k * V + tid];
+                w += red[k * V + NS + tid];
             }
             double* pp = a.part + ((j0 + tid) * (int64_t)a.tiles + tile) * 2;
             *reinterpret_cast<double2*>(pp) = make_double2(u, w);
@@ -296,6 +314,17 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
     kern<<<dim3((unsigned)chunks, (unsigned)tiles), NT, smem, ctx->stream>>>(a);
     ++ctx->launches;
     BK_CUDA_TRY(ctx, cudaGetLastError());
+    if (getenv("BK_COMB_PROFILE")) {
+        long long h[64];
+        cudaStreamSynchronize(ctx->stream);
+        cudaMemcpyFromSymbol(h, g_comb_prof, sizeof(h));
+        fprintf(stderr, "[bk_comb_profile S=%d nz=%d] cycles: C load %lld, first planes %lld;", S,
+                op->nz, h[1] - h[0], h[2] - h[1]);
+        for (int z = 0; z < op->nz && 4 + 2 * z < 64; ++z)
+            fprintf(stderr, " z%d stencil %lld form %lld;", z, h[3 + 2 * z] - (z ? h[2 + 2 * z] : h[2]),
+                    h[4 + 2 * z] - h[3 + 2 * z]);
+        fprintf(stderr, "\n");
+    }
     if (resid) {
         resid_finalize<<<(unsigned)((N + 7) / 8), 256, 0, ctx->stream>>>(a.part, tiles, N, resid);
         ++ctx->launches;
@@ -316,10 +345,16 @@ bk_status combine_action_device(bk_ctx* ctx, const bk_operator* op, const double
     if (N == 0) return BK_OK;
     if (s < 1 || s > S || ldc < N) return fail(ctx, BK_INTERNAL, "combine_action: bad widths");
     switch (S) {
-        case 8: return run<8, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid);
-        case 16: return run<16, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid);
-        case 32: return run<32, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid);
-        case 64: return run<64, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+        // 16 samples per CTA for a single plane; 8 for 3D grids, whose
+        // 3-plane T ring then fits 3 CTAs per SM
+        case 8: return op->nz == 1 ? run<8, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid)
+                                   : run<8, 8>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+        case 16: return op->nz == 1 ? run<16, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid)
+                                    : run<16, 8>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+        case 32: return op->nz == 1 ? run<32, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid)
+                                    : run<32, 8>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+        case 64: return op->nz == 1 ? run<64, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid)
+                                    : run<64, 8>(ctx, op, X, s, C, ldc, N, T, Q, resid);
         default: return fail(ctx, BK_INTERNAL, "combine_action: unpadded width");
     }
 }
