@@ -41,6 +41,7 @@ WORKLOADS = {
 }
 C4_CHIPS_PER_STEP = 16   # chips per GPU per timed step (5000 chips total at full scale)
 C4_MAX_ITER = 5000
+C4_STREAMS = 8            # chips per batched solve (one cooperative launch, 1/8 of the SMs each)
 # Tolerance pins: 1e-12 for configs 1-3; configs 4-5 use 1e-10
 # because their true relative residual plateaus at ~1.1-2e-12 in fp64 (measured:
 # C5 512x512x16 at 1.1e-12..2.0e-12 after 1200 iterations; C4 chip 4 at 1.28e-12
@@ -73,6 +74,8 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        if os.environ.get("BK_BENCH_NO_CLOCKS"):
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -219,7 +222,7 @@ def run_reference_arm(args):
         "ms_per_step": float(np.mean(wall_s)) * 1e3,
         "extrapolated_ms_per_full_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-        "config": config_dict(args.config, world),
+        "config": config_dict(args.config, world, chips_per_step(args)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -253,17 +256,29 @@ def ncu_traffic(config):
         return json.load(f).get(f"config{config}")
 
 
-def config_dict(config, world):
+CHIPS_BY_CONFIG = {1: 8, 2: 8, 3: 4}  # independent chips per GPU per step, solved together
+
+
+def chips_per_step(args):
+    if args.config not in CHIPS_BY_CONFIG:
+        return 1
+    return args.chips if args.chips else CHIPS_BY_CONFIG[args.config]
+
+
+def config_dict(config, world, chips=1):
     import paper_2510_23221_b200 as bk
 
     cid, nx, ny, nz, s, N = bk.CONFIGS[config]
     d = {"workload": WORKLOADS[config], "grid": [nx, ny, nz], "s": s, "samples_per_chip": N,
-         "chips_per_step_per_gpu": 1, "tol": TOL_BY_CONFIG[config], "precond": "jacobi",
-         "parallelism": f"chip-sharded x{world} (no collective)",
+         "chips_per_step_per_gpu": chips, "tol": TOL_BY_CONFIG[config], "precond": "jacobi",
+         "parallelism": f"chip-sharded x{world} (no collective)"
+                        + (f", {chips} independent chips per GPU per step, z-stacked and solved "
+                           f"by one cooperative launch ({chips} SM shares)" if chips > 1 else ""),
          "l2": "flushed between timed steps (512 MiB write)"}
     if config == 4:
         d["chips_per_step_per_gpu"] = C4_CHIPS_PER_STEP
         d["max_iter"] = C4_MAX_ITER
+        d["concurrent_chips"] = C4_STREAMS
         d["note"] = "chips whose basis solve misses the tolerance are dropped and counted"
     if config == 5:
         d["output_ring_samples"] = C5_RING
@@ -347,14 +362,66 @@ def run_ours(args):
         t = torch.tensor([total_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_s = float(t.item())
-    value = N * args.steps * world / total_s
+    single_value = N * args.steps * world / total_s
+
+    # ---- value: K independent chips per GPU per step (chip ids rank K + c)
+    # through bk_generate_batch(streams=K): the chips are z-stacked and their
+    # basis blocks solved by one cooperative launch, each chip on 1/K of the
+    # SMs (one chip's solve is latency-bound, so K of them share the GPU).
+    # Device-resident inputs and outputs, CUDA events around the synchronous
+    # call, L2 flushed before every step, max over ranks.
+    from types import SimpleNamespace
+    K = chips_per_step(args)
+    if K > 1:
+        to_dev = lambda a: torch.from_numpy(a).to(dev)  # noqa: E731
+        chips_d = []
+        for c in range(K):
+            ic = bk.synth_chip(cid, nx, ny, nz, s, N, chip_id=rank * K + c)
+            chips_d.append(SimpleNamespace(grid=ic.grid, bc=ic.bc, k=to_dev(ic.k),
+                                           q_basis=to_dev(ic.q_basis), coef=to_dev(ic.coef)))
+        Tk = [torch.empty((N, n), dtype=torch.float64, device=dev) for _ in range(K)]
+        Qk = [torch.empty((N, n), dtype=torch.float64, device=dev) for _ in range(K)]
+        Rk = [torch.empty(N, dtype=torch.float64, device=dev) for _ in range(K)]
+
+        def bstep():
+            return bk.generate_batch(chips_d, cfg, t_out=Tk, q_out=Qk, resid_out=Rk, streams=K,
+                                     ctx=ctx)
+
+        for _ in range(args.warmup):
+            bstep()
+        barrier()
+        launches0 = ctx.launch_count
+        bevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(args.steps)]
+        with ClockSampler(local) as clk:
+            barrier()
+            for i in range(args.steps):
+                flush.fill_(float(i))
+                bevs[i][0].record(stream)
+                _, _, _, breps, _ = bstep()
+                bevs[i][1].record(stream)
+                if not all(r.all_converged() for r in breps):
+                    raise SystemExit("basis solve did not converge (concurrent chips)")
+            barrier()
+        launches = ctx.launch_count - launches0
+        bstep_ms = [a.elapsed_time(b) for a, b in bevs]
+        btotal_s = sum(bstep_ms) * 1e-3
+        max_resid = max(max_resid, max(float(r.max().item()) for r in Rk))
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([btotal_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            btotal_s = float(t.item())
+        value = K * N * args.steps * world / btotal_s
+        del Tk, Qk, Rk
+    else:
+        value, bstep_ms = single_value, step_ms
 
     # ---- e2e: the same pipeline through the public C ABI with pinned HOST
     # buffers: one bk_generate_batch call over e2e_steps chips (a generation
     # job's call); every chip stages its inputs H2D and drains (T, q, resid)
     # D2H inside the timed region. The batch drains chip c while chip c+1
     # computes, so the PCIe drain (2.1 GB per C2 chip) overlaps the solve.
-    from types import SimpleNamespace
     k_h = torch.from_numpy(inp.k).pin_memory()
     q_h = torch.from_numpy(inp.q_basis).pin_memory()
     c_h = torch.from_numpy(inp.coef).pin_memory()
@@ -364,7 +431,8 @@ def run_ours(args):
     T_h = [torch.empty((N, n), dtype=torch.float64).pin_memory() for _ in range(e2e_steps)]
     Q_h = [torch.empty((N, n), dtype=torch.float64).pin_memory() for _ in range(e2e_steps)]
     R_h = [torch.empty(N, dtype=torch.float64).pin_memory() for _ in range(e2e_steps)]
-    bk.generate_batch(chips_h[:1], cfg, t_out=T_h[:1], q_out=Q_h[:1], resid_out=R_h[:1],
+    # warm-up over two chips: both output parities' workspaces exist before timing
+    bk.generate_batch(chips_h[:2], cfg, t_out=T_h[:2], q_out=Q_h[:2], resid_out=R_h[:2],
                       streams=1, ctx=ctx)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -409,10 +477,12 @@ def run_ours(args):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": float(np.mean(step_ms)), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": float(np.mean(bstep_ms)), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE-config generators, DESIGN.md §Inputs)",
-        "config": config_dict(args.config, world),
+        "config": config_dict(args.config, world, K),
+        "single_chip": {"value": single_value, "unit": UNIT, "ms_per_chip": float(np.mean(step_ms)),
+                        "note": "one chip per step on the whole GPU (latency view)"},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": int((n + n * s + s * N) * 8),
                 "d2h_bytes_per_step": int((2 * n * N + N) * 8),
@@ -451,7 +521,8 @@ def _finish(args, world, rank, line):
 
 def run_ours_batch(args, ctx, world, rank, local):
     """Config 4: a step = C4_CHIPS_PER_STEP distinct chips per GPU (chip ids
-    offset by rank), solved back to back through bk_generate_batch."""
+    offset by rank), solved through bk_generate_batch, C4_STREAMS chips at a time
+    on equal SM shares."""
     import torch
 
     import paper_2510_23221_b200 as bk
@@ -481,7 +552,8 @@ def run_ours_batch(args, ctx, world, rank, local):
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step():
-        return bk.generate_batch(dchips, cfg, T, Q, R, streams=1, ctx=ctx, check_converged=False)
+        return bk.generate_batch(dchips, cfg, T, Q, R, streams=C4_STREAMS, ctx=ctx,
+                                 check_converged=False)
 
     for _ in range(args.warmup):
         step()
@@ -631,6 +703,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--chips", type=int, default=0,
+                    help="concurrent chips per GPU per step (configs 1-3; 0 = default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-iter-cap", type=int, default=24)
     ap.add_argument("--ref-action-samples", type=int, default=64)

@@ -187,12 +187,18 @@ bk_status bk_generate_chip(bk_ctx* ctx, const bk_grid* grid, const double* k,
                            double* T, double* Q, double* resid, bk_solve_report* report,
                            bk_phase_timings* timings);
 
-/* Batched per-chip pipeline for many independent chips (BASELINE config 4):
- * chip c runs bk_generate_chip on its own inputs. `streams` chips are in flight
- * at once, each on its own stream, workspace and 1/streams of the SMs, so the
- * latency-bound solves of different chips overlap. Per-chip arrays of
- * pointers (host or device); T/Q/resid entries may be NULL. reports may be NULL
- * (else n_chips entries whose residual arrays hold s values each). */
+/* Batched per-chip pipeline for many independent chips (BASELINE config 4;
+ * also configs 1-3 run as multi-chip jobs): the per-chip loop of
+ * generate_blockoa (pipeline.cpp:365-597). streams = 1: chips one after another
+ * (host output buffers drain chip c over PCIe while chip c+1 computes).
+ * streams = K > 1 with chips of identical dims, s <= 32 and device outputs:
+ * groups of K chips are z-stacked (block-diagonal system) and their basis
+ * blocks solved by ONE cooperative launch, chip k on 1/K of the SMs, so the
+ * latency-bound solves overlap; each chip's results are bitwise those of
+ * bk_generate_chip with a 1/K SM budget (bk_set_cg_sm_budget). Other cases
+ * fall back to streams = 1. Per-chip arrays of pointers (host or device);
+ * T/Q/resid entries may be NULL. reports may be NULL (else n_chips entries
+ * whose residual arrays hold s values each). */
 bk_status bk_generate_batch(bk_ctx* ctx, int n_chips, const bk_grid* grids,
                             const double* const* k, const bk_face* bc /* n_chips x 6 */,
                             const double* const* Qbasis, int s, const double* const* C,

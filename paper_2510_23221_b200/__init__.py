@@ -593,10 +593,12 @@ def generate_chip(grid: GridSpec, k, bc: BoundarySpec, q_basis, coef, cfg: Solve
 
 def generate_batch(chips, cfg: SolverConfig, t_out=None, q_out=None, resid_out=None,
                    streams: int = 8, ctx: Optional[Context] = None, check_converged: bool = True):
-    """Batched per-chip pipeline (BASELINE config 4): `chips` is a list of
-    ChipInputs (or dicts with grid, bc, k, q_basis, coef) sharing s and N.
-    `streams` chips are solved concurrently, each on 1/streams of the SMs.
-    Returns (T list, Q list, resid list, [SolveReport], PhaseTimings)."""
+    """Batched per-chip pipeline (bk_generate_batch): `chips` is a list of
+    ChipInputs (or objects with grid, bc, k, q_basis, coef) sharing s and N.
+    streams = K > 1 with identical dims and device outputs: groups of K chips
+    are solved by one cooperative launch (chip k on 1/K of the SMs); otherwise
+    chips run one after another. Returns (T list, Q list, resid list,
+    [SolveReport], PhaseTimings)."""
     ctx = _ctx(ctx)
     n = len(chips)
     if n == 0:

@@ -4,9 +4,12 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <chrono>
 #include <new>
+#include <map>
+#include <mutex>
 #include <thread>
 #include <string>
 #include <vector>
@@ -54,6 +57,19 @@ bk_status read_small(bk_ctx* ctx, void* host_dst, const void* dev_src, size_t by
     BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     std::memcpy(host_dst, ctx->hmap, bytes);
     return BK_OK;
+}
+
+cudaError_t set_max_smem(const void* f, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> given;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& g = given[{dev, f}];
+    if (bytes <= g) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) g = bytes;
+    return e;
 }
 
 bool is_device_ptr(const void* p) {
@@ -371,6 +387,108 @@ bk_status generate_chip_impl(bk_ctx* ctx, const bk_grid* grid, const double* k,
     return BK_OK;
 }
 
+// Batched pipeline of bk_generate_batch (streams = K > 1): groups of K chips
+// of identical dims are assembled into slices of one z-stacked operator (the
+// chips' block-diagonal system; boundary face conductances are 0, so no
+// coupling), their basis blocks solved by ONE cooperative launch in which
+// each chip owns 1/K of the SMs (block_cg_device_multi), then combined per
+// chip — all on the context's stream. Persistent solves of several chips thus
+// overlap without concurrent cooperative launches (which can starve a
+// partially resident grid behind other streams' kernels).
+bk_status generate_fused(bk_ctx* ctx, int n_chips, const bk_grid* grids, const double* const* k,
+                         const bk_face* bc, const double* const* Qbasis, int s,
+                         const double* const* C, int64_t N, const bk_solver_cfg* cfg,
+                         double* const* T, double* const* Q, double* const* resid,
+                         bk_solve_report* reports, int K, bk_phase_timings* timings) {
+    bk_status st = validate_cfg(ctx, cfg);
+    if (st != BK_OK) return st;
+    if (N < 0) return fail(ctx, BK_INVALID_CONFIG, "generate: n_data must be >= 0");
+    const bk_grid& g0 = grids[0];
+    const int64_t n = (int64_t)g0.nx * g0.ny * g0.nz;
+    const int S = kernel_width(s);
+    void *pStack, *pb, *px, *pc;
+    if ((st = workspace(ctx, kSlotStackDiag, (size_t)6 * K * n * sizeof(double), &pStack)) != BK_OK)
+        return st;
+    if ((st = workspace(ctx, kSlotIn2, (size_t)K * n * S * sizeof(double), &pb)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotOut2, (size_t)K * n * S * sizeof(double), &px)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotStackCoef, (size_t)K * s * N * sizeof(double) + 8, &pc)) != BK_OK)
+        return st;
+    double* const base = (double*)pStack;
+    while ((int)ctx->views.size() < K) ctx->views.push_back(new bk_operator);
+    cudaEvent_t* ev = ctx->ev;
+    float t_asm = 0.f, t_solve = 0.f, t_comb = 0.f;
+    int64_t iters = 0, matvecs = 0;
+    bool all_conv = true;
+    std::vector<CgReport> reps(K);
+    for (int c0 = 0; c0 < n_chips; c0 += K) {
+        const int Kg = std::min(K, n_chips - c0);
+        BK_CUDA_TRY(ctx, cudaEventRecord(ev[0], ctx->stream));
+        const double* cdev[64];
+        for (int j = 0; j < Kg; ++j) {
+            const int c = c0 + j;
+            bk_operator* v = ctx->views[j];
+            double* arr[6];
+            for (int q = 0; q < 6; ++q) arr[q] = base + ((int64_t)q * K + j) * n;
+            v->diag = arr[0];
+            v->cx = arr[1];
+            v->cy = arr[2];
+            v->cz = arr[3];
+            v->g = arr[4];
+            v->dinv = arr[5];
+            v->n = n;  // assemble_into fills the slices in place
+            if ((st = assemble_into(ctx, &grids[c], k[c], bc + 6 * c, v)) != BK_OK) return st;
+            Staged qd;
+            if ((st = stage_in(ctx, kSlotQ, Qbasis[c], (size_t)n * s, &qd)) != BK_OK) return st;
+            BK_CUDA_TRY(ctx, launch_rhs_padded(ctx, v, qd.dev, s, (double*)pb + (int64_t)j * n * S, S));
+            if (is_device_ptr(C[c])) {
+                cdev[j] = C[c];
+            } else {
+                double* dst = (double*)pc + (int64_t)j * s * N;
+                BK_CUDA_TRY(ctx, cudaMemcpyAsync(dst, C[c], (size_t)s * N * sizeof(double),
+                                                 cudaMemcpyHostToDevice, ctx->stream));
+                cdev[j] = dst;
+            }
+        }
+        BK_CUDA_TRY(ctx, cudaEventRecord(ev[1], ctx->stream));
+        bk_operator stk = *ctx->views[0];
+        stk.nz = g0.nz * Kg;
+        stk.n = n * Kg;
+        stk.volz = nullptr;
+        stk.h_volz.clear();
+        if ((st = block_cg_device_multi(ctx, &stk, Kg, (const double*)pb, S, cfg, (double*)px,
+                                        reps.data())) != BK_OK)
+            return st;
+        BK_CUDA_TRY(ctx, cudaEventRecord(ev[2], ctx->stream));
+        for (int j = 0; j < Kg; ++j) {
+            const int c = c0 + j;
+            if ((st = combine_action_device(ctx, ctx->views[j], (const double*)px + (int64_t)j * n * S,
+                                            S, s, cdev[j], N, N, T ? T[c] : nullptr,
+                                            Q ? Q[c] : nullptr, resid ? resid[c] : nullptr)) != BK_OK)
+                return st;
+            if (reports) fill_report(reps[j], s, 0.0, &reports[c]);
+            iters += reps[j].iterations;
+            matvecs += reps[j].matvecs + N;
+            for (int q = 0; q < s; ++q) all_conv = all_conv && reps[j].converged[q];
+        }
+        BK_CUDA_TRY(ctx, cudaEventRecord(ev[3], ctx->stream));
+        BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        t_asm += elapsed(ev[0], ev[1]);
+        t_solve += elapsed(ev[1], ev[2]);
+        t_comb += elapsed(ev[2], ev[3]);
+    }
+    if (timings) {
+        std::memset(timings, 0, sizeof(*timings));
+        timings->assemble_s = t_asm * 1e-3;
+        timings->basis_solve_s = t_solve * 1e-3;
+        timings->combine_action_s = t_comb * 1e-3;
+        timings->total_s = (t_asm + t_solve + t_comb) * 1e-3;
+        timings->iterations_total = iters;
+        timings->matvecs_total = matvecs;
+    }
+    if (!all_conv) return fail(ctx, BK_NOT_CONVERGED, "basis solve did not reach tolerance");
+    return BK_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -422,6 +540,10 @@ void bk_destroy(bk_ctx* ctx) {
     if (ctx->scratch) {
         free_op_buffers(ctx->scratch);
         delete ctx->scratch;
+    }
+    for (bk_operator* v : ctx->views) {  // slices of a workspace: only volz is owned
+        cudaFree(v->volz);
+        delete v;
     }
     if (ctx->hmap) cudaFreeHost(ctx->hmap);
     cudaStreamDestroy(ctx->own_stream);
@@ -759,6 +881,24 @@ bk_status bk_generate_batch(bk_ctx* ctx, int n_chips, const bk_grid* grids,
     if (streams < 1) streams = 1;
     if (streams > n_chips && n_chips > 0) streams = n_chips;
     cudaSetDevice(ctx->device);
+    // streams > 1: the batched pipeline (one cooperative launch per group of
+    // chips) when the chips share dims, fit the persistent solver and write
+    // device outputs; otherwise chips run one after another
+    if (streams > 1) {
+        bool fused = streams <= 64 && s >= 1 && s <= 32;
+        const int64_t n0 = (int64_t)grids[0].nx * grids[0].ny * grids[0].nz;
+        fused = fused && n0 < ((int64_t)1 << 21) && !getenv("BK_CG_LARGE") && !getenv("BK_CG_GENERIC");
+        for (int c = 0; c < n_chips && fused; ++c) {
+            fused = grids[c].nx == grids[0].nx && grids[c].ny == grids[0].ny &&
+                    grids[c].nz == grids[0].nz;
+            for (double* const* out : {T, Q, resid})
+                if (out && out[c] && !is_device_ptr(out[c])) fused = false;
+        }
+        if (fused)
+            return generate_fused(ctx, n_chips, grids, k, bc, Qbasis, s, C, N, cfg, T, Q, resid,
+                                  reports, streams, timings);
+        streams = 1;
+    }
     // sub-contexts: own stream + workspace, an equal share of the SMs each
     while ((int)ctx->subs.size() < streams) {
         bk_ctx* sub = nullptr;
@@ -766,7 +906,8 @@ bk_status bk_generate_batch(bk_ctx* ctx, int n_chips, const bk_grid* grids,
         if (st != BK_OK) return fail(ctx, st, "generate_batch: sub-context");
         ctx->subs.push_back(sub);
     }
-    const int share = ctx->num_sms / streams > 0 ? ctx->num_sms / streams : 1;
+    int share = ctx->num_sms / streams > 0 ? ctx->num_sms / streams : 1;
+    if (const char* e = getenv("BK_BATCH_SHARE")) share = atoi(e);
     for (int w = 0; w < streams; ++w) ctx->subs[w]->cg_max_ctas = share;
     std::vector<bk_status> st(streams, BK_OK);
     std::vector<std::string> msg(streams);

@@ -607,8 +607,7 @@ bk_status run_block_cg(bk_ctx* ctx, const bk_operator* op, const double* B, int 
     const size_t vec_bytes = (size_t)n * S * sizeof(double);
     auto kern = block_cg_kernel<S>;
     const size_t smem = sizeof(Sm<S>);
-    BK_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
+    BK_CUDA_TRY(ctx, bk::set_max_smem((const void*)kern, smem));
     int occ = 0;
     BK_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BS, smem));
     if (occ < 1) return fail(ctx, BK_INTERNAL, "block_cg kernel cannot be resident");

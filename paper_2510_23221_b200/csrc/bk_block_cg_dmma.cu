@@ -23,6 +23,7 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "bk_common.cuh"
@@ -64,6 +65,14 @@ struct Args {
     int precond;
     bk::CgReport* rep;
     long long* prof;  // optional phase timestamps (CTA 0), PROF_ITERS x PROF_MARKS
+    // several independent chips of identical dims in one launch: chip k owns
+    // cells [k nchip, (k+1) nchip) of the z-stacked (block-diagonal) system,
+    // CTAs [k cpc, (k+1) cpc), reduction partials part + k cpc (S^2+S),
+    // results red + k (S^2+S), report rep + k and barrier bars + 2k
+    int nchips;
+    int cpc;
+    int64_t nchip;
+    unsigned* bars;
 };
 
 __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b) {
@@ -296,13 +305,48 @@ __device__ __forceinline__ void cta_sum_vec(double (&v)[S / 8][2], double* scrat
     __syncthreads();
 }
 
-template <int BS>
-__device__ void grid_reduce(cg::grid_group& grid, double* __restrict__ part,
+// Barrier over the NB CTAs of one chip's group (count, generation) — the
+// grid.sync protocol restricted to a group: the master thread reads the
+// generation, arrives, and the last arrival resets the count and bumps the
+// generation. All CTAs of the launch are co-resident (one cooperative launch).
+__device__ __forceinline__ void group_barrier(unsigned* bar, unsigned NB) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* vb = bar;
+        const unsigned gen = vb[1];
+        __threadfence();
+        if (atomicAdd(bar, 1u) == NB - 1) {
+            vb[0] = 0u;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (vb[1] == gen) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <bool MULTI>
+struct Group {
+    int chip, b, NB;
+    unsigned* bar;
+    __device__ __forceinline__ void sync(cg::grid_group& grid) const {
+        if constexpr (MULTI)
+            group_barrier(bar, (unsigned)NB);
+        else
+            grid.sync();
+    }
+};
+
+template <int BS, bool MULTI>
+__device__ void grid_reduce(const Group<MULTI>& gr, cg::grid_group& grid, double* __restrict__ part,
                             double* __restrict__ redg, const double* src, int E, double* dst) {
     constexpr int NW = BS / 32;
-    const int b = blockIdx.x, NB = gridDim.x;
+    const int b = gr.b, NB = gr.NB;
     for (int e = threadIdx.x; e < E; e += BS) part[(int64_t)b * E + e] = src[e];
-    grid.sync();
+    gr.sync(grid);
     const int e0 = (int)((int64_t)E * b / NB), e1 = (int)((int64_t)E * (b + 1) / NB);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int e = e0 + warp; e < e1; e += NW) {
@@ -312,7 +356,7 @@ __device__ void grid_reduce(cg::grid_group& grid, double* __restrict__ part,
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) __stcg(redg + e, s);
     }
-    grid.sync();
+    gr.sync(grid);
     for (int e = threadIdx.x; e < E; e += BS) dst[e] = __ldcg(redg + e);
     __syncthreads();
 }
@@ -607,7 +651,7 @@ __device__ __forceinline__ double dinv_at(const Args& a, int64_t c, int64_t c1, 
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-template <int S, bool RES>
+template <int S, bool RES, bool MULTI>
 __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args a) {
     constexpr int BS = CtaShape<S>::BS, NW = CtaShape<S>::NW;
     constexpr int NT = S / 8;
@@ -619,16 +663,34 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int NB = gridDim.x, b = blockIdx.x;
+    Group<MULTI> gr;
+    if constexpr (MULTI) {
+        gr.NB = a.cpc;
+        gr.chip = (int)blockIdx.x / gr.NB;
+        gr.b = (int)blockIdx.x % gr.NB;
+        gr.bar = a.bars + 2 * gr.chip;
+    } else {
+        gr.NB = (int)gridDim.x;
+        gr.chip = 0;
+        gr.b = (int)blockIdx.x;
+        gr.bar = nullptr;
+    }
+    const int NB = gr.NB, b = gr.b;
     constexpr bool kAlias = scratch_aliases_tiles<S>();
     double* const scr = kAlias ? &sm.tileR[0][0] : sm.scratch;
     constexpr int kScrStride = kAlias ? 16 * Strides<S>::RS : S * S;
-    // CTA ranges in whole 16-cell tiles (the last CTA takes the ragged end)
-    const int64_t ntiles = (a.n + 15) / 16;
-    const int64_t c0 = 16 * (ntiles * b / NB);
-    const int64_t c1 = b == NB - 1 ? a.n : 16 * (ntiles * (b + 1) / NB);
+    // CTA ranges in whole 16-cell tiles of this chip (the last CTA takes the
+    // ragged end); per-chip reduction buffers and report
+    const int64_t nchip = MULTI ? a.nchip : a.n;
+    const int64_t cbase = MULTI ? (int64_t)gr.chip * nchip : 0;
+    const int64_t ntiles = (nchip + 15) / 16;
+    const int64_t c0 = cbase + 16 * (ntiles * b / NB);
+    const int64_t c1 = b == NB - 1 ? cbase + nchip : cbase + 16 * (ntiles * (b + 1) / NB);
+    double* const partc = MULTI ? a.part + (int64_t)gr.chip * NB * (S * S + S) : a.part;
+    double* const redc = MULTI ? a.red + (int64_t)gr.chip * (S * S + S) : a.red;
+    bk::CgReport* const repc = MULTI ? a.rep + gr.chip : a.rep;
     const bool jac = a.precond != 0;
-    const bool prof = a.prof != nullptr && b == 0 && tid == 0;
+    const bool prof = a.prof != nullptr && gr.chip == 0 && b == 0 && tid == 0;
     double* tr = sm.tileR[warp];
     double* tz = sm.tileZ[warp];
 
@@ -660,7 +722,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
                 Xv.load(base, g, t, x);
                 store_ctile<S>(a.X, base, c1, g, t, x);
             }
-            grid.sync();
+            gr.sync(grid);
         }
     };
 
@@ -695,7 +757,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         G.spill(scr + warp * kScrStride, g, t);
         cta_sum_mat<S>(scr, kScrStride, sm.aug);
         cta_sum_vec<S>(bn, scr, kScrStride, sm.aug + S * S, warp, lane);
-        grid_reduce<BS>(grid, a.part, a.red, sm.aug, E, sm.aug + E);
+        grid_reduce<BS, MULTI>(gr, grid, partc, redc, sm.aug, E, sm.aug + E);
         for (int e = tid; e < S * S; e += BS) sm.s_old[e] = sm.aug[E + e];
         if (tid < S) {
             const double bnv = sqrt(sm.aug[E + S * S + tid]);
@@ -718,7 +780,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         G.spill(scr + warp * kScrStride, g, t);
         cta_sum_mat<S>(scr, kScrStride, sm.aug);
         if (pm) pm[1] = gtimer();
-        grid_reduce<BS>(grid, a.part, a.red, sm.aug, S * S, sm.mat);
+        grid_reduce<BS, MULTI>(gr, grid, partc, redc, sm.aug, S * S, sm.mat);
         if (pm) pm[2] = gtimer();
         matvecs += sm.sa;
         small_solve<S>(sm, sm.mat, sm.s_old, sm.coef);  // alpha
@@ -766,7 +828,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         cta_sum_mat<S>(scr, kScrStride, sm.aug);
         cta_sum_vec<S>(rr, scr, kScrStride, sm.aug + S * S, warp, lane);
         if (pm) pm[4] = gtimer();
-        grid_reduce<BS>(grid, a.part, a.red, sm.aug, E, sm.aug + E);
+        grid_reduce<BS, MULTI>(gr, grid, partc, redc, sm.aug, E, sm.aug + E);
         for (int e = tid; e < S * S; e += BS) sm.mat[e] = sm.aug[E + e];  // S_new
         if (tid < S) sm.vec[tid] = sm.aug[E + S * S + tid];              // rr
         __syncthreads();
@@ -801,7 +863,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
                 }
             }
             cta_sum_vec<S>(rs, scr, kScrStride, sm.aug, warp, lane);
-            grid_reduce<BS>(grid, a.part, a.red, sm.aug, S, sm.aug + S);
+            grid_reduce<BS, MULTI>(gr, grid, partc, redc, sm.aug, S, sm.aug + S);
             matvecs += nver;
             if (tid == 0) {
                 sm.fail = 0;
@@ -852,7 +914,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
             }
             G.spill(scr + warp * kScrStride, g, t);
             cta_sum_mat<S>(scr, kScrStride, sm.aug);
-            grid_reduce<BS>(grid, a.part, a.red, sm.aug, S * S, sm.s_old);
+            grid_reduce<BS, MULTI>(gr, grid, partc, redc, sm.aug, S * S, sm.s_old);
             matvecs += sm.sa;
             continue;
         }
@@ -882,7 +944,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
             }
             store_ctile<S>(a.P, base, c1, g, t, p);
         }
-        grid.sync();
+        gr.sync(grid);
         if (pm) pm[7] = gtimer();
     }
 
@@ -908,7 +970,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
             }
         }
         cta_sum_vec<S>(rs, scr, kScrStride, sm.aug, warp, lane);
-        grid_reduce<BS>(grid, a.part, a.red, sm.aug, S, sm.aug + S);
+        grid_reduce<BS, MULTI>(gr, grid, partc, redc, sm.aug, S, sm.aug + S);
         matvecs += sm.sa;
         if (tid < S && sm.act[tid]) {
             const double rt = sqrt(sm.aug[S + tid]) / sm.bnorm[tid];
@@ -918,11 +980,11 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         __syncthreads();
     }
     if (b == 0 && tid == 0) {
-        a.rep->iterations = iters;
-        a.rep->matvecs = matvecs;
+        repc->iterations = iters;
+        repc->matvecs = matvecs;
         for (int q = 0; q < S; ++q) {
-            a.rep->final_res[q] = sm.fres[q];
-            a.rep->converged[q] = (char)sm.conv[q];
+            repc->final_res[q] = sm.fres[q];
+            repc->converged[q] = (char)sm.conv[q];
         }
     }
 }
@@ -943,11 +1005,10 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
     // shared-memory-resident X/R when every CTA's range fits (S <= 16)
     const int64_t max_cells = 16 * ((ntiles + nb - 1) / nb);
     const bool resident = S <= 16 && max_cells <= kResCells && getenv("BK_CG_NO_RESIDENT") == nullptr;
-    const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true>
-                                : (const void*)block_cg_dmma_kernel<S, false>;
+    const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, false>
+                                : (const void*)block_cg_dmma_kernel<S, false, false>;
     const size_t smem = resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>);
-    BK_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
+    BK_CUDA_TRY(ctx, bk::set_max_smem((const void*)kern, smem));
     int occ = 0;
     BK_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BS, smem));
     if (occ < 1) return fail(ctx, BK_INTERNAL, "block_cg: DMMA kernel cannot be resident");
@@ -995,18 +1056,26 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
     a.max_iter = cfg->max_iter;
     a.precond = cfg->precond;
     a.rep = (CgReport*)pRep;
+    a.nchips = 1;
+    a.cpc = (int)nb;
+    a.nchip = n;
+    a.bars = nullptr;
     const bool want_prof = getenv("BK_CG_PROFILE") != nullptr;
     a.prof = want_prof ? (long long*)((char*)pRep + sizeof(CgReport)) : nullptr;
     if (want_prof)
         BK_CUDA_TRY(ctx, cudaMemsetAsync(a.prof, 0, PROF_ITERS * PROF_MARKS * sizeof(long long),
                                          ctx->stream));
     void* args[] = {&a};
+    const bool trace = getenv("BK_BATCH_TRACE") != nullptr;
+    if (trace) fprintf(stderr, "[trace ctx %p] launch cg nb=%lld\n", (void*)ctx, (long long)nb);
     BK_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(kern, dim3((unsigned)nb), dim3(BS), args, smem,
                                                  ctx->stream));
+    if (trace) fprintf(stderr, "[trace ctx %p] launched\n", (void*)ctx);
     ++ctx->launches;
     if (padded) BK_CUDA_TRY(ctx, launch_pad_cols(ctx, (const double*)pX, S, X, s, n));
     {
         const bk_status rs = read_small(ctx, rep, pRep, sizeof(CgReport));
+        if (trace) fprintf(stderr, "[trace ctx %p] cg done\n", (void*)ctx);
         if (rs != BK_OK) return rs;
     }
     if (want_prof) {
@@ -1039,6 +1108,86 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
 }  // namespace
 
 namespace bk {
+
+// K independent chips of identical dims, z-stacked into one block-diagonal
+// system (op: nz = K nz_chip, n = K n_chip; B, X: K n_chip x S), solved by one
+// cooperative launch in which chip k owns an equal share of the SMs.
+template <int S>
+bk_status run_dmma_multi(bk_ctx* ctx, const bk_operator* op, int K, const double* B,
+                         const bk_solver_cfg* cfg, double* X, CgReport* reps) {
+    const int64_t n = op->n, nchip = n / K;
+    constexpr int BS = CtaShape<S>::BS;
+    int cpc = ctx->num_sms / K;
+    const int64_t ntiles = (nchip + 15) / 16;
+    if ((int64_t)cpc * 2 > ntiles) cpc = (int)((ntiles + 1) / 2);
+    if (cpc < 1) return fail(ctx, BK_INVALID_CONFIG, "block_cg: too many chips for the SMs");
+    const int64_t nb = (int64_t)K * cpc;
+    const int64_t max_cells = 16 * ((ntiles + cpc - 1) / cpc);
+    const bool resident = S <= 16 && max_cells <= kResCells && getenv("BK_CG_NO_RESIDENT") == nullptr;
+    const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, true>
+                                : (const void*)block_cg_dmma_kernel<S, false, true>;
+    const size_t smem = resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>);
+    BK_CUDA_TRY(ctx, set_max_smem(kern, smem));
+    int occ = 0;
+    BK_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BS, smem));
+    if (occ < 1 || nb > (int64_t)occ * ctx->num_sms)
+        return fail(ctx, BK_INTERNAL, "block_cg: batched DMMA kernel cannot be resident");
+    constexpr int E = S * S + S;
+    const size_t vec_bytes = (size_t)n * S * sizeof(double);
+    void *pR, *pP, *pW, *pPart, *pRed, *pRep, *pBar;
+    bk_status st;
+    if ((st = workspace(ctx, kSlotCgR, vec_bytes, &pR)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotCgP, vec_bytes, &pP)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotCgW, vec_bytes, &pW)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotCgPart, (size_t)nb * E * sizeof(double), &pPart)) != BK_OK)
+        return st;
+    if ((st = workspace(ctx, kSlotCgRed, (size_t)K * E * sizeof(double), &pRed)) != BK_OK)
+        return st;
+    if ((st = workspace(ctx, kSlotCgCtl, (size_t)K * sizeof(CgReport), &pRep)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotCgBars, (size_t)2 * K * sizeof(unsigned), &pBar)) != BK_OK)
+        return st;
+    BK_CUDA_TRY(ctx, cudaMemsetAsync(pBar, 0, (size_t)2 * K * sizeof(unsigned), ctx->stream));
+    Args a;
+    a.nx = op->nx;
+    a.ny = op->ny;
+    a.nz = op->nz;
+    a.n = n;
+    a.diag = op->diag;
+    a.cx = op->cx;
+    a.cy = op->cy;
+    a.cz = op->cz;
+    a.dinv = op->dinv;
+    a.B = B;
+    a.X = X;
+    a.R = (double*)pR;
+    a.P = (double*)pP;
+    a.W = (double*)pW;
+    a.part = (double*)pPart;
+    a.red = (double*)pRed;
+    a.tol = cfg->rel_tol;
+    a.max_iter = cfg->max_iter;
+    a.precond = cfg->precond;
+    a.rep = (CgReport*)pRep;
+    a.prof = nullptr;
+    a.nchips = K;
+    a.cpc = cpc;
+    a.nchip = nchip;
+    a.bars = (unsigned*)pBar;
+    void* args[] = {&a};
+    BK_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(kern, dim3((unsigned)nb), dim3(BS), args, smem,
+                                                 ctx->stream));
+    ++ctx->launches;
+    return read_small(ctx, reps, pRep, (size_t)K * sizeof(CgReport));
+}
+
+bk_status block_cg_device_multi(bk_ctx* ctx, const bk_operator* op, int K, const double* B, int S,
+                                const bk_solver_cfg* cfg, double* X, CgReport* reps) {
+    if (K < 1 || op->n % K) return fail(ctx, BK_INTERNAL, "block_cg_multi: bad chip count");
+    if (S == 8) return run_dmma_multi<8>(ctx, op, K, B, cfg, X, reps);
+    if (S == 16) return run_dmma_multi<16>(ctx, op, K, B, cfg, X, reps);
+    if (S == 32) return run_dmma_multi<32>(ctx, op, K, B, cfg, X, reps);
+    return fail(ctx, BK_INTERNAL, "block_cg_multi: kernel width must be 8, 16 or 32");
+}
 
 bk_status block_cg_device(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
                           const bk_solver_cfg* cfg, double* X, CgReport* rep) {

@@ -978,7 +978,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     const size_t cs = sizeof(CSm<S>);
     {
         const auto set = [&](const void* f, size_t b) {
-            return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+            return bk::set_max_smem(f, b);
         };
         BK_CUDA_TRY(ctx, set((const void*)k_anchor<S, kInit>, swa));
         BK_CUDA_TRY(ctx, set((const void*)k_anchor<S, kRestart>, swa));
@@ -1127,7 +1127,7 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
                      swp = smem_pupdate<S>();
     const size_t cs = sizeof(CSm<S>);
     auto set = [&](const void* f, size_t bytes) {
-        return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        return bk::set_max_smem(f, bytes);
     };
     auto reduce = [&](int e_count, int nparts) {
         k_reduce<<<(e_count + 7) / 8, 256, 0, s>>>(b->part, nparts, e_count, b->red);

@@ -307,8 +307,7 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
     const int nring = op->nz < 3 ? op->nz : 3;
     const size_t smem = (size_t)(S * CSTRIDE(NS) + nring * HC * NS) * sizeof(double);
     auto kern = combine_action_kernel<S, NS>;
-    BK_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
+    BK_CUDA_TRY(ctx, bk::set_max_smem((const void*)kern, smem));
     const int64_t chunks = (N + NS - 1) / NS;
     if (tiles > 65535) return fail(ctx, BK_INVALID_CONFIG, "combine_action: grid too large");
     kern<<<dim3((unsigned)chunks, (unsigned)tiles), NT, smem, ctx->stream>>>(a);

@@ -33,6 +33,7 @@ struct bk_ctx {
     bk_operator* scratch = nullptr;  // operator reused by bk_generate_chip
     int cg_max_ctas = 0;             // 0 = every SM (see bk_set_cg_sm_budget)
     std::vector<bk_ctx*> subs;       // per-stream sub-contexts of bk_generate_batch
+    std::vector<bk_operator*> views; // per-chip views into the batched pipeline's stacked operator
     cudaStream_t copy_stream = nullptr;    // D2H of host outputs, overlapped with compute
     std::vector<cudaEvent_t> chunk_ev;     // per-chunk "outputs ready" events
     cudaEvent_t drain_ev[2] = {};          // copy stream done with output parity p
@@ -94,9 +95,16 @@ enum Slot : int {
     kSlotT1,        // ... and parity 1: a batch drains chip c while chip c+1 computes
     kSlotQo1,
     kSlotRes1,
+    kSlotCgBars,    // group barriers of the batched (multi-chip) solve
+    kSlotStackDiag, // z-stacked operator of the batched pipeline (6 arrays)
+    kSlotStackCoef, // per-chip combination coefficients of the batched pipeline
 };
 
 bk_status fail(bk_ctx* ctx, bk_status st, const std::string& msg);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when `f` needs more
+// than it was already given (once per function and device in steady state):
+// the attribute is not rewritten while other streams run the same kernel.
+cudaError_t set_max_smem(const void* f, size_t bytes);
 // Grow-only workspace; contents are not preserved on growth.
 bk_status workspace(bk_ctx* ctx, int slot, size_t bytes, void** out);
 bool is_device_ptr(const void* p);
@@ -142,6 +150,10 @@ bk_status block_cg_generic(bk_ctx* ctx, const bk_operator* op, const double* B, 
 
 // S = kernel width of X (n x S, zero-padded), s = real basis width (rows of
 // C read), C row stride ldc (>= N: a sample sub-range of a wider C).
+// K chips of identical dims z-stacked (op: nz = K nz_chip): one cooperative
+// launch, chip k on an equal SM share (S = 8, 16, 32). reps: K reports.
+bk_status block_cg_device_multi(bk_ctx* ctx, const bk_operator* op, int K, const double* B, int S,
+                                const bk_solver_cfg* cfg, double* X, CgReport* reps);
 bk_status combine_action_device(bk_ctx* ctx, const bk_operator* op, const double* X, int S,
                                 int s, const double* C, int64_t ldc, int64_t N, double* T,
                                 double* Q, double* resid);

@@ -391,24 +391,66 @@ def test_launch_counter_and_native_library_loaded(bk, ctx):
 
 
 def test_generate_batch_matches_per_chip(bk, ctx, oracle):
-    """Config 4 batch path: every chip's outputs equal its single-chip run
-    (bitwise: same kernels, same launch shape per stream count) and the oracle."""
+    """Config 4 batch path. streams = 1 (and host outputs with more streams):
+    chips one after another, bitwise the single-chip runs. streams = K with
+    device outputs: groups of K chips z-stacked and solved by one cooperative
+    launch, chip k on 1/K of the SMs — bitwise the single-chip run given the
+    same SM share (same CTA ranges and reduction order). Oracle parity."""
+    import torch
+
     chips = [bk.synth_chip(4, 32, 24, 4, 16, 8, chip_id=c) for c in range(5)]
-    for streams in (1, 2):
+    for streams in (1, 2):  # host outputs: sequential
         T, Q, R, reps, tim = bk.generate_batch(chips, cfg_jacobi(), streams=streams, ctx=ctx)
         assert len(reps) == 5 and all(r.all_converged() for r in reps)
         assert tim.total_s > 0 and tim.iterations_total == sum(r.iterations for r in reps)
-        sub = bk.Context(0)
-        bk.set_cg_sm_budget(sub, sub_budget(streams))
         for c, ch in enumerate(chips):
             T1, Q1, R1, rep1, _ = bk.generate_chip(ch.grid, ch.k, ch.bc, ch.q_basis, ch.coef,
-                                                   cfg_jacobi(), ctx=sub)
+                                                   cfg_jacobi(), ctx=ctx)
             assert np.array_equal(T[c], T1) and np.array_equal(Q[c], Q1)
     o = oracle.assemble(grid_tuple(chips[2].grid), chips[2].k, chips[2].bc.as_tuples(),
                         dz=chips[2].grid.dz)
     X, _ = oracle.block_cg(o, oracle.rhs_from_power(o, chips[2].q_basis), TOL, 100000, 1)
     To, Qo, _ = oracle.combine_action(o, X, chips[2].coef)
     assert rel_l2(T[2], To) <= PARITY and rel_l2(Q[2], Qo) <= PARITY
+    # batched pipeline: 5 chips in groups of 3 (3 + 2), device outputs
+    dev = torch.device("cuda", 0)
+    n, N = chips[0].grid.cell_count(), 8
+    Td = [torch.empty((N, n), dtype=torch.float64, device=dev) for _ in chips]
+    Qd = [torch.empty((N, n), dtype=torch.float64, device=dev) for _ in chips]
+    Rd = [torch.empty(N, dtype=torch.float64, device=dev) for _ in chips]
+    _, _, _, reps, tim = bk.generate_batch(chips, cfg_jacobi(), t_out=Td, q_out=Qd, resid_out=Rd,
+                                           streams=3, ctx=ctx)
+    torch.cuda.synchronize()
+    assert all(r.all_converged() for r in reps)
+    for c, ch in enumerate(chips):
+        sub = bk.Context(0)
+        bk.set_cg_sm_budget(sub, sub_budget(3 if c < 3 else 2))
+        T1, Q1, R1, rep1, _ = bk.generate_chip(ch.grid, ch.k, ch.bc, ch.q_basis, ch.coef,
+                                               cfg_jacobi(), ctx=sub)
+        assert reps[c].iterations == rep1.iterations
+        assert np.array_equal(Td[c].cpu().numpy(), T1) and np.array_equal(Qd[c].cpu().numpy(), Q1)
+
+
+def test_generate_batch_stacked_2d_vs_oracle(bk, ctx, oracle):
+    """Batched pipeline on 2D chips (C2-like, resident solver): every chip
+    within tolerance of the oracle."""
+    import torch
+
+    chips = [bk.synth_chip(2, 48, 40, 1, 16, 12, chip_id=c) for c in range(4)]
+    dev = torch.device("cuda", 0)
+    n, N = chips[0].grid.cell_count(), 12
+    Td = [torch.empty((N, n), dtype=torch.float64, device=dev) for _ in chips]
+    Qd = [torch.empty((N, n), dtype=torch.float64, device=dev) for _ in chips]
+    Rd = [torch.empty(N, dtype=torch.float64, device=dev) for _ in chips]
+    _, _, _, reps, _ = bk.generate_batch(chips, cfg_jacobi(), t_out=Td, q_out=Qd, resid_out=Rd,
+                                         streams=4, ctx=ctx)
+    torch.cuda.synchronize()
+    for c, ch in enumerate(chips):
+        o = oracle.assemble(grid_tuple(ch.grid), ch.k, ch.bc.as_tuples())
+        X, _ = oracle.block_cg(o, oracle.rhs_from_power(o, ch.q_basis), TOL, 100000, 1)
+        To, Qo, _ = oracle.combine_action(o, X, ch.coef)
+        assert reps[c].all_converged()
+        assert rel_l2(Td[c].cpu().numpy(), To) <= PARITY and rel_l2(Qd[c].cpu().numpy(), Qo) <= PARITY
 
 
 def sub_budget(streams):
