@@ -256,7 +256,7 @@ def ncu_traffic(config):
         return json.load(f).get(f"config{config}")
 
 
-CHIPS_BY_CONFIG = {1: 8, 2: 8, 3: 4}  # independent chips per GPU per step, solved together
+CHIPS_BY_CONFIG = {1: 8, 2: 16, 3: 4}  # independent chips per GPU per step, solved together
 
 
 def chips_per_step(args):
