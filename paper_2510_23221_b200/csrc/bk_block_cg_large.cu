@@ -479,6 +479,174 @@ __global__ void __launch_bounds__(LBS, 2) k_spmm_gram(SweepArgs a) {
     G.write(a.part + (int64_t)blockIdx.x * (S * S), warp, g, t);
 }
 
+// ---------------------------------------------------------------------------
+// phase 1 for S = 64 with TMA bulk copies (even nx): per 16-cell run, one
+// thread issues cp.async.bulk copies of the centre run with its x-halo, the
+// y-1 / y+1 / z-1 / z+1 runs and the stencil coefficients into a 2-stage
+// shared-memory ring (mbarrier completion); the stencil then reads shared
+// memory only. A few bulk instructions per group instead of thousands of
+// 16-byte copies, and the loads of group g+1 overlap the sweep of group g.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tMBW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra MBW_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+struct TmaStage64 {
+    static constexpr int S = 64;
+    static constexpr int ROWS = 82;       // centre (x-halo) 18 + 4 runs x 16
+    static constexpr int ROWD = S;        // dense rows
+    static constexpr int COEF = 6 * 24;   // 6 coefficient runs (<= 18 values, padded)
+    static constexpr int DOUBLES = ROWS * ROWD + COEF;
+};
+
+// issue the copies of group `grp` (one tile, TPB = 1) into stage `st`
+__device__ __forceinline__ void tma_stage64(double* st, unsigned long long* bar, const SweepArgs& a,
+                                            int grp, int ntiles) {
+    constexpr int S = 64;
+    TileCells tc;
+    tile_cells(a.sl, grp, ntiles, tc);
+    const int nx = a.sl.nx, nv = tc.nv;
+    const int64_t pz = (int64_t)nx * (a.sl.nyl + 2);
+    const int64_t plane = (int64_t)nx * a.sl.ny;
+    const unsigned rowb = S * 8;
+    // centre run with halo: cells max(ix0-1, 0) .. min(ix0+nv, nx-1)
+    const int lo = tc.ix0 > 0 ? -1 : 0;
+    const int hi = tc.ix0 + nv < nx ? nv : nv - 1;  // inclusive, relative to ix0
+    unsigned total = (unsigned)(hi - lo + 1) * rowb + 2 * nv * rowb;
+    const bool zm = tc.iz > 0, zp = tc.iz < a.sl.nz - 1;
+    if (zm) total += nv * rowb;
+    if (zp) total += nv * rowb;
+    double* coef = st + TmaStage64::ROWS * TmaStage64::ROWD;
+    // coefficient runs (16-byte aligned sources): diag[g0..+16), cx[g0-2..+18),
+    // cy[g0-nx..+16), cy[g0..+16), cz[g0-plane..+16), cz[g0..+16)
+    const int64_t g0 = tc.g0;
+    const bool ym = tc.iyg > 0;
+    total += 16 * 8 + 18 * 8 + 16 * 8 + 16 * 8;  // diag, cx, cy(y-) , cy(y+)
+    if (zm) total += 16 * 8;
+    total += 16 * 8;  // cz(z+) run always readable (last plane: value unused)
+    mbar_expect_tx(bar, total);
+    bulk_g2s(st + (1 + lo) * S, a.P + (tc.l0 + lo) * S, (unsigned)(hi - lo + 1) * rowb, bar);
+    bulk_g2s(st + 18 * S, a.P + (tc.l0 - nx) * S, nv * rowb, bar);
+    bulk_g2s(st + 34 * S, a.P + (tc.l0 + nx) * S, nv * rowb, bar);
+    if (zm) bulk_g2s(st + 50 * S, a.P + (tc.l0 - pz) * S, nv * rowb, bar);
+    if (zp) bulk_g2s(st + 66 * S, a.P + (tc.l0 + pz) * S, nv * rowb, bar);
+    bulk_g2s(coef, a.st.diag + g0, 16 * 8, bar);
+    bulk_g2s(coef + 24, a.st.cx + g0 - 2 + (tc.ix0 == 0 && g0 < 2 ? 2 : 0), 18 * 8, bar);
+    bulk_g2s(coef + 48, a.st.cy + (ym ? g0 - nx : g0), 16 * 8, bar);
+    bulk_g2s(coef + 72, a.st.cy + g0, 16 * 8, bar);
+    if (zm) bulk_g2s(coef + 96, a.st.cz + g0 - plane, 16 * 8, bar);
+    bulk_g2s(coef + 120, a.st.cz + g0, 16 * 8, bar);
+}
+
+__global__ void __launch_bounds__(LBS, 2) k_spmm_gram_tma64(SweepArgs a) {
+    constexpr int S = 64;
+    using G_ = Geo<S>;
+    constexpr int RS = G_::RS, LPC = 16, CPW = 2;
+    extern __shared__ __align__(128) double sm_[];
+    __shared__ __align__(8) unsigned long long bars[2];
+    double* U = sm_ + 2 * TmaStage64::DOUBLES;
+    double* V = U + G_::TILE;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int r = warp * CPW + lane / LPC;  // cell of the run
+    const int ca = 2 * (lane % LPC), cb2 = ca + S / 2;
+    const int ntiles = n_tiles(a.sl);
+    const int ngroups = ntiles;  // TPB = 1
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    OwnedGram<S> G;
+    G.zero();
+    int grp = blockIdx.x;
+    if (threadIdx.x == 0 && grp < ngroups) tma_stage64(sm_, &bars[0], a, grp, ntiles);
+    for (int it = 0; grp < ngroups; grp += gridDim.x, ++it) {
+        const int nxt = grp + gridDim.x;
+        if (threadIdx.x == 0 && nxt < ngroups) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tma_stage64(sm_ + ((it + 1) & 1) * TmaStage64::DOUBLES, &bars[(it + 1) & 1], a, nxt,
+                        ntiles);
+        }
+        TileCells tc;
+        tile_cells(a.sl, grp, ntiles, tc);
+        mbar_wait(&bars[it & 1], (unsigned)((it >> 1) & 1));
+        const double* rows = sm_ + (it & 1) * TmaStage64::DOUBLES;
+        const double* cf = rows + TmaStage64::ROWS * TmaStage64::ROWD;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0}, ctr[4] = {0.0, 0.0, 0.0, 0.0};
+        if (r < tc.nv) {
+            const int ix = tc.ix0 + r;
+            auto row = [&](int rr, double c, bool has) {
+                if (!has) return;
+                const double2 x0 = *reinterpret_cast<const double2*>(rows + rr * S + ca);
+                const double2 x1 = *reinterpret_cast<const double2*>(rows + rr * S + cb2);
+                acc[0] = fma(c, x0.x, acc[0]);
+                acc[1] = fma(c, x0.y, acc[1]);
+                acc[2] = fma(c, x1.x, acc[2]);
+                acc[3] = fma(c, x1.y, acc[3]);
+            };
+            const int xo = (tc.ix0 == 0 && tc.g0 < 2) ? 2 : 0;  // cx run start shift
+            // CSR order z-, y-, x-, diag, x+, y+, z+ (values = -conductance)
+            row(50 + r, -cf[96 + r], tc.iz > 0);
+            row(18 + r, -cf[48 + r], tc.iyg > 0);
+            row(r, -cf[24 + 1 + r - xo], ix > 0);
+            {
+                const double2 x0 = *reinterpret_cast<const double2*>(rows + (r + 1) * S + ca);
+                const double2 x1 = *reinterpret_cast<const double2*>(rows + (r + 1) * S + cb2);
+                ctr[0] = x0.x;
+                ctr[1] = x0.y;
+                ctr[2] = x1.x;
+                ctr[3] = x1.y;
+                const double d = cf[r];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[j] = fma(d, ctr[j], acc[j]);
+            }
+            row(r + 2, -cf[24 + 2 + r - xo], ix < a.sl.nx - 1);
+            row(34 + r, -cf[72 + r], tc.iyg < a.sl.ny - 1);
+            row(66 + r, -cf[120 + r], tc.iz < a.sl.nz - 1);
+            const int64_t l = tc.l0 + r;
+            *reinterpret_cast<double2*>(a.W + l * S + ca) = make_double2(acc[0], acc[1]);
+            *reinterpret_cast<double2*>(a.W + l * S + cb2) = make_double2(acc[2], acc[3]);
+        }
+        *reinterpret_cast<double2*>(U + r * RS + ca) = make_double2(ctr[0], ctr[1]);
+        *reinterpret_cast<double2*>(U + r * RS + cb2) = make_double2(ctr[2], ctr[3]);
+        *reinterpret_cast<double2*>(V + r * RS + ca) = make_double2(acc[0], acc[1]);
+        *reinterpret_cast<double2*>(V + r * RS + cb2) = make_double2(acc[2], acc[3]);
+        __syncthreads();
+        G.accumulate(U, V, warp, g, t);
+        __syncthreads();
+    }
+    G.write(a.part + (int64_t)blockIdx.x * (S * S), warp, g, t);
+}
+
+constexpr size_t smem_spmm_tma64() {
+    return (2 * (size_t)TmaStage64::DOUBLES + 2 * (size_t)Geo<64>::TILE) * sizeof(double);
+}
+
 __device__ __forceinline__ void frag_from_smem(const double* T, int RS, int row0, int col,
                                                double (&o)[4]) {
     const double2 a = *reinterpret_cast<const double2*>(T + row0 * RS + col);
@@ -624,6 +792,40 @@ __global__ void __launch_bounds__(LBS, 2) k_pupdate(SweepArgs a) {
         __syncthreads();  // buffer it % NST is refilled by the prefetch of the next iteration
     }
     cp_wait<0>();
+}
+
+template <int S>
+cudaError_t launch_update(const SweepArgs& a, int nb, cudaStream_t s) {
+    const cudaError_t e = bk::set_max_smem((const void*)k_update<S>, smem_update<S>());
+    if (e != cudaSuccess) return e;
+    k_update<S><<<nb, LBS, smem_update<S>(), s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int S>
+cudaError_t launch_pupdate(const SweepArgs& a, int nb, cudaStream_t s) {
+    const cudaError_t e = bk::set_max_smem((const void*)k_pupdate<S>, smem_pupdate<S>());
+    if (e != cudaSuccess) return e;
+    k_pupdate<S><<<nb, LBS, smem_pupdate<S>(), s>>>(a);
+    return cudaGetLastError();
+}
+
+// phase 1 launch: the TMA variant for S = 64 on grids whose x-runs are full
+// (nx % 16 == 0), else the cp.async-free direct-load kernel
+template <int S>
+cudaError_t launch_spmm(const SweepArgs& a, int nb, cudaStream_t s) {
+    if constexpr (S == 64) {
+        if (a.sl.nx % 16 == 0 && getenv("BK_NO_TMA_SPMM") == nullptr) {
+            const cudaError_t e = bk::set_max_smem((const void*)k_spmm_gram_tma64, smem_spmm_tma64());
+            if (e != cudaSuccess) return e;
+            k_spmm_gram_tma64<<<nb, LBS, smem_spmm_tma64(), s>>>(a);
+            return cudaGetLastError();
+        }
+    }
+    const cudaError_t e = bk::set_max_smem((const void*)k_spmm_gram<S>, smem_spmm<S>());
+    if (e != cudaSuccess) return e;
+    k_spmm_gram<S><<<nb, LBS, smem_spmm<S>(), s>>>(a);
+    return cudaGetLastError();
 }
 
 // CTAs of the sweep kernels (2 per SM: register-bound), same for the
@@ -1000,12 +1202,12 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     if ((st = read_cmd(&cmd, &sa)) != BK_OK) return st;
     for (int m = 1; m <= cfg->max_iter && sa > 0; ++m) {
         halo(a.P);
-        k_spmm_gram<S><<<nb, LBS, sws, s>>>(a);
+        BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s));
         ++ctx->launches;
         reduce(S * S, nb);
         k_ctl_alpha<S><<<1, CBS, cs, s>>>(ctl, red);
         ++ctx->launches;
-        k_update<S><<<nb, LBS, swu, s>>>(a);
+        BK_CUDA_TRY(ctx, launch_update<S>(a, nb, s));
         ++ctx->launches;
         reduce(E, nb);
         k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, red, m);
@@ -1028,7 +1230,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
                 continue;
             }
         }
-        k_pupdate<S><<<nb, LBS, swp, s>>>(a);
+        BK_CUDA_TRY(ctx, launch_pupdate<S>(a, nb, s));
         ++ctx->launches;
     }
     // honest residuals for still-active columns
@@ -1149,8 +1351,7 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
             ++ctx->launches;
             break;
         case BK_DD_SPMM:
-            BK_CUDA_TRY(ctx, set((const void*)k_spmm_gram<S>, sws));
-            k_spmm_gram<S><<<nb, LBS, sws, s>>>(a);
+            BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s));
             ++ctx->launches;
             reduce(S * S, nb);
             break;
@@ -1161,7 +1362,7 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
             break;
         case BK_DD_UPDATE:
             BK_CUDA_TRY(ctx, set((const void*)k_update<S>, swu));
-            k_update<S><<<nb, LBS, swu, s>>>(a);
+            BK_CUDA_TRY(ctx, launch_update<S>(a, nb, s));
             ++ctx->launches;
             reduce(E, nb);
             break;
@@ -1192,7 +1393,7 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
             break;
         case BK_DD_PUPDATE:
             BK_CUDA_TRY(ctx, set((const void*)k_pupdate<S>, swp));
-            k_pupdate<S><<<nb, LBS, swp, s>>>(a);
+            BK_CUDA_TRY(ctx, launch_pupdate<S>(a, nb, s));
             ++ctx->launches;
             break;
         case BK_DD_CTL_FINAL: {
