@@ -1169,6 +1169,18 @@ bk_status run_dmma_multi(bk_ctx* ctx, const bk_operator* op, int K, const double
     a.precond = cfg->precond;
     a.rep = (CgReport*)pRep;
     a.prof = nullptr;
+    const bool want_prof = getenv("BK_CG_PROFILE") != nullptr;
+    long long* dprof = nullptr;
+    if (want_prof) {
+        void* pp;
+        if ((st = workspace(ctx, kSlotCgFlags, PROF_ITERS * PROF_MARKS * sizeof(long long), &pp)) !=
+            BK_OK)
+            return st;
+        dprof = (long long*)pp;
+        BK_CUDA_TRY(ctx, cudaMemsetAsync(dprof, 0, PROF_ITERS * PROF_MARKS * sizeof(long long),
+                                         ctx->stream));
+        a.prof = dprof;
+    }
     a.nchips = K;
     a.cpc = cpc;
     a.nchip = nchip;
@@ -1177,7 +1189,27 @@ bk_status run_dmma_multi(bk_ctx* ctx, const bk_operator* op, int K, const double
     BK_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(kern, dim3((unsigned)nb), dim3(BS), args, smem,
                                                  ctx->stream));
     ++ctx->launches;
-    return read_small(ctx, reps, pRep, (size_t)K * sizeof(CgReport));
+    st = read_small(ctx, reps, pRep, (size_t)K * sizeof(CgReport));
+    if (st == BK_OK && want_prof) {
+        std::vector<long long> pr(PROF_ITERS * PROF_MARKS);
+        cudaMemcpy(pr.data(), dprof, pr.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+        double acc[8] = {};
+        int cnt = 0;
+        for (int i = 1; i < PROF_ITERS; ++i) {
+            const long long* r = pr.data() + i * PROF_MARKS;
+            if (!r[0] || !r[7]) continue;
+            for (int k = 1; k < 8; ++k) acc[k] += (double)(r[k] - r[k - 1]);
+            ++cnt;
+        }
+        if (cnt)
+            fprintf(stderr,
+                    "[bk_cg_profile batched K=%d cpc=%d res=%d chip 0] per-iteration ns: phase1 %.0f | "
+                    "reduceG %.0f | solve_a %.0f | phase2 %.0f | reduceS %.0f | control+solve_b %.0f | "
+                    "phase3+sync %.0f\n",
+                    K, cpc, (int)resident, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
+                    acc[5] / cnt, acc[6] / cnt, acc[7] / cnt);
+    }
+    return st;
 }
 
 bk_status block_cg_device_multi(bk_ctx* ctx, const bk_operator* op, int K, const double* B, int S,

@@ -96,6 +96,7 @@ enum Slot : int {
     kSlotQo1,
     kSlotRes1,
     kSlotCgBars,    // group barriers of the batched (multi-chip) solve
+    kSlotCgFlags,   // phase timestamps of a profiled batched solve
     kSlotStackDiag, // z-stacked operator of the batched pipeline (6 arrays)
     kSlotStackCoef, // per-chip combination coefficients of the batched pipeline
 };
