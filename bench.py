@@ -429,7 +429,7 @@ def run_ours(args):
     # against BlocKOA's T for the same samples.
     direct = None
     if rank == 0 and not args.no_direct:
-        M = min(N, 64 if args.config <= 2 else 16)
+        M = min(N, {1: 64, 2: 32}.get(args.config, 16))
         qs = inp.q_basis @ inp.coef[:, :M]  # the samples' power maps (u_inf = 0: no lift)
         one = torch.ones((1, 1), dtype=torch.float64, device=dev)
         dchips = [SimpleNamespace(grid=inp.grid, bc=inp.bc, k=k_d,
