@@ -651,8 +651,30 @@ def run_ours_batch(args, ctx, world, rank, local):
                      "peak_source": peak_kind},
         "timing": "per-step wall clock around bk_generate_batch (synchronous), max over ranks",
         "gpu_launches": int(ctx.launch_count - launches0), "clocks": clk.summary(),
+        "input_synthesis": synthesis_cost(bk, torch, ctx, nchip, float(np.mean(times)), N),
     }
     return _finish(args, world, rank, line)
+
+
+def synthesis_cost(bk, torch, ctx, nchip, step_s, N):
+    """chip inputs generated on the host (bk_synth_chip, one
+    thread) vs on the device (bk_synth_chip_device), per chip, and the config-4
+    throughput when every step also synthesises its chips on the device."""
+    cid, nx, ny, nz, s, _ = __import__("paper_2510_23221_b200").CONFIGS[4]
+    t = time.perf_counter()
+    for c in range(4):
+        bk.synth_chip(cid, nx, ny, nz, s, N, chip_id=1000 + c)
+    host = (time.perf_counter() - t) / 4
+    bk.synth_chip_device(cid, nx, ny, nz, s, N, chip_id=999, ctx=ctx)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for c in range(nchip):
+        bk.synth_chip_device(cid, nx, ny, nz, s, N, chip_id=1000 + c, ctx=ctx)
+    torch.cuda.synchronize()
+    devc = (time.perf_counter() - t) / nchip
+    return {"host_ms_per_chip": host * 1e3, "device_ms_per_chip": devc * 1e3,
+            "value_with_device_synthesis": nchip * N / (step_s + nchip * devc),
+            "value_with_host_synthesis_1_thread": nchip * N / (step_s + nchip * host)}
 
 
 def run_ours_large(args, ctx, world, rank, local):

@@ -291,6 +291,16 @@ bk_status bk_synth_chip(const bk_synth_spec* spec, bk_grid* grid_out, double* dz
                         int* has_dz, bk_face bc_out[6], double* k, double* Qbasis,
                         double* C);
 
+/* The same chip with its fields evaluated on the device: the
+ * random draws stay on the host (identical Rng streams), k (n) and the basis
+ * maps Qbasis (n x s, row-major) are written to DEVICE buffers by kernels on
+ * the context's stream; C (s x N) may be host or device. k for configs 1, 2, 4
+ * and C are bitwise bk_synth_chip's; the maps and the lognormal k of configs
+ * 3, 5 differ only through CUDA's exp vs the host libm (a few ulp). */
+bk_status bk_synth_chip_device(bk_ctx* ctx, const bk_synth_spec* spec, bk_grid* grid_out,
+                               double* dz_out, int* has_dz, bk_face bc_out[6], double* k_dev,
+                               double* Qbasis_dev, double* C);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,7 +42,8 @@ __all__ = [
     "GridSpec", "Dirichlet", "Robin", "Adiabatic", "BoundarySpec", "SolverConfig",
     "SolveReport", "BlockCgResult", "PhaseTimings", "DiscreteOperator", "Context",
     "assemble", "operator_from_csr", "block_cg", "combine_action", "generate_chip", "generate_batch", "rhs_from_power",
-    "power_from_rhs", "cg_error_bound", "derive_seed", "synth_chip", "library_path",
+    "power_from_rhs", "cg_error_bound", "derive_seed", "synth_chip", "synth_chip_device",
+    "library_path",
     "Error", "InvalidSpecError", "InvalidConfigError", "DimensionMismatchError",
     "NonPositiveConductivityError", "NonPositiveHtcError", "EmptyBasisError",
     "NotConvergedError", "InvalidKappaError", "DeviceError",
@@ -168,6 +169,8 @@ def _load():
         lib.bk_rng_normal.restype = None
         lib.bk_synth_chip.argtypes = [C.POINTER(_Synth), C.POINTER(_Grid), dp, C.POINTER(C.c_int),
                                       C.POINTER(_Face), dp, dp, dp]
+        lib.bk_synth_chip_device.argtypes = [vp, C.POINTER(_Synth), C.POINTER(_Grid), dp,
+                                             C.POINTER(C.c_int), C.POINTER(_Face), dp, dp, dp]
         lib.bk_abi_version.restype = C.c_int
         _lib = lib
     return _lib
@@ -721,6 +724,37 @@ def synth_chip(config: int, nx: int, ny: int, nz: int, s: int, N: int, master_se
     fl = []
     for f in faces:
         fl.append(Dirichlet(f.a) if f.kind == 0 else Robin(f.a, f.b) if f.kind == 1 else Adiabatic())
+    return ChipInputs(grid, BoundarySpec(fl), k, q, c)
+
+
+def synth_chip_device(config: int, nx: int, ny: int, nz: int, s: int, N: int,
+                      master_seed: int = 1, chip_id: int = 0,
+                      ctx: Optional[Context] = None) -> ChipInputs:
+    """synth_chip with the fields evaluated on the GPU: the same
+    random draws (host), k and q_basis as CUDA torch tensors written by device
+    kernels, coef as a CUDA tensor. k of configs 1, 2, 4 and coef are bitwise
+    synth_chip's; the maps agree to a few ulp (CUDA exp vs host libm)."""
+    import torch
+
+    ctx = _ctx(ctx)
+    lib = _load()
+    sp = _Synth(config, nx, ny, nz, s, N, master_seed, chip_id)
+    g = _Grid()
+    dz = np.zeros(nz, np.float64)
+    has_dz = C.c_int(0)
+    faces = (_Face * 6)()
+    dev = torch.device("cuda", ctx.device)
+    n = nx * ny * nz
+    k = torch.empty(n, dtype=torch.float64, device=dev)
+    q = torch.empty((n, s), dtype=torch.float64, device=dev)
+    c = torch.empty((s, N), dtype=torch.float64, device=dev)
+    st = lib.bk_synth_chip_device(ctx.h, C.byref(sp), C.byref(g), dz.ctypes.data_as(C.c_void_p),
+                                  C.byref(has_dz), faces, C.c_void_p(k.data_ptr()),
+                                  C.c_void_p(q.data_ptr()), C.c_void_p(c.data_ptr()))
+    _raise(st, ctx.h, "synth_chip_device")
+    grid = GridSpec(g.nx, g.ny, g.nz, g.lx, g.ly, g.lz, dz.copy() if has_dz.value else None)
+    fl = [Dirichlet(f.a) if f.kind == 0 else Robin(f.a, f.b) if f.kind == 1 else Adiabatic()
+          for f in faces]
     return ChipInputs(grid, BoundarySpec(fl), k, q, c)
 
 

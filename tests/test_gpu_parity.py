@@ -509,3 +509,43 @@ def test_slab_decomposition_matches_single_gpu(bk, ctx, nslabs):
     else:
         assert rel_l2(Xh, ref.x) <= PARITY
         assert abs(rep.iterations - ref.report.iterations) <= max(3, ref.report.iterations // 10)
+
+
+# ------------------------------------------------------ device-side synthesis
+@pytest.mark.parametrize("case", [(1, 40, 32, 1, 8, 6), (2, 48, 40, 1, 16, 5), (3, 24, 20, 8, 32, 4),
+                                  (4, 32, 24, 4, 16, 8), (5, 16, 16, 16, 64, 3)])
+def test_synth_chip_device_matches_host(bk, ctx, case):
+    """the device generator evaluates the host generator's plan.
+    Geometry, boundary, coefficients and the tile / layer k are bitwise; the
+    blob maps and the lognormal k differ only through CUDA exp vs libm."""
+    h = bk.synth_chip(*case, chip_id=5)
+    d = bk.synth_chip_device(*case, chip_id=5, ctx=ctx)
+    assert (h.grid.nx, h.grid.ny, h.grid.nz, h.grid.lz) == (d.grid.nx, d.grid.ny, d.grid.nz, d.grid.lz)
+    assert h.bc.as_tuples() == d.bc.as_tuples()
+    assert np.array_equal(h.coef, d.coef.cpu().numpy())
+    kd, qd = d.k.cpu().numpy(), d.q_basis.cpu().numpy()
+    if case[0] in (1, 2, 4):
+        assert np.array_equal(h.k, kd)
+    else:
+        assert np.max(np.abs(kd - h.k) / h.k) <= 1e-15
+    assert np.max(np.abs(qd - h.q_basis)) <= 1e-14 * np.max(np.abs(h.q_basis))
+    assert np.array_equal(qd == 0.0, h.q_basis == 0.0)
+
+
+def test_generate_from_device_synthesis(bk, ctx):
+    """A config-4 chip generated straight from device-synthesised inputs:
+    within tolerance of the host-synthesised chip's outputs."""
+    import torch
+
+    h = bk.synth_chip(4, 32, 24, 4, 16, 8, chip_id=2)
+    d = bk.synth_chip_device(4, 32, 24, 4, 16, 8, chip_id=2, ctx=ctx)
+    Th, Qh, Rh, reph, _ = bk.generate_chip(h.grid, h.k, h.bc, h.q_basis, h.coef, cfg_jacobi(), ctx=ctx)
+    n = d.grid.cell_count()
+    Td = torch.empty((8, n), dtype=torch.float64, device="cuda")
+    Qd = torch.empty_like(Td)
+    Rd = torch.empty(8, dtype=torch.float64, device="cuda")
+    _, _, _, repd, _ = bk.generate_chip(d.grid, d.k, d.bc, d.q_basis, d.coef, cfg_jacobi(),
+                                        t_out=Td, q_out=Qd, resid_out=Rd, ctx=ctx)
+    torch.cuda.synchronize()
+    assert repd.all_converged()
+    assert rel_l2(Td.cpu().numpy(), Th) <= PARITY and rel_l2(Qd.cpu().numpy(), Qh) <= PARITY
