@@ -10,7 +10,6 @@
 #include <new>
 #include <map>
 #include <mutex>
-#include <thread>
 #include <string>
 #include <vector>
 
@@ -524,8 +523,6 @@ bk_status bk_create(int device, bk_ctx** out) {
 
 void bk_destroy(bk_ctx* ctx) {
     if (!ctx) return;
-    for (bk_ctx* sub : ctx->subs) bk_destroy(sub);
-    ctx->subs.clear();
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (int i = 0; i < bk_ctx::kSlots; ++i) cudaFree(ctx->ws[i]);
@@ -572,9 +569,7 @@ bk_status bk_synchronize(bk_ctx* ctx) {
 
 int64_t bk_launch_count(const bk_ctx* ctx) {
     if (!ctx) return 0;
-    int64_t n = ctx->launches;
-    for (const bk_ctx* sub : ctx->subs) n += sub->launches;
-    return n;
+    return ctx->launches;
 }
 
 bk_status bk_assemble(bk_ctx* ctx, const bk_grid* grid, const double* k, const bk_face bc[6],
@@ -899,75 +894,45 @@ bk_status bk_generate_batch(bk_ctx* ctx, int n_chips, const bk_grid* grids,
                                   reports, streams, timings);
         streams = 1;
     }
-    // sub-contexts: own stream + workspace, an equal share of the SMs each
-    while ((int)ctx->subs.size() < streams) {
-        bk_ctx* sub = nullptr;
-        const bk_status st = bk_create(ctx->device, &sub);
-        if (st != BK_OK) return fail(ctx, st, "generate_batch: sub-context");
-        ctx->subs.push_back(sub);
-    }
-    int share = ctx->num_sms / streams > 0 ? ctx->num_sms / streams : 1;
-    if (const char* e = getenv("BK_BATCH_SHARE")) share = atoi(e);
-    for (int w = 0; w < streams; ++w) ctx->subs[w]->cg_max_ctas = share;
-    std::vector<bk_status> st(streams, BK_OK);
-    std::vector<std::string> msg(streams);
-    std::vector<bk_phase_timings> tim(streams);
-    for (auto& t : tim) std::memset(&t, 0, sizeof(t));
+    // one chip after another on the caller's context; host outputs of chip c
+    // drain over PCIe (copy stream, alternating output parities) while chip
+    // c+1 computes
+    bk_status first = BK_OK;
+    std::string msg;
+    bk_phase_timings tot;
+    std::memset(&tot, 0, sizeof(tot));
     const auto t0 = std::chrono::steady_clock::now();
-    auto worker = [&](int w) {
-        bk_ctx* sub = ctx->subs[w];
-        const int64_t launches0 = sub->launches;
-        int parity = 0;
-        for (int c = w; c < n_chips; c += streams, parity ^= 1) {
-            bk_phase_timings pt;
-            bk_solve_report* rep = reports ? &reports[c] : nullptr;
-            const bk_status r = generate_chip_impl(sub, &grids[c], k[c], bc + 6 * c, Qbasis[c], s,
-                                                   C[c], N, cfg, T ? T[c] : nullptr,
-                                                   Q ? Q[c] : nullptr, resid ? resid[c] : nullptr,
-                                                   rep, &pt, true, parity);
-            if (r != BK_OK && st[w] == BK_OK) {
-                st[w] = r;
-                msg[w] = sub->err;
-                if (r != BK_NOT_CONVERGED) break;
-            }
-            tim[w].assemble_s += pt.assemble_s;
-            tim[w].basis_solve_s += pt.basis_solve_s;
-            tim[w].combine_action_s += pt.combine_action_s;
-            tim[w].h2d_s += pt.h2d_s;
-            tim[w].d2h_s += pt.d2h_s;
-            tim[w].iterations_total += pt.iterations_total;
-            tim[w].matvecs_total += pt.matvecs_total;
+    int parity = 0;
+    for (int c = 0; c < n_chips; ++c, parity ^= 1) {
+        bk_phase_timings pt;
+        bk_solve_report* rep = reports ? &reports[c] : nullptr;
+        const bk_status r = generate_chip_impl(ctx, &grids[c], k[c], bc + 6 * c, Qbasis[c], s, C[c],
+                                               N, cfg, T ? T[c] : nullptr, Q ? Q[c] : nullptr,
+                                               resid ? resid[c] : nullptr, rep, &pt, true, parity);
+        if (r != BK_OK && first == BK_OK) {
+            first = r;
+            msg = ctx->err;
+            if (r != BK_NOT_CONVERGED) break;
         }
-        // outputs of the last chips are still draining
-        if (sub->copy_stream && cudaStreamSynchronize(sub->copy_stream) != cudaSuccess &&
-            st[w] == BK_OK) {
-            st[w] = BK_CUDA_ERROR;
-            msg[w] = cudaGetErrorString(cudaGetLastError());
-        }
-        sub->drain_pending[0] = sub->drain_pending[1] = false;
-        (void)launches0;
-    };
-    std::vector<std::thread> pool;
-    for (int w = 1; w < streams; ++w) pool.emplace_back(worker, w);
-    worker(0);
-    for (auto& th : pool) th.join();
-    const double wall =
-        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    if (timings) {
-        std::memset(timings, 0, sizeof(*timings));
-        for (const auto& t : tim) {
-            timings->assemble_s += t.assemble_s;
-            timings->basis_solve_s += t.basis_solve_s;
-            timings->combine_action_s += t.combine_action_s;
-            timings->h2d_s += t.h2d_s;
-            timings->d2h_s += t.d2h_s;
-            timings->iterations_total += t.iterations_total;
-            timings->matvecs_total += t.matvecs_total;
-        }
-        timings->total_s = wall;
+        tot.assemble_s += pt.assemble_s;
+        tot.basis_solve_s += pt.basis_solve_s;
+        tot.combine_action_s += pt.combine_action_s;
+        tot.h2d_s += pt.h2d_s;
+        tot.d2h_s += pt.d2h_s;
+        tot.iterations_total += pt.iterations_total;
+        tot.matvecs_total += pt.matvecs_total;
     }
-    for (int w = 0; w < streams; ++w)
-        if (st[w] != BK_OK) return fail(ctx, st[w], msg[w]);
+    // outputs of the last chips are still draining
+    if (ctx->copy_stream && cudaStreamSynchronize(ctx->copy_stream) != cudaSuccess && first == BK_OK) {
+        first = BK_CUDA_ERROR;
+        msg = cudaGetErrorString(cudaGetLastError());
+    }
+    ctx->drain_pending[0] = ctx->drain_pending[1] = false;
+    if (timings) {
+        *timings = tot;
+        timings->total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    if (first != BK_OK) return fail(ctx, first, msg);
     return BK_OK;
 }
 

@@ -32,7 +32,6 @@ struct bk_ctx {
     int64_t launches = 0;
     bk_operator* scratch = nullptr;  // operator reused by bk_generate_chip
     int cg_max_ctas = 0;             // 0 = every SM (see bk_set_cg_sm_budget)
-    std::vector<bk_ctx*> subs;       // per-stream sub-contexts of bk_generate_batch
     std::vector<bk_operator*> views; // per-chip views into the batched pipeline's stacked operator
     cudaStream_t copy_stream = nullptr;    // D2H of host outputs, overlapped with compute
     std::vector<cudaEvent_t> chunk_ev;     // per-chunk "outputs ready" events
