@@ -44,6 +44,10 @@ typedef enum {
     BK_EMPTY_BASIS = 6,          /* EmptyBasisError         errors.hpp:49 */
     BK_NOT_CONVERGED = 7,        /* NotConvergedError       errors.hpp:39 */
     BK_INVALID_KAPPA = 8,        /* InvalidKappaError       errors.hpp:44 */
+    BK_IO_ERROR = 9,             /* IoError                 errors.hpp:54 */
+    BK_EXISTS = 10,              /* ExistsError             errors.hpp:59 */
+    BK_CORRUPT_MANIFEST = 11,    /* CorruptManifestError    errors.hpp:64 */
+    BK_SIZE_MISMATCH = 12,       /* SizeMismatchError       errors.hpp:69 */
     BK_CUDA_ERROR = 20,
     BK_OOM = 21,
     BK_NO_DEVICE = 22,
@@ -300,6 +304,61 @@ bk_status bk_synth_chip(const bk_synth_spec* spec, bk_grid* grid_out, double* dz
 bk_status bk_synth_chip_device(bk_ctx* ctx, const bk_synth_spec* spec, bk_grid* grid_out,
                                double* dz_out, int* has_dz, bk_face bc_out[6], double* k_dev,
                                double* Qbasis_dev, double* C);
+
+/* ---- dataset sink and validation (dataset_io.hpp) ---------------------------- */
+
+/* field_digest(f)   discretize.hpp:99, discretize.cpp:302-319: FNV-1a over
+ * (nx, ny, nz) then the raw little-endian value bytes. Host pointer. */
+uint64_t bk_field_digest(int nx, int ny, int nz, const double* values);
+
+/* write_dataset(ds, dir, {overwrite})   dataset_io.hpp:27, dataset_io.cpp:160-225,
+ * as a streaming writer. open stages `<dir>.tmp-<pid>` next to dir (BK_EXISTS if
+ * dir already holds a manifest and !overwrite); each append adds n_samples
+ * samples: k (n, the chip's field, repeated once per sample), Q and U (n_samples
+ * x n, sample-major) to k.bin / q.bin / u.bin. Pointers may be host or device
+ * (device ones need ctx; they are drained through pinned buffers, PCIe copy
+ * overlapped with the file write). commit writes manifest.json (the caller's
+ * JSON text, same keys as dataset_io.cpp:120-142) and renames the staged
+ * directory into place. bk_dataset_close frees the writer and discards
+ * anything not committed. The writer is returned by open even on failure so
+ * bk_dataset_error can be read. */
+typedef struct bk_dataset_writer bk_dataset_writer;
+bk_status bk_dataset_open(const char* dir, int overwrite, int64_t n_cells,
+                          bk_dataset_writer** out);
+bk_status bk_dataset_append(bk_dataset_writer* w, bk_ctx* ctx, const double* k,
+                            int64_t n_samples, const double* Q, const double* U);
+bk_status bk_dataset_commit(bk_dataset_writer* w, const char* manifest_json);
+void bk_dataset_close(bk_dataset_writer* w);
+const char* bk_dataset_error(const bk_dataset_writer* w);
+int64_t bk_dataset_count(const bk_dataset_writer* w);
+double bk_dataset_write_seconds(const bk_dataset_writer* w);
+
+/* relative_residual(op, u, q)   discretize.hpp:91, discretize.cpp:275-286, for
+ * N samples: resid[j] = ||V Q_j + g - A U_j|| / ||V Q_j + g|| (0 or +inf when
+ * the denominator is 0). U, Q: N x n sample-major, host (e.g. a memory-mapped
+ * file; streamed through pinned buffers) or device; resid host or device. */
+bk_status bk_residuals(bk_ctx* ctx, const bk_operator* op, const double* U, const double* Q,
+                       int64_t N, double* resid);
+
+/* ValidationReport (dataset_io.hpp:36-41) */
+typedef struct {
+    int64_t pass_count;
+    int64_t fail_count;
+    double max_residual;
+} bk_validation;
+
+/* The sample loop of validate_dataset(dir, tol)   dataset_io.cpp:328-361, over
+ * a dataset already read (read_dataset is host I/O): K, U, Q are n_data x n
+ * (K host; U, Q host or device), ids the per-sample floorplan ids, (decl_ids,
+ * decl_digests) the manifest's floorplan_digests. A sample whose k digest
+ * contradicts its declared digest gets residual +inf and fails; the others are
+ * checked against one operator per distinct k, assembled on the GPU from grid
+ * and bc. residuals: n_data host values. */
+bk_status bk_validate_samples(bk_ctx* ctx, const bk_grid* grid, const bk_face bc[6],
+                              const double* K, const double* U, const double* Q, int64_t n_data,
+                              const uint64_t* ids, int n_decl, const uint64_t* decl_ids,
+                              const uint64_t* decl_digests, double tol, double* residuals,
+                              bk_validation* report);
 
 #ifdef __cplusplus
 }

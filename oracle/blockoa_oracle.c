@@ -27,6 +27,7 @@
  *                       operator_action pipeline.cpp:242-251 +
  *                       relative_residual discretize.cpp:275-286
  *   orc_rng_*           Rng / derive_seed rng.hpp:14-63, rng.cpp:8-60
+ *   orc_field_digest    field_digest discretize.cpp:302-319
  *
  * Floating point: built with -ffp-contract=off; the places where the reference
  * build (g++ -O3, default -ffp-contract=fast) contracts `acc += a*b` are written
@@ -359,17 +360,37 @@ void orc_power_from_rhs(const orc_op* op, const double* b, double* q) {
     for (int64_t i = 0; i < op->n; ++i) q[i] = (b[i] - op->g[i]) / op->vol[i];
 }
 
+/* field_digest (discretize.cpp:302-319): FNV-1a 64 over nx, ny, nz (8 LE
+ * bytes each) then every value's raw bits, low byte first. */
+uint64_t orc_field_digest(int nx, int ny, int nz, const double* v) {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    const uint64_t dims[3] = {(uint64_t)nx, (uint64_t)ny, (uint64_t)nz};
+    const int64_t n = (int64_t)nx * ny * nz;
+    for (int64_t w = 0; w < n + 3; ++w) {
+        uint64_t word;
+        if (w < 3)
+            word = dims[w];
+        else
+            memcpy(&word, v + (w - 3), 8);
+        for (int b = 0; b < 8; ++b) {
+            h ^= (word >> (8 * b)) & 0xffu;
+            h *= 0x100000001b3ULL;
+        }
+    }
+    return h;
+}
+
 /* ||A u - (V q + g)|| / ||V q + g||  (discretize.cpp:275-286) */
 double orc_relative_residual(const orc_op* op, const double* u, const double* q) {
     double nb = 0.0, nr = 0.0;
     for (int64_t i = 0; i < op->n; ++i) {
         double acc = 0.0;
         for (int64_t p = op->row_ptr[i]; p < op->row_ptr[i + 1]; ++p)
-            acc += op->val[p] * u[op->col[p]];
+            acc = fma(op->val[p], u[op->col[p]], acc); /* contracted, as the reference build */
         const double b = fma(op->vol[i], q[i], op->g[i]);
         const double r = b - acc;
-        nb += b * b;
-        nr += r * r;
+        nb = fma(b, b, nb); /* norm2, discretize.cpp:269-273 */
+        nr = fma(r, r, nr);
     }
     nb = sqrt(nb);
     nr = sqrt(nr);

@@ -132,6 +132,12 @@ class _Base:
         f.restype = C.c_double
         return float(f(op.handle, _ptr(u), _ptr(q)))
 
+    def field_digest(self, dims, values):
+        f = self._f("field_digest")
+        f.restype = C.c_uint64
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        return int(f(C.c_int(dims[0]), C.c_int(dims[1]), C.c_int(dims[2]), _ptr(v)))
+
     def cg_error_bound(self, kappa, m, e0):
         f = self._f("cg_error_bound")
         f.restype = C.c_double
@@ -373,3 +379,53 @@ class Reference(_Base):
         out = np.empty(n, np.uint64)
         self.lib.ref_rng_below(C.c_uint64(seed), C.c_uint64(bound), C.c_longlong(n), _ptr(out))
         return out
+
+    # ---- dataset I/O (dataset_io.hpp) ----------------------------------------
+    def write_dataset(self, dir, grid, bc, k, q, u, ids, method="blockoa", master_seed=0,
+                      tol_claimed=1e-12, tool_version="blockoa-0.1.0", digests=(),
+                      timings=(0.0, 0.0, 0.0, 0.0, 0.0), counters=(0, 0), requested=None,
+                      dropped=0, overwrite=False):
+        """Reference write_dataset (dataset_io.cpp:160-225) of n_data samples
+        given as n_data x n arrays; returns the status code (0 = ok)."""
+        nx, ny, nz, lx, ly, lz = grid
+        kind, a, b = _bc_arrays(bc)
+        k, q, u = (np.ascontiguousarray(x, dtype=np.float64) for x in (k, q, u))
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        did = np.ascontiguousarray([d[0] for d in digests], dtype=np.uint64)
+        dig = np.ascontiguousarray([d[1] for d in digests], dtype=np.uint64)
+        tim = np.ascontiguousarray(timings, dtype=np.float64)
+        cnt = np.ascontiguousarray(counters, dtype=np.int64)
+        n_data = ids.size
+        return int(self.lib.ref_write_dataset(
+            str(dir).encode(), C.c_int(int(overwrite)), C.c_int(nx), C.c_int(ny), C.c_int(nz),
+            C.c_double(lx), C.c_double(ly), C.c_double(lz), _ptr(kind), _ptr(a), _ptr(b),
+            C.c_longlong(n_data), _ptr(k), _ptr(q), _ptr(u), _ptr(ids), method.encode(),
+            C.c_ulonglong(master_seed), C.c_double(tol_claimed), tool_version.encode(),
+            C.c_int(did.size), _ptr(did), _ptr(dig), _ptr(tim), _ptr(cnt),
+            C.c_longlong(n_data if requested is None else requested), C.c_longlong(dropped)))
+
+    def read_dataset(self, dir):
+        """Reference read_dataset: (status, dims, extent, k, q, u, ids)."""
+        nd = C.c_longlong(0)
+        dims = np.zeros(3, np.int32)
+        ext = np.zeros(3, np.float64)
+        st = int(self.lib.ref_read_dataset(str(dir).encode(), C.byref(nd), _ptr(dims), _ptr(ext),
+                                           None, None, None, None))
+        if st:
+            return st, None, None, None, None, None, None
+        n = int(dims.prod())
+        k = np.empty((nd.value, n)); q = np.empty((nd.value, n)); u = np.empty((nd.value, n))
+        ids = np.empty(nd.value, np.uint64)
+        st = int(self.lib.ref_read_dataset(str(dir).encode(), C.byref(nd), _ptr(dims), _ptr(ext),
+                                           _ptr(k), _ptr(q), _ptr(u), _ptr(ids)))
+        return st, tuple(int(d) for d in dims), tuple(float(e) for e in ext), k, q, u, ids
+
+    def validate_dataset(self, dir, tol, cap=1 << 20):
+        """Reference validate_dataset: (status, pass, fail, max_residual, residuals)."""
+        res = np.empty(cap, np.float64)
+        n, p, f = C.c_longlong(0), C.c_longlong(0), C.c_longlong(0)
+        mx = C.c_double(0)
+        st = int(self.lib.ref_validate_dataset(str(dir).encode(), C.c_double(tol), _ptr(res),
+                                               C.c_longlong(cap), C.byref(n), C.byref(p),
+                                               C.byref(f), C.byref(mx)))
+        return st, p.value, f.value, mx.value, res[:n.value].copy()

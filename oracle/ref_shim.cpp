@@ -16,6 +16,9 @@
 //   combine_from_weights   pipeline.hpp:85    (pipeline.cpp:187-225)
 //   operator_action        pipeline.hpp:95    (pipeline.cpp:242-251)
 //   Rng / derive_seed      rng.hpp:14-63      (rng.cpp)
+//   field_digest           discretize.hpp:99  (discretize.cpp:302-319)
+//   write_dataset / read_dataset / validate_dataset
+//                          dataset_io.hpp:27-47 (dataset_io.cpp:160-361)
 // Exceptions are mapped to the status codes of include/blockoa_b200.h.
 
 #include <cstdint>
@@ -25,6 +28,8 @@
 #include <string>
 #include <vector>
 
+#include "blockoa/dataset.hpp"
+#include "blockoa/dataset_io.hpp"
 #include "blockoa/discretize.hpp"
 #include "blockoa/errors.hpp"
 #include "blockoa/parallel.hpp"
@@ -65,6 +70,18 @@ int map_exception() {
     } catch (const InvalidKappaError& e) {
         g_err = e.what();
         return 8;
+    } catch (const ExistsError& e) {
+        g_err = e.what();
+        return 10;
+    } catch (const CorruptManifestError& e) {
+        g_err = e.what();
+        return 11;
+    } catch (const SizeMismatchError& e) {
+        g_err = e.what();
+        return 12;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return 9;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 99;
@@ -349,6 +366,110 @@ void ref_rng_below(unsigned long long seed, unsigned long long bound, long long 
                    unsigned long long* out) {
     Rng r(seed);
     for (long long i = 0; i < n; ++i) out[i] = r.below(bound);
+}
+
+// ---- dataset I/O (dataset_io.hpp) --------------------------------------------
+unsigned long long ref_field_digest(int nx, int ny, int nz, const double* values) {
+    GridSpec grid{nx, ny, nz, 1.0, 1.0, 1.0};
+    ScalarField f{grid, Unit::conductivity_w_per_m_k,
+                  std::vector<double>(values, values + grid.cell_count())};
+    return field_digest(f);
+}
+
+// Dataset from flat sample-major arrays (n_data x n each); timings =
+// {basis_solve_s, combine_s, operator_action_s, solve_s, total_s},
+// counters = {iterations_total, matvecs_total}.
+int ref_write_dataset(const char* dir, int overwrite, int nx, int ny, int nz, double lx,
+                      double ly, double lz, const int* bc_kind, const double* bc_a,
+                      const double* bc_b, long long n_data, const double* k, const double* q,
+                      const double* u, const unsigned long long* ids, const char* method,
+                      unsigned long long master_seed, double tol_claimed,
+                      const char* tool_version, int n_dig, const unsigned long long* dig_ids,
+                      const unsigned long long* digs, const double* timings,
+                      const long long* counters, long long requested, long long dropped) {
+    try {
+        Dataset ds;
+        ds.grid = GridSpec{nx, ny, nz, lx, ly, lz};
+        ds.bc = make_bc(bc_kind, bc_a, bc_b);
+        const std::int64_t n = ds.grid.cell_count();
+        ds.samples.resize(static_cast<std::size_t>(n_data));
+        for (long long j = 0; j < n_data; ++j) {
+            Sample& s = ds.samples[static_cast<std::size_t>(j)];
+            s.floorplan_id = ids[j];
+            s.k = ScalarField{ds.grid, Unit::conductivity_w_per_m_k,
+                              std::vector<double>(k + j * n, k + (j + 1) * n)};
+            s.q = ScalarField{ds.grid, Unit::power_density_w_per_m3,
+                              std::vector<double>(q + j * n, q + (j + 1) * n)};
+            s.u = ScalarField{ds.grid, Unit::temperature_c,
+                              std::vector<double>(u + j * n, u + (j + 1) * n)};
+        }
+        DatasetManifest& m = ds.manifest;
+        m.method = method;
+        m.n_data = n_data;
+        m.master_seed = master_seed;
+        for (long long j = 0; j < n_data; ++j) m.floorplan_ids.push_back(ids[j]);
+        for (int d = 0; d < n_dig; ++d) m.floorplan_digests.emplace_back(dig_ids[d], digs[d]);
+        m.timings.basis_solve_s = timings[0];
+        m.timings.combine_s = timings[1];
+        m.timings.operator_action_s = timings[2];
+        m.timings.solve_s = timings[3];
+        m.timings.total_s = timings[4];
+        m.timings.iterations_total = counters[0];
+        m.timings.matvecs_total = counters[1];
+        m.residual_tol_claimed = tol_claimed;
+        m.tool_version = tool_version;
+        m.requested_n_data = requested;
+        m.dropped_count = dropped;
+        WriteOptions opts;
+        opts.overwrite = overwrite != 0;
+        write_dataset(ds, dir, opts);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// read_dataset: call once with k == nullptr to get *n_data and dims/extent,
+// then again with arrays of n_data x n (k, q, u) and n_data ids.
+int ref_read_dataset(const char* dir, long long* n_data, int* dims, double* extent, double* k,
+                     double* q, double* u, unsigned long long* ids) {
+    try {
+        const Dataset ds = read_dataset(dir);
+        *n_data = static_cast<long long>(ds.samples.size());
+        dims[0] = ds.grid.nx;
+        dims[1] = ds.grid.ny;
+        dims[2] = ds.grid.nz;
+        extent[0] = ds.grid.lx;
+        extent[1] = ds.grid.ly;
+        extent[2] = ds.grid.lz;
+        if (!k) return 0;
+        const std::int64_t n = ds.grid.cell_count();
+        for (std::size_t j = 0; j < ds.samples.size(); ++j) {
+            std::memcpy(k + j * n, ds.samples[j].k.values.data(), n * sizeof(double));
+            std::memcpy(q + j * n, ds.samples[j].q.values.data(), n * sizeof(double));
+            std::memcpy(u + j * n, ds.samples[j].u.values.data(), n * sizeof(double));
+            ids[j] = ds.samples[j].floorplan_id;
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+int ref_validate_dataset(const char* dir, double tol, double* residuals, long long cap,
+                         long long* n_out, long long* pass, long long* fail, double* max_res) {
+    try {
+        const ValidationReport r = validate_dataset(dir, tol);
+        *n_out = static_cast<long long>(r.residuals.size());
+        for (std::size_t j = 0; j < r.residuals.size() && static_cast<long long>(j) < cap; ++j)
+            residuals[j] = r.residuals[j];
+        *pass = r.pass_count;
+        *fail = r.fail_count;
+        *max_res = r.max_residual;
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
 }
 
 }  // extern "C"

@@ -22,6 +22,7 @@ this module                 reference
 ``generate_chip``           ``generate_blockoa`` for one basis group
                             pipeline.cpp:365-597
 ``cg_error_bound``          ``cg_error_bound`` solvers.cpp:672-680
+``write_dataset`` ...       dataset_io.hpp (see paper_2510_23221_b200/dataset.py)
 exceptions                  errors.hpp:9-71
 ==========================  ==================================================
 
@@ -44,9 +45,13 @@ __all__ = [
     "assemble", "operator_from_csr", "block_cg", "combine_action", "generate_chip", "generate_batch", "rhs_from_power",
     "power_from_rhs", "cg_error_bound", "derive_seed", "synth_chip", "synth_chip_device",
     "library_path",
+    "Dataset", "DatasetManifest", "DatasetWriter", "ManifestTimings", "ValidationReport",
+    "WriteSummary", "field_digest", "read_dataset", "relative_residual", "validate_dataset",
+    "write_dataset",
     "Error", "InvalidSpecError", "InvalidConfigError", "DimensionMismatchError",
     "NonPositiveConductivityError", "NonPositiveHtcError", "EmptyBasisError",
-    "NotConvergedError", "InvalidKappaError", "DeviceError",
+    "NotConvergedError", "InvalidKappaError", "IoError", "ExistsError",
+    "CorruptManifestError", "SizeMismatchError", "DeviceError",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -70,6 +75,10 @@ class NonPositiveHtcError(Error): ...
 class EmptyBasisError(Error): ...
 class NotConvergedError(Error): ...
 class InvalidKappaError(Error): ...
+class IoError(Error): ...
+class ExistsError(IoError): ...
+class CorruptManifestError(IoError): ...
+class SizeMismatchError(IoError): ...
 class DeviceError(Error):
     """CUDA failure, out of device memory, or no usable sm_100 device."""
 
@@ -77,7 +86,8 @@ class DeviceError(Error):
 _STATUS = {
     1: InvalidSpecError, 2: InvalidConfigError, 3: DimensionMismatchError,
     4: NonPositiveConductivityError, 5: NonPositiveHtcError, 6: EmptyBasisError,
-    7: NotConvergedError, 8: InvalidKappaError, 20: DeviceError, 21: DeviceError,
+    7: NotConvergedError, 8: InvalidKappaError, 9: IoError, 10: ExistsError,
+    11: CorruptManifestError, 12: SizeMismatchError, 20: DeviceError, 21: DeviceError,
     22: DeviceError, 99: Error,
 }
 
@@ -171,6 +181,22 @@ def _load():
                                       C.POINTER(_Face), dp, dp, dp]
         lib.bk_synth_chip_device.argtypes = [vp, C.POINTER(_Synth), C.POINTER(_Grid), dp,
                                              C.POINTER(C.c_int), C.POINTER(_Face), dp, dp, dp]
+        lib.bk_field_digest.argtypes = [C.c_int, C.c_int, C.c_int, vp]
+        lib.bk_field_digest.restype = C.c_uint64
+        lib.bk_dataset_open.argtypes = [C.c_char_p, C.c_int, C.c_int64, vp]
+        lib.bk_dataset_append.argtypes = [vp, vp, vp, C.c_int64, vp, vp]
+        lib.bk_dataset_commit.argtypes = [vp, C.c_char_p]
+        lib.bk_dataset_close.argtypes = [vp]
+        lib.bk_dataset_close.restype = None
+        lib.bk_dataset_error.argtypes = [vp]
+        lib.bk_dataset_error.restype = C.c_char_p
+        lib.bk_dataset_count.argtypes = [vp]
+        lib.bk_dataset_count.restype = C.c_int64
+        lib.bk_dataset_write_seconds.argtypes = [vp]
+        lib.bk_dataset_write_seconds.restype = C.c_double
+        lib.bk_residuals.argtypes = [vp, vp, vp, vp, C.c_int64, vp]
+        lib.bk_validate_samples.argtypes = [vp, C.POINTER(_Grid), C.POINTER(_Face), vp, vp, vp,
+                                            C.c_int64, vp, C.c_int, vp, vp, C.c_double, vp, vp]
         lib.bk_abi_version.restype = C.c_int
         _lib = lib
     return _lib
@@ -767,3 +793,9 @@ CONFIGS = {
     5: (5, 512, 512, 16, 64, 5000),
 }
 C4_CHIPS = 5000
+
+
+# dataset sink / validation (dataset_io.hpp) — imported last: it builds on the above
+from .dataset import (Dataset, DatasetManifest, DatasetWriter, ManifestTimings,  # noqa: E402
+                      ValidationReport, WriteSummary, field_digest, read_dataset,
+                      relative_residual, validate_dataset, write_dataset)

@@ -543,6 +543,10 @@ void bk_destroy(bk_ctx* ctx) {
         delete v;
     }
     if (ctx->hmap) cudaFreeHost(ctx->hmap);
+    for (void* p : ctx->pin)
+        if (p) cudaFreeHost(p);
+    for (auto& e : ctx->stage_ev)
+        if (e) cudaEventDestroy(e);
     cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }

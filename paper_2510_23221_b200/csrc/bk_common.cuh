@@ -39,6 +39,9 @@ struct bk_ctx {
     void* hmap = nullptr;                  // mapped pinned host page for small readbacks
     void* hmap_dev = nullptr;
     bool drain_pending[2] = {};
+    void* pin[2] = {};                     // pinned staging of the dataset writer / validator
+    size_t pin_bytes = 0;
+    cudaEvent_t stage_ev[4] = {};
     // grow-only device workspace slots
     static constexpr int kSlots = 32;
     void* ws[kSlots] = {};
@@ -98,9 +101,13 @@ enum Slot : int {
     kSlotCgFlags,   // phase timestamps of a profiled batched solve
     kSlotStackDiag, // z-stacked operator of the batched pipeline (6 arrays)
     kSlotStackCoef, // per-chip combination coefficients of the batched pipeline
+    kSlotValRes,    // per-sample residuals of bk_residuals / bk_validate_samples
 };
 
 bk_status fail(bk_ctx* ctx, bk_status st, const std::string& msg);
+// relative_residual for N samples (U, Q: N x n device); resid device, N values
+bk_status residuals_device(bk_ctx* ctx, const bk_operator* op, const double* U, const double* Q,
+                           int64_t N, double* resid);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when `f` needs more
 // than it was already given (once per function and device in steady state):
 // the attribute is not rewritten while other streams run the same kernel.
