@@ -386,11 +386,11 @@ double orc_relative_residual(const orc_op* op, const double* u, const double* q)
     for (int64_t i = 0; i < op->n; ++i) {
         double acc = 0.0;
         for (int64_t p = op->row_ptr[i]; p < op->row_ptr[i + 1]; ++p)
-            acc = fma(op->val[p], u[op->col[p]], acc); /* contracted, as the reference build */
+            acc += op->val[p] * u[op->col[p]]; /* CsrMatrix::apply: not contracted in the reference build */
         const double b = fma(op->vol[i], q[i], op->g[i]);
         const double r = b - acc;
-        nb = fma(b, b, nb); /* norm2, discretize.cpp:269-273 */
-        nr = fma(r, r, nr);
+        nb += b * b; /* norm2, discretize.cpp:269-273 */
+        nr += r * r;
     }
     nb = sqrt(nb);
     nr = sqrt(nr);

@@ -53,10 +53,14 @@ struct ResArgs {
 
 // CTA (tile, sample group): each thread owns kResCellsPerThread cells, loads
 // their stencil row once and applies it to kResSamples samples. Per cell the
-// arithmetic is the reference's: b = fma(V, q, g) (rhs_from_power, contracted)
-// and A u as the CSR-order FMA chain z-, y-, x-, diag, x+, y+, z+
-// (CsrMatrix::apply, discretize.cpp:39-51), so r_i = b_i - (A u)_i is bitwise
-// the reference's; only the two sums are reordered (fixed tree, deterministic).
+// arithmetic is the reference build's: b = fma(V, q, g) (rhs_from_power,
+// contracted) and A u in CSR order z-, y-, x-, diag, x+, y+, z+ as separate
+// multiply and add (CsrMatrix::apply, discretize.cpp:39-51, is not contracted
+// by the reference build), so r_i = b_i - (A u)_i is bitwise the reference's.
+// This matters: validated samples have residuals ~1e-17 only because A u is
+// recomputed exactly as the generator computed it — another summation order
+// leaves ~1e-13 of cancellation noise. Only the two norms are reordered (fixed
+// tree, deterministic).
 __global__ void __launch_bounds__(kResThreads) residual_kernel(ResArgs a) {
     const int tile = blockIdx.x;
     const int64_t j0 = (int64_t)blockIdx.y * kResSamples;
@@ -85,13 +89,13 @@ __global__ void __launch_bounds__(kResThreads) residual_kernel(ResArgs a) {
             if (j < ns) {
                 const double* u = a.U + (j0 + j) * a.n + i;
                 double acc = 0.0;
-                if (iz > 0) acc = fma(czm, u[-plane], acc);
-                if (iy > 0) acc = fma(cym, u[-a.nx], acc);
-                if (ix > 0) acc = fma(cxm, u[-1], acc);
-                acc = fma(dg, u[0], acc);
-                if (ix < a.nx - 1) acc = fma(cxp, u[1], acc);
-                if (iy < a.ny - 1) acc = fma(cyp, u[a.nx], acc);
-                if (iz < a.nz - 1) acc = fma(czp, u[plane], acc);
+                if (iz > 0) acc = __dadd_rn(acc, __dmul_rn(czm, u[-plane]));
+                if (iy > 0) acc = __dadd_rn(acc, __dmul_rn(cym, u[-a.nx]));
+                if (ix > 0) acc = __dadd_rn(acc, __dmul_rn(cxm, u[-1]));
+                acc = __dadd_rn(acc, __dmul_rn(dg, u[0]));
+                if (ix < a.nx - 1) acc = __dadd_rn(acc, __dmul_rn(cxp, u[1]));
+                if (iy < a.ny - 1) acc = __dadd_rn(acc, __dmul_rn(cyp, u[a.nx]));
+                if (iz < a.nz - 1) acc = __dadd_rn(acc, __dmul_rn(czp, u[plane]));
                 const double b = fma(vi, a.Q[(j0 + j) * a.n + i], gi);
                 const double r = b - acc;
                 nu[j] = fma(r, r, nu[j]);

@@ -66,6 +66,20 @@ def test_field_digest_bit_exact(bk, oracle, reference):
     assert bk.field_digest(v, bk.GridSpec(3, 4, 1)) != bk.field_digest(v, bk.GridSpec(4, 3, 1))
 
 
+def test_oracle_relative_residual_bit_exact(oracle, reference):
+    # pins the rounding the GPU residual kernel must reproduce per cell:
+    # CsrMatrix::apply and norm2 uncontracted, rhs_from_power contracted
+    rng = np.random.default_rng(9)
+    grid = (20, 16, 3, 0.01, 0.008, 0.001)
+    bc = [(0, 20.0, 0.0), (2, 0.0, 0.0), (1, 50.0, 25.0), (2, 0.0, 0.0), (2, 0.0, 0.0),
+          (1, 1e3, 25.0)]
+    k = rng.uniform(1.0, 400.0, 960)
+    oo, rr = oracle.assemble(grid, k, bc), reference.assemble(grid, k, bc)
+    for _ in range(20):
+        u, q = rng.uniform(20.0, 90.0, 960), rng.uniform(0.0, 1e6, 960)
+        assert oracle.relative_residual(oo, u, q) == reference.relative_residual(rr, u, q)
+
+
 def test_writer_byte_identical_to_reference(bk, reference, tmp_path):
     grid = bk.GridSpec(12, 9, 3, 0.012, 0.009, 0.00045)
     k, q, u, ids = _samples(grid, 7)
@@ -243,7 +257,7 @@ def test_generated_chip_to_dataset_validates(bk, ctx, reference, tmp_path):
     import torch
 
     ins = _c1_chip(bk)
-    cfg = bk.SolverConfig(1e-12, 100000, True)
+    cfg = bk.SolverConfig(1e-12, 100000, "jacobi")
     n, N = ins.grid.cell_count(), ins.coef.shape[1]
     T = torch.empty((N, n), dtype=torch.float64, device="cuda")
     Q = torch.empty_like(T)
