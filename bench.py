@@ -504,6 +504,11 @@ def run_ours(args):
     same = all(torch.equal(T_h[i], Td_h) and torch.equal(Q_h[i], Qd_h) for i in range(e2e_steps))
     del T_h, Q_h, R_h
 
+    peak, peak_kind = peaks()
+    dataset = None
+    if rank == 0 and not args.no_dataset:
+        dataset = dataset_leg(bk, torch, ctx, stream, inp, k_d, T_d, Q_d, R_d, peak)
+
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
@@ -514,7 +519,6 @@ def run_ours(args):
     bytes_per_iter = n * (40 + 80 * s)
     mean_iters = float(np.mean(iters))
     achieved = mean_iters * bytes_per_iter / float(np.mean(solve_s)) / 1e9
-    peak, peak_kind = peaks()
     traffic = ncu_traffic(args.config)
 
     cpu = None
@@ -562,12 +566,71 @@ def run_ours(args):
         "phase_ms": {"solve": float(np.mean(solve_s)) * 1e3},
         "max_sample_residual": max_resid,
         "direct_cg_baseline": direct,
+        "dataset": dataset,
     }
     print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def dataset_leg(bk, torch, ctx, stream, inp, k_d, T_d, Q_d, R_d, peak):
+    """(1) the GPU validation kernel (relative_residual of every
+    sample, bk_residuals) over the chip's N device-resident samples, vs the HBM
+    roofline; (2) the dataset sink — a bounded subset of the chip drained from
+    HBM into k.bin/q.bin/u.bin + manifest by DatasetWriter; (3)
+    validate_dataset of that subset read back from the files."""
+    import shutil
+    import tempfile
+    import time
+
+    N, n = int(T_d.shape[0]), int(T_d.shape[1])
+    op = bk.assemble(k_d, inp.grid, inp.bc, ctx)
+    rv = torch.empty(N, dtype=torch.float64, device=T_d.device)
+    bk.relative_residual(op, T_d, Q_d, out=rv)
+    torch.cuda.synchronize()
+    reps = 3
+    v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    v0.record(stream)
+    for _ in range(reps):
+        bk.relative_residual(op, T_d, Q_d, out=rv)
+    v1.record(stream)
+    torch.cuda.synchronize()
+    vt = v0.elapsed_time(v1) * 1e-3 / reps
+    alg = 16 * n * N + 40 * n  # u, q per sample + diag, cx, cy, cz, g once
+    rel = ((rv - R_d).abs() / R_d.abs().clamp_min(1e-300)).max().item()
+
+    M = min(N, 512)
+    tmp = tempfile.mkdtemp(prefix="bk_bench_ds_")
+    d = os.path.join(tmp, "ds")
+    try:
+        t0 = time.perf_counter()
+        with bk.DatasetWriter(d, inp.grid, inp.bc, master_seed=1, ctx=ctx) as w:
+            w.append(k_d, Q_d[:M], T_d[:M], 0)
+            wsec = w.write_seconds
+            w.commit()
+        sink_s = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        rep = bk.validate_dataset(d, 1e-12, ctx)
+        val_s = time.perf_counter() - t0
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+    return {
+        "validate_kernel": {"value": N / vt, "unit": "samples/s", "ms": vt * 1e3,
+                            "achieved": alg / vt / 1e9, "peak": peak, "unit_bw": "GB/s",
+                            "frac": alg / vt / 1e9 / peak, "algorithmic_bytes": alg,
+                            "max_rel_diff_vs_pipeline_residual": rel,
+                            "max_residual": float(rv.max().item()),
+                            "kernel": "residual_kernel (bk_residuals, device inputs)"},
+        "sink": {"samples": M, "value": M / sink_s, "unit": "samples/s",
+                 "gb_per_s": 3 * M * n * 8 / sink_s / 1e9, "write_syscall_s": wsec,
+                 "seconds": sink_s,
+                 "path": "DatasetWriter.append(device tensors) + commit -> local /tmp"},
+        "validate_from_files": {"samples": M, "value": M / val_s, "unit": "samples/s",
+                                "seconds": val_s, "pass": rep.pass_count,
+                                "fail": rep.fail_count, "max_residual": rep.max_residual},
+    }
 
 
 def _finish(args, world, rank, line):
@@ -788,6 +851,8 @@ def main():
     ap.add_argument("--chips", type=int, default=0,
                     help="concurrent chips per GPU per step (configs 1-3; 0 = default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dataset", action="store_true",
+                    help="skip the dataset sink / validation leg (SURVEY 8(f2))")
     ap.add_argument("--no-direct", action="store_true",
                     help="skip the per-sample CG (direct) baseline")
     ap.add_argument("--ref-iter-cap", type=int, default=24)

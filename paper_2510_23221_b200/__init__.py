@@ -55,7 +55,9 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libblockoa_b200.so")
+# BK_LIBRARY: an alternative in-tree build of the same library (A/B timing of
+# kernel variants); default the package's own libblockoa_b200.so
+LIB_PATH = os.environ.get("BK_LIBRARY") or os.path.join(HERE, "libblockoa_b200.so")
 
 
 def library_path() -> str:

@@ -39,7 +39,7 @@ namespace {
 constexpr int kResThreads = 256;
 constexpr int kResCellsPerThread = 4;
 constexpr int kResTile = kResThreads * kResCellsPerThread;  // cells per CTA
-constexpr int kResSamples = 8;                              // samples per CTA
+constexpr int kResSamples = 4;                              // samples per CTA (4 beat 1, 2, 8, 16 on B200)
 
 struct ResArgs {
     int nx, ny, nz;
