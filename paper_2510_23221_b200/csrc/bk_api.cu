@@ -320,11 +320,7 @@ bk_status generate_chip_impl(bk_ctx* ctx, const bk_grid* grid, const double* k,
         // drain each chunk on the copy stream while the next one is computed
         // (D2H of T, q — 16 n bytes per sample over PCIe — is the largest
         // cost of a host-memory call)
-        if (!ctx->copy_stream) {
-            BK_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-            for (auto& e : ctx->drain_ev)
-                BK_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        }
+        if ((st = ensure_copy_stream(ctx)) != BK_OK) return st;
         const int64_t per = std::max<int64_t>(16, ((int64_t)(64 << 20) / (16 * n)) / 16 * 16);
         const int64_t nch = (N + per - 1) / per;
         while ((int64_t)ctx->chunk_ev.size() < nch) {

@@ -114,6 +114,7 @@ bk_status residuals_device(bk_ctx* ctx, const bk_operator* op, const double* U, 
 cudaError_t set_max_smem(const void* f, size_t bytes);
 // Grow-only workspace; contents are not preserved on growth.
 bk_status workspace(bk_ctx* ctx, int slot, size_t bytes, void** out);
+bk_status ensure_copy_stream(bk_ctx* ctx);
 bool is_device_ptr(const void* p);
 // Copy a few bytes device -> host through a kernel writing mapped pinned
 // memory (no copy engine: it never queues behind a large in-flight D2H drain)

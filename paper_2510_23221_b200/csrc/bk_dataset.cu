@@ -156,14 +156,6 @@ __global__ void residual_finalize(const double* __restrict__ part, int tiles, in
     }
 }
 
-bk_status ensure_copy_stream(bk_ctx* ctx) {
-    if (!ctx->copy_stream)
-        BK_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-    for (auto& e : ctx->stage_ev)
-        if (!e) BK_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    return BK_OK;
-}
-
 // two pinned staging buffers of `bytes` each (grow-only, owned by ctx)
 bk_status ensure_pinned(bk_ctx* ctx, size_t bytes) {
     if (ctx->pin_bytes >= bytes) return BK_OK;
@@ -185,6 +177,19 @@ constexpr size_t kStageBytes = size_t(128) << 20;  // per pinned buffer
 }  // namespace
 
 namespace bk {
+
+// the copy stream and every event that orders work on it (created together:
+// the chip drain and the dataset sink both rely on them)
+bk_status ensure_copy_stream(bk_ctx* ctx) {
+    if (!ctx->copy_stream)
+        BK_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->stage_ev)
+        if (!e) BK_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : ctx->drain_ev)
+        if (!e) BK_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return BK_OK;
+}
+
 
 // resid (device, N) for device U, Q (N x n each)
 bk_status residuals_device(bk_ctx* ctx, const bk_operator* op, const double* U, const double* Q,
