@@ -4,20 +4,36 @@
 //   q_j = (A T_j - g) / V             operator_action       pipeline.cpp:242-251
 //   resid_j = ||A T_j - (V q_j + g)|| / ||V q_j + g||       pipeline.cpp:548-571
 //
-// Each CTA owns a 32 x 8 x-y tile of cells (all z, marched plane by plane,
-// 2.5D blocking) and a chunk of NS samples. A plane of T for the tile plus a
-// one-cell x-y halo is formed in shared memory straight from X (L2-resident,
-// n x s) and the coefficients; the stencil is then applied to the smem tile and
-// T and q leave the SM exactly once, sample-major. A ring of three planes
-// supplies the z-1 / z+1 neighbours. No T round trip through HBM, no second
-// pass for q.
+// Work item = (32 x 8 x-y tile of cells, all z, chunk of NS samples).
+// Persistent CTAs (two per SM) walk their items; for each z-plane
+// the tile's X rows plus a one-cell x-y halo (34 x 10 cells) arrive by TMA:
+// one 4D tensor-map copy per 16-column panel (box 16 x 34 x 10 x 1, 128-byte
+// swizzle, out-of-domain halo cells zero-filled by the copy engine) into a
+// mbarrier-tracked slot that the producer refills as soon as it is consumed,
+// running ahead across planes and items. T for the
+// halo plane is formed from the swizzled panels on the FP64 tensor cores
+// (m16n8k4 DMMA: M = halo cells, N = samples, K = basis columns) into a ring
+// of three T planes; the 7-point stencil is then applied from shared memory
+// (2.5D march: the ring supplies z - 1 / z + 1), and T and q leave the SM
+// exactly once, sample-major, with streaming stores. No T round trip through
+// HBM, no second pass for q.
+//
+// Why this shape (ncu, profiles/): the previous kernel read the DMMA A
+// fragments (8 bytes per lane, 8 rows per instruction) straight from L2; the
+// L1 data pipe spent one wavefront per 32-byte sector and ran at 94 % busy,
+// 58 % of it on X. TMA moves X without L1 wavefronts; each swizzled fragment
+// load is two wavefronts per 256 bytes (conflict free).
 //
 // Bitwise contract: T uses the reference's per-element order (first term a
 // product, then one fma per basis column in ascending order — the DMMA's
-// accumulation order, verified bitwise); A T uses the
-// scalar CsrMatrix::apply order (separate multiply and add, CSR column order);
-// q = (y - g) / V is correctly rounded. So given the same X, T and q equal the
-// reference's bit for bit (tests/test_gpu_parity.py checks it).
+// accumulation order, verified bitwise; panels and k-steps are consumed in
+// ascending column order); A T uses the scalar CsrMatrix::apply order
+// (separate multiply and add, CSR column order); q = (y - g) / V is correctly
+// rounded. So given the same X, T and q equal the reference's bit for bit
+// (tests/test_gpu_parity.py checks it).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdio>
 #include <cstdlib>
 
@@ -25,8 +41,35 @@
 
 namespace {
 
-constexpr int TX = 32, TY = 8, HX = TX + 2, HY = TY + 2, HC = HX * HY;
-constexpr int NT = 256;  // = TX * TY: one interior cell per thread in the stencil phase
+constexpr int TX = 32, TY = 8, HX = TX + 2, HY = TY + 2, HC = HX * HY;  // 340 halo cells
+constexpr int MT = (HC + 15) / 16;     // DMMA m-tiles per halo plane (22)
+
+// Work-item shape: NS samples per item, NT threads. NT = 512 runs one CTA per
+// SM (thread = interior cell x 8 samples, two sample halves) with two TMA
+// panel slots; NT = 256 runs two CTAs per SM (thread = interior cell x NS
+// samples) with one slot each, so one CTA's stencil overlaps the other's DMMA
+// chains.
+template <int NS, int NT_>
+struct Shape {
+    static constexpr int NT = NT_;
+    static constexpr int NW = NT / 32;
+    static constexpr int MPW = (MT + NW - 1) / NW;  // m-tiles per warp
+    static constexpr int NB = NS / 8;               // DMMA n-blocks (8 samples each)
+    static constexpr int SPT = NS * 256 / NT;       // samples per thread
+    static constexpr int NP = NT == 512 ? 2 : 1;    // TMA panel slots
+    static constexpr int CSP = NS + 4;              // row stride of C in shared memory
+    static constexpr int CTAS = NT == 512 ? 1 : 2;  // CTAs per SM
+};
+
+// A panel = PW basis columns of every halo cell of one plane (one TMA box).
+template <int S>
+struct Panel {
+    static constexpr int PW = S >= 16 ? 16 : 8;
+    static constexpr int R = S / PW;                        // panels per plane
+    static constexpr unsigned BYTES = HC * PW * 8;          // transaction bytes
+    static constexpr int SLOT = (BYTES + 1023) / 1024 * 1024;
+    static constexpr unsigned SWM = PW == 16 ? 7 : 3;       // 128- / 64-byte swizzle
+};
 
 struct ActArgs {
     int nx, ny, nz;
@@ -39,12 +82,12 @@ struct ActArgs {
     const double* cz;
     const double* g;
     const double* volz;
-    const double* X;  // n x S
     const double* C;  // S x N
     double* T;        // N x n (nullable)
     double* Q;        // N x n (nullable)
     double* part;     // N x tiles x 2 residual partials (nullable)
-    int tiles;
+    int tilesx, tiles;
+    int chunks, items;  // items = chunks x tiles < 2^31 (checked on the host)
     int s;            // real basis width (<= S)
 };
 
@@ -63,189 +106,329 @@ __device__ __forceinline__ void dmma_c(double (&d)[4], double a0, double a1, dou
         : "d"(a0), "d"(a1), "d"(b));
 }
 
-// B-fragment rows of C in shared memory: at most two lanes per 8-byte bank slot
-constexpr int CSTRIDE(int NS) { return NS == 8 ? 8 : NS + 4; }
-
-// debug: stage timestamps of CTA (0, 0) when BK_COMB_PROFILE is set
-__device__ long long g_comb_prof[64];
-__device__ __forceinline__ void comb_mark(int k) {
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && k < 64) g_comb_prof[k] = clock64();
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tCMW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra CMW_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+// 4D tiled TMA load: box (PW, 34, 10, 1) at (col, x0 - 1, y0 - 1, z)
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "r"(smem_u32(bar))
+        : "memory");
 }
 
-// T for one z-plane of the tile + halo into buf[q * HC + h] (sample-major, so
-// the stencil's neighbour reads are bank-conflict free), on FP64 tensor cores:
-// T (halo cells x NS samples) = X_rows (cells x S) . C (S x NS) as m16n8k4 DMMA
-// with M = cells, N = samples, K = basis columns. The DMMA accumulates in k
-// order with one rounding per multiply-add — measured bitwise identical to the
-// reference's fma chain (scripts/dmma_bitwise.cu: 0 of 25600 differ) — so T
-// stays bitwise the reference's combine_from_weights.
-template <int S, int NS>
-__device__ __forceinline__ void form_plane(const ActArgs& a, int x0, int y0, int z,
-                                           const double* __restrict__ Cs, double* __restrict__ buf) {
-    constexpr int CS = CSTRIDE(NS);
-    constexpr int MTILES = (HC + 15) / 16;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+// debug: stage timestamps (clock64) of CTA 0's fifth work item when
+// BK_COMB_PROFILE is set
+__device__ long long g_comb_prof[64];
+
+// the stencil coefficients of one cell (CSR values of its row)
+struct Coef {
+    double gi, di, zm, ym, xm, xp, yp, zp;
+};
+__device__ __forceinline__ void load_coef(const ActArgs& a, int gx, int gy, int z, Coef& k) {
     const int64_t plane = (int64_t)a.nx * a.ny;
-    for (int mt = warp; mt < MTILES; mt += NT / 32) {
+    const int64_t i = gx + (int64_t)a.nx * gy + plane * z;
+    k.gi = a.g[i];
+    k.di = a.diag[i];
+    k.zm = z > 0 ? -a.cz[i - plane] : 0.0;
+    k.ym = gy > 0 ? -a.cy[i - a.nx] : 0.0;
+    k.xm = gx > 0 ? -a.cx[i - 1] : 0.0;
+    k.xp = gx < a.nx - 1 ? -a.cx[i] : 0.0;
+    k.yp = gy < a.ny - 1 ? -a.cy[i] : 0.0;
+    k.zp = z < a.nz - 1 ? -a.cz[i] : 0.0;
+}
+
+// PL: single-plane grid (nz == 1), compiled without the z-ring logic
+template <int S, int NS, int NT_, bool PL>
+__global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
+    combine_action_kernel(const __grid_constant__ CUtensorMap tmx, ActArgs a) {
+    using P = Panel<S>;
+    using SH = Shape<NS, NT_>;
+    constexpr int NT = SH::NT, NW = SH::NW, MPW = SH::MPW, NB = SH::NB, NP = SH::NP, CSP = SH::CSP;
+    constexpr int SPT = SH::SPT;
+    extern __shared__ unsigned char smraw[];
+    unsigned char* panels = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
+    const int nz = PL ? 1 : a.nz;
+    const int nring = nz < 3 ? nz : 3;
+    double* ring = reinterpret_cast<double*>(panels + NP * P::SLOT);  // nring x NS x HC
+    double* Cs = ring + nring * NS * HC;                                // S x CSP
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(Cs + S * CSP);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int64_t plane = (int64_t)a.nx * a.ny;
+
+    if (tid == 0) {
+        for (int p = 0; p < NP; ++p) mbar_init(&bar[p], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // producer (thread 0): walks the panels in consumption order (item, z,
+    // column block); slot = panel index mod NP
+    int p_item = blockIdx.x, p_z = 0, p_r = 0, p_slot = 0;
+    auto issue = [&]() {
+        if (p_item >= a.items) return;
+        const int tile = p_item / a.chunks;
+        const int x0 = (tile % a.tilesx) * TX, y0 = (tile / a.tilesx) * TY;
+        mbar_expect_tx(&bar[p_slot], P::BYTES);
+        tma_load_4d(panels + p_slot * P::SLOT, &tmx, p_r * P::PW, x0 - 1, y0 - 1, p_z,
+                    &bar[p_slot]);
+        p_slot = p_slot + 1 == NP ? 0 : p_slot + 1;
+        if (++p_r == P::R) {
+            p_r = 0;
+            if (++p_z == nz) {
+                p_z = 0;
+                p_item += gridDim.x;
+            }
+        }
+    };
+    if (tid == 0)
+        for (int p = 0; p < NP; ++p) issue();
+    unsigned pc = 0;  // panels consumed (uniform across the CTA)
+    bool prof = false;
+    int pm = 0;
+    auto mark = [&]() {
+        if (prof && pm < 64) g_comb_prof[pm++] = clock64();
+    };
+
+    // DMMA accumulators of m-tile mt (all NB sample blocks) -> T ring plane buf,
+    // sample-major [q][h] (conflict-free: HC = 4 mod 8)
+    auto store_tile = [&](int mt, const double (&ac)[NB][4], double* buf) {
         const int h0 = 16 * mt + g, h1 = h0 + 8;
-        const double* xr[2];
-        bool in[2];
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int h = r ? h1 : h0;
-            const int gx = x0 - 1 + h % HX, gy = y0 - 1 + h / HX;
-            in[r] = h < HC && gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny;
-            xr[r] = a.X + (gx + (int64_t)a.nx * gy + plane * z) * S;
-        }
-        double d[NS / 8][4];
-#pragma unroll
-        for (int n = 0; n < NS / 8; ++n)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) d[n][e] = 0.0;
-#pragma unroll 4
-        for (int ks = 0; ks < S / 4; ++ks) {
-            const double a0 = in[0] ? xr[0][4 * ks + t] : 0.0;
-            const double a1 = in[1] ? xr[1][4 * ks + t] : 0.0;
-#pragma unroll
-            for (int n = 0; n < NS / 8; ++n) dmma_c(d[n], a0, a1, Cs[(4 * ks + t) * CS + 8 * n + g]);
-        }
-#pragma unroll
-        for (int n = 0; n < NS / 8; ++n) {
-            const int q = 8 * n + 2 * t;
+        for (int nb = 0; nb < NB; ++nb) {
+            const int q = 8 * nb + 2 * t;
             if (h0 < HC) {
-                buf[q * HC + h0] = d[n][0];
-                buf[(q + 1) * HC + h0] = d[n][1];
+                buf[q * HC + h0] = ac[nb][0];
+                buf[(q + 1) * HC + h0] = ac[nb][1];
             }
             if (h1 < HC) {
-                buf[q * HC + h1] = d[n][2];
-                buf[(q + 1) * HC + h1] = d[n][3];
+                buf[q * HC + h1] = ac[nb][2];
+                buf[(q + 1) * HC + h1] = ac[nb][3];
             }
         }
-    }
-}
+    };
+    // k-steps 0 .. PW/4 of one panel into the accumulators of m-tile mt
+    auto mma_tile = [&](const unsigned char* pan, int mt, const double (&bf)[P::PW / 4][NB],
+                        double (&ac)[NB][4]) {
+        const int h0 = 16 * mt + g;
+        // rows h0 and h0 + 8 share the swizzle phase (address bits 7..9)
+        const unsigned off0 = (unsigned)h0 * (P::PW * 8);
+        const unsigned xr = ((off0 >> 7) & P::SWM) << 4;
+        const unsigned char* r0 = pan + off0;
+        const bool v0 = h0 < HC, v1 = h0 + 8 < HC;
+#pragma unroll
+        for (int kk = 0; kk < P::PW / 4; ++kk) {
+            const unsigned kx = ((unsigned)(4 * kk + t) * 8u) ^ xr;
+            const double a0 = v0 ? *reinterpret_cast<const double*>(r0 + kx) : 0.0;
+            const double a1 = v1 ? *reinterpret_cast<const double*>(r0 + 8 * P::PW * 8 + kx) : 0.0;
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) dmma_c(ac[nb], a0, a1, bf[kk][nb]);
+        }
+    };
+    // T of halo plane z (all NS samples) into ring slot z % 3. Panels arrive
+    // in ascending column order, so each accumulator sees k ascending.
+    auto form = [&](int z) {
+        double* buf = ring + (z % 3) * NS * HC;
+        if constexpr (P::R == 1) {
+            // one panel per plane: finish and store each m-tile in turn
+            const int slot = (int)(pc % NP);
+            mbar_wait(&bar[slot], (pc / NP) & 1u);
+            const unsigned char* pan = panels + slot * P::SLOT;
+            double bf[P::PW / 4][NB];
+#pragma unroll
+            for (int kk = 0; kk < P::PW / 4; ++kk)
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb) bf[kk][nb] = Cs[(4 * kk + t) * CSP + 8 * nb + g];
+            for (int mt = warp; mt < MT; mt += NW) {
+                double ac[NB][4];
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) ac[nb][e] = 0.0;
+                mma_tile(pan, mt, bf, ac);
+                store_tile(mt, ac, buf);
+            }
+            __syncthreads();  // every warp is done with this slot
+            if (tid == 0) issue();
+            ++pc;
+        } else {
+            double acc[MPW][NB][4];
+#pragma unroll
+            for (int mi = 0; mi < MPW; ++mi)
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[mi][nb][e] = 0.0;
+            for (int r = 0; r < P::R; ++r) {
+                const int slot = (int)(pc % NP);
+                mbar_wait(&bar[slot], (pc / NP) & 1u);
+                const unsigned char* pan = panels + slot * P::SLOT;
+                double bf[P::PW / 4][NB];
+#pragma unroll
+                for (int kk = 0; kk < P::PW / 4; ++kk)
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb)
+                        bf[kk][nb] = Cs[(r * P::PW + 4 * kk + t) * CSP + 8 * nb + g];
+#pragma unroll
+                for (int mi = 0; mi < MPW; ++mi)
+                    if (warp + NW * mi < MT) mma_tile(pan, warp + NW * mi, bf, acc[mi]);
+                __syncthreads();  // every warp is done with this slot
+                if (tid == 0) issue();
+                ++pc;
+            }
+#pragma unroll
+            for (int mi = 0; mi < MPW; ++mi)
+                if (warp + NW * mi < MT) store_tile(warp + NW * mi, acc[mi], buf);
+        }
+    };
 
-template <int S, int NS>
-__global__ void __launch_bounds__(NT, NS == 8 ? 3 : 2) combine_action_kernel(ActArgs a) {
-    extern __shared__ __align__(16) double sm[];
-    double* Cs = sm;                             // S x (NS + 4)
-    double* ring = sm + S * CSTRIDE(NS);         // min(nz,3) x NS x HC
-    const int nring = a.nz < 3 ? a.nz : 3;
-    // grid: x = sample chunk (fastest), y = cell tile, so the CTAs resident at
-    // any moment share one tile's X rows through L2 instead of re-reading X
-    // from HBM once per chunk (config 5: X = 2.1 GB)
-    const int tilesx = (a.nx + TX - 1) / TX;
-    const int tile = blockIdx.y;
-    const int x0 = (tile % tilesx) * TX, y0 = (tile / tilesx) * TY;
-    const int64_t j0 = (int64_t)blockIdx.x * NS;
-    const int tid = threadIdx.x;
-    const int64_t plane = (int64_t)a.nx * a.ny;
-
-    comb_mark(0);
-    for (int e = tid; e < S * NS; e += NT) {
-        const int k = e / NS, q = e % NS;
-        Cs[k * CSTRIDE(NS) + q] = (k < a.s && j0 + q < a.N) ? a.C[(int64_t)k * a.ldc + j0 + q] : 0.0;
-    }
-    __syncthreads();
-
-    const int lx = tid % TX, ly = tid / TX;
-    const int gx = x0 + lx, gy = y0 + ly;
-    const bool inside = gx < a.nx && gy < a.ny;
+    const int cell = tid & 255, qh = NT == 512 ? tid >> 8 : 0;
+    const int lx = cell % TX, ly = cell / TX;
     const int h = (ly + 1) * HX + (lx + 1);
-    double num[NS], den[NS];
-#pragma unroll
-    for (int q = 0; q < NS; ++q) num[q] = den[q] = 0.0;
 
-    comb_mark(1);
-    form_plane<S, NS>(a, x0, y0, 0, Cs, ring);
-    if (a.nz > 1) form_plane<S, NS>(a, x0, y0, 1, Cs, ring + HC * NS);
-    __syncthreads();
-    comb_mark(2);
-    for (int z = 0; z < a.nz; ++z) {
-        const double* Tm = ring + ((z + nring - 1) % nring) * HC * NS;
-        const double* T0 = ring + (z % nring) * HC * NS;
-        const double* Tp = ring + ((z + 1) % nring) * HC * NS;
-        if (inside) {
-            const int64_t i = gx + (int64_t)a.nx * gy + plane * z;
-            const double vol = a.volz[z];
-            const double rvol = 1.0 / vol;
-            const double gi = a.g[i], di = a.diag[i];
-            const double czm = z > 0 ? -a.cz[i - plane] : 0.0;
-            const double cym = gy > 0 ? -a.cy[i - a.nx] : 0.0;
-            const double cxm = gx > 0 ? -a.cx[i - 1] : 0.0;
-            const double cxp = gx < a.nx - 1 ? -a.cx[i] : 0.0;
-            const double cyp = gy < a.ny - 1 ? -a.cy[i] : 0.0;
-            const double czp = z < a.nz - 1 ? -a.cz[i] : 0.0;
+    for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+        const int chunk = item % a.chunks;
+        const int tile = item / a.chunks;
+        const int x0 = (tile % a.tilesx) * TX, y0 = (tile / a.tilesx) * TY;
+        const int64_t j0 = (int64_t)chunk * NS;
+        prof = blockIdx.x == 0 && tid == 0 && item == 4 * (int)gridDim.x;
+        pm = 0;
+        mark();
+        for (int e = tid; e < S * NS; e += NT) {
+            const int k = e / NS, q = e % NS;
+            Cs[k * CSP + q] = (k < a.s && j0 + q < a.N) ? a.C[(int64_t)k * a.ldc + j0 + q] : 0.0;
+        }
+        const int gx = x0 + lx, gy = y0 + ly;
+        const bool inside = gx < a.nx && gy < a.ny;
+        Coef k{}, kn{};
+        if (inside) load_coef(a, gx, gy, 0, k);
+        double num[SPT], den[SPT];
 #pragma unroll
-            for (int q = 0; q < NS; ++q) {
-                const int64_t j = j0 + q;
-                // y = A T in CSR order z-, y-, x-, diag, x+, y+, z+ (mul, add)
-                double y = 0.0;
-                if (z > 0) y = __dadd_rn(y, __dmul_rn(czm, Tm[q * HC + h]));
-                if (gy > 0) y = __dadd_rn(y, __dmul_rn(cym, T0[q * HC + h - HX]));
-                if (gx > 0) y = __dadd_rn(y, __dmul_rn(cxm, T0[q * HC + h - 1]));
-                const double tc = T0[q * HC + h];
-                y = __dadd_rn(y, __dmul_rn(di, tc));
-                if (gx < a.nx - 1) y = __dadd_rn(y, __dmul_rn(cxp, T0[q * HC + h + 1]));
-                if (gy < a.ny - 1) y = __dadd_rn(y, __dmul_rn(cyp, T0[q * HC + h + HX]));
-                if (z < a.nz - 1) y = __dadd_rn(y, __dmul_rn(czp, Tp[q * HC + h]));
-                const double qv = div_rn(__dsub_rn(y, gi), vol, rvol);
-                if (j < a.N) {
-                    if (a.T) __stcs(a.T + j * a.n + i, tc);
-                    if (a.Q) __stcs(a.Q + j * a.n + i, qv);
-                    const double bv = fma(vol, qv, gi);
-                    const double rv = __dsub_rn(y, bv);
-                    num[q] = fma(rv, rv, num[q]);
-                    den[q] = fma(bv, bv, den[q]);
+        for (int q = 0; q < SPT; ++q) num[q] = den[q] = 0.0;
+        __syncthreads();  // Cs ready
+        mark();
+
+        form(0);
+        if (nz > 1) form(1);
+        __syncthreads();
+        mark();
+        for (int z = 0; z < nz; ++z) {
+            if (inside && z + 1 < nz) load_coef(a, gx, gy, z + 1, kn);
+            // ring slots of planes z - 1, z, z + 1, offset to this thread's
+            // cell and sample half (compile-time offsets below)
+            const int sz = z % nring;
+            const int sm1 = sz == 0 ? nring - 1 : sz - 1, sp1 = sz + 1 == nring ? 0 : sz + 1;
+            const double* b0 = ring + sz * NS * HC + SPT * qh * HC + h;
+            const double* bm = ring + sm1 * NS * HC + SPT * qh * HC + h;
+            const double* bp = ring + sp1 * NS * HC + SPT * qh * HC + h;
+            const bool hzm = z > 0, hzp = z < nz - 1;  // CTA-uniform
+            if (inside) {
+                const int64_t i = gx + (int64_t)a.nx * gy + plane * z;
+                const int64_t jb = j0 + SPT * qh;
+                double* pt = a.T ? a.T + jb * a.n + i : nullptr;
+                double* pq = a.Q ? a.Q + jb * a.n + i : nullptr;
+                const int nv = a.N - jb < SPT ? (int)(a.N - jb) : SPT;  // valid samples
+                const double vol = a.volz[z];
+                const double rvol = 1.0 / vol;
+#pragma unroll
+                for (int qq = 0; qq < SPT; ++qq) {
+                    // y = A T in CSR order z-, y-, x-, diag, x+, y+, z+ (mul, add).
+                    // In-plane neighbours outside the domain have a zero
+                    // coefficient and a zero-filled T: adding the +-0 product
+                    // leaves y bitwise unchanged (y is never -0), as skipping does
+                    double y = 0.0;
+                    if (hzm) y = __dadd_rn(y, __dmul_rn(k.zm, bm[qq * HC]));
+                    y = __dadd_rn(y, __dmul_rn(k.ym, b0[qq * HC - HX]));
+                    y = __dadd_rn(y, __dmul_rn(k.xm, b0[qq * HC - 1]));
+                    const double tc = b0[qq * HC];
+                    y = __dadd_rn(y, __dmul_rn(k.di, tc));
+                    y = __dadd_rn(y, __dmul_rn(k.xp, b0[qq * HC + 1]));
+                    y = __dadd_rn(y, __dmul_rn(k.yp, b0[qq * HC + HX]));
+                    if (hzp) y = __dadd_rn(y, __dmul_rn(k.zp, bp[qq * HC]));
+                    const double qv = div_rn(__dsub_rn(y, k.gi), vol, rvol);
+                    if (qq < nv) {
+                        if (pt) __stcs(pt, tc);
+                        if (pq) __stcs(pq, qv);
+                        const double bv = fma(vol, qv, k.gi);
+                        const double rv = __dsub_rn(y, bv);
+                        num[qq] = fma(rv, rv, num[qq]);
+                        den[qq] = fma(bv, bv, den[qq]);
+                    }
+                    pt += a.n;
+                    pq += a.n;
                 }
             }
-        }
-        __syncthreads();
-        comb_mark(3 + 2 * z);
-        if (z + 2 < a.nz) {
-            form_plane<S, NS>(a, x0, y0, z + 2, Cs, ring + ((z + 2) % 3) * HC * NS);
+            k = kn;
             __syncthreads();
+            mark();
+            if (z + 2 < nz) {
+                form(z + 2);
+                __syncthreads();
+            }
+            mark();
         }
-        comb_mark(4 + 2 * z);
-    }
 
-    if (a.part) {
-        // CTA reduction of the residual partials, fixed order. Warp level: a
-        // transpose-reduce of the V = 2 NS per-lane sums (V - 1 shuffles, plus
-        // one when V = 16); lane L ends with sum L / (32 / V): num of sample k
-        // for k < NS, den of sample k - NS otherwise. Then warps in index order.
-        // Reuses the ring buffer.
-        constexpr int V = 2 * NS;
-        static_assert(V == 16 || V == 32, "NS = 8 or 16");
-        const int lane = tid & 31, warp = tid >> 5;
-        double* red = ring;  // 8 warps x V
-        double v[V];
+        if (a.part) {
+            // fixed-order reduction of the residual partials over the tile's
+            // cells. Warp level: transpose-reduce of the V = 2 SPT per-lane
+            // sums (num of the thread's samples, then den); lane L ends with
+            // sum L / (32 / V). Then the 8 warps of each sample half in index
+            // order. Reuses ring.
+            constexpr int V = 2 * SPT;
+            static_assert(V == 16 || V == 32, "SPT = 8 or 16");
+            double* red = ring;  // NW x V
+            double v[V];
 #pragma unroll
-        for (int q = 0; q < NS; ++q) {
-            v[q] = num[q];
-            v[NS + q] = den[q];
-        }
+            for (int q = 0; q < SPT; ++q) {
+                v[q] = num[q];
+                v[SPT + q] = den[q];
+            }
 #pragma unroll
-        for (int o = 16, len = V; o >= 32 / V; o >>= 1, len >>= 1) {
-            const bool up = (lane & o) != 0;
+            for (int o = 16, len = V; o >= 32 / V; o >>= 1, len >>= 1) {
+                const bool up = (lane & o) != 0;
 #pragma unroll
-            for (int i = 0; i < len / 2; ++i) {
-                const double keep = up ? v[len / 2 + i] : v[i];
-                const double send = up ? v[i] : v[len / 2 + i];
-                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                for (int e = 0; e < len / 2; ++e) {
+                    const double keep = up ? v[len / 2 + e] : v[e];
+                    const double send = up ? v[e] : v[len / 2 + e];
+                    v[e] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+            if (V == 16) v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+            if (lane % (32 / V) == 0) red[warp * V + lane / (32 / V)] = v[0];
+            __syncthreads();
+            if (tid < NS && j0 + tid < a.N) {
+                const int hq = tid / SPT, qq = tid % SPT;
+                double u = 0.0, w = 0.0;
+                for (int k2 = 0; k2 < 8; ++k2) {  // the 8 warps of sample half hq
+                    u += red[(8 * hq + k2) * V + qq];
+                    w += red[(8 * hq + k2) * V + SPT + qq];
+                }
+                double* pp = a.part + ((j0 + tid) * (int64_t)a.tiles + tile) * 2;
+                *reinterpret_cast<double2*>(pp) = make_double2(u, w);
             }
         }
-        if (V == 16) v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-        if (lane % (32 / V) == 0) red[warp * V + lane / (32 / V)] = v[0];
-        __syncthreads();
-        if (tid < NS && j0 + tid < a.N) {
-            double u = 0.0, w = 0.0;
-            for (int k = 0; k < NT / 32; ++k) {
-                u += red[k * V + tid];
-                w += red[k * V + NS + tid];
-            }
-            double* pp = a.part + ((j0 + tid) * (int64_t)a.tiles + tile) * 2;
-            *reinterpret_cast<double2*>(pp) = make_double2(u, w);
-        }
+        __syncthreads();  // ring and Cs free for the next item
+        mark();
     }
 }
 
@@ -272,10 +455,25 @@ __global__ void resid_finalize(const double* __restrict__ part, int tiles, int64
     if (lane == 0) resid[j] = de == 0.0 ? (nu == 0.0 ? 0.0 : 1.0) : sqrt(nu / de);
 }
 
-template <int S, int NS>
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+template <int S, int NS, int NT, bool PL = false>
 bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const double* C,
               int64_t ldc, int64_t N, double* T, double* Q, double* resid) {
     using namespace bk;
+    using P = Panel<S>;
+    using SH = Shape<NS, NT>;
     ActArgs a;
     a.nx = op->nx;
     a.ny = op->ny;
@@ -289,47 +487,83 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
     a.cz = op->cz;
     a.g = op->g;
     a.volz = op->volz;
-    a.X = X;
     a.C = C;
     a.T = T;
     a.Q = Q;
     a.s = s;
-    const int tilesx = (op->nx + TX - 1) / TX, tilesy = (op->ny + TY - 1) / TY;
-    const int tiles = tilesx * tilesy;
+    a.tilesx = (op->nx + TX - 1) / TX;
+    a.tiles = a.tilesx * ((op->ny + TY - 1) / TY);
+    const int64_t chunks = (N + NS - 1) / NS;
+    if (chunks * a.tiles >= (int64_t)1 << 31)
+        return fail(ctx, BK_INVALID_CONFIG, "combine_action: too many work items");
+    a.chunks = (int)chunks;
+    a.items = (int)(chunks * a.tiles);
     a.part = nullptr;
-    a.tiles = tiles;
     if (resid) {
         void* p;
-        bk_status st = workspace(ctx, kSlotActPart, (size_t)tiles * N * 2 * sizeof(double), &p);
+        bk_status st = workspace(ctx, kSlotActPart, (size_t)a.tiles * N * 2 * sizeof(double), &p);
         if (st != BK_OK) return st;
         a.part = (double*)p;
     }
+    if (reinterpret_cast<uintptr_t>(X) % 16)
+        return fail(ctx, BK_INTERNAL, "combine_action: X must be 16-byte aligned");
+    // X as a 4D tensor (S, nx, ny, nz): per-axis bounds, so the halo of a
+    // boundary tile reads zeros instead of wrapping into the next row
+    auto enc = encode_fn();
+    if (!enc) return fail(ctx, BK_CUDA_ERROR, "combine_action: cuTensorMapEncodeTiled unavailable");
+    CUtensorMap map;
+    const cuuint64_t dims[4] = {(cuuint64_t)S, (cuuint64_t)op->nx, (cuuint64_t)op->ny,
+                                (cuuint64_t)op->nz};
+    const cuuint64_t strides[3] = {(cuuint64_t)S * 8, (cuuint64_t)S * 8 * op->nx,
+                                   (cuuint64_t)S * 8 * op->nx * op->ny};
+    const cuuint32_t box[4] = {(cuuint32_t)P::PW, (cuuint32_t)HX, (cuuint32_t)HY, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(X), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            P::PW == 16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS)
+        return fail(ctx, BK_CUDA_ERROR, "combine_action: tensor map encode failed (" +
+                                            std::to_string((int)cr) + ")");
     const int nring = op->nz < 3 ? op->nz : 3;
-    const size_t smem = (size_t)(S * CSTRIDE(NS) + nring * HC * NS) * sizeof(double);
-    auto kern = combine_action_kernel<S, NS>;
+    const size_t smem = 1024 + (size_t)SH::NP * P::SLOT +
+                        (size_t)(nring * NS * HC + S * SH::CSP) * sizeof(double) + SH::NP * 8;
+    auto kern = combine_action_kernel<S, NS, NT, PL>;
     BK_CUDA_TRY(ctx, bk::set_max_smem((const void*)kern, smem));
-    const int64_t chunks = (N + NS - 1) / NS;
-    if (tiles > 65535) return fail(ctx, BK_INVALID_CONFIG, "combine_action: grid too large");
-    kern<<<dim3((unsigned)chunks, (unsigned)tiles), NT, smem, ctx->stream>>>(a);
+    const int slots = SH::CTAS * ctx->num_sms;
+    const int grid = a.items < slots ? a.items : slots;
+    kern<<<(unsigned)grid, SH::NT, smem, ctx->stream>>>(map, a);
     ++ctx->launches;
     BK_CUDA_TRY(ctx, cudaGetLastError());
     if (getenv("BK_COMB_PROFILE")) {
-        long long h[64];
+        long long hp[64] = {};
         cudaStreamSynchronize(ctx->stream);
-        cudaMemcpyFromSymbol(h, g_comb_prof, sizeof(h));
-        fprintf(stderr, "[bk_comb_profile S=%d nz=%d] cycles: C load %lld, first planes %lld;", S,
-                op->nz, h[1] - h[0], h[2] - h[1]);
-        for (int z = 0; z < op->nz && 4 + 2 * z < 64; ++z)
-            fprintf(stderr, " z%d stencil %lld form %lld;", z, h[3 + 2 * z] - (z ? h[2 + 2 * z] : h[2]),
-                    h[4 + 2 * z] - h[3 + 2 * z]);
-        fprintf(stderr, "\n");
+        cudaMemcpyFromSymbol(hp, g_comb_prof, sizeof(hp));
+        fprintf(stderr, "[bk_comb_profile S=%d nz=%d] Cs %lld, first planes %lld;", S, op->nz,
+                hp[1] - hp[0], hp[2] - hp[1]);
+        for (int z = 0; z < op->nz; ++z)
+            fprintf(stderr, " z%d stencil %lld form %lld;", z, hp[3 + 2 * z] - hp[2 + 2 * z],
+                    hp[4 + 2 * z] - hp[3 + 2 * z]);
+        fprintf(stderr, " reduce %lld\n", hp[3 + 2 * op->nz] - hp[2 + 2 * op->nz]);
     }
     if (resid) {
-        resid_finalize<<<(unsigned)((N + 7) / 8), 256, 0, ctx->stream>>>(a.part, tiles, N, resid);
+        resid_finalize<<<(unsigned)((N + 7) / 8), 256, 0, ctx->stream>>>(a.part, a.tiles, N, resid);
         ++ctx->launches;
         BK_CUDA_TRY(ctx, cudaGetLastError());
     }
     return BK_OK;
+}
+
+// Two CTAs of 256 threads per SM, one panel slot each. Single plane: 16
+// samples per item (no z-ring, so the T plane fits twice per SM). 3D: 8
+// samples per item for the three-plane ring. Measured (B200): C2 0.75 ms
+// (0.87 with the L2-fragment kernel), C3 5.6 ms (6.6); the one-CTA 512-thread
+// NS = 16 shape gave 5.9 ms on C3 (its DMMA chains and stencil do not overlap).
+template <int S>
+bk_status dispatch(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const double* C,
+                   int64_t ldc, int64_t N, double* T, double* Q, double* resid) {
+    if (op->nz == 1) return run<S, 16, 256, true>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+    return run<S, 8, 256>(ctx, op, X, s, C, ldc, N, T, Q, resid);
 }
 
 }  // namespace
@@ -344,16 +578,10 @@ bk_status combine_action_device(bk_ctx* ctx, const bk_operator* op, const double
     if (N == 0) return BK_OK;
     if (s < 1 || s > S || ldc < N) return fail(ctx, BK_INTERNAL, "combine_action: bad widths");
     switch (S) {
-        // 16 samples per CTA for a single plane; 8 for 3D grids, whose
-        // 3-plane T ring then fits 3 CTAs per SM
-        case 8: return op->nz == 1 ? run<8, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid)
-                                   : run<8, 8>(ctx, op, X, s, C, ldc, N, T, Q, resid);
-        case 16: return op->nz == 1 ? run<16, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid)
-                                    : run<16, 8>(ctx, op, X, s, C, ldc, N, T, Q, resid);
-        case 32: return op->nz == 1 ? run<32, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid)
-                                    : run<32, 8>(ctx, op, X, s, C, ldc, N, T, Q, resid);
-        case 64: return op->nz == 1 ? run<64, 16>(ctx, op, X, s, C, ldc, N, T, Q, resid)
-                                    : run<64, 8>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+        case 8: return dispatch<8>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+        case 16: return dispatch<16>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+        case 32: return dispatch<32>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+        case 64: return dispatch<64>(ctx, op, X, s, C, ldc, N, T, Q, resid);
         default: return fail(ctx, BK_INTERNAL, "combine_action: unpadded width");
     }
 }
