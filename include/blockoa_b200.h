@@ -305,6 +305,80 @@ bk_status bk_synth_chip_device(bk_ctx* ctx, const bk_synth_spec* spec, bk_grid* 
                                double* dz_out, int* has_dz, bk_face bc_out[6], double* k_dev,
                                double* Qbasis_dev, double* C);
 
+/* ---- reference-semantics generation (chip model + generate_blockoa) -------- */
+
+/* ChipSpec (chip.hpp:55-80) with material names resolved to conductivities.
+ * Lengths in meters; layers bottom to top tiling [0, extent[2]); power ranges
+ * in W/mm^2 (closed intervals). role: BK_LAYER_CORE / CACHE / TIM. */
+typedef enum { BK_LAYER_CORE = 0, BK_LAYER_CACHE = 1, BK_LAYER_TIM = 2 } bk_layer_role;
+#define BK_MAX_LAYERS 16
+typedef struct {
+    double z_lo, z_hi;
+    double k; /* conductivity of the layer material, W/(m K) */
+    int role; /* bk_layer_role */
+} bk_layer;
+typedef struct {
+    double extent[3];
+    int n_layers;
+    bk_layer layers[BK_MAX_LAYERS];
+    int core_blocks, high_power, caches_per_layer; /* BlockCounts */
+    double p_high[2], p_normal[2], p_cache[2];      /* PowerRanges, W/mm^2 */
+    int tsv_count;                                  /* 0: no TSVs */
+    double tsv_width;                               /* m */
+    double tsv_k;                                   /* TSV material conductivity */
+} bk_chip_spec;
+
+/* ChipSpec::default_chip()   chip.cpp:74-100 (10 x 10 x 0.51 mm, TIM / cache /
+ * TIM / cache / TIM / core, 156 core blocks, 6 high power, 2 caches per layer,
+ * 12 copper TSVs). */
+void bk_default_chip(bk_chip_spec* out);
+
+/* Host chip model, bit-exact with the reference: build_floorplans(spec, n_k,
+ * seed) (chip.cpp:180-221), rasterize_conductivity (chip.cpp:238-274) -> k
+ * [n_k][n]; for each group j and basis column t, sample_power(fp_j, spec,
+ * derive_seed(seed, "basis", j eta + t)) and rasterize_power (chip.cpp:223-306)
+ * -> q [n_k eta][n] (generate_basis, pipeline.cpp:92-134). The grid spans the
+ * chip extent. q may be NULL. */
+bk_status bk_chip_fields(const bk_chip_spec* spec, int nx, int ny, int nz, int n_k, int eta,
+                         uint64_t seed, double* k, double* q);
+
+/* draw_weights(n_basis, sample_seed_for(seed, l + 1)) for l < n_data
+ * (pipeline.cpp:88-90, 136-152): normalised Gaussian weights -> w
+ * [n_data][n_basis]. Host. */
+bk_status bk_draw_weights(int n_basis, uint64_t seed, int64_t n_data, double* w);
+
+typedef enum { BK_NOISE_NONE = 0, BK_NOISE_UNIFORM = 1, BK_NOISE_GAUSSIAN = 2 } bk_noise_kind;
+
+/* GenerationConfig (pipeline.hpp:28-43). The grid spans the chip extent. */
+typedef struct {
+    int nx, ny, nz;
+    bk_face bc[6];
+    int64_t n_data;
+    int n_basis; /* total basis columns; n_k must divide it (eta = n_basis / n_k) */
+    int n_k;     /* floorplan groups */
+    uint64_t master_seed;
+    int noise_kind; /* bk_noise_kind */
+    double noise_lo, noise_hi, noise_sigma;
+    bk_solver_cfg solver;
+    bk_chip_spec chip;
+} bk_blockoa_cfg;
+
+/* generate_blockoa(cfg)   pipeline.hpp:106, pipeline.cpp:365-597, on the GPU:
+ * the n_k floorplan groups' operators and eta power maps each (host chip model
+ * above), ONE batched block-CG launch for all groups, then per group the fused
+ * combine + action kernel over ALL groups' basis columns (groups ascending,
+ * columns ascending, normalised Gaussian weights drawn on the host), the
+ * interior noise stream of every sample generated on the device (uniform;
+ * gaussian noise is drawn on the host), q = (A_g T - g)/V with the group's
+ * operator in apply_block's fused-multiply-add order, sample l in group
+ * l mod n_k. n_basis <= 64, eta <= 32. Outputs (host or device, NULL to
+ * skip): k [n_k][n], U and Q [n_data][n], resid [n_data], floorplan_id
+ * [n_data]; reports: n_k entries. BK_NOT_CONVERGED if a basis group missed
+ * the tolerance (NotConvergedError, pipeline.cpp:128-132). */
+bk_status bk_generate_blockoa(bk_ctx* ctx, const bk_blockoa_cfg* cfg, double* k, double* U,
+                              double* Q, double* resid, int64_t* floorplan_id,
+                              bk_solve_report* reports, bk_phase_timings* timings);
+
 /* ---- dataset sink and validation (dataset_io.hpp) ---------------------------- */
 
 /* field_digest(f)   discretize.hpp:99, discretize.cpp:302-319: FNV-1a over

@@ -381,6 +381,56 @@ class Reference(_Base):
         return out
 
     # ---- dataset I/O (dataset_io.hpp) ----------------------------------------
+    # ---- chip model + generate_blockoa on ChipSpec::default_chip() -------------
+    def chip_fields(self, grid, n_k, eta, seed):
+        """(k [n_k, n], q [n_k * eta, n]) of build_floorplans / rasterize_* as
+        generate_basis draws them (chip.cpp:180-306, pipeline.cpp:92-134)."""
+        nx, ny, nz = grid
+        n = nx * ny * nz
+        k = np.empty((n_k, n), np.float64)
+        q = np.empty((n_k * eta, n), np.float64)
+        st = self.lib.ref_chip_fields(C.c_int(nx), C.c_int(ny), C.c_int(nz), C.c_int(n_k),
+                                      C.c_int(eta), C.c_ulonglong(seed), _ptr(k), _ptr(q))
+        if st:
+            self._err(st, "chip_fields")
+        return k, q
+
+    def draw_weights(self, n_basis, seed, n_data):
+        w = np.empty((n_data, n_basis), np.float64)
+        st = self.lib.ref_draw_weights(C.c_int(n_basis), C.c_ulonglong(seed),
+                                       C.c_longlong(n_data), _ptr(w))
+        if st:
+            self._err(st, "draw_weights")
+        return w
+
+    def generate_blockoa(self, grid, n_data, n_basis, n_k, seed, bc, noise=("uniform", -0.01, 0.01),
+                         tol=1e-9, max_iter=50000, threads=1):
+        """generate_blockoa (pipeline.cpp:365-597) on the default chip: dict of
+        k [n_k, n], u / q [n_data, n], residual, floorplan_id, iterations and
+        the reference's own basis / total wall seconds."""
+        nx, ny, nz = grid
+        n = nx * ny * nz
+        kind, a, b = _bc_arrays(bc)
+        nkind = {"none": 0, "uniform": 1, "gaussian": 2}[noise[0]]
+        lo, hi = (noise[1], noise[2]) if nkind == 1 else (0.0, 0.0)
+        sigma = noise[1] if nkind == 2 else 0.0
+        k = np.empty((n_k, n), np.float64)
+        u = np.empty((n_data, n), np.float64)
+        q = np.empty((n_data, n), np.float64)
+        r = np.empty(n_data, np.float64)
+        fp = np.empty(n_data, np.int64)
+        it = np.zeros(1, np.int32)
+        sec = np.zeros(2, np.float64)
+        st = self.lib.ref_generate_blockoa(
+            C.c_int(nx), C.c_int(ny), C.c_int(nz), C.c_longlong(n_data), C.c_int(n_basis),
+            C.c_int(n_k), C.c_ulonglong(seed), C.c_int(nkind), C.c_double(lo), C.c_double(hi),
+            C.c_double(sigma), C.c_double(tol), C.c_int(max_iter), C.c_int(threads), _ptr(kind),
+            _ptr(a), _ptr(b), _ptr(k), _ptr(u), _ptr(q), _ptr(r), _ptr(fp), _ptr(it), _ptr(sec))
+        if st:
+            self._err(st, "generate_blockoa")
+        return dict(k=k, u=u, q=q, residual=r, floorplan_id=fp, iterations=int(it[0]),
+                    basis_s=float(sec[0]), total_s=float(sec[1]))
+
     def write_dataset(self, dir, grid, bc, k, q, u, ids, method="blockoa", master_seed=0,
                       tol_claimed=1e-12, tool_version="blockoa-0.1.0", digests=(),
                       timings=(0.0, 0.0, 0.0, 0.0, 0.0), counters=(0, 0), requested=None,

@@ -17,6 +17,8 @@
 //   operator_action        pipeline.hpp:95    (pipeline.cpp:242-251)
 //   Rng / derive_seed      rng.hpp:14-63      (rng.cpp)
 //   field_digest           discretize.hpp:99  (discretize.cpp:302-319)
+//   build_floorplans / sample_power / rasterize_*  chip.hpp:103-124 (chip.cpp:180-306)
+//   generate_blockoa       pipeline.hpp:106   (pipeline.cpp:365-597)
 //   write_dataset / read_dataset / validate_dataset
 //                          dataset_io.hpp:27-47 (dataset_io.cpp:160-361)
 // Exceptions are mapped to the status codes of include/blockoa_b200.h.
@@ -28,6 +30,7 @@
 #include <string>
 #include <vector>
 
+#include "blockoa/chip.hpp"
 #include "blockoa/dataset.hpp"
 #include "blockoa/dataset_io.hpp"
 #include "blockoa/discretize.hpp"
@@ -466,6 +469,95 @@ int ref_validate_dataset(const char* dir, double tol, double* residuals, long lo
         *pass = r.pass_count;
         *fail = r.fail_count;
         *max_res = r.max_residual;
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// ---- chip model and the reference-semantics pipeline (default_chip) ---------
+// k fields [n_k][n] of build_floorplans(default_chip, n_k, seed) and the basis
+// power maps [n_k * eta][n] exactly as generate_basis draws them
+// (pipeline.cpp:92-134).
+int ref_chip_fields(int nx, int ny, int nz, int n_k, int eta, unsigned long long seed, double* k,
+                    double* q) {
+    try {
+        const ChipSpec spec = ChipSpec::default_chip();
+        const GridSpec grid{nx, ny, nz, spec.extent[0], spec.extent[1], spec.extent[2]};
+        const std::int64_t n = grid.cell_count();
+        const auto fps = build_floorplans(spec, n_k, seed);
+        for (int j = 0; j < n_k; ++j) {
+            const ScalarField kf = rasterize_conductivity(fps[j], spec, grid);
+            std::memcpy(k + j * n, kf.values.data(), n * sizeof(double));
+            for (int t = 0; t < eta; ++t) {
+                const std::uint64_t ds = derive_seed(seed, "basis", (std::uint64_t)j * eta + t);
+                const ScalarField qf =
+                    rasterize_power(sample_power(fps[j], spec, ds), fps[j], spec, grid);
+                std::memcpy(q + ((std::int64_t)j * eta + t) * n, qf.values.data(), n * sizeof(double));
+            }
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// draw_weights(n_basis, sample_seed_for(seed, l + 1)) for l < n_data -> w[n_data][n_basis]
+int ref_draw_weights(int n_basis, unsigned long long seed, long long n_data, double* w) {
+    try {
+        for (long long l = 0; l < n_data; ++l) {
+            const auto mu = draw_weights(n_basis, sample_seed_for(seed, l + 1));
+            std::memcpy(w + l * n_basis, mu.data(), n_basis * sizeof(double));
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// generate_blockoa on ChipSpec::default_chip() (pipeline.cpp:365-597).
+// noise_kind: 0 none, 1 uniform [lo, hi), 2 gaussian sigma. Outputs: k of each
+// group [n_k][n], per sample u/q [n_data][n], residual, floorplan id; basis
+// iterations per group; wall seconds of the basis solve and of the whole call.
+int ref_generate_blockoa(int nx, int ny, int nz, long long n_data, int n_basis, int n_k,
+                         unsigned long long seed, int noise_kind, double lo, double hi,
+                         double sigma, double tol, int max_iter, int threads,
+                         const int* bc_kind, const double* bc_a, const double* bc_b, double* k,
+                         double* u, double* q, double* resid, long long* fp_id, int* iters,
+                         double* seconds) {
+    try {
+        GenerationConfig cfg;
+        cfg.chip = ChipSpec::default_chip();
+        cfg.grid = GridSpec{nx, ny, nz, cfg.chip.extent[0], cfg.chip.extent[1], cfg.chip.extent[2]};
+        cfg.bc = make_bc(bc_kind, bc_a, bc_b);
+        cfg.n_data = n_data;
+        cfg.n_basis = n_basis;
+        cfg.n_k = n_k;
+        cfg.master_seed = seed;
+        cfg.noise.kind = noise_kind == 0   ? NoiseConfig::Kind::none
+                         : noise_kind == 1 ? NoiseConfig::Kind::uniform
+                                           : NoiseConfig::Kind::gaussian;
+        cfg.noise.lo = lo;
+        cfg.noise.hi = hi;
+        cfg.noise.sigma = sigma;
+        cfg.solver = make_cfg(tol, max_iter, 1);
+        cfg.threads = threads;
+        const GenerationResult r = generate_blockoa(cfg);
+        const std::int64_t n = cfg.grid.cell_count();
+        const auto& ds = r.dataset;
+        for (long long l = 0; l < n_data; ++l) {
+            const Sample& sm = ds.samples[(std::size_t)l];
+            if (u) std::memcpy(u + l * n, sm.u.values.data(), n * sizeof(double));
+            if (q) std::memcpy(q + l * n, sm.q.values.data(), n * sizeof(double));
+            if (resid) resid[l] = sm.residual;
+            if (fp_id) fp_id[l] = (long long)sm.floorplan_id;
+            if (k && l < n_k) std::memcpy(k + l * n, sm.k.values.data(), n * sizeof(double));
+        }
+        if (iters) iters[0] = (int)r.timings.iterations_total;
+        if (seconds) {
+            seconds[0] = r.timings.basis_solve_s;
+            seconds[1] = r.timings.total_s;
+        }
         return 0;
     } catch (...) {
         return map_exception();

@@ -126,6 +126,26 @@ class _Synth(C.Structure):
                 ("chip_id", C.c_uint64)]
 
 
+class _Layer(C.Structure):
+    _fields_ = [("z_lo", C.c_double), ("z_hi", C.c_double), ("k", C.c_double), ("role", C.c_int)]
+
+
+class _Chip(C.Structure):
+    _fields_ = [("extent", C.c_double * 3), ("n_layers", C.c_int), ("layers", _Layer * 16),
+                ("core_blocks", C.c_int), ("high_power", C.c_int), ("caches_per_layer", C.c_int),
+                ("p_high", C.c_double * 2), ("p_normal", C.c_double * 2),
+                ("p_cache", C.c_double * 2), ("tsv_count", C.c_int), ("tsv_width", C.c_double),
+                ("tsv_k", C.c_double)]
+
+
+class _GenCfg(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("bc", _Face * 6),
+                ("n_data", C.c_int64), ("n_basis", C.c_int), ("n_k", C.c_int),
+                ("master_seed", C.c_uint64), ("noise_kind", C.c_int), ("noise_lo", C.c_double),
+                ("noise_hi", C.c_double), ("noise_sigma", C.c_double), ("solver", _Cfg),
+                ("chip", _Chip)]
+
+
 _lib = None
 
 
@@ -200,6 +220,12 @@ def _load():
         lib.bk_validate_samples.argtypes = [vp, C.POINTER(_Grid), C.POINTER(_Face), vp, vp, vp,
                                             C.c_int64, vp, C.c_int, vp, vp, C.c_double, vp, vp]
         lib.bk_abi_version.restype = C.c_int
+        lib.bk_default_chip.argtypes = [C.POINTER(_Chip)]
+        lib.bk_default_chip.restype = None
+        lib.bk_chip_fields.argtypes = [C.POINTER(_Chip), C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, C.c_uint64, vp, vp]
+        lib.bk_draw_weights.argtypes = [C.c_int, C.c_uint64, C.c_int64, vp]
+        lib.bk_generate_blockoa.argtypes = [vp, C.POINTER(_GenCfg), vp, vp, vp, vp, vp, vp, vp]
         _lib = lib
     return _lib
 
@@ -801,3 +827,179 @@ C4_CHIPS = 5000
 from .dataset import (Dataset, DatasetManifest, DatasetWriter, ManifestTimings,  # noqa: E402
                       ValidationReport, WriteSummary, field_digest, read_dataset,
                       relative_residual, validate_dataset, write_dataset)
+
+
+# ---------------------------------------------------------------- reference-semantics generation
+@dataclass
+class ChipSpec:
+    """ChipSpec (chip.hpp:55-80) with materials resolved to conductivities:
+    layers are (z_lo, z_hi, k, role) bottom to top, role in {"core", "cache",
+    "tim"}; lengths in meters, power ranges in W/mm^2."""
+    extent: tuple = (10e-3, 10e-3, 0.51e-3)
+    layers: list = field(default_factory=list)
+    core_blocks: int = 0
+    high_power: int = 0
+    caches_per_layer: int = 0
+    p_high: tuple = (0.0, 0.0)
+    p_normal: tuple = (0.0, 0.0)
+    p_cache: tuple = (0.0, 0.0)
+    tsv_count: int = 0
+    tsv_width: float = 0.0
+    tsv_k: float = 0.0
+
+    _ROLES = {"core": 0, "cache": 1, "tim": 2}
+
+    @staticmethod
+    def default_chip() -> "ChipSpec":
+        """ChipSpec::default_chip() (chip.cpp:74-100), from the library."""
+        c = _Chip()
+        _load().bk_default_chip(C.byref(c))
+        names = {v: k for k, v in ChipSpec._ROLES.items()}
+        return ChipSpec(tuple(c.extent), [(c.layers[i].z_lo, c.layers[i].z_hi, c.layers[i].k,
+                                           names[c.layers[i].role]) for i in range(c.n_layers)],
+                        c.core_blocks, c.high_power, c.caches_per_layer, tuple(c.p_high),
+                        tuple(c.p_normal), tuple(c.p_cache), c.tsv_count, c.tsv_width, c.tsv_k)
+
+    def _c(self):
+        c = _Chip()
+        c.extent[:] = list(self.extent)
+        if len(self.layers) > 16:
+            raise InvalidSpecError("chip: at most 16 layers")
+        c.n_layers = len(self.layers)
+        for i, (lo, hi, k, role) in enumerate(self.layers):
+            c.layers[i] = _Layer(lo, hi, k, self._ROLES[role])
+        c.core_blocks, c.high_power, c.caches_per_layer = (self.core_blocks, self.high_power,
+                                                           self.caches_per_layer)
+        c.p_high[:], c.p_normal[:], c.p_cache[:] = (list(self.p_high), list(self.p_normal),
+                                                    list(self.p_cache))
+        c.tsv_count, c.tsv_width, c.tsv_k = self.tsv_count, self.tsv_width, self.tsv_k
+        return c
+
+
+@dataclass
+class NoiseConfig:
+    """NoiseConfig (pipeline.hpp:17-26): kind "none" | "uniform" | "gaussian"."""
+    kind: str = "none"
+    lo: float = 0.0
+    hi: float = 0.0
+    sigma: float = 0.0
+
+
+@dataclass
+class GenerationConfig:
+    """GenerationConfig (pipeline.hpp:28-43); the grid spans the chip extent."""
+    n_data: int = 0
+    n_basis: int = 1
+    n_k: int = 1
+    solver: SolverConfig = field(default_factory=SolverConfig)
+    noise: NoiseConfig = field(default_factory=NoiseConfig)
+    master_seed: int = 0
+    grid: tuple = (24, 24, 12)
+    bc: BoundarySpec = field(default_factory=BoundarySpec)
+    chip: ChipSpec = field(default_factory=ChipSpec.default_chip)
+
+    def eta(self) -> int:
+        return self.n_basis // self.n_k
+
+    @staticmethod
+    def default_run_config() -> "GenerationConfig":
+        """configs/default.json (run_config.cpp:273-291): 24 x 24 x 12 over the
+        default chip, Dirichlet 50 degC sides, Robin h = 3e4 / 50 degC top and
+        bottom, 500 samples from 5 floorplans x 10 basis maps, uniform noise
+        +-0.01 degC, Jacobi block CG to 1e-9."""
+        bc = BoundarySpec([Dirichlet(50.0)] * 4 + [Robin(3e4, 50.0)] * 2)
+        return GenerationConfig(500, 50, 5, SolverConfig(1e-9, 50000, "jacobi"),
+                                NoiseConfig("uniform", -0.01, 0.01), 1, (24, 24, 12), bc)
+
+    def _c(self):
+        c = _GenCfg()
+        c.nx, c.ny, c.nz = self.grid
+        fc = self.bc._c()
+        for f in range(6):
+            c.bc[f] = fc[f]
+        c.n_data, c.n_basis, c.n_k, c.master_seed = self.n_data, self.n_basis, self.n_k, \
+            self.master_seed
+        kinds = {"none": 0, "uniform": 1, "gaussian": 2}
+        if self.noise.kind not in kinds:
+            raise InvalidConfigError(f"noise: unknown kind {self.noise.kind!r}")
+        c.noise_kind = kinds[self.noise.kind]
+        c.noise_lo, c.noise_hi, c.noise_sigma = self.noise.lo, self.noise.hi, self.noise.sigma
+        c.solver = self.solver._c()
+        c.chip = self.chip._c()
+        return c
+
+
+def chip_fields(chip: ChipSpec, grid, n_k: int, eta: int, seed: int):
+    """(k [n_k, n], q [n_k * eta, n]): the floorplan groups' conductivity and
+    basis power maps (build_floorplans / rasterize_*, chip.cpp:180-306; draw
+    seeds as generate_basis, pipeline.cpp:92-134). Host, bit-exact."""
+    nx, ny, nz = grid
+    n = nx * ny * nz
+    k = np.empty((n_k, n), np.float64)
+    q = np.empty((n_k * eta, n), np.float64)
+    c = chip._c()
+    _raise(_load().bk_chip_fields(C.byref(c), nx, ny, nz, n_k, eta, seed,
+                                  k.ctypes.data_as(C.c_void_p), q.ctypes.data_as(C.c_void_p)),
+           None, "chip_fields")
+    return k, q
+
+
+def draw_weights(n_basis: int, seed: int, n_data: int):
+    """[n_data, n_basis]: draw_weights(n_basis, sample_seed_for(seed, l + 1))
+    (pipeline.cpp:136-152) per sample l. Host, bit-exact."""
+    w = np.empty((n_data, n_basis), np.float64)
+    _raise(_load().bk_draw_weights(n_basis, seed, n_data, w.ctypes.data_as(C.c_void_p)), None,
+           "draw_weights")
+    return w
+
+
+@dataclass
+class GenerationResult:
+    """generate_blockoa's result (pipeline.hpp:99-103) as arrays: k per
+    floorplan group, per-sample u (= T) and q, residual and floorplan id."""
+    k: object
+    u: object
+    q: object
+    residual: object
+    floorplan_id: np.ndarray
+    reports: list
+    timings: PhaseTimings
+
+
+def generate_blockoa(cfg: GenerationConfig, u_out=None, q_out=None, resid_out=None,
+                     ctx: Optional[Context] = None, check_converged: bool = True):
+    """generate_blockoa(cfg) (pipeline.cpp:365-597) on the GPU: one batched
+    block-CG launch for the n_k floorplan groups, then per group the fused
+    combine + action kernel over all groups' basis columns (normalised Gaussian
+    weights), per-sample interior noise, q = A_g (T) in apply_block order.
+    Sample l belongs to group l mod n_k. Outputs may be numpy (host) or CUDA
+    torch tensors."""
+    ctx = _ctx(ctx)
+    nx, ny, nz = cfg.grid
+    n, N, nk = nx * ny * nz, int(cfg.n_data), int(cfg.n_k)
+    eta = cfg.eta() if nk > 0 else 0
+    k = np.empty((nk, n), np.float64)
+    u_out = np.empty((N, n), np.float64) if u_out is None else u_out
+    q_out = np.empty((N, n), np.float64) if q_out is None else q_out
+    resid_out = np.empty(N, np.float64) if resid_out is None else resid_out
+    fp = np.empty(N, np.int64)
+    ptrs = [_ptr(a) for a in (u_out, q_out, resid_out)]
+    res = [np.zeros(max(eta, 1), np.float64) for _ in range(max(nk, 1))]
+    conv = [np.zeros(max(eta, 1), np.int8) for _ in range(max(nk, 1))]
+    reps = (_Report * max(nk, 1))()
+    for j in range(max(nk, 1)):
+        reps[j] = _Report(0, 0, 0.0, res[j].ctypes.data_as(C.c_void_p),
+                          conv[j].ctypes.data_as(C.c_void_p))
+    tim = _Timings()
+    c = cfg._c()
+    st = _load().bk_generate_blockoa(ctx.h, C.byref(c), k.ctypes.data_as(C.c_void_p), ptrs[0][0],
+                                     ptrs[1][0], ptrs[2][0], fp.ctypes.data_as(C.c_void_p), reps,
+                                     C.byref(tim))
+    if st == 7 and not check_converged:
+        st = 0
+    _raise(st, ctx.h, "generate_blockoa")
+    timings = PhaseTimings(tim.assemble_s, tim.basis_solve_s, tim.combine_action_s, tim.h2d_s,
+                           tim.d2h_s, tim.total_s, tim.iterations_total, tim.matvecs_total)
+    return GenerationResult(k, u_out, q_out, resid_out, fp,
+                            [_report(eta, reps[j], res[j], conv[j]) for j in range(nk)], timings)
+

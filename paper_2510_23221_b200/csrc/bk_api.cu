@@ -13,7 +13,9 @@
 #include <string>
 #include <vector>
 
+#include "bk_chip.h"
 #include "bk_common.cuh"
+#include "bk_synth.h"
 
 namespace bk {
 
@@ -484,6 +486,244 @@ bk_status generate_fused(bk_ctx* ctx, int n_chips, const bk_grid* grids, const d
     return BK_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// generate_blockoa (pipeline.cpp:365-597) with the reference's own semantics
+// ---------------------------------------------------------------------------
+// all groups' basis columns side by side: Xall[i][j eta + t] = X_j[i][t]
+// (groups ascending, columns ascending: combine_tile16's term order), zero
+// past n_basis up to the kernel width SB
+__global__ void pack_basis_kernel(const double* __restrict__ X, int64_t n, int S, int eta, int nk,
+                                  int SB, double* __restrict__ Xall) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n * SB) return;
+    const int64_t i = e / SB;
+    const int c = (int)(e % SB), j = c / eta, t = c % eta;
+    Xall[e] = j < nk ? X[((int64_t)j * n + i) * S + t] : 0.0;
+}
+
+// Interior noise of sample l, one thread per sample: its own xoshiro256**
+// stream (Rng(derive_seed(sample_seed, "eps")), pipeline.cpp:158-172, 470-503)
+// walked over the interior cells in z, y, x order; uniform(lo, hi) evaluated
+// as the reference build does (fused lo + u (hi - lo)). Boundary-adjacent
+// cells stay zero (the buffer is cleared first).
+__global__ void noise_uniform_kernel(const uint64_t* __restrict__ state, int64_t N, int nx, int ny,
+                                     int nz, double lo, double hi, double* __restrict__ eps) {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l >= N) return;
+    uint64_t s0 = state[4 * l], s1 = state[4 * l + 1], s2 = state[4 * l + 2], s3 = state[4 * l + 3];
+    const int64_t n = (int64_t)nx * ny * nz;
+    double* e = eps + l * n;
+    const double span = hi - lo;
+    for (int iz = 1; iz + 1 < nz; ++iz)
+        for (int iy = 1; iy + 1 < ny; ++iy)
+            for (int ix = 1; ix + 1 < nx; ++ix) {
+                const uint64_t x = s1 * 5;
+                const uint64_t out = ((x << 7) | (x >> 57)) * 9;
+                const uint64_t tt = s1 << 17;
+                s2 ^= s0;
+                s3 ^= s1;
+                s1 ^= s2;
+                s0 ^= s3;
+                s2 ^= tt;
+                s3 = (s3 << 45) | (s3 >> 19);
+                const double u = (double)(out >> 11) * 0x1.0p-53;
+                e[ix + (int64_t)nx * (iy + (int64_t)ny * iz)] = __fma_rn(u, span, lo);
+            }
+}
+
+bk_status generate_blockoa_impl(bk_ctx* ctx, const bk_blockoa_cfg* cfg, double* k_out, double* U,
+                                double* Q, double* resid, int64_t* fp_out,
+                                bk_solve_report* reports, bk_phase_timings* timings) {
+    if (!cfg) return fail(ctx, BK_INVALID_CONFIG, "generate_blockoa: null config");
+    bk_status st = validate_cfg(ctx, &cfg->solver);
+    if (st != BK_OK) return st;
+    // GenerationConfig::validate (pipeline.cpp) and the limits of this path
+    const int nk = cfg->n_k;
+    if (nk < 1 || cfg->n_basis < 1 || cfg->n_basis % nk)
+        return fail(ctx, BK_INVALID_CONFIG, "generate_blockoa: n_basis must be a positive multiple of n_k");
+    if (cfg->n_data < 0) return fail(ctx, BK_INVALID_CONFIG, "generate_blockoa: n_data must be >= 0");
+    const int eta = cfg->n_basis / nk;
+    if (cfg->n_basis > 64 || eta > 32 || nk > 64)
+        return fail(ctx, BK_INVALID_CONFIG,
+                    "generate_blockoa: this path supports n_basis <= 64, eta <= 32, n_k <= 64");
+    if (cfg->noise_kind < BK_NOISE_NONE || cfg->noise_kind > BK_NOISE_GAUSSIAN)
+        return fail(ctx, BK_INVALID_CONFIG, "noise: unknown kind");
+    if (cfg->noise_kind == BK_NOISE_UNIFORM && !(cfg->noise_lo <= cfg->noise_hi))
+        return fail(ctx, BK_INVALID_CONFIG, "noise: uniform needs lo <= hi");
+    if (cfg->noise_kind == BK_NOISE_GAUSSIAN && !(cfg->noise_sigma >= 0.0))
+        return fail(ctx, BK_INVALID_CONFIG, "noise: gaussian needs sigma >= 0");
+    const bk_chip_spec& chip = cfg->chip;
+    bk_grid grid{cfg->nx, cfg->ny, cfg->nz, chip.extent[0], chip.extent[1], chip.extent[2], nullptr};
+    if ((st = validate_grid(ctx, &grid)) != BK_OK) return st;
+    const int64_t n = (int64_t)grid.nx * grid.ny * grid.nz, N = cfg->n_data;
+    const int S = kernel_width(eta), SB = kernel_width(cfg->n_basis);
+
+    cudaEvent_t* ev = ctx->ev;
+    const auto t_host = std::chrono::steady_clock::now();
+    // host: floorplans, k fields, basis power maps (chip model, bit-exact)
+    std::vector<double> kf((size_t)nk * n), qm((size_t)nk * eta * n), qt((size_t)n * eta);
+    if ((st = bk_chip_fields(&chip, grid.nx, grid.ny, grid.nz, nk, eta, cfg->master_seed, kf.data(),
+                             qm.data())) != BK_OK)
+        return fail(ctx, st, "generate_blockoa: invalid chip spec");
+    // weights, group-major columns: group g's samples l = g, g + n_k, ...
+    std::vector<int64_t> off(nk + 1, 0);
+    for (int g = 0; g < nk; ++g) off[g + 1] = off[g] + (N > g ? (N - g + nk - 1) / nk : 0);
+    std::vector<double> w((size_t)cfg->n_basis * std::max<int64_t>(N, 1)), mu(cfg->n_basis);
+    for (int64_t l = 0; l < N; ++l) {
+        bk::draw_weights(cfg->n_basis, cfg->master_seed, l, mu.data());
+        const int64_t col = off[l % nk] + l / nk;
+        for (int c = 0; c < cfg->n_basis; ++c) w[(size_t)c * N + col] = mu[c];
+    }
+    const double host_s =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_host).count();
+
+    void *pStack, *pb, *px, *pxa, *peps = nullptr, *pw, *pseed;
+    if ((st = workspace(ctx, kSlotStackDiag, (size_t)6 * nk * n * sizeof(double), &pStack)) != BK_OK)
+        return st;
+    if ((st = workspace(ctx, kSlotIn2, (size_t)nk * n * S * sizeof(double), &pb)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotOut2, (size_t)nk * n * S * sizeof(double), &px)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotBoaX, (size_t)n * SB * sizeof(double), &pxa)) != BK_OK) return st;
+    if ((st = workspace(ctx, kSlotBoaW, w.size() * sizeof(double), &pw)) != BK_OK) return st;
+    while ((int)ctx->views.size() < nk) ctx->views.push_back(new bk_operator);
+
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[0], ctx->stream));
+    double* const base = (double*)pStack;
+    for (int j = 0; j < nk; ++j) {
+        bk_operator* v = ctx->views[j];
+        double* arr[6];
+        for (int q = 0; q < 6; ++q) arr[q] = base + ((int64_t)q * nk + j) * n;
+        v->diag = arr[0];
+        v->cx = arr[1];
+        v->cy = arr[2];
+        v->cz = arr[3];
+        v->g = arr[4];
+        v->dinv = arr[5];
+        v->n = n;
+        if ((st = assemble_into(ctx, &grid, kf.data() + j * n, cfg->bc, v)) != BK_OK) return st;
+        // maps [t][n] -> cell-major n x eta, then B = V q + g (rhs_from_power)
+        for (int64_t i = 0; i < n; ++i)
+            for (int t = 0; t < eta; ++t) qt[i * eta + t] = qm[((size_t)j * eta + t) * n + i];
+        Staged qd;
+        if ((st = stage_in(ctx, kSlotQ, qt.data(), (size_t)n * eta, &qd)) != BK_OK) return st;
+        BK_CUDA_TRY(ctx, launch_rhs_padded(ctx, v, qd.dev, eta, (double*)pb + (int64_t)j * n * S, S));
+    }
+    BK_CUDA_TRY(ctx, cudaMemcpyAsync(pw, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                     ctx->stream));
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[1], ctx->stream));
+    // ONE batched block-CG launch over the n_k groups (z-stacked, per-group CTA
+    // shares, barriers, reductions and convergence control)
+    std::vector<CgReport> reps(nk);
+    bk_operator stk = *ctx->views[0];
+    stk.nz = grid.nz * nk;
+    stk.n = n * nk;
+    stk.volz = nullptr;
+    stk.h_volz.clear();
+    if ((st = block_cg_device_multi(ctx, &stk, nk, (const double*)pb, S, &cfg->solver, (double*)px,
+                                    reps.data())) != BK_OK)
+        return st;
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[2], ctx->stream));
+    pack_basis_kernel<<<(unsigned)((n * SB + 255) / 256), 256, 0, ctx->stream>>>(
+        (const double*)px, n, S, eta, nk, SB, (double*)pxa);
+    ++ctx->launches;
+    BK_CUDA_TRY(ctx, cudaGetLastError());
+    // noise: device streams (uniform) or host draws (gaussian: libm Box-Muller)
+    if (cfg->noise_kind != BK_NOISE_NONE && N > 0) {
+        if ((st = workspace(ctx, kSlotBoaEps, (size_t)N * n * sizeof(double), &peps)) != BK_OK)
+            return st;
+        if (cfg->noise_kind == BK_NOISE_UNIFORM) {
+            std::vector<uint64_t> states((size_t)4 * N);
+            for (int64_t l = 0; l < N; ++l) {
+                uint64_t sd = bk_derive_seed(
+                    bk_derive_seed(cfg->master_seed, "sample", (uint64_t)(l + 1)), "eps", 0);
+                for (int q = 0; q < 4; ++q) states[4 * l + q] = bk::sm64(sd);
+            }
+            if ((st = workspace(ctx, kSlotBoaSeed, states.size() * sizeof(uint64_t), &pseed)) != BK_OK)
+                return st;
+            BK_CUDA_TRY(ctx, cudaMemcpyAsync(pseed, states.data(), states.size() * sizeof(uint64_t),
+                                             cudaMemcpyHostToDevice, ctx->stream));
+            BK_CUDA_TRY(ctx, cudaMemsetAsync(peps, 0, (size_t)N * n * sizeof(double), ctx->stream));
+            noise_uniform_kernel<<<(unsigned)((N + 63) / 64), 64, 0, ctx->stream>>>(
+                (const uint64_t*)pseed, N, grid.nx, grid.ny, grid.nz, cfg->noise_lo, cfg->noise_hi,
+                (double*)peps);
+            ++ctx->launches;
+            BK_CUDA_TRY(ctx, cudaGetLastError());
+        } else {
+            std::vector<double> eps((size_t)N * n, 0.0);
+            for (int64_t l = 0; l < N; ++l) {
+                bk::Xoshiro rng(bk_derive_seed(
+                    bk_derive_seed(cfg->master_seed, "sample", (uint64_t)(l + 1)), "eps", 0));
+                for (int iz = 1; iz + 1 < grid.nz; ++iz)
+                    for (int iy = 1; iy + 1 < grid.ny; ++iy)
+                        for (int ix = 1; ix + 1 < grid.nx; ++ix)
+                            eps[l * n + ix + (int64_t)grid.nx * (iy + (int64_t)grid.ny * iz)] =
+                                cfg->noise_sigma * rng.normal();
+            }
+            BK_CUDA_TRY(ctx, cudaMemcpyAsync(peps, eps.data(), eps.size() * sizeof(double),
+                                             cudaMemcpyHostToDevice, ctx->stream));
+            BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // eps is a local
+        }
+    }
+    Staged ud, qo, rd;
+    if ((st = stage_out(ctx, kSlotBoaU, U, (size_t)N * n, &ud)) != BK_OK) return st;
+    if ((st = stage_out(ctx, kSlotBoaQ, Q, (size_t)N * n, &qo)) != BK_OK) return st;
+    if ((st = stage_out(ctx, kSlotBoaRes, resid, (size_t)N, &rd)) != BK_OK) return st;
+    // per group: all groups' basis columns, the group's operator, its samples
+    // written with row stride n_k n (sample l = g + m n_k)
+    for (int g = 0; g < nk; ++g) {
+        const int64_t m = off[g + 1] - off[g];
+        if (m == 0) continue;
+        ActExtra ex;
+        ex.ldo = (int64_t)nk * n;
+        ex.rstride = nk;
+        ex.eps = peps ? (const double*)peps + g * n : nullptr;
+        ex.fma = 1;
+        if ((st = combine_action_device(ctx, ctx->views[g], (const double*)pxa, SB, cfg->n_basis,
+                                        (const double*)pw + off[g], N, m,
+                                        ud.dev ? ud.dev + g * n : nullptr,
+                                        qo.dev ? qo.dev + g * n : nullptr,
+                                        rd.dev ? rd.dev + g : nullptr, ex)) != BK_OK)
+            return st;
+    }
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[3], ctx->stream));
+    if ((st = drain(ctx, ud, U, (size_t)N * n)) != BK_OK) return st;
+    if ((st = drain(ctx, qo, Q, (size_t)N * n)) != BK_OK) return st;
+    if ((st = drain(ctx, rd, resid, (size_t)N)) != BK_OK) return st;
+    if (k_out) {
+        BK_CUDA_TRY(ctx, cudaMemcpyAsync(k_out, kf.data(), kf.size() * sizeof(double),
+                                         cudaMemcpyDefault, ctx->stream));
+    }
+    if (fp_out) {
+        std::vector<int64_t> ids(N);
+        for (int64_t l = 0; l < N; ++l) ids[l] = l % nk;  // floorplan id = group index
+        BK_CUDA_TRY(ctx, cudaMemcpyAsync(fp_out, ids.data(), N * sizeof(int64_t), cudaMemcpyDefault,
+                                         ctx->stream));
+        BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    BK_CUDA_TRY(ctx, cudaEventRecord(ev[4], ctx->stream));
+    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    bool all_conv = true;
+    int64_t iters = 0, matvecs = 0;
+    for (int j = 0; j < nk; ++j) {
+        if (reports) fill_report(reps[j], eta, elapsed(ev[1], ev[2]) * 1e-3, &reports[j]);
+        iters += reps[j].iterations;
+        matvecs += reps[j].matvecs;
+        for (int t = 0; t < eta; ++t) all_conv = all_conv && reps[j].converged[t];
+    }
+    if (timings) {
+        std::memset(timings, 0, sizeof(*timings));
+        timings->assemble_s = elapsed(ev[0], ev[1]) * 1e-3 + host_s;
+        timings->basis_solve_s = elapsed(ev[1], ev[2]) * 1e-3;
+        timings->combine_action_s = elapsed(ev[2], ev[3]) * 1e-3;
+        timings->d2h_s = elapsed(ev[3], ev[4]) * 1e-3;
+        timings->total_s = elapsed(ev[0], ev[4]) * 1e-3 + host_s;
+        timings->iterations_total = iters;
+        timings->matvecs_total = matvecs + N;
+    }
+    if (!all_conv) return fail(ctx, BK_NOT_CONVERGED, "basis solve did not reach tolerance");
+    return BK_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -934,6 +1174,17 @@ bk_status bk_generate_batch(bk_ctx* ctx, int n_chips, const bk_grid* grids,
     }
     if (first != BK_OK) return fail(ctx, first, msg);
     return BK_OK;
+}
+
+bk_status bk_generate_blockoa(bk_ctx* ctx, const bk_blockoa_cfg* cfg, double* k, double* U,
+                              double* Q, double* resid, int64_t* floorplan_id,
+                              bk_solve_report* reports, bk_phase_timings* timings) {
+    if (!ctx) return BK_INVALID_CONFIG;
+    try {  // host-side vectors: no exception may cross the C ABI
+        return generate_blockoa_impl(ctx, cfg, k, U, Q, resid, floorplan_id, reports, timings);
+    } catch (const std::bad_alloc&) {
+        return fail(ctx, BK_OOM, "generate_blockoa: host allocation failed");
+    }
 }
 
 }  // extern "C"

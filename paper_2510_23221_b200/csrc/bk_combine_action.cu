@@ -89,6 +89,12 @@ struct ActArgs {
     int tilesx, tiles;
     int chunks, items;  // items = chunks x tiles < 2^31 (checked on the host)
     int s;            // real basis width (<= S)
+    // generate_blockoa extras (bk::ActExtra): output / noise row stride, the
+    // per-sample interior noise added to T before the action, and the
+    // stencil's rounding order
+    int64_t ldo;
+    const double* eps;  // N x ldo (nullable)
+    int fma;            // 1: apply_block's fused chain, 0: scalar apply's mul + add
 };
 
 // correctly rounded x / v given r = RN(1/v) (one Newton-style correction).
@@ -210,20 +216,41 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
         if (prof && pm < 64) g_comb_prof[pm++] = clock64();
     };
 
+    int ix0 = 0, iy0 = 0;  // current item: tile origin and first sample
+    int64_t ij0 = 0;
+    // T + eps at halo cell h of plane z for item sample q (eps is zero outside
+    // the domain, where T is zero-filled too): combine_from_weights' noise add
+    // (pipeline.cpp:220-223, 470-503)
+    auto noisy = [&](double v, int h, int q, int z) {
+        const int gx = ix0 - 1 + h % HX, gy = iy0 - 1 + h / HX;
+        if (gx < 0 || gx >= a.nx || gy < 0 || gy >= a.ny || ij0 + q >= a.N) return v;
+        return __dadd_rn(v, a.eps[(ij0 + q) * a.ldo + gx + (int64_t)a.nx * (gy + (int64_t)a.ny * z)]);
+    };
     // DMMA accumulators of m-tile mt (all NB sample blocks) -> T ring plane buf,
     // sample-major [q][h] (conflict-free: HC = 4 mod 8)
-    auto store_tile = [&](int mt, const double (&ac)[NB][4], double* buf) {
+    auto store_tile = [&](int mt, const double (&ac)[NB][4], double* buf, int z) {
         const int h0 = 16 * mt + g, h1 = h0 + 8;
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) {
             const int q = 8 * nb + 2 * t;
+            double v[4] = {ac[nb][0], ac[nb][1], ac[nb][2], ac[nb][3]};
+            if (a.eps) {
+                if (h0 < HC) {
+                    v[0] = noisy(v[0], h0, q, z);
+                    v[1] = noisy(v[1], h0, q + 1, z);
+                }
+                if (h1 < HC) {
+                    v[2] = noisy(v[2], h1, q, z);
+                    v[3] = noisy(v[3], h1, q + 1, z);
+                }
+            }
             if (h0 < HC) {
-                buf[q * HC + h0] = ac[nb][0];
-                buf[(q + 1) * HC + h0] = ac[nb][1];
+                buf[q * HC + h0] = v[0];
+                buf[(q + 1) * HC + h0] = v[1];
             }
             if (h1 < HC) {
-                buf[q * HC + h1] = ac[nb][2];
-                buf[(q + 1) * HC + h1] = ac[nb][3];
+                buf[q * HC + h1] = v[2];
+                buf[(q + 1) * HC + h1] = v[3];
             }
         }
     };
@@ -266,7 +293,7 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
 #pragma unroll
                     for (int e = 0; e < 4; ++e) ac[nb][e] = 0.0;
                 mma_tile(pan, mt, bf, ac);
-                store_tile(mt, ac, buf);
+                store_tile(mt, ac, buf, z);
             }
             __syncthreads();  // every warp is done with this slot
             if (tid == 0) issue();
@@ -298,7 +325,7 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
             }
 #pragma unroll
             for (int mi = 0; mi < MPW; ++mi)
-                if (warp + NW * mi < MT) store_tile(warp + NW * mi, acc[mi], buf);
+                if (warp + NW * mi < MT) store_tile(warp + NW * mi, acc[mi], buf, z);
         }
     };
 
@@ -311,6 +338,9 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
         const int tile = item / a.chunks;
         const int x0 = (tile % a.tilesx) * TX, y0 = (tile / a.tilesx) * TY;
         const int64_t j0 = (int64_t)chunk * NS;
+        ix0 = x0;
+        iy0 = y0;
+        ij0 = j0;
         prof = blockIdx.x == 0 && tid == 0 && item == 4 * (int)gridDim.x;
         pm = 0;
         mark();
@@ -345,8 +375,8 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
             if (inside) {
                 const int64_t i = gx + (int64_t)a.nx * gy + plane * z;
                 const int64_t jb = j0 + SPT * qh;
-                double* pt = a.T ? a.T + jb * a.n + i : nullptr;
-                double* pq = a.Q ? a.Q + jb * a.n + i : nullptr;
+                double* pt = a.T ? a.T + jb * a.ldo + i : nullptr;
+                double* pq = a.Q ? a.Q + jb * a.ldo + i : nullptr;
                 const int nv = a.N - jb < SPT ? (int)(a.N - jb) : SPT;  // valid samples
                 const double vol = a.volz[z];
                 const double rvol = 1.0 / vol;
@@ -357,14 +387,25 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
                     // coefficient and a zero-filled T: adding the +-0 product
                     // leaves y bitwise unchanged (y is never -0), as skipping does
                     double y = 0.0;
-                    if (hzm) y = __dadd_rn(y, __dmul_rn(k.zm, bm[qq * HC]));
-                    y = __dadd_rn(y, __dmul_rn(k.ym, b0[qq * HC - HX]));
-                    y = __dadd_rn(y, __dmul_rn(k.xm, b0[qq * HC - 1]));
                     const double tc = b0[qq * HC];
-                    y = __dadd_rn(y, __dmul_rn(k.di, tc));
-                    y = __dadd_rn(y, __dmul_rn(k.xp, b0[qq * HC + 1]));
-                    y = __dadd_rn(y, __dmul_rn(k.yp, b0[qq * HC + HX]));
-                    if (hzp) y = __dadd_rn(y, __dmul_rn(k.zp, bp[qq * HC]));
+                    if (!a.fma) {
+                        if (hzm) y = __dadd_rn(y, __dmul_rn(k.zm, bm[qq * HC]));
+                        y = __dadd_rn(y, __dmul_rn(k.ym, b0[qq * HC - HX]));
+                        y = __dadd_rn(y, __dmul_rn(k.xm, b0[qq * HC - 1]));
+                        y = __dadd_rn(y, __dmul_rn(k.di, tc));
+                        y = __dadd_rn(y, __dmul_rn(k.xp, b0[qq * HC + 1]));
+                        y = __dadd_rn(y, __dmul_rn(k.yp, b0[qq * HC + HX]));
+                        if (hzp) y = __dadd_rn(y, __dmul_rn(k.zp, bp[qq * HC]));
+                    } else {
+                        // CsrMatrix::apply_block's chain (discretize.cpp:57-95)
+                        if (hzm) y = __fma_rn(k.zm, bm[qq * HC], y);
+                        y = __fma_rn(k.ym, b0[qq * HC - HX], y);
+                        y = __fma_rn(k.xm, b0[qq * HC - 1], y);
+                        y = __fma_rn(k.di, tc, y);
+                        y = __fma_rn(k.xp, b0[qq * HC + 1], y);
+                        y = __fma_rn(k.yp, b0[qq * HC + HX], y);
+                        if (hzp) y = __fma_rn(k.zp, bp[qq * HC], y);
+                    }
                     const double qv = div_rn(__dsub_rn(y, k.gi), vol, rvol);
                     if (qq < nv) {
                         if (pt) __stcs(pt, tc);
@@ -374,8 +415,8 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
                         num[qq] = fma(rv, rv, num[qq]);
                         den[qq] = fma(bv, bv, den[qq]);
                     }
-                    pt += a.n;
-                    pq += a.n;
+                    pt += a.ldo;
+                    pq += a.ldo;
                 }
             }
             k = kn;
@@ -436,7 +477,7 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
 // sums, then a fixed shuffle tree — deterministic); de == 0 handled as
 // pipeline.cpp:570-571.
 __global__ void resid_finalize(const double* __restrict__ part, int tiles, int64_t N,
-                               double* __restrict__ resid) {
+                               double* __restrict__ resid, int64_t rstride) {
     const int lane = threadIdx.x & 31;
     const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (j >= N) return;
@@ -452,7 +493,7 @@ __global__ void resid_finalize(const double* __restrict__ part, int tiles, int64
         nu += __shfl_xor_sync(0xffffffffu, nu, o);
         de += __shfl_xor_sync(0xffffffffu, de, o);
     }
-    if (lane == 0) resid[j] = de == 0.0 ? (nu == 0.0 ? 0.0 : 1.0) : sqrt(nu / de);
+    if (lane == 0) resid[j * rstride] = de == 0.0 ? (nu == 0.0 ? 0.0 : 1.0) : sqrt(nu / de);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -470,7 +511,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 template <int S, int NS, int NT, bool PL = false>
 bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const double* C,
-              int64_t ldc, int64_t N, double* T, double* Q, double* resid) {
+              int64_t ldc, int64_t N, double* T, double* Q, double* resid,
+              const bk::ActExtra& ex) {
     using namespace bk;
     using P = Panel<S>;
     using SH = Shape<NS, NT>;
@@ -491,6 +533,9 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
     a.T = T;
     a.Q = Q;
     a.s = s;
+    a.ldo = ex.ldo > 0 ? ex.ldo : op->n;
+    a.eps = ex.eps;
+    a.fma = ex.fma;
     a.tilesx = (op->nx + TX - 1) / TX;
     a.tiles = a.tilesx * ((op->ny + TY - 1) / TY);
     const int64_t chunks = (N + NS - 1) / NS;
@@ -547,7 +592,8 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
         fprintf(stderr, " reduce %lld\n", hp[3 + 2 * op->nz] - hp[2 + 2 * op->nz]);
     }
     if (resid) {
-        resid_finalize<<<(unsigned)((N + 7) / 8), 256, 0, ctx->stream>>>(a.part, a.tiles, N, resid);
+        resid_finalize<<<(unsigned)((N + 7) / 8), 256, 0, ctx->stream>>>(a.part, a.tiles, N, resid,
+                                                                       ex.rstride > 0 ? ex.rstride : 1);
         ++ctx->launches;
         BK_CUDA_TRY(ctx, cudaGetLastError());
     }
@@ -561,9 +607,10 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
 // NS = 16 shape gave 5.9 ms on C3 (its DMMA chains and stencil do not overlap).
 template <int S>
 bk_status dispatch(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const double* C,
-                   int64_t ldc, int64_t N, double* T, double* Q, double* resid) {
-    if (op->nz == 1) return run<S, 16, 256, true>(ctx, op, X, s, C, ldc, N, T, Q, resid);
-    return run<S, 8, 256>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+                   int64_t ldc, int64_t N, double* T, double* Q, double* resid,
+                   const bk::ActExtra& ex) {
+    if (op->nz == 1) return run<S, 16, 256, true>(ctx, op, X, s, C, ldc, N, T, Q, resid, ex);
+    return run<S, 8, 256>(ctx, op, X, s, C, ldc, N, T, Q, resid, ex);
 }
 
 }  // namespace
@@ -574,14 +621,14 @@ namespace bk {
 // s x N with row stride ldc.
 bk_status combine_action_device(bk_ctx* ctx, const bk_operator* op, const double* X, int S,
                                 int s, const double* C, int64_t ldc, int64_t N, double* T,
-                                double* Q, double* resid) {
+                                double* Q, double* resid, const ActExtra& ex) {
     if (N == 0) return BK_OK;
     if (s < 1 || s > S || ldc < N) return fail(ctx, BK_INTERNAL, "combine_action: bad widths");
     switch (S) {
-        case 8: return dispatch<8>(ctx, op, X, s, C, ldc, N, T, Q, resid);
-        case 16: return dispatch<16>(ctx, op, X, s, C, ldc, N, T, Q, resid);
-        case 32: return dispatch<32>(ctx, op, X, s, C, ldc, N, T, Q, resid);
-        case 64: return dispatch<64>(ctx, op, X, s, C, ldc, N, T, Q, resid);
+        case 8: return dispatch<8>(ctx, op, X, s, C, ldc, N, T, Q, resid, ex);
+        case 16: return dispatch<16>(ctx, op, X, s, C, ldc, N, T, Q, resid, ex);
+        case 32: return dispatch<32>(ctx, op, X, s, C, ldc, N, T, Q, resid, ex);
+        case 64: return dispatch<64>(ctx, op, X, s, C, ldc, N, T, Q, resid, ex);
         default: return fail(ctx, BK_INTERNAL, "combine_action: unpadded width");
     }
 }

@@ -43,7 +43,7 @@ struct bk_ctx {
     size_t pin_bytes = 0;
     cudaEvent_t stage_ev[4] = {};
     // grow-only device workspace slots
-    static constexpr int kSlots = 32;
+    static constexpr int kSlots = 40;
     void* ws[kSlots] = {};
     size_t ws_bytes[kSlots] = {};
 };
@@ -102,6 +102,13 @@ enum Slot : int {
     kSlotStackDiag, // z-stacked operator of the batched pipeline (6 arrays)
     kSlotStackCoef, // per-chip combination coefficients of the batched pipeline
     kSlotValRes,    // per-sample residuals of bk_residuals / bk_validate_samples
+    kSlotBoaX,      // bk_generate_blockoa: all groups' basis columns (n x SB)
+    kSlotBoaEps,    //   per-sample interior noise (n_data x n)
+    kSlotBoaW,      //   weights (n_basis x n_data, group-major columns)
+    kSlotBoaSeed,   //   noise stream states
+    kSlotBoaU,      //   staged outputs
+    kSlotBoaQ,
+    kSlotBoaRes,
 };
 
 bk_status fail(bk_ctx* ctx, bk_status st, const std::string& msg);
@@ -162,8 +169,19 @@ bk_status block_cg_generic(bk_ctx* ctx, const bk_operator* op, const double* B, 
 // launch, chip k on an equal SM share (S = 8, 16, 32). reps: K reports.
 bk_status block_cg_device_multi(bk_ctx* ctx, const bk_operator* op, int K, const double* B, int S,
                                 const bk_solver_cfg* cfg, double* X, CgReport* reps);
+// generate_blockoa's variant of the fused combine + action (bk_generate_blockoa):
+// outputs (and eps) with row stride ldo (0: n), resid with stride rstride
+// (0: 1), per-sample interior noise eps added to T before the action, and
+// apply_block's fused-multiply-add stencil order (fma = 1) instead of the
+// scalar apply's multiply + add.
+struct ActExtra {
+    int64_t ldo = 0;
+    int64_t rstride = 0;
+    const double* eps = nullptr;
+    int fma = 0;
+};
 bk_status combine_action_device(bk_ctx* ctx, const bk_operator* op, const double* X, int S,
                                 int s, const double* C, int64_t ldc, int64_t N, double* T,
-                                double* Q, double* resid);
+                                double* Q, double* resid, const ActExtra& ex = ActExtra{});
 
 }  // namespace bk

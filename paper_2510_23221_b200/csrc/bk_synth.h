@@ -2,12 +2,75 @@
 // generator and the device one (bk_synth_dev.cu). Plain C++.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <vector>
 
 #include "blockoa_b200.h"
 
 namespace bk {
+
+// Rng (rng.hpp:14-63) restated bit-exactly: xoshiro256** seeded by splitmix64,
+// 53-bit uniforms, cached Box-Muller pairs, rejection-sampled integers.
+inline std::uint64_t sm64(std::uint64_t& st) {
+    std::uint64_t z = (st += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+class Xoshiro {
+public:
+    explicit Xoshiro(std::uint64_t seed) {
+        std::uint64_t st = seed;
+        for (auto& w : s_) w = sm64(st);
+    }
+    std::uint64_t next() {
+        const std::uint64_t out = rotl(s_[1] * 5, 7) * 9;
+        const std::uint64_t t = s_[1] << 17;
+        s_[2] ^= s_[0];
+        s_[3] ^= s_[1];
+        s_[1] ^= s_[2];
+        s_[0] ^= s_[3];
+        s_[2] ^= t;
+        s_[3] = rotl(s_[3], 45);
+        return out;
+    }
+    double u01() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + u01() * (hi - lo); }
+    // the same draw as the reference build evaluates it where GCC contracts
+    // the inlined lo + u * (hi - lo) into one fused multiply-add (chip.cpp,
+    // pipeline.cpp call sites; pinned bitwise by tests/test_chip.py)
+    double uniform_fma(double lo, double hi) { return std::fma(u01(), hi - lo, lo); }
+    double normal() {
+        if (have_) {
+            have_ = false;
+            return spare_;
+        }
+        const double u1 = 1.0 - u01();
+        const double u2 = u01();
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        const double th = 2.0 * 3.141592653589793 * u2;
+        spare_ = r * std::sin(th);
+        have_ = true;
+        return r * std::cos(th);
+    }
+    std::uint64_t below(std::uint64_t n) {
+        const std::uint64_t lim = n * (~std::uint64_t{0} / n);
+        std::uint64_t x;
+        do {
+            x = next();
+        } while (x >= lim);
+        return x % n;
+    }
+
+private:
+    static std::uint64_t rotl(std::uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+    std::uint64_t s_[4];
+    double spare_ = 0.0;
+    bool have_ = false;
+};
+
 
 struct SynthPlan {
     int config = 0, nx = 0, ny = 0, nz = 0, s = 0;
