@@ -508,6 +508,9 @@ def run_ours(args):
     dataset = None
     if rank == 0 and not args.no_dataset:
         dataset = dataset_leg(bk, torch, ctx, stream, inp, k_d, T_d, Q_d, R_d, peak)
+    refpipe = None
+    if rank == 0 and not args.no_refpipe:
+        refpipe = reference_pipeline_leg(bk, torch, ctx)
 
     if rank != 0:
         if world > 1:
@@ -567,12 +570,77 @@ def run_ours(args):
         "max_sample_residual": max_resid,
         "direct_cg_baseline": direct,
         "dataset": dataset,
+        "reference_pipeline": refpipe,
     }
     print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def reference_pipeline_leg(bk, torch, ctx, reps=3):
+    """the reference's own generate_blockoa on configs/default.json
+    (24 x 24 x 12 over the default chip, 5 floorplans x 10 basis maps, 500
+    samples, uniform noise, rel_tol 1e-9) through bk_generate_blockoa — device
+    outputs, and host outputs (U, Q, resid copied back inside the timed call) —
+    against the reference build running the same call on this host (threads =
+    1, the reference default, and all cores: it parallelises over floorplan
+    groups). Wall clock around synchronised calls (host chip model included)."""
+    import time
+
+    cfg = bk.GenerationConfig.default_run_config()
+    n, N = 24 * 24 * 12, cfg.n_data
+    dev = torch.device("cuda", 0)
+    U = torch.empty((N, n), dtype=torch.float64, device=dev)
+    Q, R = torch.empty_like(U), torch.empty(N, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        bk.generate_blockoa(cfg, u_out=U, q_out=Q, resid_out=R, ctx=ctx)
+    t_dev, t_host = [], []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = bk.generate_blockoa(cfg, u_out=U, q_out=Q, resid_out=R, ctx=ctx)
+        torch.cuda.synchronize()
+        t_dev.append(time.perf_counter() - t0)
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        h = bk.generate_blockoa(cfg, ctx=ctx)
+        t_host.append(time.perf_counter() - t0)
+    out = {"workload": "configs/default.json: 24x24x12, n_k=5, n_basis=50, n_data=500, "
+                       "uniform noise, rel_tol 1e-9",
+           "value": N / min(t_dev), "unit": "samples/s", "ms": min(t_dev) * 1e3,
+           "e2e": {"value": N / min(t_host), "unit": "samples/s", "ms": min(t_host) * 1e3,
+                   "d2h_bytes": int((2 * n * N + N) * 8)},
+           "phase_ms": {"basis_solve": r.timings.basis_solve_s * 1e3,
+                        "combine_action": r.timings.combine_action_s * 1e3,
+                        "host_and_assemble": r.timings.assemble_s * 1e3},
+           "iterations_total": int(r.timings.iterations_total), "reference": None}
+    try:
+        from oracle.oracle import Reference, reference_available
+        if reference_available():
+            ref = Reference()
+            runs = {}
+            for thr in sorted({1, os.cpu_count() or 1}):
+                d = ref.generate_blockoa(cfg.grid, N, cfg.n_basis, cfg.n_k, cfg.master_seed,
+                                         cfg.bc.as_tuples(), ("uniform", -0.01, 0.01), 1e-9, 50000,
+                                         threads=thr)
+                runs[thr] = d
+            best = min(runs, key=lambda t: runs[t]["total_s"])
+            d = runs[best]
+            out["reference"] = {
+                "value": N / d["total_s"], "unit": "samples/s", "ms": d["total_s"] * 1e3,
+                "cores": best, "basis_ms": d["basis_s"] * 1e3, "iterations_total": d["iterations"],
+                "by_threads_ms": {str(t): runs[t]["total_s"] * 1e3 for t in runs},
+                "kind": "reference (oracle/_ref, unmodified core)"}
+            out["speedup_vs_reference"] = d["total_s"] / min(t_dev)
+            out["speedup_vs_reference_e2e"] = d["total_s"] / min(t_host)
+            rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+            out["max_rel_l2_u"] = max(rel(h.u[l], d["u"][l]) for l in range(N))
+            out["max_rel_l2_q"] = max(rel(h.q[l], d["q"][l]) for l in range(N))
+    except Exception as e:  # the leg is informative; the headline line must still print
+        out["reference_error"] = repr(e)
+    return out
 
 
 def dataset_leg(bk, torch, ctx, stream, inp, k_d, T_d, Q_d, R_d, peak):
@@ -855,6 +923,8 @@ def main():
                     help="skip the dataset sink / validation leg (SURVEY 8(f2))")
     ap.add_argument("--no-direct", action="store_true",
                     help="skip the per-sample CG (direct) baseline")
+    ap.add_argument("--no-refpipe", action="store_true",
+                    help="skip the reference-semantics generate_blockoa leg (SURVEY 8(f3))")
     ap.add_argument("--ref-iter-cap", type=int, default=24)
     ap.add_argument("--ref-action-samples", type=int, default=64)
     args = ap.parse_args()
