@@ -147,15 +147,19 @@ struct Coef {
     bool hxm, hxp, hym, hyp, hzm, hzp;
 };
 
+// zlo / zhi: the z range of the cell's chip. A z-stacked batch couples its
+// chips through zero face conductances only; skipping those z terms (as the
+// single chip has no z neighbour there) leaves every sum bitwise unchanged and
+// saves two P-row loads per cell of a stacked 2D chip.
 __device__ __forceinline__ void load_coef_at(const Args& a, int64_t c, int ix, int iy, int iz,
-                                             Coef& k) {
+                                             int zlo, int zhi, Coef& k) {
     const int64_t plane = (int64_t)a.nx * a.ny;
-    k.hzm = iz > 0;
+    k.hzm = iz > zlo;
     k.hym = iy > 0;
     k.hxm = ix > 0;
     k.hxp = ix < a.nx - 1;
     k.hyp = iy < a.ny - 1;
-    k.hzp = iz < a.nz - 1;
+    k.hzp = iz < zhi;
     k.d = a.diag[c];
     k.zm = k.hzm ? -a.cz[c - plane] : 0.0;
     k.ym = k.hym ? -a.cy[c - a.nx] : 0.0;
@@ -167,9 +171,9 @@ __device__ __forceinline__ void load_coef_at(const Args& a, int64_t c, int ix, i
     k.oym = a.nx;
 }
 
-__device__ __forceinline__ void load_coef(const Args& a, int64_t c, Coef& k) {
+__device__ __forceinline__ void load_coef(const Args& a, int64_t c, int zlo, int zhi, Coef& k) {
     const int ci = (int)c;
-    load_coef_at(a, c, ci % a.nx, (ci / a.nx) % a.ny, ci / (a.nx * a.ny), k);
+    load_coef_at(a, c, ci % a.nx, (ci / a.nx) % a.ny, ci / (a.nx * a.ny), zlo, zhi, k);
 }
 
 // grid coordinates of cell c, then stepped by `d` cells (no division per step)
@@ -406,8 +410,9 @@ __device__ __forceinline__ void small_solve(Sm<S, RES>& sm, const double* M, con
 // (apply_block_fixed, discretize.cpp:57-71); W leaves with 128-bit stores, and
 // P / W are staged in the warp's smem tiles for the DMMA Gram (K = cells).
 template <int S>
-__device__ __forceinline__ void phase_spmm_gram(const Args& a, int64_t c0, int64_t c1, int warp,
-                                                int lane, double* tp, double* tw, GramAcc<S>& G) {
+__device__ __forceinline__ void phase_spmm_gram(const Args& a, int64_t c0, int64_t c1, int zlo,
+                                                int zhi, int warp, int lane, double* tp,
+                                                double* tw, GramAcc<S>& G) {
     constexpr int NW = CtaShape<S>::NW;
     constexpr int RS = Strides<S>::RS;
     constexpr int LPR = S / 2;     // lanes per row (one 16-byte column pair each)
@@ -427,7 +432,7 @@ __device__ __forceinline__ void phase_spmm_gram(const Args& a, int64_t c0, int64
             double2 acc = make_double2(0.0, 0.0), ctr = make_double2(0.0, 0.0);
             if (cell < c1) {
                 Coef k;
-                load_coef_at(a, cell, xyz.ix, xyz.iy, xyz.iz, k);
+                load_coef_at(a, cell, xyz.ix, xyz.iy, xyz.iz, zlo, zhi, k);
                 auto row = [&](int64_t c, double coef, bool has) {
                     if (!has) return;
                     const double2 x = *reinterpret_cast<const double2*>(a.P + c * S + col);
@@ -686,6 +691,9 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
     const int64_t ntiles = (nchip + 15) / 16;
     const int64_t c0 = cbase + 16 * (ntiles * b / NB);
     const int64_t c1 = b == NB - 1 ? cbase + nchip : cbase + 16 * (ntiles * (b + 1) / NB);
+    // the chip's z range inside the z-stacked batch (the whole grid otherwise)
+    const int nzc = MULTI ? a.nz / a.nchips : a.nz;
+    const int zlo = gr.chip * nzc, zhi = zlo + nzc - 1;
     double* const partc = MULTI ? a.part + (int64_t)gr.chip * NB * (S * S + S) : a.part;
     double* const redc = MULTI ? a.red + (int64_t)gr.chip * (S * S + S) : a.red;
     bk::CgReport* const repc = MULTI ? a.rep + gr.chip : a.rep;
@@ -775,7 +783,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         if (pm) pm[0] = gtimer();
         // ---- phase 1: W = A P, G = P^T W
         G.zero();
-        phase_spmm_gram<S>(a, c0, c1, warp, lane, tr, tz, G);
+        phase_spmm_gram<S>(a, c0, c1, zlo, zhi, warp, lane, tr, tz, G);
         if (pm) pm[8] = gtimer();
         G.spill(scr + warp * kScrStride, g, t);
         cta_sum_mat<S>(scr, kScrStride, sm.aug);
@@ -851,7 +859,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
                     const int64_t cell = base + g + 8 * h;
                     if (cell >= c1) continue;
                     Coef k;
-                    load_coef(a, cell, k);
+                    load_coef(a, cell, zlo, zhi, k);
 #pragma unroll
                     for (int n = 0; n < NT; ++n)
 #pragma unroll
@@ -894,7 +902,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
                     const int64_t cell = base + g + 8 * h;
                     const bool v = cell < c1;
                     Coef k;
-                    if (v) load_coef(a, cell, k);
+                    if (v) load_coef(a, cell, zlo, zhi, k);
                     const double di = dinv_of(cell);
 #pragma unroll
                     for (int n = 0; n < NT; ++n)
@@ -958,7 +966,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
                 const int64_t cell = base + g + 8 * h;
                 if (cell >= c1) continue;
                 Coef k;
-                load_coef(a, cell, k);
+                load_coef(a, cell, zlo, zhi, k);
 #pragma unroll
                 for (int n = 0; n < NT; ++n)
 #pragma unroll
