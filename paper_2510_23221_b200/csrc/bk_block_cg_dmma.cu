@@ -65,6 +65,7 @@ struct Args {
     int precond;
     bk::CgReport* rep;
     long long* prof;  // optional phase timestamps (CTA 0), PROF_ITERS x PROF_MARKS
+    int ring;         // phase 1 through the row ring (phase_spmm_gram_ring)
     // several independent chips of identical dims in one launch: chip k owns
     // cells [k nchip, (k+1) nchip) of the z-stacked (block-diagonal) system,
     // CTAs [k cpc, (k+1) cpc), reduction partials part + k cpc (S^2+S),
@@ -471,6 +472,150 @@ __device__ __forceinline__ void phase_spmm_gram(const Args& a, int64_t c0, int64
     }
 }
 
+// ---------------------------------------------------------------------------
+// phase 1 through a shared-memory row ring (single-plane chips outside
+// resident mode: the batched C2 solve). The per-tile version above keeps only
+// one tile's loads in flight per warp (~2.4 KB): at 16 warps per SM that is
+// below the bytes in flight DRAM needs, and the batched sweep ran at 2.9 TB/s.
+// Here thread 0 streams whole x-rows — the P row (nx S doubles) and the diag,
+// cx, cy rows — into a 4-slot ring by TMA bulk copies (mbarrier completion)
+// two rows ahead of the row the warps sweep, so each row's P arrives once and
+// the y +- 1 neighbours are read from shared memory. Same per-element FMA
+// chain, same 16-cell Gram tiles (in row order): bitwise the per-tile sweep's
+// W; the Gram partials are summed in a different tile order.
+// ---------------------------------------------------------------------------
+constexpr int kRing = 4;
+__device__ __forceinline__ unsigned sm_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void ring_expect(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void ring_copy(void* dst, const void* src, unsigned bytes,
+                                          unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(sm_u32(dst)),
+        "l"(src), "r"(bytes), "r"(sm_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void ring_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tRGW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra RGW_%=;\n\t}" ::"r"(sm_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+struct Ring {
+    double* P;                // kRing x nx S
+    double* C;                // kRing x 3 nx: diag, cx, cy rows
+    unsigned long long* bar;  // kRing
+    unsigned ph;              // per-slot parity bits (uniform across the CTA)
+};
+
+template <int S>
+__device__ void phase_spmm_gram_ring(const Args& a, int64_t c0, int64_t c1, int64_t rlo,
+                                     int64_t rhi, int warp, int lane, Ring& rg, double* tw,
+                                     GramAcc<S>& G) {
+    constexpr int NW = CtaShape<S>::NW;
+    constexpr int RS = Strides<S>::RS;
+    constexpr int LPR = S / 2, CPI = 32 / LPR, U = 16 / CPI;
+    const int nx = a.nx;
+    const int q = lane / LPR, col = 2 * (lane % LPR);
+    const int g = lane >> 2, t = lane & 3;
+    const int64_t r0 = c0 / nx, r1 = (c1 - 1) / nx;
+    // rows the sweep reads: r0 - 1 .. r1 + 1, inside the chip
+    const int64_t ra = r0 - 1 > rlo ? r0 - 1 : rlo, rb = r1 + 1 < rhi ? r1 + 1 : rhi;
+    const unsigned pbytes = (unsigned)nx * S * 8, cbytes = (unsigned)nx * 8;
+    auto issue = [&](int64_t r) {  // thread 0
+        if (r < ra || r > rb) return;
+        const int sl = (int)(r & (kRing - 1));
+        ring_expect(&rg.bar[sl], pbytes + 3 * cbytes);
+        ring_copy(rg.P + (int64_t)sl * nx * S, a.P + r * nx * S, pbytes, &rg.bar[sl]);
+        double* cs = rg.C + (int64_t)sl * 3 * nx;
+        ring_copy(cs, a.diag + r * nx, cbytes, &rg.bar[sl]);
+        ring_copy(cs + nx, a.cx + r * nx, cbytes, &rg.bar[sl]);
+        ring_copy(cs + 2 * nx, a.cy + r * nx, cbytes, &rg.bar[sl]);
+    };
+    auto wait_row = [&](int64_t r) {  // every thread, once per issued row
+        if (r < ra || r > rb) return;
+        const int sl = (int)(r & (kRing - 1));
+        ring_wait(&rg.bar[sl], (rg.ph >> sl) & 1u);
+        rg.ph ^= 1u << sl;
+    };
+    if (threadIdx.x == 0) {
+        // the ring's previous contents were read / written by the generic proxy
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int64_t r = ra; r <= r0 + 2; ++r) issue(r);
+    }
+    wait_row(r0 - 1);
+    wait_row(r0);
+    for (int64_t r = r0; r <= r1; ++r) {
+        wait_row(r + 1);
+        const int64_t cs = r * nx > c0 ? r * nx : c0;
+        const int64_t ce = (r + 1) * nx < c1 ? (r + 1) * nx : c1;
+        const int iy = (int)(r % a.ny);
+        const bool hym = iy > 0 && r - 1 >= rlo, hyp = iy < a.ny - 1 && r + 1 <= rhi;
+        const double* Pm = rg.P + (int64_t)((r - 1) & (kRing - 1)) * nx * S;
+        const double* P0 = rg.P + (int64_t)(r & (kRing - 1)) * nx * S;
+        const double* Pp = rg.P + (int64_t)((r + 1) & (kRing - 1)) * nx * S;
+        const double* C0 = rg.C + (int64_t)(r & (kRing - 1)) * 3 * nx;
+        const double* cym = rg.C + (int64_t)((r - 1) & (kRing - 1)) * 3 * nx + 2 * nx;
+        const int ntile = (int)((ce - cs + 15) / 16);
+        for (int j = warp; j < ntile; j += NW) {
+            const int64_t base = cs + 16 * j;
+            const int xb = (int)(base - r * nx);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int lr = q + CPI * u;
+                const int x = xb + lr;
+                double2 acc = make_double2(0.0, 0.0);
+                if (base + lr < ce) {
+                    // CSR order y-, x-, diag, x+, y+ (single plane: no z terms)
+                    const bool hxm = x > 0, hxp = x < nx - 1;
+                    auto row = [&](const double* src, double coef) {
+                        const double2 v = *reinterpret_cast<const double2*>(src + col);
+                        acc.x = fma(coef, v.x, acc.x);
+                        acc.y = fma(coef, v.y, acc.y);
+                    };
+                    if (hym) row(Pm + x * S, -cym[x]);
+                    if (hxm) row(P0 + (x - 1) * S, -C0[nx + x - 1]);
+                    row(P0 + x * S, C0[x]);
+                    if (hxp) row(P0 + (x + 1) * S, -C0[nx + x]);
+                    if (hyp) row(Pp + x * S, -C0[2 * nx + x]);
+                    *reinterpret_cast<double2*>(a.W + (base + lr) * S + col) = acc;
+                }
+                *reinterpret_cast<double2*>(tw + lr * RS + col) = acc;
+            }
+            __syncwarp();
+            // G += P^T W over the tile's 16 cells: P straight from the ring row
+            // (rows past the range contribute 0 through W = 0)
+            const double* tp = P0 + xb * S;
+            const int nv = (int)(ce - base < 16 ? ce - base : 16);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const int c4 = 4 * kk + t;
+#pragma unroll
+                for (int m = 0; m < GramAcc<S>::MT; ++m) {
+                    const double a0 = c4 < nv ? tp[c4 * S + 16 * m + g] : 0.0;
+                    const double a1 =
+                        (c4 < nv && 16 * m + 8 + g < S) ? tp[c4 * S + 16 * m + 8 + g] : 0.0;
+#pragma unroll
+                    for (int n = 0; n < GramAcc<S>::NT; ++n)
+                        if (gram_tile_needed(m, n)) dmma(G.d[m][n], a0, a1, tw[c4 * RS + 8 * n + g]);
+                }
+            }
+            __syncwarp();
+        }
+        __syncthreads();  // row r - 1's slot is free
+        if (threadIdx.x == 0) issue(r + 3);
+    }
+}
+
 // Rows [base, base + 16) of V (n x S) into the warp tile T[16][RS] by
 // cp.async whole-row 16-byte copies (rows past c1 zero-filled). The caller
 // commits / waits; __syncwarp before reading.
@@ -701,6 +846,22 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
     const bool prof = a.prof != nullptr && gr.chip == 0 && b == 0 && tid == 0;
     double* tr = sm.tileR[warp];
     double* tz = sm.tileZ[warp];
+    // row ring of phase 1 (a.ring): coefficient rows in the tileR area (free
+    // during phase 1), P rows and the slot barriers past Sm
+    Ring rg;
+    rg.C = &sm.tileR[0][0];
+    rg.P = reinterpret_cast<double*>(smem_raw + (sizeof(Sm<S, RES>) + 15) / 16 * 16);
+    rg.bar = reinterpret_cast<unsigned long long*>(rg.P + (int64_t)kRing * a.nx * S);
+    rg.ph = 0;
+    if (a.ring) {
+        if (tid == 0) {
+            for (int i = 0; i < kRing; ++i)
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(&rg.bar[i])));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    const int64_t rlo = cbase / a.nx, rhi = (cbase + nchip) / a.nx - 1;  // the chip's x-rows
 
     double* xres = nullptr;
     double* rres = nullptr;
@@ -783,7 +944,10 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         if (pm) pm[0] = gtimer();
         // ---- phase 1: W = A P, G = P^T W
         G.zero();
-        phase_spmm_gram<S>(a, c0, c1, zlo, zhi, warp, lane, tr, tz, G);
+        if (a.ring)
+            phase_spmm_gram_ring<S>(a, c0, c1, rlo, rhi, warp, lane, rg, tz, G);
+        else
+            phase_spmm_gram<S>(a, c0, c1, zlo, zhi, warp, lane, tr, tz, G);
         if (pm) pm[8] = gtimer();
         G.spill(scr + warp * kScrStride, g, t);
         cta_sum_mat<S>(scr, kScrStride, sm.aug);
@@ -997,6 +1161,21 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
     }
 }
 
+// Row-ring phase 1 (phase_spmm_gram_ring) for single-plane chips outside
+// resident mode when the ring fits; BK_CG_RING=0/1 overrides (A/B).
+template <int S>
+size_t ring_bytes(int nx) {
+    return 16 + (size_t)kRing * nx * S * sizeof(double) + kRing * sizeof(unsigned long long);
+}
+template <int S>
+bool want_ring(bool resident, int nx, int nz_chip) {
+    if (resident || nz_chip != 1 || nx % 16 != 0 || S > 16) return false;
+    if ((size_t)3 * kRing * nx > (size_t)CtaShape<S>::NW * 16 * Strides<S>::RS) return false;
+    if (sizeof(Sm<S, false>) + ring_bytes<S>(nx) > 232448) return false;
+    if (const char* e = getenv("BK_CG_RING")) return atoi(e) != 0;
+    return true;
+}
+
 template <int S>
 bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
                    const bk_solver_cfg* cfg, double* X, bk::CgReport* rep) {
@@ -1015,7 +1194,9 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
     const bool resident = S <= 16 && max_cells <= kResCells && getenv("BK_CG_NO_RESIDENT") == nullptr;
     const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, false>
                                 : (const void*)block_cg_dmma_kernel<S, false, false>;
-    const size_t smem = resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>);
+    const bool ring = want_ring<S>(resident, op->nx, op->nz);
+    const size_t smem = (resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>)) +
+                        (ring ? ring_bytes<S>(op->nx) : 0);
     BK_CUDA_TRY(ctx, bk::set_max_smem((const void*)kern, smem));
     int occ = 0;
     BK_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BS, smem));
@@ -1068,6 +1249,7 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
     a.cpc = (int)nb;
     a.nchip = n;
     a.bars = nullptr;
+    a.ring = ring;
     const bool want_prof = getenv("BK_CG_PROFILE") != nullptr;
     a.prof = want_prof ? (long long*)((char*)pRep + sizeof(CgReport)) : nullptr;
     if (want_prof)
@@ -1134,7 +1316,9 @@ bk_status run_dmma_multi(bk_ctx* ctx, const bk_operator* op, int K, const double
     const bool resident = S <= 16 && max_cells <= kResCells && getenv("BK_CG_NO_RESIDENT") == nullptr;
     const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, true>
                                 : (const void*)block_cg_dmma_kernel<S, false, true>;
-    const size_t smem = resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>);
+    const bool ring = want_ring<S>(resident, op->nx, op->nz / K);
+    const size_t smem = (resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>)) +
+                        (ring ? ring_bytes<S>(op->nx) : 0);
     BK_CUDA_TRY(ctx, set_max_smem(kern, smem));
     int occ = 0;
     BK_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BS, smem));
@@ -1193,6 +1377,7 @@ bk_status run_dmma_multi(bk_ctx* ctx, const bk_operator* op, int K, const double
     a.cpc = cpc;
     a.nchip = nchip;
     a.bars = (unsigned*)pBar;
+    a.ring = ring;
     void* args[] = {&a};
     BK_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(kern, dim3((unsigned)nb), dim3(BS), args, smem,
                                                  ctx->stream));
