@@ -110,3 +110,19 @@ def test_config_errors(bk, ctx):
     cfg.n_basis, cfg.n_k = 66, 2
     with pytest.raises(bk.InvalidConfigError):
         bk.generate_blockoa(cfg, ctx=ctx)
+
+
+@pytest.mark.parametrize("n_data,n_k,n_basis", [(3, 5, 50), (0, 2, 8), (7, 1, 8)])
+def test_ragged_sample_counts_vs_reference(bk, ctx, reference, n_data, n_k, n_basis):
+    """Groups without samples (n_data < n_k), no samples at all, one group."""
+    cfg = bk.GenerationConfig.default_run_config()
+    cfg.grid, cfg.n_data, cfg.n_k, cfg.n_basis = (12, 10, 6), n_data, n_k, n_basis
+    cfg.solver.rel_tol = 1e-12
+    r = bk.generate_blockoa(cfg, ctx=ctx)
+    assert r.u.shape == (n_data, 720) and len(r.reports) == n_k
+    if n_data == 0:
+        return
+    d = _ref(reference, cfg)
+    assert np.array_equal(r.floorplan_id, d["floorplan_id"])
+    for l in range(n_data):
+        assert rel_l2(r.u[l], d["u"][l]) <= PARITY and rel_l2(r.q[l], d["q"][l]) <= PARITY, l
