@@ -416,10 +416,15 @@ __device__ __forceinline__ void phase_spmm_gram(const Args& a, int64_t c0, int64
                                                 double* tw, GramAcc<S>& G) {
     constexpr int NW = CtaShape<S>::NW;
     constexpr int RS = Strides<S>::RS;
-    constexpr int LPR = S / 2;     // lanes per row (one 16-byte column pair each)
+    // columns per lane: 2 (one 16-byte pair) up to S = 16; 4 for S = 32, which
+    // halves the cells per lane per tile (U = 4 instead of 8) and with them the
+    // dependent load / FMA rounds of the per-tile sweep
+    constexpr int CPL = S >= 32 ? 4 : 2;
+    constexpr int H = CPL / 2;     // 16-byte column pairs per lane
+    constexpr int LPR = S / CPL;   // lanes per row
     constexpr int CPI = 32 / LPR;  // cells per load instruction
     constexpr int U = 16 / CPI;    // cells per lane per tile
-    const int q = lane / LPR, col = 2 * (lane % LPR);
+    const int q = lane / LPR, col = CPL * (lane % LPR);
     const int g = lane >> 2, t = lane & 3;
     const int64_t plane = (int64_t)a.nx * a.ny;
     for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
@@ -430,29 +435,42 @@ __device__ __forceinline__ void phase_spmm_gram(const Args& a, int64_t c0, int64
             const int lr = q + CPI * u;  // row of the tile
             const int64_t cell = base + lr;
             if (u > 0) xyz.step(a, CPI);
-            double2 acc = make_double2(0.0, 0.0), ctr = make_double2(0.0, 0.0);
+            double2 acc[H], ctr[H];
+#pragma unroll
+            for (int h = 0; h < H; ++h) acc[h] = ctr[h] = make_double2(0.0, 0.0);
             if (cell < c1) {
                 Coef k;
                 load_coef_at(a, cell, xyz.ix, xyz.iy, xyz.iz, zlo, zhi, k);
                 auto row = [&](int64_t c, double coef, bool has) {
                     if (!has) return;
-                    const double2 x = *reinterpret_cast<const double2*>(a.P + c * S + col);
-                    acc.x = fma(coef, x.x, acc.x);
-                    acc.y = fma(coef, x.y, acc.y);
+#pragma unroll
+                    for (int h = 0; h < H; ++h) {
+                        const double2 x = *reinterpret_cast<const double2*>(a.P + c * S + col + 2 * h);
+                        acc[h].x = fma(coef, x.x, acc[h].x);
+                        acc[h].y = fma(coef, x.y, acc[h].y);
+                    }
                 };
                 row(cell - plane, k.zm, k.hzm);
                 row(cell - a.nx, k.ym, k.hym);
                 row(cell - 1, k.xm, k.hxm);
-                ctr = *reinterpret_cast<const double2*>(a.P + cell * S + col);
-                acc.x = fma(k.d, ctr.x, acc.x);
-                acc.y = fma(k.d, ctr.y, acc.y);
+#pragma unroll
+                for (int h = 0; h < H; ++h) {
+                    ctr[h] = *reinterpret_cast<const double2*>(a.P + cell * S + col + 2 * h);
+                    acc[h].x = fma(k.d, ctr[h].x, acc[h].x);
+                    acc[h].y = fma(k.d, ctr[h].y, acc[h].y);
+                }
                 row(cell + 1, k.xp, k.hxp);
                 row(cell + a.nx, k.yp, k.hyp);
                 row(cell + plane, k.zp, k.hzp);
-                *reinterpret_cast<double2*>(a.W + cell * S + col) = acc;
+#pragma unroll
+                for (int h = 0; h < H; ++h)
+                    *reinterpret_cast<double2*>(a.W + cell * S + col + 2 * h) = acc[h];
             }
-            *reinterpret_cast<double2*>(tp + lr * RS + col) = ctr;
-            *reinterpret_cast<double2*>(tw + lr * RS + col) = acc;
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                *reinterpret_cast<double2*>(tp + lr * RS + col + 2 * h) = ctr[h];
+                *reinterpret_cast<double2*>(tw + lr * RS + col + 2 * h) = acc[h];
+            }
         }
         __syncwarp();
         // G += P^T W over the tile's 16 cells (K = cells)
