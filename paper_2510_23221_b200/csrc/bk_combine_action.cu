@@ -602,7 +602,7 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
 
 // Two CTAs of 256 threads per SM, one panel slot each. Single plane: 16
 // samples per item (no z-ring, so the T plane fits twice per SM). 3D: 8
-// samples per item for the three-plane ring. Measured (B200): C2 0.75 ms
+// samples per item for the three-plane ring (S = 64: see below). Measured (B200): C2 0.75 ms
 // (0.87 with the L2-fragment kernel), C3 5.6 ms (6.6); the one-CTA 512-thread
 // NS = 16 shape gave 5.9 ms on C3 (its DMMA chains and stencil do not overlap).
 template <int S>
@@ -610,6 +610,10 @@ bk_status dispatch(bk_ctx* ctx, const bk_operator* op, const double* X, int s, c
                    int64_t ldc, int64_t N, double* T, double* Q, double* resid,
                    const bk::ActExtra& ex) {
     if (op->nz == 1) return run<S, 16, 256, true>(ctx, op, X, s, C, ldc, N, T, Q, resid, ex);
+    // S = 64: four panels per plane; one 512-thread CTA per SM with two panel
+    // slots keeps the next panel in flight (C5: 500 samples 27.9 ms vs 53.9 ms
+    // with two one-slot CTAs, whose every panel waited out a full TMA round trip)
+    if (S == 64) return run<S, 16, 512>(ctx, op, X, s, C, ldc, N, T, Q, resid, ex);
     return run<S, 8, 256>(ctx, op, X, s, C, ldc, N, T, Q, resid, ex);
 }
 
