@@ -310,23 +310,21 @@ __device__ __forceinline__ void cta_sum_vec(double (&v)[S / 8][2], double* scrat
     __syncthreads();
 }
 
-// Barrier over the NB CTAs of one chip's group (count, generation) — the
-// grid.sync protocol restricted to a group: the master thread reads the
-// generation, arrives, and the last arrival resets the count and bumps the
-// generation. All CTAs of the launch are co-resident (one cooperative launch).
-__device__ __forceinline__ void group_barrier(unsigned* bar, unsigned NB) {
+// Barrier over the NB CTAs of one chip's group, the grid.sync protocol on one
+// word per chip: the group's CTA 0 adds 0x80000000 - (NB - 1), every other
+// CTA adds 1, so the word's top bit flips exactly when the last CTA arrives;
+// each master thread then spins until it sees the flip. One fence and one
+// atomic per CTA (the previous count + generation pair cost the last arrival
+// a second fence and atomic on the critical path). All CTAs of the launch are
+// co-resident (one cooperative launch).
+__device__ __forceinline__ void group_barrier(unsigned* bar, unsigned NB, bool first) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned* vb = bar;
-        const unsigned gen = vb[1];
+        const unsigned inc = first ? 0x80000000u - (NB - 1) : 1u;
         __threadfence();
-        if (atomicAdd(bar, 1u) == NB - 1) {
-            vb[0] = 0u;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (vb[1] == gen) {
-            }
+        const unsigned old = atomicAdd(bar, inc);
+        volatile unsigned* vb = bar;
+        while (((old ^ *vb) & 0x80000000u) == 0u) {
         }
         __threadfence();
     }
@@ -339,7 +337,7 @@ struct Group {
     unsigned* bar;
     __device__ __forceinline__ void sync(cg::grid_group& grid) const {
         if constexpr (MULTI)
-            group_barrier(bar, (unsigned)NB);
+            group_barrier(bar, (unsigned)NB, b == 0);
         else
             grid.sync();
     }
