@@ -170,13 +170,21 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
     using P = Panel<S>;
     using SH = Shape<NS, NT_>;
     constexpr int NT = SH::NT, NW = SH::NW, MPW = SH::MPW, NB = SH::NB, NP = SH::NP, CSP = SH::CSP;
-    constexpr int SPT = SH::SPT;
+    // Single-plane kernels (PL): thread = (pair of x-adjacent cells, half of the
+    // NS samples); the T ring rows are padded to HXR = 36 with the interior
+    // starting at an even index, so a pair and its y-neighbour pairs are single
+    // 16-byte loads (5 shared loads per pair instead of 7 per cell).
+    constexpr int SPT = PL ? NS / 2 : SH::SPT;       // samples per thread
+    constexpr int HALVES = PL ? 2 : (NT == 512 ? 2 : 1);
+    constexpr int WPH = NW / HALVES;                 // warps per sample half
+    constexpr int HXR = PL ? 36 : HX;                // ring row stride
+    constexpr int HCR = PL ? HY * 36 + 4 : HC;       // ring sample stride (4 mod 8)
     extern __shared__ unsigned char smraw[];
     unsigned char* panels = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
     const int nz = PL ? 1 : a.nz;
     const int nring = nz < 3 ? nz : 3;
-    double* ring = reinterpret_cast<double*>(panels + NP * P::SLOT);  // nring x NS x HC
-    double* Cs = ring + nring * NS * HC;                                // S x CSP
+    double* ring = reinterpret_cast<double*>(panels + NP * P::SLOT);  // nring x NS x HCR
+    double* Cs = ring + nring * NS * HCR;                               // S x CSP
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(Cs + S * CSP);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -188,11 +196,20 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
     }
     __syncthreads();
 
+    // Single plane: each CTA owns a contiguous range of items (sample chunk
+    // fastest), so it stays on one tile for many chunks and loads the tile's
+    // coefficients and X panel once per tile. 3D: items strided by the grid,
+    // so the CTAs resident at once share one tile's X planes through L2
+    // (contiguous ranges measured slower there: C3 5.97 -> 6.47 ms).
+    const int i_begin = PL ? (int)((int64_t)blockIdx.x * a.items / gridDim.x) : (int)blockIdx.x;
+    const int i_end = PL ? (int)((int64_t)(blockIdx.x + 1) * a.items / gridDim.x) : a.items;
+    const int i_step = PL ? 1 : (int)gridDim.x;
+    constexpr bool KEEP = PL && P::R == 1 && NP == 1;  // panel kept across a tile's items
     // producer (thread 0): walks the panels in consumption order (item, z,
-    // column block); slot = panel index mod NP
-    int p_item = blockIdx.x, p_z = 0, p_r = 0, p_slot = 0;
+    // column block); slot = panel index mod NP. KEEP: one panel per tile.
+    int p_item = i_begin, p_z = 0, p_r = 0, p_slot = 0;
     auto issue = [&]() {
-        if (p_item >= a.items) return;
+        if (p_item >= i_end) return;
         const int tile = p_item / a.chunks;
         const int x0 = (tile % a.tilesx) * TX, y0 = (tile / a.tilesx) * TY;
         mbar_expect_tx(&bar[p_slot], P::BYTES);
@@ -203,7 +220,9 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
             p_r = 0;
             if (++p_z == nz) {
                 p_z = 0;
-                p_item += gridDim.x;
+                p_item += i_step;
+                if (KEEP)  // next panel: the next tile's
+                    while (p_item < i_end && p_item / a.chunks == (p_item - 1) / a.chunks) ++p_item;
             }
         }
     };
@@ -218,6 +237,7 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
 
     int ix0 = 0, iy0 = 0;  // current item: tile origin and first sample
     int64_t ij0 = 0;
+    bool new_tile = true, last_of_tile = true;  // KEEP: panel / coefficient reuse
     // T + eps at halo cell h of plane z for item sample q (eps is zero outside
     // the domain, where T is zero-filled too): combine_from_weights' noise add
     // (pipeline.cpp:220-223, 470-503)
@@ -228,8 +248,11 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
     };
     // DMMA accumulators of m-tile mt (all NB sample blocks) -> T ring plane buf,
     // sample-major [q][h] (conflict-free: HC = 4 mod 8)
+    // ring index of halo cell h (box order hy * 34 + hx)
+    auto ridx = [&](int hh) { return PL ? (hh / HX) * HXR + hh % HX + 1 : hh; };
     auto store_tile = [&](int mt, const double (&ac)[NB][4], double* buf, int z) {
         const int h0 = 16 * mt + g, h1 = h0 + 8;
+        const int r0 = ridx(h0), r1 = ridx(h1);
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) {
             const int q = 8 * nb + 2 * t;
@@ -245,12 +268,12 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
                 }
             }
             if (h0 < HC) {
-                buf[q * HC + h0] = v[0];
-                buf[(q + 1) * HC + h0] = v[1];
+                buf[q * HCR + r0] = v[0];
+                buf[(q + 1) * HCR + r0] = v[1];
             }
             if (h1 < HC) {
-                buf[q * HC + h1] = v[2];
-                buf[(q + 1) * HC + h1] = v[3];
+                buf[q * HCR + r1] = v[2];
+                buf[(q + 1) * HCR + r1] = v[3];
             }
         }
     };
@@ -275,11 +298,11 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
     // T of halo plane z (all NS samples) into ring slot z % 3. Panels arrive
     // in ascending column order, so each accumulator sees k ascending.
     auto form = [&](int z) {
-        double* buf = ring + (z % 3) * NS * HC;
+        double* buf = ring + (z % 3) * NS * HCR;
         if constexpr (P::R == 1) {
             // one panel per plane: finish and store each m-tile in turn
             const int slot = (int)(pc % NP);
-            mbar_wait(&bar[slot], (pc / NP) & 1u);
+            if (!KEEP || new_tile) mbar_wait(&bar[slot], (pc / NP) & 1u);
             const unsigned char* pan = panels + slot * P::SLOT;
             double bf[P::PW / 4][NB];
 #pragma unroll
@@ -296,8 +319,10 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
                 store_tile(mt, ac, buf, z);
             }
             __syncthreads();  // every warp is done with this slot
-            if (tid == 0) issue();
-            ++pc;
+            if (!KEEP || last_of_tile) {
+                if (tid == 0) issue();
+                ++pc;
+            }
         } else {
             double acc[MPW][NB][4];
 #pragma unroll
@@ -329,19 +354,26 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
         }
     };
 
-    const int cell = tid & 255, qh = NT == 512 ? tid >> 8 : 0;
+    // PL: pair p = tid & 127 covers cells (2 (p % 16), p / 16) and its x + 1
+    const int cell = PL ? 2 * (tid & 127) : (tid & 255);
+    const int qh = PL ? tid >> 7 : (NT == 512 ? tid >> 8 : 0);
     const int lx = cell % TX, ly = cell / TX;
     const int h = (ly + 1) * HX + (lx + 1);
 
-    for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+    Coef k{}, k2{};  // k2: the second cell of a planar pair
+    int prev_tile = -1;
+    for (int item = i_begin; item < i_end; item += i_step) {
         const int chunk = item % a.chunks;
         const int tile = item / a.chunks;
+        new_tile = tile != prev_tile;
+        last_of_tile = item + i_step >= i_end || (item + i_step) / a.chunks != tile;
+        prev_tile = tile;
         const int x0 = (tile % a.tilesx) * TX, y0 = (tile / a.tilesx) * TY;
         const int64_t j0 = (int64_t)chunk * NS;
         ix0 = x0;
         iy0 = y0;
         ij0 = j0;
-        prof = blockIdx.x == 0 && tid == 0 && item == 4 * (int)gridDim.x;
+        prof = blockIdx.x == 0 && tid == 0 && item == i_begin + 4 * i_step;
         pm = 0;
         mark();
         for (int e = tid; e < S * NS; e += NT) {
@@ -350,8 +382,13 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
         }
         const int gx = x0 + lx, gy = y0 + ly;
         const bool inside = gx < a.nx && gy < a.ny;
-        Coef k{}, kn{};
-        if (inside) load_coef(a, gx, gy, 0, k);
+        const bool inside2 = PL && gx + 1 < a.nx && gy < a.ny;  // the pair's second cell
+        Coef kn{};
+        // planar: the pair's coefficients persist across the tile's items
+        if (!PL || new_tile) {
+            if (inside) load_coef(a, gx, gy, 0, k);
+            if (inside2) load_coef(a, gx + 1, gy, 0, k2);
+        }
         double num[SPT], den[SPT];
 #pragma unroll
         for (int q = 0; q < SPT; ++q) num[q] = den[q] = 0.0;
@@ -360,7 +397,9 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
 
         form(0);
         if (nz > 1) form(1);
-        __syncthreads();
+        // one panel per plane: form already ended with a barrier after its
+        // T stores; otherwise the stores follow the last panel's barrier
+        if (P::R > 1) __syncthreads();
         mark();
         for (int z = 0; z < nz; ++z) {
             if (inside && z + 1 < nz) load_coef(a, gx, gy, z + 1, kn);
@@ -372,7 +411,80 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
             const double* bm = ring + sm1 * NS * HC + SPT * qh * HC + h;
             const double* bp = ring + sp1 * NS * HC + SPT * qh * HC + h;
             const bool hzm = z > 0, hzp = z < nz - 1;  // CTA-uniform
-            if (inside) {
+            if (PL && inside) {
+                // pair (A = x, B = x + 1): 16-byte loads of (A, B) centre and
+                // y -+ 1 rows, 8-byte loads of x - 1 and x + 2; each cell's y in
+                // CSR order y-, x-, diag, x+, y+ exactly as the scalar path
+                const int hb = (ly + 1) * HXR + lx + 2;  // even: 16-byte aligned
+                const double* b = ring + SPT * qh * HCR + hb;
+                const int64_t i = gx + (int64_t)a.nx * gy;
+                const int64_t jb = j0 + SPT * qh;
+                double* pt = a.T ? a.T + jb * a.ldo + i : nullptr;
+                double* pq = a.Q ? a.Q + jb * a.ldo + i : nullptr;
+                const int nv = a.N - jb < SPT ? (int)(a.N - jb) : SPT;
+                const double vol = a.volz[0];
+                const double rvol = 1.0 / vol;
+                const bool vec = inside2 && ((i | a.ldo) & 1) == 0;  // 16-byte stores
+#pragma unroll
+                for (int qq = 0; qq < SPT; ++qq) {
+                    const double2 c2 = *reinterpret_cast<const double2*>(b + qq * HCR);
+                    const double2 m2 = *reinterpret_cast<const double2*>(b + qq * HCR - HXR);
+                    const double2 p2 = *reinterpret_cast<const double2*>(b + qq * HCR + HXR);
+                    const double xl = b[qq * HCR - 1], xr = b[qq * HCR + 2];
+                    double ya, yb;
+                    // first term added to +0.0 as the scalar path does (a -0
+                    // product must not survive as y)
+                    if (!a.fma) {
+                        ya = __dadd_rn(0.0, __dmul_rn(k.ym, m2.x));
+                        ya = __dadd_rn(ya, __dmul_rn(k.xm, xl));
+                        ya = __dadd_rn(ya, __dmul_rn(k.di, c2.x));
+                        ya = __dadd_rn(ya, __dmul_rn(k.xp, c2.y));
+                        ya = __dadd_rn(ya, __dmul_rn(k.yp, p2.x));
+                        yb = __dadd_rn(0.0, __dmul_rn(k2.ym, m2.y));
+                        yb = __dadd_rn(yb, __dmul_rn(k2.xm, c2.x));
+                        yb = __dadd_rn(yb, __dmul_rn(k2.di, c2.y));
+                        yb = __dadd_rn(yb, __dmul_rn(k2.xp, xr));
+                        yb = __dadd_rn(yb, __dmul_rn(k2.yp, p2.y));
+                    } else {
+                        ya = __fma_rn(k.ym, m2.x, 0.0);
+                        ya = __fma_rn(k.xm, xl, ya);
+                        ya = __fma_rn(k.di, c2.x, ya);
+                        ya = __fma_rn(k.xp, c2.y, ya);
+                        ya = __fma_rn(k.yp, p2.x, ya);
+                        yb = __fma_rn(k2.ym, m2.y, 0.0);
+                        yb = __fma_rn(k2.xm, c2.x, yb);
+                        yb = __fma_rn(k2.di, c2.y, yb);
+                        yb = __fma_rn(k2.xp, xr, yb);
+                        yb = __fma_rn(k2.yp, p2.y, yb);
+                    }
+                    const double qa = div_rn(__dsub_rn(ya, k.gi), vol, rvol);
+                    const double qb = div_rn(__dsub_rn(yb, k2.gi), vol, rvol);
+                    if (qq < nv) {
+                        if (vec) {
+                            if (pt) __stcs(reinterpret_cast<double2*>(pt), c2);
+                            if (pq) __stcs(reinterpret_cast<double2*>(pq), make_double2(qa, qb));
+                        } else {
+                            if (pt) __stcs(pt, c2.x);
+                            if (pq) __stcs(pq, qa);
+                            if (inside2 && pt) __stcs(pt + 1, c2.y);
+                            if (inside2 && pq) __stcs(pq + 1, qb);
+                        }
+                        const double ba = fma(vol, qa, k.gi);
+                        const double ra = __dsub_rn(ya, ba);
+                        num[qq] = fma(ra, ra, num[qq]);
+                        den[qq] = fma(ba, ba, den[qq]);
+                        if (inside2) {
+                            const double bb = fma(vol, qb, k2.gi);
+                            const double rb = __dsub_rn(yb, bb);
+                            num[qq] = fma(rb, rb, num[qq]);
+                            den[qq] = fma(bb, bb, den[qq]);
+                        }
+                    }
+                    pt += a.ldo;
+                    pq += a.ldo;
+                }
+            }
+            if (!PL && inside) {
                 const int64_t i = gx + (int64_t)a.nx * gy + plane * z;
                 const int64_t jb = j0 + SPT * qh;
                 double* pt = a.T ? a.T + jb * a.ldo + i : nullptr;
@@ -419,12 +531,12 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
                     pq += a.ldo;
                 }
             }
-            k = kn;
+            if (!PL) k = kn;  // planar: k persists across the tile's items
             __syncthreads();
             mark();
             if (z + 2 < nz) {
                 form(z + 2);
-                __syncthreads();
+                if (P::R > 1) __syncthreads();
             }
             mark();
         }
@@ -460,9 +572,9 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
             if (tid < NS && j0 + tid < a.N) {
                 const int hq = tid / SPT, qq = tid % SPT;
                 double u = 0.0, w = 0.0;
-                for (int k2 = 0; k2 < 8; ++k2) {  // the 8 warps of sample half hq
-                    u += red[(8 * hq + k2) * V + qq];
-                    w += red[(8 * hq + k2) * V + SPT + qq];
+                for (int w2 = 0; w2 < WPH; ++w2) {  // the warps of sample half hq
+                    u += red[(WPH * hq + w2) * V + qq];
+                    w += red[(WPH * hq + w2) * V + SPT + qq];
                 }
                 double* pp = a.part + ((j0 + tid) * (int64_t)a.tiles + tile) * 2;
                 *reinterpret_cast<double2*>(pp) = make_double2(u, w);
@@ -571,8 +683,9 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
         return fail(ctx, BK_CUDA_ERROR, "combine_action: tensor map encode failed (" +
                                             std::to_string((int)cr) + ")");
     const int nring = op->nz < 3 ? op->nz : 3;
+    const int hcr = PL ? HY * 36 + 4 : HC;  // the kernel's ring sample stride
     const size_t smem = 1024 + (size_t)SH::NP * P::SLOT +
-                        (size_t)(nring * NS * HC + S * SH::CSP) * sizeof(double) + SH::NP * 8;
+                        (size_t)(nring * NS * hcr + S * SH::CSP) * sizeof(double) + SH::NP * 8;
     auto kern = combine_action_kernel<S, NS, NT, PL>;
     BK_CUDA_TRY(ctx, bk::set_max_smem((const void*)kern, smem));
     const int slots = SH::CTAS * ctx->num_sms;
