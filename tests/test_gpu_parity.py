@@ -252,8 +252,11 @@ def test_combine_action_bitwise_vs_reference_golden(bk, ctx, name):
 def test_combine_action_bitwise_vs_oracle_odd_shapes(bk, ctx, oracle):
     # widths 5 and 20 run on the padded 8 / 32 kernels: only the real s rows of
     # C may be read
+    # single-plane grids with S = 32 / 64 (two / four TMA panels per plane),
+    # odd nx (the cell-pair path's unpaired last column), 3D with S = 64
     for case, N in (((1, 37, 29, 1, 8), 19), ((3, 33, 17, 8, 32), 21), ((4, 20, 9, 4, 16), 8),
-                    ((1, 37, 29, 1, 5), 19), ((3, 16, 12, 8, 20), 33)):
+                    ((1, 37, 29, 1, 5), 19), ((3, 16, 12, 8, 20), 33),
+                    ((1, 41, 23, 1, 20), 37), ((1, 35, 9, 1, 40), 18), ((3, 19, 21, 8, 64), 17)):
         inp = bk.synth_chip(*case, N)
         g = inp.grid
         op = bk.assemble(inp.k, g, inp.bc, ctx)
