@@ -529,8 +529,8 @@ __device__ __forceinline__ void ring_wait(unsigned long long* bar, unsigned pari
 struct Ring {
     double* P;                // kRing x nx S
     double* C;                // kRing x 3 nx: diag, cx, cy rows
-    unsigned long long* bar;  // kRing
-    unsigned ph;              // per-slot parity bits (uniform across the CTA)
+    unsigned long long* bar;  // kRing "full" (TMA landed), then kRing "empty" (NW warps done)
+    unsigned ph;              // parity bits: full slots (all threads), empty slots (thread 0)
 };
 
 template <int S>
@@ -627,9 +627,21 @@ __device__ void phase_spmm_gram_ring(const Args& a, int64_t c0, int64_t c1, int6
             }
             __syncwarp();
         }
-        __syncthreads();  // row r - 1's slot is free
-        if (threadIdx.x == 0) issue(r + 3);
+        // row r was the last reader of row r - 1's slot: each warp releases it,
+        // and the producer refills it once all have (no CTA-wide barrier per
+        // row: warps drift, hiding one another's Gram / stencil latency)
+        __syncwarp();
+        const int fr = (int)((r - 1) & (kRing - 1));
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_u32(&rg.bar[kRing + fr]))
+                         : "memory");
+        if (threadIdx.x == 0) {
+            ring_wait(&rg.bar[kRing + fr], (rg.ph >> (kRing + fr)) & 1u);
+            rg.ph ^= 1u << (kRing + fr);
+            issue(r + 3);
+        }
     }
+    __syncthreads();  // the coefficient rows (tileR area) are read no more
 }
 
 // Rows [base, base + 16) of V (n x S) into the warp tile T[16][RS] by
@@ -873,6 +885,9 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         if (tid == 0) {
             for (int i = 0; i < kRing; ++i)
                 asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(&rg.bar[i])));
+            for (int i = kRing; i < 2 * kRing; ++i)
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_u32(&rg.bar[i])),
+                             "r"(NW));
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
@@ -1181,7 +1196,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
 // resident mode when the ring fits; BK_CG_RING=0/1 overrides (A/B).
 template <int S>
 size_t ring_bytes(int nx) {
-    return 16 + (size_t)kRing * nx * S * sizeof(double) + kRing * sizeof(unsigned long long);
+    return 16 + (size_t)kRing * nx * S * sizeof(double) + 2 * kRing * sizeof(unsigned long long);
 }
 template <int S>
 bool want_ring(bool resident, int nx, int nz_chip) {
