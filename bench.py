@@ -39,10 +39,10 @@ WORKLOADS = {
     4: "C4: batch of distinct chips 128x128x4 (per-chip dz, k, h), s=16, 8 samples/chip",
     5: "C5: 512x512x16 layered stack, s=64, N=5000 (outputs streamed through a device ring)",
 }
-C4_CHIPS_PER_STEP = 16   # chips per GPU per timed step (5000 chips total at full scale)
+C4_CHIPS_PER_STEP = 32   # chips per GPU per timed step (5000 chips total at full scale)
 C4_MAX_ITER = 5000
 DIRECT_MAX_ITER = 5000    # per-sample CG baseline (a lone column can stall at the fp64 floor)
-C4_STREAMS = 8            # chips per batched solve (one cooperative launch, 1/8 of the SMs each)
+C4_STREAMS = 32           # chips per batched solve (one cooperative launch, 1/32 of the SMs each; measured best of 8/16/32)
 # Tolerance pins: 1e-12 for configs 1-3; configs 4-5 use 1e-10
 # because their true relative residual plateaus at ~1.1-2e-12 in fp64 (measured:
 # C5 512x512x16 at 1.1e-12..2.0e-12 after 1200 iterations; C4 chip 4 at 1.28e-12
