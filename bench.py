@@ -257,7 +257,7 @@ def ncu_traffic(config):
         return json.load(f).get(f"config{config}")
 
 
-CHIPS_BY_CONFIG = {1: 64, 2: 16, 3: 8}  # independent chips per GPU per step, solved together
+CHIPS_BY_CONFIG = {1: 64, 2: 16, 3: 12}  # independent chips per GPU per step, solved together
 
 
 def chips_per_step(args):
