@@ -118,6 +118,7 @@ struct Sm {
     double s_old[S * S];
     double mat[S * S];
     alignas(16) double coef[S * Strides<S>::RS];
+    alignas(16) double akeep[S * Strides<S>::RS];  // alpha, for the deferred X update
     alignas(16) double aug[S * Strides<S>::LD + 2 * S];
     // per-warp matrix partials; aliased onto the warp's own transpose tile
     // when it fits (written only after that warp's tile loop)
@@ -829,7 +830,9 @@ __device__ __forceinline__ double dinv_at(const Args& a, int64_t c, int64_t c1, 
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-template <int S, bool RES, bool MULTI>
+// DEF: X += P alpha deferred from phase 2 to phase 3 (see below); a
+// compile-time choice so the other instantiations keep their registers
+template <int S, bool RES, bool MULTI, bool DEF>
 __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args a) {
     constexpr int BS = CtaShape<S>::BS, NW = CtaShape<S>::NW;
     constexpr int NT = S / 8;
@@ -987,20 +990,31 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         if (pm) pm[2] = gtimer();
         matvecs += sm.sa;
         small_solve<S>(sm, sm.mat, sm.s_old, sm.coef);  // alpha
+        for (int e = tid; e < S * Strides<S>::RS; e += BS) sm.akeep[e] = sm.coef[e];
+        // X += P alpha deferred to phase 3 (which reads the same P tile: one P
+        // read fewer per iteration). Measured: ring mode (C2 x16) +3.3 %, S = 32
+        // (C3 x12) +5 %; the per-tile S = 16 sweep (C4) -4 % (the extra X
+        // traffic of phase 3 evicts the P rows phase 1 then re-reads), so off
+        // there (the host picks DEF = ring || S >= 32).
+        constexpr bool defer = DEF;
+        bool xdone = !defer;
         if (pm) pm[3] = gtimer();
 
-        // ---- phase 2: X += P alpha, R -= W alpha, rr, Z, S_new = R^T Z
+        // ---- phase 2: [X += P alpha unless deferred], R -= W alpha, rr, Z,
+        // S_new = R^T Z
         G.zero();
         double rr[NT][2] = {};
         for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
             double pa[KS][2], wa[KS][2], x[NT][4], r[NT][4];
-            stage_tile<S>(tr, a.P, base, c1, lane);
+            if (!defer) {
+                stage_tile<S>(tr, a.P, base, c1, lane);
+                Xv.load(base, g, t, x);
+            }
             stage_tile<S>(tz, a.W, base, c1, lane);
-            Xv.load(base, g, t, x);
             Rv.load(base, g, t, r);
             cp_commit_wait_all();
             __syncwarp();
-            afrag_smem<S>(tr, g, t, pa, 1.0);
+            if (!defer) afrag_smem<S>(tr, g, t, pa, 1.0);
             afrag_smem<S>(tz, g, t, wa, -1.0);
             __syncwarp();  // tr / tz are rewritten by tile_gram below
 #pragma unroll
@@ -1008,10 +1022,10 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) {
                     const double bb = sm.coef[(4 * ks + t) * Strides<S>::RS + 8 * n + g];
-                    dmma(x[n], pa[ks][0], pa[ks][1], bb);
+                    if (!defer) dmma(x[n], pa[ks][0], pa[ks][1], bb);
                     dmma(r[n], wa[ks][0], wa[ks][1], bb);
                 }
-            Xv.store(base, g, t, x);
+            if (!defer) Xv.store(base, g, t, x);
             Rv.store(base, g, t, r);
             const double d0 = dinv_of(base + g), d1 = dinv_of(base + g + 8);
             double z[NT][4];
@@ -1045,7 +1059,29 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
 #pragma unroll
         for (int q = 0; q < S; ++q) nver += sm.vflag[q];
         bool restart = false;
+        // X += P alpha (deferred from phase 2) for every sweep that reads X
+        auto x_update = [&]() {
+            for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
+                double pa[KS][2], x[NT][4];
+                stage_tile<S>(tr, a.P, base, c1, lane);
+                Xv.load(base, g, t, x);
+                cp_commit_wait_all();
+                __syncwarp();
+                afrag_smem<S>(tr, g, t, pa, 1.0);
+                __syncwarp();
+#pragma unroll
+                for (int n = 0; n < NT; ++n)
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks)
+                        dmma(x[n], pa[ks][0], pa[ks][1],
+                             sm.akeep[(4 * ks + t) * Strides<S>::RS + 8 * n + g]);
+                Xv.store(base, g, t, x);
+            }
+            __syncthreads();
+            xdone = true;
+        };
         if (nver > 0) {
+            if (!xdone) x_update();
             publish_x();
             double rs[NT][2] = {};
             for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
@@ -1127,13 +1163,23 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         for (int e = tid; e < S * S; e += BS) sm.s_old[e] = sm.mat[e];
         if (pm) pm[6] = gtimer();
         for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
-            double pa[KS][2], p[NT][4];
+            double pa[KS][2], p[NT][4], x[NT][4];
             stage_tile<S>(tr, a.P, base, c1, lane);
             Rv.load(base, g, t, p);
+            if (!xdone) Xv.load(base, g, t, x);
             cp_commit_wait_all();
             __syncwarp();
             afrag_smem<S>(tr, g, t, pa, 1.0);
             __syncwarp();
+            if (!xdone) {  // X += P alpha with the same P tile (deferred from phase 2)
+#pragma unroll
+                for (int n = 0; n < NT; ++n)
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks)
+                        dmma(x[n], pa[ks][0], pa[ks][1],
+                             sm.akeep[(4 * ks + t) * Strides<S>::RS + 8 * n + g]);
+                Xv.store(base, g, t, x);
+            }
             const double d0 = dinv_of(base + g), d1 = dinv_of(base + g + 8);
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
@@ -1223,9 +1269,10 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
     // shared-memory-resident X/R when every CTA's range fits (S <= 16)
     const int64_t max_cells = 16 * ((ntiles + nb - 1) / nb);
     const bool resident = S <= 16 && max_cells <= kResCells && getenv("BK_CG_NO_RESIDENT") == nullptr;
-    const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, false>
-                                : (const void*)block_cg_dmma_kernel<S, false, false>;
     const bool ring = want_ring<S>(resident, op->nx, op->nz);
+    const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, false, false>
+                       : (ring || S >= 32) ? (const void*)block_cg_dmma_kernel<S, false, false, true>
+                                           : (const void*)block_cg_dmma_kernel<S, false, false, false>;
     const size_t smem = (resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>)) +
                         (ring ? ring_bytes<S>(op->nx) : 0);
     BK_CUDA_TRY(ctx, bk::set_max_smem((const void*)kern, smem));
@@ -1345,9 +1392,10 @@ bk_status run_dmma_multi(bk_ctx* ctx, const bk_operator* op, int K, const double
     const int64_t nb = (int64_t)K * cpc;
     const int64_t max_cells = 16 * ((ntiles + cpc - 1) / cpc);
     const bool resident = S <= 16 && max_cells <= kResCells && getenv("BK_CG_NO_RESIDENT") == nullptr;
-    const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, true>
-                                : (const void*)block_cg_dmma_kernel<S, false, true>;
     const bool ring = want_ring<S>(resident, op->nx, op->nz / K);
+    const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, true, false>
+                       : (ring || S >= 32) ? (const void*)block_cg_dmma_kernel<S, false, true, true>
+                                           : (const void*)block_cg_dmma_kernel<S, false, true, false>;
     const size_t smem = (resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>)) +
                         (ring ? ring_bytes<S>(op->nx) : 0);
     BK_CUDA_TRY(ctx, set_max_smem(kern, smem));
