@@ -268,6 +268,7 @@ struct SweepArgs {
     double* W;
     double* part;        // [gridDim.x][E]
     const double* coef;  // S x (S + 4) (alpha or beta)
+    const double* coef2; // alpha kept for the deferred X update (k_pupdate modes 1, 2)
     const int* act;      // per-column mask for masked sweeps
     int precond;
 };
@@ -317,14 +318,17 @@ __device__ __forceinline__ void write_colsum(double* out, double* vred, int ts, 
 
 // stages in flight for the update sweep: 3 (two groups ahead) when two CTAs
 // still fit an SM, else 2
-template <int S>
+// XD: X += P alpha deferred to k_pupdate — the stage holds W, R, D^-1 and a Z
+// scratch tile instead of P, W, X, R, D^-1
+template <int S, bool XD = false>
 struct UpdRing {
-    static constexpr size_t stage = (4 * (size_t)Geo<S>::TILE + Geo<S>::CELLS) * sizeof(double);
+    static constexpr size_t stage =
+        ((XD ? 3 : 4) * (size_t)Geo<S>::TILE + Geo<S>::CELLS) * sizeof(double);
     static constexpr int NST = (2 * (3 * stage + Geo<S>::TPB * S * 8 + 1024) <= 228 * 1024) ? 3 : 2;
 };
-template <int S>
+template <int S, bool XD = false>
 constexpr size_t smem_update() {
-    return UpdRing<S>::NST * UpdRing<S>::stage + Geo<S>::TPB * S * sizeof(double);
+    return UpdRing<S, XD>::NST * UpdRing<S, XD>::stage + Geo<S>::TPB * S * sizeof(double);
 }
 template <int S>
 constexpr size_t smem_anchor() {
@@ -334,9 +338,10 @@ template <int S>
 constexpr size_t smem_spmm() {
     return 2 * (size_t)Geo<S>::TILE * sizeof(double);
 }
-template <int S>
+// k_pupdate MODE 0: P = Z + P beta; 1: and X += P alpha (deferred); 2: X += P alpha only
+template <int S, int MODE = 0>
 constexpr size_t smem_pupdate() {
-    return 3 * (2 * (size_t)Geo<S>::TILE + Geo<S>::CELLS) * sizeof(double);
+    return 3 * ((MODE == 1 ? 3 : 2) * (size_t)Geo<S>::TILE + Geo<S>::CELLS) * sizeof(double);
 }
 
 // ---------------------------------------------------------------------------
@@ -661,12 +666,15 @@ __device__ __forceinline__ void frag_from_smem(const double* T, int RS, int row0
 // registers), rr, Z = D^-1 R; partials [R^T Z | rr]. Every input row of a
 // tile group (P, W, X, R, D^-1) is staged by cp.async one group ahead; the
 // updated R and Z overwrite the consumed R / X stage rows and feed the Gram.
-template <int S>
+template <int S, bool XD = false>
 __global__ void __launch_bounds__(LBS, 2) k_update(SweepArgs a) {
     using G_ = Geo<S>;
     constexpr int RS = G_::RS, KS = S / 4, TL = G_::TILE;
-    constexpr int STAGE = 4 * TL + G_::CELLS;  // P, W, X, R, dinv
-    constexpr int NST = UpdRing<S>::NST;
+    // stage layout: P, W, X, R, dinv — or (XD) W, R, dinv, Z scratch
+    constexpr int STAGE = (XD ? 3 : 4) * TL + G_::CELLS;
+    constexpr int OW = XD ? 0 : TL, OR = XD ? TL : 3 * TL, OD = XD ? 2 * TL : 4 * TL;
+    constexpr int OZ = XD ? 2 * TL + G_::CELLS : 2 * TL;
+    constexpr int NST = UpdRing<S, XD>::NST;
     extern __shared__ __align__(16) double sm_[];
     double* vred = sm_ + NST * STAGE;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -680,9 +688,13 @@ __global__ void __launch_bounds__(LBS, 2) k_update(SweepArgs a) {
     OwnedGram<S> G;
     G.zero();
     double rr0 = 0.0, rr1 = 0.0;
-    const double* const srcs[4] = {a.P, a.W, a.X, a.R};
+    const double* const srcs4[4] = {a.P, a.W, a.X, a.R};
+    const double* const srcs2[2] = {a.W, a.R};
     auto stage = [&](int buf, int gr) {
-        stage_multi<S, 4>(sm_ + buf * STAGE, srcs, jac ? a.st.dinv : nullptr, a.sl, gr, ntiles);
+        if constexpr (XD)
+            stage_multi<S, 2>(sm_ + buf * STAGE, srcs2, jac ? a.st.dinv : nullptr, a.sl, gr, ntiles);
+        else
+            stage_multi<S, 4>(sm_ + buf * STAGE, srcs4, jac ? a.st.dinv : nullptr, a.sl, gr, ntiles);
     };
     int grp = blockIdx.x;
 #pragma unroll
@@ -701,21 +713,21 @@ __global__ void __launch_bounds__(LBS, 2) k_update(SweepArgs a) {
         __syncthreads();
         double* st = sm_ + (it % NST) * STAGE;
         const double* Pt = st + ts * 16 * RS;
-        const double* Wt = st + TL + ts * 16 * RS;
-        double* Xt = st + 2 * TL;  // becomes V (Z) after the update
-        double* Rt = st + 3 * TL;  // becomes U (R)
+        const double* Wt = st + OW + ts * 16 * RS;
+        double* Xt = st + OZ;  // X (becomes V = Z after the update), or the Z scratch (XD)
+        double* Rt = st + OR;  // becomes U (R)
         double x[4], rv[4];
-        frag_from_smem(Xt, RS, ts * 16 + g, col, x);
+        if constexpr (!XD) frag_from_smem(Xt, RS, ts * 16 + g, col, x);
         frag_from_smem(Rt, RS, ts * 16 + g, col, rv);
-        const double d0 = jac ? st[4 * TL + ts * 16 + g] : 1.0;
-        const double d1 = jac ? st[4 * TL + ts * 16 + g + 8] : 1.0;
+        const double d0 = jac ? st[OD + ts * 16 + g] : 1.0;
+        const double d1 = jac ? st[OD + ts * 16 + g + 8] : 1.0;
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
             const int kc = 4 * ks + t;
-            dmma_l(x, Pt[g * RS + kc], Pt[(g + 8) * RS + kc], cf[ks]);
+            if constexpr (!XD) dmma_l(x, Pt[g * RS + kc], Pt[(g + 8) * RS + kc], cf[ks]);
             dmma_l(rv, -Wt[g * RS + kc], -Wt[(g + 8) * RS + kc], cf[ks]);
         }
-        st_frag(a.X, S, tc, g, col, v0, v1, x);
+        if constexpr (!XD) st_frag(a.X, S, tc, g, col, v0, v1, x);
         st_frag(a.R, S, tc, g, col, v0, v1, rv);
         double z[4];
         z[0] = d0 * rv[0];
@@ -739,11 +751,14 @@ __global__ void __launch_bounds__(LBS, 2) k_update(SweepArgs a) {
 
 // phase 3: P = D^-1 R + P beta (DMMA, accumulator initialised to Z; P, R and
 // D^-1 rows of the group staged one group ahead)
-template <int S>
+template <int S, int MODE = 0>
 __global__ void __launch_bounds__(LBS, 2) k_pupdate(SweepArgs a) {
     using G_ = Geo<S>;
     constexpr int RS = G_::RS, KS = S / 4, TL = G_::TILE;
-    constexpr int STAGE = 2 * TL + G_::CELLS;  // P, R, dinv
+    // MODE 0: P, R, dinv; 1: P, R, X, dinv; 2: P, X
+    constexpr int NA = MODE == 1 ? 3 : 2;
+    constexpr int STAGE = NA * TL + G_::CELLS;
+    constexpr int OX = MODE == 1 ? 2 * TL : TL;
     constexpr int NST = 3;
     extern __shared__ __align__(16) double sm_[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -751,12 +766,20 @@ __global__ void __launch_bounds__(LBS, 2) k_pupdate(SweepArgs a) {
     const int ntiles = n_tiles(a.sl);
     const int ngroups = (ntiles + G_::TPB - 1) / G_::TPB;
     const bool jac = a.precond != 0;
-    double cf[KS];
+    double cf[KS], ca[KS];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) cf[ks] = a.coef[(4 * ks + t) * RS + 8 * cb + g];
-    const double* const srcs[2] = {a.P, a.R};
+    for (int ks = 0; ks < KS; ++ks) {
+        if (MODE != 2) cf[ks] = a.coef[(4 * ks + t) * RS + 8 * cb + g];    // beta
+        if (MODE != 0) ca[ks] = a.coef2[(4 * ks + t) * RS + 8 * cb + g];   // alpha
+    }
+    const double* const srcs[2] = {a.P, MODE == 2 ? a.X : a.R};
+    const double* const srcs3[3] = {a.P, a.R, a.X};
     auto stage = [&](int buf, int gr) {
-        stage_multi<S, 2>(sm_ + buf * STAGE, srcs, jac ? a.st.dinv : nullptr, a.sl, gr, ntiles);
+        if constexpr (MODE == 1)
+            stage_multi<S, 3>(sm_ + buf * STAGE, srcs3, jac ? a.st.dinv : nullptr, a.sl, gr, ntiles);
+        else
+            stage_multi<S, 2>(sm_ + buf * STAGE, srcs, (MODE == 0 && jac) ? a.st.dinv : nullptr,
+                              a.sl, gr, ntiles);
     };
     int grp = blockIdx.x;
 #pragma unroll
@@ -775,38 +798,51 @@ __global__ void __launch_bounds__(LBS, 2) k_pupdate(SweepArgs a) {
         __syncthreads();
         const double* st = sm_ + (it % NST) * STAGE;
         const double* Pt = st + ts * 16 * RS;
-        double p[4];
-        frag_from_smem(st + TL, RS, ts * 16 + g, col, p);
-        const double d0 = jac ? st[2 * TL + ts * 16 + g] : 1.0;
-        const double d1 = jac ? st[2 * TL + ts * 16 + g + 8] : 1.0;
-        p[0] *= d0;
-        p[1] *= d0;
-        p[2] *= d1;
-        p[3] *= d1;
+        if constexpr (MODE != 0) {
+            // X += P alpha (deferred from k_update; the same DMMA chain)
+            double x[4];
+            frag_from_smem(st + OX, RS, ts * 16 + g, col, x);
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-            const int kc = 4 * ks + t;
-            dmma_l(p, Pt[g * RS + kc], Pt[(g + 8) * RS + kc], cf[ks]);
+            for (int ks = 0; ks < KS; ++ks) {
+                const int kc = 4 * ks + t;
+                dmma_l(x, Pt[g * RS + kc], Pt[(g + 8) * RS + kc], ca[ks]);
+            }
+            st_frag(a.X, S, tc, g, col, v0, v1, x);
         }
-        st_frag(a.P, S, tc, g, col, v0, v1, p);
+        if constexpr (MODE != 2) {
+            double p[4];
+            frag_from_smem(st + TL, RS, ts * 16 + g, col, p);
+            const double d0 = jac ? st[NA * TL + ts * 16 + g] : 1.0;
+            const double d1 = jac ? st[NA * TL + ts * 16 + g + 8] : 1.0;
+            p[0] *= d0;
+            p[1] *= d0;
+            p[2] *= d1;
+            p[3] *= d1;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                const int kc = 4 * ks + t;
+                dmma_l(p, Pt[g * RS + kc], Pt[(g + 8) * RS + kc], cf[ks]);
+            }
+            st_frag(a.P, S, tc, g, col, v0, v1, p);
+        }
         __syncthreads();  // buffer it % NST is refilled by the prefetch of the next iteration
     }
     cp_wait<0>();
 }
 
-template <int S>
+template <int S, bool XD = false>
 cudaError_t launch_update(const SweepArgs& a, int nb, cudaStream_t s) {
-    const cudaError_t e = bk::set_max_smem((const void*)k_update<S>, smem_update<S>());
+    const cudaError_t e = bk::set_max_smem((const void*)k_update<S, XD>, smem_update<S, XD>());
     if (e != cudaSuccess) return e;
-    k_update<S><<<nb, LBS, smem_update<S>(), s>>>(a);
+    k_update<S, XD><<<nb, LBS, smem_update<S, XD>(), s>>>(a);
     return cudaGetLastError();
 }
 
-template <int S>
+template <int S, int MODE = 0>
 cudaError_t launch_pupdate(const SweepArgs& a, int nb, cudaStream_t s) {
-    const cudaError_t e = bk::set_max_smem((const void*)k_pupdate<S>, smem_pupdate<S>());
+    const cudaError_t e = bk::set_max_smem((const void*)k_pupdate<S, MODE>, smem_pupdate<S, MODE>());
     if (e != cudaSuccess) return e;
-    k_pupdate<S><<<nb, LBS, smem_pupdate<S>(), s>>>(a);
+    k_pupdate<S, MODE><<<nb, LBS, smem_pupdate<S, MODE>(), s>>>(a);
     return cudaGetLastError();
 }
 
@@ -920,6 +956,7 @@ struct Ctl {
     double s_old[S * S];
     double snew[S * S];
     double coef[S * (S + 4)];
+    double akeep[S * (S + 4)];  // alpha of the iteration (X += P alpha is deferred to k_pupdate)
     double bnorm[S];
     double fres[S];
     double rr[S];
@@ -1002,6 +1039,8 @@ __global__ void __launch_bounds__(CBS) k_ctl_alpha(Ctl<S>* c, const double* red)
     ctl_index(c, sm);
     ctl_solve(c, sm, red, c->s_old);
     if (threadIdx.x == 0) c->matvecs += sm.sa;
+    __syncthreads();
+    for (int e = threadIdx.x; e < S * (S + 4); e += blockDim.x) c->akeep[e] = c->coef[e];
 }
 
 // red = [S_new | rr]: per-column recurrence test (solvers.cpp:582-590); beta
@@ -1200,6 +1239,10 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     BK_CUDA_TRY(ctx, cudaGetLastError());
     int cmd = 0, sa = 0;
     if ((st = read_cmd(&cmd, &sa)) != BK_OK) return st;
+    // X += P alpha is deferred from the update sweep to the P update, which
+    // reads the same P rows (one P read fewer per iteration; bitwise the same
+    // X); a verification first applies the pending update (k_pupdate MODE 2)
+    a.coef2 = ctl->akeep;
     for (int m = 1; m <= cfg->max_iter && sa > 0; ++m) {
         halo(a.P);
         BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s));
@@ -1207,14 +1250,18 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
         reduce(S * S, nb);
         k_ctl_alpha<S><<<1, CBS, cs, s>>>(ctl, red);
         ++ctx->launches;
-        BK_CUDA_TRY(ctx, launch_update<S>(a, nb, s));
+        BK_CUDA_TRY(ctx, (launch_update<S, true>(a, nb, s)));
         ++ctx->launches;
         reduce(E, nb);
         k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, red, m);
         ++ctx->launches;
         BK_CUDA_TRY(ctx, cudaGetLastError());
         if ((st = read_cmd(&cmd, &sa)) != BK_OK) return st;
+        bool x_done = false;
         if (cmd == kCmdVerify) {
+            BK_CUDA_TRY(ctx, (launch_pupdate<S, 2>(a, nb, s)));
+            ++ctx->launches;
+            x_done = true;
             halo(a.X);
             true_res();
             k_ctl_verify<S><<<1, CBS, cs, s>>>(ctl, red);
@@ -1230,7 +1277,10 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
                 continue;
             }
         }
-        BK_CUDA_TRY(ctx, launch_pupdate<S>(a, nb, s));
+        if (x_done)
+            BK_CUDA_TRY(ctx, (launch_pupdate<S, 0>(a, nb, s)));
+        else
+            BK_CUDA_TRY(ctx, (launch_pupdate<S, 1>(a, nb, s)));
         ++ctx->launches;
     }
     // honest residuals for still-active columns
