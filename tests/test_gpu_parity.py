@@ -463,6 +463,26 @@ def sub_budget(streams):
     return max(1, sms // streams)
 
 
+@pytest.mark.parametrize("case", [(2, 64, 48, 1, 16), (1, 48, 40, 1, 8)])
+def test_block_cg_row_ring_path_vs_oracle(bk, ctx, oracle, case, monkeypatch):
+    """Single-plane chips outside resident mode run phase 1 through the TMA row
+    ring, with X += P alpha deferred to phase 3 (S = 16): capped iterates equal
+    the oracle's, a full solve converges to it."""
+    monkeypatch.setenv("BK_CG_NO_RESIDENT", "1")
+    inp = bk.synth_chip(*case, 4)
+    op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
+    o = oracle.assemble(grid_tuple(inp.grid), inp.k, inp.bc.as_tuples())
+    B = oracle.rhs_from_power(o, inp.q_basis)
+    for m in (1, 2, 7):
+        r = bk.block_cg(op, B, cfg_jacobi(m))
+        X, rep = oracle.block_cg(o, B, TOL, m, 1)
+        assert r.report.iterations == m and r.report.matvec_count == rep["matvec_count"]
+        assert rel_l2(r.x, X) <= 1e-12
+    r = bk.block_cg(op, B, cfg_jacobi())
+    X, rep = oracle.block_cg(o, B, TOL, 100000, 1)
+    assert r.report.all_converged() and rel_l2(r.x, X) <= PARITY
+
+
 @pytest.mark.parametrize("case", [(1, 32, 32, 1, 8), (2, 40, 36, 1, 16), (3, 16, 16, 8, 32),
                                   (4, 24, 20, 4, 16)])
 def test_block_cg_multikernel_path_vs_oracle(bk, ctx, oracle, case, monkeypatch):
