@@ -7,19 +7,22 @@
 // registers by the sweep that loads them — no shared-memory staging except a
 // warp-private transpose for R^T Z.
 //
-//   phase 1  per warp, 4-cell k-groups: lane (g = lane/4, t = lane%4) computes the
-//            stencil W[cell t][g + 8c] (CSR-order FMA chain, bitwise the reference
-//            apply_block) and already holds the A (= P^T) and B (= W) fragments of
-//            the Gram G = P^T W, accumulated by DMMA with K = cells.
-//   phase 2  per warp, 16-cell tiles: X += P alpha and R -= W alpha as DMMA GEMMs
-//            (M = cells, N = columns, K = s), rr and Z = D^-1 R in the epilogue,
-//            S_new = R^T Z by DMMA after a warp-private smem transpose.
+//   phase 1  W = A P (CSR-order FMA chain, bitwise the reference apply_block)
+//            and the Gram G = P^T W by DMMA with K = cells, per warp in 16-cell
+//            tiles; for single-plane chips outside resident mode the P rows and
+//            coefficient rows stream through a 4-slot shared-memory ring filled
+//            by TMA bulk copies two rows ahead (phase_spmm_gram_ring).
+//   phase 2  R -= W alpha as a DMMA GEMM (M = cells, N = columns, K = s), rr
+//            and Z = D^-1 R in the epilogue, S_new = R^T Z by DMMA after a
+//            warp-private smem transpose; X += P alpha here too, or (DEF) in
+//            phase 3, which reads the same P tile (one P read fewer).
 //   phase 3  P = Z + P beta, DMMA with the accumulator initialised to Z.
 //
-// Grid-wide: cooperative launch, cg::grid.sync (1.2 us measured), fixed-order
-// distributed reductions (no floating-point atomics: bitwise deterministic),
-// redundant per-CTA s x s solves (Gauss-Jordan with the reference's pivoted
-// Cholesky as the rank-deficient fallback).
+// Grid-wide: one chip on all SMs (cooperative launch, cg::grid.sync, 1.2 us
+// measured) or K z-stacked chips with per-chip CTA groups and one-word
+// flip-bit group barriers; fixed-order distributed reductions (no
+// floating-point atomics: bitwise deterministic); redundant per-CTA s x s
+// solves (Gauss-Jordan with the reference's pivoted-Cholesky rank semantics).
 #include <cooperative_groups.h>
 
 #include <cmath>
