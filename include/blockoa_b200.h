@@ -214,6 +214,18 @@ bk_status bk_generate_batch(bk_ctx* ctx, int n_chips, const bk_grid* grids,
  * (0 = all SMs). */
 bk_status bk_set_cg_sm_budget(bk_ctx* ctx, int max_ctas);
 
+/* Per-context debug / A-B switches, initialised from the environment when the
+ * context is created (BK_CG_RING, BK_CG_NO_RESIDENT, BK_CG_LARGE,
+ * BK_CG_PROFILE, BK_NO_TMA_SPMM, BK_COMB_PROFILE, BK_BATCH_TRACE). Names:
+ * "ring" (-1 automatic, 0 off, 1 on), "no_resident", "force_large",
+ * "cg_profile", "no_tma_spmm", "comb_profile", "batch_trace" (0 / 1).
+ * Not part of the reference API; used by the tests to pin kernel variants. */
+bk_status bk_set_option(bk_ctx* ctx, const char* name, int value);
+/* Kernel instantiation the last block-CG solve on ctx ran, e.g.
+ * "block_cg_dmma_kernel<16,0,1,1> ring chips=16" (template arguments S,
+ * resident, multi-chip, deferred X update) or "block_cg_large<64> tma". */
+const char* bk_last_solver_variant(const bk_ctx* ctx);
+
 /* ---- y-slab domain decomposition (BASELINE config 5 across GPUs) -----------
  * A rank owns global rows [y0, y0 + nyl) of the grid of `op` (the GLOBAL
  * operator, assembled identically on every rank). Its block vectors use the

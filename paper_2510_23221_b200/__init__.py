@@ -32,6 +32,7 @@ fallback — without the built library or a GPU every call raises.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 from dataclasses import dataclass, field
@@ -167,6 +168,9 @@ def _load():
         lib.bk_synchronize.argtypes = [vp]
         lib.bk_launch_count.argtypes = [vp]
         lib.bk_launch_count.restype = C.c_int64
+        lib.bk_set_option.argtypes = [vp, C.c_char_p, C.c_int]
+        lib.bk_last_solver_variant.argtypes = [vp]
+        lib.bk_last_solver_variant.restype = C.c_char_p
         lib.bk_assemble.argtypes = [vp, C.POINTER(_Grid), dp, C.POINTER(_Face), C.POINTER(vp)]
         lib.bk_operator_free.argtypes = [vp]
         lib.bk_operator_free.restype = None
@@ -429,6 +433,28 @@ class Context:
     @property
     def launch_count(self) -> int:
         return int(_load().bk_launch_count(self.h))
+
+    @property
+    def last_solver_variant(self) -> str:
+        """Kernel instantiation of the last block-CG solve on this context."""
+        return _load().bk_last_solver_variant(self.h).decode()
+
+    def set_option(self, name: str, value: int) -> None:
+        """Per-context kernel-variant switch (bk_set_option): "ring" (-1 auto,
+        0, 1), "no_resident", "force_large", "cg_profile", "no_tma_spmm",
+        "comb_profile", "batch_trace"."""
+        _raise(_load().bk_set_option(self.h, name.encode(), int(value)), self.h, "set_option")
+
+    @contextlib.contextmanager
+    def options(self, **kv):
+        """Temporarily set kernel-variant switches (restored to 0 / auto)."""
+        for k, v in kv.items():
+            self.set_option(k, v)
+        try:
+            yield self
+        finally:
+            for k in kv:
+                self.set_option(k, -1 if k == "ring" else 0)
 
 
 _default_ctx: Optional[Context] = None

@@ -746,6 +746,13 @@ bk_status bk_create(int device, bk_ctx** out) {
     bk_ctx* ctx = new (std::nothrow) bk_ctx;
     if (!ctx) return BK_OOM;
     ctx->device = device;
+    if (const char* e = getenv("BK_CG_RING")) ctx->knobs.ring = atoi(e) != 0;
+    ctx->knobs.no_resident = getenv("BK_CG_NO_RESIDENT") != nullptr;
+    ctx->knobs.force_large = getenv("BK_CG_LARGE") != nullptr;
+    ctx->knobs.cg_profile = getenv("BK_CG_PROFILE") != nullptr;
+    ctx->knobs.no_tma_spmm = getenv("BK_NO_TMA_SPMM") != nullptr;
+    ctx->knobs.comb_profile = getenv("BK_COMB_PROFILE") != nullptr;
+    ctx->knobs.batch_trace = getenv("BK_BATCH_TRACE") != nullptr;
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete ctx;
@@ -754,6 +761,24 @@ bk_status bk_create(int device, bk_ctx** out) {
     ctx->stream = ctx->own_stream;
     for (auto& e : ctx->ev) cudaEventCreate(&e);
     *out = ctx;
+    return BK_OK;
+}
+
+const char* bk_last_solver_variant(const bk_ctx* ctx) {
+    return ctx ? ctx->last_variant.c_str() : "";
+}
+
+bk_status bk_set_option(bk_ctx* ctx, const char* name, int value) {
+    if (!ctx || !name) return BK_INVALID_CONFIG;
+    const std::string k(name);
+    if (k == "ring") ctx->knobs.ring = value < 0 ? -1 : value != 0;
+    else if (k == "no_resident") ctx->knobs.no_resident = value != 0;
+    else if (k == "force_large") ctx->knobs.force_large = value != 0;
+    else if (k == "cg_profile") ctx->knobs.cg_profile = value != 0;
+    else if (k == "no_tma_spmm") ctx->knobs.no_tma_spmm = value != 0;
+    else if (k == "comb_profile") ctx->knobs.comb_profile = value != 0;
+    else if (k == "batch_trace") ctx->knobs.batch_trace = value != 0;
+    else return fail(ctx, BK_INVALID_CONFIG, "bk_set_option: unknown option " + k);
     return BK_OK;
 }
 
@@ -1122,7 +1147,7 @@ bk_status bk_generate_batch(bk_ctx* ctx, int n_chips, const bk_grid* grids,
     if (streams > 1) {
         bool fused = streams <= 64 && s >= 1 && s <= 32;
         const int64_t n0 = (int64_t)grids[0].nx * grids[0].ny * grids[0].nz;
-        fused = fused && n0 < ((int64_t)1 << 21) && !getenv("BK_CG_LARGE") && !getenv("BK_CG_GENERIC");
+        fused = fused && n0 < ((int64_t)1 << 21) && !ctx->knobs.force_large;
         for (int c = 0; c < n_chips && fused; ++c) {
             fused = grids[c].nx == grids[0].nx && grids[c].ny == grids[0].ny &&
                     grids[c].nz == grids[0].nz;

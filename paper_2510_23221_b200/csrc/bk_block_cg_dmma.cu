@@ -1,8 +1,7 @@
 // Block conjugate gradient — DMMA variant (kernel widths S = 8, 16, 32).
 //
-// Same algorithm and control flow as the generic kernel (bk_block_cg.cu; the
-// reference is block_cg, solvers.cpp:452-665), restructured around FP64 tensor
-// cores: every dense s x s product runs on mma.sync.m16n8k4.f64 (measured
+// The reference algorithm is block_cg (solvers.cpp:452-665), restructured
+// around FP64 tensor cores: every dense s x s product runs on mma.sync.m16n8k4.f64 (measured
 // 74 TFLOP/s on B200 vs 37 for SIMT DFMA), with operand fragments produced in
 // registers by the sweep that loads them — no shared-memory staging except a
 // warp-private transpose for R^T Z.
@@ -28,6 +27,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "bk_common.cuh"
 #include "bk_small_solve.cuh"
@@ -339,7 +339,14 @@ template <bool MULTI>
 struct Group {
     int chip, b, NB;
     unsigned* bar;
+    bool ring;  // phase 1 reads P through the async proxy (TMA row ring)
     __device__ __forceinline__ void sync(cg::grid_group& grid) const {
+        // P (and every other block vector) is written with generic stores and,
+        // in ring mode, read back by cp.async.bulk (async proxy) after this
+        // barrier, possibly by another CTA: order the writer's generic global
+        // stores before the async-proxy reads (PTX memory model, proxy fence
+        // on the writing side; the issuing thread fences again before issue)
+        if (ring) asm volatile("fence.proxy.async.global;" ::: "memory");
         if constexpr (MULTI)
             group_barrier(bar, (unsigned)NB, b == 0);
         else
@@ -568,8 +575,11 @@ __device__ void phase_spmm_gram_ring(const Args& a, int64_t c0, int64_t c1, int6
         rg.ph ^= 1u << sl;
     };
     if (threadIdx.x == 0) {
-        // the ring's previous contents were read / written by the generic proxy
+        // the ring's previous contents were read / written by the generic proxy;
+        // P rows of this and neighbouring CTAs were written by generic global
+        // stores before the last group barrier
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
         for (int64_t r = ra; r <= r0 + 2; ++r) issue(r);
     }
     wait_row(r0 - 1);
@@ -859,6 +869,7 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         gr.b = (int)blockIdx.x;
         gr.bar = nullptr;
     }
+    gr.ring = a.ring != 0;
     const int NB = gr.NB, b = gr.b;
     constexpr bool kAlias = scratch_aliases_tiles<S>();
     double* const scr = kAlias ? &sm.tileR[0][0] : sm.scratch;
@@ -1248,12 +1259,18 @@ size_t ring_bytes(int nx) {
     return 16 + (size_t)kRing * nx * S * sizeof(double) + 2 * kRing * sizeof(unsigned long long);
 }
 template <int S>
-bool want_ring(bool resident, int nx, int nz_chip) {
+bool want_ring(const bk_ctx* ctx, bool resident, int nx, int nz_chip) {
     if (resident || nz_chip != 1 || nx % 16 != 0 || S > 16) return false;
     if ((size_t)3 * kRing * nx > (size_t)CtaShape<S>::NW * 16 * Strides<S>::RS) return false;
     if (sizeof(Sm<S, false>) + ring_bytes<S>(nx) > 232448) return false;
-    if (const char* e = getenv("BK_CG_RING")) return atoi(e) != 0;
+    if (ctx->knobs.ring >= 0) return ctx->knobs.ring != 0;
     return true;
+}
+
+template <int S>
+std::string variant_name(bool res, bool multi, bool def, bool ring) {
+    return "block_cg_dmma_kernel<" + std::to_string(S) + "," + (res ? "1" : "0") + "," +
+           (multi ? "1" : "0") + "," + (def ? "1" : "0") + ">" + (ring ? " ring" : "");
 }
 
 template <int S>
@@ -1271,13 +1288,14 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
     if (nb < 1) nb = 1;
     // shared-memory-resident X/R when every CTA's range fits (S <= 16)
     const int64_t max_cells = 16 * ((ntiles + nb - 1) / nb);
-    const bool resident = S <= 16 && max_cells <= kResCells && getenv("BK_CG_NO_RESIDENT") == nullptr;
-    const bool ring = want_ring<S>(resident, op->nx, op->nz);
+    const bool resident = S <= 16 && max_cells <= kResCells && !ctx->knobs.no_resident;
+    const bool ring = want_ring<S>(ctx, resident, op->nx, op->nz);
     const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, false, false>
                        : (ring || S >= 32) ? (const void*)block_cg_dmma_kernel<S, false, false, true>
                                            : (const void*)block_cg_dmma_kernel<S, false, false, false>;
     const size_t smem = (resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>)) +
                         (ring ? ring_bytes<S>(op->nx) : 0);
+    ctx->last_variant = variant_name<S>(resident, false, !resident && (ring || S >= 32), ring);
     BK_CUDA_TRY(ctx, bk::set_max_smem((const void*)kern, smem));
     int occ = 0;
     BK_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BS, smem));
@@ -1331,13 +1349,13 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
     a.nchip = n;
     a.bars = nullptr;
     a.ring = ring;
-    const bool want_prof = getenv("BK_CG_PROFILE") != nullptr;
+    const bool want_prof = ctx->knobs.cg_profile;
     a.prof = want_prof ? (long long*)((char*)pRep + sizeof(CgReport)) : nullptr;
     if (want_prof)
         BK_CUDA_TRY(ctx, cudaMemsetAsync(a.prof, 0, PROF_ITERS * PROF_MARKS * sizeof(long long),
                                          ctx->stream));
     void* args[] = {&a};
-    const bool trace = getenv("BK_BATCH_TRACE") != nullptr;
+    const bool trace = ctx->knobs.batch_trace;
     if (trace) fprintf(stderr, "[trace ctx %p] launch cg nb=%lld\n", (void*)ctx, (long long)nb);
     BK_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(kern, dim3((unsigned)nb), dim3(BS), args, smem,
                                                  ctx->stream));
@@ -1394,13 +1412,15 @@ bk_status run_dmma_multi(bk_ctx* ctx, const bk_operator* op, int K, const double
     if (cpc < 1) return fail(ctx, BK_INVALID_CONFIG, "block_cg: too many chips for the SMs");
     const int64_t nb = (int64_t)K * cpc;
     const int64_t max_cells = 16 * ((ntiles + cpc - 1) / cpc);
-    const bool resident = S <= 16 && max_cells <= kResCells && getenv("BK_CG_NO_RESIDENT") == nullptr;
-    const bool ring = want_ring<S>(resident, op->nx, op->nz / K);
+    const bool resident = S <= 16 && max_cells <= kResCells && !ctx->knobs.no_resident;
+    const bool ring = want_ring<S>(ctx, resident, op->nx, op->nz / K);
     const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, true, false>
                        : (ring || S >= 32) ? (const void*)block_cg_dmma_kernel<S, false, true, true>
                                            : (const void*)block_cg_dmma_kernel<S, false, true, false>;
     const size_t smem = (resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>)) +
                         (ring ? ring_bytes<S>(op->nx) : 0);
+    ctx->last_variant = variant_name<S>(resident, true, !resident && (ring || S >= 32), ring) +
+                        " chips=" + std::to_string(K);
     BK_CUDA_TRY(ctx, set_max_smem(kern, smem));
     int occ = 0;
     BK_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BS, smem));
@@ -1443,7 +1463,7 @@ bk_status run_dmma_multi(bk_ctx* ctx, const bk_operator* op, int K, const double
     a.precond = cfg->precond;
     a.rep = (CgReport*)pRep;
     a.prof = nullptr;
-    const bool want_prof = getenv("BK_CG_PROFILE") != nullptr;
+    const bool want_prof = ctx->knobs.cg_profile;
     long long* dprof = nullptr;
     if (want_prof) {
         void* pp;
@@ -1498,15 +1518,13 @@ bk_status block_cg_device_multi(bk_ctx* ctx, const bk_operator* op, int K, const
 
 bk_status block_cg_device(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
                           const bk_solver_cfg* cfg, double* X, CgReport* rep) {
-    if (getenv("BK_CG_GENERIC")) return block_cg_generic(ctx, op, B, s, cfg, X, rep);
     // wide blocks or large grids: one kernel per phase (HBM-bound phases of
     // milliseconds make launch / host-control costs negligible)
     const bool large = s > 32 || (op->n >= (int64_t)1 << 21 && s > 16);
-    if (getenv("BK_CG_LARGE") || large) return block_cg_large(ctx, op, B, s, cfg, X, rep);
+    if (ctx->knobs.force_large || large) return block_cg_large(ctx, op, B, s, cfg, X, rep);
     if (s <= 8) return run_dmma<8>(ctx, op, B, s, cfg, X, rep);
     if (s <= 16) return run_dmma<16>(ctx, op, B, s, cfg, X, rep);
-    if (s <= 32) return run_dmma<32>(ctx, op, B, s, cfg, X, rep);
-    return block_cg_generic(ctx, op, B, s, cfg, X, rep);
+    return run_dmma<32>(ctx, op, B, s, cfg, X, rep);
 }
 
 }  // namespace bk

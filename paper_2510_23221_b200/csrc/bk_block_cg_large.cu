@@ -21,6 +21,7 @@
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "bk_common.cuh"
@@ -849,9 +850,9 @@ cudaError_t launch_pupdate(const SweepArgs& a, int nb, cudaStream_t s) {
 // phase 1 launch: the TMA variant for S = 64 on grids whose x-runs are full
 // (nx % 16 == 0), else the cp.async-free direct-load kernel
 template <int S>
-cudaError_t launch_spmm(const SweepArgs& a, int nb, cudaStream_t s) {
+cudaError_t launch_spmm(const SweepArgs& a, int nb, cudaStream_t s, bool no_tma) {
     if constexpr (S == 64) {
-        if (a.sl.nx % 16 == 0 && getenv("BK_NO_TMA_SPMM") == nullptr) {
+        if (a.sl.nx % 16 == 0 && !no_tma) {
             const cudaError_t e = bk::set_max_smem((const void*)k_spmm_gram_tma64, smem_spmm_tma64());
             if (e != cudaSuccess) return e;
             k_spmm_gram_tma64<<<nb, LBS, smem_spmm_tma64(), s>>>(a);
@@ -1175,6 +1176,8 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     a.precond = cfg->precond;
     const int nb = sweep_ctas(ctx, sl, S);
     constexpr int E = S * S + S;
+    ctx->last_variant = "block_cg_large<" + std::to_string(S) + ">" +
+                        ((S == 64 && sl.nx % 16 == 0 && !ctx->knobs.no_tma_spmm) ? " tma" : "");
     void *pPart, *pRed, *pCtl, *pHost;
     bk_status st;
     if ((st = workspace(ctx, kSlotCgPart, (size_t)nb * E * 8, &pPart)) != BK_OK) return st;
@@ -1245,7 +1248,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     a.coef2 = ctl->akeep;
     for (int m = 1; m <= cfg->max_iter && sa > 0; ++m) {
         halo(a.P);
-        BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s));
+        BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s, ctx->knobs.no_tma_spmm));
         ++ctx->launches;
         reduce(S * S, nb);
         k_ctl_alpha<S><<<1, CBS, cs, s>>>(ctl, red);
@@ -1401,7 +1404,7 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
             ++ctx->launches;
             break;
         case BK_DD_SPMM:
-            BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s));
+            BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s, ctx->knobs.no_tma_spmm));
             ++ctx->launches;
             reduce(S * S, nb);
             break;

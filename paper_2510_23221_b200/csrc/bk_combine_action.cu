@@ -694,7 +694,7 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
     kern<<<(unsigned)grid, SH::NT, smem, ctx->stream>>>(map, a);
     ++ctx->launches;
     BK_CUDA_TRY(ctx, cudaGetLastError());
-    if (getenv("BK_COMB_PROFILE")) {
+    if (ctx->knobs.comb_profile) {
         long long hp[64] = {};
         cudaStreamSynchronize(ctx->stream);
         cudaMemcpyFromSymbol(hp, g_comb_prof, sizeof(hp));

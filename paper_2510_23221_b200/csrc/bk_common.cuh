@@ -22,7 +22,23 @@
         }                                                                         \
     } while (0)
 
+// Debug / A-B switches of one context: read once from the environment when
+// the context is created (BK_CG_RING=0|1, BK_CG_NO_RESIDENT, BK_CG_LARGE,
+// BK_CG_PROFILE, BK_NO_TMA_SPMM, BK_COMB_PROFILE, BK_BATCH_TRACE) and
+// settable per context through bk_set_option.
+struct bk_knobs {
+    int ring = -1;             // -1: automatic, 0 / 1: force the row ring off / on
+    bool no_resident = false;  // never keep X / R resident in shared memory
+    bool force_large = false;  // multi-kernel engine for every solve
+    bool cg_profile = false;   // in-kernel phase timestamps (stderr)
+    bool no_tma_spmm = false;  // S = 64 phase 1 without TMA
+    bool comb_profile = false; // combine/action stage timestamps (stderr)
+    bool batch_trace = false;
+};
+
 struct bk_ctx {
+    bk_knobs knobs;
+    std::string last_variant;  // kernel instantiation of the last block-CG solve
     int device = 0;
     int num_sms = 0;
     cudaStream_t own_stream = nullptr;
@@ -160,8 +176,7 @@ bk_status block_cg_device(bk_ctx* ctx, const bk_operator* op, const double* B, i
                           const bk_solver_cfg* cfg, double* X, CgReport* rep);
 bk_status block_cg_large(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
                          const bk_solver_cfg* cfg, double* X, CgReport* rep);
-bk_status block_cg_generic(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
-                           const bk_solver_cfg* cfg, double* X, CgReport* rep);
+
 
 // S = kernel width of X (n x S, zero-padded), s = real basis width (rows of
 // C read), C row stride ldc (>= N: a sample sub-range of a wider C).

@@ -1,0 +1,111 @@
+"""GPU parity of the exact kernel instantiations bench.py times.
+
+The C2 batched step (bench.py CHIPS_BY_CONFIG[2] = 16 chips per launch) runs
+bk_generate_batch(streams=K) on z-stacked single-plane chips too large for
+shared-memory residency, so the solve is block_cg_dmma_kernel<16,0,1,1>: one
+cooperative launch for K chips (per-chip CTA groups and group barriers), phase 1
+through the TMA row ring, X += P alpha deferred to phase 3. These tests run
+that instantiation (asserted through bk_last_solver_variant) against the CPU
+oracle (block_cg, solvers.cpp:452-665; combine/action, pipeline.cpp:187-251):
+
+* capped iterates (m = 1, 2, 7) equal the oracle's to 1e-12 with identical
+  matvec counts (unit coefficients: T_j = X[:, j], pipeline.cpp:201-220);
+* the full solve's (T, q) within 1e-9 relative L2 of the oracle's.
+"""
+import numpy as np
+import pytest
+
+from conftest import grid_tuple, rel_l2
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+PARITY = 1e-9
+
+
+def cfg(max_iter=100000):
+    import paper_2510_23221_b200 as bk
+    return bk.SolverConfig(TOL, max_iter, "jacobi")
+
+
+def dev_chips(bk, chips, eye=False):
+    import torch
+    from types import SimpleNamespace
+
+    dev = torch.device("cuda", 0)
+    out = []
+    for ch in chips:
+        s = ch.q_basis.shape[1]
+        coef = np.eye(s) if eye else ch.coef
+        out.append(SimpleNamespace(grid=ch.grid, bc=ch.bc, k=torch.from_numpy(ch.k).to(dev),
+                                   q_basis=torch.from_numpy(ch.q_basis).to(dev),
+                                   coef=torch.from_numpy(np.ascontiguousarray(coef)).to(dev)))
+    return out
+
+
+def run_batch(bk, ctx, dchips, c, streams):
+    import torch
+
+    dev = torch.device("cuda", 0)
+    n, N = dchips[0].grid.cell_count(), int(dchips[0].coef.shape[1])
+    T = [torch.empty((N, n), dtype=torch.float64, device=dev) for _ in dchips]
+    Q = [torch.empty((N, n), dtype=torch.float64, device=dev) for _ in dchips]
+    R = [torch.empty(N, dtype=torch.float64, device=dev) for _ in dchips]
+    _, _, _, reps, _ = bk.generate_batch(dchips, c, t_out=T, q_out=Q, resid_out=R,
+                                         streams=streams, ctx=ctx, check_converged=False)
+    torch.cuda.synchronize()
+    return [t.cpu().numpy() for t in T], [q.cpu().numpy() for q in Q], \
+        [r.cpu().numpy() for r in R], reps
+
+
+# (nx, ny, chips per launch, chips whose full solve is compared with the oracle)
+CASES = [(64, 48, 4, 4), (256, 256, 2, 1)]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_batched_ring_deferred_capped_iterates(bk, ctx, oracle, case):
+    nx, ny, K, _ = case
+    chips = [bk.synth_chip(2, nx, ny, 1, 16, 16, chip_id=c) for c in range(K)]
+    dch = dev_chips(bk, chips, eye=True)
+    ops = []
+    for ch in chips:
+        o = oracle.assemble(grid_tuple(ch.grid), ch.k, ch.bc.as_tuples())
+        ops.append((o, oracle.rhs_from_power(o, ch.q_basis)))
+    with ctx.options(no_resident=1):
+        for m in (1, 2, 7):
+            T, _, _, reps = run_batch(bk, ctx, dch, cfg(m), K)
+            assert ctx.last_solver_variant == f"block_cg_dmma_kernel<16,0,1,1> ring chips={K}"
+            for c, (o, B) in enumerate(ops):
+                X, rep = oracle.block_cg(o, B, TOL, m, 1)
+                assert reps[c].iterations == m
+                assert reps[c].matvec_count == rep["matvec_count"]
+                assert rel_l2(T[c].T, X) <= 1e-12, (m, c)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_batched_ring_deferred_full_chain(bk, ctx, oracle, case):
+    nx, ny, K, n_full = case
+    chips = [bk.synth_chip(2, nx, ny, 1, 16, 16, chip_id=c) for c in range(K)]
+    dch = dev_chips(bk, chips)
+    with ctx.options(no_resident=1):
+        T, Q, R, reps = run_batch(bk, ctx, dch, cfg(), K)
+        assert ctx.last_solver_variant == f"block_cg_dmma_kernel<16,0,1,1> ring chips={K}"
+    for c in range(n_full):
+        ch = chips[c]
+        o = oracle.assemble(grid_tuple(ch.grid), ch.k, ch.bc.as_tuples())
+        X, rep = oracle.block_cg(o, oracle.rhs_from_power(o, ch.q_basis), TOL, 100000, 1)
+        To, Qo, Ro = oracle.combine_action(o, X, ch.coef)
+        assert reps[c].all_converged() and rep["converged"].all()
+        assert abs(reps[c].iterations - rep["iterations"]) <= max(3, rep["iterations"] // 10)
+        for j in range(ch.coef.shape[1]):
+            assert rel_l2(T[c][j], To[j]) <= PARITY, (c, j)
+            assert rel_l2(Q[c][j], Qo[j]) <= PARITY, (c, j)
+        assert float(np.max(R[c])) <= 1e-12
+
+
+def test_bench_c2_default_is_the_ring_kernel(bk, ctx):
+    """Without overrides, 16 z-stacked C2 chips (the bench step) select the
+    ring / multi / deferred instantiation the tests above pin."""
+    chips = [bk.synth_chip(2, 256, 256, 1, 16, 4, chip_id=c) for c in range(16)]
+    T, _, _, reps = run_batch(bk, ctx, dev_chips(bk, chips), cfg(3), 16)
+    assert ctx.last_solver_variant == "block_cg_dmma_kernel<16,0,1,1> ring chips=16"
+    assert all(r.iterations == 3 for r in reps)

@@ -464,45 +464,45 @@ def sub_budget(streams):
 
 
 @pytest.mark.parametrize("case", [(2, 64, 48, 1, 16), (1, 48, 40, 1, 8)])
-def test_block_cg_row_ring_path_vs_oracle(bk, ctx, oracle, case, monkeypatch):
+def test_block_cg_row_ring_path_vs_oracle(bk, ctx, oracle, case):
     """Single-plane chips outside resident mode run phase 1 through the TMA row
     ring, with X += P alpha deferred to phase 3 (S = 16): capped iterates equal
     the oracle's, a full solve converges to it."""
-    monkeypatch.setenv("BK_CG_NO_RESIDENT", "1")
     inp = bk.synth_chip(*case, 4)
     op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
     o = oracle.assemble(grid_tuple(inp.grid), inp.k, inp.bc.as_tuples())
     B = oracle.rhs_from_power(o, inp.q_basis)
-    for m in (1, 2, 7):
-        r = bk.block_cg(op, B, cfg_jacobi(m))
-        X, rep = oracle.block_cg(o, B, TOL, m, 1)
-        assert r.report.iterations == m and r.report.matvec_count == rep["matvec_count"]
-        assert rel_l2(r.x, X) <= 1e-12
-    r = bk.block_cg(op, B, cfg_jacobi())
+    with ctx.options(no_resident=1):
+        for m in (1, 2, 7):
+            r = bk.block_cg(op, B, cfg_jacobi(m))
+            X, rep = oracle.block_cg(o, B, TOL, m, 1)
+            assert r.report.iterations == m and r.report.matvec_count == rep["matvec_count"]
+            assert rel_l2(r.x, X) <= 1e-12
+        r = bk.block_cg(op, B, cfg_jacobi())
     X, rep = oracle.block_cg(o, B, TOL, 100000, 1)
     assert r.report.all_converged() and rel_l2(r.x, X) <= PARITY
 
 
 @pytest.mark.parametrize("case", [(1, 32, 32, 1, 8), (2, 40, 36, 1, 16), (3, 16, 16, 8, 32),
                                   (4, 24, 20, 4, 16)])
-def test_block_cg_multikernel_path_vs_oracle(bk, ctx, oracle, case, monkeypatch):
+def test_block_cg_multikernel_path_vs_oracle(bk, ctx, oracle, case):
     """The one-kernel-per-phase engine (used for s > 32 / large grids and by the
     slab decomposition) forced on small cases: same solution as the oracle."""
-    monkeypatch.setenv("BK_CG_LARGE", "1")
     inp = bk.synth_chip(*case, 4)
     op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
     o = oracle.assemble(grid_tuple(inp.grid), inp.k, inp.bc.as_tuples(), dz=inp.grid.dz)
     B = oracle.rhs_from_power(o, inp.q_basis)
-    r = bk.block_cg(op, B, cfg_jacobi())
-    X, rep = oracle.block_cg(o, B, TOL, 100000, 1)
-    assert r.report.all_converged() and rep["converged"].all()
-    assert rel_l2(r.x, X) <= PARITY
-    assert abs(r.report.iterations - rep["iterations"]) <= max(3, rep["iterations"] // 10)
-    for m in (1, 3):
-        rm = bk.block_cg(op, B, cfg_jacobi(m))
-        Xm, repm = oracle.block_cg(o, B, TOL, m, 1)
-        assert rm.report.iterations == m and rm.report.matvec_count == repm["matvec_count"]
-        assert rel_l2(rm.x, Xm) <= 1e-12
+    with ctx.options(force_large=1):
+        r = bk.block_cg(op, B, cfg_jacobi())
+        X, rep = oracle.block_cg(o, B, TOL, 100000, 1)
+        assert r.report.all_converged() and rep["converged"].all()
+        assert rel_l2(r.x, X) <= PARITY
+        assert abs(r.report.iterations - rep["iterations"]) <= max(3, rep["iterations"] // 10)
+        for m in (1, 3):
+            rm = bk.block_cg(op, B, cfg_jacobi(m))
+            Xm, repm = oracle.block_cg(o, B, TOL, m, 1)
+            assert rm.report.iterations == m and rm.report.matvec_count == repm["matvec_count"]
+            assert rel_l2(rm.x, Xm) <= 1e-12
 
 
 @pytest.mark.parametrize("nslabs", [1, 2, 3])
