@@ -3,15 +3,19 @@
 
 A step is one pass of the hot path over one chip of synthetic input: assemble
 the stencil, form B = V q + g, block-CG basis solve, fused combine + operator
-action writing N (T, q) sample pairs. Default workload = BASELINE config 2
-(256x256x1 2D die, s=16 basis maps, N=2048 samples, block CG to 1e-12 with
-Jacobi). Multi-GPU: one process per GPU, each rank solves its own seeded chip
-(chip_id = rank) — independent chips, no data-path collective, weak scaling.
+action writing the chip's N (T, q) sample pairs. Default workload = BASELINE
+config 5, the largest config that fits one GPU: 512x512x16 layered stack
+(4.2 M cells), s = 64 basis maps, N = 5000 samples, block CG with Jacobi.
+Configs 1-4 are selectable with --config (the N=1 line of config 2, the
+batched 16-chip step, is also reported inside the config-5 line under
+"extra_configs"). Multi-GPU: one process per GPU; configs 1-4 shard
+independent chips (no data-path collective, weak scaling); config 5 splits the
+chip into y-slabs (halo rows + NCCL Gram all-reduce, strong scaling).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5]
     python bench.py --impl reference ...   # the reference CPU core (oracle/_ref)
 
-Prints ONE JSON line on rank 0 (see DESIGN.md §Measurement for every field).
+Prints ONE JSON line on rank 0 (DESIGN.md §6 describes every field).
 """
 from __future__ import annotations
 
@@ -30,26 +34,41 @@ sys.path.insert(0, ROOT)
 
 METRIC = "(q,T) samples/sec"
 UNIT = "samples/s"
-TOL = 1e-12
 
+# (config id, nx, ny, nz, s, N) — BASELINE.json configs 1..5 (N per chip)
+CONFIGS = {
+    1: (1, 64, 64, 1, 8, 256),
+    2: (2, 256, 256, 1, 16, 2048),
+    3: (3, 128, 128, 8, 32, 5000),
+    4: (4, 128, 128, 4, 16, 8),
+    5: (5, 512, 512, 16, 64, 5000),
+}
 WORKLOADS = {
     1: "C1: 64x64x1 2D die (4x4 k tiles, 3 blobs/map), s=8, N=256",
     2: "C2: 256x256x1 2D die (16x16 k tiles, 5 blobs/map), s=16, N=2048",
     3: "C3: 128x128x8 layered stack (lognormal k), s=32, N=5000",
     4: "C4: batch of distinct chips 128x128x4 (per-chip dz, k, h), s=16, 8 samples/chip",
-    5: "C5: 512x512x16 layered stack, s=64, N=5000 (outputs streamed through a device ring)",
+    5: "C5: 512x512x16 layered stack (lognormal k), s=64, N=5000",
 }
+DEFAULT_CONFIG = 5
 C4_CHIPS_PER_STEP = 32   # chips per GPU per timed step (5000 chips total at full scale)
 C4_MAX_ITER = 5000
-DIRECT_MAX_ITER = 5000    # per-sample CG baseline (a lone column can stall at the fp64 floor)
-C4_STREAMS = 32           # chips per batched solve (one cooperative launch, 1/32 of the SMs each; measured best of 8/16/32)
+DIRECT_MAX_ITER = 5000    # per-sample CG baseline
+C4_STREAMS = 32           # chips per batched solve (one cooperative launch, 1/32 of the SMs each)
 # Tolerance pins: 1e-12 for configs 1-3; configs 4-5 use 1e-10
-# because their true relative residual plateaus at ~1.1-2e-12 in fp64 (measured:
-# C5 512x512x16 at 1.1e-12..2.0e-12 after 1200 iterations; C4 chip 4 at 1.28e-12
-# in the oracle), where 1e-12 sends the reference algorithm into endless
-# verify/restart cycles.
+# because their true relative residual plateaus at ~1.1-2e-12 in fp64, where
+# 1e-12 sends the reference algorithm into endless verify/restart cycles.
 TOL_BY_CONFIG = {1: 1e-12, 2: 1e-12, 3: 1e-12, 4: 1e-10, 5: 1e-10}
-C5_RING = 500            # samples per combine/action chunk for C5 (2 x 8.4 GB ring)
+C5_RING = 500            # samples per combine/action launch for C5 (device-resident ring)
+# C5 reference-arm extrapolation: the reference core's own full C5 solve takes
+# ~4.6 h on one core, so it is timed capped and scaled by this iteration count
+# (the GPU engine's count on the same chip at the same tolerance; refreshed
+# from the bench line of the current engine)
+C5_ITERATIONS = 694
+C5_SLAB_ROWS = 64        # y-rows of the reference arm's bounded sample (1/8 of the chip)
+C5_REF_SAMPLES = 16      # samples of the reference arm's combine + action sample
+CHIPS_BY_CONFIG = {1: 64, 2: 16, 3: 12}  # independent chips per GPU per step, solved together
+DMMA_PEAK_TFLOPS = 73.9  # mma.sync.m16n8k4.f64, measured (profiles/r1_summary.md)
 
 
 def peaks():
@@ -57,8 +76,59 @@ def peaks():
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def ncu_traffic(key):
+    """Measured DRAM traffic of a roofline kernel (profiles/ncu_traffic.json)."""
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(tp):
+        return None
+    with open(tp) as f:
+        return json.load(f).get(str(key) if not str(key).startswith("config") else key)
+
+
+def action_roofline(n, s, N, comb_s, peak):
+    """Combine + operator action (SURVEY §8(d)): algorithmic bytes
+    n(8s + 40) + 16 n N and the T = X C product 2 n s N on FP64 tensor cores."""
+    byts = n * (8 * s + 40) + 16 * n * N
+    flops = 2 * n * s * N
+    gbs = byts / comb_s / 1e9
+    tf = flops / comb_s / 1e12
+    return {"kernel": "combine_action_kernel", "ms": comb_s * 1e3, "achieved_GBps": gbs,
+            "peak_GBps": peak, "frac": gbs / peak, "nominal_peak_GBps": 8000.0,
+            "algorithmic_bytes": int(byts), "dmma_TFLOPs": tf,
+            "dmma_peak_TFLOPs": DMMA_PEAK_TFLOPS, "dmma_frac": tf / DMMA_PEAK_TFLOPS}
+
+
+def config_dict(config, world, chips=1):
+    cid, nx, ny, nz, s, N = CONFIGS[config]
+    d = {"workload": WORKLOADS[config], "grid": [nx, ny, nz], "s": s, "samples_per_chip": N,
+         "chips_per_step_per_gpu": chips, "tol": TOL_BY_CONFIG[config], "precond": "jacobi",
+         "parallelism": f"chip-sharded x{world} (no collective)"
+                        + (f", {chips} independent chips per GPU per step, z-stacked and solved "
+                           f"by one cooperative launch ({chips} SM shares)" if chips > 1 else ""),
+         "l2": "flushed between timed steps (512 MiB write)"}
+    if config == 4:
+        d["chips_per_step_per_gpu"] = C4_CHIPS_PER_STEP
+        d["max_iter"] = C4_MAX_ITER
+        d["concurrent_chips"] = C4_STREAMS
+        d["note"] = "chips whose basis solve misses the tolerance are dropped and counted"
+    if config == 5:
+        d["output_ring_samples"] = C5_RING
+        d["l2"] = ("inputs larger than L2: every block vector is 2.1 GB (4.2 M cells x 64 x 8 B) "
+                   "vs the 126 MB L2, and each step streams 5000 x 4.2 M x 16 B of outputs")
+        d["parallelism"] = (f"y-slab DD x{world} (NCCL Gram all-reduce + halo rows), samples split"
+                            if world > 1 else "single GPU")
+    return d
 
 
 # ------------------------------------------------------------------ clocks
@@ -121,199 +191,215 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# ------------------------------------------------------------------ distributed
-def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
 
 
 # ------------------------------------------------------------------ reference arm
-def reference_sample(config: int, threads: int, iter_cap: int, action_samples: int,
-                     chip_offset: int = 0):
-    """Bounded sample of the workload on the reference core (oracle/_ref).
+# The reference is the unmodified CPU core (oracle/_ref, compiled from
+# /root/reference by oracle/Makefile); inputs come from the checker-side
+# generator (oracle/blockoa_oracle.c orc_synth_chip, pinned bitwise to the
+# product's generator by tests/test_oracle.py), so this arm never loads the
+# product library.
+REF_ITERS = {1: None, 2: 464, 3: 241, 4: 228, 5: C5_ITERATIONS}
 
-    `threads` independent chips run concurrently (the reference parallelises
-    across chips/groups only, pipeline.cpp:101,410,511; block_cg itself is
-    single-threaded). Per chip: assemble + rhs_from_power in full, block_cg
-    capped at `iter_cap` iterations and scaled by the full iteration count the
-    reference needs on this workload (tests/golden/c2_full_meta.npz, produced by
-    the reference itself), combine_from_weights + operator_action on
-    `action_samples` of the N samples, scaled to N. Returns per-chip seconds
-    (max over threads) and a description.
-    """
-    import paper_2510_23221_b200 as bk
-    from oracle.oracle import Reference
 
-    ref = Reference()
-    cid, nx, ny, nz, s, N = bk.CONFIGS[config]
-    if config == 2:
-        meta = np.load(os.path.join(ROOT, "tests", "golden", "c2_full_meta.npz"))
-        full_iters = int(meta["iterations"])
-    else:  # config 1: the whole solve is cheap, run it in full
-        full_iters, iter_cap = 0, 100000
-    inputs = [bk.synth_chip(cid, nx, ny, nz, s, N, chip_id=chip_offset + t) for t in range(threads)]
+def _ref_case(oracle, config, chip_id, rows=None):
+    cid, nx, ny, nz, s, N = CONFIGS[config]
+    ch = oracle.synth_chip(cid, nx, ny, nz, s, N, chip_id=chip_id)
+    if rows is None or rows >= ny:
+        return ch, 1.0
+    # a y-slab of the chip: rows [0, rows), same cells, same stencil (the cut
+    # faces are adiabatic, as the chip's sides)
+    k3 = ch.k.reshape(nz, ny, nx)
+    q3 = ch.q_basis.reshape(nz, ny, nx, s)
+    g = ch.grid
+    ch.k = np.ascontiguousarray(k3[:, :rows, :]).ravel()
+    ch.q_basis = np.ascontiguousarray(q3[:, :rows, :, :]).reshape(-1, s)
+    ch.grid = (nx, rows, nz, g[3], g[4] * rows / ny, g[5])
+    return ch, ny / rows
+
+
+def reference_single_chip_step(ref, ch, tol, s, N, m, samples, threads):
+    """One bounded sample of a single-chip config on the reference core:
+    assemble + rhs_from_power (discretize.cpp:114-256) in full on the sample,
+    block_cg (solvers.cpp:452-665, single-threaded as in the reference) capped
+    at m iterations, combine_from_weights + operator_action + relative_residual
+    (pipeline.cpp:187-251) for `samples` samples in parallel_for over
+    `threads` workers. Returns measured seconds per part."""
+    t0 = time.perf_counter()
+    op = ref.assemble(ch.grid, ch.k, ch.bc, dz=ch.dz)
+    B = np.empty_like(ch.q_basis)
+    for j in range(s):
+        B[:, j] = ref.rhs_from_power(op, np.ascontiguousarray(ch.q_basis[:, j]))
+    t1 = time.perf_counter()
+    X, rep = ref.block_cg(op, B, tol, m, 1)
+    t2 = time.perf_counter()
+    basis = ref.basis(op, X)
+    t3 = time.perf_counter()
+    basis.combine_action(ch.coef, 0, samples, threads=threads, outputs=False)
+    t4 = time.perf_counter()
+    return {"setup": t1 - t0, "cg": t2 - t1, "m": rep["iterations"], "action": t4 - t3,
+            "wall": (t2 - t0) + (t4 - t3)}
+
+
+def single_chip_estimate(meas, config, scale, samples):
+    """Full-chip seconds from capped samples: per-iteration cost = mean(m=2) -
+    mean(m=1); init = mean(m=1) - per-iteration; scaled by the iteration
+    count REF_ITERS[config] and the slab factor; the action sample scaled to N."""
+    N = CONFIGS[config][5]
+    c1 = [x["cg"] for x in meas if x["m"] == 1]
+    c2 = [x["cg"] for x in meas if x["m"] == 2]
+    it = max(float(np.mean(c2)) - float(np.mean(c1)), 1e-9)
+    init = max(float(np.mean(c1)) - it, 0.0)
+    setup = float(np.mean([x["setup"] for x in meas]))
+    act = float(np.mean([x["action"] for x in meas])) * N / samples
+    iters = REF_ITERS[config]
+    full = scale * (setup + init + iters * it + act)
+    return full, {"per_iteration_s": it * scale, "init_s": init * scale, "setup_s": setup * scale,
+                  "action_s": act * scale, "iterations": iters}
+
+
+def reference_multi_chip_step(ref, oracle, config, threads, iter_cap, action_samples, offset):
+    """Configs 1, 2, 4: `threads` independent chips run concurrently, one per
+    host thread (the reference parallelises across chips/groups only,
+    pipeline.cpp:101,410,511). Per chip: assemble + rhs in full, block_cg capped
+    at `iter_cap` iterations and scaled by the reference's iteration count,
+    combine + action on `action_samples` of the N samples, scaled to N.
+    Returns per-chip seconds (max over threads)."""
+    cid, nx, ny, nz, s, N = CONFIGS[config]
+    full_iters = REF_ITERS[config]
+    if full_iters is None:  # config 1: the whole solve is cheap, run it in full
+        iter_cap = 100000
+    chips = [oracle.synth_chip(cid, nx, ny, nz, s, N, chip_id=offset + t) for t in range(threads)]
+    tol = TOL_BY_CONFIG[config]
     out = [None] * threads
 
     def work(t):
-        inp = inputs[t]
-        g = inp.grid
+        ch = chips[t]
         t0 = time.perf_counter()
-        op = ref.assemble((g.nx, g.ny, g.nz, g.lx, g.ly, g.lz), inp.k, inp.bc.as_tuples())
-        B = np.stack([ref.rhs_from_power(op, inp.q_basis[:, j]) for j in range(s)], axis=1)
+        op = ref.assemble(ch.grid, ch.k, ch.bc, dz=ch.dz)
+        B = np.stack([ref.rhs_from_power(op, ch.q_basis[:, j]) for j in range(s)], axis=1)
         t1 = time.perf_counter()
-        X, rep = ref.block_cg(op, B, TOL, iter_cap, 1)
+        X, rep = ref.block_cg(op, B, tol, iter_cap, 1)
         t2 = time.perf_counter()
-        ref.combine_action(op, X, np.ascontiguousarray(inp.coef[:, :action_samples]), threads=1)
+        basis = ref.basis(op, X)
         t3 = time.perf_counter()
+        ns = min(action_samples, N)
+        basis.combine_action(ch.coef, 0, ns, threads=1, outputs=False)
+        t4 = time.perf_counter()
         scale = full_iters / max(rep["iterations"], 1) if full_iters else 1.0
-        est = (t1 - t0) + (t2 - t1) * scale \
-            + (t3 - t2) * N / action_samples
-        out[t] = est
+        out[t] = (t1 - t0) + (t2 - t1) * scale + (t4 - t3) * N / ns
 
-    w0 = time.perf_counter()
     ths = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+    w0 = time.perf_counter()
     for th in ths:
         th.start()
     for th in ths:
         th.join()
-    reference_sample.last_wall_s = time.perf_counter() - w0
-    per_chip_s = max(out)
-    desc = (f"{threads} concurrent chips (1 host thread each) of {WORKLOADS[config]}; per chip: "
-            f"assemble+rhs in full, block_cg timed over {iter_cap} iterations and scaled to the "
-            f"reference's {full_iters}-iteration solve, combine+operator_action timed on "
-            f"{action_samples} of {N} samples and scaled; reference core built -O3 x86-64-v3")
-    return per_chip_s, desc
+    return max(out), time.perf_counter() - w0
+
+
+def reference_description(config, threads, extra=None):
+    cid, nx, ny, nz, s, N = CONFIGS[config]
+    if config in (3, 5):
+        rows = C5_SLAB_ROWS if config == 5 else ny
+        return (f"one chip of {WORKLOADS[config]}"
+                + (f", bounded sample = a y-slab of {rows} of {ny} rows "
+                   f"({nx}x{rows}x{nz}, scaled x{ny // rows})" if rows < ny else "")
+                + f"; per step: assemble + rhs_from_power, block_cg capped at 1 or 2 iterations "
+                  f"(alternating; per-iteration cost = mean(m=2) - mean(m=1)) on 1 thread "
+                  f"(block_cg is single-threaded), scaled to {REF_ITERS[config]} iterations (the "
+                  f"GPU solve's count on this chip; the reference's own full solve is not run), "
+                  f"combine_from_weights + operator_action + relative_residual on "
+                  f"{C5_REF_SAMPLES} samples in parallel_for over {threads} threads, scaled to "
+                  f"{N}; inputs from the checker-side generator (orc_synth_chip, bitwise the "
+                  f"product's); reference core built -O3 x86-64-v3")
+    return (f"{threads} concurrent chips (1 host thread each) of {WORKLOADS[config]}; per chip: "
+            f"assemble+rhs in full, block_cg capped and scaled to the reference's "
+            f"{REF_ITERS[config] or 'full'}-iteration solve, combine+operator_action on a "
+            f"sample subset scaled to {N}; inputs from the checker-side generator")
+
+
+def reference_run(config, steps, warmup, iter_cap=24, action_samples=64):
+    """Bounded-sample timing of the reference core on `config`; returns
+    (value samples/s, measured ms per step, cores, description, details)."""
+    from oracle.oracle import Oracle, Reference
+
+    oracle, ref = Oracle(), Reference()
+    threads = os.cpu_count() or 1
+    cid, nx, ny, nz, s, N = CONFIGS[config]
+    if config in (3, 5):
+        rows = C5_SLAB_ROWS if config == 5 else None
+        ch, scale = _ref_case(oracle, config, 0, rows)
+        meas, walls = [], []
+        total = warmup + max(steps, 2)
+        for i in range(total):
+            m = 1 + (i % 2)
+            x = reference_single_chip_step(ref, ch, TOL_BY_CONFIG[config], s, N, m,
+                                           C5_REF_SAMPLES, threads)
+            if i >= warmup:
+                meas.append(x)
+                walls.append(x["wall"])
+        full, det = single_chip_estimate(meas, config, scale, C5_REF_SAMPLES)
+        value = N / full
+        det["extrapolated_s_per_chip"] = full
+        return value, float(np.mean(walls)) * 1e3, threads, \
+            reference_description(config, threads), det
+    per, walls = [], []
+    for i in range(warmup + steps):
+        pc, wall = reference_multi_chip_step(ref, oracle, config, threads, iter_cap,
+                                             action_samples, 0)
+        if i >= warmup:
+            per.append(pc)
+            walls.append(wall)
+    value = threads * N / float(np.mean(per))
+    return value, float(np.mean(walls)) * 1e3, threads, reference_description(config, threads), \
+        {"extrapolated_s_per_chip": float(np.mean(per))}
 
 
 def run_reference_arm(args):
     world, rank, local = dist_env()
     if rank != 0:
         return 0
-    import paper_2510_23221_b200 as bk
     from oracle.oracle import reference_available
 
     if not reference_available():
         print(json.dumps({"impl": "reference", "metric": METRIC,
                           "unavailable": "oracle/_ref/libblockoa_ref.so not built"}))
         return 0
-    if args.config not in (1, 2):
-        print(json.dumps({"impl": "reference", "metric": METRIC,
-                          "unavailable": f"reference arm calibrated for configs 1-2 only "
-                                         f"(config {args.config} takes hours on the CPU core)"}))
-        return 0
-    threads = os.cpu_count() or 1
-    N = bk.CONFIGS[args.config][5]
-    for _ in range(args.warmup):
-        reference_sample(args.config, threads, args.ref_iter_cap, args.ref_action_samples)
-    step_s, wall_s = [], []
-    for _ in range(args.steps):
-        per_chip, desc = reference_sample(args.config, threads, args.ref_iter_cap,
-                                          args.ref_action_samples)
-        step_s.append(per_chip)
-        wall_s.append(reference_sample.last_wall_s)
-    ms = float(np.mean(step_s)) * 1e3
-    value = threads * N / (ms * 1e-3)
+    value, ms, cores, desc, det = reference_run(args.config, args.steps, args.warmup,
+                                                args.ref_iter_cap, args.ref_action_samples)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         # measured wall time of one bounded-sample step; `value` is the full
-        # workload's throughput extrapolated from it (see cpu_baseline.sample)
-        "ms_per_step": float(np.mean(wall_s)) * 1e3,
-        "extrapolated_ms_per_full_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-        "config": config_dict(args.config, world, chips_per_step(args)),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+        # workload's throughput extrapolated from the timed steps (see sample)
+        "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if args.config == 5 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded BASELINE-config generators, DESIGN.md §3)",
+        "config": config_dict(args.config, 1, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": desc},
+        "extrapolation": det,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
     return 0
 
 
-DMMA_PEAK_TFLOPS = 73.9  # mma.sync.m16n8k4.f64, measured (profiles/r1_summary.md)
-
-
-def action_roofline(n, s, N, comb_s, peak):
-    """Combine + operator action (SURVEY §8(d)): algorithmic bytes
-    n(8s + 40) + 16 n N and the T = X C product 2 n s N on FP64 tensor cores."""
-    byts = n * (8 * s + 40) + 16 * n * N
-    flops = 2 * n * s * N
-    gbs = byts / comb_s / 1e9
-    tf = flops / comb_s / 1e12
-    return {"kernel": "combine_action_kernel", "ms": comb_s * 1e3, "achieved_GBps": gbs,
-            "peak_GBps": peak, "frac": gbs / peak, "nominal_peak_GBps": 8000.0,
-            "dmma_TFLOPs": tf, "dmma_peak_TFLOPs": DMMA_PEAK_TFLOPS,
-            "dmma_frac": tf / DMMA_PEAK_TFLOPS}
-
-
-def ncu_traffic(config):
-    """Measured DRAM traffic of the roofline kernel (profiles/ncu_traffic.json)."""
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if not os.path.exists(tp):
-        return None
-    with open(tp) as f:
-        return json.load(f).get(f"config{config}")
-
-
-CHIPS_BY_CONFIG = {1: 64, 2: 16, 3: 12}  # independent chips per GPU per step, solved together
-
-
-def chips_per_step(args):
-    if args.config not in CHIPS_BY_CONFIG:
-        return 1
-    return args.chips if args.chips else CHIPS_BY_CONFIG[args.config]
-
-
-def config_dict(config, world, chips=1):
-    import paper_2510_23221_b200 as bk
-
-    cid, nx, ny, nz, s, N = bk.CONFIGS[config]
-    d = {"workload": WORKLOADS[config], "grid": [nx, ny, nz], "s": s, "samples_per_chip": N,
-         "chips_per_step_per_gpu": chips, "tol": TOL_BY_CONFIG[config], "precond": "jacobi",
-         "parallelism": f"chip-sharded x{world} (no collective)"
-                        + (f", {chips} independent chips per GPU per step, z-stacked and solved "
-                           f"by one cooperative launch ({chips} SM shares)" if chips > 1 else ""),
-         "l2": "flushed between timed steps (512 MiB write)"}
-    if config == 4:
-        d["chips_per_step_per_gpu"] = C4_CHIPS_PER_STEP
-        d["max_iter"] = C4_MAX_ITER
-        d["concurrent_chips"] = C4_STREAMS
-        d["note"] = "chips whose basis solve misses the tolerance are dropped and counted"
-    if config == 5:
-        d["output_ring_samples"] = C5_RING
-        d["parallelism"] = (f"y-slab DD x{world} (NCCL Gram all-reduce + halo rows), samples split"
-                            if world > 1 else "single GPU")
-    return d
-
-
-# ------------------------------------------------------------------ our arm
-def run_ours(args):
+def run_chips(args, ctx, world, rank, local, config, legs=True):
+    """Configs 1-3: the single-chip latency view (one chip per step on the
+    whole GPU) and `value` = K independent chips per GPU per step solved by one
+    batched cooperative launch (bk_generate_batch). Returns the JSON line
+    (rank 0) or None."""
     import torch
 
     import paper_2510_23221_b200 as bk
 
-    world, rank, local = dist_env()
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py: no CUDA device (the product has no CPU path)")
-    torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    ctx = bk.Context(local)
     stream = torch.cuda.current_stream()
-    ctx.set_stream(stream.cuda_stream)
-
-    if args.config == 4:
-        return run_ours_batch(args, ctx, world, rank, local)
-    if args.config == 5:
-        return run_ours_large(args, ctx, world, rank, local)
-    cid, nx, ny, nz, s, N = bk.CONFIGS[args.config]
+    cid, nx, ny, nz, s, N = CONFIGS[config]
     inp = bk.synth_chip(cid, nx, ny, nz, s, N, chip_id=rank)
     n = inp.grid.cell_count()
-    cfg = bk.SolverConfig(TOL, 100000, "jacobi")
+    cfg = bk.SolverConfig(TOL_BY_CONFIG[config], 100000, "jacobi")
     dev = torch.device("cuda", local)
     k_d = torch.from_numpy(inp.k).to(dev)
     q_d = torch.from_numpy(inp.q_basis).to(dev)
@@ -372,7 +458,7 @@ def run_ours(args):
     # Device-resident inputs and outputs, CUDA events around the synchronous
     # call, L2 flushed before every step, max over ranks.
     from types import SimpleNamespace
-    K = chips_per_step(args)
+    K = CHIPS_BY_CONFIG.get(config, 1) if not args.chips else args.chips
     if K > 1:
         to_dev = lambda a: torch.from_numpy(a).to(dev)  # noqa: E731
         chips_d = []
@@ -417,10 +503,29 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             btotal_s = float(t.item())
         value = K * N * args.steps * world / btotal_s
+        batch_variant = ctx.last_solver_variant
+        # spot check: chip 0 of the timed batch against the one-chip pipeline
+        # with the same SM budget (bitwise: same kernels, same CTA ranges)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        ntile = (n + 15) // 16
+        cpc = sms // K
+        if cpc * 2 > ntile:
+            cpc = (ntile + 1) // 2
+        sub = bk.Context(local)
+        sub.set_stream(stream.cuda_stream)
+        bk.set_cg_sm_budget(sub, cpc)
+        T1, Q1, _, rep1, _ = bk.generate_chip(chips_d[0].grid, chips_d[0].k, chips_d[0].bc,
+                                              chips_d[0].q_basis, chips_d[0].coef, cfg, ctx=sub)
+        spot = {"chip": 0, "budget_ctas": cpc, "one_chip_variant": sub.last_solver_variant,
+                "bitwise_T": bool(np.array_equal(Tk[0].cpu().numpy(), T1)),
+                "bitwise_q": bool(np.array_equal(Qk[0].cpu().numpy(), Q1)),
+                "iterations": [int(breps[0].iterations), int(rep1.iterations)]}
+        sub.close()
         del Tk, Qk, Rk
     else:
         value, bstep_ms = single_value, step_ms
         bsolve, biters = [], []
+        batch_variant, spot = ctx.last_solver_variant, None
 
     # ---- direct baseline (the paper's comparison): each sample
     # solved on its own — block CG with one column is the reference's cg
@@ -428,8 +533,8 @@ def run_ours(args):
     # batched 16 one-column systems per cooperative launch. Cross-checked
     # against BlocKOA's T for the same samples.
     direct = None
-    if rank == 0 and not args.no_direct:
-        M = min(N, {1: 64, 2: 32}.get(args.config, 16))
+    if rank == 0 and legs and not args.no_direct:
+        M = min(N, {1: 64, 2: 32}.get(config, 16))
         qs = inp.q_basis @ inp.coef[:, :M]  # the samples' power maps (u_inf = 0: no lift)
         one = torch.ones((1, 1), dtype=torch.float64, device=dev)
         dchips = [SimpleNamespace(grid=inp.grid, bc=inp.bc, k=k_d,
@@ -439,7 +544,7 @@ def run_ours(args):
         Qdir = [torch.empty((1, n), dtype=torch.float64, device=dev) for _ in range(M)]
         Rdir = [torch.empty(1, dtype=torch.float64, device=dev) for _ in range(M)]
         Kd = min(16, M)
-        dcfg = bk.SolverConfig(TOL, DIRECT_MAX_ITER, "jacobi")
+        dcfg = bk.SolverConfig(TOL_BY_CONFIG[config], DIRECT_MAX_ITER, "jacobi")
         bk.generate_batch(dchips[:Kd], dcfg, t_out=Tdir[:Kd], q_out=Qdir[:Kd], resid_out=Rdir[:Kd],
                           streams=Kd, ctx=ctx, check_converged=False)
         barrier()
@@ -506,40 +611,35 @@ def run_ours(args):
 
     peak, peak_kind = peaks()
     dataset = None
-    if rank == 0 and not args.no_dataset:
+    if rank == 0 and legs and not args.no_dataset:
         dataset = dataset_leg(bk, torch, ctx, stream, inp, k_d, T_d, Q_d, R_d, peak)
     refpipe = None
-    if rank == 0 and not args.no_refpipe:
+    if rank == 0 and legs and not args.no_refpipe:
         refpipe = reference_pipeline_leg(bk, torch, ctx)
 
     if rank != 0:
-        if world > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
-        return 0
+        return None
 
     # ---- roofline of the dominant kernel (persistent block CG)
     bytes_per_iter = n * (40 + 80 * s)
     mean_iters = float(np.mean(iters))
     achieved = mean_iters * bytes_per_iter / float(np.mean(solve_s)) / 1e9
-    traffic = ncu_traffic(args.config)
+    traffic = ncu_traffic(f"config{config}")
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         from oracle.oracle import reference_available
         if reference_available():
-            thr = os.cpu_count() or 1
-            per_chip, desc = reference_sample(args.config, thr, args.ref_iter_cap,
-                                              args.ref_action_samples)
-            cpu = {"value": thr * N / per_chip, "unit": UNIT, "cores": thr, "kind": "reference",
-                   "sample": desc}
+            v, ms, cores, desc, det = reference_run(config, 1 if config != 3 else 2, 0,
+                                                    args.ref_iter_cap, args.ref_action_samples)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": desc}
 
     # the dominant kernel of the timed step: the batched solve (one launch for
     # the K chips, 78 % of the step's GPU time in profiles/r1_launches_c2.csv);
     # the single-chip persistent solve (L2-resident) is reported beside it
     single_roof = {"kernel": "block_cg_dmma_kernel (persistent, one chip per launch)",
                    "achieved": achieved, "frac": achieved / peak,
-                   "traffic": ncu_traffic(f"{args.config}_single"),
+                   "traffic": ncu_traffic(f"config{config}_single"),
                    "algorithmic_bytes_per_launch": int(mean_iters * bytes_per_iter),
                    "iterations_per_solve": mean_iters, "solve_ms": float(np.mean(solve_s)) * 1e3,
                    "note": "block vectors L2-resident: bandwidth-equivalent figure"}
@@ -563,7 +663,9 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": float(np.mean(bstep_ms)), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE-config generators, DESIGN.md §Inputs)",
-        "config": config_dict(args.config, world, K),
+        "config": config_dict(config, world, K),
+        "solver_variant": batch_variant,
+        "spot_check": spot,
         "single_chip": {"value": single_value, "unit": UNIT, "ms_per_chip": float(np.mean(step_ms)),
                         "note": "one chip per step on the whole GPU (latency view)"},
         "e2e": {"value": e2e_value, "unit": UNIT,
@@ -582,11 +684,7 @@ def run_ours(args):
         "dataset": dataset,
         "reference_pipeline": refpipe,
     }
-    print(json.dumps(line))
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
-    return 0
+    return line
 
 
 def reference_pipeline_leg(bk, torch, ctx, reps=3):
@@ -653,6 +751,7 @@ def reference_pipeline_leg(bk, torch, ctx, reps=3):
     return out
 
 
+
 def dataset_leg(bk, torch, ctx, stream, inp, k_d, T_d, Q_d, R_d, peak):
     """(1) the GPU validation kernel (relative_residual of every
     sample, bk_residuals) over the chip's N device-resident samples, vs the HBM
@@ -711,13 +810,28 @@ def dataset_leg(bk, torch, ctx, stream, inp, k_d, T_d, Q_d, R_d, peak):
     }
 
 
-def _finish(args, world, rank, line):
-    if rank == 0:
-        print(json.dumps(line))
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
-    return 0
+
+def synthesis_cost(bk, torch, ctx, nchip, step_s, N):
+    """SURVEY §8(f1): chip inputs generated on the host (bk_synth_chip, one
+    thread) vs on the device (bk_synth_chip_device), per chip, and the config-4
+    throughput when every step also synthesises its chips on the device."""
+    cid, nx, ny, nz, s, _ = CONFIGS[4]
+    t = time.perf_counter()
+    for c in range(4):
+        bk.synth_chip(cid, nx, ny, nz, s, N, chip_id=1000 + c)
+    host = (time.perf_counter() - t) / 4
+    bk.synth_chip_device(cid, nx, ny, nz, s, N, chip_id=999, ctx=ctx)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for c in range(nchip):
+        bk.synth_chip_device(cid, nx, ny, nz, s, N, chip_id=1000 + c, ctx=ctx)
+    torch.cuda.synchronize()
+    devc = (time.perf_counter() - t) / nchip
+    return {"host_ms_per_chip": host * 1e3, "device_ms_per_chip": devc * 1e3,
+            "value_with_device_synthesis": nchip * N / (step_s + nchip * devc),
+            "value_with_host_synthesis_1_thread": nchip * N / (step_s + nchip * host)}
+
+
 
 
 def run_ours_batch(args, ctx, world, rank, local):
@@ -728,7 +842,7 @@ def run_ours_batch(args, ctx, world, rank, local):
 
     import paper_2510_23221_b200 as bk
 
-    cid, nx, ny, nz, s, N = bk.CONFIGS[4]
+    cid, nx, ny, nz, s, N = CONFIGS[4]
     dev = torch.device("cuda", local)
     nchip = C4_CHIPS_PER_STEP
     chips = [bk.synth_chip(cid, nx, ny, nz, s, N, chip_id=rank * nchip + c) for c in range(nchip)]
@@ -797,41 +911,28 @@ def run_ours_batch(args, ctx, world, rank, local):
     return _finish(args, world, rank, line)
 
 
-def synthesis_cost(bk, torch, ctx, nchip, step_s, N):
-    """SURVEY §8(f1): chip inputs generated on the host (bk_synth_chip, one
-    thread) vs on the device (bk_synth_chip_device), per chip, and the config-4
-    throughput when every step also synthesises its chips on the device."""
-    cid, nx, ny, nz, s, _ = __import__("paper_2510_23221_b200").CONFIGS[4]
-    t = time.perf_counter()
-    for c in range(4):
-        bk.synth_chip(cid, nx, ny, nz, s, N, chip_id=1000 + c)
-    host = (time.perf_counter() - t) / 4
-    bk.synth_chip_device(cid, nx, ny, nz, s, N, chip_id=999, ctx=ctx)
-    torch.cuda.synchronize()
-    t = time.perf_counter()
-    for c in range(nchip):
-        bk.synth_chip_device(cid, nx, ny, nz, s, N, chip_id=1000 + c, ctx=ctx)
-    torch.cuda.synchronize()
-    devc = (time.perf_counter() - t) / nchip
-    return {"host_ms_per_chip": host * 1e3, "device_ms_per_chip": devc * 1e3,
-            "value_with_device_synthesis": nchip * N / (step_s + nchip * devc),
-            "value_with_host_synthesis_1_thread": nchip * N / (step_s + nchip * host)}
 
 
-def run_ours_large(args, ctx, world, rank, local):
-    """Config 5: one 512x512x16 chip, s=64, N=5000. N=1: the single-GPU
-    multi-kernel solve; N>1: the chip is split into y-slabs (one per rank,
-    dd.py: NCCL Gram all-reduce + NVLink halo rows), X is all-gathered and the
-    5000 samples are split across ranks (strong scaling). (T, q) are written
-    chunk by chunk into a device ring of C5_RING samples (samples count when
-    written to HBM)."""
+def run_c5(args, ctx, world, rank, local):
+    """Config 5 (the headline): one 512x512x16 chip, s = 64, N = 5000 per step.
+
+    value: CUDA events on the library's stream around each step — assemble,
+    rhs_from_power, block CG (multi-kernel engine), then combine + operator
+    action of all 5000 samples in launches of C5_RING samples into a
+    device-resident ring (samples count when written to HBM). N > 1: the chip
+    is split into y-slabs (dd.py), X gathered, samples split (strong scaling).
+    e2e: bk_generate_stream over host (pinned) inputs, every sample drained to
+    pinned host memory through the library's output ring while the next chip
+    solves."""
     import torch
 
     import paper_2510_23221_b200 as bk
     from paper_2510_23221_b200 import dd
+    from paper_2510_23221_b200.sharding import max_over_ranks
 
-    cid, nx, ny, nz, s, N = bk.CONFIGS[5]
+    cid, nx, ny, nz, s, N = CONFIGS[5]
     dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
     inp = bk.synth_chip(cid, nx, ny, nz, s, N, chip_id=0)
     n = inp.grid.cell_count()
     k = torch.from_numpy(inp.k).to(dev)
@@ -845,14 +946,16 @@ def run_ours_large(args, ctx, world, rank, local):
     Q = torch.empty_like(T)
     R = torch.empty(C5_RING, dtype=torch.float64, device=dev)
     cfg = bk.SolverConfig(TOL_BY_CONFIG[5], 100000, "jacobi")
-    stream = torch.cuda.current_stream()
-    ctx.set_stream(stream.cuda_stream)
     parts = dd.partition_rows(ny, world)
+    ctx.set_option("phase_timing", 1)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def step():
+        e = [ev() for _ in range(4)]
+        e[0].record(stream)
         op = bk.assemble(k, inp.grid, inp.bc, ctx)
         bk.rhs_from_power(op, qb, out=B)
-        t0 = time.perf_counter()
+        e[1].record(stream)
         if world == 1:
             rep = bk.block_cg(op, B, cfg, out=X).report
         else:
@@ -864,59 +967,180 @@ def run_ours_large(args, ctx, world, rank, local):
             X.zero_()
             slab.store_x(X)
             dist.all_reduce(X)  # disjoint slabs: sum == all-gather
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
+        e[2].record(stream)
         for c in coef:
             m = int(c.shape[1])
             bk.combine_action(op, X, c, t_out=T[:m], q_out=Q[:m], resid_out=R[:m])
-        torch.cuda.synchronize()
-        return rep, t1 - t0, time.perf_counter() - t1
+        e[3].record(stream)
+        return rep, e, ctx.last_solve_phases()
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     launches0 = ctx.launch_count
-    times, solve, act, iters = [], [], [], []
+    recs = []
     with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
         for i in range(args.steps):
-            torch.cuda.synchronize()
-            if world > 1:
-                import torch.distributed as dist
-                dist.barrier()
-            t0 = time.perf_counter()
-            rep, ts, ta = step()
-            times.append(time.perf_counter() - t0)
-            solve.append(ts)
-            act.append(ta)
-            iters.append(rep.iterations)
-    from paper_2510_23221_b200.sharding import max_over_ranks
-    total = max_over_ranks(sum(times), dev)
+            recs.append(step())
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    launches = ctx.launch_count - launches0
+    step_s = [r[1][0].elapsed_time(r[1][3]) * 1e-3 for r in recs]
+    solve_s = [r[1][1].elapsed_time(r[1][2]) * 1e-3 for r in recs]
+    act_s = [r[1][2].elapsed_time(r[1][3]) * 1e-3 for r in recs]
+    iters = [r[0].iterations for r in recs]
+    conv = all(r[0].all_converged() for r in recs)
+    total = max_over_ranks(sum(step_s), dev)
     value = N * args.steps / total
-    # multi-kernel engine per iteration (large engine): 11 block
-    # vectors of 8 s bytes per cell (spmm P, W; update P, W, X, R, X', R';
-    # pupdate P, R, P') + stencil (32 B) and D^-1 twice (16 B)
-    bytes_per_iter = n * (88 * s + 48)
-    achieved = float(np.mean(iters)) * bytes_per_iter / max_over_ranks(float(np.mean(solve)), dev) / 1e9
+    max_resid = float(R.max().item())
     peak, peak_kind = peaks()
+
+    # roofline of the dominant kernel group: the block-CG solve (multi-kernel
+    # engine, ~95 % of the step), canonical algorithmic bytes per iteration
+    # n (40 + 80 s) over the device time of the solve
+    bytes_iter = n * (40 + 80 * s)
+    mi = float(np.mean(iters))
+    solve_mean = max_over_ranks(float(np.mean(solve_s)), dev)
+    achieved = mi * bytes_iter / solve_mean / 1e9
+    ph = recs[-1][2]
+    spmm = None
+    if world == 1 and ph["spmm"]["launches"]:
+        # stencil-SpMM + Gram sweep: reads P (8 s B/cell) and the stencil
+        # {diag, cx, cy, cz} (32 B/cell), writes W (8 s B/cell)
+        sb = n * (32 + 16 * s)
+        sm = ph["spmm"]["ms"] / ph["spmm"]["launches"] * 1e-3
+        spmm = {"kernel": "k_spmm_gram_tma64 (W = A P, G = P^T W)", "achieved_GBps": sb / sm / 1e9,
+                "peak_GBps": peak, "frac": sb / sm / 1e9 / peak, "ms_per_launch": sm * 1e3,
+                "algorithmic_bytes_per_launch": int(sb),
+                "traffic": ncu_traffic("config5_spmm")}
+    phases = {k: dict(v, ms_per_launch=(v["ms"] / v["launches"] if v["launches"] else None))
+              for k, v in ph.items()}
+
+    # e2e: the public streaming API with pinned host inputs; every sample of
+    # every chip goes D2H into pinned host memory inside the timed region
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        k_h = torch.from_numpy(inp.k).pin_memory()
+        q_h = torch.from_numpy(inp.q_basis).pin_memory()
+        c_h = torch.from_numpy(inp.coef).pin_memory()
+        from types import SimpleNamespace
+        chip_h = SimpleNamespace(grid=inp.grid, bc=inp.bc, k=k_h, q_basis=q_h, coef=c_h)
+        ctx.set_option("phase_timing", 0)
+        bk.generate_stream([chip_h], cfg, sink=None, ctx=ctx)  # warm-up: rings allocated
+        e2e_chips = max(2, min(args.steps, 3))
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        reps_h, tim_h = bk.generate_stream([chip_h] * e2e_chips, cfg, sink=None, ctx=ctx)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_s = e0.elapsed_time(e1) * 1e-3
+        e2e = {"value": N * e2e_chips / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int((n + n * s + s * N) * 8),
+               "d2h_bytes_per_step": int((2 * n * N + N) * 8),
+               "chips": e2e_chips, "ms_per_chip": e2e_s / e2e_chips * 1e3,
+               "pcie_GBps": (2 * n * N + N) * 8 * e2e_chips / e2e_s / 1e9,
+               "api": "bk_generate_stream (pinned host inputs; every sample drained to pinned "
+                      "host memory while the next chip solves)",
+               "converged": all(r.all_converged() for r in reps_h)}
+
+    if rank != 0:
+        return None
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle.oracle import reference_available
+        if reference_available():
+            v, ms, cores, desc, det = reference_run(5, 2, 0)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": desc,
+                   "extrapolation": det}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE-config generators, DESIGN.md §Inputs)",
-        "config": config_dict(5, world), "converged": bool(rep.all_converged()),
-        "roofline": {"bound": "hbm", "achieved": achieved * world, "peak": peak * world,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(5),
-                     "traffic_unit": "DRAM bytes per iteration (ncu), vs algorithmic_bytes_per_iter",
-                     "algorithmic_bytes_per_iter": int(bytes_per_iter),
-                     "kernel": "multi-kernel block CG (S=64) per rank",
-                     "iterations_per_solve": float(np.mean(iters)),
-                     "solve_ms": float(np.mean(solve)) * 1e3,
-                     "combine_action_ms": float(np.mean(act)) * 1e3, "peak_source": peak_kind},
-        "action": action_roofline(n, s, N // world, float(np.mean(act)), peak),
-        "timing": "per-step wall clock (synchronous C-ABI calls), max over ranks",
-        "gpu_launches": int(ctx.launch_count - launches0), "clocks": clk.summary(),
+        "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE-config generators, DESIGN.md §3)",
+        "config": config_dict(5, world),
+        "converged": conv, "iterations_per_solve": mi,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic("config5_iter"),
+                     "traffic_unit": "DRAM bytes per iteration (ncu, sum of the sweep kernels)",
+                     "kernel": "block-CG solve, multi-kernel engine (S = 64): one iteration = "
+                               "stencil-SpMM + Gram, R update + S_new, P (+ X) update",
+                     "algorithmic_bytes_per_iter": int(bytes_iter),
+                     "iterations_per_solve": mi, "solve_ms": solve_mean * 1e3,
+                     "peak_source": peak_kind,
+                     "phases_last_solve": phases},
+        "spmm": spmm,
+        "action": action_roofline(n, s, N // world, float(np.mean(act_s)), peak),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "phase_ms": {"solve": float(np.mean(solve_s)) * 1e3,
+                     "combine_action": float(np.mean(act_s)) * 1e3,
+                     "assemble_rhs": float(np.mean(step_s) - np.mean(solve_s) - np.mean(act_s)) * 1e3},
+        "max_sample_residual": max_resid,
+        "timing": "CUDA events on the library stream around each step; max over ranks",
+        "solver_variant": ctx.last_solver_variant,
     }
-    return _finish(args, world, rank, line)
+    return line
+
+
+def _finish(args, world, rank, line):
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+
+    import paper_2510_23221_b200 as bk
+
+    world, rank, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product has no CPU path)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = bk.Context(local)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+
+    if args.config == 4:
+        return run_ours_batch(args, ctx, world, rank, local)
+    if args.config == 5:
+        line = run_c5(args, ctx, world, rank, local)
+        if line is not None and not args.no_extra:
+            # the C2 batched step (configs[1]) beside the headline: its own
+            # value, roofline and the f2-f4 legs measured on C2 chips
+            ctx.set_option("phase_timing", 0)
+            c2 = run_chips(args, ctx, world, rank, local, 2, legs=True)
+            if c2 is not None:
+                line["extra_configs"] = {"C2": {k: c2.get(k) for k in (
+                    "value", "unit", "ms_per_step", "config", "solver_variant", "spot_check",
+                    "single_chip", "e2e", "roofline", "action", "cpu_baseline", "gpu_launches",
+                    "clocks", "max_sample_residual", "direct_cg_baseline", "dataset",
+                    "reference_pipeline")}}
+    else:
+        line = run_chips(args, ctx, world, rank, local, args.config)
+    if rank == 0 and line is not None:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
 
 
 def main():
@@ -925,10 +1149,13 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--chips", type=int, default=0,
                     help="concurrent chips per GPU per step (configs 1-3; 0 = default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="config 5: skip the C2 line reported under extra_configs")
+    ap.add_argument("--no-e2e", action="store_true", help="config 5: skip the e2e leg")
     ap.add_argument("--no-dataset", action="store_true",
                     help="skip the dataset sink / validation leg (SURVEY 8(f2))")
     ap.add_argument("--no-direct", action="store_true",

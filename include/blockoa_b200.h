@@ -210,6 +210,27 @@ bk_status bk_generate_batch(bk_ctx* ctx, int n_chips, const bk_grid* grids,
                             double* const* Q, double* const* resid, bk_solve_report* reports,
                             int streams, bk_phase_timings* timings);
 
+/* Streaming per-chip pipeline for jobs whose outputs do not fit in memory at
+ * once (BASELINE config 5: 335 GB of (T, q) per chip): the per-chip loop of
+ * generate_blockoa (pipeline.cpp:365-597) with the samples handed to a host
+ * sink chunk by chunk. Chips are solved one after another; each chip's samples
+ * are combined + operator-actioned in chunks of `chunk` samples (0 = ~2 GB of
+ * T + q per chunk) into a device ring, copied over PCIe into a pinned host
+ * ring, and passed to sink(user, chip, j0, m, n, T, Q, resid) — T, Q are m x n
+ * sample-major, resid m values, valid only during the call — from a library
+ * worker thread while the next chip's basis solve runs. sink may be NULL (the
+ * samples are still copied to host memory). A non-zero return from sink
+ * aborts with BK_IO_ERROR. Inputs are host or device pointers (per-chip
+ * arrays as in bk_generate_batch). reports: n_chips entries or NULL. */
+typedef int (*bk_sample_sink)(void* user, int chip, int64_t j0, int64_t m, int64_t n,
+                              const double* T, const double* Q, const double* resid);
+bk_status bk_generate_stream(bk_ctx* ctx, int n_chips, const bk_grid* grids,
+                             const double* const* k, const bk_face* bc /* n_chips x 6 */,
+                             const double* const* Qbasis, int s, const double* const* C,
+                             int64_t N, const bk_solver_cfg* cfg, int64_t chunk,
+                             bk_sample_sink sink, void* user, bk_solve_report* reports,
+                             bk_phase_timings* timings);
+
 /* Cap the number of CTAs (and thus SMs) one block-CG solve may use on ctx
  * (0 = all SMs). */
 bk_status bk_set_cg_sm_budget(bk_ctx* ctx, int max_ctas);
@@ -225,6 +246,11 @@ bk_status bk_set_option(bk_ctx* ctx, const char* name, int value);
  * "block_cg_dmma_kernel<16,0,1,1> ring chips=16" (template arguments S,
  * resident, multi-chip, deferred X update) or "block_cg_large<64> tma". */
 const char* bk_last_solver_variant(const bk_ctx* ctx);
+/* With option "phase_timing" = 1: device time (ms, CUDA events) and launch
+ * count per sweep kind of the last multi-kernel block-CG solve on ctx, 4
+ * entries: [0] stencil-SpMM + Gram (W = A P, P^T W), [1] R update + S_new,
+ * [2] P update (+ the deferred X update), [3] reserved. */
+bk_status bk_last_solve_phases(const bk_ctx* ctx, double* ms, int64_t* counts);
 
 /* ---- y-slab domain decomposition (BASELINE config 5 across GPUs) -----------
  * A rank owns global rows [y0, y0 + nyl) of the grid of `op` (the GLOBAL

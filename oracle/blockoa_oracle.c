@@ -777,3 +777,169 @@ double orc_cg_error_bound(double kappa, int m, double e0, int* status) {
     const double rk = sqrt(kappa);
     return 2.0 * pow((rk - 1.0) / (rk + 1.0), m) * e0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Seeded BASELINE-config inputs (DESIGN.md §3 pins)       */
+/* ------------------------------------------------------------------------- */
+/* Test infrastructure, like everything in this file: the reference arm of
+ * bench.py and the CPU tests draw the chips' inputs here so the checker side
+ * never loads the product library. The pins are the ones DESIGN.md §3 states
+ * (the reference has no generator for the BASELINE configs); every draw goes
+ * through the Rng restatement above (rng.hpp:14-63), in this order per chip
+ * seed derive_seed(master, "chip", chip_id):
+ *   configs 1/2: "k" stream, one U[10,150] per 16x16-cell tile, tile-row-major;
+ *   configs 3/5: "layers" stream, bulk k ~ U[1,3]; "lognormal" stream, one
+ *                normal per cell (flat order) for k *= exp(ln(1.2) Z);
+ *   config 4:    "layers" stream, dz_l ~ U[50,500] um for every layer, then
+ *                k_l ~ U[1,400] for every layer, then h_top, h_bot ~ U[1e2,1e4];
+ *   per basis map t, stream ("basis", t): for each blob cx ~ U[0,nx),
+ *                cy ~ U[0,ny), sigma ~ U[2,8] * scale, amp ~ U[0,1e6]; for each
+ *                rectangle x0 = below(nx), y0 = below(ny), w, h = wmin +
+ *                below(wmax - wmin + 1), power ~ U[0,2e6];
+ *   stream ("coef", 0): C[t][j] ~ U[0,1) row-major.
+ * tests/test_oracle.py pins this function bitwise against the product's host
+ * generator (bk_synth_chip) for every config. */
+typedef struct {
+    int nx, ny, nz;
+    double lx, ly, lz;
+    int has_dz;
+    int bc_kind[6]; /* 0 Dirichlet, 1 Robin, 2 adiabatic */
+    double bc_a[6], bc_b[6];
+} orc_chip_meta;
+
+static double urand(orc_rng* r, double lo, double hi) { return lo + rng_u01(r) * (hi - lo); }
+
+int orc_synth_chip(int config, int nx, int ny, int nz, int s, int64_t N, uint64_t master_seed,
+                   uint64_t chip_id, orc_chip_meta* meta, double* dz, double* k, double* Q,
+                   double* C) {
+    if (nx < 1 || ny < 1 || nz < 1 || s < 1 || N < 0) return ORC_INVALID_SPEC;
+    const int64_t plane = (int64_t)nx * ny, n = plane * nz;
+    const uint64_t chip = orc_derive_seed(master_seed, "chip", chip_id);
+    memset(meta, 0, sizeof(*meta));
+    meta->nx = nx;
+    meta->ny = ny;
+    meta->nz = nz;
+    meta->lx = 10e-3;
+    meta->ly = 10e-3;
+    for (int f = 0; f < 6; ++f) meta->bc_kind[f] = 2;
+    int nblobs = 0, nrects = 0, z0 = 0, z1 = nz, cpl = 1, tile = 16, tx = 1;
+    double scale = 1.0, kl[16] = {0};
+    orc_rng r;
+    if (config == 1 || config == 2) {
+        meta->lz = 0.15e-3 * nz;
+        meta->bc_kind[5] = 1;
+        meta->bc_a[5] = 1e3;
+        tx = (nx + tile - 1) / tile;
+        const int ty = (ny + tile - 1) / tile;
+        double* tk = (double*)malloc(sizeof(double) * (size_t)tx * ty);
+        if (!tk) return ORC_OOM;
+        rng_init(&r, orc_derive_seed(chip, "k", 0));
+        for (int i = 0; i < tx * ty; ++i) tk[i] = urand(&r, 10.0, 150.0);
+        if (k)
+            for (int64_t i = 0; i < n; ++i) {
+                const int ix = (int)(i % nx), iy = (int)((i / nx) % ny);
+                k[i] = tk[(iy / tile) * tx + ix / tile];
+            }
+        free(tk);
+        nblobs = config == 1 ? 3 : 5;
+    } else if (config == 3 || config == 5) {
+        if (nz % 8) return ORC_INVALID_SPEC;
+        cpl = nz / 8;
+        meta->lz = 0.8e-3;
+        meta->bc_kind[4] = 1;
+        meta->bc_a[4] = 1e2;
+        meta->bc_kind[5] = 1;
+        meta->bc_a[5] = 1e4;
+        rng_init(&r, orc_derive_seed(chip, "layers", 0));
+        const double stack[8] = {urand(&r, 1.0, 3.0), 150.0, 5.0, 150.0, 5.0, 150.0, 5.0, 400.0};
+        if (k) {
+            const double ls = log(1.2);
+            rng_init(&r, orc_derive_seed(chip, "lognormal", 0));
+            for (int64_t i = 0; i < n; ++i) {
+                const double z = rng_normal(&r);
+                k[i] = stack[(i / plane) / cpl] * exp(ls * z);
+            }
+        }
+        z0 = cpl;
+        z1 = 2 * cpl;
+        nblobs = 3;
+        nrects = 4;
+        scale = nx / 128.0;
+    } else if (config == 4) {
+        if (nz > 16) return ORC_INVALID_SPEC;
+        rng_init(&r, orc_derive_seed(chip, "layers", 0));
+        double lz = 0.0;
+        for (int l = 0; l < nz; ++l) {
+            dz[l] = urand(&r, 50e-6, 500e-6);
+            lz += dz[l];
+        }
+        for (int l = 0; l < nz; ++l) kl[l] = urand(&r, 1.0, 400.0);
+        const double h_top = urand(&r, 1e2, 1e4), h_bot = urand(&r, 1e2, 1e4);
+        meta->lz = lz;
+        meta->has_dz = 1;
+        meta->bc_kind[4] = 1;
+        meta->bc_a[4] = h_bot;
+        meta->bc_kind[5] = 1;
+        meta->bc_a[5] = h_top;
+        if (k)
+            for (int64_t i = 0; i < n; ++i) k[i] = kl[i / plane];
+        z0 = nz > 1 ? 1 : 0;
+        z1 = z0 + 1;
+        nblobs = 5;
+        scale = nx / 128.0;
+    } else {
+        return ORC_INVALID_CONFIG;
+    }
+    if (Q) {
+        memset(Q, 0, sizeof(double) * (size_t)n * s);
+        double* pl = (double*)malloc(sizeof(double) * (size_t)plane);
+        if (!pl) return ORC_OOM;
+        int wmin = (int)(4 * scale);
+        if (wmin < 1) wmin = 1;
+        int wmax = (int)(32 * scale);
+        if (wmax < wmin) wmax = wmin;
+        for (int t = 0; t < s; ++t) {
+            rng_init(&r, orc_derive_seed(chip, "basis", (uint64_t)t));
+            for (int64_t c = 0; c < plane; ++c) pl[c] = 0.0;
+            /* blobs: parameters first, then the plane sum in blob order */
+            double bp[8][4];
+            for (int b = 0; b < nblobs; ++b) {
+                bp[b][0] = urand(&r, 0.0, nx);
+                bp[b][1] = urand(&r, 0.0, ny);
+                const double sig = urand(&r, 2.0, 8.0) * scale;
+                bp[b][3] = urand(&r, 0.0, 1e6);
+                bp[b][2] = 1.0 / (2.0 * sig * sig);
+            }
+            double rp[8][5];
+            for (int q = 0; q < nrects; ++q) {
+                rp[q][0] = (double)rng_below(&r, (uint64_t)nx);
+                rp[q][1] = (double)rng_below(&r, (uint64_t)ny);
+                rp[q][2] = wmin + (double)rng_below(&r, (uint64_t)(wmax - wmin + 1));
+                rp[q][3] = wmin + (double)rng_below(&r, (uint64_t)(wmax - wmin + 1));
+                rp[q][4] = urand(&r, 0.0, 2e6);
+            }
+            for (int b = 0; b < nblobs; ++b)
+                for (int iy = 0; iy < ny; ++iy) {
+                    const double dy = iy + 0.5 - bp[b][1];
+                    for (int ix = 0; ix < nx; ++ix) {
+                        const double dx = ix + 0.5 - bp[b][0];
+                        pl[(int64_t)iy * nx + ix] += bp[b][3] * exp(-(dx * dx + dy * dy) * bp[b][2]);
+                    }
+                }
+            for (int q = 0; q < nrects; ++q) {
+                const int x0 = (int)rp[q][0], y0 = (int)rp[q][1];
+                const int w = (int)rp[q][2], h = (int)rp[q][3];
+                for (int iy = y0; iy < ny && iy < y0 + h; ++iy)
+                    for (int ix = x0; ix < nx && ix < x0 + w; ++ix) pl[(int64_t)iy * nx + ix] += rp[q][4];
+            }
+            for (int iz = z0; iz < z1; ++iz)
+                for (int64_t c = 0; c < plane; ++c) Q[(iz * plane + c) * s + t] = pl[c];
+        }
+        free(pl);
+    }
+    if (C) {
+        rng_init(&r, orc_derive_seed(chip, "coef", 0));
+        for (int64_t i = 0; i < (int64_t)s * N; ++i) C[i] = rng_u01(&r);
+    }
+    return ORC_OK;
+}

@@ -19,6 +19,8 @@ import os
 import subprocess
 import threading
 
+from dataclasses import dataclass
+
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -249,6 +251,45 @@ class Oracle(_Base):
         self.lib.orc_rng_below(C.c_uint64(seed), C.c_uint64(bound), C.c_int64(n), _ptr(out))
         return out
 
+    def synth_chip(self, config, nx, ny, nz, s, N, master_seed=1, chip_id=0, fields=True):
+        """Seeded BASELINE-config inputs (orc_synth_chip; DESIGN.md §3 pins),
+        bitwise the product's host generator (tests/test_oracle.py). Returns a
+        ChipCase: grid tuple (nx, ny, nz, lx, ly, lz), dz (or None), bc as
+        (kind, a, b) tuples, k [n], q_basis [n, s], coef [s, N]. fields=False
+        skips k and q_basis (coefficients and metadata only)."""
+        meta = _ChipMeta()
+        n = nx * ny * nz
+        dz = np.zeros(max(nz, 1), np.float64)
+        k = np.empty(n, np.float64) if fields else None
+        q = np.empty((n, s), np.float64) if fields else None
+        c = np.empty((s, N), np.float64)
+        st = self.lib.orc_synth_chip(C.c_int(config), C.c_int(nx), C.c_int(ny), C.c_int(nz),
+                                     C.c_int(s), C.c_int64(N), C.c_uint64(master_seed),
+                                     C.c_uint64(chip_id), C.byref(meta), _ptr(dz), _ptr(k),
+                                     _ptr(q), _ptr(c))
+        if st:
+            raise CheckerError(st, "orc_synth_chip")
+        bc = tuple((int(meta.bc_kind[f]), float(meta.bc_a[f]), float(meta.bc_b[f]))
+                   for f in range(6))
+        return ChipCase((meta.nx, meta.ny, meta.nz, meta.lx, meta.ly, meta.lz),
+                        dz.copy() if meta.has_dz else None, bc, k, q, c)
+
+
+class _ChipMeta(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("lx", C.c_double),
+                ("ly", C.c_double), ("lz", C.c_double), ("has_dz", C.c_int),
+                ("bc_kind", C.c_int * 6), ("bc_a", C.c_double * 6), ("bc_b", C.c_double * 6)]
+
+
+@dataclass
+class ChipCase:
+    grid: tuple
+    dz: object
+    bc: tuple
+    k: object
+    q_basis: object
+    coef: object
+
 
 class Reference(_Base):
     """The unmodified reference core via oracle/ref_shim.cpp."""
@@ -356,6 +397,17 @@ class Reference(_Base):
             self._err(st, "combine_action")
         return T, Q, R
 
+    def basis(self, op, X):
+        """A one-group BasisSet holding op and the solved basis X (the state
+        generate_blockoa has after generate_basis), for timed per-sample
+        combine + operator action calls (RefBasis.combine_action)."""
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        self.lib.ref_basis_create.restype = C.c_void_p
+        h = self.lib.ref_basis_create(op.handle, _ptr(X), C.c_int(X.shape[1]))
+        if not h:
+            self._err(21, "basis_create")
+        return RefBasis(self.lib, C.c_void_p(h), op.n)
+
     def derive_seed(self, seed, tag, index=0):
         return int(self.lib.ref_derive_seed(C.c_uint64(seed), tag.encode(), C.c_uint64(index)))
 
@@ -420,7 +472,7 @@ class Reference(_Base):
         r = np.empty(n_data, np.float64)
         fp = np.empty(n_data, np.int64)
         it = np.zeros(1, np.int32)
-        sec = np.zeros(2, np.float64)
+        sec = np.zeros(4, np.float64)
         st = self.lib.ref_generate_blockoa(
             C.c_int(nx), C.c_int(ny), C.c_int(nz), C.c_longlong(n_data), C.c_int(n_basis),
             C.c_int(n_k), C.c_ulonglong(seed), C.c_int(nkind), C.c_double(lo), C.c_double(hi),
@@ -429,7 +481,8 @@ class Reference(_Base):
         if st:
             self._err(st, "generate_blockoa")
         return dict(k=k, u=u, q=q, residual=r, floorplan_id=fp, iterations=int(it[0]),
-                    basis_s=float(sec[0]), total_s=float(sec[1]))
+                    basis_s=float(sec[0]), total_s=float(sec[1]), combine_s=float(sec[2]),
+                    action_s=float(sec[3]))
 
     def write_dataset(self, dir, grid, bc, k, q, u, ids, method="blockoa", master_seed=0,
                       tol_claimed=1e-12, tool_version="blockoa-0.1.0", digests=(),
@@ -479,3 +532,35 @@ class Reference(_Base):
                                                C.c_longlong(cap), C.byref(n), C.byref(p),
                                                C.byref(f), C.byref(mx)))
         return st, p.value, f.value, mx.value, res[:n.value].copy()
+
+
+class RefBasis:
+    """Handle of a reference BasisSet (oracle/ref_shim.cpp ref_basis_*)."""
+
+    def __init__(self, lib, handle, n):
+        self.lib, self.handle, self.n = lib, handle, n
+
+    def __del__(self):
+        try:
+            self.lib.ref_basis_free(self.handle)
+        except Exception:
+            pass
+
+    def combine_action(self, Cm, j0=0, j1=None, threads=1, outputs=True):
+        """combine_from_weights + operator_action + relative_residual
+        (pipeline.cpp:187-251, discretize.cpp:275-286) for samples [j0, j1) of
+        Cm (s x N), parallel_for over `threads` workers as generate_blockoa
+        does (pipeline.cpp:410, 511)."""
+        Cm = np.ascontiguousarray(Cm, dtype=np.float64)
+        N = Cm.shape[1]
+        j1 = N if j1 is None else j1
+        m = j1 - j0
+        T = np.empty((m, self.n), np.float64) if outputs else None
+        Q = np.empty((m, self.n), np.float64) if outputs else None
+        R = np.empty(m, np.float64)
+        st = self.lib.ref_basis_combine_action(self.handle, _ptr(Cm), C.c_longlong(N),
+                                               C.c_longlong(j0), C.c_longlong(j1), _ptr(T),
+                                               _ptr(Q), _ptr(R), C.c_int(threads))
+        if st:
+            raise CheckerError(st, "ref_basis_combine_action")
+        return T, Q, R

@@ -343,6 +343,52 @@ int ref_combine_action(const void* vop, const double* x, int s, const double* c,
     }
 }
 
+// The same per-sample path with the basis group built once (the state
+// generate_blockoa holds after generate_basis, pipeline.cpp:92-134), so a timed
+// call measures only combine_from_weights + operator_action +
+// relative_residual for samples [j0, j1) of C (row-major s x n_samples).
+void* ref_basis_create(const void* vop, const double* x, int s) {
+    try {
+        const auto* op = static_cast<const DiscreteOperator*>(vop);
+        auto* basis = new BasisSet;
+        basis->groups.resize(1);
+        BasisGroup& grp = basis->groups[0];
+        grp.op = *op;
+        grp.x.n = op->A.n;
+        grp.x.s = s;
+        grp.x.data.assign(x, x + static_cast<std::size_t>(op->A.n) * s);
+        return basis;
+    } catch (...) {
+        map_exception();
+        return nullptr;
+    }
+}
+
+void ref_basis_free(void* b) { delete static_cast<BasisSet*>(b); }
+
+int ref_basis_combine_action(const void* vb, const double* c, long long n_samples, long long j0,
+                             long long j1, double* t_out, double* q_out, double* resid,
+                             int threads) {
+    try {
+        const auto* basis = static_cast<const BasisSet*>(vb);
+        const BasisGroup& grp = basis->groups[0];
+        const int s = grp.x.s;
+        const std::int64_t n = grp.x.n;
+        parallel_for(j0, j1, threads, [&](std::int64_t j) {
+            std::vector<double> w(static_cast<std::size_t>(s));
+            for (int t = 0; t < s; ++t) w[t] = c[static_cast<std::size_t>(t) * n_samples + j];
+            std::vector<double> tj = combine_from_weights(*basis, w);
+            ScalarField qj = operator_action(*basis, 0, tj);
+            if (t_out) std::memcpy(t_out + (j - j0) * n, tj.data(), n * sizeof(double));
+            if (q_out) std::memcpy(q_out + (j - j0) * n, qj.values.data(), n * sizeof(double));
+            if (resid) resid[j - j0] = relative_residual(grp.op, tj, qj);
+        });
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 // ---- RNG (rng.hpp) ------------------------------------------------------------
 unsigned long long ref_derive_seed(unsigned long long seed, const char* tag,
                                    unsigned long long index) {
@@ -518,7 +564,8 @@ int ref_draw_weights(int n_basis, unsigned long long seed, long long n_data, dou
 // generate_blockoa on ChipSpec::default_chip() (pipeline.cpp:365-597).
 // noise_kind: 0 none, 1 uniform [lo, hi), 2 gaussian sigma. Outputs: k of each
 // group [n_k][n], per sample u/q [n_data][n], residual, floorplan id; basis
-// iterations per group; wall seconds of the basis solve and of the whole call.
+// iterations per group; wall seconds (PhaseTimings, dataset.hpp:17-25) of the
+// basis solve, the whole call, the combination and the operator action.
 int ref_generate_blockoa(int nx, int ny, int nz, long long n_data, int n_basis, int n_k,
                          unsigned long long seed, int noise_kind, double lo, double hi,
                          double sigma, double tol, int max_iter, int threads,
@@ -557,6 +604,8 @@ int ref_generate_blockoa(int nx, int ny, int nz, long long n_data, int n_basis, 
         if (seconds) {
             seconds[0] = r.timings.basis_solve_s;
             seconds[1] = r.timings.total_s;
+            seconds[2] = r.timings.combine_s;
+            seconds[3] = r.timings.operator_action_s;
         }
         return 0;
     } catch (...) {

@@ -171,6 +171,7 @@ def _load():
         lib.bk_set_option.argtypes = [vp, C.c_char_p, C.c_int]
         lib.bk_last_solver_variant.argtypes = [vp]
         lib.bk_last_solver_variant.restype = C.c_char_p
+        lib.bk_last_solve_phases.argtypes = [vp, vp, vp]
         lib.bk_assemble.argtypes = [vp, C.POINTER(_Grid), dp, C.POINTER(_Face), C.POINTER(vp)]
         lib.bk_operator_free.argtypes = [vp]
         lib.bk_operator_free.restype = None
@@ -190,6 +191,9 @@ def _load():
                                           C.POINTER(_Cfg), vp, vp, vp, vp, C.c_int,
                                           C.POINTER(_Timings)]
         lib.bk_set_cg_sm_budget.argtypes = [vp, C.c_int]
+        lib.bk_generate_stream.argtypes = [vp, C.c_int, vp, vp, vp, vp, C.c_int, vp, C.c_int64,
+                                           C.POINTER(_Cfg), C.c_int64, vp, vp, vp,
+                                           C.POINTER(_Timings)]
         lib.bk_dd_sizes.argtypes = [vp, vp, C.c_int, C.c_int, vp, vp, vp, vp, vp]
         lib.bk_dd_step.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.c_int,
                                    vp, vp, vp]
@@ -439,10 +443,20 @@ class Context:
         """Kernel instantiation of the last block-CG solve on this context."""
         return _load().bk_last_solver_variant(self.h).decode()
 
+    def last_solve_phases(self) -> dict:
+        """Per-sweep-kind device ms and launch counts of the last multi-kernel
+        solve (needs option phase_timing = 1)."""
+        ms = np.zeros(4, np.float64)
+        cnt = np.zeros(4, np.int64)
+        _raise(_load().bk_last_solve_phases(self.h, ms.ctypes.data_as(C.c_void_p),
+                                            cnt.ctypes.data_as(C.c_void_p)), self.h, "phases")
+        names = ("spmm", "update", "pupdate", "other")
+        return {nm: {"ms": float(ms[i]), "launches": int(cnt[i])} for i, nm in enumerate(names)}
+
     def set_option(self, name: str, value: int) -> None:
         """Per-context kernel-variant switch (bk_set_option): "ring" (-1 auto,
         0, 1), "no_resident", "force_large", "cg_profile", "no_tma_spmm",
-        "comb_profile", "batch_trace"."""
+        "comb_profile", "batch_trace", "phase_timing"."""
         _raise(_load().bk_set_option(self.h, name.encode(), int(value)), self.h, "set_option")
 
     @contextlib.contextmanager
@@ -740,6 +754,86 @@ def generate_batch(chips, cfg: SolverConfig, t_out=None, q_out=None, resid_out=N
     timings = PhaseTimings(tim.assemble_s, tim.basis_solve_s, tim.combine_action_s, tim.h2d_s,
                            tim.d2h_s, tim.total_s, tim.iterations_total, tim.matvecs_total)
     return t_out, q_out, resid_out, reports, timings
+
+
+_SINK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                    C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double))
+
+
+def generate_stream(chips, cfg: SolverConfig, sink=None, chunk: int = 0,
+                    ctx: Optional[Context] = None, check_converged: bool = True):
+    """Streaming per-chip pipeline (bk_generate_stream) for jobs whose outputs
+    do not fit in memory: chips solved one after another, each chip's samples
+    combined in chunks, copied to pinned host memory and handed to
+    sink(chip, j0, T, Q, resid) (numpy views of m x n / m values, valid only
+    during the call; return True to abort) from a library thread while the
+    next chip solves. sink=None still copies every sample to host memory.
+    Returns ([SolveReport], PhaseTimings)."""
+    ctx = _ctx(ctx)
+    n = len(chips)
+    if n == 0:
+        return [], None
+    s = _cols(chips[0].q_basis)
+    N = int(chips[0].coef.shape[1])
+    grids = (_Grid * n)()
+    faces = (_Face * (6 * n))()
+    keep = []
+    for c, ch in enumerate(chips):
+        g, kd = ch.grid._c()
+        keep.append(kd)
+        grids[c] = g
+        fc = ch.bc._c()
+        for f in range(6):
+            faces[6 * c + f] = fc[f]
+        if _cols(ch.q_basis) != s or int(ch.coef.shape[1]) != N:
+            raise DimensionMismatchError("generate_stream: chips must share s and N")
+
+    def ptr_array(arrs):
+        out = (C.c_void_p * n)()
+        for i, a in enumerate(arrs):
+            p, kk = _ptr(a)
+            keep.append(kk)
+            out[i] = p.value if p is not None else None
+        return out
+
+    kp = ptr_array([ch.k for ch in chips])
+    qp = ptr_array([ch.q_basis for ch in chips])
+    cp = ptr_array([ch.coef for ch in chips])
+    res = [np.zeros(s) for _ in chips]
+    conv = [np.zeros(s, np.int8) for _ in chips]
+    reps = (_Report * n)()
+    for c in range(n):
+        reps[c] = _Report(0, 0, 0.0, res[c].ctypes.data_as(C.c_void_p),
+                          conv[c].ctypes.data_as(C.c_void_p))
+    errors = []
+
+    def _cb(user, chip, j0, m, ncell, T, Q, R):
+        try:
+            tv = np.ctypeslib.as_array(T, shape=(int(m), int(ncell)))
+            qv = np.ctypeslib.as_array(Q, shape=(int(m), int(ncell)))
+            rv = np.ctypeslib.as_array(R, shape=(int(m),))
+            return 1 if sink(int(chip), int(j0), tv, qv, rv) else 0
+        except Exception as e:  # surfaced after the call
+            errors.append(e)
+            return 1
+
+    cb = _SINK(_cb) if sink is not None else C.cast(None, _SINK)
+    cfg_c = cfg._c()
+    tim = _Timings()
+    st = _load().bk_generate_stream(ctx.h, n, C.cast(grids, C.c_void_p), C.cast(kp, C.c_void_p),
+                                    C.cast(faces, C.c_void_p), C.cast(qp, C.c_void_p), s,
+                                    C.cast(cp, C.c_void_p), N, C.byref(cfg_c), int(chunk),
+                                    C.cast(cb, C.c_void_p), None, C.cast(reps, C.c_void_p),
+                                    C.byref(tim))
+    if errors:
+        raise errors[0]
+    if st == 7 and not check_converged:
+        st = 0
+    _raise(st, ctx.h, "generate_stream")
+    reports = [_report(s, reps[c], res[c], conv[c]) for c in range(n)]
+    timings = PhaseTimings(tim.assemble_s, tim.basis_solve_s, tim.combine_action_s, tim.h2d_s,
+                           tim.d2h_s, tim.total_s, tim.iterations_total, tim.matvecs_total)
+    return reports, timings
 
 
 def set_cg_sm_budget(ctx: Context, max_ctas: int) -> None:

@@ -141,6 +141,11 @@ bk_status drain(bk_ctx* ctx, const Staged& s, double* host, size_t count) {
 
 int kernel_width(int s) { return s <= 8 ? 8 : s <= 16 ? 16 : s <= 32 ? 32 : 64; }
 
+}  // namespace
+
+// shared with bk_stream.cu
+namespace bk {
+
 bk_status validate_grid(bk_ctx* ctx, const bk_grid* g) {
     if (!g) return fail(ctx, BK_INVALID_SPEC, "grid: null");
     if (g->nx < 1 || g->ny < 1 || g->nz < 1)
@@ -252,6 +257,10 @@ void fill_report(const CgReport& r, int s, double wall, bk_solve_report* out) {
         if (out->converged) out->converged[j] = r.converged[j];
     }
 }
+
+}  // namespace bk
+
+namespace {
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.f;
@@ -764,6 +773,15 @@ bk_status bk_create(int device, bk_ctx** out) {
     return BK_OK;
 }
 
+bk_status bk_last_solve_phases(const bk_ctx* ctx, double* ms, int64_t* counts) {
+    if (!ctx || !ms || !counts) return BK_INVALID_CONFIG;
+    for (int k = 0; k < bk_phase_clock::kKinds; ++k) {
+        ms[k] = ctx->pclk.ms[k];
+        counts[k] = ctx->pclk.count[k];
+    }
+    return BK_OK;
+}
+
 const char* bk_last_solver_variant(const bk_ctx* ctx) {
     return ctx ? ctx->last_variant.c_str() : "";
 }
@@ -778,6 +796,7 @@ bk_status bk_set_option(bk_ctx* ctx, const char* name, int value) {
     else if (k == "no_tma_spmm") ctx->knobs.no_tma_spmm = value != 0;
     else if (k == "comb_profile") ctx->knobs.comb_profile = value != 0;
     else if (k == "batch_trace") ctx->knobs.batch_trace = value != 0;
+    else if (k == "phase_timing") ctx->knobs.phase_timing = value != 0;
     else return fail(ctx, BK_INVALID_CONFIG, "bk_set_option: unknown option " + k);
     return BK_OK;
 }
@@ -786,6 +805,13 @@ void bk_destroy(bk_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->out_ctx) bk_destroy(ctx->out_ctx);
+    for (cudaEvent_t e : ctx->pclk.ev) cudaEventDestroy(e);
+    for (bk_operator* o : ctx->stream_ops)
+        if (o) {
+            free_op_buffers(o);
+            delete o;
+        }
     for (int i = 0; i < bk_ctx::kSlots; ++i) cudaFree(ctx->ws[i]);
     for (auto& e : ctx->ev) cudaEventDestroy(e);
     for (auto& e : ctx->chunk_ev) cudaEventDestroy(e);

@@ -1234,6 +1234,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
         BK_CUDA_TRY(ctx, set((const void*)k_ctl_update<S>, cs));
         BK_CUDA_TRY(ctx, set((const void*)k_ctl_verify<S>, cs));
     }
+    phase_reset(ctx);
     k_anchor<S, kInit><<<nb, LBS, swa, s>>>(a);
     ++ctx->launches;
     reduce(E, nb);
@@ -1248,12 +1249,16 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     a.coef2 = ctl->akeep;
     for (int m = 1; m <= cfg->max_iter && sa > 0; ++m) {
         halo(a.P);
+        phase_mark(ctx, -1);
         BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s, ctx->knobs.no_tma_spmm));
+        phase_mark(ctx, 0);
         ++ctx->launches;
         reduce(S * S, nb);
         k_ctl_alpha<S><<<1, CBS, cs, s>>>(ctl, red);
         ++ctx->launches;
+        phase_mark(ctx, -1);
         BK_CUDA_TRY(ctx, (launch_update<S, true>(a, nb, s)));
+        phase_mark(ctx, 1);
         ++ctx->launches;
         reduce(E, nb);
         k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, red, m);
@@ -1280,10 +1285,12 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
                 continue;
             }
         }
+        phase_mark(ctx, -1);
         if (x_done)
             BK_CUDA_TRY(ctx, (launch_pupdate<S, 0>(a, nb, s)));
         else
             BK_CUDA_TRY(ctx, (launch_pupdate<S, 1>(a, nb, s)));
+        phase_mark(ctx, 2);
         ++ctx->launches;
     }
     // honest residuals for still-active columns
@@ -1295,6 +1302,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     k_ctl_final<S><<<1, 32, 0, s>>>(ctl, red, drep);
     ++ctx->launches;
     BK_CUDA_TRY(ctx, cudaGetLastError());
+    phase_collect(ctx);
     return read_small(ctx, rep, drep, sizeof(CgReport));
 }
 

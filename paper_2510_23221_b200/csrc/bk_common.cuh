@@ -34,10 +34,25 @@ struct bk_knobs {
     bool no_tma_spmm = false;  // S = 64 phase 1 without TMA
     bool comb_profile = false; // combine/action stage timestamps (stderr)
     bool batch_trace = false;
+    bool phase_timing = false; // per-kernel-kind event timing of the multi-kernel solve
+};
+
+// Optional per-kernel-kind timing of the multi-kernel solve (option
+// "phase_timing"): event pairs around each sweep launch, summed per kind at the
+// end of the solve (bk_last_solve_phases). Kinds: 0 stencil-SpMM + Gram,
+// 1 R update + S_new, 2 P (+ X) update, 3 other (anchor / verify / restart).
+struct bk_phase_clock {
+    static constexpr int kKinds = 4;
+    std::vector<cudaEvent_t> ev;  // pool, grow-only
+    std::vector<int> kind;        // per recorded pair
+    size_t used = 0;
+    double ms[kKinds] = {};
+    int64_t count[kKinds] = {};
 };
 
 struct bk_ctx {
     bk_knobs knobs;
+    bk_phase_clock pclk;
     std::string last_variant;  // kernel instantiation of the last block-CG solve
     int device = 0;
     int num_sms = 0;
@@ -58,8 +73,10 @@ struct bk_ctx {
     void* pin[2] = {};                     // pinned staging of the dataset writer / validator
     size_t pin_bytes = 0;
     cudaEvent_t stage_ev[4] = {};
+    bk_ctx* out_ctx = nullptr;            // output worker of bk_generate_stream (own streams)
+    bk_operator* stream_ops[2] = {};       // per-parity chip operators of bk_generate_stream
     // grow-only device workspace slots
-    static constexpr int kSlots = 40;
+    static constexpr int kSlots = 48;
     void* ws[kSlots] = {};
     size_t ws_bytes[kSlots] = {};
 };
@@ -125,9 +142,46 @@ enum Slot : int {
     kSlotBoaU,      //   staged outputs
     kSlotBoaQ,
     kSlotBoaRes,
+    kSlotStrX0,     // bk_generate_stream: per-parity basis X and coefficients C
+    kSlotStrX1,
+    kSlotStrC0,
+    kSlotStrC1,
 };
 
 bk_status fail(bk_ctx* ctx, bk_status st, const std::string& msg);
+
+// phase clock (no-ops unless ctx->knobs.phase_timing)
+inline void phase_reset(bk_ctx* ctx) {
+    ctx->pclk.used = 0;
+    ctx->pclk.kind.clear();
+    for (int k = 0; k < bk_phase_clock::kKinds; ++k) {
+        ctx->pclk.ms[k] = 0.0;
+        ctx->pclk.count[k] = 0;
+    }
+}
+inline void phase_mark(bk_ctx* ctx, int kind_or_start) {  // -1: start of a pair
+    if (!ctx->knobs.phase_timing) return;
+    auto& c = ctx->pclk;
+    if (c.used == c.ev.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        c.ev.push_back(e);
+    }
+    cudaEventRecord(c.ev[c.used++], ctx->stream);
+    if (kind_or_start >= 0) c.kind.push_back(kind_or_start);
+}
+inline void phase_collect(bk_ctx* ctx) {
+    if (!ctx->knobs.phase_timing) return;
+    auto& c = ctx->pclk;
+    if (c.used == 0) return;
+    cudaEventSynchronize(c.ev[c.used - 1]);
+    for (size_t p = 0; p < c.kind.size() && 2 * p + 1 < c.used; ++p) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c.ev[2 * p], c.ev[2 * p + 1]);
+        c.ms[c.kind[p]] += ms;
+        c.count[c.kind[p]] += 1;
+    }
+}
 // relative_residual for N samples (U, Q: N x n device); resid device, N values
 bk_status residuals_device(bk_ctx* ctx, const bk_operator* op, const double* U, const double* Q,
                            int64_t N, double* resid);

@@ -290,3 +290,23 @@ def test_reference_block_cg_breaks_down_with_shared_lift(reference, bk):
     B0 = np.stack([reference.rhs_from_power(op0, inp.q_basis[:, t]) for t in range(16)], axis=1)
     X0, rep0 = reference.block_cg(op0, B0, TOL, 400, 1)
     assert rep0["converged"].all()
+
+
+@pytest.mark.parametrize("case", [(1, 64, 64, 1, 8, 256), (2, 48, 40, 1, 16, 12),
+                                  (3, 24, 20, 8, 32, 7), (4, 32, 24, 4, 16, 8),
+                                  (5, 32, 16, 16, 64, 5), (2, 256, 256, 1, 16, 2048)])
+def test_oracle_synth_bitwise_product_synth(oracle, bk, case):
+    """The checker-side input generator (orc_synth_chip, used by bench.py's
+    reference arm so it never loads the product) draws bitwise the same chip as
+    the product's host generator bk_synth_chip, for every BASELINE config."""
+    for chip_id in (0, 7):
+        o = oracle.synth_chip(*case, chip_id=chip_id)
+        p = bk.synth_chip(*case, chip_id=chip_id)
+        g = p.grid
+        assert o.grid == (g.nx, g.ny, g.nz, g.lx, g.ly, g.lz)
+        assert (o.dz is None) == (g.dz is None)
+        if o.dz is not None:
+            assert np.array_equal(o.dz, g.dz)
+        assert o.bc == tuple(p.bc.as_tuples())
+        for a, b in ((o.k, p.k), (o.q_basis, p.q_basis), (o.coef, p.coef)):
+            assert a.shape == b.shape and np.array_equal(a, b)
