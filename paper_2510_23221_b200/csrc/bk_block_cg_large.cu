@@ -847,6 +847,8 @@ cudaError_t launch_pupdate(const SweepArgs& a, int nb, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+#include "bk_sweep64.cuh"
+
 // phase 1 launch: the TMA variant for S = 64 on grids whose x-runs are full
 // (nx % 16 == 0), else the cp.async-free direct-load kernel
 template <int S>
@@ -1176,8 +1178,12 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     a.precond = cfg->precond;
     const int nb = sweep_ctas(ctx, sl, S);
     constexpr int E = S * S + S;
+    // warp-specialised TMA update sweep for S = 64 on full 16-cell x-runs
+    const bool ws_update = S == 64 && update64_ws_ok(sl) && !ctx->knobs.no_ws_update;
+    const int64_t nloc_ws = (int64_t)sl.nx * (sl.nyl + 2) * sl.nz;
     ctx->last_variant = "block_cg_large<" + std::to_string(S) + ">" +
-                        ((S == 64 && sl.nx % 16 == 0 && !ctx->knobs.no_tma_spmm) ? " tma" : "");
+                        ((S == 64 && sl.nx % 16 == 0 && !ctx->knobs.no_tma_spmm) ? " tma" : "") +
+                        (ws_update ? " ws-update" : "");
     void *pPart, *pRed, *pCtl, *pHost;
     bk_status st;
     if ((st = workspace(ctx, kSlotCgPart, (size_t)nb * E * 8, &pPart)) != BK_OK) return st;
@@ -1257,10 +1263,16 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
         k_ctl_alpha<S><<<1, CBS, cs, s>>>(ctl, red);
         ++ctx->launches;
         phase_mark(ctx, -1);
-        BK_CUDA_TRY(ctx, (launch_update<S, true>(a, nb, s)));
+        int nbu = nb;
+        if (S == 64 && ws_update) {
+            nbu = ctx->num_sms < nb ? ctx->num_sms : nb;
+            BK_CUDA_TRY(ctx, launch_update64_ws(a, nloc_ws, nbu, s));
+        } else {
+            BK_CUDA_TRY(ctx, (launch_update<S, true>(a, nb, s)));
+        }
         phase_mark(ctx, 1);
         ++ctx->launches;
-        reduce(E, nb);
+        reduce(E, nbu);
         k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, red, m);
         ++ctx->launches;
         BK_CUDA_TRY(ctx, cudaGetLastError());
@@ -1288,6 +1300,8 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
         phase_mark(ctx, -1);
         if (x_done)
             BK_CUDA_TRY(ctx, (launch_pupdate<S, 0>(a, nb, s)));
+        else if (S == 64 && ws_update)
+            BK_CUDA_TRY(ctx, launch_pupdate64_ws(a, nloc_ws, ctx->num_sms < nb ? ctx->num_sms : nb, s));
         else
             BK_CUDA_TRY(ctx, (launch_pupdate<S, 1>(a, nb, s)));
         phase_mark(ctx, 2);

@@ -35,6 +35,7 @@ struct bk_knobs {
     bool comb_profile = false; // combine/action stage timestamps (stderr)
     bool batch_trace = false;
     bool phase_timing = false; // per-kernel-kind event timing of the multi-kernel solve
+    bool no_ws_update = false; // S = 64: the cp.async update sweep instead of the warp-specialised one
 };
 
 // Optional per-kernel-kind timing of the multi-kernel solve (option

@@ -1,0 +1,487 @@
+// Update sweep for S = 64 (BASELINE config 5), warp-specialised.
+//
+// Included by bk_block_cg_large.cu after its sweep helpers. Phase 2 of
+// block_cg (solvers.cpp:557-564; update_fused_fixed :246-278 for s <= 16,
+// add_product / gram :199-211, :636-640 above): R -= W alpha, rr_j = sum r^2,
+// Z = D^-1 R, S_new = R^T Z — with X += P alpha deferred to the P update.
+//
+// At S = 64 this sweep is FP64-pipe bound, not HBM bound: per 16-cell run it
+// moves 24 KB but issues 128 m16n8k4 DMMAs for R -= W alpha and 80 for the
+// upper-triangle Gram (13.3 kflop per cell; the B200 FP64 tensor rate is
+// ~37 TFLOP/s, measured, scripts/dmma_tput.cu, shared with SIMT DFMA). The
+// design keeps the FP64 pipe fed:
+//   * one CTA per SM: 3 teams of 4 consumer warps + 1 producer warp (13
+//     warps: at most 4 per SM sub-partition, so 128 registers per thread);
+//   * the producer streams each team's next runs (W and R as four 16-column
+//     panels each, TMA 2D tensor copies with 128-byte swizzle, plus the run's
+//     D^-1 by a bulk copy) into a per-team ring of stages, full / empty
+//     mbarriers per stage — the consumers never issue a load;
+//   * a team owns one run at a time, warp w of the team the output columns
+//     16w .. 16w + 15 (two n-tiles; alpha fragments from shared memory);
+//     teams synchronise only among their own 128 threads (named barriers), so
+//     the teams drift and overlap one another's DMMA, epilogue and wait
+//     phases;
+//   * after the update the team writes R and Z into the stage's W / R panels
+//     (same swizzle) and each warp accumulates 5 of the 20 upper 16 x 8 Gram
+//     tiles; the stage is released by one arrival per warp.
+// Fixed group-to-team assignment and a fixed-order sum of the teams' partials:
+// run-to-run deterministic.
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+namespace sweep64 {
+
+constexpr int kTeams = 3;  // 13 warps: 4 per SMSP at most -> up to 128 registers
+constexpr int kTeamWarps = 4;
+constexpr int kConsumers = kTeams * kTeamWarps * 32;  // 384
+constexpr int kThreads = kConsumers + 32;               // + producer warp
+constexpr int kStages = 3;                              // per team
+constexpr int kPanelBytes = 16 * 128;                   // 16 rows x 16 doubles
+constexpr int kArrBytes = 4 * kPanelBytes;              // one array of a run: 8 KB
+constexpr int kStageBytes = 2 * kArrBytes;              // W, R
+
+struct Smem {
+    unsigned char stage[kTeams][kStages][kStageBytes];  // 1024-aligned
+    unsigned char rstage[kTeams][2][kArrBytes];          // updated R of a run (Gram input)
+    double alpha[64 * 64];                               // alpha, swizzled (alpha_at)
+    double dinv[kTeams][kStages][16];                    // D^-1 of each stage's run
+    unsigned long long full[kTeams][kStages];
+    unsigned long long empty[kTeams][kStages];
+};
+constexpr size_t smem_bytes() { return sizeof(Smem) + 1024; }
+
+// element (row r, column c) of a 16-row, 64-column array stored as four
+// 128B-swizzled 16-column panels: the 16-byte chunk (c % 16) / 2 of row r
+// sits at chunk ((c % 16) / 2) ^ (r % 8)
+__device__ __forceinline__ int swz(int r, int c) {
+    return (c >> 4) * kPanelBytes + r * 128 + ((((c & 15) >> 1) ^ (r & 7)) << 4) + ((c & 1) << 3);
+}
+// DMMA row g (0..7) of an m-tile <-> cell pi(g) of the run (rows g + 8 <->
+// pi(g) + 8): the 3-bit reversal makes the swizzle keys of the 8 lanes of a
+// 128-bit access (g = 2j, 2j + 1) differ in bit 2 and those of a half-warp's
+// 64-bit access (g = 0..3 or 4..7) all even or all odd — conflict-free reads
+// of the swizzled panels (the update is elementwise in the cell dimension,
+// so any row order is the same computation)
+// alpha[k][c] at k * 64 + (c ^ 4 (k % 4)): the B-fragment loads (lanes g, t
+// read row k = 4 ks + t, column c0 + g) hit 16 distinct 8-byte slots per
+// half-warp
+__device__ __forceinline__ int alpha_at(int k, int c) { return k * 64 + (c ^ ((k & 3) << 2)); }
+__device__ __forceinline__ int pi8(int g) { return ((g & 1) << 2) | (g & 2) | (g >> 2); }
+// Gram k-step kc, lane t -> cell of the run (all 16 covered once; the 4
+// cells of a k-step have swizzle keys of equal parity)
+__device__ __forceinline__ int gram_cell(int kc, int t) { return (kc & 1) + 2 * t + 8 * (kc >> 1); }
+__device__ __forceinline__ double lds(const unsigned char* base, int r, int c) {
+    return *reinterpret_cast<const double*>(base + swz(r, c));
+}
+__device__ __forceinline__ double2 lds2(const unsigned char* base, int r, int c) {  // c even
+    return *reinterpret_cast<const double2*>(base + swz(r, c));
+}
+__device__ __forceinline__ void sts2(unsigned char* base, int r, int c, double x, double y) {
+    *reinterpret_cast<double2*>(base + swz(r, c)) = make_double2(x, y);  // c even
+}
+
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                       unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void team_sync(int team) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(kTeamWarps * 32) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// the 20 upper-triangle tiles (m 16-row block, n 8-column block) of the 64 x 64
+// Gram, 5 per warp of a team (balanced)
+__device__ __forceinline__ void gram_tile(int w, int i, int& m, int& n) {
+    // tiles in row order: m = 0 -> n 0..7, m = 1 -> n 2..7, m = 2 -> n 4..7, m = 3 -> n 6..7
+    const int k = 5 * w + i;
+    m = (k >= 8) + (k >= 14) + (k >= 18);
+    n = k - (m == 0 ? 0 : m == 1 ? 6 : m == 2 ? 10 : 12);
+}
+
+// W (a.W) and R (a.R) as 2D tensors (64 columns, nloc rows)
+__global__ void __launch_bounds__(kThreads, 1)
+    k_update64_ws(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapR,
+                  SweepArgs a) {
+    constexpr int S = 64;
+    extern __shared__ __align__(1024) unsigned char smraw_[];
+    // 1024-byte aligned (128B-swizzle atoms); pointer arithmetic on the shared
+    // array keeps the state space, so the accesses compile to LDS / STS
+    Smem& sm = *reinterpret_cast<Smem*>(smraw_ + ((1024u - (smem_u32(smraw_) & 1023u)) & 1023u));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int ntiles = n_tiles(a.sl);  // 16-cell runs
+    const int nteams = gridDim.x * kTeams;
+    const bool jac = a.precond != 0;
+    for (int e = threadIdx.x; e < S * S; e += blockDim.x)
+        sm.alpha[alpha_at(e / S, e % S)] = a.coef[(e / S) * (S + 4) + e % S];
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < kTeams; ++q)
+            for (int s = 0; s < kStages; ++s) {
+                mbar_init(&sm.full[q][s], 1);
+                mbar_init(&sm.empty[q][s], kTeamWarps);
+            }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kTeams * kTeamWarps) {  // ---- producer
+        if (lane == 0) {
+            int it[kTeams] = {};
+            bool live = true;
+            while (live) {
+                live = false;
+                for (int q = 0; q < kTeams; ++q) {
+                    const int grp = blockIdx.x * kTeams + q + it[q] * nteams;
+                    if (grp >= ntiles) continue;
+                    live = true;
+                    const int s = it[q] % kStages;
+                    if (it[q] >= kStages) mbar_wait(&sm.empty[q][s], ((it[q] / kStages) - 1) & 1);
+                    TileCells tc;
+                    tile_cells(a.sl, grp, ntiles, tc);
+                    unsigned char* st = sm.stage[q][s];
+                    unsigned long long* bar = &sm.full[q][s];
+                    mbar_expect_tx(bar, 2 * kArrBytes + (jac ? 128 : 0));
+                    for (int p = 0; p < 4; ++p) {
+                        tma_2d(st + p * kPanelBytes, &mapW, 16 * p, (int)tc.l0, bar);
+                        tma_2d(st + kArrBytes + p * kPanelBytes, &mapR, 16 * p, (int)tc.l0, bar);
+                    }
+                    if (jac) bulk_g2s(sm.dinv[q][s], a.st.dinv + tc.g0, 128, bar);
+                    ++it[q];
+                }
+            }
+        }
+        return;
+    }
+
+    // ---- consumers: team q, warp w of the team owns columns 16 w .. 16 w + 15.
+    // Software-pipelined so that a team needs ONE barrier per run: the update
+    // of run i + 1 (independent DMMA work) sits between a warp's write of run
+    // i's R into the team's staging buffer and the barrier after which the team
+    // reads that buffer for run i's Gram. Staging is double-buffered: a warp
+    // that passed the barrier of run i knows every warp finished the Gram of
+    // run i - 1, so buffer (i + 1) % 2 is free for run i + 1.
+    const int q = warp / kTeamWarps, w = warp % kTeamWarps;
+    double gacc[5][4];
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) gacc[i][e] = 0.0;
+    int gm[5], gn[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) gram_tile(w, i, gm[i], gn[i]);
+    double rr[4] = {0.0, 0.0, 0.0, 0.0};  // columns 16w + 8nt + 2t + e
+    const int first = blockIdx.x * kTeams + q;
+
+    // R -= W alpha for the run in stage `it`: D (16 cells x 8 columns) per
+    // n-tile, K = 64; also fetches D^-1 of the Gram rows kc + 4t (kc = 0..3)
+    // and releases the stage
+    auto update = [&](int it, double (&d)[2][4], double (&dg)[4], double& d0, double& d1) {
+        const int s = it % kStages;
+        mbar_wait(&sm.full[q][s], (it / kStages) & 1);
+        const unsigned char* Wt = sm.stage[q][s];
+        const unsigned char* Rt = Wt + kArrBytes;
+        const double* dv = sm.dinv[q][s];
+        const int rg = pi8(g);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            const int c = 16 * w + 8 * nt + 2 * t;
+            const double2 lo = lds2(Rt, rg, c), hi = lds2(Rt, rg + 8, c);
+            d[nt][0] = lo.x;
+            d[nt][1] = lo.y;
+            d[nt][2] = hi.x;
+            d[nt][3] = hi.y;
+        }
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+            const int k = 4 * ks + t;
+            const double a0 = -lds(Wt, rg, k), a1 = -lds(Wt, rg + 8, k);
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+                dmma_l(d[nt], a0, a1, sm.alpha[alpha_at(k, 16 * w + 8 * nt + g)]);
+        }
+        d0 = jac ? dv[rg] : 1.0;
+        d1 = jac ? dv[rg + 8] : 1.0;
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) dg[kc] = jac ? dv[gram_cell(kc, t)] : 1.0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[q][s]);
+    };
+    // rr, R to HBM, R into staging buffer b (Z = D^-1 R is formed in the Gram)
+    auto epilogue = [&](int grp, const double (&d)[2][4], int b) {
+        TileCells tc;
+        tile_cells(a.sl, grp, ntiles, tc);
+        unsigned char* St = sm.rstage[q][b];
+        const int rg = pi8(g);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            rr[2 * nt] += d[nt][0] * d[nt][0] + d[nt][2] * d[nt][2];
+            rr[2 * nt + 1] += d[nt][1] * d[nt][1] + d[nt][3] * d[nt][3];
+            const int c = 16 * w + 8 * nt + 2 * t;
+            *reinterpret_cast<double2*>(a.R + (tc.l0 + rg) * S + c) = make_double2(d[nt][0], d[nt][1]);
+            *reinterpret_cast<double2*>(a.R + (tc.l0 + rg + 8) * S + c) =
+                make_double2(d[nt][2], d[nt][3]);
+            sts2(St, rg, c, d[nt][0], d[nt][1]);
+            sts2(St, rg + 8, c, d[nt][2], d[nt][3]);
+        }
+    };
+    // S_new += R^T Z over a run's 16 cells: k-step kc covers cells
+    // gram_cell(kc, t') (conflict-free reads); Z = D^-1 R
+    // formed from the staged R with the row's D^-1 (the same product the
+    // cp.async sweep stores)
+    auto gram = [&](int b, const double (&dg)[4]) {
+        const unsigned char* St = sm.rstage[q][b];
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) {
+            const int c = gram_cell(kc, t);
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                const double a0 = lds(St, c, 16 * gm[i] + g);
+                const double a1 = lds(St, c, 16 * gm[i] + 8 + g);
+                dmma_l(gacc[i], a0, a1, dg[kc] * lds(St, c, 8 * gn[i] + g));
+            }
+        }
+    };
+
+    if (first < ntiles) {
+        double d[2][4], dg[4], d0, d1;
+        update(0, d, dg, d0, d1);
+        (void)d0;
+        (void)d1;
+        epilogue(first, d, 0);
+        int it = 0;
+        for (int grp = first; grp < ntiles; grp += nteams, ++it) {
+            const int nxt = grp + nteams;
+            double dn[2][4], dgn[4], e0, e1;
+            if (nxt < ntiles) update(it + 1, dn, dgn, e0, e1);
+            team_sync(q);  // every warp of the team staged run `it`
+            gram(it & 1, dg);
+            if (nxt < ntiles) {
+                epilogue(nxt, dn, (it + 1) & 1);
+#pragma unroll
+                for (int kc = 0; kc < 4; ++kc) dg[kc] = dgn[kc];
+            }
+        }
+    }
+
+    // ---- per-CTA partials [S_new (64 x 64) | rr (64)], teams summed in order
+    asm volatile("bar.sync %0, %1;" ::"r"(9), "r"(kConsumers) : "memory");
+    double* red = reinterpret_cast<double*>(sm.stage[0][0]);  // kTeams x (64*64 + 64) doubles
+    static_assert(kTeams * (64 * 64 + 64) * 8 <= sizeof(Smem::stage), "reduction buffer");
+    double* mine = red + q * (S * S + S);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const int r0 = 16 * gm[i] + g, c0 = 8 * gn[i] + 2 * t;
+        mine[r0 * S + c0] = gacc[i][0];
+        mine[r0 * S + c0 + 1] = gacc[i][1];
+        mine[(r0 + 8) * S + c0] = gacc[i][2];
+        mine[(r0 + 8) * S + c0 + 1] = gacc[i][3];
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        double x = rr[e];
+        x += __shfl_xor_sync(0xffffffffu, x, 4);
+        x += __shfl_xor_sync(0xffffffffu, x, 8);
+        x += __shfl_xor_sync(0xffffffffu, x, 16);
+        if (g == 0) mine[S * S + 16 * w + 8 * (e >> 1) + 2 * t + (e & 1)] = x;
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(9), "r"(kConsumers) : "memory");
+    double* out = a.part + (int64_t)blockIdx.x * (S * S + S);
+    for (int e = threadIdx.x; e < S * S + S; e += kConsumers) {
+        if (e < S * S && (e % S) / 8 < 2 * ((e / S) / 16)) {  // below-diagonal tiles
+            out[e] = 0.0;
+            continue;
+        }
+        double v = red[e];
+        for (int k = 1; k < kTeams; ++k) v += red[k * (S * S + S) + e];
+        out[e] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// P update for S = 64 (the common MODE 1 of k_pupdate): P = D^-1 R + P beta
+// and the deferred X += P alpha (solvers.cpp:645-649 and :566-576), both
+// GEMMs from the same staged P fragments. Same structure as the update sweep
+// (producer warp, per-team TMA ring of P / R / X panels); no reduction, so no
+// team barrier at all — each warp owns 16 output columns of P and X, reads
+// its accumulator inits (Z, X) and every P row from the stage, releases the
+// stage with one arrival and stores its results from registers. Per-element
+// DMMA chains in ascending k, as k_pupdate: bitwise the same P and X.
+// ---------------------------------------------------------------------------
+constexpr int kPStages = 2;
+struct SmemP {
+    unsigned char stage[kTeams][kPStages][3 * kArrBytes];  // P, R, X panels
+    double alpha[64 * 64];                                   // swizzled (alpha_at)
+    double beta[64 * 64];
+    double dinv[kTeams][kPStages][16];
+    unsigned long long full[kTeams][kPStages];
+    unsigned long long empty[kTeams][kPStages];
+};
+constexpr size_t smem_bytes_p() { return sizeof(SmemP) + 1024; }
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_pupdate64_ws(const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapR,
+                   const __grid_constant__ CUtensorMap mapX, SweepArgs a) {
+    constexpr int S = 64;
+    extern __shared__ __align__(1024) unsigned char smraw_[];
+    SmemP& sm = *reinterpret_cast<SmemP*>(smraw_ + ((1024u - (smem_u32(smraw_) & 1023u)) & 1023u));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int ntiles = n_tiles(a.sl);
+    const int nteams = gridDim.x * kTeams;
+    const bool jac = a.precond != 0;
+    for (int e = threadIdx.x; e < S * S; e += blockDim.x) {
+        sm.beta[alpha_at(e / S, e % S)] = a.coef[(e / S) * (S + 4) + e % S];
+        sm.alpha[alpha_at(e / S, e % S)] = a.coef2[(e / S) * (S + 4) + e % S];
+    }
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < kTeams; ++q)
+            for (int s = 0; s < kPStages; ++s) {
+                mbar_init(&sm.full[q][s], 1);
+                mbar_init(&sm.empty[q][s], kTeamWarps);
+            }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kTeams * kTeamWarps) {  // ---- producer
+        if (lane == 0) {
+            int it[kTeams] = {};
+            bool live = true;
+            while (live) {
+                live = false;
+                for (int q = 0; q < kTeams; ++q) {
+                    const int grp = blockIdx.x * kTeams + q + it[q] * nteams;
+                    if (grp >= ntiles) continue;
+                    live = true;
+                    const int s = it[q] % kPStages;
+                    if (it[q] >= kPStages) mbar_wait(&sm.empty[q][s], ((it[q] / kPStages) - 1) & 1);
+                    TileCells tc;
+                    tile_cells(a.sl, grp, ntiles, tc);
+                    unsigned char* st = sm.stage[q][s];
+                    unsigned long long* bar = &sm.full[q][s];
+                    mbar_expect_tx(bar, 3 * kArrBytes + (jac ? 128 : 0));
+                    for (int p = 0; p < 4; ++p) {
+                        tma_2d(st + p * kPanelBytes, &mapP, 16 * p, (int)tc.l0, bar);
+                        tma_2d(st + kArrBytes + p * kPanelBytes, &mapR, 16 * p, (int)tc.l0, bar);
+                        tma_2d(st + 2 * kArrBytes + p * kPanelBytes, &mapX, 16 * p, (int)tc.l0, bar);
+                    }
+                    if (jac) bulk_g2s(sm.dinv[q][s], a.st.dinv + tc.g0, 128, bar);
+                    ++it[q];
+                }
+            }
+        }
+        return;
+    }
+
+    const int q = warp / kTeamWarps, w = warp % kTeamWarps;
+    const int rg = pi8(g);
+    int it = 0;
+    for (int grp = blockIdx.x * kTeams + q; grp < ntiles; grp += nteams, ++it) {
+        const int s = it % kPStages;
+        mbar_wait(&sm.full[q][s], (it / kPStages) & 1);
+        const unsigned char* Pt = sm.stage[q][s];
+        const unsigned char* Rt = Pt + kArrBytes;
+        const unsigned char* Xt = Pt + 2 * kArrBytes;
+        const double d0 = jac ? sm.dinv[q][s][rg] : 1.0, d1 = jac ? sm.dinv[q][s][rg + 8] : 1.0;
+        double pv[2][4], xv[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            const int c = 16 * w + 8 * nt + 2 * t;
+            const double2 r0 = lds2(Rt, rg, c), r1 = lds2(Rt, rg + 8, c);
+            const double2 x0 = lds2(Xt, rg, c), x1 = lds2(Xt, rg + 8, c);
+            pv[nt][0] = r0.x * d0;
+            pv[nt][1] = r0.y * d0;
+            pv[nt][2] = r1.x * d1;
+            pv[nt][3] = r1.y * d1;
+            xv[nt][0] = x0.x;
+            xv[nt][1] = x0.y;
+            xv[nt][2] = x1.x;
+            xv[nt][3] = x1.y;
+        }
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+            const int k = 4 * ks + t;
+            const double a0 = lds(Pt, rg, k), a1 = lds(Pt, rg + 8, k);
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                const int c = alpha_at(k, 16 * w + 8 * nt + g);
+                dmma_l(xv[nt], a0, a1, sm.alpha[c]);
+                dmma_l(pv[nt], a0, a1, sm.beta[c]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[q][s]);
+        TileCells tc;
+        tile_cells(a.sl, grp, ntiles, tc);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            const int c = 16 * w + 8 * nt + 2 * t;
+            *reinterpret_cast<double2*>(a.P + (tc.l0 + rg) * S + c) = make_double2(pv[nt][0], pv[nt][1]);
+            *reinterpret_cast<double2*>(a.P + (tc.l0 + rg + 8) * S + c) =
+                make_double2(pv[nt][2], pv[nt][3]);
+            *reinterpret_cast<double2*>(a.X + (tc.l0 + rg) * S + c) = make_double2(xv[nt][0], xv[nt][1]);
+            *reinterpret_cast<double2*>(a.X + (tc.l0 + rg + 8) * S + c) =
+                make_double2(xv[nt][2], xv[nt][3]);
+        }
+    }
+}
+
+inline PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) !=
+                cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// [nrows][64] doubles as a 2D tensor, box 16 columns x 16 rows, 128B swizzle
+inline bool make_map(CUtensorMap* m, const double* base, int64_t nrows) {
+    auto enc = encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {64, (cuuint64_t)nrows};
+    const cuuint64_t strides[1] = {64 * 8};
+    const cuuint32_t box[2] = {16, 16};
+    const cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace sweep64
+
+// the warp-specialised S = 64 update (XD layout: X is updated by k_pupdate)
+inline bool update64_ws_ok(const Slab& sl) { return sl.nx % 16 == 0; }
+inline cudaError_t launch_update64_ws(const SweepArgs& a, int64_t nloc, int nsm, cudaStream_t s) {
+    CUtensorMap mw, mr;
+    if (!sweep64::make_map(&mw, a.W, nloc) || !sweep64::make_map(&mr, a.R, nloc))
+        return cudaErrorInvalidValue;
+    const size_t smem = sweep64::smem_bytes();
+    const cudaError_t e = bk::set_max_smem((const void*)sweep64::k_update64_ws, smem);
+    if (e != cudaSuccess) return e;
+    sweep64::k_update64_ws<<<nsm, sweep64::kThreads, smem, s>>>(mw, mr, a);
+    return cudaGetLastError();
+}
+
+// the warp-specialised S = 64 P update with the deferred X update (MODE 1)
+inline cudaError_t launch_pupdate64_ws(const SweepArgs& a, int64_t nloc, int nsm, cudaStream_t s) {
+    CUtensorMap mp, mr, mx;
+    if (!sweep64::make_map(&mp, a.P, nloc) || !sweep64::make_map(&mr, a.R, nloc) ||
+        !sweep64::make_map(&mx, a.X, nloc))
+        return cudaErrorInvalidValue;
+    const size_t smem = sweep64::smem_bytes_p();
+    const cudaError_t e = bk::set_max_smem((const void*)sweep64::k_pupdate64_ws, smem);
+    if (e != cudaSuccess) return e;
+    sweep64::k_pupdate64_ws<<<nsm, sweep64::kThreads, smem, s>>>(mp, mr, mx, a);
+    return cudaGetLastError();
+}

@@ -521,7 +521,14 @@ def test_slab_decomposition_matches_single_gpu(bk, ctx, nslabs):
     B = torch.empty_like(q)
     bk.rhs_from_power(op, q, out=B)
     torch.cuda.synchronize()
-    ref = bk.block_cg(op, B.cpu().numpy(), cfg_jacobi())
+    # the slab steps (bk_dd_step) use the cp.async update sweep with X updated
+    # in phase 2; the single-GPU engine's warp-specialised S = 64 update sweep
+    # defers X to the P update — same iterates to rounding, so the bitwise
+    # one-slab check runs against the matching single-GPU variant
+    with ctx.options(no_ws_update=1):
+        ref = bk.block_cg(op, B.cpu().numpy(), cfg_jacobi())
+    ref_ws = bk.block_cg(op, B.cpu().numpy(), cfg_jacobi())
+    assert rel_l2(ref_ws.x, ref.x) <= PARITY
     parts = dd.partition_rows(inp.grid.ny, nslabs)
     X, rep = dd.solve_decomposed(bk, ctx, op, B, cfg_jacobi(), parts)
     torch.cuda.synchronize()
