@@ -1034,7 +1034,7 @@ def run_c5(args, ctx, world, rank, local):
         chip_h = SimpleNamespace(grid=inp.grid, bc=inp.bc, k=k_h, q_basis=q_h, coef=c_h)
         ctx.set_option("phase_timing", 0)
         bk.generate_stream([chip_h], cfg, sink=None, ctx=ctx)  # warm-up: rings allocated
-        e2e_chips = max(2, min(args.steps, 3))
+        e2e_chips = max(2, min(args.steps, 5))
         torch.cuda.synchronize()
         e0, e1 = ev(), ev()
         e0.record(stream)

@@ -1180,10 +1180,11 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     constexpr int E = S * S + S;
     // warp-specialised TMA update sweep for S = 64 on full 16-cell x-runs
     const bool ws_update = S == 64 && update64_ws_ok(sl) && !ctx->knobs.no_ws_update;
+    const bool ws_spmm = S == 64 && update64_ws_ok(sl) && !ctx->knobs.no_ws_spmm;
     const int64_t nloc_ws = (int64_t)sl.nx * (sl.nyl + 2) * sl.nz;
     ctx->last_variant = "block_cg_large<" + std::to_string(S) + ">" +
                         ((S == 64 && sl.nx % 16 == 0 && !ctx->knobs.no_tma_spmm) ? " tma" : "") +
-                        (ws_update ? " ws-update" : "");
+                        (ws_update ? " ws-update" : "") + (ws_spmm ? " ws-spmm" : "");
     void *pPart, *pRed, *pCtl, *pHost;
     bk_status st;
     if ((st = workspace(ctx, kSlotCgPart, (size_t)nb * E * 8, &pPart)) != BK_OK) return st;
@@ -1256,10 +1257,16 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     for (int m = 1; m <= cfg->max_iter && sa > 0; ++m) {
         halo(a.P);
         phase_mark(ctx, -1);
-        BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s, ctx->knobs.no_tma_spmm));
+        int nbs = nb;
+        if (S == 64 && ws_spmm) {
+            nbs = ctx->num_sms < nb ? ctx->num_sms : nb;
+            BK_CUDA_TRY(ctx, launch_spmm64_ws(a, nbs, s));
+        } else {
+            BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s, ctx->knobs.no_tma_spmm));
+        }
         phase_mark(ctx, 0);
         ++ctx->launches;
-        reduce(S * S, nb);
+        reduce(S * S, nbs);
         k_ctl_alpha<S><<<1, CBS, cs, s>>>(ctl, red);
         ++ctx->launches;
         phase_mark(ctx, -1);

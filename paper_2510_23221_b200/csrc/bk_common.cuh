@@ -35,7 +35,8 @@ struct bk_knobs {
     bool comb_profile = false; // combine/action stage timestamps (stderr)
     bool batch_trace = false;
     bool phase_timing = false; // per-kernel-kind event timing of the multi-kernel solve
-    bool no_ws_update = false; // S = 64: the cp.async update sweep instead of the warp-specialised one
+    bool no_ws_update = false; // S = 64: the cp.async update sweeps instead of the warp-specialised ones
+    bool no_ws_spmm = false;   // S = 64: the per-run TMA stencil sweep instead of the z-marching one
 };
 
 // Optional per-kernel-kind timing of the multi-kernel solve (option

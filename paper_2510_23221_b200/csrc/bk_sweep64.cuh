@@ -432,6 +432,255 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Stencil sweep for S = 64: W = A P (CsrMatrix::apply_block order, FMA chain
+// z-, y-, x-, diag, x+, y+, z+; discretize.cpp:57-95) and the upper-triangle
+// Gram G = P^T W (spmm_gram_fixed, solvers.cpp:221-242), z-marching.
+//
+// A team (4 warps) owns a pencil — a 16-cell x-run at fixed y — and walks
+// it through z, so each P run arrives once from L2 and serves as the centre
+// (with its x-halo cells) and as the z -+ 1 neighbour of the adjacent planes
+// from a 4-slot ring; per step only the y -+ 1 runs and six coefficient runs
+// stream in (a 2-unit ring). The producer warp issues all copies (1D bulk,
+// mbarrier completion) two steps ahead; consumers never load from global.
+// Per step: each thread forms W for one cell and 8 columns (16-byte shared
+// reads of whole rows: conflict-free), stores W, stages P and W (swizzled,
+// double-buffered) for the Gram, one team barrier, then each warp
+// accumulates 5 of the 20 Gram tiles (conflict-free maps as in the update).
+// ---------------------------------------------------------------------------
+constexpr int kSTeams = 2;
+constexpr int kSWarps = kSTeams * kTeamWarps;   // 8 consumer warps
+constexpr int kSThreads = kSWarps * 32 + 32;    // + producer
+constexpr int kCRows = 18;                      // centre run with its x-halo cells
+constexpr int kCoefLD = 24;                     // doubles per coefficient run
+struct SmemS {
+    double cring[kSTeams][4][kCRows * 64];      // centre P runs, plane v in slot v % 4
+    double yrun[kSTeams][2][2][16 * 64];        // y - 1 / y + 1 runs of a step
+    double coef[kSTeams][2][6 * kCoefLD];       // diag, cx (x-halo), cy(y-1), cy, cz(z-1), cz
+    unsigned char gst[kSTeams][2][2 * kArrBytes];  // Gram staging P | W (swizzled), 1024-aligned
+    unsigned long long full[kSTeams][2], empty[kSTeams][2], pro[kSTeams];
+};
+constexpr size_t smem_bytes_s() { return sizeof(SmemS) + 1024; }
+
+struct Pencil {
+    int ix0, iyl, iyg;
+    __device__ int64_t lrow(const Slab& sl, int z) const {  // slab-local row of cell ix0 at plane z
+        return ix0 + (int64_t)sl.nx * (iyl + (int64_t)(sl.nyl + 2) * z);
+    }
+    __device__ int64_t grow(const Slab& sl, int z) const {
+        return ix0 + (int64_t)sl.nx * (iyg + (int64_t)sl.ny * z);
+    }
+};
+__device__ __forceinline__ Pencil pencil_of(const Slab& sl, int p) {
+    const int ntx = sl.nx / 16;
+    Pencil pc;
+    pc.ix0 = 16 * (p % ntx);
+    pc.iyl = 1 + p / ntx;
+    pc.iyg = sl.y0 + pc.iyl - 1;
+    return pc;
+}
+
+__global__ void __launch_bounds__(kSThreads, 1) k_spmm64_ws(SweepArgs a) {
+    constexpr int S = 64;
+    extern __shared__ __align__(1024) unsigned char smraw_[];
+    SmemS& sm = *reinterpret_cast<SmemS*>(smraw_ + ((1024u - (smem_u32(smraw_) & 1023u)) & 1023u));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Slab& sl = a.sl;
+    const int nz = sl.nz;
+    const int npen = (sl.nx / 16) * sl.nyl;
+    const int nteams = gridDim.x * kSTeams;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < kSTeams; ++q) {
+            for (int s = 0; s < 2; ++s) {
+                mbar_init(&sm.full[q][s], 1);
+                mbar_init(&sm.empty[q][s], kTeamWarps);
+            }
+            mbar_init(&sm.pro[q], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kSWarps) {  // ---- producer
+        if (lane == 0) {
+            const int64_t plane = (int64_t)sl.nx * sl.ny;
+            const unsigned rowb = S * 8;
+            // centre run of plane z of pencil pc into ring slot `slot`
+            auto centre = [&](int q, const Pencil& pc, int z, int slot, unsigned long long* bar) {
+                const int lo = pc.ix0 > 0 ? -1 : 0, hi = pc.ix0 + 16 < sl.nx ? 16 : 15;
+                bulk_g2s(sm.cring[q][slot] + (1 + lo) * S, a.P + (pc.lrow(sl, z) + lo) * S,
+                         (unsigned)(hi - lo + 1) * rowb, bar);
+            };
+            auto centre_bytes = [&](const Pencil& pc) -> unsigned {
+                const int lo = pc.ix0 > 0 ? -1 : 0, hi = pc.ix0 + 16 < sl.nx ? 16 : 15;
+                return (unsigned)(hi - lo + 1) * rowb;
+            };
+            int p[kSTeams], z[kSTeams], u[kSTeams], v[kSTeams];
+            bool live[kSTeams];
+            for (int q = 0; q < kSTeams; ++q) {
+                p[q] = blockIdx.x * kSTeams + q;
+                z[q] = 0;
+                u[q] = 0;
+                v[q] = 0;
+                live[q] = p[q] < npen;
+                if (live[q]) {  // prologue: plane 0 of the first pencil
+                    const Pencil pc = pencil_of(sl, p[q]);
+                    mbar_expect_tx(&sm.pro[q], centre_bytes(pc));
+                    centre(q, pc, 0, 0, &sm.pro[q]);
+                }
+            }
+            bool any = true;
+            while (any) {
+                any = false;
+                for (int q = 0; q < kSTeams; ++q) {
+                    if (!live[q]) continue;
+                    any = true;
+                    const int s = u[q] & 1;
+                    if (u[q] >= 2) mbar_wait(&sm.empty[q][s], ((u[q] >> 1) - 1) & 1);
+                    const Pencil pc = pencil_of(sl, p[q]);
+                    const int64_t g0 = pc.grow(sl, z[q]), l0 = pc.lrow(sl, z[q]);
+                    unsigned long long* bar = &sm.full[q][s];
+                    // next plane in this team's sequence
+                    int pn = p[q], zn = z[q] + 1;
+                    if (zn == nz) {
+                        pn += nteams;
+                        zn = 0;
+                    }
+                    const bool has_next = pn < npen;
+                    Pencil pcn = has_next ? pencil_of(sl, pn) : pc;
+                    unsigned bytes = 2 * 16 * rowb + 16 * 8 + 18 * 8 + 16 * 8 * 4;
+                    if (has_next) bytes += centre_bytes(pcn);
+                    mbar_expect_tx(bar, bytes);
+                    bulk_g2s(sm.yrun[q][s][0], a.P + (l0 - sl.nx) * S, 16 * rowb, bar);
+                    bulk_g2s(sm.yrun[q][s][1], a.P + (l0 + sl.nx) * S, 16 * rowb, bar);
+                    double* cf = sm.coef[q][s];
+                    bulk_g2s(cf, a.st.diag + g0, 16 * 8, bar);
+                    bulk_g2s(cf + kCoefLD, a.st.cx + (g0 >= 2 ? g0 - 2 : g0), 18 * 8, bar);
+                    bulk_g2s(cf + 2 * kCoefLD, a.st.cy + (pc.iyg > 0 ? g0 - sl.nx : g0), 16 * 8, bar);
+                    bulk_g2s(cf + 3 * kCoefLD, a.st.cy + g0, 16 * 8, bar);
+                    bulk_g2s(cf + 4 * kCoefLD, a.st.cz + (z[q] > 0 ? g0 - plane : g0), 16 * 8, bar);
+                    bulk_g2s(cf + 5 * kCoefLD, a.st.cz + g0, 16 * 8, bar);
+                    if (has_next) centre(q, pcn, zn, (v[q] + 1) & 3, bar);
+                    ++u[q];
+                    ++v[q];
+                    p[q] = pn;
+                    z[q] = zn;
+                    live[q] = has_next;
+                }
+            }
+        }
+        return;
+    }
+
+    // ---- consumers
+    const int q = warp / kTeamWarps, w = warp % kTeamWarps;
+    const int tt = threadIdx.x & 127;        // thread of the team
+    const int r = tt >> 3, cq = tt & 7;      // cell of the run, column quad
+    const int g = lane >> 2, t = lane & 3;
+    double gacc[5][4];
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) gacc[i][e] = 0.0;
+    int gm[5], gn[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) gram_tile(w, i, gm[i], gn[i]);
+    const int first = blockIdx.x * kSTeams + q;
+    if (first < npen) mbar_wait(&sm.pro[q], 0);
+    int u = 0;
+    for (int pp = first; pp < npen; pp += nteams) {
+        const Pencil pc = pencil_of(sl, pp);
+        const int ix = pc.ix0 + r;
+        for (int zz = 0; zz < nz; ++zz, ++u) {
+            const int xo = (pc.grow(sl, zz) < 2) ? 2 : 0;  // cx run started at g0 (array start)
+            const int s = u & 1;
+            mbar_wait(&sm.full[q][s], (u >> 1) & 1);
+            const double* C0 = sm.cring[q][u & 3];
+            const double* Cm = sm.cring[q][(u + 3) & 3];
+            const double* Cp = sm.cring[q][(u + 1) & 3];
+            const double* Ym = sm.yrun[q][s][0];
+            const double* Yp = sm.yrun[q][s][1];
+            const double* cf = sm.coef[q][s];
+            const bool hzm = zz > 0, hzp = zz < nz - 1, hym = pc.iyg > 0, hyp = pc.iyg < sl.ny - 1;
+            const bool hxm = ix > 0, hxp = ix < sl.nx - 1;
+            const double czm = -cf[4 * kCoefLD + r], cym = -cf[2 * kCoefLD + r];
+            const double cxm = -cf[kCoefLD + r + 1 - xo], dg = cf[r];
+            const double cxp = -cf[kCoefLD + r + 2 - xo], cyp = -cf[3 * kCoefLD + r];
+            const double czp = -cf[5 * kCoefLD + r];
+            double2 acc[4], ctr[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c = 2 * cq + 16 * j;
+                auto ld = [&](const double* row) {
+                    return *reinterpret_cast<const double2*>(row + c);
+                };
+                double2 x = make_double2(0.0, 0.0);
+                auto fm = [&](double cc, double2 v) {
+                    x.x = fma(cc, v.x, x.x);
+                    x.y = fma(cc, v.y, x.y);
+                };
+                if (hzm) fm(czm, ld(Cm + (1 + r) * S));
+                if (hym) fm(cym, ld(Ym + r * S));
+                if (hxm) fm(cxm, ld(C0 + r * S));
+                ctr[j] = ld(C0 + (1 + r) * S);
+                fm(dg, ctr[j]);
+                if (hxp) fm(cxp, ld(C0 + (2 + r) * S));
+                if (hyp) fm(cyp, ld(Yp + r * S));
+                if (hzp) fm(czp, ld(Cp + (1 + r) * S));
+                acc[j] = x;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty[q][s]);
+            const int64_t l = pc.lrow(sl, zz) + r;
+            unsigned char* Ut = sm.gst[q][s];
+            unsigned char* Vt = Ut + kArrBytes;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c = 2 * cq + 16 * j;
+                *reinterpret_cast<double2*>(a.W + l * S + c) = acc[j];
+                sts2(Ut, r, c, ctr[j].x, ctr[j].y);
+                sts2(Vt, r, c, acc[j].x, acc[j].y);
+            }
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(kTeamWarps * 32) : "memory");
+#pragma unroll
+            for (int kc = 0; kc < 4; ++kc) {
+                const int cc = gram_cell(kc, t);
+#pragma unroll
+                for (int i = 0; i < 5; ++i) {
+                    const double a0 = lds(Ut, cc, 16 * gm[i] + g);
+                    const double a1 = lds(Ut, cc, 16 * gm[i] + 8 + g);
+                    dmma_l(gacc[i], a0, a1, lds(Vt, cc, 8 * gn[i] + g));
+                }
+            }
+        }
+    }
+
+    // ---- per-CTA partial G (64 x 64), teams summed in order
+    asm volatile("bar.sync %0, %1;" ::"r"(9), "r"(kSWarps * 32) : "memory");
+    double* red = &sm.cring[0][0][0];
+    static_assert(kSTeams * 64 * 64 * 8 <= sizeof(SmemS::cring), "reduction buffer");
+    double* mine = red + q * (S * S);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const int r0 = 16 * gm[i] + g, c0 = 8 * gn[i] + 2 * t;
+        mine[r0 * S + c0] = gacc[i][0];
+        mine[r0 * S + c0 + 1] = gacc[i][1];
+        mine[(r0 + 8) * S + c0] = gacc[i][2];
+        mine[(r0 + 8) * S + c0 + 1] = gacc[i][3];
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(9), "r"(kSWarps * 32) : "memory");
+    double* out = a.part + (int64_t)blockIdx.x * (S * S);
+    for (int e = threadIdx.x; e < S * S; e += kSWarps * 32) {
+        if ((e % S) / 8 < 2 * ((e / S) / 16)) {
+            out[e] = 0.0;
+            continue;
+        }
+        double v = red[e];
+        for (int k = 1; k < kSTeams; ++k) v += red[k * (S * S) + e];
+        out[e] = v;
+    }
+}
+
 inline PFN_cuTensorMapEncodeTiled_v12000 encoder() {
     static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void* p = nullptr;
@@ -483,5 +732,14 @@ inline cudaError_t launch_pupdate64_ws(const SweepArgs& a, int64_t nloc, int nsm
     const cudaError_t e = bk::set_max_smem((const void*)sweep64::k_pupdate64_ws, smem);
     if (e != cudaSuccess) return e;
     sweep64::k_pupdate64_ws<<<nsm, sweep64::kThreads, smem, s>>>(mp, mr, mx, a);
+    return cudaGetLastError();
+}
+
+// z-marching stencil sweep with the Gram (full 16-cell x-runs, 16-aligned x)
+inline cudaError_t launch_spmm64_ws(const SweepArgs& a, int nsm, cudaStream_t s) {
+    const size_t smem = sweep64::smem_bytes_s();
+    const cudaError_t e = bk::set_max_smem((const void*)sweep64::k_spmm64_ws, smem);
+    if (e != cudaSuccess) return e;
+    sweep64::k_spmm64_ws<<<nsm, sweep64::kSThreads, smem, s>>>(a);
     return cudaGetLastError();
 }

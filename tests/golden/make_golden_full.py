@@ -39,6 +39,7 @@ from oracle.oracle import Oracle, Reference  # noqa: E402
 OUT = os.path.dirname(os.path.abspath(__file__))
 WORK = os.environ.get("BK_GOLDEN_WORK", "/tmp/bk_golden_c5")
 N_ROWS = 8192
+MAX_ITER_CG = 20000
 SAMPLES = [0, 1, 2499, 4999]
 
 
@@ -151,7 +152,7 @@ def _cg_worker(args):
             continue
         b = np.load(os.path.join(WORK, f"b_{j:02d}.npy"))
         t = time.time()
-        x, rep = ref.cg(op, b, tol, 100000, 1)
+        x, rep = ref.cg(op, b, tol, MAX_ITER_CG, 1)
         rep = {kk: (float(v) if not isinstance(v, (bool, int)) else v) for kk, v in rep.items()}
         rep["seconds"] = time.time() - t
         np.save(xp + ".tmp.npy", x)
@@ -160,9 +161,13 @@ def _cg_worker(args):
         print("column", j, rep, flush=True)
 
 
-def c5_cg(workers: int, tol: float = 1e-12):
+def c5_cg(workers: int, tol: float = 1e-11):
     """Per-column reference cg (solvers.cpp:82-171) of the full C5 basis, the
-    SURVEY §8(c) golden for config 5 (resumable; results in $BK_GOLDEN_WORK)."""
+    SURVEY §8(c) golden for config 5 (resumable; results in $BK_GOLDEN_WORK).
+    tol 1e-11, not 1e-12: a lone C5 column, like a C2 one (tests/test_oracle.py),
+    plateaus around 1e-12 in fp64, where the reference cg runs to max_iter
+    (measured: 1 of 6 columns reached 1e-12 within ~35 minutes); 1e-11 is
+    still ten times tighter than the GPU's pinned 1e-10."""
     from multiprocessing import Pool
 
     os.makedirs(WORK, exist_ok=True)

@@ -521,11 +521,12 @@ def test_slab_decomposition_matches_single_gpu(bk, ctx, nslabs):
     B = torch.empty_like(q)
     bk.rhs_from_power(op, q, out=B)
     torch.cuda.synchronize()
-    # the slab steps (bk_dd_step) use the cp.async update sweep with X updated
-    # in phase 2; the single-GPU engine's warp-specialised S = 64 update sweep
-    # defers X to the P update — same iterates to rounding, so the bitwise
-    # one-slab check runs against the matching single-GPU variant
-    with ctx.options(no_ws_update=1):
+    # the slab steps (bk_dd_step) use the per-run sweeps with X updated in
+    # phase 2; the single-GPU engine's warp-specialised S = 64 sweeps sum the
+    # Gram partials in another order and defer X to the P update — same
+    # iterates to rounding, so the bitwise one-slab check runs against the
+    # matching single-GPU variant
+    with ctx.options(no_ws_update=1, no_ws_spmm=1):
         ref = bk.block_cg(op, B.cpu().numpy(), cfg_jacobi())
     ref_ws = bk.block_cg(op, B.cpu().numpy(), cfg_jacobi())
     assert rel_l2(ref_ws.x, ref.x) <= PARITY
