@@ -64,11 +64,18 @@ C5_RING = 500            # samples per combine/action launch for C5 (device-resi
 # ~4.6 h on one core, so it is timed capped and scaled by this iteration count
 # (the GPU engine's count on the same chip at the same tolerance; refreshed
 # from the bench line of the current engine)
-C5_ITERATIONS = 694
+C5_ITERATIONS = 702
 C5_SLAB_ROWS = 64        # y-rows of the reference arm's bounded sample (1/8 of the chip)
 C5_REF_SAMPLES = 16      # samples of the reference arm's combine + action sample
 CHIPS_BY_CONFIG = {1: 64, 2: 16, 3: 12}  # independent chips per GPU per step, solved together
-DMMA_PEAK_TFLOPS = 73.9  # mma.sync.m16n8k4.f64, measured (profiles/r1_summary.md)
+# FP64 peak of this B200 pool, measured (scripts/dmma_tput.cu, round 2): mma.sync
+# m16n8k4/k8/k16 f64 with 16-32 warps per SM 36.6-37.0 TFLOP/s; SIMT DFMA 34.6;
+# DMMA + DFMA together 36.1 (one FP64 pipe). (Round 1's 73.9 counted each
+# m16n8k4 twice.)
+FP64_PEAK_TFLOPS = 37.0
+FP64_PEAK_SOURCE = ("measured: scripts/dmma_tput.cu, mma.sync.m16n8k4.f64 at 32 warps/SM "
+                    "(profiles/r2_summary.md)")
+DMMA_PEAK_TFLOPS = FP64_PEAK_TFLOPS
 
 
 def peaks():
@@ -1006,9 +1013,15 @@ def run_c5(args, ctx, world, rank, local):
     # engine, ~95 % of the step), canonical algorithmic bytes per iteration
     # n (40 + 80 s) over the device time of the solve
     bytes_iter = n * (40 + 80 * s)
+    # algorithmic FP64 flops per cell and iteration: R, P, X updates (3 x 2 s^2),
+    # the two symmetric Grams P^T W and R^T Z (2 x s (s + 1)), the 7-point
+    # stencil (14 s); 141.7 GFLOP per iteration at C5 — above the machine
+    # balance (FP64 37.0 TFLOP/s vs 6.5 TB/s), so the iteration is FP64-bound
+    flops_iter = n * (6 * s * s + 2 * s * (s + 1) + 14 * s)
     mi = float(np.mean(iters))
     solve_mean = max_over_ranks(float(np.mean(solve_s)), dev)
     achieved = mi * bytes_iter / solve_mean / 1e9
+    achieved_tf = mi * flops_iter / solve_mean / 1e12
     ph = recs[-1][2]
     spmm = None
     if world == 1 and ph["spmm"]["launches"]:
@@ -1016,7 +1029,8 @@ def run_c5(args, ctx, world, rank, local):
         # {diag, cx, cy, cz} (32 B/cell), writes W (8 s B/cell)
         sb = n * (32 + 16 * s)
         sm = ph["spmm"]["ms"] / ph["spmm"]["launches"] * 1e-3
-        spmm = {"kernel": "k_spmm_gram_tma64 (W = A P, G = P^T W)", "achieved_GBps": sb / sm / 1e9,
+        spmm = {"kernel": "k_spmm64_ws (W = A P, G = P^T W; z-marching, warp-specialised)",
+                "achieved_GBps": sb / sm / 1e9,
                 "peak_GBps": peak, "frac": sb / sm / 1e9 / peak, "ms_per_launch": sm * 1e3,
                 "algorithmic_bytes_per_launch": int(sb),
                 "traffic": ncu_traffic("config5_spmm")}
@@ -1067,14 +1081,19 @@ def run_c5(args, ctx, world, rank, local):
         "data": "synthetic (seeded BASELINE-config generators, DESIGN.md §3)",
         "config": config_dict(5, world),
         "converged": conv, "iterations_per_solve": mi,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic("config5_iter"),
+        "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": achieved_tf / FP64_PEAK_TFLOPS,
+                     "traffic": ncu_traffic("config5_iter"),
                      "traffic_unit": "DRAM bytes per iteration (ncu, sum of the sweep kernels)",
-                     "kernel": "block-CG solve, multi-kernel engine (S = 64): one iteration = "
-                               "stencil-SpMM + Gram, R update + S_new, P (+ X) update",
+                     "kernel": "block-CG iteration, multi-kernel engine (S = 64): k_spmm64_ws "
+                               "(stencil-SpMM + Gram), k_update64_ws (R update + S_new), "
+                               "k_pupdate64_ws (P + deferred X update), reductions, s x s solves",
+                     "algorithmic_flops_per_iter": int(flops_iter),
                      "algorithmic_bytes_per_iter": int(bytes_iter),
                      "iterations_per_solve": mi, "solve_ms": solve_mean * 1e3,
-                     "peak_source": peak_kind,
+                     "peak_source": FP64_PEAK_SOURCE,
+                     "hbm_view": {"achieved": achieved, "peak": peak, "unit": "GB/s",
+                                  "frac": achieved / peak, "peak_source": peak_kind},
                      "phases_last_solve": phases},
         "spmm": spmm,
         "action": action_roofline(n, s, N // world, float(np.mean(act_s)), peak),

@@ -65,6 +65,51 @@ __global__ void k_tput(double* out, int n) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// half the warps run DMMA chains, half DFMA chains (8 independent per
+// thread): do the FP64 tensor pipe and the SIMT FP64 pipe run concurrently?
+__global__ void k_mixed(double* out, int n, int mode) {
+    const int warp = threadIdx.x >> 5;
+    const bool do_mma = mode == 0 || (mode == 2 && (warp & 1) == 0);
+    const bool do_fma = mode == 1 || (mode == 2 && (warp & 1) == 1);
+    double d[4][4];
+    for (int c = 0; c < 4; ++c)
+        for (int e = 0; e < 4; ++e) d[c][e] = threadIdx.x * 1e-3 + c;
+    double f[8];
+    for (int c = 0; c < 8; ++c) f[c] = threadIdx.x * 1e-3 + c;
+    const double a[2] = {1.0000001, 0.9999999}, b[1] = {1.0000002};
+    if (do_mma)
+        for (int it = 0; it < n; ++it)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) Mma<4>::run(d[c], a, b);
+    if (do_fma)
+        for (int it = 0; it < 4 * n; ++it)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) f[c] = fma(f[c], 1.0000001, 1e-9);
+    double s = 0;
+    for (int c = 0; c < 4; ++c) s += d[c][0] + d[c][3];
+    for (int c = 0; c < 8; ++c) s += f[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+void run_mixed(int mode, double* out) {
+    const int n = 2000, blocks = 148 * 2, threads = 512;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_mixed<<<blocks, threads>>>(out, 10, mode);
+    cudaEventRecord(e0);
+    k_mixed<<<blocks, threads>>>(out, n, mode);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double wm = mode == 0 ? 16 : mode == 2 ? 8 : 0, wf = mode == 1 ? 16 : mode == 2 ? 8 : 0;
+    const double mma = 2.0 * 16 * 8 * 4 * 4 * (double)n * wm * blocks;
+    const double fmaf = 2.0 * 32 * 8 * 4.0 * n * wf * blocks;
+    printf("mixed mode %d (0 dmma, 1 dfma, 2 both): %.2f ms  dmma %.1f + dfma %.1f = %.1f TFLOP/s\n",
+           mode, ms, mma / ms / 1e9, fmaf / ms / 1e9, (mma + fmaf) / ms / 1e9);
+}
+
 template <int K, int CH, bool SMEM>
 void run(int warps, double* out) {
     const int n = 2000;
@@ -98,6 +143,9 @@ int main() {
         run<8, 4, true>(w, out);
         run<16, 4, true>(w, out);
     }
+    run_mixed(0, out);
+    run_mixed(1, out);
+    run_mixed(2, out);
     run<4, 1, false>(16, out);
     run<4, 2, false>(16, out);
     return 0;
