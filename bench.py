@@ -133,7 +133,8 @@ def config_dict(config, world, chips=1):
         d["output_ring_samples"] = C5_RING
         d["l2"] = ("inputs larger than L2: every block vector is 2.1 GB (4.2 M cells x 64 x 8 B) "
                    "vs the 126 MB L2, and each step streams 5000 x 4.2 M x 16 B of outputs")
-        d["parallelism"] = (f"y-slab DD x{world} (NCCL Gram all-reduce + halo rows), samples split"
+        d["parallelism"] = (f"y-slab DD x{world} (NCCL Gram all-reduce + halo rows); each rank "
+                            f"forms all samples on its slab after one X-halo exchange"
                             if world > 1 else "single GPU")
     return d
 
@@ -944,16 +945,19 @@ def run_c5(args, ctx, world, rank, local):
     n = inp.grid.cell_count()
     k = torch.from_numpy(inp.k).to(dev)
     qb = torch.from_numpy(inp.q_basis).to(dev)
-    lo, hi = rank * N // world, (rank + 1) * N // world
-    coef = [torch.from_numpy(np.ascontiguousarray(inp.coef[:, j:min(j + C5_RING, hi)])).to(dev)
-            for j in range(lo, hi, C5_RING)]
+    # every rank forms all N samples: on the whole chip (N = 1) or on its own
+    # y-slab after one X-halo exchange (N > 1, no gather of X)
+    coef = [torch.from_numpy(np.ascontiguousarray(inp.coef[:, j:min(j + C5_RING, N)])).to(dev)
+            for j in range(0, N, C5_RING)]
+    parts = dd.partition_rows(ny, world)
+    y0, nyl = parts[rank]
+    n_out = n if world == 1 else nx * nyl * nz
     B = torch.empty_like(qb)
     X = torch.empty_like(qb)
-    T = torch.empty((C5_RING, n), dtype=torch.float64, device=dev)
+    T = torch.empty((C5_RING, n_out), dtype=torch.float64, device=dev)
     Q = torch.empty_like(T)
     R = torch.empty(C5_RING, dtype=torch.float64, device=dev)
     cfg = bk.SolverConfig(TOL_BY_CONFIG[5], 100000, "jacobi")
-    parts = dd.partition_rows(ny, world)
     ctx.set_option("phase_timing", 1)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
@@ -965,19 +969,19 @@ def run_c5(args, ctx, world, rank, local):
         e[1].record(stream)
         if world == 1:
             rep = bk.block_cg(op, B, cfg, out=X).report
+            e[2].record(stream)
+            for c in coef:
+                m = int(c.shape[1])
+                bk.combine_action(op, X, c, t_out=T[:m], q_out=Q[:m], resid_out=R[:m])
         else:
-            import torch.distributed as dist
-            y0, nyl = parts[rank]
             slab = dd.Slab(bk, ctx, op, y0, nyl, 64).allocate()
             slab.load_rhs(B)
-            rep = dd.dd_block_cg([slab], dd.TorchComm(), cfg)
-            X.zero_()
-            slab.store_x(X)
-            dist.all_reduce(X)  # disjoint slabs: sum == all-gather
-        e[2].record(stream)
-        for c in coef:
-            m = int(c.shape[1])
-            bk.combine_action(op, X, c, t_out=T[:m], q_out=Q[:m], resid_out=R[:m])
+            comm = dd.TorchComm()
+            rep = dd.dd_block_cg([slab], comm, cfg)
+            e[2].record(stream)
+            for i, c in enumerate(coef):
+                m = int(c.shape[1])
+                dd.slab_outputs([slab], comm, c, [T[:m]], [Q[:m]], [R[:m]], halo=i == 0)
         e[3].record(stream)
         return rep, e, ctx.last_solve_phases()
 
@@ -1096,7 +1100,7 @@ def run_c5(args, ctx, world, rank, local):
                                   "frac": achieved / peak, "peak_source": peak_kind},
                      "phases_last_solve": phases},
         "spmm": spmm,
-        "action": action_roofline(n, s, N // world, float(np.mean(act_s)), peak),
+        "action": action_roofline(n // world, s, N, float(np.mean(act_s)), peak),
         "e2e": e2e,
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),

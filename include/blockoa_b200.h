@@ -304,6 +304,20 @@ bk_status bk_dd_step(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, int S,
 bk_status bk_dd_pack(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, int S, double* glob,
                      double* loc, int to_local);
 
+/* Slab-local combination + operator action after the decomposed solve: each
+ * rank forms T_j = X C_j and q_j = (A T_j - g)/V for ALL samples j on its own
+ * rows [y0, y0 + nyl) (pipeline.cpp:187-251), from its slab of X in the
+ * ghost-row layout with the ghost rows refreshed once (the neighbours' edge
+ * rows: one X-halo exchange instead of gathering X). Tloc / Qloc: N x
+ * (nx nyl nz) sample-major, slab-local flat index ix + nx (iyl + nyl iz).
+ * nd (N x 2, may be NULL): this rank's per-sample (num, den) partials of the
+ * residual of pipeline.cpp:548-571; sum them across ranks and call
+ * bk_dd_resid_from_nd. Device pointers; 3D grids (nz > 1). */
+bk_status bk_dd_combine_action(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, int S,
+                               const double* Xloc, int s, const double* C, int64_t N,
+                               double* Tloc, double* Qloc, double* nd);
+bk_status bk_dd_resid_from_nd(bk_ctx* ctx, const double* nd, int64_t N, double* resid);
+
 /* cg_error_bound(kappa, m, e0)    solvers.hpp:92, solvers.cpp:672-680 (host). */
 bk_status bk_cg_error_bound(double kappa, int m, double e0, double* out);
 

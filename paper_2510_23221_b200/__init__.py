@@ -198,6 +198,9 @@ def _load():
         lib.bk_dd_step.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.c_int,
                                    vp, vp, vp]
         lib.bk_dd_pack.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int]
+        lib.bk_dd_combine_action.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp,
+                                             C.c_int64, vp, vp, vp]
+        lib.bk_dd_resid_from_nd.argtypes = [vp, vp, C.c_int64, vp]
         lib.bk_cg_error_bound.argtypes = [C.c_double, C.c_int, C.c_double, C.POINTER(C.c_double)]
         lib.bk_derive_seed.argtypes = [C.c_uint64, C.c_char_p, C.c_uint64]
         lib.bk_derive_seed.restype = C.c_uint64

@@ -1141,6 +1141,37 @@ bk_status bk_combine_action(bk_ctx* ctx, const bk_operator* op, const double* X,
     return BK_OK;
 }
 
+bk_status bk_dd_combine_action(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, int S,
+                               const double* Xloc, int s, const double* C, int64_t N,
+                               double* Tloc, double* Qloc, double* nd) {
+    if (!ctx || !op || !Xloc || !C) return BK_INVALID_CONFIG;
+    if (s < 1 || s > S || (S != 8 && S != 16 && S != 32 && S != 64))
+        return fail(ctx, BK_INVALID_CONFIG, "dd_combine_action: bad widths");
+    if (op->nz < 2) return fail(ctx, BK_INVALID_CONFIG, "dd_combine_action: slabs need nz > 1");
+    if (y0 < 0 || nyl < 1 || y0 + nyl > op->ny)
+        return fail(ctx, BK_DIMENSION_MISMATCH, "dd_combine_action: slab outside the grid");
+    if (N < 0) return fail(ctx, BK_DIMENSION_MISMATCH, "dd_combine_action: negative sample count");
+    for (const void* p : {(const void*)Xloc, (const void*)C, (const void*)Tloc, (const void*)Qloc,
+                          (const void*)nd})
+        if (p && !is_device_ptr(p))
+            return fail(ctx, BK_INVALID_CONFIG, "dd_combine_action: device pointers only");
+    cudaSetDevice(ctx->device);
+    if (N == 0) return BK_OK;
+    ActExtra ex;
+    ex.slab_y0 = y0;
+    ex.slab_ny = nyl;
+    ex.nd_out = nd != nullptr;
+    return combine_action_device(ctx, op, Xloc, S, s, C, N, N, Tloc, Qloc, nd, ex);
+}
+
+bk_status bk_dd_resid_from_nd(bk_ctx* ctx, const double* nd, int64_t N, double* resid) {
+    if (!ctx || !nd || !resid) return BK_INVALID_CONFIG;
+    cudaSetDevice(ctx->device);
+    BK_CUDA_TRY(ctx, launch_resid_from_nd(ctx->stream, nd, N, resid));
+    ++ctx->launches;
+    return BK_OK;
+}
+
 bk_status bk_generate_chip(bk_ctx* ctx, const bk_grid* grid, const double* k, const bk_face bc[6],
                            const double* Qbasis, int s, const double* C, int64_t N,
                            const bk_solver_cfg* cfg, double* T, double* Q, double* resid,

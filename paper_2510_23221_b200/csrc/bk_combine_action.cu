@@ -95,6 +95,11 @@ struct ActArgs {
     int64_t ldo;
     const double* eps;  // N x ldo (nullable)
     int fma;            // 1: apply_block's fused chain, 0: scalar apply's mul + add
+    // slab of the y-slab decomposition: local rows 0 .. ny - 1 are global rows
+    // cy0 .. cy0 + ny - 1 of a grid with cny rows (coefficients and boundary
+    // tests use global rows; outputs are slab-local); X carries one ghost row
+    // per side, so the tensor map's y coordinate is shifted by ty = 1
+    int cy0, cny, ty;
 };
 
 // correctly rounded x / v given r = RN(1/v) (one Newton-style correction).
@@ -151,15 +156,16 @@ struct Coef {
     double gi, di, zm, ym, xm, xp, yp, zp;
 };
 __device__ __forceinline__ void load_coef(const ActArgs& a, int gx, int gy, int z, Coef& k) {
-    const int64_t plane = (int64_t)a.nx * a.ny;
-    const int64_t i = gx + (int64_t)a.nx * gy + plane * z;
+    const int gyg = gy + a.cy0;  // global row
+    const int64_t plane = (int64_t)a.nx * a.cny;
+    const int64_t i = gx + (int64_t)a.nx * gyg + plane * z;
     k.gi = a.g[i];
     k.di = a.diag[i];
     k.zm = z > 0 ? -a.cz[i - plane] : 0.0;
-    k.ym = gy > 0 ? -a.cy[i - a.nx] : 0.0;
+    k.ym = gyg > 0 ? -a.cy[i - a.nx] : 0.0;
     k.xm = gx > 0 ? -a.cx[i - 1] : 0.0;
     k.xp = gx < a.nx - 1 ? -a.cx[i] : 0.0;
-    k.yp = gy < a.ny - 1 ? -a.cy[i] : 0.0;
+    k.yp = gyg < a.cny - 1 ? -a.cy[i] : 0.0;
     k.zp = z < a.nz - 1 ? -a.cz[i] : 0.0;
 }
 
@@ -213,7 +219,7 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
         const int tile = p_item / a.chunks;
         const int x0 = (tile % a.tilesx) * TX, y0 = (tile / a.tilesx) * TY;
         mbar_expect_tx(&bar[p_slot], P::BYTES);
-        tma_load_4d(panels + p_slot * P::SLOT, &tmx, p_r * P::PW, x0 - 1, y0 - 1, p_z,
+        tma_load_4d(panels + p_slot * P::SLOT, &tmx, p_r * P::PW, x0 - 1, y0 - 1 + a.ty, p_z,
                     &bar[p_slot]);
         p_slot = p_slot + 1 == NP ? 0 : p_slot + 1;
         if (++p_r == P::R) {
@@ -605,7 +611,20 @@ __global__ void resid_finalize(const double* __restrict__ part, int tiles, int64
         nu += __shfl_xor_sync(0xffffffffu, nu, o);
         de += __shfl_xor_sync(0xffffffffu, de, o);
     }
-    if (lane == 0) resid[j * rstride] = de == 0.0 ? (nu == 0.0 ? 0.0 : 1.0) : sqrt(nu / de);
+    if (lane == 0) {
+        if (rstride < 0)  // slab partial: (num, den) of this rank, summed across ranks later
+            reinterpret_cast<double2*>(resid)[j] = make_double2(nu, de);
+        else
+            resid[j * rstride] = de == 0.0 ? (nu == 0.0 ? 0.0 : 1.0) : sqrt(nu / de);
+    }
+}
+
+// resid_j from the (num, den) sums of all ranks (pipeline.cpp:568-571)
+__global__ void resid_from_nd(const double2* __restrict__ nd, int64_t N, double* __restrict__ resid) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    const double nu = nd[j].x, de = nd[j].y;
+    resid[j] = de == 0.0 ? (nu == 0.0 ? 0.0 : 1.0) : sqrt(nu / de);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -631,9 +650,13 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
     using SH = Shape<NS, NT>;
     ActArgs a;
     a.nx = op->nx;
-    a.ny = op->ny;
+    const bool slab = ex.slab_ny > 0;
+    a.ny = slab ? ex.slab_ny : op->ny;
     a.nz = op->nz;
-    a.n = op->n;
+    a.n = (int64_t)a.nx * a.ny * a.nz;
+    a.cy0 = slab ? ex.slab_y0 : 0;
+    a.cny = op->ny;
+    a.ty = slab ? 1 : 0;
     a.N = N;
     a.ldc = ldc;
     a.diag = op->diag;
@@ -646,11 +669,11 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
     a.T = T;
     a.Q = Q;
     a.s = s;
-    a.ldo = ex.ldo > 0 ? ex.ldo : op->n;
+    a.ldo = ex.ldo > 0 ? ex.ldo : a.n;
     a.eps = ex.eps;
     a.fma = ex.fma;
     a.tilesx = (op->nx + TX - 1) / TX;
-    a.tiles = a.tilesx * ((op->ny + TY - 1) / TY);
+    a.tiles = a.tilesx * ((a.ny + TY - 1) / TY);
     const int64_t chunks = (N + NS - 1) / NS;
     if (chunks * a.tiles >= (int64_t)1 << 31)
         return fail(ctx, BK_INVALID_CONFIG, "combine_action: too many work items");
@@ -670,10 +693,13 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
     auto enc = encode_fn();
     if (!enc) return fail(ctx, BK_CUDA_ERROR, "combine_action: cuTensorMapEncodeTiled unavailable");
     CUtensorMap map;
-    const cuuint64_t dims[4] = {(cuuint64_t)S, (cuuint64_t)op->nx, (cuuint64_t)op->ny,
+    // (slab: the ghost-row layout nx x (ny + 2) x nz, ghost rows real
+    // neighbour data or zero at the physical boundary)
+    const int64_t nyt = slab ? a.ny + 2 : a.ny;
+    const cuuint64_t dims[4] = {(cuuint64_t)S, (cuuint64_t)op->nx, (cuuint64_t)nyt,
                                 (cuuint64_t)op->nz};
     const cuuint64_t strides[3] = {(cuuint64_t)S * 8, (cuuint64_t)S * 8 * op->nx,
-                                   (cuuint64_t)S * 8 * op->nx * op->ny};
+                                   (cuuint64_t)S * 8 * op->nx * nyt};
     const cuuint32_t box[4] = {(cuuint32_t)P::PW, (cuuint32_t)HX, (cuuint32_t)HY, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(X), dims,
@@ -706,8 +732,8 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
         fprintf(stderr, " reduce %lld\n", hp[3 + 2 * op->nz] - hp[2 + 2 * op->nz]);
     }
     if (resid) {
-        resid_finalize<<<(unsigned)((N + 7) / 8), 256, 0, ctx->stream>>>(a.part, a.tiles, N, resid,
-                                                                       ex.rstride > 0 ? ex.rstride : 1);
+        resid_finalize<<<(unsigned)((N + 7) / 8), 256, 0, ctx->stream>>>(
+            a.part, a.tiles, N, resid, ex.nd_out ? -1 : ex.rstride > 0 ? ex.rstride : 1);
         ++ctx->launches;
         BK_CUDA_TRY(ctx, cudaGetLastError());
     }
@@ -734,6 +760,13 @@ bk_status dispatch(bk_ctx* ctx, const bk_operator* op, const double* X, int s, c
 }  // namespace
 
 namespace bk {
+
+cudaError_t launch_resid_from_nd(cudaStream_t s, const double* nd, int64_t N, double* resid) {
+    if (N <= 0) return cudaSuccess;
+    resid_from_nd<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(
+        reinterpret_cast<const double2*>(nd), N, resid);
+    return cudaGetLastError();
+}
 
 // X is the kernel-width block n x S (zero-padded past the real width s); C is
 // s x N with row stride ldc.

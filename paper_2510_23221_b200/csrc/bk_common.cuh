@@ -250,7 +250,12 @@ struct ActExtra {
     int64_t rstride = 0;
     const double* eps = nullptr;
     int fma = 0;
+    // y-slab of the decomposition (slab_ny > 0): X in the ghost-row layout,
+    // outputs slab-local, `resid` receives per-sample (num, den) partials
+    int slab_y0 = 0, slab_ny = 0;
+    bool nd_out = false;
 };
+cudaError_t launch_resid_from_nd(cudaStream_t s, const double* nd, int64_t N, double* resid);
 bk_status combine_action_device(bk_ctx* ctx, const bk_operator* op, const double* X, int S,
                                 int s, const double* C, int64_t ldc, int64_t N, double* T,
                                 double* Q, double* resid, const ActExtra& ex = ActExtra{});

@@ -112,6 +112,29 @@ class Slab:
                                       C.c_void_p(X_global.data_ptr()),
                                       C.c_void_p(self.X.data_ptr()), 0), self.ctx.h, "dd_pack")
 
+    def load_x(self, X_global):
+        """Pack this slab's rows of a global n x S device block into X."""
+        lib = self.bk._load()
+        self.bk._raise(lib.bk_dd_pack(self.ctx.h, self.op.h, self.y0, self.nyl, self.S,
+                                      C.c_void_p(X_global.data_ptr()),
+                                      C.c_void_p(self.X.data_ptr()), 1), self.ctx.h, "dd_pack")
+
+    def combine_action(self, coef, T, Q, nd):
+        """Slab-local combine + operator action (bk_dd_combine_action) of every
+        sample in coef (s x N device tensor) on this slab's rows; X's ghost rows
+        must hold the neighbours' edge rows (one X halo exchange after the
+        solve). T, Q: N x (nx nyl nz) device; nd: N x 2 residual partials."""
+        lib = self.bk._load()
+        s, N = int(coef.shape[0]), int(coef.shape[1])
+        ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        self.bk._raise(lib.bk_dd_combine_action(self.ctx.h, self.op.h, self.y0, self.nyl, self.S,
+                                                C.c_void_p(self.X.data_ptr()), s, ptr(coef), N,
+                                                ptr(T), ptr(Q), ptr(nd)),
+                       self.ctx.h, "dd_combine_action")
+
+    def cells(self) -> int:
+        return self.op.grid.nx * self.nyl * self.op.grid.nz
+
     def step(self, kind, cfg_c, m=0, report=None):
         lib = self.bk._load()
         cmd, sa = C.c_int(-1), C.c_int(-1)
@@ -129,6 +152,14 @@ def _red_count(kind: int, S: int) -> int:
 
 class LocalComm:
     """Virtual ranks in one process (one GPU): fixed-order sums and device copies."""
+
+    def sum(self, tensors):
+        """Sum one tensor per slab in slab order; every slab gets the total."""
+        total = tensors[0].clone()
+        for t in tensors[1:]:
+            total += t
+        for t in tensors:
+            t.copy_(total)
 
     def allreduce(self, slabs, count):
         total = slabs[0].red[:count].clone()
@@ -161,6 +192,10 @@ class TorchComm:
         (sl,) = slabs
         buf = sl.red[:count]
         self.dist.all_reduce(buf, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def sum(self, tensors):
+        (t,) = tensors
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
 
     def halo(self, slabs, name):
         (sl,) = slabs
@@ -278,3 +313,28 @@ def solve_decomposed(bk, ctx, op, B_global, cfg, parts, comm=None, X_global=None
     for sl in slabs:
         sl.store_x(X_global)
     return X_global, rep
+
+
+def slab_outputs(slabs, comm, coef, T, Q, resid, halo=True):
+    """After the decomposed solve: ONE halo exchange of X's edge rows, then
+    every slab forms all samples of coef on its own rows (no gather of X);
+    the per-sample residual partials are summed across slabs (N x 2 doubles)
+    and finished on each rank. T, Q, resid: one tensor per slab (T[i], Q[i]:
+    N x slab cells; resid[i]: N, identical on every slab afterwards)."""
+    import torch
+
+    if halo:  # once per solve; later sample chunks reuse the ghost rows
+        comm.halo(slabs, "X")
+    N = int(coef.shape[1])
+    nds = []
+    for sl, t, q in zip(slabs, T, Q):
+        nd = torch.zeros((N, 2), dtype=torch.float64, device=t.device)
+        sl.combine_action(coef, t, q, nd)
+        nds.append(nd)
+    comm.sum(nds)
+    lib = slabs[0].bk._load()
+    for sl, nd, r in zip(slabs, nds, resid):
+        slabs[0].bk._raise(lib.bk_dd_resid_from_nd(sl.ctx.h, C.c_void_p(nd.data_ptr()), N,
+                                                   C.c_void_p(r.data_ptr())), sl.ctx.h,
+                           "dd_resid_from_nd")
+

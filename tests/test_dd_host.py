@@ -44,7 +44,10 @@ def _worker(rank, world, port, q):
     sl = _S()
     sl.red = torch.arange(6, dtype=torch.float64) * (rank + 1)
     TorchComm().allreduce([sl], 4)
-    q.put((rank, y0, nyl, v.numpy().copy(), sl.red.numpy().copy()))
+    # per-sample residual partials (num, den) of the slab-local outputs
+    nd = torch.tensor([[1.0 + rank, 2.0 * (rank + 1)], [0.5, 0.25]], dtype=torch.float64)
+    TorchComm().sum([nd])
+    q.put((rank, y0, nyl, v.numpy().copy(), sl.red.numpy().copy(), nd.numpy().copy()))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -61,7 +64,8 @@ def test_halo_and_allreduce_two_ranks():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, y0, nyl, v, red in out:
+    for rank, y0, nyl, v, red, nd in out:
+        assert nd.tolist() == [[3.0, 6.0], [1.0, 0.5]]
         nz, _, nx, S = v.shape
         # ghost row 0 holds global row y0-1 (or stays -1 at the domain edge)
         for iz in range(nz):

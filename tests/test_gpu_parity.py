@@ -580,3 +580,48 @@ def test_generate_from_device_synthesis(bk, ctx):
     torch.cuda.synchronize()
     assert repd.all_converged()
     assert rel_l2(Td.cpu().numpy(), Th) <= PARITY and rel_l2(Qd.cpu().numpy(), Qh) <= PARITY
+
+
+@pytest.mark.parametrize("case,nslabs", [((5, 48, 40, 16, 64, 21), 1), ((5, 48, 40, 16, 64, 21), 3),
+                                         ((3, 32, 24, 8, 32, 11), 2)])
+def test_slab_local_combine_matches_global(bk, ctx, case, nslabs):
+    """Config-5 multi-GPU outputs without gathering X: one X-halo exchange, then
+    every slab forms all samples on its own rows (bk_dd_combine_action). Given
+    the same X, each slab's T and q are bitwise the global kernel's rows; the
+    per-sample residual from the summed (num, den) partials matches."""
+    import torch
+
+    from paper_2510_23221_b200 import dd
+
+    inp = bk.synth_chip(*case)
+    g = inp.grid
+    op = bk.assemble(inp.k, g, inp.bc, ctx)
+    dev = torch.device("cuda", 0)
+    S = case[4]
+    q = torch.from_numpy(inp.q_basis).to(dev)
+    B = torch.empty_like(q)
+    bk.rhs_from_power(op, q, out=B)
+    X = torch.empty_like(q)
+    bk.block_cg(op, B, cfg_jacobi(60), out=X)
+    coef = torch.from_numpy(inp.coef).to(dev)
+    N, n = inp.coef.shape[1], g.cell_count()
+    T = torch.empty((N, n), dtype=torch.float64, device=dev)
+    Q, R = torch.empty_like(T), torch.empty(N, dtype=torch.float64, device=dev)
+    bk.combine_action(op, X, coef, t_out=T, q_out=Q, resid_out=R)
+    slabs = dd.make_slabs(bk, ctx, op, S, dd.partition_rows(g.ny, nslabs))
+    for sl in slabs:
+        sl.load_x(X)
+    Tl = [torch.full((N, sl.cells()), float("nan"), dtype=torch.float64, device=dev) for sl in slabs]
+    Ql = [torch.full_like(t, float("nan")) for t in Tl]
+    Rl = [torch.empty(N, dtype=torch.float64, device=dev) for _ in slabs]
+    dd.slab_outputs(slabs, dd.LocalComm(), coef, Tl, Ql, Rl)
+    torch.cuda.synchronize()
+    Tg = T.cpu().numpy().reshape(N, g.nz, g.ny, g.nx)
+    Qg = Q.cpu().numpy().reshape(N, g.nz, g.ny, g.nx)
+    for sl, t, qq, r in zip(slabs, Tl, Ql, Rl):
+        ts = t.cpu().numpy().reshape(N, g.nz, sl.nyl, g.nx)
+        qs = qq.cpu().numpy().reshape(N, g.nz, sl.nyl, g.nx)
+        assert np.array_equal(ts, Tg[:, :, sl.y0:sl.y0 + sl.nyl, :])
+        assert np.array_equal(qs, Qg[:, :, sl.y0:sl.y0 + sl.nyl, :])
+        rr, RR = r.cpu().numpy(), R.cpu().numpy()
+        assert np.max(np.abs(rr - RR) / np.maximum(RR, 1e-300)) <= 1e-12
