@@ -958,7 +958,9 @@ def run_c5(args, ctx, world, rank, local):
     Q = torch.empty_like(T)
     R = torch.empty(C5_RING, dtype=torch.float64, device=dev)
     cfg = bk.SolverConfig(TOL_BY_CONFIG[5], 100000, "jacobi")
-    ctx.set_option("phase_timing", 1)
+    # per-sweep event pairs cost ~0.3 ms per iteration (5 %): the timed steps
+    # run without them, one extra untimed solve gives the phase breakdown
+    ctx.set_option("phase_timing", 0)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def step():
@@ -983,7 +985,7 @@ def run_c5(args, ctx, world, rank, local):
                 m = int(c.shape[1])
                 dd.slab_outputs([slab], comm, c, [T[:m]], [Q[:m]], [R[:m]], halo=i == 0)
         e[3].record(stream)
-        return rep, e, ctx.last_solve_phases()
+        return rep, e
 
     for _ in range(args.warmup):
         step()
@@ -1026,7 +1028,13 @@ def run_c5(args, ctx, world, rank, local):
     solve_mean = max_over_ranks(float(np.mean(solve_s)), dev)
     achieved = mi * bytes_iter / solve_mean / 1e9
     achieved_tf = mi * flops_iter / solve_mean / 1e12
-    ph = recs[-1][2]
+    ph = None
+    if world == 1:
+        with ctx.options(phase_timing=1):
+            op = bk.assemble(k, inp.grid, inp.bc, ctx)
+            bk.rhs_from_power(op, qb, out=B)
+            bk.block_cg(op, B, cfg, out=X)
+            ph = ctx.last_solve_phases()
     spmm = None
     if world == 1 and ph["spmm"]["launches"]:
         # stencil-SpMM + Gram sweep: reads P (8 s B/cell) and the stencil
@@ -1038,8 +1046,8 @@ def run_c5(args, ctx, world, rank, local):
                 "peak_GBps": peak, "frac": sb / sm / 1e9 / peak, "ms_per_launch": sm * 1e3,
                 "algorithmic_bytes_per_launch": int(sb),
                 "traffic": ncu_traffic("config5_spmm")}
-    phases = {k: dict(v, ms_per_launch=(v["ms"] / v["launches"] if v["launches"] else None))
-              for k, v in ph.items()}
+    phases = ({k: dict(v, ms_per_launch=(v["ms"] / v["launches"] if v["launches"] else None))
+               for k, v in ph.items()} if ph else None)
 
     # e2e: the public streaming API with pinned host inputs; every sample of
     # every chip goes D2H into pinned host memory inside the timed region
@@ -1098,7 +1106,8 @@ def run_c5(args, ctx, world, rank, local):
                      "peak_source": FP64_PEAK_SOURCE,
                      "hbm_view": {"achieved": achieved, "peak": peak, "unit": "GB/s",
                                   "frac": achieved / peak, "peak_source": peak_kind},
-                     "phases_last_solve": phases},
+                     "phases_last_solve": phases,
+                     "phases_note": "event pairs around each sweep, from one extra untimed solve"},
         "spmm": spmm,
         "action": action_roofline(n // world, s, N, float(np.mean(act_s)), peak),
         "e2e": e2e,

@@ -271,6 +271,7 @@ struct SweepArgs {
     const double* coef;  // S x (S + 4) (alpha or beta)
     const double* coef2; // alpha kept for the deferred X update (k_pupdate modes 1, 2)
     const int* act;      // per-column mask for masked sweeps
+    const int* gate;     // P updates inside the device-driven loop: run only if *gate == 0
     int precond;
 };
 
@@ -767,6 +768,7 @@ __global__ void __launch_bounds__(LBS, 2) k_pupdate(SweepArgs a) {
     const int ntiles = n_tiles(a.sl);
     const int ngroups = (ntiles + G_::TPB - 1) / G_::TPB;
     const bool jac = a.precond != 0;
+    if (a.gate && *a.gate != 0) return;  // graph loop: this iteration needs a verification
     double cf[KS], ca[KS];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
@@ -1049,10 +1051,16 @@ __global__ void __launch_bounds__(CBS) k_ctl_alpha(Ctl<S>* c, const double* red)
 // red = [S_new | rr]: per-column recurrence test (solvers.cpp:582-590); beta
 // (S_old^+ S_new) right away unless a true-residual verification is needed
 template <int S>
-__global__ void __launch_bounds__(CBS) k_ctl_update(Ctl<S>* c, const double* red, int m) {
+// m <= 0: the device-driven loop (iteration = c->iters + 1, and the loop's
+// while-condition is set to continue unless a verification is due or the
+// iteration cap is reached)
+__global__ void __launch_bounds__(CBS) k_ctl_update(Ctl<S>* c, const double* red, int m,
+                                                    cudaGraphConditionalHandle loop, int max_iter) {
     extern __shared__ __align__(16) unsigned char smraw_[];
     CSm<S>& sm = *reinterpret_cast<CSm<S>*>(smraw_);
     __shared__ int nver;
+    const bool graph = m <= 0;
+    if (graph) m = c->iters + 1;
     for (int e = threadIdx.x; e < S * S; e += CBS) c->snew[e] = red[e];
     if (threadIdx.x < S) {
         const int q = threadIdx.x;
@@ -1069,13 +1077,19 @@ __global__ void __launch_bounds__(CBS) k_ctl_update(Ctl<S>* c, const double* red
     }
     __syncthreads();
     if (nver > 0) {
-        if (threadIdx.x == 0) c->cmd = kCmdVerify;
+        if (threadIdx.x == 0) {
+            c->cmd = kCmdVerify;
+            if (graph) cudaGraphSetConditional(loop, 0);
+        }
         return;
     }
     ctl_index(c, sm);
     ctl_solve(c, sm, c->s_old, c->snew);  // beta
     for (int e = threadIdx.x; e < S * S; e += CBS) c->s_old[e] = c->snew[e];
-    if (threadIdx.x == 0) c->cmd = kCmdPupdate;
+    if (threadIdx.x == 0) {
+        c->cmd = kCmdPupdate;
+        if (graph) cudaGraphSetConditional(loop, m < max_iter ? 1u : 0u);
+    }
 }
 
 // red = true ||b - A x||^2 of the flagged columns: freeze converged columns
@@ -1167,7 +1181,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
                            double* Wloc, const bk_solver_cfg* cfg, CgReport* rep,
                            const LargeComm* comm) {
     Slab sl{op->nx, nyl, op->nz, op->ny, y0, (int64_t)op->nx * nyl * op->nz};
-    SweepArgs a;
+    SweepArgs a{};
     a.sl = sl;
     a.st = StencilPtr{op->diag, op->cx, op->cy, op->cz, op->dinv};
     a.B = Bloc;
@@ -1254,12 +1268,15 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     // reads the same P rows (one P read fewer per iteration; bitwise the same
     // X); a verification first applies the pending update (k_pupdate MODE 2)
     a.coef2 = ctl->akeep;
-    for (int m = 1; m <= cfg->max_iter && sa > 0; ++m) {
+    const bool ws = S == 64 && ws_spmm && ws_update;
+    const int nbs = ws_spmm && ctx->num_sms < nb ? ctx->num_sms : nb;
+    const int nbu = ws_update && ctx->num_sms < nb ? ctx->num_sms : nb;
+    // one iteration's sweeps up to and including the convergence test
+    // (m <= 0: inside the device-driven loop, see k_ctl_update)
+    auto sweeps = [&](int m, cudaGraphConditionalHandle loop) -> bk_status {
         halo(a.P);
         phase_mark(ctx, -1);
-        int nbs = nb;
-        if (S == 64 && ws_spmm) {
-            nbs = ctx->num_sms < nb ? ctx->num_sms : nb;
+        if (ws_spmm) {
             BK_CUDA_TRY(ctx, launch_spmm64_ws(a, nbs, s));
         } else {
             BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s, ctx->knobs.no_tma_spmm));
@@ -1270,9 +1287,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
         k_ctl_alpha<S><<<1, CBS, cs, s>>>(ctl, red);
         ++ctx->launches;
         phase_mark(ctx, -1);
-        int nbu = nb;
-        if (S == 64 && ws_update) {
-            nbu = ctx->num_sms < nb ? ctx->num_sms : nb;
+        if (ws_update) {
             BK_CUDA_TRY(ctx, launch_update64_ws(a, nloc_ws, nbu, s));
         } else {
             BK_CUDA_TRY(ctx, (launch_update<S, true>(a, nb, s)));
@@ -1280,37 +1295,126 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
         phase_mark(ctx, 1);
         ++ctx->launches;
         reduce(E, nbu);
-        k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, red, m);
+        k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, red, m, loop, cfg->max_iter);
         ++ctx->launches;
         BK_CUDA_TRY(ctx, cudaGetLastError());
-        if ((st = read_cmd(&cmd, &sa)) != BK_OK) return st;
-        bool x_done = false;
-        if (cmd == kCmdVerify) {
-            BK_CUDA_TRY(ctx, (launch_pupdate<S, 2>(a, nb, s)));
-            ++ctx->launches;
-            x_done = true;
-            halo(a.X);
-            true_res();
-            k_ctl_verify<S><<<1, CBS, cs, s>>>(ctl, red);
-            ++ctx->launches;
+        return BK_OK;
+    };
+    // the P update closing an iteration (X += P alpha deferred into it)
+    auto pupdate = [&]() -> bk_status {
+        phase_mark(ctx, -1);
+        if (ws_update)
+            BK_CUDA_TRY(ctx, launch_pupdate64_ws(a, nloc_ws, nbu, s));
+        else
+            BK_CUDA_TRY(ctx, (launch_pupdate<S, 1>(a, nb, s)));
+        phase_mark(ctx, 2);
+        ++ctx->launches;
+        return BK_OK;
+    };
+    // Device-driven loop (option graph_loop; single slab, no per-sweep event
+    // timing): the iteration is a CUDA graph body under a while-node;
+    // k_ctl_update clears the condition when a true-residual verification is
+    // due or max_iter is reached, and the body's P update is gated on the same
+    // control word, so the host only wakes up for verifications
+    // (solvers.cpp:582-634). Bitwise the host-driven loop. Not the default: on
+    // C5 the host-driven loop already hides its one control read per
+    // iteration behind the queued sweeps (5.96 vs 6.07 ms per iteration,
+    // scripts/c5_loop_ab.py).
+    cudaGraphExec_t gexec = nullptr;
+    int launches_per_iter = 0;
+    if (!comm && !ctx->knobs.phase_timing && ctx->knobs.graph_loop && sa > 0) {
+        cudaGraph_t g = nullptr;
+        cudaStream_t cap = nullptr;
+        cudaGraphConditionalHandle h;
+        cudaGraphNodeParams cp = {};
+        cudaGraphNode_t node;
+        bool ok = cudaGraphCreate(&g, 0) == cudaSuccess &&
+                  cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+        if (ok) {
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            ok = cudaGraphAddNode(&node, g, nullptr, 0, &cp) == cudaSuccess &&
+                 cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) == cudaSuccess;
+        }
+        if (ok) {
+            const cudaStream_t keep = s;
+            const int64_t l0 = ctx->launches;
+            s = cap;
+            ok = cudaStreamBeginCaptureToGraph(cap, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeRelaxed) == cudaSuccess;
+            bk_status bs = BK_OK;
+            if (ok) {
+                a.gate = &ctl->cmd;
+                bs = sweeps(0, h);
+                if (bs == BK_OK) bs = pupdate();
+                a.gate = nullptr;
+                cudaGraph_t body = nullptr;
+                ok = cudaStreamEndCapture(cap, &body) == cudaSuccess && bs == BK_OK;
+            }
+            s = keep;
+            launches_per_iter = (int)(ctx->launches - l0);
+            ctx->launches = l0;
+            ok = ok && cudaGraphInstantiate(&gexec, g, 0) == cudaSuccess;
+            if (bs != BK_OK) ok = false;
+        }
+        if (cap) cudaStreamDestroy(cap);
+        if (g) cudaGraphDestroy(g);
+        if (!ok) {
+            if (gexec) cudaGraphExecDestroy(gexec);
+            gexec = nullptr;
+            cudaGetLastError();
+            return fail(ctx, BK_INTERNAL, "block_cg: building the device-driven iteration loop failed");
+        }
+    }
+    struct GraphGuard {
+        cudaGraphExec_t& e;
+        ~GraphGuard() {
+            if (e) cudaGraphExecDestroy(e);
+        }
+    } gguard{gexec};
+    auto read_iters = [&](int* iters) -> bk_status {
+        return read_small(ctx, iters, &ctl->iters, sizeof(int));
+    };
+    int m = 0;  // iterations done
+    while (m < cfg->max_iter && sa > 0) {
+        if (gexec) {
+            BK_CUDA_TRY(ctx, cudaGraphLaunch(gexec, s));
+            int it = 0;
             if ((st = read_cmd(&cmd, &sa)) != BK_OK) return st;
-            if (cmd == kCmdDone) break;
-            if (cmd == kCmdRestart) {
-                k_anchor<S, kRestart><<<nb, LBS, swa, s>>>(a);
-                ++ctx->launches;
-                reduce(E, nb);
-                k_ctl_restart<S><<<1, CBS, 0, s>>>(ctl, red);
-                ++ctx->launches;
+            if ((st = read_iters(&it)) != BK_OK) return st;
+            ctx->launches += (int64_t)launches_per_iter * (it - m);
+            m = it;
+            if (cmd == kCmdPupdate) continue;  // iteration cap: the loop's last P update ran
+        } else {
+            ++m;
+            if ((st = sweeps(m, 0)) != BK_OK) return st;
+            if ((st = read_cmd(&cmd, &sa)) != BK_OK) return st;
+            if (cmd == kCmdPupdate) {
+                if ((st = pupdate()) != BK_OK) return st;
                 continue;
             }
         }
+        // cmd == kCmdVerify
+        BK_CUDA_TRY(ctx, (launch_pupdate<S, 2>(a, nb, s)));
+        ++ctx->launches;
+        halo(a.X);
+        true_res();
+        k_ctl_verify<S><<<1, CBS, cs, s>>>(ctl, red);
+        ++ctx->launches;
+        if ((st = read_cmd(&cmd, &sa)) != BK_OK) return st;
+        if (cmd == kCmdDone) break;
+        if (cmd == kCmdRestart) {
+            k_anchor<S, kRestart><<<nb, LBS, swa, s>>>(a);
+            ++ctx->launches;
+            reduce(E, nb);
+            k_ctl_restart<S><<<1, CBS, 0, s>>>(ctl, red);
+            ++ctx->launches;
+            continue;
+        }
         phase_mark(ctx, -1);
-        if (x_done)
-            BK_CUDA_TRY(ctx, (launch_pupdate<S, 0>(a, nb, s)));
-        else if (S == 64 && ws_update)
-            BK_CUDA_TRY(ctx, launch_pupdate64_ws(a, nloc_ws, ctx->num_sms < nb ? ctx->num_sms : nb, s));
-        else
-            BK_CUDA_TRY(ctx, (launch_pupdate<S, 1>(a, nb, s)));
+        BK_CUDA_TRY(ctx, (launch_pupdate<S, 0>(a, nb, s)));
         phase_mark(ctx, 2);
         ++ctx->launches;
     }
@@ -1390,7 +1494,7 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
                     bk_solve_report* report) {
     using namespace bk;
     Slab sl{op->nx, nyl, op->nz, op->ny, y0, (int64_t)op->nx * nyl * op->nz};
-    SweepArgs a;
+    SweepArgs a{};
     a.sl = sl;
     a.st = StencilPtr{op->diag, op->cx, op->cy, op->cz, op->dinv};
     a.B = b->B;
@@ -1450,7 +1554,7 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
             break;
         case BK_DD_CTL_UPDATE:
             BK_CUDA_TRY(ctx, set((const void*)k_ctl_update<S>, cs));
-            k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, b->red, m);
+            k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, b->red, m, 0, 0);
             ++ctx->launches;
             break;
         case BK_DD_TRUE_RES:

@@ -37,6 +37,7 @@ struct bk_knobs {
     bool phase_timing = false; // per-kernel-kind event timing of the multi-kernel solve
     bool no_ws_update = false; // S = 64: the cp.async update sweeps instead of the warp-specialised ones
     bool no_ws_spmm = false;   // S = 64: the per-run TMA stencil sweep instead of the z-marching one
+    bool graph_loop = false;   // multi-kernel solve: device-driven iterations (CUDA graph while-loop)
 };
 
 // Optional per-kernel-kind timing of the multi-kernel solve (option

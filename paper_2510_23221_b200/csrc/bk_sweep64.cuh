@@ -335,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ntiles = n_tiles(a.sl);
     const int nteams = gridDim.x * kTeams;
     const bool jac = a.precond != 0;
+    if (a.gate && *a.gate != 0) return;  // graph loop: a verification is due
     for (int e = threadIdx.x; e < S * S; e += blockDim.x) {
         sm.beta[alpha_at(e / S, e % S)] = a.coef[(e / S) * (S + 4) + e % S];
         sm.alpha[alpha_at(e / S, e % S)] = a.coef2[(e / S) * (S + 4) + e % S];

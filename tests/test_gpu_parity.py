@@ -505,6 +505,29 @@ def test_block_cg_multikernel_path_vs_oracle(bk, ctx, oracle, case):
             assert rel_l2(rm.x, Xm) <= 1e-12
 
 
+@pytest.mark.parametrize("case", [(5, 48, 40, 16, 64), (3, 16, 16, 8, 32), (1, 32, 32, 1, 8)])
+def test_block_cg_graph_loop_bitwise(bk, ctx, oracle, case):
+    """Device-driven iterations (option graph_loop: the iteration as a CUDA
+    graph body under a while-node, verifications handed back to the host) give
+    bitwise the host-driven engine's X and report, full solve and capped."""
+    inp = bk.synth_chip(*case, 4)
+    op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
+    o = oracle.assemble(grid_tuple(inp.grid), inp.k, inp.bc.as_tuples(), dz=inp.grid.dz)
+    B = oracle.rhs_from_power(o, inp.q_basis)
+    for m in (1, 2, 7, 100000):
+        cfg = cfg_jacobi(m) if m < 100000 else cfg_jacobi()
+        with ctx.options(force_large=1):
+            h = bk.block_cg(op, B, cfg)
+        with ctx.options(force_large=1, graph_loop=1):
+            g = bk.block_cg(op, B, cfg)
+        assert np.array_equal(h.x, g.x), m
+        assert h.report.iterations == g.report.iterations
+        assert h.report.matvec_count == g.report.matvec_count
+        assert np.array_equal(h.report.final_rel_residual, g.report.final_rel_residual)
+    X, rep = oracle.block_cg(o, B, TOL, 100000, 1)
+    assert g.report.all_converged() and rel_l2(g.x, X) <= PARITY
+
+
 @pytest.mark.parametrize("nslabs", [1, 2, 3])
 def test_slab_decomposition_matches_single_gpu(bk, ctx, nslabs):
     """y-slab decomposition (config 5 structure: s = 64) with virtual ranks on
