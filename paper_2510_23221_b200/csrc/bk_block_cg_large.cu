@@ -1008,7 +1008,10 @@ __device__ void ctl_solve(Ctl<S>* c, CSm<S>& sm, const double* M, const double* 
         sm.m1[e] = RHS[e];
     }
     __syncthreads();
-    small_solve_t<S, CBS>(sm, sm.m0, sm.m1, sm.out);
+    if constexpr (S == 64)
+        small_solve_reg<S, CBS>(sm, sm.m0, sm.m1, sm.out);
+    else
+        small_solve_t<S, CBS>(sm, sm.m0, sm.m1, sm.out);
     for (int e = threadIdx.x; e < S * (S + 4); e += CBS) c->coef[e] = sm.out[e];
     __syncthreads();
 }
@@ -1621,7 +1624,79 @@ int64_t ctl_bytes_t() {
 
 }  // namespace
 
+// debug harness (scripts/ only): cycles of the S = 64 control solve in one
+// CTA of CBS threads, by the number of warps running the pivot loop
+template <int NWS>
+__device__ long long ctl_solve_cycles(CSm<64>& sm, const double* M, const double* R, int reps) {
+    __syncthreads();
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) small_solve_t<64, CBS, false, 0, NWS>(sm, M, R, sm.out);
+    __syncthreads();
+    return (clock64() - t0) / reps;
+}
+template <int VAR>
+__device__ long long reg_cycles(CSm<64>& sm, int reps) {
+    __syncthreads();
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) small_solve_reg<64, CBS, VAR>(sm, sm.m0, sm.m1, sm.out);
+    __syncthreads();
+    return (clock64() - t0) / reps;
+}
+__global__ void __launch_bounds__(CBS) k_ctl_solve_bench(int reps, long long* out, double* res) {
+    extern __shared__ __align__(16) unsigned char smraw_[];
+    CSm<64>& sm = *reinterpret_cast<CSm<64>*>(smraw_);
+    constexpr int S = 64;
+    for (int e = threadIdx.x; e < S * S; e += CBS) {
+        const int i = e / S, j = e % S;
+        sm.m0[e] = (i == j ? 1.0 : 0.01 / (1 + i + j)) * exp(-0.05 * (i + j));
+        sm.m1[e] = (i == j ? 2.0 : 0.1) * exp(-0.025 * (i + j));
+    }
+    if (threadIdx.x < S) sm.idx[threadIdx.x] = threadIdx.x;
+    if (threadIdx.x == 0) sm.sa = S;
+    __syncthreads();
+    long long c[5];
+    c[0] = ctl_solve_cycles<16>(sm, sm.m0, sm.m1, reps);
+    c[1] = ctl_solve_cycles<8>(sm, sm.m0, sm.m1, reps);
+    c[2] = ctl_solve_cycles<4>(sm, sm.m0, sm.m1, reps);
+    c[3] = ctl_solve_cycles<2>(sm, sm.m0, sm.m1, reps);
+    for (int e = threadIdx.x; e < S * S; e += CBS) res[e] = sm.out[(e / S) * Strides<S>::RS + e % S];
+    __syncthreads();
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) small_solve_reg<64, CBS>(sm, sm.m0, sm.m1, sm.out);
+    __syncthreads();
+    c[4] = (clock64() - t0) / reps;
+    if (threadIdx.x == 0) {
+        for (int v = 0; v < 5; ++v) out[v] = c[v];
+        out[5] = sm.rank;
+    }
+    for (int e = threadIdx.x; e < S * S; e += CBS)
+        res[S * S + e] = sm.out[(e / S) * Strides<S>::RS + e % S];
+    long long cv[4];
+    cv[0] = reg_cycles<1>(sm, reps);
+    cv[1] = reg_cycles<2>(sm, reps);
+    cv[2] = reg_cycles<3>(sm, reps);
+    cv[3] = reg_cycles<4>(sm, reps);
+    if (threadIdx.x == 0)
+        for (int v = 0; v < 4; ++v) out[6 + v] = cv[v];
+}
+
 extern "C" {
+
+int bk_debug_ctl_solve_cycles(int reps, long long* cycles6, double* coef2) {
+    long long* d;
+    double* r;
+    cudaMalloc(&d, 16 * 8);
+    cudaMalloc(&r, 2 * 64 * 64 * 8);
+    cudaFuncSetAttribute(k_ctl_solve_bench, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(CSm<64>));
+    k_ctl_solve_bench<<<1, CBS, sizeof(CSm<64>)>>>(reps, d, r);
+    const int err = (int)cudaDeviceSynchronize();
+    cudaMemcpy(cycles6, d, 10 * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(coef2, r, 2 * 64 * 64 * 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    cudaFree(r);
+    return err;
+}
 
 bk_status bk_dd_sizes(bk_ctx* ctx, const bk_operator* op, int nyl, int S, int64_t* local_elems,
                       int* nb, int64_t* part_elems, int64_t* red_elems, int64_t* ctl_bytes) {

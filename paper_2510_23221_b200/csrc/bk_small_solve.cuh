@@ -215,4 +215,158 @@ __device__ void small_solve_t(SMT& sm, const double* M, const double* RHS, doubl
 }
 
 
+// Register-resident variant for S = 64 and 512 threads (the multi-kernel
+// engine's control kernels): the same pivot sequence, rank cutoff and
+// per-element arithmetic as small_solve_t (bitwise the same result), but the
+// augmented [M | RHS] block lives in registers — warp w holds rows w + 16 a,
+// lane l columns l + 32 b (a, b < 4) — so a pivot step moves only the pivot
+// row and column through shared memory (published by their owners into a
+// double buffer) instead of streaming the whole block through shared memory
+// twice. One barrier per pivot; every warp tracks the Schur diagonal and finds
+// the next pivot redundantly, as small_solve_t.
+// VAR (timing experiments only): 1 no block update, 2 fixed pivot order,
+// 3 no barrier, 4 no reciprocal
+template <int S, int BS, int VAR = 0, class SMT>
+__device__ void small_solve_reg(SMT& sm, const double* M, const double* RHS, double* out) {
+    static_assert(S == 64 && BS == 512, "register layout: 16 warps x 4 rows, 32 lanes x 4 columns");
+    constexpr int RS = Strides<S>::RS;
+    constexpr int NR = 4, NC = 4;           // rows / columns per thread
+    constexpr int BUF = 2 * S + S;          // pivot row (2S) | pivot column (S)
+    const int sa = sm.sa;
+    double* const pbuf = sm.aug;            // 2 x BUF doubles
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double v[NR][NC];
+#pragma unroll
+    for (int a = 0; a < NR; ++a) {
+        const int i = warp + 16 * a;
+#pragma unroll
+        for (int b = 0; b < NC; ++b) {
+            const int q = lane + 32 * b;
+            double x = 0.0;
+            if (i < sa && q < 2 * sa) {
+                const int ai = sm.idx[i];
+                if (q < sa) {
+                    const int bq = sm.idx[q];
+                    x = ai <= bq ? M[ai * S + bq] : M[bq * S + ai];
+                } else {
+                    const int bq = sm.idx[q - sa];
+                    x = ai <= bq ? RHS[ai * S + bq] : RHS[bq * S + ai];
+                }
+            }
+            v[a][b] = x;
+        }
+    }
+    double dg[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int i = lane + 32 * r;
+        dg[r] = i < sa ? M[sm.idx[i] * S + sm.idx[i]] : 0.0;  // aug[i][i]
+    }
+    unsigned long long donem = 0ull;
+    auto search = [&](unsigned long long excl) -> unsigned long long {
+        unsigned long long key = 0ull;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int i = lane + 32 * r;
+            const unsigned long long kk = (i < sa && !((excl >> i) & 1ull)) ? pivot_key(dg[r], i) : 0ull;
+            key = kk > key ? kk : key;
+        }
+        return warp_max_u64(key);
+    };
+    auto pivot_of = [&](unsigned long long key, int& p, double& pv) {
+        p = key ? 63 - (int)(key & 63ull) : -1;
+        const int src = p < 0 ? 0 : (p & 31);
+        const double p0 = __shfl_sync(0xffffffffu, dg[0], src);
+        const double p1 = __shfl_sync(0xffffffffu, dg[1], src);
+        pv = p < 0 ? 0.0 : (p >= 32 ? p1 : p0);
+    };
+    // owners of row p / column p write them into buffer `buf`
+    auto publish = [&](int p, int buf) {
+        // (selects, not v[p >> 4][b]: keep v in registers)
+        double* rb = pbuf + buf * BUF;
+        if (warp == (p & 15)) {
+            const int a = p >> 4;
+#pragma unroll
+            for (int b = 0; b < NC; ++b)
+                rb[lane + 32 * b] = a == 0 ? v[0][b] : a == 1 ? v[1][b] : a == 2 ? v[2][b] : v[3][b];
+        }
+        if (lane == (p & 31)) {
+            const int b = p >> 5;
+#pragma unroll
+            for (int a = 0; a < NR; ++a)
+                rb[2 * S + warp + 16 * a] = b == 0 ? v[a][0] : b == 1 ? v[a][1] : b == 2 ? v[a][2] : v[a][3];
+        }
+    };
+    int p;
+    double pv;
+    const unsigned long long best = search(0ull);
+    pivot_of(best, p, pv);
+    const double cutoff = fmax(pv * sa * 2.220446049250313e-16, 2.2250738585072014e-308);
+    double rinv = __drcp_rn(pv);
+    int rank = 0, buf = 0;
+    if (p >= 0) publish(p, 0);
+    __syncthreads();
+    while (p >= 0 && pv > cutoff) {  // uniform
+        donem |= 1ull << p;
+        const double* rb = pbuf + buf * BUF;
+        double rowp[NC], colp[NR], dgc[2], dgr[2];
+#pragma unroll
+        for (int b = 0; b < NC; ++b) rowp[b] = rb[lane + 32 * b];
+#pragma unroll
+        for (int a = 0; a < NR; ++a) colp[a] = rb[2 * S + warp + 16 * a];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            dgc[r] = rb[2 * S + lane + 32 * r];
+            dgr[r] = rb[lane + 32 * r];
+        }
+#pragma unroll
+        for (int a = 0; a < NR; ++a) {
+            const int i = warp + 16 * a;
+            if (VAR == 1 || i >= sa || i == p) continue;
+            const double f = colp[a] * rinv;
+#pragma unroll
+            for (int b = 0; b < NC; ++b) {
+                const int q = lane + 32 * b;
+                if (q >= 2 * sa || (q < sa && ((donem >> q) & 1ull))) continue;
+                v[a][b] = fma(-f, rowp[b], v[a][b]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int i = lane + 32 * r;
+            if (i < sa && !((donem >> i) & 1ull)) dg[r] = fma(-(dgc[r] * rinv), dgr[r], dg[r]);
+        }
+        int pn;
+        double pvn;
+        unsigned long long nk = search(donem);
+        if (VAR == 2) nk = (p + 1 < sa) ? ((1ull << 62) | (unsigned long long)(63 - (p + 1))) : 0ull;
+        pivot_of(nk, pn, pvn);
+        if (VAR == 2) pvn = fmax(pvn, 1.0);
+        ++rank;
+        buf ^= 1;
+        if (pn >= 0 && pvn > cutoff) publish(pn, buf);
+        if (VAR != 3) __syncthreads();
+        p = pn;
+        pv = pvn;
+        rinv = VAR == 4 ? pvn : __drcp_rn(pvn > 0.0 ? pvn : 1.0);
+    }
+    for (int e = threadIdx.x; e < S * RS; e += BS) out[e] = 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < NR; ++a) {
+        const int i = warp + 16 * a;  // warp-uniform
+        if (i >= sa || !((donem >> i) & 1ull)) continue;
+        const double d0 = __shfl_sync(0xffffffffu, v[a][0], i & 31);
+        const double d1 = __shfl_sync(0xffffffffu, v[a][1], i & 31);
+        const double di = __drcp_rn(i < 32 ? d0 : d1);  // aug[i][i]
+#pragma unroll
+        for (int b = 0; b < NC; ++b) {
+            const int q = lane + 32 * b - sa;
+            if (q >= 0 && q < sa) out[sm.idx[i] * RS + sm.idx[q]] = v[a][b] * di;
+        }
+    }
+    if (threadIdx.x == 0) sm.rank = rank;
+    __syncthreads();
+}
+
 }  // namespace bkcg

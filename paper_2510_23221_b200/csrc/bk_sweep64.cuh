@@ -10,20 +10,20 @@
 // upper-triangle Gram (13.3 kflop per cell; the B200 FP64 tensor rate is
 // ~37 TFLOP/s, measured, scripts/dmma_tput.cu, shared with SIMT DFMA). The
 // design keeps the FP64 pipe fed:
-//   * one CTA per SM: 3 teams of 4 consumer warps + 1 producer warp (13
-//     warps: at most 4 per SM sub-partition, so 128 registers per thread);
-//   * the producer streams each team's next runs (W and R as four 16-column
-//     panels each, TMA 2D tensor copies with 128-byte swizzle, plus the run's
-//     D^-1 by a bulk copy) into a per-team ring of stages, full / empty
-//     mbarriers per stage — the consumers never issue a load;
+//   * one CTA per SM: 3 teams of 4 warps (12 warps, 3 per SM sub-partition,
+//     so up to 168 registers per thread);
+//   * each team's leader thread streams the team's next runs (W and R as four
+//     16-column panels each, TMA 2D tensor copies with 128-byte swizzle, plus
+//     the run's D^-1 by a bulk copy) into the team's ring of stages, one full
+//     mbarrier per stage; a stage is refilled right after the team barrier
+//     that proves all four warps consumed it — no other loads are issued;
 //   * a team owns one run at a time, warp w of the team the output columns
 //     16w .. 16w + 15 (two n-tiles; alpha fragments from shared memory);
 //     teams synchronise only among their own 128 threads (named barriers), so
 //     the teams drift and overlap one another's DMMA, epilogue and wait
 //     phases;
-//   * after the update the team writes R and Z into the stage's W / R panels
-//     (same swizzle) and each warp accumulates 5 of the 20 upper 16 x 8 Gram
-//     tiles; the stage is released by one arrival per warp.
+//   * after the update the team stages R (same swizzle) and each warp
+//     accumulates 5 of the 20 upper 16 x 8 Gram tiles of R^T D^-1 R.
 // Fixed group-to-team assignment and a fixed-order sum of the teams' partials:
 // run-to-run deterministic.
 #pragma once
@@ -48,7 +48,6 @@ struct Smem {
     double alpha[64 * 64];                               // alpha, swizzled (alpha_at)
     double dinv[kTeams][kStages][16];                    // D^-1 of each stage's run
     unsigned long long full[kTeams][kStages];
-    unsigned long long empty[kTeams][kStages];
 };
 constexpr size_t smem_bytes() { return sizeof(Smem) + 1024; }
 
@@ -106,8 +105,14 @@ __device__ __forceinline__ void gram_tile(int w, int i, int& m, int& n) {
     n = k - (m == 0 ? 0 : m == 1 ? 6 : m == 2 ? 10 : 12);
 }
 
-// W (a.W) and R (a.R) as 2D tensors (64 columns, nloc rows)
-__global__ void __launch_bounds__(kThreads, 1)
+// W (a.W) and R (a.R) as 2D tensors (64 columns, nloc rows). No producer
+// warp: 12 warps (3 per SM sub-partition, so up to 168 registers — the
+// 13-warp form capped them at 128 and spilled inside the run loop); each
+// team's leader thread issues its own team's copies: the first kStages runs up
+// front, then run it + 4 into the stage of run it + 1 right after the team
+// barrier of run it (every warp of the team has consumed runs <= it + 1 by
+// then), so two runs are in flight while the team works on a third.
+__global__ void __launch_bounds__(kConsumers, 1)
     k_update64_ws(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapR,
                   SweepArgs a) {
     constexpr int S = 64;
@@ -121,53 +126,39 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool jac = a.precond != 0;
     for (int e = threadIdx.x; e < S * S; e += blockDim.x)
         sm.alpha[alpha_at(e / S, e % S)] = a.coef[(e / S) * (S + 4) + e % S];
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < kTeams; ++q)
-            for (int s = 0; s < kStages; ++s) {
-                mbar_init(&sm.full[q][s], 1);
-                mbar_init(&sm.empty[q][s], kTeamWarps);
-            }
+    const int q = warp / kTeamWarps, w = warp % kTeamWarps;
+    const int first = blockIdx.x * kTeams + q;
+    const bool leader = w == 0 && lane == 0;
+    // run it of this team -> stage it % kStages
+    auto issue = [&](int it) {
+        const int grp = first + it * nteams;
+        if (grp >= ntiles) return;
+        const int s = it % kStages;
+        TileCells tc;
+        tile_cells(a.sl, grp, ntiles, tc);
+        unsigned char* st = sm.stage[q][s];
+        unsigned long long* bar = &sm.full[q][s];
+        mbar_expect_tx(bar, 2 * kArrBytes + (jac ? 128 : 0));
+        for (int p = 0; p < 4; ++p) {
+            tma_2d(st + p * kPanelBytes, &mapW, 16 * p, (int)tc.l0, bar);
+            tma_2d(st + kArrBytes + p * kPanelBytes, &mapR, 16 * p, (int)tc.l0, bar);
+        }
+        if (jac) bulk_g2s(sm.dinv[q][s], a.st.dinv + tc.g0, 128, bar);
+    };
+    if (leader) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&sm.full[q][s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int it = 0; it < kStages; ++it) issue(it);
     }
     __syncthreads();
 
-    if (warp == kTeams * kTeamWarps) {  // ---- producer
-        if (lane == 0) {
-            int it[kTeams] = {};
-            bool live = true;
-            while (live) {
-                live = false;
-                for (int q = 0; q < kTeams; ++q) {
-                    const int grp = blockIdx.x * kTeams + q + it[q] * nteams;
-                    if (grp >= ntiles) continue;
-                    live = true;
-                    const int s = it[q] % kStages;
-                    if (it[q] >= kStages) mbar_wait(&sm.empty[q][s], ((it[q] / kStages) - 1) & 1);
-                    TileCells tc;
-                    tile_cells(a.sl, grp, ntiles, tc);
-                    unsigned char* st = sm.stage[q][s];
-                    unsigned long long* bar = &sm.full[q][s];
-                    mbar_expect_tx(bar, 2 * kArrBytes + (jac ? 128 : 0));
-                    for (int p = 0; p < 4; ++p) {
-                        tma_2d(st + p * kPanelBytes, &mapW, 16 * p, (int)tc.l0, bar);
-                        tma_2d(st + kArrBytes + p * kPanelBytes, &mapR, 16 * p, (int)tc.l0, bar);
-                    }
-                    if (jac) bulk_g2s(sm.dinv[q][s], a.st.dinv + tc.g0, 128, bar);
-                    ++it[q];
-                }
-            }
-        }
-        return;
-    }
-
-    // ---- consumers: team q, warp w of the team owns columns 16 w .. 16 w + 15.
+    // ---- team q, warp w of the team owns columns 16 w .. 16 w + 15.
     // Software-pipelined so that a team needs ONE barrier per run: the update
     // of run i + 1 (independent DMMA work) sits between a warp's write of run
     // i's R into the team's staging buffer and the barrier after which the team
     // reads that buffer for run i's Gram. Staging is double-buffered: a warp
     // that passed the barrier of run i knows every warp finished the Gram of
     // run i - 1, so buffer (i + 1) % 2 is free for run i + 1.
-    const int q = warp / kTeamWarps, w = warp % kTeamWarps;
     double gacc[5][4];
 #pragma unroll
     for (int i = 0; i < 5; ++i)
@@ -177,11 +168,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int i = 0; i < 5; ++i) gram_tile(w, i, gm[i], gn[i]);
     double rr[4] = {0.0, 0.0, 0.0, 0.0};  // columns 16w + 8nt + 2t + e
-    const int first = blockIdx.x * kTeams + q;
 
     // R -= W alpha for the run in stage `it`: D (16 cells x 8 columns) per
     // n-tile, K = 64; also fetches D^-1 of the Gram rows kc + 4t (kc = 0..3)
-    // and releases the stage
     auto update = [&](int it, double (&d)[2][4], double (&dg)[4], double& d0, double& d1) {
         const int s = it % kStages;
         mbar_wait(&sm.full[q][s], (it / kStages) & 1);
@@ -210,8 +199,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         d1 = jac ? dv[rg + 8] : 1.0;
 #pragma unroll
         for (int kc = 0; kc < 4; ++kc) dg[kc] = jac ? dv[gram_cell(kc, t)] : 1.0;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[q][s]);
     };
     // rr, R to HBM, R into staging buffer b (Z = D^-1 R is formed in the Gram)
     auto epilogue = [&](int grp, const double (&d)[2][4], int b) {
@@ -260,7 +247,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int nxt = grp + nteams;
             double dn[2][4], dgn[4], e0, e1;
             if (nxt < ntiles) update(it + 1, dn, dgn, e0, e1);
-            team_sync(q);  // every warp of the team staged run `it`
+            team_sync(q);  // every warp of the team staged run `it` and consumed run it + 1
+            if (leader) {  // refill the stages of runs it and it + 1 (kStages = 3)
+                if (it == 0) issue(kStages);
+                issue(it + kStages + 1);
+            }
             gram(it & 1, dg);
             if (nxt < ntiles) {
                 epilogue(nxt, dn, (it + 1) & 1);
@@ -719,7 +710,7 @@ inline cudaError_t launch_update64_ws(const SweepArgs& a, int64_t nloc, int nsm,
     const size_t smem = sweep64::smem_bytes();
     const cudaError_t e = bk::set_max_smem((const void*)sweep64::k_update64_ws, smem);
     if (e != cudaSuccess) return e;
-    sweep64::k_update64_ws<<<nsm, sweep64::kThreads, smem, s>>>(mw, mr, a);
+    sweep64::k_update64_ws<<<nsm, sweep64::kConsumers, smem, s>>>(mw, mr, a);
     return cudaGetLastError();
 }
 

@@ -1,6 +1,7 @@
 #!/bin/bash
 # scratch job file for one gpurun call (the command of the latest A/B run)
 cd $GRAFT_REPO_ROOT
-python scripts/c5_loop_ab.py 3 > gpurun_out/ab3.log 2>&1 && \
-ncu --set full --import-source on --clock-control none -k regex:"k_ctl_alpha|k_ctl_update|k_update64_ws|k_spmm64_ws" -s 4 -c 4 -o gpurun_out/c5_ctl python scripts/c5_loop_ab.py 3 > gpurun_out/ncu_ctl.log 2>&1
-timeout 900 python bench.py --steps 3 --warmup 3 --no-extra > gpurun_out/bench2.log 2>&1
+python scripts/ctl_solve_bench.py > gpurun_out/ctl_solve.log 2>&1
+timeout 600 python -m pytest tests -m gpu -x -q -k "large or c5 or fullsize or dd or graph or multikernel or slab or stress" > gpurun_out/t.log 2>&1
+python scripts/c5_loop_ab.py > gpurun_out/ab.log 2>&1
+python scripts/c5_phases.py 20 > gpurun_out/ph.log 2>&1
