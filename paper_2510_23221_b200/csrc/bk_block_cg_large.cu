@@ -988,14 +988,25 @@ struct CSm {
     alignas(16) double out[S * Strides<S>::RS];
 };
 
+// compacted indices of the active columns, ascending (one warp: ballot +
+// prefix popcount instead of a serial scan of the mask in global memory)
 template <int S>
 __device__ void ctl_index(Ctl<S>* c, CSm<S>& sm) {
-    if (threadIdx.x == 0) {
-        int k = 0;
-        for (int q = 0; q < S; ++q)
-            if (c->act[q]) sm.idx[k++] = q;
-        sm.sa = k;
-        c->sa = k;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int base = 0;
+#pragma unroll
+        for (int q0 = 0; q0 < S; q0 += 32) {
+            const int q = q0 + lane;
+            const bool on = q < S && c->act[q];
+            const unsigned m = __ballot_sync(0xffffffffu, on);
+            if (on) sm.idx[base + __popc(m & ((1u << lane) - 1u))] = q;
+            base += __popc(m);
+        }
+        if (lane == 0) {
+            sm.sa = base;
+            c->sa = base;
+        }
     }
     __syncthreads();
 }
@@ -1634,15 +1645,34 @@ __device__ long long ctl_solve_cycles(CSm<64>& sm, const double* M, const double
     __syncthreads();
     return (clock64() - t0) / reps;
 }
-template <int VAR>
+// the register solve with all BS = 32 NWR threads in the pivot loop
+template <int NWR>
+__global__ void __launch_bounds__(NWR * 32) k_ctl_solve_bench_nw(int reps, long long* out) {
+    extern __shared__ __align__(16) unsigned char smraw_[];
+    CSm<64>& sm = *reinterpret_cast<CSm<64>*>(smraw_);
+    constexpr int S = 64, BS = NWR * 32;
+    for (int e = threadIdx.x; e < S * S; e += BS) {
+        const int i = e / S, j = e % S;
+        sm.m0[e] = (i == j ? 1.0 : 0.01 / (1 + i + j)) * exp(-0.05 * (i + j));
+        sm.m1[e] = (i == j ? 2.0 : 0.1) * exp(-0.025 * (i + j));
+    }
+    if (threadIdx.x < S) sm.idx[threadIdx.x] = threadIdx.x;
+    if (threadIdx.x == 0) sm.sa = S;
+    __syncthreads();
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) small_solve_reg<64, BS, 0, NWR>(sm, sm.m0, sm.m1, sm.out);
+    __syncthreads();
+    if (threadIdx.x == 0) *out = (clock64() - t0) / reps;
+}
+template <int VAR, int NWR = 16>
 __device__ long long reg_cycles(CSm<64>& sm, int reps) {
     __syncthreads();
     const long long t0 = clock64();
-    for (int r = 0; r < reps; ++r) small_solve_reg<64, CBS, VAR>(sm, sm.m0, sm.m1, sm.out);
+    for (int r = 0; r < reps; ++r) small_solve_reg<64, CBS, VAR, NWR>(sm, sm.m0, sm.m1, sm.out);
     __syncthreads();
     return (clock64() - t0) / reps;
 }
-__global__ void __launch_bounds__(CBS) k_ctl_solve_bench(int reps, long long* out, double* res) {
+__global__ void __launch_bounds__(CBS) k_ctl_solve_bench(int reps, long long* out, double* res, int only_reg) {
     extern __shared__ __align__(16) unsigned char smraw_[];
     CSm<64>& sm = *reinterpret_cast<CSm<64>*>(smraw_);
     constexpr int S = 64;
@@ -1654,11 +1684,13 @@ __global__ void __launch_bounds__(CBS) k_ctl_solve_bench(int reps, long long* ou
     if (threadIdx.x < S) sm.idx[threadIdx.x] = threadIdx.x;
     if (threadIdx.x == 0) sm.sa = S;
     __syncthreads();
-    long long c[5];
-    c[0] = ctl_solve_cycles<16>(sm, sm.m0, sm.m1, reps);
-    c[1] = ctl_solve_cycles<8>(sm, sm.m0, sm.m1, reps);
-    c[2] = ctl_solve_cycles<4>(sm, sm.m0, sm.m1, reps);
-    c[3] = ctl_solve_cycles<2>(sm, sm.m0, sm.m1, reps);
+    long long c[5] = {};
+    if (!only_reg) {
+        c[0] = ctl_solve_cycles<16>(sm, sm.m0, sm.m1, reps);
+        c[1] = ctl_solve_cycles<8>(sm, sm.m0, sm.m1, reps);
+        c[2] = ctl_solve_cycles<4>(sm, sm.m0, sm.m1, reps);
+        c[3] = ctl_solve_cycles<2>(sm, sm.m0, sm.m1, reps);
+    }
     for (int e = threadIdx.x; e < S * S; e += CBS) res[e] = sm.out[(e / S) * Strides<S>::RS + e % S];
     __syncthreads();
     const long long t0 = clock64();
@@ -1671,26 +1703,35 @@ __global__ void __launch_bounds__(CBS) k_ctl_solve_bench(int reps, long long* ou
     }
     for (int e = threadIdx.x; e < S * S; e += CBS)
         res[S * S + e] = sm.out[(e / S) * Strides<S>::RS + e % S];
-    long long cv[4];
-    cv[0] = reg_cycles<1>(sm, reps);
-    cv[1] = reg_cycles<2>(sm, reps);
-    cv[2] = reg_cycles<3>(sm, reps);
-    cv[3] = reg_cycles<4>(sm, reps);
+    long long cv[4] = {};
+    if (!only_reg) {
+        cv[0] = reg_cycles<1>(sm, reps);
+        cv[3] = reg_cycles<3>(sm, reps);
+    }
     if (threadIdx.x == 0)
         for (int v = 0; v < 4; ++v) out[6 + v] = cv[v];
 }
 
 extern "C" {
 
-int bk_debug_ctl_solve_cycles(int reps, long long* cycles6, double* coef2) {
+int bk_debug_ctl_solve_cycles(int reps, long long* cycles6, double* coef2, int only_reg) {
     long long* d;
     double* r;
     cudaMalloc(&d, 16 * 8);
     cudaMalloc(&r, 2 * 64 * 64 * 8);
     cudaFuncSetAttribute(k_ctl_solve_bench, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(CSm<64>));
-    k_ctl_solve_bench<<<1, CBS, sizeof(CSm<64>)>>>(reps, d, r);
-    const int err = (int)cudaDeviceSynchronize();
+    k_ctl_solve_bench<<<1, CBS, sizeof(CSm<64>)>>>(reps, d, r, only_reg);
+    int err = (int)cudaDeviceSynchronize();
+    if (!only_reg) {
+        cudaFuncSetAttribute(k_ctl_solve_bench_nw<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(CSm<64>));
+        cudaFuncSetAttribute(k_ctl_solve_bench_nw<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(CSm<64>));
+        k_ctl_solve_bench_nw<8><<<1, 256, sizeof(CSm<64>)>>>(reps, d + 7);
+        k_ctl_solve_bench_nw<4><<<1, 128, sizeof(CSm<64>)>>>(reps, d + 8);
+        err |= (int)cudaDeviceSynchronize();
+    }
     cudaMemcpy(cycles6, d, 10 * 8, cudaMemcpyDeviceToHost);
     cudaMemcpy(coef2, r, 2 * 64 * 64 * 8, cudaMemcpyDeviceToHost);
     cudaFree(d);

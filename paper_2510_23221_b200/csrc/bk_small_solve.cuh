@@ -166,17 +166,20 @@ __device__ void small_solve_t(SMT& sm, const double* M, const double* RHS, doubl
             colp[r] = i < sa ? aug[i * LD + p] : 0.0;
             rowp[r] = i < sa ? aug[p * LD + i] : 0.0;
         }
-        // block update (issued first so it overlaps the pivot search below)
+        // block update (issued first so it overlaps the pivot search below);
+        // branch-free (predicated stores / selects: divergent `continue`s here
+        // compiled to a reconvergence barrier per element)
 #pragma unroll
         for (int r = 0; r < RPW; ++r) {
             const int i = warp + NW * r;
-            if (i >= sa || i == p) continue;
+            const bool row_ok = i < sa && i != p;
             const double f = fi[r] * rinv;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
                 const int q = lane + 32 * c;
-                if (q >= 2 * sa || (q < sa && ((donem >> q) & 1ull))) continue;
-                aug[i * LD + q] = fma(-f, apq[c], aiq[r][c]);
+                const bool ok = row_ok && q < 2 * sa && !(q < sa && ((donem >> q) & 1ull));
+                const double nv = fma(-f, apq[c], aiq[r][c]);
+                if (ok) aug[i * LD + q] = nv;
             }
         }
         // Schur diagonal after this pivot (same arithmetic as aug[i][i] above)
@@ -184,7 +187,8 @@ __device__ void small_solve_t(SMT& sm, const double* M, const double* RHS, doubl
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int i = lane + 32 * r;
-            if (i < sa && !((donem >> i) & 1ull)) dg[r] = fma(-(colp[r] * rinv), rowp[r], dg[r]);
+            const double nd = fma(-(colp[r] * rinv), rowp[r], dg[r]);
+            dg[r] = (i < sa && !((donem >> i) & 1ull)) ? nd : dg[r];
         }
         unsigned long long nb = search(donem);
         if (VAR == 2) nb = (p + 1 < sa) ? ((1ull << 32) | (unsigned long long)(63 - (p + 1))) : 0ull;
@@ -221,24 +225,43 @@ __device__ void small_solve_t(SMT& sm, const double* M, const double* RHS, doubl
 // augmented [M | RHS] block lives in registers — warp w holds rows w + 16 a,
 // lane l columns l + 32 b (a, b < 4) — so a pivot step moves only the pivot
 // row and column through shared memory (published by their owners into a
-// double buffer) instead of streaming the whole block through shared memory
-// twice. One barrier per pivot; every warp tracks the Schur diagonal and finds
-// the next pivot redundantly, as small_solve_t.
+// double buffer). One barrier per pivot; every warp tracks the Schur diagonal
+// and finds the next pivot redundantly, as small_solve_t.
+// The block update is unconditional (a predicated update per element made
+// the loop issue-bound on integer / select work): entries small_solve_t
+// leaves alone are either restored (the pivot row, from the published copy)
+// or never read again (columns of earlier pivots feed only themselves; the
+// diagonal of a pivoted row is taken from the recorded pivot value, which is
+// the same number — the Schur-diagonal recurrence uses aug[i][i]'s arithmetic).
 // VAR (timing experiments only): 1 no block update, 2 fixed pivot order,
 // 3 no barrier, 4 no reciprocal
-template <int S, int BS, int VAR = 0, class SMT>
+// NWR: warps in the pivot loop (warp w < NWR holds rows w + NWR a); the
+// others wait at the final barrier. Fewer warps = less replicated pivot
+// bookkeeping per pivot against more update work per thread.
+template <int S, int BS, int VAR = 0, int NWR = 16, class SMT>
 __device__ void small_solve_reg(SMT& sm, const double* M, const double* RHS, double* out) {
-    static_assert(S == 64 && BS == 512, "register layout: 16 warps x 4 rows, 32 lanes x 4 columns");
+    static_assert(S == 64 && BS >= NWR * 32 && (NWR == 4 || NWR == 8 || NWR == 16),
+                  "register layout: NWR warps x 64 / NWR rows, 32 lanes x 4 columns");
     constexpr int RS = Strides<S>::RS;
-    constexpr int NR = 4, NC = 4;           // rows / columns per thread
+    constexpr int NR = S / NWR, NC = 4;     // rows / columns per thread
+    auto wbar = []() {
+        if (NWR == BS / 32)
+            __syncthreads();
+        else
+            asm volatile("bar.sync 1, %0;" ::"n"(NWR * 32) : "memory");
+    };
     constexpr int BUF = 2 * S + S;          // pivot row (2S) | pivot column (S)
     const int sa = sm.sa;
     double* const pbuf = sm.aug;            // 2 x BUF doubles
+    double* const pivv = sm.aug + 2 * BUF;  // pivot value of each pivoted row
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int rank = 0;
+    unsigned long long donem = 0ull;
+    if (warp < NWR) {
     double v[NR][NC];
 #pragma unroll
     for (int a = 0; a < NR; ++a) {
-        const int i = warp + 16 * a;
+        const int i = warp + NWR * a;
 #pragma unroll
         for (int b = 0; b < NC; ++b) {
             const int q = lane + 32 * b;
@@ -262,7 +285,6 @@ __device__ void small_solve_reg(SMT& sm, const double* M, const double* RHS, dou
         const int i = lane + 32 * r;
         dg[r] = i < sa ? M[sm.idx[i] * S + sm.idx[i]] : 0.0;  // aug[i][i]
     }
-    unsigned long long donem = 0ull;
     auto search = [&](unsigned long long excl) -> unsigned long long {
         unsigned long long key = 0ull;
 #pragma unroll
@@ -280,21 +302,24 @@ __device__ void small_solve_reg(SMT& sm, const double* M, const double* RHS, dou
         const double p1 = __shfl_sync(0xffffffffu, dg[1], src);
         pv = p < 0 ? 0.0 : (p >= 32 ? p1 : p0);
     };
-    // owners of row p / column p write them into buffer `buf`
+    // owners of row p / column p write them into buffer `buf` (p < 64, so
+    // column p is column p & 31 of register block b = p >> 5 <= 1)
     auto publish = [&](int p, int buf) {
-        // (selects, not v[p >> 4][b]: keep v in registers)
         double* rb = pbuf + buf * BUF;
-        if (warp == (p & 15)) {
-            const int a = p >> 4;
+        if (warp == p % NWR) {
+            const int ap = p / NWR;
 #pragma unroll
-            for (int b = 0; b < NC; ++b)
-                rb[lane + 32 * b] = a == 0 ? v[0][b] : a == 1 ? v[1][b] : a == 2 ? v[2][b] : v[3][b];
+            for (int b = 0; b < NC; ++b) {
+                double x = v[0][b];
+#pragma unroll
+                for (int a = 1; a < NR; ++a) x = a == ap ? v[a][b] : x;
+                rb[lane + 32 * b] = x;
+            }
         }
         if (lane == (p & 31)) {
-            const int b = p >> 5;
+            const bool hi = p >= 32;
 #pragma unroll
-            for (int a = 0; a < NR; ++a)
-                rb[2 * S + warp + 16 * a] = b == 0 ? v[a][0] : b == 1 ? v[a][1] : b == 2 ? v[a][2] : v[a][3];
+            for (int a = 0; a < NR; ++a) rb[2 * S + warp + NWR * a] = hi ? v[a][1] : v[a][0];
         }
     };
     int p;
@@ -303,38 +328,43 @@ __device__ void small_solve_reg(SMT& sm, const double* M, const double* RHS, dou
     pivot_of(best, p, pv);
     const double cutoff = fmax(pv * sa * 2.220446049250313e-16, 2.2250738585072014e-308);
     double rinv = __drcp_rn(pv);
-    int rank = 0, buf = 0;
+    int buf = 0;
     if (p >= 0) publish(p, 0);
-    __syncthreads();
+    wbar();
     while (p >= 0 && pv > cutoff) {  // uniform
         donem |= 1ull << p;
+        if (threadIdx.x == 0) pivv[p] = pv;
         const double* rb = pbuf + buf * BUF;
         double rowp[NC], colp[NR], dgc[2], dgr[2];
 #pragma unroll
         for (int b = 0; b < NC; ++b) rowp[b] = rb[lane + 32 * b];
 #pragma unroll
-        for (int a = 0; a < NR; ++a) colp[a] = rb[2 * S + warp + 16 * a];
+        for (int a = 0; a < NR; ++a) colp[a] = rb[2 * S + warp + NWR * a];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             dgc[r] = rb[2 * S + lane + 32 * r];
             dgr[r] = rb[lane + 32 * r];
         }
+        if (VAR != 1) {
 #pragma unroll
-        for (int a = 0; a < NR; ++a) {
-            const int i = warp + 16 * a;
-            if (VAR == 1 || i >= sa || i == p) continue;
-            const double f = colp[a] * rinv;
+            for (int a = 0; a < NR; ++a) {
+                const double f = colp[a] * rinv;
 #pragma unroll
-            for (int b = 0; b < NC; ++b) {
-                const int q = lane + 32 * b;
-                if (q >= 2 * sa || (q < sa && ((donem >> q) & 1ull))) continue;
-                v[a][b] = fma(-f, rowp[b], v[a][b]);
+                for (int b = 0; b < NC; ++b) v[a][b] = fma(-f, rowp[b], v[a][b]);
+            }
+            if (warp == p % NWR) {  // the pivot row is not updated
+                const int ap = p / NWR;
+#pragma unroll
+                for (int a = 0; a < NR; ++a)
+#pragma unroll
+                    for (int b = 0; b < NC; ++b) v[a][b] = a == ap ? rowp[b] : v[a][b];
             }
         }
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             const int i = lane + 32 * r;
-            if (i < sa && !((donem >> i) & 1ull)) dg[r] = fma(-(dgc[r] * rinv), dgr[r], dg[r]);
+            const double nd = fma(-(dgc[r] * rinv), dgr[r], dg[r]);
+            dg[r] = (i < sa && !((donem >> i) & 1ull)) ? nd : dg[r];
         }
         int pn;
         double pvn;
@@ -345,28 +375,28 @@ __device__ void small_solve_reg(SMT& sm, const double* M, const double* RHS, dou
         ++rank;
         buf ^= 1;
         if (pn >= 0 && pvn > cutoff) publish(pn, buf);
-        if (VAR != 3) __syncthreads();
+        if (VAR != 3) wbar();
         p = pn;
         pv = pvn;
         rinv = VAR == 4 ? pvn : __drcp_rn(pvn > 0.0 ? pvn : 1.0);
     }
-    for (int e = threadIdx.x; e < S * RS; e += BS) out[e] = 0.0;
-    __syncthreads();
+    // the RHS block, scaled by the pivoted rows' diagonals, to registers'
+    // owners' output rows after the zero fill below
+    for (int e = threadIdx.x; e < S * RS; e += NWR * 32) out[e] = 0.0;
+    wbar();
 #pragma unroll
     for (int a = 0; a < NR; ++a) {
-        const int i = warp + 16 * a;  // warp-uniform
+        const int i = warp + NWR * a;  // warp-uniform
         if (i >= sa || !((donem >> i) & 1ull)) continue;
-        const double d0 = __shfl_sync(0xffffffffu, v[a][0], i & 31);
-        const double d1 = __shfl_sync(0xffffffffu, v[a][1], i & 31);
-        const double di = __drcp_rn(i < 32 ? d0 : d1);  // aug[i][i]
+        const double di = __drcp_rn(pivv[i]);  // aug[i][i]
 #pragma unroll
         for (int b = 0; b < NC; ++b) {
             const int q = lane + 32 * b - sa;
             if (q >= 0 && q < sa) out[sm.idx[i] * RS + sm.idx[q]] = v[a][b] * di;
         }
     }
+    }  // warp < NWR
     if (threadIdx.x == 0) sm.rank = rank;
     __syncthreads();
 }
-
 }  // namespace bkcg
