@@ -272,6 +272,7 @@ struct SweepArgs {
     const double* coef2; // alpha kept for the deferred X update (k_pupdate modes 1, 2)
     const int* act;      // per-column mask for masked sweeps
     const int* gate;     // P updates inside the device-driven loop: run only if *gate == 0
+    const double* pcoef; // S = 64 stencil sweep: per-run packed coefficients (k_pack_coef64)
     int precond;
 };
 
@@ -1215,6 +1216,15 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
                         (ws_update ? " ws-update" : "") + (ws_spmm ? " ws-spmm" : "");
     void *pPart, *pRed, *pCtl, *pHost;
     bk_status st;
+    if (ws_spmm && !ctx->knobs.spmm_teams) {  // packed per-run coefficients of the stencil sweep
+        void* pc;
+        const size_t runs = (size_t)(sl.nx / 16) * sl.ny * sl.nz;
+        if ((st = workspace(ctx, kSlotCgCoef64, runs * sweep64::kPC * 8, &pc)) != BK_OK) return st;
+        sweep64::k_pack_coef64<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(sl, a.st, (double*)pc);
+        ++ctx->launches;
+        BK_CUDA_TRY(ctx, cudaGetLastError());
+        a.pcoef = (const double*)pc;
+    }
     if ((st = workspace(ctx, kSlotCgPart, (size_t)nb * E * 8, &pPart)) != BK_OK) return st;
     if ((st = workspace(ctx, kSlotCgRed, (size_t)E * 8, &pRed)) != BK_OK) return st;
     if ((st = workspace(ctx, kSlotCgCtl, sizeof(Ctl<S>) + sizeof(CgReport), &pCtl)) != BK_OK)
@@ -1291,7 +1301,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
         halo(a.P);
         phase_mark(ctx, -1);
         if (ws_spmm) {
-            BK_CUDA_TRY(ctx, launch_spmm64_ws(a, nbs, s));
+            BK_CUDA_TRY(ctx, launch_spmm64_ws(a, nbs, s, ctx->knobs.spmm_teams));
         } else {
             BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s, ctx->knobs.no_tma_spmm));
         }

@@ -37,6 +37,7 @@ struct bk_knobs {
     bool phase_timing = false; // per-kernel-kind event timing of the multi-kernel solve
     bool no_ws_update = false; // S = 64: the cp.async update sweeps instead of the warp-specialised ones
     bool no_ws_spmm = false;   // S = 64: the per-run TMA stencil sweep instead of the z-marching one
+    bool spmm_teams = false;   // S = 64: the two-team stencil sweep instead of the role-split one
     bool graph_loop = false;   // multi-kernel solve: device-driven iterations (CUDA graph while-loop)
 };
 
@@ -149,6 +150,7 @@ enum Slot : int {
     kSlotStrX1,
     kSlotStrC0,
     kSlotStrC1,
+    kSlotCgCoef64,  // S = 64 stencil sweep: coefficients packed per 16-cell run
 };
 
 bk_status fail(bk_ctx* ctx, bk_status st, const std::string& msg);

@@ -28,6 +28,10 @@
 // run-to-run deterministic.
 #pragma once
 
+#ifndef BK_EXP  // timing experiments only (scripts/ab)
+#define BK_EXP 0
+#endif
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -105,53 +109,84 @@ __device__ __forceinline__ void gram_tile(int w, int i, int& m, int& n) {
     n = k - (m == 0 ? 0 : m == 1 ? 6 : m == 2 ? 10 : 12);
 }
 
-// W (a.W) and R (a.R) as 2D tensors (64 columns, nloc rows). No producer
-// warp: 12 warps (3 per SM sub-partition, so up to 168 registers — the
-// 13-warp form capped them at 128 and spilled inside the run loop); each
-// team's leader thread issues its own team's copies: the first kStages runs up
-// front, then run it + 4 into the stage of run it + 1 right after the team
-// barrier of run it (every warp of the team has consumed runs <= it + 1 by
-// then), so two runs are in flight while the team works on a third.
-__global__ void __launch_bounds__(kConsumers, 1)
-    k_update64_ws(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapR,
-                  SweepArgs a) {
-    constexpr int S = 64;
-    extern __shared__ __align__(1024) unsigned char smraw_[];
-    // 1024-byte aligned (128B-swizzle atoms); pointer arithmetic on the shared
-    // array keeps the state space, so the accesses compile to LDS / STS
-    Smem& sm = *reinterpret_cast<Smem*>(smraw_ + ((1024u - (smem_u32(smraw_) & 1023u)) & 1023u));
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const int ntiles = n_tiles(a.sl);  // 16-cell runs
-    const int nteams = gridDim.x * kTeams;
-    const bool jac = a.precond != 0;
-    for (int e = threadIdx.x; e < S * S; e += blockDim.x)
-        sm.alpha[alpha_at(e / S, e % S)] = a.coef[(e / S) * (S + 4) + e % S];
-    const int q = warp / kTeamWarps, w = warp % kTeamWarps;
-    const int first = blockIdx.x * kTeams + q;
-    const bool leader = w == 0 && lane == 0;
-    // run it of this team -> stage it % kStages
-    auto issue = [&](int it) {
-        const int grp = first + it * nteams;
-        if (grp >= ntiles) return;
-        const int s = it % kStages;
-        TileCells tc;
-        tile_cells(a.sl, grp, ntiles, tc);
-        unsigned char* st = sm.stage[q][s];
-        unsigned long long* bar = &sm.full[q][s];
-        mbar_expect_tx(bar, 2 * kArrBytes + (jac ? 128 : 0));
-        for (int p = 0; p < 4; ++p) {
-            tma_2d(st + p * kPanelBytes, &mapW, 16 * p, (int)tc.l0, bar);
-            tma_2d(st + kArrBytes + p * kPanelBytes, &mapR, 16 * p, (int)tc.l0, bar);
+// The same 5 tiles per warp as gram_tile, with the warp's distinct m-blocks
+// and n-blocks listed so a k-step loads each A fragment (rows of m-block M[j])
+// and each B fragment (columns of n-block N[j]) once: 7-9 fragment loads per
+// k-step instead of 15 (the Gram's shared-memory reads halve).
+template <int W>
+struct GramSet;
+template <>
+struct GramSet<0> {  // (0,0..4)
+    static constexpr int NM = 1, NN = 5;
+    static __device__ __forceinline__ constexpr int M(int j) { return j == 0 ? 0 : 0; }
+    static __device__ __forceinline__ constexpr int N(int j) { return j == 0 ? 0 : j == 1 ? 1 : j == 2 ? 2 : j == 3 ? 3 : 4; }
+    static __device__ __forceinline__ constexpr int TM(int j) { return j == 0 ? 0 : j == 1 ? 0 : j == 2 ? 0 : j == 3 ? 0 : 0; }
+    static __device__ __forceinline__ constexpr int TN(int j) { return j == 0 ? 0 : j == 1 ? 1 : j == 2 ? 2 : j == 3 ? 3 : 4; }
+};
+template <>
+struct GramSet<1> {  // (0,5..7), (1,2..3)
+    static constexpr int NM = 2, NN = 5;
+    static __device__ __forceinline__ constexpr int M(int j) { return j == 0 ? 0 : 1; }
+    static __device__ __forceinline__ constexpr int N(int j) { return j == 0 ? 5 : j == 1 ? 6 : j == 2 ? 7 : j == 3 ? 2 : 3; }
+    static __device__ __forceinline__ constexpr int TM(int j) { return j == 0 ? 0 : j == 1 ? 0 : j == 2 ? 0 : j == 3 ? 1 : 1; }
+    static __device__ __forceinline__ constexpr int TN(int j) { return j == 0 ? 0 : j == 1 ? 1 : j == 2 ? 2 : j == 3 ? 3 : 4; }
+};
+template <>
+struct GramSet<2> {  // (1,4..7), (2,4)
+    static constexpr int NM = 2, NN = 4;
+    static __device__ __forceinline__ constexpr int M(int j) { return j == 0 ? 1 : 2; }
+    static __device__ __forceinline__ constexpr int N(int j) { return j == 0 ? 4 : j == 1 ? 5 : j == 2 ? 6 : j == 3 ? 7 : 0; }
+    static __device__ __forceinline__ constexpr int TM(int j) { return j == 0 ? 0 : j == 1 ? 0 : j == 2 ? 0 : j == 3 ? 0 : 1; }
+    static __device__ __forceinline__ constexpr int TN(int j) { return j == 0 ? 0 : j == 1 ? 1 : j == 2 ? 2 : j == 3 ? 3 : 0; }
+};
+template <>
+struct GramSet<3> {  // (2,5..7), (3,6..7)
+    static constexpr int NM = 2, NN = 3;
+    static __device__ __forceinline__ constexpr int M(int j) { return j == 0 ? 2 : 3; }
+    static __device__ __forceinline__ constexpr int N(int j) { return j == 0 ? 5 : j == 1 ? 6 : j == 2 ? 7 : j == 3 ? 0 : 0; }
+    static __device__ __forceinline__ constexpr int TM(int j) { return j == 0 ? 0 : j == 1 ? 0 : j == 2 ? 0 : j == 3 ? 1 : 1; }
+    static __device__ __forceinline__ constexpr int TN(int j) { return j == 0 ? 0 : j == 1 ? 1 : j == 2 ? 2 : j == 3 ? 1 : 2; }
+};
+// one staged 16-cell run into warp W's tiles: A = rows of `At` (m-blocks),
+// B = rows of `Bt` (n-blocks) scaled per cell by dg[kc] when SCALE
+template <int W, bool SCALE>
+__device__ __forceinline__ void gram_run(double (&gacc)[5][4], const unsigned char* At,
+                                         const unsigned char* Bt, const double (&dg)[4], int g,
+                                         int t) {
+    using GS = GramSet<W>;
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+        const int cc = gram_cell(kc, t);
+        double a0[GS::NM], a1[GS::NM], b[GS::NN];
+#pragma unroll
+        for (int j = 0; j < GS::NM; ++j) {
+            a0[j] = lds(At, cc, 16 * GS::M(j) + g);
+            a1[j] = lds(At, cc, 16 * GS::M(j) + 8 + g);
         }
-        if (jac) bulk_g2s(sm.dinv[q][s], a.st.dinv + tc.g0, 128, bar);
-    };
-    if (leader) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&sm.full[q][s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int it = 0; it < kStages; ++it) issue(it);
+#pragma unroll
+        for (int j = 0; j < GS::NN; ++j) {
+            const double x = lds(Bt, cc, 8 * GS::N(j) + g);
+            b[j] = SCALE ? dg[kc] * x : x;
+        }
+#pragma unroll
+        for (int i = 0; i < 5; ++i) dmma_l(gacc[i], a0[GS::TM(i)], a1[GS::TM(i)], b[GS::TN(i)]);
     }
-    __syncthreads();
+}
+template <int W>
+__device__ __forceinline__ void gram_tile_c(int i, int& m, int& n) {
+    m = GramSet<W>::M(GramSet<W>::TM(i));
+    n = GramSet<W>::N(GramSet<W>::TN(i));
+}
 
+// consumer warp W (0..3) of team q of the update sweep (the Gram tiles and
+// output columns of W are compile-time: fragment loads shared across tiles)
+template <int W, class Issue>
+__device__ __forceinline__ void update64_warp(Smem& sm, const SweepArgs& a, int q, int first,
+                                              int ntiles, int nteams, bool jac, bool leader,
+                                              Issue& issue) {
+    constexpr int S = 64;
+    constexpr int w = W;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     // ---- team q, warp w of the team owns columns 16 w .. 16 w + 15.
     // Software-pipelined so that a team needs ONE barrier per run: the update
     // of run i + 1 (independent DMMA work) sits between a warp's write of run
@@ -164,9 +199,6 @@ __global__ void __launch_bounds__(kConsumers, 1)
     for (int i = 0; i < 5; ++i)
 #pragma unroll
         for (int e = 0; e < 4; ++e) gacc[i][e] = 0.0;
-    int gm[5], gn[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) gram_tile(w, i, gm[i], gn[i]);
     double rr[4] = {0.0, 0.0, 0.0, 0.0};  // columns 16w + 8nt + 2t + e
 
     // R -= W alpha for the run in stage `it`: D (16 cells x 8 columns) per
@@ -218,24 +250,13 @@ __global__ void __launch_bounds__(kConsumers, 1)
             sts2(St, rg + 8, c, d[nt][2], d[nt][3]);
         }
     };
-    // S_new += R^T Z over a run's 16 cells: k-step kc covers cells
-    // gram_cell(kc, t') (conflict-free reads); Z = D^-1 R
-    // formed from the staged R with the row's D^-1 (the same product the
-    // cp.async sweep stores)
+    // S_new += R^T Z over a run's 16 cells (Z = D^-1 R formed from the staged R
+    // with each cell's D^-1 — the product the cp.async sweep stores);
+    // conflict-free k-step -> cell map, fragments loaded once per k-step
     auto gram = [&](int b, const double (&dg)[4]) {
         const unsigned char* St = sm.rstage[q][b];
-#pragma unroll
-        for (int kc = 0; kc < 4; ++kc) {
-            const int c = gram_cell(kc, t);
-#pragma unroll
-            for (int i = 0; i < 5; ++i) {
-                const double a0 = lds(St, c, 16 * gm[i] + g);
-                const double a1 = lds(St, c, 16 * gm[i] + 8 + g);
-                dmma_l(gacc[i], a0, a1, dg[kc] * lds(St, c, 8 * gn[i] + g));
-            }
-        }
+        gram_run<W, true>(gacc, St, St, dg, g, t);
     };
-
     if (first < ntiles) {
         double d[2][4], dg[4], d0, d1;
         update(0, d, dg, d0, d1);
@@ -268,7 +289,9 @@ __global__ void __launch_bounds__(kConsumers, 1)
     double* mine = red + q * (S * S + S);
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-        const int r0 = 16 * gm[i] + g, c0 = 8 * gn[i] + 2 * t;
+        int gm, gn;
+        gram_tile_c<W>(i, gm, gn);
+        const int r0 = 16 * gm + g, c0 = 8 * gn + 2 * t;
         mine[r0 * S + c0] = gacc[i][0];
         mine[r0 * S + c0 + 1] = gacc[i][1];
         mine[(r0 + 8) * S + c0] = gacc[i][2];
@@ -292,6 +315,61 @@ __global__ void __launch_bounds__(kConsumers, 1)
         double v = red[e];
         for (int k = 1; k < kTeams; ++k) v += red[k * (S * S + S) + e];
         out[e] = v;
+    }
+}
+
+// W (a.W) and R (a.R) as 2D tensors (64 columns, nloc rows). No producer
+// warp: 12 warps (3 per SM sub-partition, so up to 168 registers — the
+// 13-warp form capped them at 128 and spilled inside the run loop); each
+// team's leader thread issues its own team's copies: the first kStages runs up
+// front, then run it + 4 into the stage of run it + 1 right after the team
+// barrier of run it (every warp of the team has consumed runs <= it + 1 by
+// then), so two runs are in flight while the team works on a third.
+__global__ void __launch_bounds__(kConsumers, 1)
+    k_update64_ws(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapR,
+                  SweepArgs a) {
+    constexpr int S = 64;
+    extern __shared__ __align__(1024) unsigned char smraw_[];
+    // 1024-byte aligned (128B-swizzle atoms); pointer arithmetic on the shared
+    // array keeps the state space, so the accesses compile to LDS / STS
+    Smem& sm = *reinterpret_cast<Smem*>(smraw_ + ((1024u - (smem_u32(smraw_) & 1023u)) & 1023u));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int ntiles = n_tiles(a.sl);  // 16-cell runs
+    const int nteams = gridDim.x * kTeams;
+    const bool jac = a.precond != 0;
+    for (int e = threadIdx.x; e < S * S; e += blockDim.x)
+        sm.alpha[alpha_at(e / S, e % S)] = a.coef[(e / S) * (S + 4) + e % S];
+    const int q = warp / kTeamWarps, w = warp % kTeamWarps;
+    const int first = blockIdx.x * kTeams + q;
+    const bool leader = w == 0 && lane == 0;
+    // run it of this team -> stage it % kStages
+    auto issue = [&](int it) {
+        const int grp = first + it * nteams;
+        if (grp >= ntiles) return;
+        const int s = it % kStages;
+        TileCells tc;
+        tile_cells(a.sl, grp, ntiles, tc);
+        unsigned char* st = sm.stage[q][s];
+        unsigned long long* bar = &sm.full[q][s];
+        mbar_expect_tx(bar, 2 * kArrBytes + (jac ? 128 : 0));
+        for (int p = 0; p < 4; ++p) {
+            tma_2d(st + p * kPanelBytes, &mapW, 16 * p, (int)tc.l0, bar);
+            tma_2d(st + kArrBytes + p * kPanelBytes, &mapR, 16 * p, (int)tc.l0, bar);
+        }
+        if (jac) bulk_g2s(sm.dinv[q][s], a.st.dinv + tc.g0, 128, bar);
+    };
+    if (leader) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&sm.full[q][s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int it = 0; it < kStages; ++it) issue(it);
+    }
+    __syncthreads();
+
+    switch (w) {
+        case 0: update64_warp<0>(sm, a, q, first, ntiles, nteams, jac, leader, issue); break;
+        case 1: update64_warp<1>(sm, a, q, first, ntiles, nteams, jac, leader, issue); break;
+        case 2: update64_warp<2>(sm, a, q, first, ntiles, nteams, jac, leader, issue); break;
+        default: update64_warp<3>(sm, a, q, first, ntiles, nteams, jac, leader, issue); break;
     }
 }
 
@@ -673,6 +751,267 @@ __global__ void __launch_bounds__(kSThreads, 1) k_spmm64_ws(SweepArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Role-split form of the stencil sweep (the default): one pencil stream per
+// CTA, 4 stencil warps + 4 Gram warps + 1 producer warp. The stencil warps
+// (one per SM sub-partition) form W for step u + 1 while the Gram warps (one
+// per sub-partition) run step u's 80 DMMAs, so every sub-partition always has
+// a warp issuing DMMA and the stencil's loads, SIMT FMAs and stores hide
+// behind it — in the two-team form a team's stencil, barrier and Gram phases
+// ran back to back and the FP64 pipe sat idle ~40 % of the time (ncu).
+// Same producer scheme as k_spmm64_ws with a deeper ring (kRS steps ahead);
+// the stencil -> Gram hand-off goes through kRG swizzled staging buffers with
+// full / empty mbarriers (4 arrivals: one per warp after __syncwarp).
+// Each Gram warp owns 5 of the 20 upper tiles for the whole sweep (one
+// accumulation chain per tile in step order): run-to-run deterministic.
+// ---------------------------------------------------------------------------
+// Per-run packed stencil coefficients (one bulk copy per step instead of six
+// 128-byte copies: measured 0.2 ms of a 1.3 ms sweep), negated as the
+// stencil uses them: [diag 16 | -cx of cells x0 - 1 .. x0 + 15 (17) | -cy
+// toward y - 1 (16) | -cy toward y + 1 (16) | -cz toward z - 1 (16) | -cz
+// toward z + 1 (16) | pad 3], zero across the domain boundary. Run T (global
+// x-run index) at T * kPC.
+constexpr int kPC = 100;
+constexpr int kPD = 0, kPXM = 16, kPYM = 33, kPYP = 49, kPZM = 65, kPZP = 81;
+__global__ void k_pack_coef64(Slab sl, StencilPtr st, double* __restrict__ out) {
+    const int ntx = sl.nx / 16;
+    const int64_t nrun = (int64_t)ntx * sl.ny * sl.nz;
+    const int64_t plane = (int64_t)sl.nx * sl.ny;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nrun * kPC;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t T = e / kPC;
+        const int k = (int)(e % kPC);
+        const int ix0 = 16 * (int)(T % ntx);
+        const int64_t q = T / ntx;
+        const int iy = (int)(q % sl.ny), iz = (int)(q / sl.ny);
+        const int64_t g0 = ix0 + (int64_t)sl.nx * (iy + (int64_t)sl.ny * iz);
+        double v = 0.0;
+        if (k < kPXM) {
+            v = st.diag[g0 + k];
+        } else if (k < kPYM) {
+            const int c = k - kPXM;  // cell x0 - 1 + c
+            if (ix0 + c - 1 >= 0) v = -st.cx[g0 + c - 1];
+        } else if (k < kPYP) {
+            if (iy > 0) v = -st.cy[g0 - sl.nx + (k - kPYM)];
+        } else if (k < kPZM) {
+            v = -st.cy[g0 + (k - kPYP)];
+        } else if (k < kPZP) {
+            if (iz > 0) v = -st.cz[g0 - plane + (k - kPZM)];
+        } else if (k < kPZP + 16) {
+            v = -st.cz[g0 + (k - kPZP)];
+        }
+        out[e] = v;
+    }
+}
+
+constexpr int kRS = 6;                          // input bundles in flight
+constexpr int kRC = kRS + 2;                    // centre-run slots
+constexpr int kRG = 2;                          // stencil -> Gram staging buffers
+constexpr int kRThreads = 9 * 32;
+struct SmemR {
+    unsigned char gst[kRG][2 * kArrBytes];      // P | W of a step, swizzled (1024-aligned)
+    double cring[kRC][kCRows * 64];             // centre P runs with x-halo cells
+    double yrun[kRS][2][16 * 64];               // y - 1 / y + 1 runs
+    double coef[kRS][kPC];
+    unsigned long long full[kRS], empty[kRS], gfull[kRG], gempty[kRG], pro;
+};
+constexpr size_t smem_bytes_r() { return sizeof(SmemR) + 1024; }
+
+// Gram warp W of the role-split sweep: consumes every staged step, then
+// writes its tiles of the CTA's partial G (and zeros in its share of the
+// lower tiles)
+template <int W>
+__device__ __forceinline__ void spmm_gram_warp(SmemR& sm, const SweepArgs& a, int nsteps) {
+    constexpr int S = 64;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    double gacc[5][4];
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) gacc[i][e] = 0.0;
+    const double one[4] = {1.0, 1.0, 1.0, 1.0};
+    for (int u = 0; u < nsteps; ++u) {
+        const int b = u % kRG;
+        mbar_wait(&sm.gfull[b], (u / kRG) & 1);
+        const unsigned char* Ut = sm.gst[b];
+        if (BK_EXP != 3) gram_run<W, false>(gacc, Ut, Ut + kArrBytes, one, g, t);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.gempty[b]);
+    }
+    double* out = a.part + (int64_t)blockIdx.x * (S * S);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        int gm, gn;
+        gram_tile_c<W>(i, gm, gn);
+        const int r0 = 16 * gm + g, c0 = 8 * gn + 2 * t;
+        out[r0 * S + c0] = gacc[i][0];
+        out[r0 * S + c0 + 1] = gacc[i][1];
+        out[(r0 + 8) * S + c0] = gacc[i][2];
+        out[(r0 + 8) * S + c0 + 1] = gacc[i][3];
+    }
+    for (int e = 32 * W + lane; e < S * S; e += 128)
+        if ((e % S) / 8 < 2 * ((e / S) / 16)) out[e] = 0.0;
+}
+
+__global__ void __launch_bounds__(kRThreads, 1) k_spmm64_rs(SweepArgs a) {
+    constexpr int S = 64;
+    extern __shared__ __align__(1024) unsigned char smraw_[];
+    SmemR& sm = *reinterpret_cast<SmemR*>(smraw_ + ((1024u - (smem_u32(smraw_) & 1023u)) & 1023u));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Slab& sl = a.sl;
+    const int nz = sl.nz;
+    const int npen = (sl.nx / 16) * sl.nyl;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kRS; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], kTeamWarps);
+        }
+        for (int s = 0; s < kRG; ++s) {
+            mbar_init(&sm.gfull[s], kTeamWarps);
+            mbar_init(&sm.gempty[s], kTeamWarps);
+        }
+        mbar_init(&sm.pro, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int first = blockIdx.x;
+    const int stride = gridDim.x;
+
+    if (warp == 8) {  // ---- producer
+        if (lane == 0 && first < npen) {
+            const int64_t plane = (int64_t)sl.nx * sl.ny;
+            const unsigned rowb = S * 8;
+            auto centre_bytes = [&](const Pencil& pc) -> unsigned {
+                const int lo = pc.ix0 > 0 ? -1 : 0, hi = pc.ix0 + 16 < sl.nx ? 16 : 15;
+                return (unsigned)(hi - lo + 1) * rowb;
+            };
+            auto centre = [&](const Pencil& pc, int z, int slot, unsigned long long* bar) {
+                const int lo = pc.ix0 > 0 ? -1 : 0, hi = pc.ix0 + 16 < sl.nx ? 16 : 15;
+                bulk_g2s(sm.cring[slot] + (1 + lo) * S, a.P + (pc.lrow(sl, z) + lo) * S,
+                         (unsigned)(hi - lo + 1) * rowb, bar);
+            };
+            int p = first, z = 0;
+            {
+                const Pencil pc = pencil_of(sl, p);
+                mbar_expect_tx(&sm.pro, centre_bytes(pc));
+                centre(pc, 0, 0, &sm.pro);
+            }
+            for (int u = 0;; ++u) {
+                const int s = u % kRS;
+                if (u >= kRS) mbar_wait(&sm.empty[s], ((u / kRS) - 1) & 1);
+                const Pencil pc = pencil_of(sl, p);
+                const int64_t g0 = pc.grow(sl, z), l0 = pc.lrow(sl, z);
+                unsigned long long* bar = &sm.full[s];
+                int pn = p, zn = z + 1;
+                if (zn == nz) {
+                    pn += stride;
+                    zn = 0;
+                }
+                const bool has_next = pn < npen;
+                const Pencil pcn = has_next ? pencil_of(sl, pn) : pc;
+                unsigned bytes = 2 * 16 * rowb + kPC * 8;
+                if (has_next) bytes += centre_bytes(pcn);
+                mbar_expect_tx(bar, bytes);
+                bulk_g2s(sm.yrun[s][0], a.P + (l0 - sl.nx) * S, 16 * rowb, bar);
+                bulk_g2s(sm.yrun[s][1], a.P + (l0 + sl.nx) * S, 16 * rowb, bar);
+                bulk_g2s(sm.coef[s], a.pcoef + (g0 / 16) * kPC, kPC * 8, bar);
+                if (has_next) centre(pcn, zn, (u + 1) % kRC, bar);
+                if (!has_next) break;
+                p = pn;
+                z = zn;
+            }
+        }
+        return;
+    }
+
+    if (warp < 4) {  // ---- stencil warps: thread = (cell r, column quad cq)
+        const int tt = threadIdx.x;  // 0..127
+        const int r = tt >> 3, cq = tt & 7;
+        if (first < npen) mbar_wait(&sm.pro, 0);
+        int u = 0;
+        // this thread's columns of its cell at planes z - 1, z, z + 1, kept in
+        // registers as the pencil marches (one centre-run load per step)
+        double2 pm[4], pz[4], pp1[4];
+        for (int pp = first; pp < npen; pp += stride) {
+            const Pencil pc = pencil_of(sl, pp);
+            const int ix = pc.ix0 + r;
+            for (int zz = 0; zz < nz; ++zz, ++u) {
+                const int s = u % kRS;
+                mbar_wait(&sm.full[s], (u / kRS) & 1);
+                const double* C0 = sm.cring[u % kRC];
+                const double* Cp = sm.cring[(u + 1) % kRC];
+                const double* Ym = sm.yrun[s][0];
+                const double* Yp = sm.yrun[s][1];
+                const double* cf = sm.coef[s];
+                const bool hzm = zz > 0, hzp = zz < nz - 1, hym = pc.iyg > 0, hyp = pc.iyg < sl.ny - 1;
+                const bool hxm = ix > 0, hxp = ix < sl.nx - 1;
+                const double czm = cf[kPZM + r], cym = cf[kPYM + r];
+                const double cxm = cf[kPXM + r], dg = cf[kPD + r];
+                const double cxp = cf[kPXM + r + 1], cyp = cf[kPYP + r];
+                const double czp = cf[kPZP + r];
+                double2 acc[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int c = 2 * cq + 16 * j;
+                    auto ld = [&](const double* row) {
+                        return *reinterpret_cast<const double2*>(row + c);
+                    };
+                    if (zz == 0) {
+                        pz[j] = ld(C0 + (1 + r) * S);
+                    } else {
+                        pm[j] = pz[j];
+                        pz[j] = pp1[j];
+                    }
+                    pp1[j] = hzp ? ld(Cp + (1 + r) * S) : make_double2(0.0, 0.0);
+                    double2 x = make_double2(0.0, 0.0);
+                    auto fm = [&](double cc, double2 v) {
+                        x.x = fma(cc, v.x, x.x);
+                        x.y = fma(cc, v.y, x.y);
+                    };
+                    if (hzm) fm(czm, pm[j]);
+                    if (hym) fm(cym, ld(Ym + r * S));
+                    if (hxm) fm(cxm, ld(C0 + r * S));
+                    fm(dg, pz[j]);
+                    if (hxp) fm(cxp, ld(C0 + (2 + r) * S));
+                    if (hyp) fm(cyp, ld(Yp + r * S));
+                    if (hzp) fm(czp, pp1[j]);
+                    acc[j] = x;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[s]);
+                const int64_t l = pc.lrow(sl, zz) + r;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (BK_EXP != 1) *reinterpret_cast<double2*>(a.W + l * S + 2 * cq + 16 * j) = acc[j];
+                const int b = u % kRG;
+                if (u >= kRG) mbar_wait(&sm.gempty[b], ((u / kRG) - 1) & 1);
+                unsigned char* Ut = sm.gst[b];
+                unsigned char* Vt = Ut + kArrBytes;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int c = 2 * cq + 16 * j;
+                    sts2(Ut, r, c, pz[j].x, pz[j].y);
+                    sts2(Vt, r, c, acc[j].x, acc[j].y);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.gfull[b]);
+            }
+        }
+        return;
+    }
+
+    // ---- Gram warps: G += P^T W, 5 of the 20 upper 16 x 8 tiles each
+    const int w = warp - 4;
+    const int npc = first < npen ? (npen - 1 - first) / stride + 1 : 0;
+    const int nsteps = npc * nz;
+    switch (w) {
+        case 0: spmm_gram_warp<0>(sm, a, nsteps); break;
+        case 1: spmm_gram_warp<1>(sm, a, nsteps); break;
+        case 2: spmm_gram_warp<2>(sm, a, nsteps); break;
+        default: spmm_gram_warp<3>(sm, a, nsteps); break;
+    }
+}
+
 inline PFN_cuTensorMapEncodeTiled_v12000 encoder() {
     static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void* p = nullptr;
@@ -727,11 +1066,19 @@ inline cudaError_t launch_pupdate64_ws(const SweepArgs& a, int64_t nloc, int nsm
     return cudaGetLastError();
 }
 
-// z-marching stencil sweep with the Gram (full 16-cell x-runs, 16-aligned x)
-inline cudaError_t launch_spmm64_ws(const SweepArgs& a, int nsm, cudaStream_t s) {
-    const size_t smem = sweep64::smem_bytes_s();
-    const cudaError_t e = bk::set_max_smem((const void*)sweep64::k_spmm64_ws, smem);
+// z-marching stencil sweep with the Gram (full 16-cell x-runs, 16-aligned x):
+// the role-split kernel, or (teams = true) the two-team form
+inline cudaError_t launch_spmm64_ws(const SweepArgs& a, int nsm, cudaStream_t s, bool teams = false) {
+    if (teams) {
+        const size_t smem = sweep64::smem_bytes_s();
+        const cudaError_t e = bk::set_max_smem((const void*)sweep64::k_spmm64_ws, smem);
+        if (e != cudaSuccess) return e;
+        sweep64::k_spmm64_ws<<<nsm, sweep64::kSThreads, smem, s>>>(a);
+        return cudaGetLastError();
+    }
+    const size_t smem = sweep64::smem_bytes_r();
+    const cudaError_t e = bk::set_max_smem((const void*)sweep64::k_spmm64_rs, smem);
     if (e != cudaSuccess) return e;
-    sweep64::k_spmm64_ws<<<nsm, sweep64::kSThreads, smem, s>>>(a);
+    sweep64::k_spmm64_rs<<<nsm, sweep64::kRThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
