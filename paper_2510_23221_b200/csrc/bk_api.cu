@@ -801,6 +801,7 @@ bk_status bk_set_option(bk_ctx* ctx, const char* name, int value) {
     else if (k == "no_ws_spmm") ctx->knobs.no_ws_spmm = value != 0;
     else if (k == "graph_loop") ctx->knobs.graph_loop = value != 0;
     else if (k == "spmm_teams") ctx->knobs.spmm_teams = value != 0;
+    else if (k == "spmm_band") ctx->knobs.spmm_band = value;
     else return fail(ctx, BK_INVALID_CONFIG, "bk_set_option: unknown option " + k);
     return BK_OK;
 }

@@ -1301,7 +1301,8 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
         halo(a.P);
         phase_mark(ctx, -1);
         if (ws_spmm) {
-            BK_CUDA_TRY(ctx, launch_spmm64_ws(a, nbs, s, ctx->knobs.spmm_teams));
+            BK_CUDA_TRY(ctx, launch_spmm64_ws(a, nbs, s, ctx->knobs.spmm_teams,
+                                              ctx->knobs.spmm_band > 0 ? ctx->knobs.spmm_band : 4));
         } else {
             BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s, ctx->knobs.no_tma_spmm));
         }

@@ -765,12 +765,13 @@ __global__ void __launch_bounds__(kSThreads, 1) k_spmm64_ws(SweepArgs a) {
 // Each Gram warp owns 5 of the 20 upper tiles for the whole sweep (one
 // accumulation chain per tile in step order): run-to-run deterministic.
 // ---------------------------------------------------------------------------
-// Per-run packed stencil coefficients (one bulk copy per step instead of six
-// 128-byte copies: measured 0.2 ms of a 1.3 ms sweep), negated as the
-// stencil uses them: [diag 16 | -cx of cells x0 - 1 .. x0 + 15 (17) | -cy
+// Per-run packed stencil coefficients (one bulk copy per band step instead of
+// six 128-byte copies per run: measured 0.2 ms of a 1.3 ms sweep), negated as
+// the stencil uses them: [diag 16 | -cx of cells x0 - 1 .. x0 + 15 (17) | -cy
 // toward y - 1 (16) | -cy toward y + 1 (16) | -cz toward z - 1 (16) | -cz
-// toward z + 1 (16) | pad 3], zero across the domain boundary. Run T (global
-// x-run index) at T * kPC.
+// toward z + 1 (16) | pad 3], zero across the domain boundary. The run at
+// (x-run xr, row y, plane z) sits at ((xr nz + z) ny + y) kPC, so the runs of
+// a y-band at one plane are contiguous.
 constexpr int kPC = 100;
 constexpr int kPD = 0, kPXM = 16, kPYM = 33, kPYP = 49, kPZM = 65, kPZP = 81;
 __global__ void k_pack_coef64(Slab sl, StencilPtr st, double* __restrict__ out) {
@@ -781,9 +782,9 @@ __global__ void k_pack_coef64(Slab sl, StencilPtr st, double* __restrict__ out) 
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t T = e / kPC;
         const int k = (int)(e % kPC);
-        const int ix0 = 16 * (int)(T % ntx);
-        const int64_t q = T / ntx;
-        const int iy = (int)(q % sl.ny), iz = (int)(q / sl.ny);
+        const int iy = (int)(T % sl.ny);
+        const int64_t q = T / sl.ny;
+        const int iz = (int)(q % sl.nz), ix0 = 16 * (int)(q / sl.nz);
         const int64_t g0 = ix0 + (int64_t)sl.nx * (iy + (int64_t)sl.ny * iz);
         double v = 0.0;
         if (k < kPXM) {
@@ -804,24 +805,45 @@ __global__ void k_pack_coef64(Slab sl, StencilPtr st, double* __restrict__ out) 
     }
 }
 
-constexpr int kRS = 6;                          // input bundles in flight
-constexpr int kRC = kRS + 2;                    // centre-run slots
+// ---------------------------------------------------------------------------
+// Role-split, y-banded form of the stencil sweep (the default). Work unit: a
+// band of B x-runs adjacent in y (same x, rows y0 .. y0 + B - 1), marched
+// through z. Per band step the producer brings the B centre runs of the next
+// plane (with x-halo cells), the two y-halo runs and the band's packed
+// coefficients (B + 3 copies): a run reaches the SM (B + 2) / B times instead
+// of 3 times — the sweep was bound by L2 -> SM delivery (ncu: with the Gram
+// removed it still took 1.19 of 1.32 ms).
+// 4 stencil warps (thread = cell r x column quad cq, looping over the band's
+// runs) + 4 Gram warps + 1 producer warp: every SM sub-partition always has a
+// Gram warp issuing DMMA while its stencil warp loads / stores. Stencil ->
+// Gram hand-off per run through kRG swizzled staging buffers with full /
+// empty mbarriers (4 arrivals: one per warp after __syncwarp). Each Gram warp
+// owns 5 of the 20 upper tiles for the whole sweep (one accumulation chain per
+// tile in run order): run-to-run deterministic.
+// ---------------------------------------------------------------------------
+template <int B>
+struct Band {
+    static constexpr int RS = B == 1 ? 6 : B == 2 ? 4 : 2;  // input bundles in flight
+    static constexpr int RC = RS + 2;                         // centre-plane slots
+};
 constexpr int kRG = 2;                          // stencil -> Gram staging buffers
 constexpr int kRThreads = 9 * 32;
+template <int B>
 struct SmemR {
-    unsigned char gst[kRG][2 * kArrBytes];      // P | W of a step, swizzled (1024-aligned)
-    double cring[kRC][kCRows * 64];             // centre P runs with x-halo cells
-    double yrun[kRS][2][16 * 64];               // y - 1 / y + 1 runs
-    double coef[kRS][kPC];
-    unsigned long long full[kRS], empty[kRS], gfull[kRG], gempty[kRG], pro;
+    static constexpr int RS = Band<B>::RS, RC = Band<B>::RC;
+    unsigned char gst[kRG][2 * kArrBytes];      // P | W of a run, swizzled (1024-aligned)
+    double cring[RC][B][kCRows * 64];           // centre runs with x-halo cells, per plane
+    double yrun[RS][2][16 * 64];                // y - 1 / y + B halo runs
+    double coef[RS][B * kPC];
+    unsigned long long full[RS], empty[RS], gfull[kRG], gempty[kRG], pro;
 };
-constexpr size_t smem_bytes_r() { return sizeof(SmemR) + 1024; }
+template <int B>
+constexpr size_t smem_bytes_r() { return sizeof(SmemR<B>) + 1024; }
 
-// Gram warp W of the role-split sweep: consumes every staged step, then
-// writes its tiles of the CTA's partial G (and zeros in its share of the
-// lower tiles)
-template <int W>
-__device__ __forceinline__ void spmm_gram_warp(SmemR& sm, const SweepArgs& a, int nsteps) {
+// Gram warp W: consumes every staged run, then writes its tiles of the CTA's
+// partial G (and zeros in its share of the lower tiles)
+template <int W, int B>
+__device__ __forceinline__ void spmm_gram_warp(SmemR<B>& sm, const SweepArgs& a, int nruns) {
     constexpr int S = 64;
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     double gacc[5][4];
@@ -830,9 +852,9 @@ __device__ __forceinline__ void spmm_gram_warp(SmemR& sm, const SweepArgs& a, in
 #pragma unroll
         for (int e = 0; e < 4; ++e) gacc[i][e] = 0.0;
     const double one[4] = {1.0, 1.0, 1.0, 1.0};
-    for (int u = 0; u < nsteps; ++u) {
-        const int b = u % kRG;
-        mbar_wait(&sm.gfull[b], (u / kRG) & 1);
+    for (int v = 0; v < nruns; ++v) {
+        const int b = v % kRG;
+        mbar_wait(&sm.gfull[b], (v / kRG) & 1);
         const unsigned char* Ut = sm.gst[b];
         if (BK_EXP != 3) gram_run<W, false>(gacc, Ut, Ut + kArrBytes, one, g, t);
         __syncwarp();
@@ -853,16 +875,25 @@ __device__ __forceinline__ void spmm_gram_warp(SmemR& sm, const SweepArgs& a, in
         if ((e % S) / 8 < 2 * ((e / S) / 16)) out[e] = 0.0;
 }
 
+template <int B>
 __global__ void __launch_bounds__(kRThreads, 1) k_spmm64_rs(SweepArgs a) {
     constexpr int S = 64;
+    constexpr int RS = Band<B>::RS, RC = Band<B>::RC;
     extern __shared__ __align__(1024) unsigned char smraw_[];
-    SmemR& sm = *reinterpret_cast<SmemR*>(smraw_ + ((1024u - (smem_u32(smraw_) & 1023u)) & 1023u));
+    SmemR<B>& sm =
+        *reinterpret_cast<SmemR<B>*>(smraw_ + ((1024u - (smem_u32(smraw_) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Slab& sl = a.sl;
     const int nz = sl.nz;
-    const int npen = (sl.nx / 16) * sl.nyl;
+    const int ntx = sl.nx / 16;
+    const int nband = ntx * (sl.nyl / B);
+    // band -> (x-run, first slab-local row); rows y0 .. y0 + B - 1
+    auto band_of = [&](int bd, int& ix0, int& iyl0) {
+        ix0 = 16 * (bd % ntx);
+        iyl0 = 1 + B * (bd / ntx);
+    };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kRS; ++s) {
+        for (int s = 0; s < RS; ++s) {
             mbar_init(&sm.full[s], 1);
             mbar_init(&sm.empty[s], kTeamWarps);
         }
@@ -876,139 +907,169 @@ __global__ void __launch_bounds__(kRThreads, 1) k_spmm64_rs(SweepArgs a) {
     __syncthreads();
     const int first = blockIdx.x;
     const int stride = gridDim.x;
+    const int64_t nxl = sl.nx, plane_l = (int64_t)sl.nx * (sl.nyl + 2);
 
     if (warp == 8) {  // ---- producer
-        if (lane == 0 && first < npen) {
-            const int64_t plane = (int64_t)sl.nx * sl.ny;
+        if (lane == 0 && first < nband) {
             const unsigned rowb = S * 8;
-            auto centre_bytes = [&](const Pencil& pc) -> unsigned {
-                const int lo = pc.ix0 > 0 ? -1 : 0, hi = pc.ix0 + 16 < sl.nx ? 16 : 15;
-                return (unsigned)(hi - lo + 1) * rowb;
+            int ix0, iyl0;
+            const int lo_x = 0;  // centre rows x0 - 1 .. x0 + 16, clipped to the grid
+            (void)lo_x;
+            auto cbytes = [&](int x0) -> unsigned {
+                const int lo = x0 > 0 ? -1 : 0, hi = x0 + 16 < sl.nx ? 16 : 15;
+                return (unsigned)(hi - lo + 1) * rowb * B;
             };
-            auto centre = [&](const Pencil& pc, int z, int slot, unsigned long long* bar) {
-                const int lo = pc.ix0 > 0 ? -1 : 0, hi = pc.ix0 + 16 < sl.nx ? 16 : 15;
-                bulk_g2s(sm.cring[slot] + (1 + lo) * S, a.P + (pc.lrow(sl, z) + lo) * S,
-                         (unsigned)(hi - lo + 1) * rowb, bar);
+            // the band's B centre runs of plane z into ring slot `slot`
+            auto centres = [&](int x0, int y0l, int z, int slot, unsigned long long* bar) {
+                const int lo = x0 > 0 ? -1 : 0, hi = x0 + 16 < sl.nx ? 16 : 15;
+#pragma unroll 1
+                for (int b = 0; b < B; ++b) {
+                    const int64_t l = x0 + nxl * (y0l + b) + plane_l * z;
+                    bulk_g2s(sm.cring[slot][b] + (1 + lo) * S, a.P + (l + lo) * S,
+                             (unsigned)(hi - lo + 1) * rowb, bar);
+                }
             };
-            int p = first, z = 0;
-            {
-                const Pencil pc = pencil_of(sl, p);
-                mbar_expect_tx(&sm.pro, centre_bytes(pc));
-                centre(pc, 0, 0, &sm.pro);
-            }
+            int bd = first, z = 0;
+            band_of(bd, ix0, iyl0);
+            mbar_expect_tx(&sm.pro, cbytes(ix0));
+            centres(ix0, iyl0, 0, 0, &sm.pro);
             for (int u = 0;; ++u) {
-                const int s = u % kRS;
-                if (u >= kRS) mbar_wait(&sm.empty[s], ((u / kRS) - 1) & 1);
-                const Pencil pc = pencil_of(sl, p);
-                const int64_t g0 = pc.grow(sl, z), l0 = pc.lrow(sl, z);
+                const int s = u % RS;
+                if (u >= RS) mbar_wait(&sm.empty[s], ((u / RS) - 1) & 1);
+                const int64_t l0 = ix0 + nxl * iyl0 + plane_l * z;  // first run of the band
+                const int iyg0 = sl.y0 + iyl0 - 1;
                 unsigned long long* bar = &sm.full[s];
-                int pn = p, zn = z + 1;
+                int bn = bd, zn = z + 1;
                 if (zn == nz) {
-                    pn += stride;
+                    bn += stride;
                     zn = 0;
                 }
-                const bool has_next = pn < npen;
-                const Pencil pcn = has_next ? pencil_of(sl, pn) : pc;
-                unsigned bytes = 2 * 16 * rowb + kPC * 8;
-                if (has_next) bytes += centre_bytes(pcn);
+                const bool has_next = bn < nband;
+                int nx0 = ix0, ny0 = iyl0;
+                if (has_next) band_of(bn, nx0, ny0);
+                unsigned bytes = 2 * 16 * rowb + B * kPC * 8;
+                if (has_next) bytes += cbytes(nx0);
                 mbar_expect_tx(bar, bytes);
-                bulk_g2s(sm.yrun[s][0], a.P + (l0 - sl.nx) * S, 16 * rowb, bar);
-                bulk_g2s(sm.yrun[s][1], a.P + (l0 + sl.nx) * S, 16 * rowb, bar);
-                bulk_g2s(sm.coef[s], a.pcoef + (g0 / 16) * kPC, kPC * 8, bar);
-                if (has_next) centre(pcn, zn, (u + 1) % kRC, bar);
+                bulk_g2s(sm.yrun[s][0], a.P + (l0 - nxl) * S, 16 * rowb, bar);
+                bulk_g2s(sm.yrun[s][1], a.P + (l0 + B * nxl) * S, 16 * rowb, bar);
+                bulk_g2s(sm.coef[s], a.pcoef + (((int64_t)(ix0 / 16) * nz + z) * sl.ny + iyg0) * kPC,
+                         B * kPC * 8, bar);
+                if (has_next) centres(nx0, ny0, zn, (u + 1) % RC, bar);
                 if (!has_next) break;
-                p = pn;
+                bd = bn;
                 z = zn;
+                ix0 = nx0;
+                iyl0 = ny0;
             }
         }
         return;
     }
 
-    if (warp < 4) {  // ---- stencil warps: thread = (cell r, column quad cq)
+    const int nbands = first < nband ? (nband - 1 - first) / stride + 1 : 0;
+    if (warp < 4) {  // ---- stencil warps: thread = (cell r, column quad cq) of every run
         const int tt = threadIdx.x;  // 0..127
         const int r = tt >> 3, cq = tt & 7;
-        if (first < npen) mbar_wait(&sm.pro, 0);
-        int u = 0;
-        // this thread's columns of its cell at planes z - 1, z, z + 1, kept in
-        // registers as the pencil marches (one centre-run load per step)
-        double2 pm[4], pz[4], pp1[4];
-        for (int pp = first; pp < npen; pp += stride) {
-            const Pencil pc = pencil_of(sl, pp);
-            const int ix = pc.ix0 + r;
+        if (nbands) mbar_wait(&sm.pro, 0);
+        int u = 0, v = 0;  // band steps, runs
+        // this thread's columns of its cell of run b at planes z and z + 1,
+        // kept in registers as the band marches (B <= 2; the z - 1 plane is
+        // read back from the ring, B = 4 reads all three from the ring)
+        constexpr bool ROT = B <= 2;
+        double2 pz[ROT ? B : 1][4], pp1[ROT ? B : 1][4];
+        for (int bd = first; bd < nband; bd += stride) {
+            int ix0, iyl0;
+            band_of(bd, ix0, iyl0);
+            const int ix = ix0 + r;
+            const int iyg0 = sl.y0 + iyl0 - 1;
+            const bool hxm = ix > 0, hxp = ix < sl.nx - 1;
             for (int zz = 0; zz < nz; ++zz, ++u) {
-                const int s = u % kRS;
-                mbar_wait(&sm.full[s], (u / kRS) & 1);
-                const double* C0 = sm.cring[u % kRC];
-                const double* Cp = sm.cring[(u + 1) % kRC];
-                const double* Ym = sm.yrun[s][0];
-                const double* Yp = sm.yrun[s][1];
-                const double* cf = sm.coef[s];
-                const bool hzm = zz > 0, hzp = zz < nz - 1, hym = pc.iyg > 0, hyp = pc.iyg < sl.ny - 1;
-                const bool hxm = ix > 0, hxp = ix < sl.nx - 1;
-                const double czm = cf[kPZM + r], cym = cf[kPYM + r];
-                const double cxm = cf[kPXM + r], dg = cf[kPD + r];
-                const double cxp = cf[kPXM + r + 1], cyp = cf[kPYP + r];
-                const double czp = cf[kPZP + r];
-                double2 acc[4];
+                const int s = u % RS;
+                mbar_wait(&sm.full[s], (u / RS) & 1);
+                const bool hzm = zz > 0, hzp = zz < nz - 1;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int c = 2 * cq + 16 * j;
-                    auto ld = [&](const double* row) {
-                        return *reinterpret_cast<const double2*>(row + c);
-                    };
-                    if (zz == 0) {
-                        pz[j] = ld(C0 + (1 + r) * S);
-                    } else {
-                        pm[j] = pz[j];
-                        pz[j] = pp1[j];
+                for (int b = 0; b < B; ++b) {
+                    const double* C0 = sm.cring[u % RC][b];
+                    const double* Cm = sm.cring[(u + RC - 1) % RC][b];
+                    const double* Cp = sm.cring[(u + 1) % RC][b];
+                    const double* Ym = b == 0 ? sm.yrun[s][0] : sm.cring[u % RC][b - 1] + S;
+                    const double* Yp = b == B - 1 ? sm.yrun[s][1] : sm.cring[u % RC][b + 1] + S;
+                    const double* cf = sm.coef[s] + b * kPC;
+                    const bool hym = iyg0 + b > 0, hyp = iyg0 + b < sl.ny - 1;
+                    const double czm = cf[kPZM + r], cym = cf[kPYM + r];
+                    const double cxm = cf[kPXM + r], dg = cf[kPD + r];
+                    const double cxp = cf[kPXM + r + 1], cyp = cf[kPYP + r];
+                    const double czp = cf[kPZP + r];
+                    double2 acc[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int c = 2 * cq + 16 * j;
+                        auto ld = [&](const double* row) {
+                            return *reinterpret_cast<const double2*>(row + c);
+                        };
+                        double2 cz, cp;
+                        if constexpr (ROT) {
+                            if (zz == 0)
+                                pz[b][j] = ld(C0 + (1 + r) * S);
+                            else
+                                pz[b][j] = pp1[b][j];
+                            pp1[b][j] = hzp ? ld(Cp + (1 + r) * S) : make_double2(0.0, 0.0);
+                            cz = pz[b][j];
+                            cp = pp1[b][j];
+                        } else {
+                            cz = ld(C0 + (1 + r) * S);
+                            cp = hzp ? ld(Cp + (1 + r) * S) : make_double2(0.0, 0.0);
+                            pz[0][j] = cz;  // staged below
+                        }
+                        double2 x = make_double2(0.0, 0.0);
+                        auto fm = [&](double cc, double2 w2) {
+                            x.x = fma(cc, w2.x, x.x);
+                            x.y = fma(cc, w2.y, x.y);
+                        };
+                        if (hzm) fm(czm, ld(Cm + (1 + r) * S));
+                        if (hym) fm(cym, ld(Ym + r * S));
+                        if (hxm) fm(cxm, ld(C0 + r * S));
+                        fm(dg, cz);
+                        if (hxp) fm(cxp, ld(C0 + (2 + r) * S));
+                        if (hyp) fm(cyp, ld(Yp + r * S));
+                        if (hzp) fm(czp, cp);
+                        acc[j] = x;
                     }
-                    pp1[j] = hzp ? ld(Cp + (1 + r) * S) : make_double2(0.0, 0.0);
-                    double2 x = make_double2(0.0, 0.0);
-                    auto fm = [&](double cc, double2 v) {
-                        x.x = fma(cc, v.x, x.x);
-                        x.y = fma(cc, v.y, x.y);
-                    };
-                    if (hzm) fm(czm, pm[j]);
-                    if (hym) fm(cym, ld(Ym + r * S));
-                    if (hxm) fm(cxm, ld(C0 + r * S));
-                    fm(dg, pz[j]);
-                    if (hxp) fm(cxp, ld(C0 + (2 + r) * S));
-                    if (hyp) fm(cyp, ld(Yp + r * S));
-                    if (hzp) fm(czp, pp1[j]);
-                    acc[j] = x;
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.empty[s]);
-                const int64_t l = pc.lrow(sl, zz) + r;
+                    if (b == B - 1) {  // the bundle is no longer read
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&sm.empty[s]);
+                    }
+                    const int64_t l = ix0 + nxl * (iyl0 + b) + plane_l * zz + r;
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (BK_EXP != 1) *reinterpret_cast<double2*>(a.W + l * S + 2 * cq + 16 * j) = acc[j];
-                const int b = u % kRG;
-                if (u >= kRG) mbar_wait(&sm.gempty[b], ((u / kRG) - 1) & 1);
-                unsigned char* Ut = sm.gst[b];
-                unsigned char* Vt = Ut + kArrBytes;
+                    for (int j = 0; j < 4; ++j)
+                        if (BK_EXP != 1)
+                            *reinterpret_cast<double2*>(a.W + l * S + 2 * cq + 16 * j) = acc[j];
+                    const int gb = v % kRG;
+                    if (v >= kRG) mbar_wait(&sm.gempty[gb], ((v / kRG) - 1) & 1);
+                    unsigned char* Ut = sm.gst[gb];
+                    unsigned char* Vt = Ut + kArrBytes;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int c = 2 * cq + 16 * j;
-                    sts2(Ut, r, c, pz[j].x, pz[j].y);
-                    sts2(Vt, r, c, acc[j].x, acc[j].y);
+                    for (int j = 0; j < 4; ++j) {
+                        const int c = 2 * cq + 16 * j;
+                        const double2 pc = pz[ROT ? b : 0][j];
+                        sts2(Ut, r, c, pc.x, pc.y);
+                        sts2(Vt, r, c, acc[j].x, acc[j].y);
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sm.gfull[gb]);
+                    ++v;
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.gfull[b]);
             }
         }
         return;
     }
 
     // ---- Gram warps: G += P^T W, 5 of the 20 upper 16 x 8 tiles each
-    const int w = warp - 4;
-    const int npc = first < npen ? (npen - 1 - first) / stride + 1 : 0;
-    const int nsteps = npc * nz;
-    switch (w) {
-        case 0: spmm_gram_warp<0>(sm, a, nsteps); break;
-        case 1: spmm_gram_warp<1>(sm, a, nsteps); break;
-        case 2: spmm_gram_warp<2>(sm, a, nsteps); break;
-        default: spmm_gram_warp<3>(sm, a, nsteps); break;
+    const int nruns = nbands * nz * B;
+    switch (warp - 4) {
+        case 0: spmm_gram_warp<0>(sm, a, nruns); break;
+        case 1: spmm_gram_warp<1>(sm, a, nruns); break;
+        case 2: spmm_gram_warp<2>(sm, a, nruns); break;
+        default: spmm_gram_warp<3>(sm, a, nruns); break;
     }
 }
 
@@ -1068,7 +1129,8 @@ inline cudaError_t launch_pupdate64_ws(const SweepArgs& a, int64_t nloc, int nsm
 
 // z-marching stencil sweep with the Gram (full 16-cell x-runs, 16-aligned x):
 // the role-split kernel, or (teams = true) the two-team form
-inline cudaError_t launch_spmm64_ws(const SweepArgs& a, int nsm, cudaStream_t s, bool teams = false) {
+inline cudaError_t launch_spmm64_ws(const SweepArgs& a, int nsm, cudaStream_t s, bool teams = false,
+                                    int band = 2) {
     if (teams) {
         const size_t smem = sweep64::smem_bytes_s();
         const cudaError_t e = bk::set_max_smem((const void*)sweep64::k_spmm64_ws, smem);
@@ -1076,9 +1138,13 @@ inline cudaError_t launch_spmm64_ws(const SweepArgs& a, int nsm, cudaStream_t s,
         sweep64::k_spmm64_ws<<<nsm, sweep64::kSThreads, smem, s>>>(a);
         return cudaGetLastError();
     }
-    const size_t smem = sweep64::smem_bytes_r();
-    const cudaError_t e = bk::set_max_smem((const void*)sweep64::k_spmm64_rs, smem);
-    if (e != cudaSuccess) return e;
-    sweep64::k_spmm64_rs<<<nsm, sweep64::kRThreads, smem, s>>>(a);
-    return cudaGetLastError();
+    auto go = [&](auto kern, size_t smem) {
+        const cudaError_t e = bk::set_max_smem((const void*)kern, smem);
+        if (e != cudaSuccess) return e;
+        kern<<<nsm, sweep64::kRThreads, smem, s>>>(a);
+        return cudaGetLastError();
+    };
+    if (band == 4 && a.sl.nyl % 4 == 0) return go(sweep64::k_spmm64_rs<4>, sweep64::smem_bytes_r<4>());
+    if (band >= 2 && a.sl.nyl % 2 == 0) return go(sweep64::k_spmm64_rs<2>, sweep64::smem_bytes_r<2>());
+    return go(sweep64::k_spmm64_rs<1>, sweep64::smem_bytes_r<1>());
 }

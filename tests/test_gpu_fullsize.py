@@ -175,8 +175,9 @@ def test_c5_capped_iterates_vs_reference(bk, ctx, c5_chip):
                     reason="c5_full_cg.npz not generated")
 def test_c5_full_vs_reference_cg(bk, ctx, c5_chip):
     """C5 full solve at the pinned 1e-10 against the reference's per-column cg
-    (solvers.cpp:82-171) at 1e-12: X and (T, q) of samples 0, 1, 2499, 4999
-    within 1e-9."""
+    (solvers.cpp:82-171) run to 1e-11 on all 64 columns (3136-3288 iterations
+    each, tests/golden/make_golden_full.py c5-cg): X and (T, q) of samples 0,
+    1, 2499, 4999 within 1e-9."""
     d = golden("c5_full_cg.npz")
     assert sha(c5_chip) == str(d["input_sha256"])
     op, X, rep = solve_full(bk, ctx, c5_chip, 1e-10)

@@ -328,7 +328,9 @@ def test_reference_cg_stalls_at_fp64_floor_on_c2_direct_columns(reference, oracl
 
 @pytest.mark.parametrize("name,case", [("c3_full.npz", (3, 128, 128, 8, 32, 5000, 0)),
                                        ("c4_full.npz", (4, 128, 128, 4, 16, 8, 0)),
-                                       ("c4_full.npz", (4, 128, 128, 4, 16, 8, 4))])
+                                       ("c4_full.npz", (4, 128, 128, 4, 16, 8, 4)),
+                                       ("c5_capped.npz", (5, 512, 512, 16, 64, 5000, 0)),
+                                       ("c5_full_cg.npz", (5, 512, 512, 16, 64, 5000, 0))])
 def test_full_size_golden_inputs_match_generator(oracle, name, case):
     """The full-size goldens were computed on the generator's current bytes."""
     d = golden(name)
@@ -336,5 +338,5 @@ def test_full_size_golden_inputs_match_generator(oracle, name, case):
     h = hashlib.sha256()
     for a in (ch.k, ch.q_basis, ch.coef):
         h.update(np.ascontiguousarray(a).tobytes())
-    key = "input_sha256" if name == "c3_full.npz" else f"chip{case[6]}_input_sha256"
+    key = "input_sha256" if name != "c4_full.npz" else f"chip{case[6]}_input_sha256"
     assert h.hexdigest() == str(d[key])
