@@ -802,6 +802,7 @@ bk_status bk_set_option(bk_ctx* ctx, const char* name, int value) {
     else if (k == "graph_loop") ctx->knobs.graph_loop = value != 0;
     else if (k == "spmm_teams") ctx->knobs.spmm_teams = value != 0;
     else if (k == "spmm_band") ctx->knobs.spmm_band = value;
+    else if (k == "comb_one_role") ctx->knobs.comb_one_role = value != 0;
     else return fail(ctx, BK_INVALID_CONFIG, "bk_set_option: unknown option " + k);
     return BK_OK;
 }

@@ -136,6 +136,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
         "r"(phase)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // 4D tiled TMA load: box (PW, 34, 10, 1) at (col, x0 - 1, y0 - 1, z)
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             int c2, int c3, unsigned long long* bar) {
@@ -591,6 +594,291 @@ __global__ void __launch_bounds__(NT_, Shape<NS, NT_>::CTAS)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Single-plane grids with one panel per plane (S <= 16: configs 1 and 2):
+// warp-specialised form (C2, 2048 samples: 0.66 ms vs 0.71 ms one-role). 4 former warps build T of a work
+// item's halo plane on DMMA into a two-buffer ring while 8 stencil warps apply
+// the operator to the previous item and stream T / q out, so the HBM writes,
+// the DMMA chains and the stencil's shared-memory loads of different items
+// overlap (the one-role kernel ran them back to back: ncu C2, FP64 pipe 21 %,
+// 4 CTA barriers per item). Same arithmetic as combine_action_kernel<.., PL>
+// (bitwise the same T, q and residual partials): former warp w owns m-tiles
+// w, w + 4, ...; the stencil warps map thread = (cell pair, sample half)
+// exactly as that kernel's 8 warps do.
+// Hand-offs: tfull[b] (NF former arrivals) / tempty[b] (stencil-warp arrivals)
+// per ring buffer; the panel (the tile's X halo) is reloaded by TMA when the
+// former warps reach a new tile (named barrier 1 among them first); the
+// residual reduction needs one named barrier (2) among the stencil warps per
+// item, with a two-buffer partial array.
+// ---------------------------------------------------------------------------
+template <int S, int NS, int NQ, int NF, int NR>
+__global__ void __launch_bounds__(32 * NF + 128 * NQ, 1)
+    combine_action_pl_ws(const __grid_constant__ CUtensorMap tmx, ActArgs a) {
+    using P = Panel<S>;
+    static_assert(P::R == 1, "one panel per plane");
+    // NQ sample groups of the stencil warps (4 NQ warps, thread = cell pair x
+    // sample group of SPT samples): more warps = more independent FP64 chains
+    constexpr int NB = NS / 8, SPT = NS / NQ, V = 2 * SPT, NSW = 4 * NQ;
+    // ring sample stride 2 mod 8: the former warps' T stores (lanes: 8 halo
+    // cells x 4 sample pairs) are conflict-free
+    constexpr int HXR = 36, HCR = HY * 36 + 2;
+    extern __shared__ unsigned char smraw[];
+    unsigned char* panel = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
+    double* ring = reinterpret_cast<double*>(panel + P::SLOT);  // 2 x NS x HCR
+    double* red = ring + NR * NS * HCR;                          // 2 x NSW warps x V
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(red + 2 * NSW * V);
+    unsigned long long* tfull = bar;        // [NR]
+    unsigned long long* tempty = bar + NR;  // [NR]
+    unsigned long long* pbar = bar + 2 * NR;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    if (tid == 0) {
+        for (int b = 0; b < NR; ++b) {
+            mbar_init(&tfull[b], NF);
+            mbar_init(&tempty[b], NSW);
+        }
+        mbar_init(pbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int i_begin = (int)((int64_t)blockIdx.x * a.items / gridDim.x);
+    const int i_end = (int)((int64_t)(blockIdx.x + 1) * a.items / gridDim.x);
+    auto ridx = [&](int hh) { return (hh / HX) * HXR + hh % HX + 1; };
+
+    if (warp < NF) {  // ---- former warps
+        int cur_tile = -1;
+        unsigned pph = 0;
+        // B fragments (coefficients C) of the next item, loaded one item ahead
+        // so the global-load latency hides behind this item's DMMA chains
+        double bfn[P::PW / 4][NB];
+        auto load_bf = [&](int item) {
+            const int64_t jn = (int64_t)(item % a.chunks) * NS;
+#pragma unroll
+            for (int kk = 0; kk < P::PW / 4; ++kk)
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb) {
+                    const int k = 4 * kk + t;
+                    const int64_t q = jn + 8 * nb + g;
+                    bfn[kk][nb] =
+                        (item < i_end && k < a.s && q < a.N) ? a.C[(int64_t)k * a.ldc + q] : 0.0;
+                }
+        };
+        load_bf(i_begin);
+        for (int item = i_begin, it = 0; item < i_end; ++item, ++it) {
+            const int tile = item / a.chunks, chunk = item % a.chunks;
+            const int x0 = (tile % a.tilesx) * TX, y0 = (tile / a.tilesx) * TY;
+            const int64_t j0 = (int64_t)chunk * NS;
+            const int b = it % NR;
+            if (it >= NR) mbar_wait(&tempty[b], ((it / NR) - 1) & 1);
+            if (tile != cur_tile) {  // every former warp is done with the old panel
+                asm volatile("bar.sync 1, %0;" ::"n"(NF * 32) : "memory");
+                if (tid == 0) {
+                    mbar_expect_tx(pbar, P::BYTES);
+                    tma_load_4d(panel, &tmx, 0, x0 - 1, y0 - 1 + a.ty, 0, pbar);
+                }
+                mbar_wait(pbar, pph);
+                pph ^= 1u;
+                cur_tile = tile;
+            }
+            double bf[P::PW / 4][NB];
+#pragma unroll
+            for (int kk = 0; kk < P::PW / 4; ++kk)
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb) bf[kk][nb] = bfn[kk][nb];
+            load_bf(item + 1);
+            double* buf = ring + b * NS * HCR;
+            for (int mt = warp; mt < MT; mt += NF) {
+                double ac[NB][4];
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) ac[nb][e] = 0.0;
+                const int h0 = 16 * mt + g;
+                const unsigned off0 = (unsigned)h0 * (P::PW * 8);
+                const unsigned xr = ((off0 >> 7) & P::SWM) << 4;
+                const unsigned char* r0p = panel + off0;
+                const bool v0 = h0 < HC, v1 = h0 + 8 < HC;
+#pragma unroll
+                for (int kk = 0; kk < P::PW / 4; ++kk) {
+                    const unsigned kx = ((unsigned)(4 * kk + t) * 8u) ^ xr;
+                    const double a0 = v0 ? *reinterpret_cast<const double*>(r0p + kx) : 0.0;
+                    const double a1 =
+                        v1 ? *reinterpret_cast<const double*>(r0p + 8 * P::PW * 8 + kx) : 0.0;
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb) dmma_c(ac[nb], a0, a1, bf[kk][nb]);
+                }
+                const int h1 = h0 + 8;
+                const int r0 = ridx(h0), r1 = ridx(h1);
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb) {
+                    const int q = 8 * nb + 2 * t;
+                    double v[4] = {ac[nb][0], ac[nb][1], ac[nb][2], ac[nb][3]};
+                    if (a.eps) {  // combine_from_weights' noise add (pipeline.cpp:220-223)
+                        auto noisy = [&](double val, int hh, int qq) {
+                            const int gx = x0 - 1 + hh % HX, gy = y0 - 1 + hh / HX;
+                            if (gx < 0 || gx >= a.nx || gy < 0 || gy >= a.ny || j0 + qq >= a.N)
+                                return val;
+                            return __dadd_rn(val, a.eps[(j0 + qq) * a.ldo + gx + (int64_t)a.nx * gy]);
+                        };
+                        if (h0 < HC) {
+                            v[0] = noisy(v[0], h0, q);
+                            v[1] = noisy(v[1], h0, q + 1);
+                        }
+                        if (h1 < HC) {
+                            v[2] = noisy(v[2], h1, q);
+                            v[3] = noisy(v[3], h1, q + 1);
+                        }
+                    }
+                    if (h0 < HC) {
+                        buf[q * HCR + r0] = v[0];
+                        buf[(q + 1) * HCR + r0] = v[1];
+                    }
+                    if (h1 < HC) {
+                        buf[q * HCR + r1] = v[2];
+                        buf[(q + 1) * HCR + r1] = v[3];
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tfull[b]);
+        }
+        return;
+    }
+
+    // ---- stencil warps: thread = (pair of x-adjacent cells, sample group)
+    const int tt = tid - 32 * NF, sw = warp - NF;
+    const int cell = 2 * (tt & 127), qh = tt >> 7;
+    const int lx = cell % TX, ly = cell / TX;
+    Coef k{}, k2{};
+    int cur_tile = -1;
+    for (int item = i_begin, it = 0; item < i_end; ++item, ++it) {
+        const int tile = item / a.chunks, chunk = item % a.chunks;
+        const int x0 = (tile % a.tilesx) * TX, y0 = (tile / a.tilesx) * TY;
+        const int64_t j0 = (int64_t)chunk * NS;
+        const int gx = x0 + lx, gy = y0 + ly;
+        const bool inside = gx < a.nx && gy < a.ny;
+        const bool inside2 = gx + 1 < a.nx && gy < a.ny;
+        if (tile != cur_tile) {
+            if (inside) load_coef(a, gx, gy, 0, k);
+            if (inside2) load_coef(a, gx + 1, gy, 0, k2);
+            cur_tile = tile;
+        }
+        const int b = it % NR;
+        mbar_wait(&tfull[b], (it / NR) & 1);
+        double num[SPT], den[SPT];
+#pragma unroll
+        for (int q = 0; q < SPT; ++q) num[q] = den[q] = 0.0;
+        if (inside) {
+            // pair (A = x, B = x + 1): 16-byte loads of (A, B) centre and
+            // y -+ 1 rows, 8-byte loads of x - 1 and x + 2; each cell's y in CSR
+            // order y-, x-, diag, x+, y+ exactly as the scalar path
+            const int hb = (ly + 1) * HXR + lx + 2;
+            const double* bp = ring + b * NS * HCR + SPT * qh * HCR + hb;
+            const int64_t i = gx + (int64_t)a.nx * gy;
+            const int64_t jb = j0 + SPT * qh;
+            double* pt = a.T ? a.T + jb * a.ldo + i : nullptr;
+            double* pq = a.Q ? a.Q + jb * a.ldo + i : nullptr;
+            const int nv = a.N - jb < SPT ? (int)(a.N - jb) : SPT;
+            const double vol = a.volz[0];
+            const double rvol = 1.0 / vol;
+            const bool vec = inside2 && ((i | a.ldo) & 1) == 0;  // 16-byte stores
+#pragma unroll
+            for (int qq = 0; qq < SPT; ++qq) {
+                const double2 c2 = *reinterpret_cast<const double2*>(bp + qq * HCR);
+                const double2 m2 = *reinterpret_cast<const double2*>(bp + qq * HCR - HXR);
+                const double2 p2 = *reinterpret_cast<const double2*>(bp + qq * HCR + HXR);
+                const double xl = bp[qq * HCR - 1], xr = bp[qq * HCR + 2];
+                double ya, yb;
+                if (!a.fma) {
+                    ya = __dadd_rn(0.0, __dmul_rn(k.ym, m2.x));
+                    ya = __dadd_rn(ya, __dmul_rn(k.xm, xl));
+                    ya = __dadd_rn(ya, __dmul_rn(k.di, c2.x));
+                    ya = __dadd_rn(ya, __dmul_rn(k.xp, c2.y));
+                    ya = __dadd_rn(ya, __dmul_rn(k.yp, p2.x));
+                    yb = __dadd_rn(0.0, __dmul_rn(k2.ym, m2.y));
+                    yb = __dadd_rn(yb, __dmul_rn(k2.xm, c2.x));
+                    yb = __dadd_rn(yb, __dmul_rn(k2.di, c2.y));
+                    yb = __dadd_rn(yb, __dmul_rn(k2.xp, xr));
+                    yb = __dadd_rn(yb, __dmul_rn(k2.yp, p2.y));
+                } else {
+                    ya = __fma_rn(k.ym, m2.x, 0.0);
+                    ya = __fma_rn(k.xm, xl, ya);
+                    ya = __fma_rn(k.di, c2.x, ya);
+                    ya = __fma_rn(k.xp, c2.y, ya);
+                    ya = __fma_rn(k.yp, p2.x, ya);
+                    yb = __fma_rn(k2.ym, m2.y, 0.0);
+                    yb = __fma_rn(k2.xm, c2.x, yb);
+                    yb = __fma_rn(k2.di, c2.y, yb);
+                    yb = __fma_rn(k2.xp, xr, yb);
+                    yb = __fma_rn(k2.yp, p2.y, yb);
+                }
+                const double qa = div_rn(__dsub_rn(ya, k.gi), vol, rvol);
+                const double qb = div_rn(__dsub_rn(yb, k2.gi), vol, rvol);
+                if (qq < nv) {
+                    if (vec) {
+                        if (pt) __stcs(reinterpret_cast<double2*>(pt), c2);
+                        if (pq) __stcs(reinterpret_cast<double2*>(pq), make_double2(qa, qb));
+                    } else {
+                        if (pt) __stcs(pt, c2.x);
+                        if (pq) __stcs(pq, qa);
+                        if (inside2 && pt) __stcs(pt + 1, c2.y);
+                        if (inside2 && pq) __stcs(pq + 1, qb);
+                    }
+                    const double ba = fma(vol, qa, k.gi);
+                    const double ra = __dsub_rn(ya, ba);
+                    num[qq] = fma(ra, ra, num[qq]);
+                    den[qq] = fma(ba, ba, den[qq]);
+                    if (inside2) {
+                        const double bb = fma(vol, qb, k2.gi);
+                        const double rb = __dsub_rn(yb, bb);
+                        num[qq] = fma(rb, rb, num[qq]);
+                        den[qq] = fma(bb, bb, den[qq]);
+                    }
+                }
+                pt += a.ldo;
+                pq += a.ldo;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[b]);  // this warp's ring reads are done
+        if (a.part) {
+            // fixed-order reduction, as combine_action_kernel: warp-level
+            // transpose-reduce of the V = 2 SPT per-lane sums, then the 4 warps
+            // of each sample half in index order
+            double v[V];
+#pragma unroll
+            for (int q = 0; q < SPT; ++q) {
+                v[q] = num[q];
+                v[SPT + q] = den[q];
+            }
+#pragma unroll
+            for (int o = 16, len = V; o >= 32 / V; o >>= 1, len >>= 1) {
+                const bool up = (lane & o) != 0;
+#pragma unroll
+                for (int e = 0; e < len / 2; ++e) {
+                    const double keep = up ? v[len / 2 + e] : v[e];
+                    const double send = up ? v[e] : v[len / 2 + e];
+                    v[e] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+#pragma unroll
+            for (int o = 32 / V / 2; o >= 1; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+            double* rb = red + (it & 1) * NSW * V;
+            if (lane % (32 / V) == 0) rb[sw * V + lane / (32 / V)] = v[0];
+            asm volatile("bar.sync 2, %0;" ::"n"(NSW * 32) : "memory");
+            if (tt < NS && j0 + tt < a.N) {
+                const int hq = tt / SPT, qq = tt % SPT;
+                double u = 0.0, w = 0.0;
+                for (int w2 = 0; w2 < 4; ++w2) {
+                    u += rb[(4 * hq + w2) * V + qq];
+                    w += rb[(4 * hq + w2) * V + SPT + qq];
+                }
+                double* pp = a.part + ((j0 + tt) * (int64_t)a.tiles + tile) * 2;
+                *reinterpret_cast<double2*>(pp) = make_double2(u, w);
+            }
+        }
+    }
+}
+
 // resid_j = sqrt(num / den) over the tiles (one warp per sample: lane-strided
 // sums, then a fixed shuffle tree — deterministic); de == 0 handled as
 // pipeline.cpp:570-571.
@@ -713,11 +1001,30 @@ bk_status run(bk_ctx* ctx, const bk_operator* op, const double* X, int s, const 
     const int hcr = PL ? HY * 36 + 4 : HC;  // the kernel's ring sample stride
     const size_t smem = 1024 + (size_t)SH::NP * P::SLOT +
                         (size_t)(nring * NS * hcr + S * SH::CSP) * sizeof(double) + SH::NP * 8;
-    auto kern = combine_action_kernel<S, NS, NT, PL>;
-    BK_CUDA_TRY(ctx, bk::set_max_smem((const void*)kern, smem));
-    const int slots = SH::CTAS * ctx->num_sms;
-    const int grid = a.items < slots ? a.items : slots;
-    kern<<<(unsigned)grid, SH::NT, smem, ctx->stream>>>(map, a);
+    bool done = false;
+    if constexpr (PL && P::R == 1 && NS == 16) {
+        if (!ctx->knobs.comb_one_role) {
+            // measured (C2, 2048 samples): 4 former warps and a two-buffer
+            // ring; 8 former warps, 16 stencil warps or three buffers were
+            // slower
+            constexpr int NQ = 2, NF = 4, NR = 2;
+            auto kern = combine_action_pl_ws<S, 16, NQ, NF, NR>;
+            const size_t sm2 = 1024 + (size_t)P::SLOT +
+                               (size_t)(NR * 16 * (HY * 36 + 2) + 2 * 4 * NQ * 2 * (16 / NQ)) * 8 +
+                               (2 * NR + 1) * 8;
+            BK_CUDA_TRY(ctx, bk::set_max_smem((const void*)kern, sm2));
+            const int grid = a.items < ctx->num_sms ? a.items : ctx->num_sms;
+            kern<<<(unsigned)grid, 32 * NF + 128 * NQ, sm2, ctx->stream>>>(map, a);
+            done = true;
+        }
+    }
+    if (!done) {
+        auto kern = combine_action_kernel<S, NS, NT, PL>;
+        BK_CUDA_TRY(ctx, bk::set_max_smem((const void*)kern, smem));
+        const int slots = SH::CTAS * ctx->num_sms;
+        const int grid = a.items < slots ? a.items : slots;
+        kern<<<(unsigned)grid, SH::NT, smem, ctx->stream>>>(map, a);
+    }
     ++ctx->launches;
     BK_CUDA_TRY(ctx, cudaGetLastError());
     if (ctx->knobs.comb_profile) {

@@ -37,7 +37,8 @@ struct bk_knobs {
     bool phase_timing = false; // per-kernel-kind event timing of the multi-kernel solve
     bool no_ws_update = false; // S = 64: the cp.async update sweeps instead of the warp-specialised ones
     bool no_ws_spmm = false;   // S = 64: the per-run TMA stencil sweep instead of the z-marching one
-    bool spmm_teams = false;
+    bool spmm_teams = false;   // S = 64: the two-team stencil sweep instead of the role-split one
+    bool comb_one_role = false; // single-plane combine/action: the one-role kernel
     int spmm_band = 0;         // S = 64 stencil sweep: x-runs per y-band (0: default 4)
     bool graph_loop = false;   // multi-kernel solve: device-driven iterations (CUDA graph while-loop)
 };

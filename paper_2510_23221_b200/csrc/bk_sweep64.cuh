@@ -28,10 +28,6 @@
 // run-to-run deterministic.
 #pragma once
 
-#ifndef BK_EXP  // timing experiments only (scripts/ab)
-#define BK_EXP 0
-#endif
-
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -856,7 +852,7 @@ __device__ __forceinline__ void spmm_gram_warp(SmemR<B>& sm, const SweepArgs& a,
         const int b = v % kRG;
         mbar_wait(&sm.gfull[b], (v / kRG) & 1);
         const unsigned char* Ut = sm.gst[b];
-        if (BK_EXP != 3) gram_run<W, false>(gacc, Ut, Ut + kArrBytes, one, g, t);
+        gram_run<W, false>(gacc, Ut, Ut + kArrBytes, one, g, t);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.gempty[b]);
     }
@@ -1041,8 +1037,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_spmm64_rs(SweepArgs a) {
                     const int64_t l = ix0 + nxl * (iyl0 + b) + plane_l * zz + r;
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        if (BK_EXP != 1)
-                            *reinterpret_cast<double2*>(a.W + l * S + 2 * cq + 16 * j) = acc[j];
+                        *reinterpret_cast<double2*>(a.W + l * S + 2 * cq + 16 * j) = acc[j];
                     const int gb = v % kRG;
                     if (v >= kRG) mbar_wait(&sm.gempty[gb], ((v / kRG) - 1) & 1);
                     unsigned char* Ut = sm.gst[gb];

@@ -231,12 +231,25 @@ def torch_empty_like(t):
     return torch.empty_like(t)
 
 
+def _on_torch_stream(slabs):
+    """The slab steps interleave library kernels with torch ops on the same
+    buffers (halo copies, partial sums, zero fills): launch them on torch's
+    current stream so they are ordered (a context's own stream is
+    non-blocking with respect to torch's)."""
+    import torch
+
+    cs = torch.cuda.current_stream().cuda_stream
+    for sl in slabs:
+        sl.ctx.set_stream(cs)
+
+
 def dd_block_cg(slabs, comm, cfg, report_arrays=True):
     """Run the decomposed block CG over `slabs` (lockstep). Returns the report
     of slab 0 (every rank's control state is identical)."""
     bk = slabs[0].bk
     S = slabs[0].S
     cfg_c = cfg._c()
+    _on_torch_stream(slabs)
 
     def all_step(kind, m=0):
         out = None
@@ -323,6 +336,7 @@ def slab_outputs(slabs, comm, coef, T, Q, resid, halo=True):
     N x slab cells; resid[i]: N, identical on every slab afterwards)."""
     import torch
 
+    _on_torch_stream(slabs)
     if halo:  # once per solve; later sample chunks reuse the ghost rows
         comm.halo(slabs, "X")
     N = int(coef.shape[1])
