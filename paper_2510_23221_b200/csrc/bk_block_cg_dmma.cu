@@ -1,10 +1,11 @@
 // Block conjugate gradient — DMMA variant (kernel widths S = 8, 16, 32).
 //
 // The reference algorithm is block_cg (solvers.cpp:452-665), restructured
-// around FP64 tensor cores: every dense s x s product runs on mma.sync.m16n8k4.f64 (measured
-// 74 TFLOP/s on B200 vs 37 for SIMT DFMA), with operand fragments produced in
-// registers by the sweep that loads them — no shared-memory staging except a
-// warp-private transpose for R^T Z.
+// around FP64 tensor cores: every dense s x s product runs on mma.sync.m16n8k4.f64 (one
+// DMMA issue per ~33 cycles per warp; B200's FP64 pipe, shared with SIMT DFMA,
+// peaks at 37 TFLOP/s — profiles/r2_summary.md), with operand fragments
+// produced in registers by the sweep that loads them — no shared-memory
+// staging except a warp-private transpose for R^T Z.
 //
 //   phase 1  W = A P (CSR-order FMA chain, bitwise the reference apply_block)
 //            and the Gram G = P^T W by DMMA with K = cells, per warp in 16-cell
