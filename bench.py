@@ -1041,7 +1041,8 @@ def run_c5(args, ctx, world, rank, local):
         # {diag, cx, cy, cz} (32 B/cell), writes W (8 s B/cell)
         sb = n * (32 + 16 * s)
         sm = ph["spmm"]["ms"] / ph["spmm"]["launches"] * 1e-3
-        spmm = {"kernel": "k_spmm64_ws (W = A P, G = P^T W; z-marching, warp-specialised)",
+        spmm = {"kernel": "k_spmm64_rs<4> (W = A P, G = P^T W; y-bands of 4 x-runs marched in z, "
+                          "stencil / Gram / producer warps)",
                 "achieved_GBps": sb / sm / 1e9,
                 "peak_GBps": peak, "frac": sb / sm / 1e9 / peak, "ms_per_launch": sm * 1e3,
                 "algorithmic_bytes_per_launch": int(sb),
@@ -1097,7 +1098,7 @@ def run_c5(args, ctx, world, rank, local):
                      "unit": "TFLOP/s", "frac": achieved_tf / FP64_PEAK_TFLOPS,
                      "traffic": ncu_traffic("config5_iter"),
                      "traffic_unit": "DRAM bytes per iteration (ncu, sum of the sweep kernels)",
-                     "kernel": "block-CG iteration, multi-kernel engine (S = 64): k_spmm64_ws "
+                     "kernel": "block-CG iteration, multi-kernel engine (S = 64): k_spmm64_rs<4> "
                                "(stencil-SpMM + Gram), k_update64_ws (R update + S_new), "
                                "k_pupdate64_ws (P + deferred X update), reductions, s x s solves",
                      "algorithmic_flops_per_iter": int(flops_iter),
