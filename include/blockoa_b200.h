@@ -285,8 +285,19 @@ typedef enum {
     BK_DD_CTL_RESTART = 9,
     BK_DD_PUPDATE = 10,      /* P = D^-1 R + P beta                             */
     BK_DD_CTL_FINAL = 11,    /* report                                          */
-    BK_DD_READ = 12          /* *cmd, *sa (synchronises the stream)             */
+    BK_DD_READ = 12,         /* *cmd, *sa (synchronises the stream)             */
+    /* deferred-X flow (the single-GPU engine's, used when bk_dd_deferred_x()
+     * is 1 — S = 64 on 16-aligned x — with the warp-specialised sweeps):
+     * BK_DD_UPDATE_D replaces BK_DD_UPDATE and leaves X alone; X += P alpha
+     * then happens in BK_DD_PUPDATE_X (with the P update) or, before a
+     * verification, in BK_DD_APPLY_X (followed by BK_DD_PUPDATE).          */
+    BK_DD_UPDATE_D = 13,     /* R -= W alpha; red = [R^T Z | rr]                */
+    BK_DD_PUPDATE_X = 14,    /* P = D^-1 R + P beta, X += P_old alpha           */
+    BK_DD_APPLY_X = 15       /* X += P alpha                                    */
 } bk_dd_step_kind;
+
+/* 1 if the slab steps of (op, S) use the deferred-X flow above. */
+int bk_dd_deferred_x(const bk_operator* op, int S);
 
 /* BK_DD_READ commands */
 #define BK_DD_CMD_PUPDATE 0

@@ -198,6 +198,8 @@ def _load():
         lib.bk_dd_step.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.c_int,
                                    vp, vp, vp]
         lib.bk_dd_pack.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int]
+        lib.bk_dd_deferred_x.argtypes = [vp, C.c_int]
+        lib.bk_dd_deferred_x.restype = C.c_int
         lib.bk_dd_combine_action.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, vp,
                                              C.c_int64, vp, vp, vp]
         lib.bk_dd_resid_from_nd.argtypes = [vp, vp, C.c_int64, vp]

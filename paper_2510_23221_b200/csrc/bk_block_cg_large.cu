@@ -1532,10 +1532,24 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
     Ctl<S>* ctl = (Ctl<S>*)b->ctl;
     CgReport* drep = (CgReport*)((char*)b->ctl + sizeof(Ctl<S>));
     a.coef = ctl->coef;
+    a.coef2 = ctl->akeep;
     a.act = ctl->act;
     constexpr int E = S * S + S;
     const int nb = b->nb;
     cudaStream_t s = ctx->stream;
+    // S = 64 on 16-aligned x: the warp-specialised sweeps of the single-GPU
+    // engine (one CTA per SM, deferred X), their partial count and the packed
+    // stencil coefficients (built by BK_DD_INIT_SWEEP)
+    const bool ws = S == 64 && update64_ws_ok(sl);
+    const int nws = ctx->num_sms < nb ? ctx->num_sms : nb;
+    const int64_t nloc_ws = (int64_t)sl.nx * (sl.nyl + 2) * sl.nz;
+    if (ws) {
+        void* pc;
+        const size_t runs = (size_t)(sl.nx / 16) * sl.ny * sl.nz;
+        bk_status wst = workspace(ctx, kSlotCgCoef64, runs * sweep64::kPC * 8, &pc);
+        if (wst != BK_OK) return wst;
+        a.pcoef = (const double*)pc;
+    }
     constexpr size_t swa = smem_anchor<S>(), sws = smem_spmm<S>(), swu = smem_update<S>(),
                      swp = smem_pupdate<S>();
     const size_t cs = sizeof(CSm<S>);
@@ -1551,6 +1565,10 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
                                     : 4L * ctx->num_sms);
     switch (step) {
         case BK_DD_INIT_SWEEP:
+            if (ws) {
+                sweep64::k_pack_coef64<<<ctx->num_sms * 8, 256, 0, s>>>(sl, a.st, (double*)a.pcoef);
+                ++ctx->launches;
+            }
             BK_CUDA_TRY(ctx, set((const void*)k_anchor<S, kInit>, swa));
             k_anchor<S, kInit><<<nb, LBS, swa, s>>>(a);
             ++ctx->launches;
@@ -1562,9 +1580,39 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
             ++ctx->launches;
             break;
         case BK_DD_SPMM:
-            BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s, ctx->knobs.no_tma_spmm));
+            if (ws) {
+                BK_CUDA_TRY(ctx, launch_spmm64_ws(a, nws, s, false,
+                                                  ctx->knobs.spmm_band > 0 ? ctx->knobs.spmm_band : 4));
+                ++ctx->launches;
+                reduce(S * S, nws);
+            } else {
+                BK_CUDA_TRY(ctx, launch_spmm<S>(a, nb, s, ctx->knobs.no_tma_spmm));
+                ++ctx->launches;
+                reduce(S * S, nb);
+            }
+            break;
+        case BK_DD_UPDATE_D:
+            if (ws) {
+                BK_CUDA_TRY(ctx, launch_update64_ws(a, nloc_ws, nws, s));
+                ++ctx->launches;
+                reduce(E, nws);
+            } else {
+                BK_CUDA_TRY(ctx, (launch_update<S, true>(a, nb, s)));
+                ++ctx->launches;
+                reduce(E, nb);
+            }
+            break;
+        case BK_DD_PUPDATE_X:
+            if (ws) {
+                BK_CUDA_TRY(ctx, launch_pupdate64_ws(a, nloc_ws, nws, s));
+            } else {
+                BK_CUDA_TRY(ctx, (launch_pupdate<S, 1>(a, nb, s)));
+            }
             ++ctx->launches;
-            reduce(S * S, nb);
+            break;
+        case BK_DD_APPLY_X:
+            BK_CUDA_TRY(ctx, (launch_pupdate<S, 2>(a, nb, s)));
+            ++ctx->launches;
             break;
         case BK_DD_CTL_ALPHA:
             BK_CUDA_TRY(ctx, set((const void*)k_ctl_alpha<S>, cs));
@@ -1748,6 +1796,10 @@ int bk_debug_ctl_solve_cycles(int reps, long long* cycles6, double* coef2, int o
     cudaFree(d);
     cudaFree(r);
     return err;
+}
+
+int bk_dd_deferred_x(const bk_operator* op, int S) {
+    return op && S == 64 && op->nx % 16 == 0 ? 1 : 0;
 }
 
 bk_status bk_dd_sizes(bk_ctx* ctx, const bk_operator* op, int nyl, int S, int64_t* local_elems,

@@ -33,7 +33,7 @@ from typing import List, Optional
 import numpy as np
 
 INIT_SWEEP, CTL_INIT, SPMM, CTL_ALPHA, UPDATE, CTL_UPDATE, TRUE_RES, CTL_VERIFY, \
-    RESTART_SWEEP, CTL_RESTART, PUPDATE, CTL_FINAL, READ = range(13)
+    RESTART_SWEEP, CTL_RESTART, PUPDATE, CTL_FINAL, READ, UPDATE_D, PUPDATE_X, APPLY_X = range(16)
 CMD_PUPDATE, CMD_VERIFY, CMD_RESTART, CMD_DONE = range(4)
 
 
@@ -146,8 +146,8 @@ class Slab:
 
 
 def _red_count(kind: int, S: int) -> int:
-    return {INIT_SWEEP: S * S + S, SPMM: S * S, UPDATE: S * S + S, TRUE_RES: S,
-            RESTART_SWEEP: S * S + S}[kind]
+    return {INIT_SWEEP: S * S + S, SPMM: S * S, UPDATE: S * S + S, UPDATE_D: S * S + S,
+            TRUE_RES: S, RESTART_SWEEP: S * S + S}[kind]
 
 
 class LocalComm:
@@ -255,7 +255,7 @@ def dd_block_cg(slabs, comm, cfg, report_arrays=True):
         out = None
         for sl in slabs:
             out = sl.step(kind, cfg_c, m)
-        if kind in (INIT_SWEEP, SPMM, UPDATE, TRUE_RES, RESTART_SWEEP):
+        if kind in (INIT_SWEEP, SPMM, UPDATE, UPDATE_D, TRUE_RES, RESTART_SWEEP):
             comm.allreduce(slabs, _red_count(kind, S))
         return out
 
@@ -264,6 +264,10 @@ def dd_block_cg(slabs, comm, cfg, report_arrays=True):
         assert all(v == vals[0] for v in vals), "ranks disagree on control state"
         return vals[0]
 
+    # S = 64 on 16-aligned x: the single-GPU engine's warp-specialised sweeps
+    # with X += P alpha deferred into the P update (bk_dd_deferred_x)
+    lib = bk._load()
+    deferred = bool(lib.bk_dd_deferred_x(slabs[0].op.h, S))
     all_step(INIT_SWEEP)
     all_step(CTL_INIT)
     cmd, sa = read()
@@ -272,10 +276,12 @@ def dd_block_cg(slabs, comm, cfg, report_arrays=True):
         comm.halo(slabs, "P")
         all_step(SPMM)
         all_step(CTL_ALPHA)
-        all_step(UPDATE)
+        all_step(UPDATE_D if deferred else UPDATE)
         all_step(CTL_UPDATE, m)
         cmd, sa = read()
         if cmd == CMD_VERIFY:
+            if deferred:
+                all_step(APPLY_X)
             comm.halo(slabs, "X")
             all_step(TRUE_RES)
             all_step(CTL_VERIFY)
@@ -287,7 +293,9 @@ def dd_block_cg(slabs, comm, cfg, report_arrays=True):
                 all_step(CTL_RESTART)
                 m += 1
                 continue
-        all_step(PUPDATE)
+            all_step(PUPDATE)
+        else:
+            all_step(PUPDATE_X if deferred else PUPDATE)
         m += 1
     _, sa = read()
     if sa > 0:

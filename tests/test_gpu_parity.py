@@ -528,31 +528,32 @@ def test_block_cg_graph_loop_bitwise(bk, ctx, oracle, case):
     assert g.report.all_converged() and rel_l2(g.x, X) <= PARITY
 
 
+@pytest.mark.parametrize("case", [(5, 48, 40, 16, 64, 2), (5, 40, 36, 16, 64, 2)])
 @pytest.mark.parametrize("nslabs", [1, 2, 3])
-def test_slab_decomposition_matches_single_gpu(bk, ctx, nslabs):
+def test_slab_decomposition_matches_single_gpu(bk, ctx, nslabs, case):
     """y-slab decomposition (config 5 structure: s = 64) with virtual ranks on
     one GPU (dd.LocalComm): same solution as the single-GPU solve; one slab is
-    bitwise the single-GPU multi-kernel engine."""
+    bitwise the single-GPU multi-kernel engine — on 16-aligned x the slab steps
+    run the same warp-specialised sweeps with X deferred to the P update
+    (bk_dd_deferred_x), otherwise the per-run sweeps with X in phase 2."""
     import torch
 
     from paper_2510_23221_b200 import dd
 
-    inp = bk.synth_chip(5, 48, 40, 16, 64, 2)
+    inp = bk.synth_chip(*case)
     op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
     dev = torch.device("cuda", 0)
     q = torch.from_numpy(inp.q_basis).to(dev)
     B = torch.empty_like(q)
     bk.rhs_from_power(op, q, out=B)
     torch.cuda.synchronize()
-    # the slab steps (bk_dd_step) use the per-run sweeps with X updated in
-    # phase 2; the single-GPU engine's warp-specialised S = 64 sweeps sum the
-    # Gram partials in another order and defer X to the P update — same
-    # iterates to rounding, so the bitwise one-slab check runs against the
-    # matching single-GPU variant
-    with ctx.options(no_ws_update=1, no_ws_spmm=1):
-        ref = bk.block_cg(op, B.cpu().numpy(), cfg_jacobi())
+    deferred = bool(bk._load().bk_dd_deferred_x(op.h, 64))
+    assert deferred == (inp.grid.nx % 16 == 0)
     ref_ws = bk.block_cg(op, B.cpu().numpy(), cfg_jacobi())
-    assert rel_l2(ref_ws.x, ref.x) <= PARITY
+    with ctx.options(no_ws_update=1, no_ws_spmm=1):
+        ref_pr = bk.block_cg(op, B.cpu().numpy(), cfg_jacobi())
+    assert rel_l2(ref_ws.x, ref_pr.x) <= PARITY
+    ref = ref_ws if deferred else ref_pr
     parts = dd.partition_rows(inp.grid.ny, nslabs)
     X, rep = dd.solve_decomposed(bk, ctx, op, B, cfg_jacobi(), parts)
     torch.cuda.synchronize()
@@ -560,6 +561,7 @@ def test_slab_decomposition_matches_single_gpu(bk, ctx, nslabs):
     assert rep.all_converged() and ref.report.all_converged()
     if nslabs == 1:
         assert np.array_equal(Xh, ref.x) and rep.iterations == ref.report.iterations
+        assert rep.matvec_count == ref.report.matvec_count
     else:
         assert rel_l2(Xh, ref.x) <= PARITY
         assert abs(rep.iterations - ref.report.iterations) <= max(3, ref.report.iterations // 10)
