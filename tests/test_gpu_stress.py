@@ -63,16 +63,21 @@ def batch_runs(bk, ctx, cases, streams, tol=1e-12, it=100000, **opts):
     ([(3, 32, 24, 8, 32, 20, 1, c) for c in range(3)], 3, {}, "block_cg_dmma_kernel<32,0,1,1>"),
     ([(4, 32, 24, 4, 16, 8, 1, c) for c in range(8)], 8, {"no_resident": 1},
      "block_cg_dmma_kernel<16,0,1,0>"),
+    ([(2, 64, 48, 1, 16, 40, 1, c) for c in range(4)], 4, {"comb_one_role": 1},
+     "block_cg_dmma_kernel<16,1,1,0>"),
 ])
 def test_batched_solve_and_combine_repeatable(bk, ctx, cases, streams, opts, expect):
     variant = batch_runs(bk, ctx, cases, streams, **opts)
     assert variant.startswith(expect), variant
 
 
-@pytest.mark.parametrize("opts", [{}, {"no_ws_update": 1, "no_ws_spmm": 1}])
+@pytest.mark.parametrize("opts", [{}, {"spmm_band": 1}, {"spmm_band": 2}, {"spmm_teams": 1},
+                                  {"graph_loop": 1}, {"no_ws_update": 1, "no_ws_spmm": 1}])
 def test_multikernel_s64_repeatable(bk, ctx, opts):
-    """The S = 64 engine (warp-specialised TMA sweeps by default) on a reduced
-    config-5 chip: X bitwise equal over repeated solves, no NaN left."""
+    """The S = 64 engine (warp-specialised TMA sweeps by default: y-banded
+    role-split stencil sweep, producer-less update, register-resident control
+    solves) on a reduced config-5 chip, every sweep variant: X bitwise equal
+    over repeated solves, no NaN left."""
     import torch
 
     inp = bk.synth_chip(5, 48, 40, 16, 64, 2)
