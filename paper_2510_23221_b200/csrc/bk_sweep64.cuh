@@ -871,7 +871,7 @@ __device__ __forceinline__ void spmm_gram_warp(SmemR<B>& sm, const SweepArgs& a,
         if ((e % S) / 8 < 2 * ((e / S) / 16)) out[e] = 0.0;
 }
 
-template <int B>
+template <int B, bool WIN = true>
 __global__ void __launch_bounds__(kRThreads, 1) k_spmm64_rs(SweepArgs a) {
     constexpr int S = 64;
     constexpr int RS = Band<B>::RS, RC = Band<B>::RC;
@@ -972,6 +972,10 @@ __global__ void __launch_bounds__(kRThreads, 1) k_spmm64_rs(SweepArgs a) {
         // read back from the ring, B = 4 reads all three from the ring)
         constexpr bool ROT = B <= 2;
         double2 pz[ROT ? B : 1][4], pp1[ROT ? B : 1][4];
+        // B = 4: the band's y-neighbours come from a register window over the
+        // runs (run b - 1 / b / b + 1 at plane z): one centre load per run
+        // serves as its own centre and as the y -+ 1 neighbour of the others
+        double2 wprv[4], wcur[4], wnxt[4];
         for (int bd = first; bd < nband; bd += stride) {
             int ix0, iyl0;
             band_of(bd, ix0, iyl0);
@@ -1002,18 +1006,34 @@ __global__ void __launch_bounds__(kRThreads, 1) k_spmm64_rs(SweepArgs a) {
                         auto ld = [&](const double* row) {
                             return *reinterpret_cast<const double2*>(row + c);
                         };
-                        double2 cz, cp;
+                        double2 cz, cp, ym2, yp2;
+                        const double2 zero2 = make_double2(0.0, 0.0);
                         if constexpr (ROT) {
                             if (zz == 0)
                                 pz[b][j] = ld(C0 + (1 + r) * S);
                             else
                                 pz[b][j] = pp1[b][j];
-                            pp1[b][j] = hzp ? ld(Cp + (1 + r) * S) : make_double2(0.0, 0.0);
+                            pp1[b][j] = hzp ? ld(Cp + (1 + r) * S) : zero2;
                             cz = pz[b][j];
                             cp = pp1[b][j];
+                            ym2 = hym ? ld(Ym + r * S) : zero2;
+                            yp2 = hyp ? ld(Yp + r * S) : zero2;
                         } else {
-                            cz = ld(C0 + (1 + r) * S);
-                            cp = hzp ? ld(Cp + (1 + r) * S) : make_double2(0.0, 0.0);
+                            if (!WIN) {
+                                wcur[j] = ld(C0 + (1 + r) * S);
+                                wprv[j] = hym ? ld(Ym + r * S) : zero2;
+                            } else if (b == 0) {
+                                wcur[j] = ld(C0 + (1 + r) * S);
+                                wprv[j] = hym ? ld(Ym + r * S) : zero2;
+                            } else {
+                                wprv[j] = wcur[j];
+                                wcur[j] = wnxt[j];
+                            }
+                            wnxt[j] = (b < B - 1 || hyp) ? ld(Yp + r * S) : zero2;
+                            cz = wcur[j];
+                            ym2 = wprv[j];
+                            yp2 = wnxt[j];
+                            cp = hzp ? ld(Cp + (1 + r) * S) : zero2;
                             pz[0][j] = cz;  // staged below
                         }
                         double2 x = make_double2(0.0, 0.0);
@@ -1022,11 +1042,11 @@ __global__ void __launch_bounds__(kRThreads, 1) k_spmm64_rs(SweepArgs a) {
                             x.y = fma(cc, w2.y, x.y);
                         };
                         if (hzm) fm(czm, ld(Cm + (1 + r) * S));
-                        if (hym) fm(cym, ld(Ym + r * S));
+                        if (hym) fm(cym, ym2);
                         if (hxm) fm(cxm, ld(C0 + r * S));
                         fm(dg, cz);
                         if (hxp) fm(cxp, ld(C0 + (2 + r) * S));
-                        if (hyp) fm(cyp, ld(Yp + r * S));
+                        if (hyp) fm(cyp, yp2);
                         if (hzp) fm(czp, cp);
                         acc[j] = x;
                     }
@@ -1140,6 +1160,8 @@ inline cudaError_t launch_spmm64_ws(const SweepArgs& a, int nsm, cudaStream_t s,
         return cudaGetLastError();
     };
     if (band == 4 && a.sl.nyl % 4 == 0) return go(sweep64::k_spmm64_rs<4>, sweep64::smem_bytes_r<4>());
+    if (band == 5 && a.sl.nyl % 4 == 0)  // band 4 without the register y-window (A/B)
+        return go(sweep64::k_spmm64_rs<4, false>, sweep64::smem_bytes_r<4>());
     if (band >= 2 && a.sl.nyl % 2 == 0) return go(sweep64::k_spmm64_rs<2>, sweep64::smem_bytes_r<2>());
     return go(sweep64::k_spmm64_rs<1>, sweep64::smem_bytes_r<1>());
 }
