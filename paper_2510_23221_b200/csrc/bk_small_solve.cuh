@@ -139,8 +139,10 @@ __device__ void small_solve_t(SMT& sm, const double* M, const double* RHS, doubl
     stamp(1);
     constexpr int RPW = (S + NW - 1) / NW;    // rows per warp
     constexpr int CPL = (2 * S + 31) / 32;    // columns per lane
+    double* const pivv = aug + S * LD + 1;  // pivot value of each pivoted row
     while (p >= 0 && pv > cutoff) {           // uniform: beyond the rank -> stop
         donem |= 1ull << p;
+        if (threadIdx.x == 0) pivv[p] = pv;
         // operands of this pivot's block update and of the Schur-diagonal
         // update (row p and column p are not written by this step)
         double apq[CPL], fi[RPW], aiq[RPW][CPL];
@@ -176,8 +178,11 @@ __device__ void small_solve_t(SMT& sm, const double* M, const double* RHS, doubl
             const double f = fi[r] * rinv;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
+                // columns of earlier pivots are updated too (they feed only
+                // themselves; pivoted rows take their diagonal from pivv), the
+                // pivot column itself is not (other threads read it this step)
                 const int q = lane + 32 * c;
-                const bool ok = row_ok && q < 2 * sa && !(q < sa && ((donem >> q) & 1ull));
+                const bool ok = row_ok && q < 2 * sa && q != p;
                 const double nv = fma(-f, apq[c], aiq[r][c]);
                 if (ok) aug[i * LD + q] = nv;
             }
@@ -210,7 +215,7 @@ __device__ void small_solve_t(SMT& sm, const double* M, const double* RHS, doubl
     if (NWS < NWA) donem = *shared_done;
     for (int i = warp; i < sa; i += NWA) {
         if (!((donem >> i) & 1ull)) continue;
-        const double di = __drcp_rn(aug[i * LD + i]);
+        const double di = __drcp_rn(aug[S * LD + 1 + i]);  // pivv[i] = aug[i][i] at its pivot
         for (int q = lane; q < sa; q += 32) out[sm.idx[i] * RS + sm.idx[q]] = aug[i * LD + sa + q] * di;
     }
     if (threadIdx.x == 0) sm.rank = rank;
