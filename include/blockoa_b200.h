@@ -127,6 +127,10 @@ int64_t bk_launch_count(const bk_ctx* ctx);
  * discretize.cpp:114-237. Builds the matrix-free SoA stencil in HBM. */
 bk_status bk_assemble(bk_ctx* ctx, const bk_grid* grid, const double* k,
                       const bk_face bc[6], bk_operator** out);
+/* The same, into an existing operator: its device buffers are reused when the
+ * cell count matches (no allocation in a per-chip loop). */
+bk_status bk_assemble_into(bk_ctx* ctx, const bk_grid* grid, const double* k,
+                           const bk_face bc[6], bk_operator* op);
 void bk_operator_free(bk_operator* op);
 int64_t bk_operator_n(const bk_operator* op);
 

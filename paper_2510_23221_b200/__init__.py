@@ -174,6 +174,7 @@ def _load():
         lib.bk_last_solve_phases.argtypes = [vp, vp, vp]
         lib.bk_assemble.argtypes = [vp, C.POINTER(_Grid), dp, C.POINTER(_Face), C.POINTER(vp)]
         lib.bk_operator_free.argtypes = [vp]
+        lib.bk_assemble_into.argtypes = [vp, C.POINTER(_Grid), dp, C.POINTER(_Face), vp]
         lib.bk_operator_free.restype = None
         lib.bk_operator_n.argtypes = [vp]
         lib.bk_operator_n.restype = C.c_int64
@@ -538,14 +539,23 @@ class DiscreteOperator:
         return out
 
 
-def assemble(k, grid: GridSpec, bc: BoundarySpec, ctx: Optional[Context] = None) -> DiscreteOperator:
-    """assemble(k, grid, bc) (discretize.cpp:114-237) -> device stencil."""
+def assemble(k, grid: GridSpec, bc: BoundarySpec, ctx: Optional[Context] = None,
+             out: Optional[DiscreteOperator] = None) -> DiscreteOperator:
+    """assemble(k, grid, bc) (discretize.cpp:114-237) -> device stencil. With
+    `out` (an operator of this context), re-assembles into its device buffers
+    (reused when the cell count matches) and returns it."""
     ctx = _ctx(ctx)
     if _numel(k) != grid.cell_count():
         raise DimensionMismatchError("assemble: conductivity grid mismatch")
     g, keep = grid._c()
     faces = bc._c()
     pk, kk = _ptr(k)
+    if out is not None:
+        if out.ctx is not ctx:
+            raise InvalidConfigError("assemble: out belongs to another context")
+        _raise(_load().bk_assemble_into(ctx.h, C.byref(g), pk, faces, out.h), ctx.h, "assemble")
+        out.grid, out.boundary, out.n = grid, bc, grid.cell_count()
+        return out
     h = C.c_void_p()
     _raise(_load().bk_assemble(ctx.h, C.byref(g), pk, faces, C.byref(h)), ctx.h, "assemble")
     return DiscreteOperator(h, ctx, grid, bc)

@@ -885,6 +885,15 @@ bk_status bk_assemble(bk_ctx* ctx, const bk_grid* grid, const double* k, const b
     return BK_OK;
 }
 
+bk_status bk_assemble_into(bk_ctx* ctx, const bk_grid* grid, const double* k, const bk_face bc[6],
+                           bk_operator* op) {
+    if (!ctx || !op || !bc) return BK_INVALID_CONFIG;
+    cudaSetDevice(ctx->device);
+    if (op->diag && op->device != ctx->device)
+        return fail(ctx, BK_INVALID_CONFIG, "assemble_into: operator lives on another device");
+    return assemble_into(ctx, grid, k, bc, op);
+}
+
 void bk_operator_free(bk_operator* op) {
     if (!op) return;
     cudaSetDevice(op->device);

@@ -1,5 +1,5 @@
 #!/bin/bash
 # scratch job file for one gpurun call (the command of the latest A/B run)
 cd $GRAFT_REPO_ROOT
-timeout 300 python scripts/solve_ab.py 3 12 no_pencil=1 > gpurun_out/ab.log 2>&1
-BK_CG_PROFILE=1 timeout 300 python scripts/solve_ab.py 3 8 >> gpurun_out/ab.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q -k "assemble or kat or mixed or csr or generate_chip" > gpurun_out/t.log 2>&1
+timeout 900 python bench.py --steps 3 --warmup 3 --no-extra --no-e2e --no-cpu-baseline > gpurun_out/b.log 2>&1

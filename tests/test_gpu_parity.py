@@ -107,6 +107,20 @@ def test_assemble_apply_rhs_bitwise_vs_oracle(bk, ctx, oracle, case):
     assert np.array_equal(bk.power_from_rhs(op, b), oracle.power_from_rhs(o, b))
 
 
+def test_assemble_into_reuses_and_matches(bk, ctx):
+    """bk_assemble_into: re-assembling another chip into an existing operator
+    (buffers reused) gives bitwise the freshly assembled operator."""
+    a = bk.synth_chip(3, 24, 20, 8, 8, 2, chip_id=0)
+    b = bk.synth_chip(3, 24, 20, 8, 8, 2, chip_id=1)
+    op = bk.assemble(a.k, a.grid, a.bc, ctx)
+    h = op.h.value
+    op2 = bk.assemble(b.k, b.grid, b.bc, ctx, out=op)
+    assert op2 is op and op.h.value == h
+    fresh = bk.assemble(b.k, b.grid, b.bc, ctx)
+    for x, y in zip(op.csr(), fresh.csr()):
+        assert np.array_equal(x, y)
+
+
 def test_operator_action_center_indicator(bk, ctx):
     """q = center column of A (27-cell, g = 0, unit volumes)."""
     op = bk.assemble(np.ones(27), bk.GridSpec(3, 3, 3, 3.0, 3.0, 3.0),
