@@ -964,6 +964,7 @@ def run_c5(args, ctx, world, rank, local):
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     opbox = [None]  # the operator's device buffers are reused chip after chip
+    slabbox = [None]
 
     def step():
         e = [ev() for _ in range(4)]
@@ -978,7 +979,10 @@ def run_c5(args, ctx, world, rank, local):
                 m = int(c.shape[1])
                 bk.combine_action(op, X, c, t_out=T[:m], q_out=Q[:m], resid_out=R[:m])
         else:
-            slab = dd.Slab(bk, ctx, op, y0, nyl, 64).allocate()
+            if slabbox[0] is None:  # the slab's block vectors are reused chip after chip
+                slabbox[0] = dd.Slab(bk, ctx, op, y0, nyl, 64).allocate()
+            slab = slabbox[0]
+            slab.op = op
             slab.load_rhs(B)
             comm = dd.TorchComm()
             rep = dd.dd_block_cg([slab], comm, cfg)
@@ -1049,6 +1053,9 @@ def run_c5(args, ctx, world, rank, local):
                 "peak_GBps": peak, "frac": sb / sm / 1e9 / peak, "ms_per_launch": sm * 1e3,
                 "algorithmic_bytes_per_launch": int(sb),
                 "traffic": ncu_traffic("config5_spmm")}
+    loops = None
+    if world == 1 and not args.no_dd_leg:
+        loops = c5_loop_leg(bk, torch, ctx, opbox[0], B, X, cfg, inp.grid.ny, dev)
     phases = ({k: dict(v, ms_per_launch=(v["ms"] / v["launches"] if v["launches"] else None))
                for k, v in ph.items()} if ph else None)
 
@@ -1112,6 +1119,7 @@ def run_c5(args, ctx, world, rank, local):
                      "phases_last_solve": phases,
                      "phases_note": "event pairs around each sweep, from one extra untimed solve"},
         "spmm": spmm,
+        "host_loops": loops,
         "action": action_roofline(n // world, s, N, float(np.mean(act_s)), peak),
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -1125,6 +1133,78 @@ def run_c5(args, ctx, world, rank, local):
         "solver_variant": ctx.last_solver_variant,
     }
     return line
+
+
+def c5_loop_leg(bk, torch, ctx, op, B, X, cfg, ny, dev):
+    """One GPU, the C5 chip's basis solve driven four ways (untimed by the
+    headline, CUDA events around each solve): the single-GPU engine with its
+    default lookahead loop and with the synchronous loop (one device drain per
+    iteration), and the y-slab decomposition's host loop (dd.py) with ONE slab
+    over a world-size-1 NCCL group — the per-iteration host work of the N > 1
+    path (ctypes steps, NCCL all-reduces, control reads) with no remote rank —
+    with and without its lookahead. Every X is compared bitwise with the
+    headline solve's."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2510_23221_b200 import dd
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    stream = torch.cuda.current_stream()
+    Xr = torch.empty_like(X)
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        rep = fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), rep
+
+    out = {}
+    ms, rep = timed(lambda: bk.block_cg(op, B, cfg, out=Xr).report)
+    out["engine_lookahead"] = {"solve_ms": ms, "iterations": rep.iterations,
+                               "ms_per_iteration": ms / rep.iterations,
+                               "bitwise_headline_x": bool(torch.equal(Xr, X))}
+    with ctx.options(no_lookahead=1):
+        ms, rep = timed(lambda: bk.block_cg(op, B, cfg, out=Xr).report)
+    out["engine_synchronous"] = {"solve_ms": ms, "iterations": rep.iterations,
+                                 "ms_per_iteration": ms / rep.iterations,
+                                 "bitwise_headline_x": bool(torch.equal(Xr, X))}
+    own = False
+    try:
+        if not dist.is_initialized():
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                    world_size=1, device_id=dev)
+            own = True
+        comm = dd.TorchComm()
+        slab = dd.Slab(bk, ctx, op, 0, ny, 64).allocate()
+        for look in (True, False):
+            def run():
+                slab.load_rhs(B)
+                return dd.dd_block_cg([slab], comm, cfg, lookahead=look)
+            ms, rep = timed(run)
+            slab.store_x(Xr)
+            torch.cuda.synchronize()
+            out["dd_1slab_nccl_" + ("lookahead" if look else "synchronous")] = {
+                "solve_ms": ms, "iterations": rep.iterations, "ms_per_iteration": ms / rep.iterations,
+                "bitwise_headline_x": bool(torch.equal(Xr, X))}
+        del slab
+    except Exception as e:  # noqa: BLE001 — a leg, not the headline
+        out["dd_error"] = f"{type(e).__name__}: {e}"
+    finally:
+        if own:
+            dist.destroy_process_group()
+    base = out["engine_lookahead"]["ms_per_iteration"]
+    for v in out.values():
+        if isinstance(v, dict):
+            v["vs_engine_lookahead"] = v["ms_per_iteration"] / base
+    return out
 
 
 def _finish(args, world, rank, line):
@@ -1191,6 +1271,8 @@ def main():
     ap.add_argument("--no-extra", action="store_true",
                     help="config 5: skip the C2 line reported under extra_configs")
     ap.add_argument("--no-e2e", action="store_true", help="config 5: skip the e2e leg")
+    ap.add_argument("--no-dd-leg", action="store_true",
+                    help="config 5: skip the host-loop leg (engine / slab loops, with and without lookahead)")
     ap.add_argument("--no-dataset", action="store_true",
                     help="skip the dataset sink / validation leg (SURVEY 8(f2))")
     ap.add_argument("--no-direct", action="store_true",

@@ -297,7 +297,16 @@ typedef enum {
      * verification, in BK_DD_APPLY_X (followed by BK_DD_PUPDATE).          */
     BK_DD_UPDATE_D = 13,     /* R -= W alpha; red = [R^T Z | rr]                */
     BK_DD_PUPDATE_X = 14,    /* P = D^-1 R + P beta, X += P_old alpha           */
-    BK_DD_APPLY_X = 15       /* X += P alpha                                    */
+    BK_DD_APPLY_X = 15,      /* X += P alpha                                    */
+    /* *cmd, *sa <- the control word, enqueued without synchronising: cmd and
+     * sa must point to pinned host memory that stays valid until the stream
+     * passes the copies (the caller waits on an event recorded after it)    */
+    BK_DD_READ_ASYNC = 16,
+    /* flag OR-ed into SPMM / CTL_ALPHA / UPDATE(_D) / CTL_UPDATE / PUPDATE(_X):
+     * the kernels run only while the control word is BK_DD_CMD_PUPDATE, so a
+     * host can enqueue iteration m + 1 before reading iteration m's word (a
+     * pending verification turns the enqueued iteration into no-ops)       */
+    BK_DD_GATED = 0x100
 } bk_dd_step_kind;
 
 /* 1 if the slab steps of (op, S) use the deferred-X flow above. */

@@ -47,7 +47,7 @@ bk_status workspace(bk_ctx* ctx, int slot, size_t bytes, void** out) {
 
 bk_status read_small(bk_ctx* ctx, void* host_dst, const void* dev_src, size_t bytes) {
     constexpr size_t kMap = 64 << 10;
-    if (bytes > kMap || bytes % 4) return fail(ctx, BK_INTERNAL, "read_small: size");
+    if (bytes > (32 << 10) || bytes % 4) return fail(ctx, BK_INTERNAL, "read_small: size");
     if (!ctx->hmap) {
         BK_CUDA_TRY(ctx, cudaHostAlloc(&ctx->hmap, kMap, cudaHostAllocMapped));
         BK_CUDA_TRY(ctx, cudaHostGetDevicePointer(&ctx->hmap_dev, ctx->hmap, 0));
@@ -57,6 +57,29 @@ bk_status read_small(bk_ctx* ctx, void* host_dst, const void* dev_src, size_t by
     ++ctx->launches;
     BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     std::memcpy(host_dst, ctx->hmap, bytes);
+    return BK_OK;
+}
+
+static constexpr size_t kLookSlot0 = 32 << 10;  // post_small slots: past read_small's words
+
+bk_status post_small(bk_ctx* ctx, int slot, const void* dev_src, size_t bytes) {
+    if (bytes > 256 || bytes % 4 || slot < 0 || slot > 1) return fail(ctx, BK_INTERNAL, "post_small: size");
+    if (!ctx->hmap) {
+        BK_CUDA_TRY(ctx, cudaHostAlloc(&ctx->hmap, 64 << 10, cudaHostAllocMapped));
+        BK_CUDA_TRY(ctx, cudaHostGetDevicePointer(&ctx->hmap_dev, ctx->hmap, 0));
+    }
+    if (!ctx->look_ev[slot]) BK_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->look_ev[slot], cudaEventDisableTiming));
+    unsigned* dst = (unsigned*)((char*)ctx->hmap_dev + kLookSlot0 + 256 * slot);
+    BK_CUDA_TRY(ctx, launch_copy_words(ctx->stream, dst, (const unsigned*)dev_src, bytes / 4));
+    ++ctx->launches;
+    BK_CUDA_TRY(ctx, cudaEventRecord(ctx->look_ev[slot], ctx->stream));
+    return BK_OK;
+}
+
+bk_status wait_small(bk_ctx* ctx, int slot, void* host_dst, size_t bytes) {
+    if (bytes > 256 || slot < 0 || slot > 1 || !ctx->look_ev[slot]) return fail(ctx, BK_INTERNAL, "wait_small");
+    BK_CUDA_TRY(ctx, cudaEventSynchronize(ctx->look_ev[slot]));
+    std::memcpy(host_dst, (const char*)ctx->hmap + kLookSlot0 + 256 * slot, bytes);
     return BK_OK;
 }
 
@@ -800,6 +823,7 @@ bk_status bk_set_option(bk_ctx* ctx, const char* name, int value) {
     else if (k == "no_ws_update") ctx->knobs.no_ws_update = value != 0;
     else if (k == "no_ws_spmm") ctx->knobs.no_ws_spmm = value != 0;
     else if (k == "graph_loop") ctx->knobs.graph_loop = value != 0;
+    else if (k == "no_lookahead") ctx->knobs.no_lookahead = value != 0;
     else if (k == "spmm_teams") ctx->knobs.spmm_teams = value != 0;
     else if (k == "spmm_band") ctx->knobs.spmm_band = value;
     else if (k == "comb_one_role") ctx->knobs.comb_one_role = value != 0;
@@ -820,6 +844,8 @@ void bk_destroy(bk_ctx* ctx) {
         }
     for (int i = 0; i < bk_ctx::kSlots; ++i) cudaFree(ctx->ws[i]);
     for (auto& e : ctx->ev) cudaEventDestroy(e);
+    for (auto& e : ctx->look_ev)
+        if (e) cudaEventDestroy(e);
     for (auto& e : ctx->chunk_ev) cudaEventDestroy(e);
     for (auto& e : ctx->drain_ev)
         if (e) cudaEventDestroy(e);

@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(LBS, 2) k_anchor(SweepArgs a) {
 // half a row apart, so one load instruction reads whole 128-byte lines.
 template <int S>
 __global__ void __launch_bounds__(LBS, 2) k_spmm_gram(SweepArgs a) {
+    if (a.gate && *a.gate != 0) return;  // gated (DD lookahead): this iteration is a no-op
     using G_ = Geo<S>;
     constexpr int RS = G_::RS, LPC = 16 / G_::TPB, CPW = 32 / LPC;
     extern __shared__ __align__(16) double sm_[];
@@ -571,6 +572,7 @@ __device__ __forceinline__ void tma_stage64(double* st, unsigned long long* bar,
 }
 
 __global__ void __launch_bounds__(LBS, 2) k_spmm_gram_tma64(SweepArgs a) {
+    if (a.gate && *a.gate != 0) return;  // gated (DD lookahead): this iteration is a no-op
     constexpr int S = 64;
     using G_ = Geo<S>;
     constexpr int RS = G_::RS, LPC = 16, CPW = 2;
@@ -671,6 +673,7 @@ __device__ __forceinline__ void frag_from_smem(const double* T, int RS, int row0
 // updated R and Z overwrite the consumed R / X stage rows and feed the Gram.
 template <int S, bool XD = false>
 __global__ void __launch_bounds__(LBS, 2) k_update(SweepArgs a) {
+    if (a.gate && *a.gate != 0) return;  // gated (DD lookahead): this iteration is a no-op
     using G_ = Geo<S>;
     constexpr int RS = G_::RS, KS = S / 4, TL = G_::TILE;
     // stage layout: P, W, X, R, dinv — or (XD) W, R, dinv, Z scratch
@@ -1053,7 +1056,8 @@ __global__ void __launch_bounds__(CBS) k_ctl_init(Ctl<S>* c, const double* red, 
 
 // red = G: alpha = G^+ S_old
 template <int S>
-__global__ void __launch_bounds__(CBS) k_ctl_alpha(Ctl<S>* c, const double* red) {
+__global__ void __launch_bounds__(CBS) k_ctl_alpha(Ctl<S>* c, const double* red, int gated) {
+    if (gated && c->cmd != kCmdPupdate) return;  // DD lookahead: a verification is pending
     extern __shared__ __align__(16) unsigned char smraw_[];
     CSm<S>& sm = *reinterpret_cast<CSm<S>*>(smraw_);
     ctl_index(c, sm);
@@ -1070,7 +1074,11 @@ template <int S>
 // while-condition is set to continue unless a verification is due or the
 // iteration cap is reached)
 __global__ void __launch_bounds__(CBS) k_ctl_update(Ctl<S>* c, const double* red, int m,
-                                                    cudaGraphConditionalHandle loop, int max_iter) {
+                                                    cudaGraphConditionalHandle loop, int max_iter,
+                                                    int gated) {
+    // DD lookahead: every thread reads cmd before thread 0 can rewrite it (the
+    // write below follows at least one __syncthreads)
+    if (gated && c->cmd != kCmdPupdate) return;
     extern __shared__ __align__(16) unsigned char smraw_[];
     CSm<S>& sm = *reinterpret_cast<CSm<S>*>(smraw_);
     __shared__ int nver;
@@ -1297,6 +1305,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     const int nbu = ws_update && ctx->num_sms < nb ? ctx->num_sms : nb;
     // one iteration's sweeps up to and including the convergence test
     // (m <= 0: inside the device-driven loop, see k_ctl_update)
+    int gated = 0;  // lookahead loop: control kernels gated on the control word too
     auto sweeps = [&](int m, cudaGraphConditionalHandle loop) -> bk_status {
         halo(a.P);
         phase_mark(ctx, -1);
@@ -1309,7 +1318,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
         phase_mark(ctx, 0);
         ++ctx->launches;
         reduce(S * S, nbs);
-        k_ctl_alpha<S><<<1, CBS, cs, s>>>(ctl, red);
+        k_ctl_alpha<S><<<1, CBS, cs, s>>>(ctl, red, gated);
         ++ctx->launches;
         phase_mark(ctx, -1);
         if (ws_update) {
@@ -1320,7 +1329,7 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
         phase_mark(ctx, 1);
         ++ctx->launches;
         reduce(E, nbu);
-        k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, red, m, loop, cfg->max_iter);
+        k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, red, m, loop, cfg->max_iter, gated);
         ++ctx->launches;
         BK_CUDA_TRY(ctx, cudaGetLastError());
         return BK_OK;
@@ -1402,7 +1411,73 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
     auto read_iters = [&](int* iters) -> bk_status {
         return read_small(ctx, iters, &ctl->iters, sizeof(int));
     };
+    // the verification due after iteration m (solvers.cpp:582-634): 1 = go on
+    // with iteration m + 1, 0 = solve finished, < 0 = error
+    auto verify = [&]() -> int {
+        if (launch_pupdate<S, 2>(a, nb, s) != cudaSuccess) return -1;
+        ++ctx->launches;
+        halo(a.X);
+        true_res();
+        k_ctl_verify<S><<<1, CBS, cs, s>>>(ctl, red);
+        ++ctx->launches;
+        if (read_cmd(&cmd, &sa) != BK_OK) return -1;
+        if (cmd == kCmdDone) return 0;
+        if (cmd == kCmdRestart) {
+            k_anchor<S, kRestart><<<nb, LBS, swa, s>>>(a);
+            ++ctx->launches;
+            reduce(E, nb);
+            k_ctl_restart<S><<<1, CBS, 0, s>>>(ctl, red);
+            ++ctx->launches;
+            return 1;
+        }
+        phase_mark(ctx, -1);
+        if (launch_pupdate<S, 0>(a, nb, s) != cudaSuccess) return -1;
+        phase_mark(ctx, 2);
+        ++ctx->launches;
+        return 1;
+    };
     int m = 0;  // iterations done
+    // Lookahead loop (default; single slab, no graph loop, no per-sweep event
+    // timing): iteration m + 1 is enqueued — every sweep and control kernel
+    // gated on the control word — before the host waits for iteration m's
+    // word, which is copied asynchronously into mapped pinned memory; the
+    // device never drains between iterations. A verification due at m turns
+    // the enqueued m + 1 into no-ops; the host verifies and re-issues m + 1.
+    // The same kernels run on the same data as the synchronous loop, so the
+    // result is bitwise the same.
+    if (!gexec && !comm && !ctx->knobs.phase_timing && !ctx->knobs.no_lookahead &&
+        m < cfg->max_iter && sa > 0) {
+        auto issue = [&](int it) -> bk_status {
+            a.gate = &ctl->cmd;
+            gated = 1;
+            bk_status is = sweeps(it, 0);
+            if (is == BK_OK) is = pupdate();
+            if (is == BK_OK) is = post_small(ctx, it & 1, &ctl->sa, 4 * sizeof(int));
+            a.gate = nullptr;
+            gated = 0;
+            return is;
+        };
+        m = 1;
+        if ((st = issue(m)) != BK_OK) return st;
+        for (;;) {
+            const bool ahead = m + 1 <= cfg->max_iter;
+            if (ahead && (st = issue(m + 1)) != BK_OK) return st;
+            int h[4];  // sa, nver, iters, cmd
+            if ((st = wait_small(ctx, m & 1, h, sizeof(h))) != BK_OK) return st;
+            if (h[3] == kCmdPupdate) {  // iteration m closed with its P update
+                if (!ahead) break;
+                ++m;
+                continue;
+            }
+            const int v = verify();  // the enqueued m + 1 ran as no-ops
+            if (v < 0) return fail(ctx, BK_CUDA_ERROR, "block_cg: verification");
+            if (v == 0) break;
+            ++m;
+            if (m > cfg->max_iter || sa <= 0) break;
+            if ((st = issue(m)) != BK_OK) return st;
+        }
+        m = cfg->max_iter;  // the synchronous loop below does not run
+    }
     while (m < cfg->max_iter && sa > 0) {
         if (gexec) {
             BK_CUDA_TRY(ctx, cudaGraphLaunch(gexec, s));
@@ -1422,26 +1497,9 @@ bk_status block_cg_large_t(bk_ctx* ctx, const bk_operator* op, int nyl, int y0,
             }
         }
         // cmd == kCmdVerify
-        BK_CUDA_TRY(ctx, (launch_pupdate<S, 2>(a, nb, s)));
-        ++ctx->launches;
-        halo(a.X);
-        true_res();
-        k_ctl_verify<S><<<1, CBS, cs, s>>>(ctl, red);
-        ++ctx->launches;
-        if ((st = read_cmd(&cmd, &sa)) != BK_OK) return st;
-        if (cmd == kCmdDone) break;
-        if (cmd == kCmdRestart) {
-            k_anchor<S, kRestart><<<nb, LBS, swa, s>>>(a);
-            ++ctx->launches;
-            reduce(E, nb);
-            k_ctl_restart<S><<<1, CBS, 0, s>>>(ctl, red);
-            ++ctx->launches;
-            continue;
-        }
-        phase_mark(ctx, -1);
-        BK_CUDA_TRY(ctx, (launch_pupdate<S, 0>(a, nb, s)));
-        phase_mark(ctx, 2);
-        ++ctx->launches;
+        const int v = verify();
+        if (v < 0) return fail(ctx, BK_CUDA_ERROR, "block_cg: verification");
+        if (v == 0) break;
     }
     // honest residuals for still-active columns
     if ((st = read_small(ctx, &sa, &ctl->sa, sizeof(int))) != BK_OK) return st;
@@ -1537,6 +1595,12 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
     constexpr int E = S * S + S;
     const int nb = b->nb;
     cudaStream_t s = ctx->stream;
+    // BK_DD_GATED: the sweep and control kernels of an iteration enqueued
+    // ahead of the host's read of the previous iteration's control word run
+    // only while that word says "P update" (no verification pending)
+    const int gated = (step & BK_DD_GATED) ? 1 : 0;
+    step &= ~BK_DD_GATED;
+    if (gated) a.gate = &ctl->cmd;
     // S = 64 on 16-aligned x: the warp-specialised sweeps of the single-GPU
     // engine (one CTA per SM, deferred X), their partial count and the packed
     // stencil coefficients (built by BK_DD_INIT_SWEEP)
@@ -1616,7 +1680,7 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
             break;
         case BK_DD_CTL_ALPHA:
             BK_CUDA_TRY(ctx, set((const void*)k_ctl_alpha<S>, cs));
-            k_ctl_alpha<S><<<1, CBS, cs, s>>>(ctl, b->red);
+            k_ctl_alpha<S><<<1, CBS, cs, s>>>(ctl, b->red, gated);
             ++ctx->launches;
             break;
         case BK_DD_UPDATE:
@@ -1627,7 +1691,7 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
             break;
         case BK_DD_CTL_UPDATE:
             BK_CUDA_TRY(ctx, set((const void*)k_ctl_update<S>, cs));
-            k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, b->red, m, 0, 0);
+            k_ctl_update<S><<<1, CBS, cs, s>>>(ctl, b->red, m, 0, 0, gated);
             ++ctx->launches;
             break;
         case BK_DD_TRUE_RES:
@@ -1671,6 +1735,11 @@ bk_status dd_step_t(bk_ctx* ctx, const bk_operator* op, int y0, int nyl, const b
             }
             break;
         }
+        case BK_DD_READ_ASYNC:
+            // cmd / sa: pinned host words, valid until the stream passes the copies
+            BK_CUDA_TRY(ctx, cudaMemcpyAsync(cmd, &ctl->cmd, sizeof(int), cudaMemcpyDeviceToHost, s));
+            BK_CUDA_TRY(ctx, cudaMemcpyAsync(sa, &ctl->sa, sizeof(int), cudaMemcpyDeviceToHost, s));
+            break;
         case BK_DD_READ: {
             int h[2];
             BK_CUDA_TRY(ctx, cudaMemcpyAsync(h, &ctl->cmd, sizeof(int), cudaMemcpyDeviceToHost, s));

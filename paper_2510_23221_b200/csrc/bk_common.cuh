@@ -41,6 +41,7 @@ struct bk_knobs {
     bool comb_one_role = false; // single-plane combine/action: the one-role kernel
     int spmm_band = 0;         // S = 64 stencil sweep: x-runs per y-band (0: default 4)
     bool graph_loop = false;   // multi-kernel solve: device-driven iterations (CUDA graph while-loop)
+    bool no_lookahead = false; // multi-kernel solve: the synchronous host loop (one drain per iteration)
 };
 
 // Optional per-kernel-kind timing of the multi-kernel solve (option
@@ -75,6 +76,7 @@ struct bk_ctx {
     cudaEvent_t drain_ev[2] = {};          // copy stream done with output parity p
     void* hmap = nullptr;                  // mapped pinned host page for small readbacks
     void* hmap_dev = nullptr;
+    cudaEvent_t look_ev[2] = {};          // post_small / wait_small slots
     bool drain_pending[2] = {};
     void* pin[2] = {};                     // pinned staging of the dataset writer / validator
     size_t pin_bytes = 0;
@@ -202,8 +204,13 @@ bk_status ensure_copy_stream(bk_ctx* ctx);
 bool is_device_ptr(const void* p);
 // Copy a few bytes device -> host through a kernel writing mapped pinned
 // memory (no copy engine: it never queues behind a large in-flight D2H drain)
-// and synchronize the stream. bytes <= 64 KiB, multiple of 4.
+// and synchronize the stream. bytes <= 32 KiB, multiple of 4.
 bk_status read_small(bk_ctx* ctx, void* host_dst, const void* dev_src, size_t bytes);
+// Asynchronous form for the lookahead loop: post_small enqueues the copy into
+// slot (0 / 1) of the same mapped page and records an event; wait_small waits
+// for that event and copies the words out. bytes <= 256, multiple of 4.
+bk_status post_small(bk_ctx* ctx, int slot, const void* dev_src, size_t bytes);
+bk_status wait_small(bk_ctx* ctx, int slot, void* host_dst, size_t bytes);
 cudaError_t launch_copy_words(cudaStream_t s, unsigned* dst, const unsigned* src, size_t words);
 
 // Kernels' host-side launchers (return cudaError_t of the launch).

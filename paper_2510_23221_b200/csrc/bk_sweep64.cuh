@@ -324,6 +324,7 @@ __device__ __forceinline__ void update64_warp(Smem& sm, const SweepArgs& a, int 
 __global__ void __launch_bounds__(kConsumers, 1)
     k_update64_ws(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapR,
                   SweepArgs a) {
+    if (a.gate && *a.gate != 0) return;  // gated (DD lookahead): this iteration is a no-op
     constexpr int S = 64;
     extern __shared__ __align__(1024) unsigned char smraw_[];
     // 1024-byte aligned (128B-swizzle atoms); pointer arithmetic on the shared
@@ -547,6 +548,7 @@ __device__ __forceinline__ Pencil pencil_of(const Slab& sl, int p) {
 }
 
 __global__ void __launch_bounds__(kSThreads, 1) k_spmm64_ws(SweepArgs a) {
+    if (a.gate && *a.gate != 0) return;  // gated (DD lookahead): this iteration is a no-op
     constexpr int S = 64;
     extern __shared__ __align__(1024) unsigned char smraw_[];
     SmemS& sm = *reinterpret_cast<SmemS*>(smraw_ + ((1024u - (smem_u32(smraw_) & 1023u)) & 1023u));
@@ -873,6 +875,7 @@ __device__ __forceinline__ void spmm_gram_warp(SmemR<B>& sm, const SweepArgs& a,
 
 template <int B, bool WIN = true>
 __global__ void __launch_bounds__(kRThreads, 1) k_spmm64_rs(SweepArgs a) {
+    if (a.gate && *a.gate != 0) return;  // gated (DD lookahead): this iteration is a no-op
     constexpr int S = 64;
     constexpr int RS = Band<B>::RS, RC = Band<B>::RC;
     extern __shared__ __align__(1024) unsigned char smraw_[];

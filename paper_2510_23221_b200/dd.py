@@ -33,7 +33,9 @@ from typing import List, Optional
 import numpy as np
 
 INIT_SWEEP, CTL_INIT, SPMM, CTL_ALPHA, UPDATE, CTL_UPDATE, TRUE_RES, CTL_VERIFY, \
-    RESTART_SWEEP, CTL_RESTART, PUPDATE, CTL_FINAL, READ, UPDATE_D, PUPDATE_X, APPLY_X = range(16)
+    RESTART_SWEEP, CTL_RESTART, PUPDATE, CTL_FINAL, READ, UPDATE_D, PUPDATE_X, APPLY_X, \
+    READ_ASYNC = range(17)
+GATED = 0x100  # BK_DD_GATED: the kernels run only while no verification is pending
 CMD_PUPDATE, CMD_VERIFY, CMD_RESTART, CMD_DONE = range(4)
 
 
@@ -146,6 +148,7 @@ class Slab:
 
 
 def _red_count(kind: int, S: int) -> int:
+    kind &= ~GATED
     return {INIT_SWEEP: S * S + S, SPMM: S * S, UPDATE: S * S + S, UPDATE_D: S * S + S,
             TRUE_RES: S, RESTART_SWEEP: S * S + S}[kind]
 
@@ -243,9 +246,50 @@ def _on_torch_stream(slabs):
         sl.ctx.set_stream(cs)
 
 
-def dd_block_cg(slabs, comm, cfg, report_arrays=True):
+class _ControlSlots:
+    """Pinned host words for BK_DD_READ_ASYNC: two slots (iterations m and
+    m + 1 in flight), each (cmd, sa) per slab plus the event that marks the
+    copies done."""
+
+    def __init__(self, nslabs):
+        import torch
+
+        self.words = [torch.zeros((nslabs, 2), dtype=torch.int32).pin_memory() for _ in range(2)]
+        self.events = [None, None]
+
+    def post(self, slabs, cfg_c, m):
+        import torch
+
+        w = self.words[m & 1]
+        for i, sl in enumerate(slabs):
+            lib = sl.bk._load()
+            ptr = w.data_ptr() + 8 * i
+            st = lib.bk_dd_step(sl.ctx.h, sl.op.h, sl.y0, sl.nyl, sl.S, C.byref(sl._bufs),
+                                C.byref(cfg_c), READ_ASYNC, m, C.c_void_p(ptr),
+                                C.c_void_p(ptr + 4), None)
+            sl.bk._raise(st, sl.ctx.h, "dd_step(READ_ASYNC)")
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.events[m & 1] = ev
+
+    def wait(self, m):
+        self.events[m & 1].synchronize()
+        vals = [tuple(int(v) for v in row) for row in self.words[m & 1].tolist()]
+        assert all(v == vals[0] for v in vals), "ranks disagree on control state"
+        return vals[0]
+
+
+def dd_block_cg(slabs, comm, cfg, report_arrays=True, lookahead=True):
     """Run the decomposed block CG over `slabs` (lockstep). Returns the report
-    of slab 0 (every rank's control state is identical)."""
+    of slab 0 (every rank's control state is identical).
+
+    lookahead: iteration m + 1 is enqueued (BK_DD_GATED kernels, halo and
+    all-reduces) before the host waits for iteration m's control word, read
+    asynchronously into pinned memory — the device never drains between
+    iterations. A verification due at m turns the enqueued m + 1 into no-ops
+    (the gate), the host runs the verification and re-issues m + 1: the same
+    kernel sequence on the same data as the synchronous loop (lookahead=False),
+    so bitwise the same X."""
     bk = slabs[0].bk
     S = slabs[0].S
     cfg_c = cfg._c()
@@ -255,7 +299,7 @@ def dd_block_cg(slabs, comm, cfg, report_arrays=True):
         out = None
         for sl in slabs:
             out = sl.step(kind, cfg_c, m)
-        if kind in (INIT_SWEEP, SPMM, UPDATE, UPDATE_D, TRUE_RES, RESTART_SWEEP):
+        if kind & ~GATED in (INIT_SWEEP, SPMM, UPDATE, UPDATE_D, TRUE_RES, RESTART_SWEEP):
             comm.allreduce(slabs, _red_count(kind, S))
         return out
 
@@ -271,32 +315,10 @@ def dd_block_cg(slabs, comm, cfg, report_arrays=True):
     all_step(INIT_SWEEP)
     all_step(CTL_INIT)
     cmd, sa = read()
-    m = 1
-    while m <= cfg.max_iter and sa > 0:
-        comm.halo(slabs, "P")
-        all_step(SPMM)
-        all_step(CTL_ALPHA)
-        all_step(UPDATE_D if deferred else UPDATE)
-        all_step(CTL_UPDATE, m)
-        cmd, sa = read()
-        if cmd == CMD_VERIFY:
-            if deferred:
-                all_step(APPLY_X)
-            comm.halo(slabs, "X")
-            all_step(TRUE_RES)
-            all_step(CTL_VERIFY)
-            cmd, sa = read()
-            if cmd == CMD_DONE:
-                break
-            if cmd == CMD_RESTART:
-                all_step(RESTART_SWEEP)
-                all_step(CTL_RESTART)
-                m += 1
-                continue
-            all_step(PUPDATE)
-        else:
-            all_step(PUPDATE_X if deferred else PUPDATE)
-        m += 1
+    if lookahead:
+        _pipelined_iterations(slabs, comm, cfg, cfg_c, all_step, read, deferred, sa)
+    else:
+        _synchronous_iterations(slabs, comm, cfg, all_step, read, deferred, sa)
     _, sa = read()
     if sa > 0:
         comm.halo(slabs, "X")
@@ -311,12 +333,88 @@ def dd_block_cg(slabs, comm, cfg, report_arrays=True):
                           matvec_count=rep.matvec_count)
 
 
+def _verify(slabs, comm, all_step, read, deferred):
+    """True-residual verification after iteration m flagged columns
+    (solvers.cpp:582-634). Returns the control word after it."""
+    if deferred:
+        all_step(APPLY_X)
+    comm.halo(slabs, "X")
+    all_step(TRUE_RES)
+    all_step(CTL_VERIFY)
+    return read()
+
+
+def _pipelined_iterations(slabs, comm, cfg, cfg_c, all_step, read, deferred, sa):
+    slots = _ControlSlots(len(slabs))
+
+    def issue(m):
+        comm.halo(slabs, "P")
+        all_step(SPMM | GATED)
+        all_step(CTL_ALPHA | GATED)
+        all_step((UPDATE_D if deferred else UPDATE) | GATED)
+        all_step(CTL_UPDATE | GATED, m)
+        all_step((PUPDATE_X if deferred else PUPDATE) | GATED)
+        slots.post(slabs, cfg_c, m)
+
+    m = 1
+    if m > cfg.max_iter or sa <= 0:
+        return
+    issue(m)
+    while True:
+        ahead = m + 1 <= cfg.max_iter
+        if ahead:
+            issue(m + 1)
+        cmd, _ = slots.wait(m)
+        if cmd == CMD_PUPDATE:  # iteration m closed with its P update
+            if not ahead:
+                return
+            m += 1
+            continue
+        # verification due at m: the enqueued m + 1 ran as no-ops
+        cmd, sa = _verify(slabs, comm, all_step, read, deferred)
+        if cmd == CMD_DONE:
+            return
+        if cmd == CMD_RESTART:
+            all_step(RESTART_SWEEP)
+            all_step(CTL_RESTART)
+        else:
+            all_step(PUPDATE)
+        m += 1
+        if m > cfg.max_iter or sa <= 0:
+            return
+        issue(m)
+
+
+def _synchronous_iterations(slabs, comm, cfg, all_step, read, deferred, sa):
+    m = 1
+    while m <= cfg.max_iter and sa > 0:
+        comm.halo(slabs, "P")
+        all_step(SPMM)
+        all_step(CTL_ALPHA)
+        all_step(UPDATE_D if deferred else UPDATE)
+        all_step(CTL_UPDATE, m)
+        cmd, sa = read()
+        if cmd == CMD_VERIFY:
+            cmd, sa = _verify(slabs, comm, all_step, read, deferred)
+            if cmd == CMD_DONE:
+                break
+            if cmd == CMD_RESTART:
+                all_step(RESTART_SWEEP)
+                all_step(CTL_RESTART)
+                m += 1
+                continue
+            all_step(PUPDATE)
+        else:
+            all_step(PUPDATE_X if deferred else PUPDATE)
+        m += 1
+
+
 def make_slabs(bk, ctx, op, s: int, parts):
     S = kernel_width(s)
     return [Slab(bk, ctx, op, y0, nyl, S).allocate() for (y0, nyl) in parts]
 
 
-def solve_decomposed(bk, ctx, op, B_global, cfg, parts, comm=None, X_global=None):
+def solve_decomposed(bk, ctx, op, B_global, cfg, parts, comm=None, X_global=None, lookahead=True):
     """Convenience: virtual (LocalComm) decomposition of one GPU's solve.
     B_global: n x S device tensor. Returns (X_global, report)."""
     import torch
@@ -328,7 +426,7 @@ def solve_decomposed(bk, ctx, op, B_global, cfg, parts, comm=None, X_global=None
     slabs = make_slabs(bk, ctx, op, S, parts)
     for sl in slabs:
         sl.load_rhs(B_global)
-    rep = dd_block_cg(slabs, comm or LocalComm(), cfg)
+    rep = dd_block_cg(slabs, comm or LocalComm(), cfg, lookahead=lookahead)
     if X_global is None:
         X_global = torch.empty_like(B_global)
     for sl in slabs:

@@ -542,6 +542,57 @@ def test_block_cg_graph_loop_bitwise(bk, ctx, oracle, case):
     assert g.report.all_converged() and rel_l2(g.x, X) <= PARITY
 
 
+@pytest.mark.parametrize("case", [(5, 48, 40, 16, 64), (3, 16, 16, 8, 32), (2, 40, 36, 1, 16)])
+def test_block_cg_lookahead_bitwise(bk, ctx, oracle, case):
+    """The default lookahead loop of the multi-kernel engine (iteration m + 1
+    enqueued with gated kernels before the host reads iteration m's control
+    word) gives bitwise the synchronous loop's X and report: capped runs, and
+    full solves through every verification."""
+    inp = bk.synth_chip(*case, 4)
+    op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
+    o = oracle.assemble(grid_tuple(inp.grid), inp.k, inp.bc.as_tuples(), dz=inp.grid.dz)
+    B = oracle.rhs_from_power(o, inp.q_basis)
+    for m in (1, 2, 7, 100000):
+        cfg = cfg_jacobi(m) if m < 100000 else cfg_jacobi()
+        with ctx.options(force_large=1, no_lookahead=1):
+            h = bk.block_cg(op, B, cfg)
+        with ctx.options(force_large=1):
+            g = bk.block_cg(op, B, cfg)
+        assert np.array_equal(h.x, g.x), m
+        assert h.report.iterations == g.report.iterations
+        assert h.report.matvec_count == g.report.matvec_count
+        assert np.array_equal(h.report.final_rel_residual, g.report.final_rel_residual)
+        assert np.array_equal(h.report.converged, g.report.converged)
+    X, rep = oracle.block_cg(o, B, TOL, 100000, 1)
+    assert g.report.all_converged() and rel_l2(g.x, X) <= PARITY
+
+
+@pytest.mark.parametrize("case", [(5, 48, 40, 16, 64, 2), (5, 40, 36, 16, 64, 2)])
+@pytest.mark.parametrize("nslabs", [2, 3])
+def test_slab_lookahead_bitwise(bk, ctx, nslabs, case):
+    """dd_block_cg's lookahead loop (BK_DD_GATED steps, asynchronous control
+    reads) is bitwise its synchronous loop, with virtual ranks on one GPU."""
+    import torch
+
+    from paper_2510_23221_b200 import dd
+
+    inp = bk.synth_chip(*case)
+    op = bk.assemble(inp.k, inp.grid, inp.bc, ctx)
+    dev = torch.device("cuda", 0)
+    q = torch.from_numpy(inp.q_basis).to(dev)
+    B = torch.empty_like(q)
+    bk.rhs_from_power(op, q, out=B)
+    parts = dd.partition_rows(inp.grid.ny, nslabs)
+    for cfg in (cfg_jacobi(3), cfg_jacobi()):
+        Xs, rs = dd.solve_decomposed(bk, ctx, op, B, cfg, parts, lookahead=False)
+        Xl, rl = dd.solve_decomposed(bk, ctx, op, B, cfg, parts, lookahead=True)
+        torch.cuda.synchronize()
+        assert torch.equal(Xs, Xl)
+        assert rs.iterations == rl.iterations and rs.matvec_count == rl.matvec_count
+        assert np.array_equal(rs.final_rel_residual, rl.final_rel_residual)
+    assert rl.all_converged()
+
+
 @pytest.mark.parametrize("case", [(5, 48, 40, 16, 64, 2), (5, 40, 36, 16, 64, 2)])
 @pytest.mark.parametrize("nslabs", [1, 2, 3])
 def test_slab_decomposition_matches_single_gpu(bk, ctx, nslabs, case):
