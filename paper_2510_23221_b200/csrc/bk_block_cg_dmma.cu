@@ -1092,7 +1092,16 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
                              sm.akeep[(4 * ks + t) * Strides<S>::RS + 8 * n + g]);
                 Xv.store(base, g, t, x);
             }
-            __syncthreads();
+            // The sweeps that follow apply the stencil to X and so read the
+            // halo cells other CTAs of the group just updated: a group
+            // barrier, not a CTA one (resident mode gets it from publish_x).
+            // Without it the true residual was formed from a mix of old and
+            // new X near CTA boundaries and a borderline column could restart
+            // in one run and freeze in the next.
+            if constexpr (RES)
+                __syncthreads();
+            else
+                gr.sync(grid);
             xdone = true;
         };
         if (nver > 0) {

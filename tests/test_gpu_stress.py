@@ -29,7 +29,7 @@ def dev_chips(bk, cases):
     return out
 
 
-def batch_runs(bk, ctx, cases, streams, tol=1e-12, it=100000, **opts):
+def batch_runs(bk, ctx, cases, streams, tol=1e-12, it=100000, reps=REPS, **opts):
     import torch
 
     chips = dev_chips(bk, cases)
@@ -37,7 +37,7 @@ def batch_runs(bk, ctx, cases, streams, tol=1e-12, it=100000, **opts):
     n, N = chips[0].grid.cell_count(), int(chips[0].coef.shape[1])
     outs = []
     with ctx.options(**opts):
-        for _ in range(REPS):
+        for _ in range(reps):
             T = [torch.full((N, n), float("nan"), dtype=torch.float64, device=dev) for _ in chips]
             Q = [torch.full((N, n), float("nan"), dtype=torch.float64, device=dev) for _ in chips]
             R = [torch.full((N,), float("nan"), dtype=torch.float64, device=dev) for _ in chips]
@@ -65,6 +65,11 @@ def batch_runs(bk, ctx, cases, streams, tol=1e-12, it=100000, **opts):
      "block_cg_dmma_kernel<16,0,1,1> ring"),
     ([(2, 48, 40, 1, 16, 24, 1, c) for c in range(8)], 8, {}, "block_cg_dmma_kernel<16,1,1,0>"),
     ([(3, 32, 24, 8, 32, 20, 1, c) for c in range(3)], 3, {}, "block_cg_dmma_kernel<32,0,1,1>"),
+    # deferred X, 3D, few cells per CTA: the true-residual sweep reads X halo
+    # cells of up to ~12 other CTAs (a CTA-only barrier after the deferred X
+    # update let it see stale ones; fixed with a group barrier)
+    ([(3, 32, 24, 8, 32, 20, 1, c) for c in range(6)], 6, {"reps": 8},
+     "block_cg_dmma_kernel<32,0,1,1>"),
     ([(4, 32, 24, 4, 16, 8, 1, c) for c in range(8)], 8, {"no_resident": 1},
      "block_cg_dmma_kernel<16,0,1,0>"),
     ([(2, 64, 48, 1, 16, 40, 1, c) for c in range(4)], 4, {"comb_one_role": 1},
