@@ -113,7 +113,7 @@ template <int W>
 struct GramSet;
 template <>
 struct GramSet<0> {  // (0,0..4)
-    static constexpr int NM = 1, NN = 5;
+    static constexpr int NM = 1, NN = 5, DIAG = 0;
     static __device__ __forceinline__ constexpr int M(int j) { return j == 0 ? 0 : 0; }
     static __device__ __forceinline__ constexpr int N(int j) { return j == 0 ? 0 : j == 1 ? 1 : j == 2 ? 2 : j == 3 ? 3 : 4; }
     static __device__ __forceinline__ constexpr int TM(int j) { return j == 0 ? 0 : j == 1 ? 0 : j == 2 ? 0 : j == 3 ? 0 : 0; }
@@ -121,7 +121,7 @@ struct GramSet<0> {  // (0,0..4)
 };
 template <>
 struct GramSet<1> {  // (0,5..7), (1,2..3)
-    static constexpr int NM = 2, NN = 5;
+    static constexpr int NM = 2, NN = 5, DIAG = 3;
     static __device__ __forceinline__ constexpr int M(int j) { return j == 0 ? 0 : 1; }
     static __device__ __forceinline__ constexpr int N(int j) { return j == 0 ? 5 : j == 1 ? 6 : j == 2 ? 7 : j == 3 ? 2 : 3; }
     static __device__ __forceinline__ constexpr int TM(int j) { return j == 0 ? 0 : j == 1 ? 0 : j == 2 ? 0 : j == 3 ? 1 : 1; }
@@ -129,7 +129,7 @@ struct GramSet<1> {  // (0,5..7), (1,2..3)
 };
 template <>
 struct GramSet<2> {  // (1,4..7), (2,4)
-    static constexpr int NM = 2, NN = 4;
+    static constexpr int NM = 2, NN = 4, DIAG = 4;
     static __device__ __forceinline__ constexpr int M(int j) { return j == 0 ? 1 : 2; }
     static __device__ __forceinline__ constexpr int N(int j) { return j == 0 ? 4 : j == 1 ? 5 : j == 2 ? 6 : j == 3 ? 7 : 0; }
     static __device__ __forceinline__ constexpr int TM(int j) { return j == 0 ? 0 : j == 1 ? 0 : j == 2 ? 0 : j == 3 ? 0 : 1; }
@@ -137,12 +137,23 @@ struct GramSet<2> {  // (1,4..7), (2,4)
 };
 template <>
 struct GramSet<3> {  // (2,5..7), (3,6..7)
-    static constexpr int NM = 2, NN = 3;
+    static constexpr int NM = 2, NN = 3, DIAG = 3;
     static __device__ __forceinline__ constexpr int M(int j) { return j == 0 ? 2 : 3; }
     static __device__ __forceinline__ constexpr int N(int j) { return j == 0 ? 5 : j == 1 ? 6 : j == 2 ? 7 : j == 3 ? 0 : 0; }
     static __device__ __forceinline__ constexpr int TM(int j) { return j == 0 ? 0 : j == 1 ? 0 : j == 2 ? 0 : j == 3 ? 1 : 1; }
     static __device__ __forceinline__ constexpr int TN(int j) { return j == 0 ? 0 : j == 1 ? 1 : j == 2 ? 2 : j == 3 ? 1 : 2; }
 };
+// Rows 0-7 of a 16 x 8 tile (accumulators d[0], d[1]): one DMMA.8x8x4 instead
+// of the m16n8k4's two. Used for each warp's diagonal tile (m, n = 2m), whose
+// rows 8-15 lie strictly below the diagonal and are never read (the s x s
+// solves read the upper triangle): 18 instead of 20 tile-halves per k-step
+// and team, -10 % of the Gram's DMMA work, upper entries bitwise unchanged.
+__device__ __forceinline__ void dmma_h(double (&d)[4], double a0, double b) {
+    asm volatile(
+        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(d[0]), "+d"(d[1])
+        : "d"(a0), "d"(b));
+}
 // one staged 16-cell run into warp W's tiles: A = rows of `At` (m-blocks),
 // B = rows of `Bt` (n-blocks) scaled per cell by dg[kc] when SCALE
 template <int W, bool SCALE>
@@ -165,7 +176,12 @@ __device__ __forceinline__ void gram_run(double (&gacc)[5][4], const unsigned ch
             b[j] = SCALE ? dg[kc] * x : x;
         }
 #pragma unroll
-        for (int i = 0; i < 5; ++i) dmma_l(gacc[i], a0[GS::TM(i)], a1[GS::TM(i)], b[GS::TN(i)]);
+        for (int i = 0; i < 5; ++i) {
+            if (i == GS::DIAG)
+                dmma_h(gacc[i], a0[GS::TM(i)], b[GS::TN(i)]);
+            else
+                dmma_l(gacc[i], a0[GS::TM(i)], a1[GS::TM(i)], b[GS::TN(i)]);
+        }
     }
 }
 template <int W>

@@ -1,5 +1,6 @@
 """Per-sweep device times of the C5 multi-kernel solve (capped iterations),
 A/B over kernel-variant options:  python scripts/c5_phases.py [iters] [opt=v ...]"""
+import hashlib
 import os
 import sys
 
@@ -36,4 +37,5 @@ for variant in ({}, opts) if opts else ({},):
             ref = Xh
         print(f"{variant or 'default'} {ctx.last_solver_variant}: {e0.elapsed_time(e1) / it:.3f} ms/iter",
               {k: round(v["ms"] / max(v["launches"], 1), 3) for k, v in ph.items()},
-              "matvecs", r.report.matvec_count, "rel diff vs first", diff, flush=True)
+              "matvecs", r.report.matvec_count, "rel diff vs first", diff,
+              "sha", hashlib.sha256(Xh.tobytes()).hexdigest()[:16], flush=True)

@@ -2,6 +2,6 @@
 # scratch job file for one gpurun call (the command of the latest A/B run)
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-for i in 1 2 3 4 5 6; do timeout 600 python -m pytest tests/test_gpu_stress.py -q -k "batched_solve_and_combine_repeatable" > gpurun_out/st$i.log 2>&1; echo "rc=$?" >> gpurun_out/st$i.log; done
-timeout 1500 python -m pytest tests -m gpu -q -x --durations=5 > gpurun_out/t.log 2>&1
+bash scripts/ab_lib.sh "python scripts/c5_phases.py 100; python scripts/c5_phases.py 100" > gpurun_out/ab.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -x -k "c5 or multikernel or s64 or slab or lookahead or graph_loop" > gpurun_out/t.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/t.log
