@@ -255,6 +255,14 @@ const char* bk_last_solver_variant(const bk_ctx* ctx);
  * entries: [0] stencil-SpMM + Gram (W = A P, P^T W), [1] R update + S_new,
  * [2] P update (+ the deferred X update), [3] reserved. */
 bk_status bk_last_solve_phases(const bk_ctx* ctx, double* ms, int64_t* counts);
+/* Measurement aid (no reference counterpart): the FP64 tensor-core rate of
+ * this GPU, TFLOP/s of register-operand mma.sync.m16n8k4.f64 chains on every
+ * SM (32 warps per SM, 4 independent accumulator chains per warp).
+ * burst = best of 10 launches of ~2 ms each; sustained = launches back to back
+ * for `seconds` (the rate the FP64 pipe holds at the board's power limit —
+ * the roofline denominator for a kernel timed inside a long FP64 step). */
+bk_status bk_measure_fp64_peak(bk_ctx* ctx, double seconds, double* burst_tflops,
+                               double* sustained_tflops);
 
 /* ---- y-slab domain decomposition (BASELINE config 5 across GPUs) -----------
  * A rank owns global rows [y0, y0 + nyl) of the grid of `op` (the GLOBAL

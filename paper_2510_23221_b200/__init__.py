@@ -172,6 +172,8 @@ def _load():
         lib.bk_last_solver_variant.argtypes = [vp]
         lib.bk_last_solver_variant.restype = C.c_char_p
         lib.bk_last_solve_phases.argtypes = [vp, vp, vp]
+        lib.bk_measure_fp64_peak.argtypes = [vp, C.c_double, C.POINTER(C.c_double),
+                                             C.POINTER(C.c_double)]
         lib.bk_assemble.argtypes = [vp, C.POINTER(_Grid), dp, C.POINTER(_Face), C.POINTER(vp)]
         lib.bk_operator_free.argtypes = [vp]
         lib.bk_assemble_into.argtypes = [vp, C.POINTER(_Grid), dp, C.POINTER(_Face), vp]
@@ -458,6 +460,15 @@ class Context:
                                             cnt.ctypes.data_as(C.c_void_p)), self.h, "phases")
         names = ("spmm", "update", "pupdate", "other")
         return {nm: {"ms": float(ms[i]), "launches": int(cnt[i])} for i, nm in enumerate(names)}
+
+    def measure_fp64_peak(self, seconds: float = 4.0) -> tuple:
+        """(burst, sustained) FP64 tensor-core TFLOP/s of this GPU
+        (bk_measure_fp64_peak): best of 10 short launches, and launches back
+        to back for `seconds` (the rate at the board's power limit)."""
+        b, s = C.c_double(0.0), C.c_double(0.0)
+        _raise(_load().bk_measure_fp64_peak(self.h, float(seconds), C.byref(b), C.byref(s)),
+               self.h, "measure_fp64_peak")
+        return float(b.value), float(s.value)
 
     def set_option(self, name: str, value: int) -> None:
         """Per-context kernel-variant switch (bk_set_option): "ring" (-1 auto,

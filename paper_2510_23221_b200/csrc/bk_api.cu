@@ -805,6 +805,68 @@ bk_status bk_last_solve_phases(const bk_ctx* ctx, double* ms, int64_t* counts) {
     return BK_OK;
 }
 
+namespace {
+// register-operand DMMA chains: 4 independent accumulators per warp
+__global__ void __launch_bounds__(1024, 1) k_fp64_peak(double* out, int iters) {
+    double d[4][4];
+    for (int c = 0; c < 4; ++c)
+        for (int e = 0; e < 4; ++e) d[c][e] = threadIdx.x * 1e-3 + c;
+    const double a0 = 1.0000001, a1 = 0.9999999, b = 1.0000002;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            asm volatile(
+                "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+                "{%0,%1,%2,%3};"
+                : "+d"(d[c][0]), "+d"(d[c][1]), "+d"(d[c][2]), "+d"(d[c][3])
+                : "d"(a0), "d"(a1), "d"(b));
+    double s = 0.0;
+    for (int c = 0; c < 4; ++c) s += d[c][0] + d[c][3];
+    out[(size_t)blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+}  // namespace
+
+bk_status bk_measure_fp64_peak(bk_ctx* ctx, double seconds, double* burst_tflops,
+                               double* sustained_tflops) {
+    if (!ctx || !burst_tflops || !sustained_tflops || !(seconds >= 0.0))
+        return BK_INVALID_CONFIG;
+    cudaSetDevice(ctx->device);
+    const int blocks = ctx->num_sms, threads = 1024, iters = 4000;
+    const double flops = 2.0 * 16 * 8 * 4 * 4 * (double)iters * (threads / 32) * blocks;
+    double* out = nullptr;
+    BK_CUDA_TRY(ctx, cudaMalloc(&out, (size_t)blocks * threads * sizeof(double)));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto done = [&](bk_status st) {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFree(out);
+        return st;
+    };
+    cudaStream_t s = ctx->stream;
+    k_fp64_peak<<<blocks, threads, 0, s>>>(out, 10);
+    float best = 0.f, ms = 0.f;
+    for (int r = 0; r < 10; ++r) {
+        cudaEventRecord(e0, s);
+        k_fp64_peak<<<blocks, threads, 0, s>>>(out, iters);
+        cudaEventRecord(e1, s);
+        if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess)
+            return done(fail(ctx, BK_CUDA_ERROR, "measure_fp64_peak: burst launch failed"));
+        if (r == 0 || ms < best) best = ms;
+    }
+    *burst_tflops = flops / (best * 1e-3) / 1e12;
+    // sustained: enough back-to-back launches to fill `seconds` at the burst rate
+    const int n = (int)(seconds * 1e3 / best) + 1;
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < n; ++r) k_fp64_peak<<<blocks, threads, 0, s>>>(out, iters);
+    cudaEventRecord(e1, s);
+    if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess)
+        return done(fail(ctx, BK_CUDA_ERROR, "measure_fp64_peak: sustained run failed"));
+    *sustained_tflops = flops * n / (ms * 1e-3) / 1e12;
+    return done(BK_OK);
+}
+
 const char* bk_last_solver_variant(const bk_ctx* ctx) {
     return ctx ? ctx->last_variant.c_str() : "";
 }
