@@ -46,17 +46,21 @@ bk_status workspace(bk_ctx* ctx, int slot, size_t bytes, void** out) {
 }
 
 bk_status read_small(bk_ctx* ctx, void* host_dst, const void* dev_src, size_t bytes) {
-    constexpr size_t kMap = 64 << 10;
-    if (bytes > (32 << 10) || bytes % 4) return fail(ctx, BK_INTERNAL, "read_small: size");
+    constexpr size_t kMap = 64 << 10, kPiece = 32 << 10;  // the upper half holds post_small's slots
+    if (bytes % 4) return fail(ctx, BK_INTERNAL, "read_small: size");
     if (!ctx->hmap) {
         BK_CUDA_TRY(ctx, cudaHostAlloc(&ctx->hmap, kMap, cudaHostAllocMapped));
         BK_CUDA_TRY(ctx, cudaHostGetDevicePointer(&ctx->hmap_dev, ctx->hmap, 0));
     }
-    BK_CUDA_TRY(ctx, launch_copy_words(ctx->stream, (unsigned*)ctx->hmap_dev,
-                                       (const unsigned*)dev_src, bytes / 4));
-    ++ctx->launches;
-    BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    std::memcpy(host_dst, ctx->hmap, bytes);
+    // pieces of at most 32 KiB (the reports of a 64-chip batch are 37 KiB)
+    for (size_t off = 0; off < bytes; off += kPiece) {
+        const size_t m = std::min(kPiece, bytes - off);
+        BK_CUDA_TRY(ctx, launch_copy_words(ctx->stream, (unsigned*)ctx->hmap_dev,
+                                           (const unsigned*)((const char*)dev_src + off), m / 4));
+        ++ctx->launches;
+        BK_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        std::memcpy((char*)host_dst + off, ctx->hmap, m);
+    }
     return BK_OK;
 }
 

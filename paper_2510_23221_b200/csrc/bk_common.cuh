@@ -204,7 +204,7 @@ bk_status ensure_copy_stream(bk_ctx* ctx);
 bool is_device_ptr(const void* p);
 // Copy a few bytes device -> host through a kernel writing mapped pinned
 // memory (no copy engine: it never queues behind a large in-flight D2H drain)
-// and synchronize the stream. bytes <= 32 KiB, multiple of 4.
+// and synchronize the stream (in pieces of 32 KiB). bytes a multiple of 4.
 bk_status read_small(bk_ctx* ctx, void* host_dst, const void* dev_src, size_t bytes);
 // Asynchronous form for the lookahead loop: post_small enqueues the copy into
 // slot (0 / 1) of the same mapped page and records an event; wait_small waits

@@ -715,3 +715,36 @@ def test_slab_local_combine_matches_global(bk, ctx, case, nslabs):
         assert np.array_equal(qs, Qg[:, :, sl.y0:sl.y0 + sl.nyl, :])
         rr, RR = r.cpu().numpy(), R.cpu().numpy()
         assert np.max(np.abs(rr - RR) / np.maximum(RR, 1e-300)) <= 1e-12
+
+
+def test_measure_fp64_peak(bk, ctx):
+    """bk_measure_fp64_peak (bench.py's live roofline denominator): a plausible
+    B200 FP64 tensor rate, sustained not above burst."""
+    burst, sustained = ctx.measure_fp64_peak(0.5)
+    assert 20.0 < burst < 60.0, burst
+    assert 0.5 * burst < sustained <= 1.02 * burst, (burst, sustained)
+
+
+def test_generate_batch_64_chips_per_launch(bk, ctx, oracle):
+    """bench.py's config-1 step: 64 chips z-stacked in ONE launch (2 CTAs per
+    chip). The 64 solve reports (37 KiB) come back through the mapped-memory
+    read in pieces — a 32 KiB cap there once made this configuration fail."""
+    import torch
+
+    chips = [bk.synth_chip(1, 16, 16, 1, 8, 4, chip_id=c) for c in range(64)]
+    dev = torch.device("cuda", 0)
+    n, N = chips[0].grid.cell_count(), 4
+    Td = [torch.empty((N, n), dtype=torch.float64, device=dev) for _ in chips]
+    Qd = [torch.empty((N, n), dtype=torch.float64, device=dev) for _ in chips]
+    Rd = [torch.empty(N, dtype=torch.float64, device=dev) for _ in chips]
+    _, _, _, reps, _ = bk.generate_batch(chips, cfg_jacobi(), t_out=Td, q_out=Qd, resid_out=Rd,
+                                         streams=64, ctx=ctx)
+    torch.cuda.synchronize()
+    assert "chips=64" in ctx.last_solver_variant, ctx.last_solver_variant
+    assert len(reps) == 64 and all(r.all_converged() for r in reps)
+    for c in (0, 37, 63):
+        ch = chips[c]
+        o = oracle.assemble(grid_tuple(ch.grid), ch.k, ch.bc.as_tuples())
+        X, orep = oracle.block_cg(o, oracle.rhs_from_power(o, ch.q_basis), TOL, 100000, 1)
+        To, Qo, _ = oracle.combine_action(o, X, ch.coef)
+        assert rel_l2(Td[c].cpu().numpy(), To) <= PARITY and rel_l2(Qd[c].cpu().numpy(), Qo) <= PARITY
