@@ -243,7 +243,9 @@ bk_status bk_set_cg_sm_budget(bk_ctx* ctx, int max_ctas);
  * context is created (BK_CG_RING, BK_CG_NO_RESIDENT, BK_CG_LARGE,
  * BK_CG_PROFILE, BK_NO_TMA_SPMM, BK_COMB_PROFILE, BK_BATCH_TRACE). Names:
  * "ring" (-1 automatic, 0 off, 1 on), "no_resident", "force_large",
- * "cg_profile", "no_tma_spmm", "comb_profile", "batch_trace" (0 / 1).
+ * "cg_profile", "no_tma_spmm", "comb_profile", "batch_trace" (0 / 1);
+ * "no_defer_x" = 1 keeps X += P alpha in phase 2 of the persistent block CG
+ * (bitwise the deferred form; tests compare the two).
  * Not part of the reference API; used by the tests to pin kernel variants. */
 bk_status bk_set_option(bk_ctx* ctx, const char* name, int value);
 /* Kernel instantiation the last block-CG solve on ctx ran, e.g.

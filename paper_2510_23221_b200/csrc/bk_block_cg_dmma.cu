@@ -1300,12 +1300,13 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
     const int64_t max_cells = 16 * ((ntiles + nb - 1) / nb);
     const bool resident = S <= 16 && max_cells <= kResCells && !ctx->knobs.no_resident;
     const bool ring = want_ring<S>(ctx, resident, op->nx, op->nz);
+    const bool defer = !resident && (ring || S >= 32) && !ctx->knobs.no_defer_x;
     const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, false, false>
-                       : (ring || S >= 32) ? (const void*)block_cg_dmma_kernel<S, false, false, true>
-                                           : (const void*)block_cg_dmma_kernel<S, false, false, false>;
+                       : defer  ? (const void*)block_cg_dmma_kernel<S, false, false, true>
+                                : (const void*)block_cg_dmma_kernel<S, false, false, false>;
     const size_t smem = (resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>)) +
                         (ring ? ring_bytes<S>(op->nx) : 0);
-    ctx->last_variant = variant_name<S>(resident, false, !resident && (ring || S >= 32), ring);
+    ctx->last_variant = variant_name<S>(resident, false, defer, ring);
     BK_CUDA_TRY(ctx, bk::set_max_smem((const void*)kern, smem));
     int occ = 0;
     BK_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BS, smem));
@@ -1424,12 +1425,13 @@ bk_status run_dmma_multi(bk_ctx* ctx, const bk_operator* op, int K, const double
     const int64_t max_cells = 16 * ((ntiles + cpc - 1) / cpc);
     const bool resident = S <= 16 && max_cells <= kResCells && !ctx->knobs.no_resident;
     const bool ring = want_ring<S>(ctx, resident, op->nx, op->nz / K);
+    const bool defer = !resident && (ring || S >= 32) && !ctx->knobs.no_defer_x;
     const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, true, false>
-                       : (ring || S >= 32) ? (const void*)block_cg_dmma_kernel<S, false, true, true>
-                                           : (const void*)block_cg_dmma_kernel<S, false, true, false>;
+                       : defer  ? (const void*)block_cg_dmma_kernel<S, false, true, true>
+                                : (const void*)block_cg_dmma_kernel<S, false, true, false>;
     const size_t smem = (resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>)) +
                         (ring ? ring_bytes<S>(op->nx) : 0);
-    ctx->last_variant = variant_name<S>(resident, true, !resident && (ring || S >= 32), ring) +
+    ctx->last_variant = variant_name<S>(resident, true, defer, ring) +
                         " chips=" + std::to_string(K);
     BK_CUDA_TRY(ctx, set_max_smem(kern, smem));
     int occ = 0;

@@ -126,3 +126,40 @@ def test_stream_pipeline_repeatable(bk, ctx):
         for key in acc:
             for a, b in zip(acc[key], got[0][key]):
                 assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("cases,streams,opts", [
+    ([(3, 32, 24, 8, 32, 20, 1, c) for c in range(6)], 6, {}),                    # 3D, S = 32
+    ([(2, 64, 48, 1, 16, 24, 1, c) for c in range(6)], 6, {"no_resident": 1}),    # 2D row ring
+])
+def test_deferred_x_bitwise_the_phase2_update(bk, ctx, cases, streams, opts):
+    """X += P alpha placed in phase 3 (deferred, the default for S = 32 and the
+    row ring) or in phase 2 (option no_defer_x) is the same DMMA chain per
+    element, so iterations, T and q must agree bit for bit. The deferred form
+    reads X halo cells of other CTAs in a verification right after updating X:
+    with only a CTA barrier there, a borderline column restarted instead of
+    freezing and the two forms (and repeated runs) differed."""
+    import torch
+
+    chips = dev_chips(bk, cases)
+    dev = torch.device("cuda", 0)
+    n, N = chips[0].grid.cell_count(), int(chips[0].coef.shape[1])
+    res = {}
+    for name, extra in (("deferred", {}), ("phase2", {"no_defer_x": 1})):
+        with ctx.options(**opts, **extra):
+            T = [torch.full((N, n), float("nan"), dtype=torch.float64, device=dev) for _ in chips]
+            Q = [torch.full((N, n), float("nan"), dtype=torch.float64, device=dev) for _ in chips]
+            R = [torch.full((N,), float("nan"), dtype=torch.float64, device=dev) for _ in chips]
+            _, _, _, reps, _ = bk.generate_batch(chips, bk.SolverConfig(1e-12, 100000, "jacobi"),
+                                                 T, Q, R, streams=streams, ctx=ctx,
+                                                 check_converged=False)
+            torch.cuda.synchronize()
+            res[name] = (ctx.last_solver_variant, [r.iterations for r in reps],
+                         [r.matvec_count for r in reps], [t.cpu().numpy() for t in T],
+                         [q.cpu().numpy() for q in Q])
+    vd, vp = res["deferred"][0], res["phase2"][0]
+    assert ",1,1>" in vd and ",1,0>" in vp, (vd, vp)
+    assert res["deferred"][1] == res["phase2"][1] and res["deferred"][2] == res["phase2"][2]
+    for c in range(len(chips)):
+        assert np.array_equal(res["deferred"][3][c], res["phase2"][3][c]), c
+        assert np.array_equal(res["deferred"][4][c], res["phase2"][4][c]), c
