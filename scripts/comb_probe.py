@@ -2,6 +2,7 @@
 basis: python scripts/comb_probe.py CONFIG [N] [option=value ...] (device
 buffers; CUDA events, best of 5); with options, also checks the outputs are
 bitwise those of the default kernel."""
+import hashlib
 import os
 import sys
 import time
@@ -46,6 +47,8 @@ for name, o in variants:
     same = None if ref is None else (torch.equal(Tv, ref[0]) and torch.equal(Qv, ref[1]),
                                      float((Rv - ref[2]).abs().max()))
     ref = ref or (Tv, Qv, Rv)
-    print(f"config {cfgid} {name}: combine+action {N} samples {dt * 1e3:.3f} ms "
+    sha = hashlib.sha256(Tv.cpu().numpy().tobytes() + Qv.cpu().numpy().tobytes()
+                         + Rv.cpu().numpy().tobytes()).hexdigest()[:16] if N * n <= 1 << 28 else "-"
+    print(f"config {cfgid} {name}: sha {sha} combine+action {N} samples {dt * 1e3:.3f} ms "
           f"({16 * n * N / dt / 1e9:.0f} GB/s written) bitwise T,q / max resid diff vs default: {same}",
           flush=True)
