@@ -1,8 +1,6 @@
 #!/bin/bash
 # scratch job file for one gpurun call (edit, then: gpurun -- 'bash scripts/gpu_job.sh').
-# Typical A/B: build the old library into scripts/ab/libblockoa_b200_before.so and run
-#   bash scripts/ab_lib.sh "python scripts/c5_phases.py 100"
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/t.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/t.log
+timeout 900 python bench.py --steps 3 --warmup 3 --no-extra --no-e2e --no-cpu-baseline --no-dd-leg > gpurun_out/b.log 2>&1
+echo "bench rc=$?" >> gpurun_out/b.log
