@@ -245,7 +245,8 @@ bk_status bk_set_cg_sm_budget(bk_ctx* ctx, int max_ctas);
  * "ring" (-1 automatic, 0 off, 1 on), "no_resident", "force_large",
  * "cg_profile", "no_tma_spmm", "comb_profile", "batch_trace" (0 / 1);
  * "no_defer_x" = 1 keeps X += P alpha in phase 2 of the persistent block CG
- * (bitwise the deferred form; tests compare the two).
+ * (bitwise the deferred form; tests compare the two); "no_w_prefetch" = 1
+ * single-buffers phase 2's W staging in the row-ring kernels (A/B).
  * Not part of the reference API; used by the tests to pin kernel variants. */
 bk_status bk_set_option(bk_ctx* ctx, const char* name, int value);
 /* Kernel instantiation the last block-CG solve on ctx ran, e.g.

@@ -889,6 +889,7 @@ bk_status bk_set_option(bk_ctx* ctx, const char* name, int value) {
     else if (k == "no_ws_update") ctx->knobs.no_ws_update = value != 0;
     else if (k == "no_ws_spmm") ctx->knobs.no_ws_spmm = value != 0;
     else if (k == "no_defer_x") ctx->knobs.no_defer_x = value != 0;
+    else if (k == "no_w_prefetch") ctx->knobs.no_w_prefetch = value != 0;
     else if (k == "graph_loop") ctx->knobs.graph_loop = value != 0;
     else if (k == "no_lookahead") ctx->knobs.no_lookahead = value != 0;
     else if (k == "spmm_teams") ctx->knobs.spmm_teams = value != 0;

@@ -70,6 +70,8 @@ struct Args {
     bk::CgReport* rep;
     long long* prof;  // optional phase timestamps (CTA 0), PROF_ITERS x PROF_MARKS
     int ring;         // phase 1 through the row ring (phase_spmm_gram_ring)
+    int pre_off;      // byte offset (from the dynamic smem base) of phase 2's W prefetch
+                      // buffers, NW x 2 tiles; -1: none (single-buffered staging)
     // several independent chips of identical dims in one launch: chip k owns
     // cells [k nchip, (k+1) nchip) of the z-stacked (block-diagonal) system,
     // CTAs [k cpc, (k+1) cpc), reduction partials part + k cpc (S^2+S),
@@ -686,6 +688,12 @@ __device__ __forceinline__ void stage_tile(double* T, const double* __restrict__
 __device__ __forceinline__ void cp_commit_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// wait until at most N of this thread's committed groups are still in flight
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // A fragments of a staged tile: f[ks][0] = T[g][4ks+t], f[ks][1] = T[g+8][4ks+t]
 template <int S>
@@ -1019,18 +1027,51 @@ __global__ void __launch_bounds__(CtaShape<S>::BS, 1) block_cg_dmma_kernel(Args 
         // S_new = R^T Z
         G.zero();
         double rr[NT][2] = {};
-        for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW) {
+        // With prefetch buffers (a.pre_off >= 0) the W tile of the warp's NEXT
+        // 16 cells is in flight (cp.async) while this tile's DMMA chains, R
+        // store and Gram run: the single-buffered form exposed one L2 / HBM
+        // round trip per tile and warp (batched C2: phase 2 at 4.9 TB/s against
+        // phase 3's 6.7).
+        // Compiled only into the row-ring kernels (DEF, S <= 16), whose ring
+        // slots hold the buffers: measured on the 3D kernels it cost more
+        // (shared memory, spills) than it hid (C3 -0.6 %, C4 -2.3 %; C2 +2.7 %).
+        constexpr bool kPre = DEF && S <= 16;
+        double* const wpre = (kPre && a.pre_off >= 0)
+                                 ? reinterpret_cast<double*>(smem_raw + a.pre_off) +
+                                       (int64_t)warp * 2 * 16 * Strides<S>::RS
+                                 : nullptr;
+        if (wpre && c0 + 16 * warp < c1) {
+            stage_tile<S>(wpre, a.W, c0 + 16 * warp, c1, lane);
+            cp_commit();
+        }
+        int tix = 0;
+        for (int64_t base = c0 + 16 * warp; base < c1; base += 16 * NW, ++tix) {
             double pa[KS][2], wa[KS][2], x[NT][4], r[NT][4];
             if (!defer) {
                 stage_tile<S>(tr, a.P, base, c1, lane);
                 Xv.load(base, g, t, x);
             }
-            stage_tile<S>(tz, a.W, base, c1, lane);
-            Rv.load(base, g, t, r);
-            cp_commit_wait_all();
+            const double* wt = tz;
+            if (wpre) {
+                if (!defer) cp_commit();  // this tile's P
+                const int64_t nxt = base + 16 * NW;
+                wt = wpre + (tix & 1) * 16 * Strides<S>::RS;
+                Rv.load(base, g, t, r);
+                if (nxt < c1) {
+                    stage_tile<S>(wpre + ((tix + 1) & 1) * 16 * Strides<S>::RS, a.W, nxt, c1, lane);
+                    cp_commit();
+                    cp_wait<1>();  // all but the prefetch: this tile's W (and P) landed
+                } else {
+                    cp_wait<0>();
+                }
+            } else {
+                stage_tile<S>(tz, a.W, base, c1, lane);
+                Rv.load(base, g, t, r);
+                cp_commit_wait_all();
+            }
             __syncwarp();
             if (!defer) afrag_smem<S>(tr, g, t, pa, 1.0);
-            afrag_smem<S>(tz, g, t, wa, -1.0);
+            afrag_smem<S>(wt, g, t, wa, -1.0);
             __syncwarp();  // tr / tz are rewritten by tile_gram below
 #pragma unroll
             for (int n = 0; n < NT; ++n)
@@ -1277,6 +1318,23 @@ bool want_ring(const bk_ctx* ctx, bool resident, int nx, int nz_chip) {
     return true;
 }
 
+// Phase 2's W prefetch buffers (NW warps x 2 tiles of 16 x RS doubles) in the
+// dynamic shared memory past Sm, for the row-ring kernels: inside the ring's P
+// slots when they are large enough (the ring is idle in phase 2; its mbarriers
+// sit past the slots), else past the ring. Returns the byte offset, -1 for
+// none, and grows `smem` as needed.
+template <int S>
+int place_prefetch(bool resident, bool ring, int nx, size_t& smem) {
+    if (resident || !ring) return -1;  // row-ring kernels only (see phase 2)
+    const size_t base = (sizeof(Sm<S, false>) + 15) / 16 * 16;
+    const size_t need = (size_t)CtaShape<S>::NW * 2 * 16 * Strides<S>::RS * sizeof(double);
+    if (need <= (size_t)kRing * nx * S * sizeof(double)) return (int)base;
+    const size_t off = (base + ring_bytes<S>(nx) + 15) / 16 * 16;
+    if (off + need > 232448) return -1;
+    if (off + need > smem) smem = off + need;
+    return (int)off;
+}
+
 template <int S>
 std::string variant_name(bool res, bool multi, bool def, bool ring) {
     return "block_cg_dmma_kernel<" + std::to_string(S) + "," + (res ? "1" : "0") + "," +
@@ -1304,8 +1362,9 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
     const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, false, false>
                        : defer  ? (const void*)block_cg_dmma_kernel<S, false, false, true>
                                 : (const void*)block_cg_dmma_kernel<S, false, false, false>;
-    const size_t smem = (resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>)) +
-                        (ring ? ring_bytes<S>(op->nx) : 0);
+    size_t smem = (resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>)) +
+                  (ring ? ring_bytes<S>(op->nx) : 0);
+    const int pre_off = ctx->knobs.no_w_prefetch ? -1 : place_prefetch<S>(resident, ring, op->nx, smem);
     ctx->last_variant = variant_name<S>(resident, false, defer, ring);
     BK_CUDA_TRY(ctx, bk::set_max_smem((const void*)kern, smem));
     int occ = 0;
@@ -1360,6 +1419,7 @@ bk_status run_dmma(bk_ctx* ctx, const bk_operator* op, const double* B, int s,
     a.nchip = n;
     a.bars = nullptr;
     a.ring = ring;
+    a.pre_off = pre_off;
     const bool want_prof = ctx->knobs.cg_profile;
     a.prof = want_prof ? (long long*)((char*)pRep + sizeof(CgReport)) : nullptr;
     if (want_prof)
@@ -1429,8 +1489,9 @@ bk_status run_dmma_multi(bk_ctx* ctx, const bk_operator* op, int K, const double
     const void* kern = resident ? (const void*)block_cg_dmma_kernel<S, true, true, false>
                        : defer  ? (const void*)block_cg_dmma_kernel<S, false, true, true>
                                 : (const void*)block_cg_dmma_kernel<S, false, true, false>;
-    const size_t smem = (resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>)) +
-                        (ring ? ring_bytes<S>(op->nx) : 0);
+    size_t smem = (resident ? sizeof(Sm<S, true>) : sizeof(Sm<S, false>)) +
+                  (ring ? ring_bytes<S>(op->nx) : 0);
+    const int pre_off = ctx->knobs.no_w_prefetch ? -1 : place_prefetch<S>(resident, ring, op->nx, smem);
     ctx->last_variant = variant_name<S>(resident, true, defer, ring) +
                         " chips=" + std::to_string(K);
     BK_CUDA_TRY(ctx, set_max_smem(kern, smem));
@@ -1492,6 +1553,7 @@ bk_status run_dmma_multi(bk_ctx* ctx, const bk_operator* op, int K, const double
     a.nchip = nchip;
     a.bars = (unsigned*)pBar;
     a.ring = ring;
+    a.pre_off = pre_off;
     void* args[] = {&a};
     BK_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(kern, dim3((unsigned)nb), dim3(BS), args, smem,
                                                  ctx->stream));

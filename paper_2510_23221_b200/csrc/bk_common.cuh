@@ -36,6 +36,7 @@ struct bk_knobs {
     bool batch_trace = false;
     bool phase_timing = false; // per-kernel-kind event timing of the multi-kernel solve
     bool no_ws_update = false; // S = 64: the cp.async update sweeps instead of the warp-specialised ones
+    bool no_w_prefetch = false;  // persistent block CG: single-buffered W staging in phase 2
     bool no_defer_x = false;   // persistent block CG: X += P alpha in phase 2 even where phase 3 would take it
     bool no_ws_spmm = false;   // S = 64: the per-run TMA stencil sweep instead of the z-marching one
     bool spmm_teams = false;   // S = 64: the two-team stencil sweep instead of the role-split one

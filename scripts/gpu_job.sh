@@ -2,5 +2,7 @@
 # scratch job file for one gpurun call (edit, then: gpurun -- 'bash scripts/gpu_job.sh').
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python bench.py --steps 3 --warmup 3 --no-extra --no-e2e --no-cpu-baseline --no-dd-leg > gpurun_out/b.log 2>&1
-echo "bench rc=$?" >> gpurun_out/b.log
+timeout 900 bash scripts/ab_lib.sh "PROBE_STREAMS=16 python scripts/batch_probe.py 2 16 3; PROBE_STREAMS=12 python scripts/batch_probe.py 3 12 3; PROBE_STREAMS=32 python scripts/batch_probe.py 4 32 3; PROBE_STREAMS=64 python scripts/batch_probe.py 1 64 3" > gpurun_out/ab.log 2>&1
+for i in 1 2 3; do timeout 300 python -m pytest tests/test_gpu_stress.py tests/test_gpu_bench_path.py -q -x > gpurun_out/st$i.log 2>&1; echo "rc=$?" >> gpurun_out/st$i.log; done
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/t.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/t.log
