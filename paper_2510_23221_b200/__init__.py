@@ -473,7 +473,10 @@ class Context:
     def set_option(self, name: str, value: int) -> None:
         """Per-context kernel-variant switch (bk_set_option): "ring" (-1 auto,
         0, 1), "no_resident", "force_large", "cg_profile", "no_tma_spmm",
-        "comb_profile", "batch_trace", "phase_timing"."""
+        "comb_profile", "batch_trace", "phase_timing", "no_ws_update",
+        "no_ws_spmm", "no_defer_x", "no_w_prefetch", "comb_one_role",
+        "graph_loop", "spmm_band", "spmm_teams" (A/B and test pins; see
+        include/blockoa_b200.h)."""
         _raise(_load().bk_set_option(self.h, name.encode(), int(value)), self.h, "set_option")
 
     @contextlib.contextmanager
